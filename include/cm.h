@@ -1,0 +1,226 @@
+/*
+ * cm.h — C ABI of the B200-native CUDA-aware allreduce ("collective memory").
+ *
+ * Drop-in boundary for the reference's allreduce hot path
+ * (/root/reference/pkg/src/collectium/, paths below relative to it). The
+ * reference is pure Python, so there is no reference FFI to bind; each entry
+ * point below names the reference interface it replaces. The Python façade
+ * (paper_1810_11112_b200/*.py) binds these with ctypes and keeps the
+ * reference's signatures, argument meanings and exception classes.
+ *
+ * Conventions
+ *  - Every function returns an int status (CM_OK = 0). On failure
+ *    cm_last_error() returns a thread-local message. Status codes map 1:1 onto
+ *    the reference exception classes of errors.py:4-56.
+ *  - Plain pointers and sizes only; `stream` is a cudaStream_t passed as void*.
+ *  - Collectives are out-of-place (const send, recv) like the reference, which
+ *    copies its input and returns a new Tensor (collectives.py:123,176); send ==
+ *    recv (in place) is also accepted. They are stream-ordered: they return
+ *    after enqueueing; device-side errors (peer shape mismatch, timeouts) are
+ *    reported by cm_comm_sync()/cm_comm_poll().
+ */
+#ifndef CM_H_
+#define CM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CM_MAX_RANKS 16
+
+/* status codes <-> errors.py exception classes */
+enum cm_status {
+  CM_OK = 0,
+  CM_ERR_SHAPE = 1,           /* ShapeError            errors.py:8   */
+  CM_ERR_INVALID_GROUP = 2,   /* InvalidGroupError     errors.py:12  */
+  CM_ERR_ROUTING = 3,         /* RoutingError          errors.py:16  */
+  CM_ERR_TRANSPORT = 4,       /* TransportError        errors.py:20  (peer timeout) */
+  CM_ERR_DEADLOCK = 5,        /* DeadlockError         errors.py:24  */
+  CM_ERR_CONFIG = 6,          /* ConfigError           errors.py:55  */
+  CM_ERR_INVALID_HANDLE = 7,  /* InvalidHandleError    errors.py:47  */
+  CM_ERR_UNKNOWN_BUFFER = 8,  /* UnknownBufferError    errors.py:51  */
+  CM_ERR_UNSUPPORTED = 9,     /* UnsupportedOperationError errors.py:36 */
+  CM_ERR_CUDA = 10,           /* CUDA runtime failure (TransportError in Python) */
+  CM_ERR_VALUE = 11           /* ValueError (bad argument)           */
+};
+
+/* element types: core.py:18-21 has float32/float64; bf16 and ints are extensions */
+enum cm_dtype { CM_FLOAT32 = 0, CM_FLOAT64 = 1, CM_BFLOAT16 = 2, CM_INT32 = 3, CM_INT64 = 4 };
+/* ReduceOp core.py:24-26 */
+enum cm_op { CM_SUM = 0, CM_MAX = 1 };
+/* ALGORITHMS collectives.py:20 */
+enum cm_algo { CM_ALGO_AUTO = 0, CM_ALGO_FLAT = 1, CM_ALGO_RING = 2, CM_ALGO_RHD = 3 };
+/* reduce-scatter / allgather ownership layouts (collectives.py:128-150 ring, :198-229 rhd) */
+enum cm_layout { CM_LAYOUT_RING = 0, CM_LAYOUT_RHD = 1 };
+/* Policy registry.py:32-35 */
+enum cm_policy { CM_NO_CACHE = 0, CM_LAZY_CACHE = 1, CM_INTERCEPT_CACHE = 2 };
+/* BufferKind registry.py:27-29 */
+enum cm_kind { CM_KIND_HOST = 0, CM_KIND_DEVICE = 1 };
+
+/* CollectiveStats collectives.py:28-32 (the reference's logical schedule) */
+typedef struct {
+  int64_t rounds;
+  int64_t messages_per_rank;
+  int64_t bytes_sent_per_rank;
+} cm_stats_t;
+
+/* RegistryStats registry.py:44-49 */
+typedef struct {
+  int64_t driver_queries;
+  int64_t cache_hits;
+  int64_t inserts;
+  int64_t invalidations;
+} cm_registry_stats_t;
+
+typedef struct cm_comm cm_comm_t;
+typedef struct cm_registry cm_registry_t;
+
+const char* cm_version(void);
+const char* cm_last_error(void);
+
+/* ---------------------------------------------------------------------------
+ * Host-side logic (no GPU required)
+ * ------------------------------------------------------------------------- */
+
+/* chunk_partition core.py:113-130 -> offsets[p], lengths[p] */
+int cm_chunk_partition(int64_t n, int p, int64_t* offsets, int64_t* lengths);
+/* ownership after reduce-scatter: ring = chunk_partition, rhd = halving segments
+ * (collectives.py:198-216; folded odd ranks own (0,0)) */
+int cm_layout(int layout, int64_t n, int p, int64_t* offsets, int64_t* lengths);
+/* resolve_algorithm collectives.py:239-247 (CM_ERR_CONFIG on bad algo/switch) */
+int cm_resolve_algorithm(int algo, int64_t nbytes, int64_t switch_bytes, int* concrete);
+/* CollectiveStats the reference reports for (algo, p, rank, n) — collectives.py:75-236 */
+int cm_algo_stats(int algo, int p, int rank, int64_t n, int dtype, int64_t switch_bytes,
+                  cm_stats_t* out);
+int cm_rs_stats(int layout, int p, int rank, int64_t n, int dtype, cm_stats_t* out);
+int cm_ag_stats(int layout, int p, int rank, int64_t n, int dtype, cm_stats_t* out);
+/* fuse() greedy first-fit aggregation.py:95-130: group_of[i] = group index of member i */
+int cm_fuse_plan(int n, const int64_t* nbytes, const int* dtypes, int64_t threshold,
+                 int* group_of, int* n_groups);
+size_t cm_dtype_size(int dtype);
+
+/* ---------------------------------------------------------------------------
+ * Pointer cache (registry.py:52-151, PAPER §V-B)
+ *   simulated=1: the reference's model — fake addresses from 0x1000, lowest
+ *     freed address reused, "driver query" = ground-truth lookup + counter.
+ *   simulated=0: real memory — alloc = cudaMalloc / cudaHostAlloc (the
+ *     intercepted allocation API), the driver query = cudaPointerGetAttributes,
+ *     range lookups resolve interior pointers of registered allocations.
+ * ------------------------------------------------------------------------- */
+int cm_registry_create(int policy, int64_t query_delay_ns, int simulated, cm_registry_t** out);
+int cm_registry_destroy(cm_registry_t* reg);
+int cm_registry_alloc(cm_registry_t* reg, int kind, int64_t size, uint64_t* address);
+int cm_registry_free(cm_registry_t* reg, uint64_t address);
+/* tell an intercept cache about memory allocated elsewhere (e.g. torch) */
+int cm_registry_register(cm_registry_t* reg, uint64_t address, int64_t size, int kind);
+int cm_registry_unregister(cm_registry_t* reg, uint64_t address);
+int cm_registry_classify(cm_registry_t* reg, uint64_t address, int* kind);
+int cm_registry_ground_truth(cm_registry_t* reg, uint64_t address, int* kind);
+int cm_registry_stats(cm_registry_t* reg, cm_registry_stats_t* out);
+int cm_registry_policy(cm_registry_t* reg, int* policy);
+/* total wall time spent in real driver queries (ns); simulated: queries*delay */
+int cm_registry_query_time_ns(cm_registry_t* reg, int64_t* ns);
+/* {"policy": ..., "driver_queries": ..., "cache_hits": ..., "inserts": ..., "invalidations": ...} */
+int cm_registry_stats_json(cm_registry_t* reg, char* buf, size_t len);
+
+/* ---------------------------------------------------------------------------
+ * Communicator: one per rank (one process per GPU). Replaces the Transport
+ * plugin (transport/base.py:8-57) — rank, size and the logical counters stay,
+ * byte send/recv is replaced by a CUDA-IPC peer-mapped symmetric heap over
+ * NVLink/NVSwitch.
+ * Bootstrap: create -> exchange cm_comm_ipc_handle() bytes over any host
+ * channel -> connect(all handles in rank order).
+ * ------------------------------------------------------------------------- */
+#define CM_IPC_HANDLE_BYTES 64
+int cm_comm_create(int rank, int size, int device, int64_t staging_bytes, int64_t pool_bytes,
+                   cm_comm_t** out);
+int cm_comm_ipc_handle(cm_comm_t* comm, void* handle_out);
+int cm_comm_connect(cm_comm_t* comm, const void* all_handles);
+/* one process drives `size` virtual ranks on ONE GPU (single-GPU emulation
+ * of the group, the GPU analogue of the reference's SimNetwork): every
+ * collective launches one cooperative kernel holding all ranks' CTAs. */
+int cm_comm_create_virtual(int size, int device, int64_t staging_bytes, cm_comm_t** out);
+int cm_comm_destroy(cm_comm_t* comm);
+int cm_comm_rank(cm_comm_t* comm, int* rank);
+int cm_comm_size(cm_comm_t* comm, int* size);
+/* device-side wait budget before a peer is declared dead (TransportError) */
+int cm_comm_set_timeout(cm_comm_t* comm, double seconds);
+/* pointer-cache policy used to classify send/recv on every call */
+int cm_comm_set_policy(cm_comm_t* comm, int policy);
+int cm_comm_registry(cm_comm_t* comm, cm_registry_t** reg);
+/* tuning knobs: "oneshot_max_bytes" (largest message reduced one-shot),
+ * "oneshot_bytes_per_cta", "twoshot_bytes_per_cta", "max_ctas";
+ * get also reads "staging_bytes" and "pool_bytes" */
+int cm_comm_set_param(cm_comm_t* comm, const char* key, int64_t value);
+int cm_comm_get_param(cm_comm_t* comm, const char* key, int64_t* value);
+/* symmetric allocation from the IPC heap (collective: same sizes, same order
+ * on every rank). Buffers from here are read by peers in place (zero copy). */
+int cm_comm_alloc(cm_comm_t* comm, int64_t bytes, void** ptr);
+int cm_comm_free(cm_comm_t* comm, void* ptr);
+/* wait for `stream`, then report any device-side error of earlier calls */
+int cm_comm_sync(cm_comm_t* comm, void* stream);
+/* non-blocking error check of completed calls */
+int cm_comm_poll(cm_comm_t* comm);
+/* logical counters (Transport.messages_sent / bytes_sent, base.py:43-57) and
+ * the real NVLink bytes this rank pulled from peers */
+int cm_comm_counters(cm_comm_t* comm, int64_t* messages_sent, int64_t* bytes_sent,
+                     int64_t* nvlink_bytes_in, int64_t* calls);
+/* number of kernels this comm has launched (bench "gpu_launches") */
+int cm_comm_launches(cm_comm_t* comm, int64_t* launches);
+
+/* allreduce collectives.py:250-260 (+ allreduce_ring :107, allreduce_rhd :155,
+ * allreduce_flat :75 via `algo`). Results are bit-identical to the reference
+ * fold order of the resolved algorithm. average=1 divides by p inside the
+ * reduction (the fused mean of aggregation.py:167-172). */
+int cm_allreduce(cm_comm_t* comm, const void* send, void* recv, int64_t count, int dtype, int op,
+                 int algo, int64_t switch_bytes, int average, void* stream, cm_stats_t* stats);
+/* reduce-scatter / allgather phases of collectives.py:128-150 (ring) and
+ * :178-229 (rhd) as public operations. recv of reduce_scatter holds this rank's
+ * layout segment; send of allgather holds it. */
+int cm_reduce_scatter(cm_comm_t* comm, const void* send, void* recv, int64_t count, int dtype,
+                      int op, int layout, void* stream, cm_stats_t* stats);
+int cm_allgather(cm_comm_t* comm, const void* send, void* recv, int64_t count, int dtype,
+                 int layout, void* stream, cm_stats_t* stats);
+/* aggregate() hot loop aggregation.py:158-174: members (already in negotiated
+ * order, one dtype) are fused greedily under `threshold`, packed into the
+ * IPC staging heap by one kernel per group, allreduced with the mean fused
+ * in, and written to recv_fused (the members' concatenation; member i's mean
+ * is recv_fused[sum(counts[:i]) : ...]). stats[] gets one entry per issued
+ * allreduce; *n_calls their number. */
+int cm_fused_allreduce(cm_comm_t* comm, int n, const void* const* sends, const int64_t* counts,
+                       int dtype, void* recv_fused, int algo, int64_t threshold,
+                       int64_t switch_bytes, int average, void* stream, cm_stats_t* stats,
+                       int* n_calls);
+
+/* virtual-group variants: arrays of `size` per-rank pointers */
+int cm_allreduce_v(cm_comm_t* comm, const void* const* sends, void* const* recvs, int64_t count,
+                   int dtype, int op, int algo, int64_t switch_bytes, int average, void* stream,
+                   cm_stats_t* stats);
+int cm_reduce_scatter_v(cm_comm_t* comm, const void* const* sends, void* const* recvs,
+                        int64_t count, int dtype, int op, int layout, void* stream,
+                        cm_stats_t* stats);
+int cm_allgather_v(cm_comm_t* comm, const void* const* sends, void* const* recvs, int64_t count,
+                   int dtype, int layout, void* stream, cm_stats_t* stats);
+
+/* ---------------------------------------------------------------------------
+ * Local kernels
+ * ------------------------------------------------------------------------- */
+/* local_reduce core.py:94-110: out = a op b (a is the accumulator) */
+int cm_local_reduce(const void* a, const void* b, void* out, int64_t count, int dtype, int op,
+                    void* stream);
+/* fuse/unfuse payload moves aggregation.py:110-111,133-135: one launch copies
+ * n (src, dst, bytes) triples */
+int cm_batched_copy(int n, const void* const* srcs, void* const* dsts, const int64_t* nbytes,
+                    void* stream);
+/* device-timed loop of cm_allreduce (CUDA events on `stream`), ms per call */
+int cm_time_allreduce(cm_comm_t* comm, const void* send, void* recv, int64_t count, int dtype,
+                      int op, int algo, int64_t switch_bytes, int iters, int warmup,
+                      void* stream, double* ms_per_call);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CM_H_ */

@@ -1,0 +1,862 @@
+// Communicator: CUDA-IPC symmetric heap over NVLink/NVSwitch, algorithm
+// selection, pointer-cache classification on every call, and kernel launches.
+//
+// Host flow of one cm_allreduce (collectives.py:250-260):
+//   resolve_algorithm (size threshold) -> classify send/recv through the
+//   pointer cache (no driver query on a cache hit, PAPER §V-B) -> pick the
+//   source mode (zero-copy from the symmetric pool, copy-in, or host staging)
+//   -> ONE kernel launch (one-shot or two-shot) -> logical CollectiveStats.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "common.hpp"
+#include "kernels.cuh"
+#include "ptrcache.hpp"
+
+using namespace cm;
+using namespace cm::dev;
+
+struct cm_comm {
+  int rank = 0, size = 1, device = 0;
+  bool virt = false;
+  size_t staging_bytes = 0, pool_bytes = 0, heap_bytes = 0;
+  char* local = nullptr;            // own heap (virtual: all vranks' heaps)
+  char* heap[MAXP] = {};
+  bool connected = false;
+  unsigned* herr_host = nullptr;
+  unsigned* herr_dev = nullptr;
+  unsigned long long timeout_cycles = 20000000000ull;  // ~10 s at 2 GHz
+  Registry reg;
+  std::map<size_t, size_t> pool_free;  // offset -> bytes
+  std::map<size_t, size_t> pool_used;
+  char* scratch = nullptr;             // device bounce buffer for host-memory buffers
+  int sms = 148;
+  // tuning knobs (cm_comm_set_param)
+  int64_t oneshot_max_bytes = 256 * 1024;
+  int64_t oneshot_bytes_per_cta = 16 * 1024;
+  int64_t twoshot_bytes_per_cta = 64 * 1024;
+  int max_ctas = 148;
+  // counters
+  int64_t messages = 0, bytes = 0, nvlink_in = 0, calls = 0, launches = 0;
+};
+
+namespace {
+
+int cuda_fail(cudaError_t e, const char* what) {
+  cudaGetLastError();
+  return fail(CM_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define CUDA_TRY(expr)                              \
+  do {                                              \
+    cudaError_t _e = (expr);                        \
+    if (_e != cudaSuccess) return cuda_fail(_e, #expr); \
+  } while (0)
+
+size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+using KFn = void (*)(CollParams);
+
+template <class D, int OP>
+KFn pick_mp(int p, bool tree) {
+  if (p <= 8) return tree ? collective_kernel<D, OP, 8, true> : collective_kernel<D, OP, 8, false>;
+  return tree ? collective_kernel<D, OP, 16, true> : collective_kernel<D, OP, 16, false>;
+}
+
+template <class D>
+KFn pick_op(int op, int p, bool tree) {
+  return op == CM_SUM ? pick_mp<D, CM_SUM>(p, tree) : pick_mp<D, CM_MAX>(p, tree);
+}
+
+KFn pick_kernel(int dtype, int op, int p, bool tree) {
+  switch (dtype) {
+    case CM_FLOAT32: return pick_op<F32>(op, p, tree);
+    case CM_FLOAT64: return pick_op<F64>(op, p, tree);
+    case CM_BFLOAT16: return pick_op<BF16>(op, p, tree);
+    case CM_INT32: return pick_op<I32>(op, p, tree);
+    case CM_INT64: return pick_op<I64>(op, p, tree);
+  }
+  return nullptr;
+}
+
+int check_dtype_op(int dtype, int op) {
+  if (!dtype_size(dtype)) return fail(CM_ERR_SHAPE, "unsupported dtype " + std::to_string(dtype));
+  if (op != CM_SUM && op != CM_MAX) return fail(CM_ERR_VALUE, "unknown reduce op " + std::to_string(op));
+  return CM_OK;
+}
+
+int check_async_error(cm_comm* c) {
+  volatile unsigned* h = c->herr_host;
+  const unsigned code = *h;
+  if (!code) return CM_OK;
+  *h = 0;
+  if (code == ERR_SHAPE)
+    return fail(CM_ERR_SHAPE,
+                "collective shape error: peers disagree on element count, dtype, op or algorithm");
+  return fail(CM_ERR_TRANSPORT, "peer did not arrive within the timeout (rank failed or "
+                                "called a different collective)");
+}
+
+// Where the data of `ptr` lives, through the pointer cache (PAPER §V-B).
+int classify(cm_comm* c, const void* ptr, int* kind) {
+  const uint64_t a = reinterpret_cast<uint64_t>(ptr);
+  // our own symmetric heap is always known (it is an intercepted allocation)
+  if (!c->virt && a >= (uint64_t)c->local && a < (uint64_t)c->local + c->heap_bytes) {
+    *kind = CM_KIND_DEVICE;
+    return CM_OK;
+  }
+  return c->reg.classify(a, kind);
+}
+
+bool in_pool(cm_comm* c, const void* ptr, int64_t bytes) {
+  if (c->virt || !c->local) return false;
+  const char* p = static_cast<const char*>(ptr);
+  const char* lo = c->local + STAGING_OFF + 2 * c->staging_bytes;
+  return p >= lo && p + bytes <= c->local + c->heap_bytes;
+}
+
+unsigned long long make_hdr(int64_t n, int dtype, int op, int order, int phases, int oneshot,
+                            int average, int layout) {
+  unsigned long long h = (unsigned long long)n & ((1ull << 40) - 1);
+  h |= (unsigned long long)(dtype & 7) << 40;
+  h |= (unsigned long long)(op & 1) << 43;
+  h |= (unsigned long long)(order & 3) << 44;
+  h |= (unsigned long long)(phases & 3) << 46;
+  h |= (unsigned long long)(oneshot & 1) << 48;
+  h |= (unsigned long long)(average & 1) << 49;
+  h |= (unsigned long long)(layout & 1) << 50;
+  return h;
+}
+
+struct Launch {
+  int64_t n = 0;
+  int dtype = 0, op = 0, order = ORD_SEQ, phases = PH_RS | PH_AG, oneshot = 0;
+  int out_rel = 0, ag_in_rel = 0, average = 0, layout = CM_LAYOUT_RING;
+  int srcmode = SRC_COPYIN;
+  const void* in[MAXP] = {};
+  void* out[MAXP] = {};
+  int64_t zc_srcoff[MAXP] = {};
+};
+
+int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
+  const int p = c->size;
+  const size_t sz = dtype_size(L.dtype);
+  CollParams P;
+  memset(&P, 0, sizeof P);
+  for (int q = 0; q < p; ++q) P.heap[q] = c->heap[q];
+  const int nloc = c->virt ? p : 1;
+  for (int q = 0; q < nloc; ++q) {
+    P.in[q] = static_cast<const char*>(L.in[q]);
+    P.out[q] = static_cast<char*>(L.out[q]);
+    P.zc_srcoff[q] = L.zc_srcoff[q];
+  }
+  int64_t off[MAXP], len[MAXP];
+  if (L.oneshot) {
+    for (int q = 0; q < p; ++q) { off[q] = 0; len[q] = L.n; }
+  } else if (L.layout == CM_LAYOUT_RHD) {
+    rhd_layout(L.n, p, off, len);
+  } else {
+    chunk_partition(L.n, p, off, len);
+  }
+  int64_t maxseg = 0;
+  for (int q = 0; q < p; ++q) {
+    P.seg_off[q] = off[q];
+    P.seg_len[q] = len[q];
+    maxseg = std::max(maxseg, len[q]);
+  }
+  // staging capacity
+  const int64_t need = (L.srcmode == SRC_ZEROCOPY) ? (maxseg + SLICE_ALIGN) * (int64_t)sz
+                                                  : L.n * (int64_t)sz;
+  if (need > (int64_t)c->staging_bytes)
+    return fail(CM_ERR_CONFIG, "message of " + std::to_string(L.n * sz) + " B needs " +
+                                   std::to_string(need) + " B of staging; the communicator has " +
+                                   std::to_string(c->staging_bytes) +
+                                   " (raise staging_bytes or allocate the buffers with comm.alloc)");
+  P.n = L.n;
+  P.hdr = make_hdr(L.n, L.dtype, L.op, L.order, L.phases, L.oneshot, L.average, L.layout);
+  P.timeout_cycles = c->timeout_cycles;
+  P.staging_bytes = (long long)c->staging_bytes;
+  P.herr = c->herr_dev;
+  P.p = p;
+  P.rank = c->rank;
+  P.virt = c->virt ? 1 : 0;
+  P.srcmode = L.srcmode;
+  P.order = L.order;
+  P.phases = L.phases;
+  P.oneshot = L.oneshot;
+  P.out_rel = L.out_rel;
+  P.ag_in_rel = L.ag_in_rel;
+  P.average = L.average;
+
+  // grid: CTAs per rank; identical on every rank (depends on n, p, dtype only)
+  const int64_t work = L.oneshot ? L.n * (int64_t)sz : maxseg * (int64_t)sz;
+  const int64_t per = L.oneshot ? c->oneshot_bytes_per_cta : c->twoshot_bytes_per_cta;
+  int64_t nb = (work + per - 1) / per;
+  nb = std::max<int64_t>(1, std::min<int64_t>(nb, std::min(c->max_ctas, MAXBLK)));
+  KFn k = pick_kernel(L.dtype, L.op, p, L.order == ORD_TREE);
+  if (!k) return fail(CM_ERR_SHAPE, "unsupported dtype");
+  void* args[] = {&P};
+  if (c->virt) {
+    int per_sm = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k, THREADS, 0));
+    const int64_t cap = (int64_t)per_sm * c->sms / p;
+    if (cap < 1) return fail(CM_ERR_CONFIG, "virtual group too large for one GPU");
+    nb = std::min(nb, cap);
+    CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k, dim3((unsigned)nb, (unsigned)p),
+                                         dim3(THREADS), args, 0, stream));
+  } else {
+    CUDA_TRY(cudaLaunchKernel((const void*)k, dim3((unsigned)nb), dim3(THREADS), args, 0, stream));
+  }
+  c->launches += 1;
+  // real bytes pulled over NVLink by this rank
+  if (!c->virt) {
+    const int r = c->rank;
+    int64_t in_bytes = 0;
+    if (L.oneshot) in_bytes = (int64_t)(p - 1) * L.n * sz;
+    else {
+      if (L.phases & PH_RS) in_bytes += (int64_t)(p - 1) * len[r] * sz;
+      if (L.phases & PH_AG)
+        for (int q = 0; q < p; ++q)
+          if (q != r) in_bytes += len[q] * sz;
+    }
+    c->nvlink_in += in_bytes;
+  }
+  return CM_OK;
+}
+
+// Resolve send/recv placement for one call. Host buffers are bounced through
+// the device scratch buffer with cudaMemcpyAsync (CUDA-aware MPI semantics).
+struct Placement {
+  int srcmode = SRC_COPYIN;
+  const void* in = nullptr;
+  void* out = nullptr;
+  int64_t zc = 0;
+  bool recv_host = false;
+};
+
+int place(cm_comm* c, const void* send, int64_t send_bytes, void* recv, int64_t recv_bytes,
+          cudaStream_t stream, Placement* pl) {
+  int ks = CM_KIND_DEVICE, kr = CM_KIND_DEVICE;
+  int st;
+  if (send_bytes > 0 && (st = classify(c, send, &ks))) return st;
+  if (recv_bytes > 0 && (st = classify(c, recv, &kr))) return st;
+  pl->in = send;
+  pl->out = recv;
+  const int64_t need = std::max(send_bytes, recv_bytes);
+  if ((ks == CM_KIND_HOST || kr == CM_KIND_HOST) && need > (int64_t)c->staging_bytes)
+    return fail(CM_ERR_CONFIG, "host buffer larger than the device bounce buffer");
+  if (ks == CM_KIND_HOST) {
+    CUDA_TRY(cudaMemcpyAsync(c->scratch, send, send_bytes, cudaMemcpyHostToDevice, stream));
+    pl->in = c->scratch;
+  } else if (in_pool(c, send, send_bytes)) {
+    pl->srcmode = SRC_ZEROCOPY;
+    pl->zc = static_cast<const char*>(send) - c->local;
+  }
+  if (kr == CM_KIND_HOST) {
+    pl->out = c->scratch;
+    pl->recv_host = true;
+  }
+  return CM_OK;
+}
+
+void count_stats(cm_comm* c, const cm_stats_t& s) {
+  c->messages += s.messages_per_rank;
+  c->bytes += s.bytes_sent_per_rank;
+  c->calls += 1;
+}
+
+int identity_copy(cm_comm* c, const void* send, void* recv, int64_t bytes, cudaStream_t stream) {
+  (void)c;
+  if (bytes > 0 && send != recv) CUDA_TRY(cudaMemcpyAsync(recv, send, bytes, cudaMemcpyDefault, stream));
+  return CM_OK;
+}
+
+// one-shot or two-shot for a concrete algorithm
+void plan_algo(cm_comm* c, int concrete, int64_t nbytes, Launch* L) {
+  const bool small = nbytes <= c->oneshot_max_bytes;
+  if (concrete == CM_ALGO_RING) {
+    L->order = ORD_RING;
+    L->oneshot = 0;
+    L->layout = CM_LAYOUT_RING;
+  } else if (concrete == CM_ALGO_RHD) {
+    L->order = ORD_TREE;
+    L->oneshot = small ? 1 : 0;
+    L->layout = CM_LAYOUT_RHD;
+  } else {
+    L->order = ORD_SEQ;
+    L->oneshot = small ? 1 : 0;
+    L->layout = CM_LAYOUT_RING;
+  }
+  L->phases = L->oneshot ? PH_RS : (PH_RS | PH_AG);
+}
+
+int do_allreduce(cm_comm* c, const void* const* sends, void* const* recvs, int64_t count,
+                 int dtype, int op, int algo, int64_t switch_bytes, int average, void* stream_,
+                 cm_stats_t* stats) {
+  int st = check_dtype_op(dtype, op);
+  if (st) return st;
+  if (count < 0) return fail(CM_ERR_SHAPE, "negative element count");
+  if (average && (dtype == CM_INT32 || dtype == CM_INT64))
+    return fail(CM_ERR_SHAPE, "averaging needs a floating-point dtype");
+  if ((st = check_async_error(c))) return st;
+  const int64_t sz = (int64_t)dtype_size(dtype), nbytes = count * sz;
+  int concrete;
+  if ((st = cm_resolve_algorithm(algo, nbytes, switch_bytes, &concrete))) return st;
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  const int p = c->size;
+  const int nloc = c->virt ? p : 1;
+  for (int q = 0; q < nloc; ++q) {
+    const int r = c->virt ? q : c->rank;
+    cm_algo_stats(concrete, p, r, count, dtype, switch_bytes, &stats[q]);
+    count_stats(c, stats[q]);
+  }
+  if (p == 1) {  // collectives.py:86-87,119-120,169-170: input returned as is
+    return identity_copy(c, sends[0], recvs[0], nbytes, stream);
+  }
+  Launch L;
+  L.n = count;
+  L.dtype = dtype;
+  L.op = op;
+  L.average = average;
+  plan_algo(c, concrete, nbytes, &L);
+  Placement pl;
+  if (!c->virt) {
+    if ((st = place(c, sends[0], nbytes, recvs[0], nbytes, stream, &pl))) return st;
+    L.srcmode = pl.srcmode;
+    L.in[0] = pl.in;
+    L.out[0] = pl.out;
+    L.zc_srcoff[0] = pl.zc;
+  } else {
+    for (int q = 0; q < p; ++q) { L.in[q] = sends[q]; L.out[q] = recvs[q]; }
+  }
+  if ((st = launch_collective(c, L, stream))) return st;
+  if (pl.recv_host) CUDA_TRY(cudaMemcpyAsync(recvs[0], pl.out, nbytes, cudaMemcpyDeviceToHost, stream));
+  return CM_OK;
+}
+
+int do_rs(cm_comm* c, const void* const* sends, void* const* recvs, int64_t count, int dtype,
+          int op, int layout, void* stream_, cm_stats_t* stats) {
+  int st = check_dtype_op(dtype, op);
+  if (st) return st;
+  if (count < 0) return fail(CM_ERR_SHAPE, "negative element count");
+  if (layout != CM_LAYOUT_RING && layout != CM_LAYOUT_RHD) return fail(CM_ERR_CONFIG, "unknown layout");
+  if ((st = check_async_error(c))) return st;
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  const int p = c->size;
+  const int64_t sz = (int64_t)dtype_size(dtype);
+  int64_t off[MAXP], len[MAXP];
+  cm_layout(layout, count, p, off, len);
+  const int nloc = c->virt ? p : 1;
+  for (int q = 0; q < nloc; ++q) {
+    const int r = c->virt ? q : c->rank;
+    cm_rs_stats(layout, p, r, count, dtype, &stats[q]);
+    count_stats(c, stats[q]);
+  }
+  if (p == 1) return identity_copy(c, sends[0], recvs[0], count * sz, stream);
+  Launch L;
+  L.n = count;
+  L.dtype = dtype;
+  L.op = op;
+  L.layout = layout;
+  L.order = layout == CM_LAYOUT_RING ? ORD_RING : ORD_TREE;
+  L.phases = PH_RS;
+  L.out_rel = 1;
+  Placement pl;
+  if (!c->virt) {
+    if ((st = place(c, sends[0], count * sz, recvs[0], len[c->rank] * sz, stream, &pl))) return st;
+    L.srcmode = pl.srcmode;
+    L.in[0] = pl.in;
+    L.out[0] = pl.out;
+    L.zc_srcoff[0] = pl.zc;
+  } else {
+    for (int q = 0; q < p; ++q) { L.in[q] = sends[q]; L.out[q] = recvs[q]; }
+  }
+  if ((st = launch_collective(c, L, stream))) return st;
+  if (pl.recv_host)
+    CUDA_TRY(cudaMemcpyAsync(recvs[0], pl.out, len[c->rank] * sz, cudaMemcpyDeviceToHost, stream));
+  return CM_OK;
+}
+
+int do_ag(cm_comm* c, const void* const* sends, void* const* recvs, int64_t count, int dtype,
+          int layout, void* stream_, cm_stats_t* stats) {
+  int st = check_dtype_op(dtype, CM_SUM);
+  if (st) return st;
+  if (count < 0) return fail(CM_ERR_SHAPE, "negative element count");
+  if (layout != CM_LAYOUT_RING && layout != CM_LAYOUT_RHD) return fail(CM_ERR_CONFIG, "unknown layout");
+  if ((st = check_async_error(c))) return st;
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  const int p = c->size;
+  const int64_t sz = (int64_t)dtype_size(dtype);
+  int64_t off[MAXP], len[MAXP];
+  cm_layout(layout, count, p, off, len);
+  const int nloc = c->virt ? p : 1;
+  for (int q = 0; q < nloc; ++q) {
+    const int r = c->virt ? q : c->rank;
+    cm_ag_stats(layout, p, r, count, dtype, &stats[q]);
+    count_stats(c, stats[q]);
+  }
+  if (p == 1) return identity_copy(c, sends[0], recvs[0], count * sz, stream);
+  Launch L;
+  L.n = count;
+  L.dtype = dtype;
+  L.op = CM_SUM;
+  L.layout = layout;
+  L.order = ORD_SEQ;
+  L.phases = PH_AG;
+  L.ag_in_rel = 1;
+  Placement pl;
+  if (!c->virt) {
+    if ((st = place(c, sends[0], len[c->rank] * sz, recvs[0], count * sz, stream, &pl))) return st;
+    L.srcmode = pl.srcmode;
+    L.in[0] = pl.in;
+    L.out[0] = pl.out;
+    L.zc_srcoff[0] = pl.zc;
+  } else {
+    for (int q = 0; q < p; ++q) { L.in[q] = sends[q]; L.out[q] = recvs[q]; }
+  }
+  if ((st = launch_collective(c, L, stream))) return st;
+  if (pl.recv_host)
+    CUDA_TRY(cudaMemcpyAsync(recvs[0], pl.out, count * sz, cudaMemcpyDeviceToHost, stream));
+  return CM_OK;
+}
+
+int launch_batched_copy(cm_comm* c, int n, const void* const* srcs, void* const* dsts,
+                        const int64_t* nbytes, bool staged, cudaStream_t stream) {
+  for (int base = 0; base < n; base += MAXCOPY) {
+    const int m = std::min(MAXCOPY, n - base);
+    CopyParams P;
+    memset(&P, 0, sizeof P);
+    P.n = m;
+    P.start[0] = 0;
+    for (int i = 0; i < m; ++i) {
+      P.src[i] = static_cast<const char*>(srcs[base + i]);
+      P.dst[i] = static_cast<char*>(dsts[base + i]);
+      P.start[i + 1] = P.start[i] + nbytes[base + i];
+    }
+    if (P.start[m] == 0) continue;
+    P.staged = staged ? 1 : 0;
+    if (c) {
+      P.heap = c->local;
+      P.staging_bytes = (long long)c->staging_bytes;
+    }
+    int64_t nb = (P.start[m] + (128 << 10) - 1) / (128 << 10);
+    nb = std::max<int64_t>(1, std::min<int64_t>(nb, 148 * 4));
+    void* args[] = {&P};
+    CUDA_TRY(cudaLaunchKernel((const void*)batched_copy_kernel, dim3((unsigned)nb), dim3(THREADS),
+                              args, 0, stream));
+    if (c) c->launches += 1;
+  }
+  return CM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int cm_comm_create(int rank, int size, int device, int64_t staging_bytes, int64_t pool_bytes,
+                   cm_comm_t** out) {
+  if (size < 1 || size > MAXP) return fail(CM_ERR_INVALID_GROUP, "group size must be in 1.." + std::to_string(MAXP));
+  if (rank < 0 || rank >= size) return fail(CM_ERR_INVALID_GROUP, "rank outside group");
+  if (staging_bytes < 0 || pool_bytes < 0) return fail(CM_ERR_VALUE, "negative size");
+  CUDA_TRY(cudaSetDevice(device));
+  auto* c = new cm_comm();
+  c->rank = rank;
+  c->size = size;
+  c->device = device;
+  c->staging_bytes = round_up(std::max<int64_t>(staging_bytes, 1), HEAP_ALIGN);
+  c->pool_bytes = round_up((size_t)pool_bytes, HEAP_ALIGN);
+  c->heap_bytes = STAGING_OFF + 2 * c->staging_bytes + c->pool_bytes;
+  c->reg.policy = CM_LAZY_CACHE;
+  c->reg.simulated = false;
+  cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
+  cudaError_t e = cudaMalloc(&c->local, c->heap_bytes);
+  if (e != cudaSuccess) { delete c; return cuda_fail(e, "cudaMalloc(heap)"); }
+  e = cudaMemset(c->local, 0, CTRL_REGION);
+  if (e == cudaSuccess) e = cudaMalloc(&c->scratch, c->staging_bytes);
+  if (e == cudaSuccess) e = cudaHostAlloc(&c->herr_host, sizeof(unsigned), cudaHostAllocMapped);
+  if (e == cudaSuccess) e = cudaHostGetDevicePointer(&c->herr_dev, c->herr_host, 0);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) { cm_comm_destroy(c); return cuda_fail(e, "cm_comm_create"); }
+  *c->herr_host = 0;
+  c->heap[rank] = c->local;
+  if (c->pool_bytes) c->pool_free[STAGING_OFF + 2 * c->staging_bytes] = c->pool_bytes;
+  if (size == 1) c->connected = true;
+  *out = c;
+  return CM_OK;
+}
+
+int cm_comm_ipc_handle(cm_comm_t* c, void* handle_out) {
+  if (c->virt) return fail(CM_ERR_UNSUPPORTED, "virtual groups have no IPC handle");
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, c->local));
+  static_assert(sizeof(h) == CM_IPC_HANDLE_BYTES, "IPC handle size");
+  memcpy(handle_out, &h, sizeof h);
+  return CM_OK;
+}
+
+int cm_comm_connect(cm_comm_t* c, const void* all_handles) {
+  if (c->virt) return CM_OK;
+  CUDA_TRY(cudaSetDevice(c->device));
+  const char* hs = static_cast<const char*>(all_handles);
+  for (int q = 0; q < c->size; ++q) {
+    if (q == c->rank) continue;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, hs + (size_t)q * CM_IPC_HANDLE_BYTES, sizeof h);
+    void* ptr = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return cuda_fail(e, ("cudaIpcOpenMemHandle(peer " + std::to_string(q) + ")").c_str());
+    c->heap[q] = static_cast<char*>(ptr);
+  }
+  c->connected = true;
+  return CM_OK;
+}
+
+int cm_comm_create_virtual(int size, int device, int64_t staging_bytes, cm_comm_t** out) {
+  if (size < 1 || size > MAXP) return fail(CM_ERR_INVALID_GROUP, "group size must be in 1.." + std::to_string(MAXP));
+  CUDA_TRY(cudaSetDevice(device));
+  auto* c = new cm_comm();
+  c->virt = true;
+  c->size = size;
+  c->device = device;
+  c->staging_bytes = round_up(std::max<int64_t>(staging_bytes, 1), HEAP_ALIGN);
+  c->heap_bytes = STAGING_OFF + 2 * c->staging_bytes;
+  c->reg.policy = CM_LAZY_CACHE;
+  c->reg.simulated = false;
+  cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
+  cudaError_t e = cudaMalloc(&c->local, c->heap_bytes * size);
+  if (e != cudaSuccess) { delete c; return cuda_fail(e, "cudaMalloc(virtual heaps)"); }
+  for (int q = 0; q < size && e == cudaSuccess; ++q) {
+    c->heap[q] = c->local + c->heap_bytes * q;
+    e = cudaMemset(c->heap[q], 0, CTRL_REGION);
+  }
+  if (e == cudaSuccess) e = cudaHostAlloc(&c->herr_host, sizeof(unsigned), cudaHostAllocMapped);
+  if (e == cudaSuccess) e = cudaHostGetDevicePointer(&c->herr_dev, c->herr_host, 0);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) { cm_comm_destroy(c); return cuda_fail(e, "cm_comm_create_virtual"); }
+  *c->herr_host = 0;
+  c->connected = true;
+  *out = c;
+  return CM_OK;
+}
+
+int cm_comm_destroy(cm_comm_t* c) {
+  if (!c) return CM_OK;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  if (!c->virt)
+    for (int q = 0; q < c->size; ++q)
+      if (q != c->rank && c->heap[q]) cudaIpcCloseMemHandle(c->heap[q]);
+  if (c->local) cudaFree(c->local);
+  if (c->scratch) cudaFree(c->scratch);
+  if (c->herr_host) cudaFreeHost(c->herr_host);
+  cudaGetLastError();
+  delete c;
+  return CM_OK;
+}
+
+int cm_comm_rank(cm_comm_t* c, int* rank) { *rank = c->rank; return CM_OK; }
+int cm_comm_size(cm_comm_t* c, int* size) { *size = c->size; return CM_OK; }
+
+int cm_comm_set_timeout(cm_comm_t* c, double seconds) {
+  if (!(seconds > 0)) return fail(CM_ERR_VALUE, "timeout must be positive");
+  int khz = 0;
+  cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, c->device);
+  if (khz <= 0) khz = 2000000;
+  c->timeout_cycles = (unsigned long long)(seconds * khz * 1e3);
+  return CM_OK;
+}
+
+int cm_comm_set_policy(cm_comm_t* c, int policy) {
+  if (policy < CM_NO_CACHE || policy > CM_INTERCEPT_CACHE) return fail(CM_ERR_VALUE, "unknown policy");
+  std::lock_guard<std::mutex> g(c->reg.mu);
+  c->reg.policy = policy;
+  c->reg.cache.clear();
+  return CM_OK;
+}
+
+int cm_comm_registry(cm_comm_t* c, cm_registry_t** reg) {
+  *reg = reinterpret_cast<cm_registry_t*>(&c->reg);
+  return CM_OK;
+}
+
+int cm_comm_set_param(cm_comm_t* c, const char* key, int64_t value) {
+  const std::string k(key);
+  if (value <= 0) return fail(CM_ERR_VALUE, "parameter must be positive");
+  if (k == "oneshot_max_bytes") c->oneshot_max_bytes = value;
+  else if (k == "oneshot_bytes_per_cta") c->oneshot_bytes_per_cta = value;
+  else if (k == "twoshot_bytes_per_cta") c->twoshot_bytes_per_cta = value;
+  else if (k == "max_ctas") c->max_ctas = (int)std::min<int64_t>(value, MAXBLK);
+  else return fail(CM_ERR_CONFIG, "unknown parameter " + k);
+  return CM_OK;
+}
+
+int cm_comm_get_param(cm_comm_t* c, const char* key, int64_t* value) {
+  const std::string k(key);
+  if (k == "oneshot_max_bytes") *value = c->oneshot_max_bytes;
+  else if (k == "oneshot_bytes_per_cta") *value = c->oneshot_bytes_per_cta;
+  else if (k == "twoshot_bytes_per_cta") *value = c->twoshot_bytes_per_cta;
+  else if (k == "max_ctas") *value = c->max_ctas;
+  else if (k == "staging_bytes") *value = (int64_t)c->staging_bytes;
+  else if (k == "pool_bytes") *value = (int64_t)c->pool_bytes;
+  else return fail(CM_ERR_CONFIG, "unknown parameter " + k);
+  return CM_OK;
+}
+
+int cm_comm_alloc(cm_comm_t* c, int64_t bytes, void** ptr) {
+  if (c->virt) return fail(CM_ERR_UNSUPPORTED, "virtual groups have no symmetric pool");
+  if (bytes <= 0) return fail(CM_ERR_VALUE, "allocation size must be positive");
+  const size_t need = round_up((size_t)bytes, 512);
+  for (auto it = c->pool_free.begin(); it != c->pool_free.end(); ++it) {
+    if (it->second >= need) {
+      const size_t off = it->first, rest = it->second - need;
+      c->pool_free.erase(it);
+      if (rest) c->pool_free[off + need] = rest;
+      c->pool_used[off] = need;
+      *ptr = c->local + off;
+      return CM_OK;
+    }
+  }
+  return fail(CM_ERR_CONFIG, "symmetric pool exhausted (" + std::to_string(bytes) + " B requested)");
+}
+
+int cm_comm_free(cm_comm_t* c, void* ptr) {
+  const size_t off = static_cast<char*>(ptr) - c->local;
+  auto it = c->pool_used.find(off);
+  if (it == c->pool_used.end()) return fail(CM_ERR_INVALID_HANDLE, "free of unknown symmetric buffer");
+  size_t o = off, len = it->second;
+  c->pool_used.erase(it);
+  auto nx = c->pool_free.lower_bound(o);
+  if (nx != c->pool_free.end() && nx->first == o + len) { len += nx->second; c->pool_free.erase(nx); }
+  auto pv = c->pool_free.lower_bound(o);
+  if (pv != c->pool_free.begin()) {
+    --pv;
+    if (pv->first + pv->second == o) { o = pv->first; len += pv->second; c->pool_free.erase(pv); }
+  }
+  c->pool_free[o] = len;
+  return CM_OK;
+}
+
+int cm_comm_sync(cm_comm_t* c, void* stream) {
+  CUDA_TRY(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  return check_async_error(c);
+}
+
+int cm_comm_poll(cm_comm_t* c) { return check_async_error(c); }
+
+int cm_comm_counters(cm_comm_t* c, int64_t* messages_sent, int64_t* bytes_sent,
+                     int64_t* nvlink_bytes_in, int64_t* calls) {
+  *messages_sent = c->messages;
+  *bytes_sent = c->bytes;
+  *nvlink_bytes_in = c->nvlink_in;
+  *calls = c->calls;
+  return CM_OK;
+}
+
+int cm_comm_launches(cm_comm_t* c, int64_t* launches) {
+  *launches = c->launches;
+  return CM_OK;
+}
+
+int cm_allreduce(cm_comm_t* c, const void* send, void* recv, int64_t count, int dtype, int op,
+                 int algo, int64_t switch_bytes, int average, void* stream, cm_stats_t* stats) {
+  if (c->virt) return fail(CM_ERR_UNSUPPORTED, "use cm_allreduce_v on a virtual group");
+  return do_allreduce(c, &send, &recv, count, dtype, op, algo, switch_bytes, average, stream, stats);
+}
+
+int cm_allreduce_v(cm_comm_t* c, const void* const* sends, void* const* recvs, int64_t count,
+                   int dtype, int op, int algo, int64_t switch_bytes, int average, void* stream,
+                   cm_stats_t* stats) {
+  if (!c->virt) return fail(CM_ERR_UNSUPPORTED, "cm_allreduce_v needs a virtual group");
+  return do_allreduce(c, sends, recvs, count, dtype, op, algo, switch_bytes, average, stream, stats);
+}
+
+int cm_reduce_scatter(cm_comm_t* c, const void* send, void* recv, int64_t count, int dtype, int op,
+                      int layout, void* stream, cm_stats_t* stats) {
+  if (c->virt) return fail(CM_ERR_UNSUPPORTED, "use cm_reduce_scatter_v on a virtual group");
+  return do_rs(c, &send, &recv, count, dtype, op, layout, stream, stats);
+}
+
+int cm_reduce_scatter_v(cm_comm_t* c, const void* const* sends, void* const* recvs, int64_t count,
+                        int dtype, int op, int layout, void* stream, cm_stats_t* stats) {
+  if (!c->virt) return fail(CM_ERR_UNSUPPORTED, "needs a virtual group");
+  return do_rs(c, sends, recvs, count, dtype, op, layout, stream, stats);
+}
+
+int cm_allgather(cm_comm_t* c, const void* send, void* recv, int64_t count, int dtype, int layout,
+                 void* stream, cm_stats_t* stats) {
+  if (c->virt) return fail(CM_ERR_UNSUPPORTED, "use cm_allgather_v on a virtual group");
+  return do_ag(c, &send, &recv, count, dtype, layout, stream, stats);
+}
+
+int cm_allgather_v(cm_comm_t* c, const void* const* sends, void* const* recvs, int64_t count,
+                   int dtype, int layout, void* stream, cm_stats_t* stats) {
+  if (!c->virt) return fail(CM_ERR_UNSUPPORTED, "needs a virtual group");
+  return do_ag(c, sends, recvs, count, dtype, layout, stream, stats);
+}
+
+int cm_fused_allreduce(cm_comm_t* c, int n, const void* const* sends, const int64_t* counts,
+                       int dtype, void* recv_fused, int algo, int64_t threshold,
+                       int64_t switch_bytes, int average, void* stream_, cm_stats_t* stats,
+                       int* n_calls) {
+  if (c->virt) return fail(CM_ERR_UNSUPPORTED, "fused allreduce needs a real communicator");
+  int st = check_dtype_op(dtype, CM_SUM);
+  if (st) return st;
+  if (average && (dtype == CM_INT32 || dtype == CM_INT64))
+    return fail(CM_ERR_SHAPE, "averaging needs a floating-point dtype");
+  if ((st = check_async_error(c))) return st;
+  if (threshold <= 0) return fail(CM_ERR_VALUE, "fusion threshold must be positive");
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  const int64_t sz = (int64_t)dtype_size(dtype);
+  std::vector<int64_t> nbytes(n);
+  std::vector<int> dts(n, dtype), group(n);
+  for (int i = 0; i < n; ++i) nbytes[i] = counts[i] * sz;
+  int ngroups = 0;
+  cm_fuse_plan(n, nbytes.data(), dts.data(), threshold, group.data(), &ngroups);
+  int rk;
+  if ((st = classify(c, recv_fused, &rk))) return st;
+  if (rk != CM_KIND_DEVICE) return fail(CM_ERR_UNSUPPORTED, "fused output must be device memory");
+  const int p = c->size;
+  int64_t fused_off = 0;  // elements
+  int i = 0;
+  for (int g = 0; g < ngroups; ++g) {
+    int j = i;
+    int64_t ng = 0;
+    bool any_host = false;
+    while (j < n && group[j] == g) {
+      int k = CM_KIND_DEVICE;
+      // aggregation.py:159-161: classify every member once per allreduce call
+      if (counts[j] > 0 && (st = classify(c, sends[j], &k))) return st;
+      any_host = any_host || (k == CM_KIND_HOST);
+      ng += counts[j];
+      ++j;
+    }
+    char* out = static_cast<char*>(recv_fused) + fused_off * sz;
+    int concrete;
+    if ((st = cm_resolve_algorithm(algo, ng * sz, switch_bytes, &concrete))) return st;
+    cm_algo_stats(concrete, p, c->rank, ng, dtype, switch_bytes, &stats[g]);
+    count_stats(c, stats[g]);
+    std::vector<const void*> srcs;
+    std::vector<void*> dsts;
+    std::vector<int64_t> bytes;
+    int64_t off = 0;
+    for (int k = i; k < j; ++k) {
+      srcs.push_back(sends[k]);
+      bytes.push_back(counts[k] * sz);
+      dsts.push_back(nullptr);
+      off += counts[k] * sz;
+    }
+    if (ng * sz > (int64_t)c->staging_bytes)
+      return fail(CM_ERR_CONFIG, "fused buffer of " + std::to_string(ng * sz) +
+                                     " B exceeds the staging area; lower the fusion threshold");
+    if (p == 1) {  // allreduce is the identity; the mean divides by 1
+      off = 0;
+      for (int k = i; k < j; ++k) { dsts[k - i] = out + off; off += counts[k] * sz; }
+      if (any_host) {
+        for (int k = i; k < j; ++k)
+          if (counts[k]) CUDA_TRY(cudaMemcpyAsync(dsts[k - i], srcs[k - i], bytes[k - i], cudaMemcpyDefault, stream));
+      } else if ((st = launch_batched_copy(c, j - i, srcs.data(), dsts.data(), bytes.data(), false, stream))) {
+        return st;
+      }
+    } else {
+      Launch L;
+      L.n = ng;
+      L.dtype = dtype;
+      L.op = CM_SUM;
+      L.average = average;
+      plan_algo(c, concrete, ng * sz, &L);
+      L.out[0] = out;
+      if (any_host) {  // bounce through device scratch, then copy-in
+        off = 0;
+        for (int k = i; k < j; ++k) {
+          if (counts[k]) CUDA_TRY(cudaMemcpyAsync(c->scratch + off, sends[k], counts[k] * sz, cudaMemcpyDefault, stream));
+          off += counts[k] * sz;
+        }
+        L.srcmode = SRC_COPYIN;
+        L.in[0] = c->scratch;
+      } else {         // pack straight into the IPC staging area (no extra copy)
+        off = 0;
+        for (int k = i; k < j; ++k) {
+          dsts[k - i] = reinterpret_cast<void*>((uintptr_t)off);
+          off += counts[k] * sz;
+        }
+        if ((st = launch_batched_copy(c, j - i, srcs.data(), dsts.data(), bytes.data(), true, stream)))
+          return st;
+        L.srcmode = SRC_PRESTAGED;
+      }
+      if ((st = launch_collective(c, L, stream))) return st;
+    }
+    fused_off += ng;
+    i = j;
+  }
+  *n_calls = ngroups;
+  return CM_OK;
+}
+
+int cm_local_reduce(const void* a, const void* b, void* out, int64_t count, int dtype, int op,
+                    void* stream) {
+  int st = check_dtype_op(dtype, op);
+  if (st) return st;
+  if (count <= 0) return CM_OK;
+  const bool vec = ((((uintptr_t)a) | ((uintptr_t)b) | ((uintptr_t)out)) & 15u) == 0;
+  const int64_t nb = std::max<int64_t>(1, std::min<int64_t>((count + THREADS * 8 - 1) / (THREADS * 8), 148 * 8));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const char* pa = static_cast<const char*>(a);
+  const char* pb = static_cast<const char*>(b);
+  char* po = static_cast<char*>(out);
+  const int v = vec ? 1 : 0;
+#define LR(D)                                                                                   \
+  if (op == CM_SUM) local_reduce_kernel<D, CM_SUM><<<(unsigned)nb, THREADS, 0, s>>>(pa, pb, po, count, v); \
+  else local_reduce_kernel<D, CM_MAX><<<(unsigned)nb, THREADS, 0, s>>>(pa, pb, po, count, v);
+  switch (dtype) {
+    case CM_FLOAT32: LR(F32); break;
+    case CM_FLOAT64: LR(F64); break;
+    case CM_BFLOAT16: LR(BF16); break;
+    case CM_INT32: LR(I32); break;
+    case CM_INT64: LR(I64); break;
+  }
+#undef LR
+  CUDA_TRY(cudaGetLastError());
+  return CM_OK;
+}
+
+int cm_batched_copy(int n, const void* const* srcs, void* const* dsts, const int64_t* nbytes,
+                    void* stream) {
+  if (n < 0) return fail(CM_ERR_VALUE, "negative count");
+  return launch_batched_copy(nullptr, n, srcs, dsts, nbytes, false, static_cast<cudaStream_t>(stream));
+}
+
+int cm_time_allreduce(cm_comm_t* c, const void* send, void* recv, int64_t count, int dtype, int op,
+                      int algo, int64_t switch_bytes, int iters, int warmup, void* stream,
+                      double* ms_per_call) {
+  if (iters < 1) return fail(CM_ERR_VALUE, "iters must be >= 1");
+  cm_stats_t stv[MAXP];
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  for (int i = 0; i < warmup; ++i) {
+    int st = c->virt ? CM_ERR_UNSUPPORTED : cm_allreduce(c, send, recv, count, dtype, op, algo, switch_bytes, 0, stream, stv);
+    if (st) return st;
+  }
+  cudaEvent_t e0, e1;
+  CUDA_TRY(cudaEventCreate(&e0));
+  CUDA_TRY(cudaEventCreate(&e1));
+  CUDA_TRY(cudaEventRecord(e0, s));
+  for (int i = 0; i < iters; ++i) {
+    int st = cm_allreduce(c, send, recv, count, dtype, op, algo, switch_bytes, 0, stream, stv);
+    if (st) return st;
+  }
+  CUDA_TRY(cudaEventRecord(e1, s));
+  CUDA_TRY(cudaEventSynchronize(e1));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  *ms_per_call = ms / iters;
+  return check_async_error(c);
+}
+
+}  // extern "C"

@@ -1,0 +1,622 @@
+// sm_100a device code for the CUDA-aware allreduce.
+//
+// One kernel family (`collective_kernel`) implements every collective of the
+// reference allreduce suite over a CUDA-IPC peer-mapped symmetric heap:
+//
+//   one-shot  : every rank reduces the whole vector from all p peers' staged
+//               copies (small messages; RHD tree order or flat order)
+//   two-shot  : reduce-scatter (rank r reduces its layout segment from all p
+//               peers, in the reference fold order) -> per-CTA flag barrier ->
+//               allgather (rank r pulls every other segment). This is the ring
+//               RSA (collectives.py:107-152) / RHD RSA (:155-236) data movement
+//               collapsed onto NVSwitch's full crossbar: the same 2(p-1)/p*S
+//               bytes per GPU per direction, two sync points instead of 2(p-1),
+//               and the per-element fold order of the reference replayed
+//               exactly so results are bit-identical.
+//   RS-only / AG-only : the public reduce_scatter / allgather.
+//
+// Synchronisation is flag based over NVLink: CTA b of rank r publishes a
+// record {epoch, header, src offset, reduced offset} into slot [parity][b][r]
+// of every peer's heap with st.release.sys, and waits on its own heap with
+// ld.acquire.sys. The epoch lives in device memory and is advanced by the last
+// CTA of each launch, so launches can be captured into CUDA graphs. Staging is
+// double-buffered by epoch parity: a rank rewrites staging[e&1] only in call
+// e+2, after every peer has entered call e+1 (and therefore left call e).
+// Waits are bounded (timeout -> CM_ERR_TRANSPORT in the host-mapped error word).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "cm.h"
+
+namespace cm {
+namespace dev {
+
+constexpr int MAXP = CM_MAX_RANKS;
+constexpr int MAXBLK = 1024;
+constexpr int THREADS = 512;
+constexpr int SLICE_ALIGN = 64;  // elements; slice boundaries are multiples of this
+
+// ---- heap layout (identical on every rank) ---------------------------------
+constexpr size_t CTRL_OFF = 0;
+constexpr size_t REC_OFF = 4096;
+constexpr size_t REC_BYTES = 32;
+constexpr size_t REC_SIZE = 2ull * MAXBLK * MAXP * REC_BYTES;
+constexpr size_t MID_OFF = REC_OFF + REC_SIZE;
+constexpr size_t MID_SIZE = (size_t)MAXBLK * MAXP * 8;
+constexpr size_t HEAP_ALIGN = 2ull << 20;
+constexpr size_t CTRL_REGION = ((MID_OFF + MID_SIZE + HEAP_ALIGN - 1) / HEAP_ALIGN) * HEAP_ALIGN;
+constexpr size_t STAGING_OFF = CTRL_REGION;
+
+struct Ctrl {
+  unsigned long long epoch;  // calls completed by this rank
+  unsigned int done;         // CTAs finished in the current call
+  unsigned int pad;
+};
+
+struct Rec {
+  unsigned long long epoch;
+  unsigned long long hdr;
+  long long srcoff;  // element i of the sender's input at heap + srcoff + i*sz
+  long long redoff;  // element i of the sender's segment at heap + redoff + (i-seg_off)*sz
+};
+
+enum SrcMode { SRC_COPYIN = 0, SRC_PRESTAGED = 1, SRC_ZEROCOPY = 2 };
+enum Order { ORD_SEQ = 0, ORD_RING = 1, ORD_TREE = 2 };
+enum Phase { PH_RS = 1, PH_AG = 2 };
+enum Err { ERR_SHAPE = 1, ERR_TRANSPORT = 4 };
+
+struct CollParams {
+  char* heap[MAXP];          // every rank's heap, mapped in this process
+  const char* in[MAXP];      // per local rank (real mode: [0])
+  char* out[MAXP];
+  long long seg_off[MAXP];   // layout segment per rank (elements)
+  long long seg_len[MAXP];
+  long long n;               // full vector length (elements)
+  long long zc_srcoff[MAXP]; // ZEROCOPY: byte offset of `in` within own heap (per local rank)
+  unsigned long long hdr;    // call signature checked against every peer
+  unsigned long long timeout_cycles;
+  long long staging_bytes;   // per parity half
+  unsigned int* herr;        // host-mapped error word
+  int p;
+  int rank;                  // real mode
+  int virt;                  // 1: blockIdx.y is the rank (single-GPU emulation)
+  int srcmode;
+  int order;                 // Order
+  int phases;                // Phase bits
+  int oneshot;               // every segment is [0, n)
+  int out_rel;               // RS writes out[i - seg_off] (reduce_scatter API)
+  int ag_in_rel;             // AG-only: `in` holds only my segment (in[i - seg_off])
+  int average;               // divide the reduced value by p (aggregate mean)
+};
+
+// ---- element types ----------------------------------------------------------
+struct F32 { using S = float;    using A = float; };
+struct F64 { using S = double;   using A = double; };
+struct BF16 { using S = uint16_t; using A = float; };
+struct I32 { using S = int32_t;  using A = int32_t; };
+struct I64 { using S = int64_t;  using A = int64_t; };
+
+__device__ __forceinline__ float bf16_to_f32(uint16_t h) {
+  return __uint_as_float(((unsigned)h) << 16);
+}
+// round-to-nearest-even, NaN -> 0x7FC0 (matches oracle/collectives.f32_to_bf16)
+__device__ __forceinline__ uint16_t f32_to_bf16(float f) {
+  const unsigned u = __float_as_uint(f);
+  if ((u & 0x7fffffffu) > 0x7f800000u) return 0x7FC0;
+  return (uint16_t)((u + 0x7fffu + ((u >> 16) & 1u)) >> 16);
+}
+
+template <class D> __device__ __forceinline__ typename D::A to_acc(typename D::S s) { return s; }
+template <> __device__ __forceinline__ float to_acc<BF16>(uint16_t s) { return bf16_to_f32(s); }
+template <class D> __device__ __forceinline__ typename D::S from_acc(typename D::A a) { return a; }
+template <> __device__ __forceinline__ uint16_t from_acc<BF16>(float a) { return f32_to_bf16(a); }
+
+// _reduce_arrays (collectives.py:57-64): `a` is the accumulator (first operand).
+// MAX is numpy.maximum bit for bit: (a > b || isnan(a)) ? a : b.
+template <int OP, typename A> __device__ __forceinline__ A op2(A a, A b);
+template <> __device__ __forceinline__ float op2<CM_SUM, float>(float a, float b) { return __fadd_rn(a, b); }
+template <> __device__ __forceinline__ double op2<CM_SUM, double>(double a, double b) { return __dadd_rn(a, b); }
+template <> __device__ __forceinline__ int32_t op2<CM_SUM, int32_t>(int32_t a, int32_t b) {
+  return (int32_t)((uint32_t)a + (uint32_t)b);
+}
+template <> __device__ __forceinline__ int64_t op2<CM_SUM, int64_t>(int64_t a, int64_t b) {
+  return (int64_t)((uint64_t)a + (uint64_t)b);
+}
+template <> __device__ __forceinline__ float op2<CM_MAX, float>(float a, float b) { return (a > b || a != a) ? a : b; }
+template <> __device__ __forceinline__ double op2<CM_MAX, double>(double a, double b) { return (a > b || a != a) ? a : b; }
+template <> __device__ __forceinline__ int32_t op2<CM_MAX, int32_t>(int32_t a, int32_t b) { return a > b ? a : b; }
+template <> __device__ __forceinline__ int64_t op2<CM_MAX, int64_t>(int64_t a, int64_t b) { return a > b ? a : b; }
+
+// IEEE division by p (aggregation.py:167-172: float32(float64(s)/p) == s/(float)p)
+template <typename A> __device__ __forceinline__ A div_p(A a, int p);
+template <> __device__ __forceinline__ float div_p<float>(float a, int p) { return __fdiv_rn(a, (float)p); }
+template <> __device__ __forceinline__ double div_p<double>(double a, int p) { return __ddiv_rn(a, (double)p); }
+template <> __device__ __forceinline__ int32_t div_p<int32_t>(int32_t a, int) { return a; }
+template <> __device__ __forceinline__ int64_t div_p<int64_t>(int64_t a, int) { return a; }
+
+// ---- memory-model helpers -----------------------------------------------------
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_sys_s64(long long* p, long long v) {
+  asm volatile("st.relaxed.sys.global.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ long long ld_relaxed_sys_s64(const long long* p) {
+  long long v;
+  asm volatile("ld.relaxed.sys.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ Rec* rec_slot(char* heap, int par, int blk, int src) {
+  return reinterpret_cast<Rec*>(heap + REC_OFF +
+                                ((size_t)(par * MAXBLK + blk) * MAXP + src) * REC_BYTES);
+}
+__device__ __forceinline__ unsigned long long* mid_slot(char* heap, int blk, int src) {
+  return reinterpret_cast<unsigned long long*>(heap + MID_OFF + ((size_t)blk * MAXP + src) * 8);
+}
+
+// bounded spin: returns false on timeout
+__device__ __forceinline__ bool wait_geq(const unsigned long long* f, unsigned long long e,
+                                         unsigned long long timeout) {
+  if (ld_acquire_sys(f) >= e) return true;
+  const long long t0 = clock64();
+  while (true) {
+    for (int i = 0; i < 64; ++i)
+      if (ld_acquire_sys(f) >= e) return true;
+    if ((unsigned long long)(clock64() - t0) > timeout) return false;
+  }
+}
+
+// Slice b of segment [off, off+len) split over nb CTAs; interior boundaries
+// are multiples of SLICE_ALIGN (absolute element index) so they are vector
+// aligned and independent of the vector width.
+__device__ __forceinline__ long long slice_bound(long long off, long long len, int k, int nb) {
+  if (k <= 0) return off;
+  if (k >= nb) return off + len;
+  long long x = off + (long long)(((__int128)len * k) / nb);
+  x = (x / SLICE_ALIGN) * SLICE_ALIGN;
+  if (x < off) x = off;
+  if (x > off + len) x = off + len;
+  return x;
+}
+
+// ---- vector load/store of W elements (16 B when W*sizeof(S)==16) ---------------
+template <class D, int W>
+__device__ __forceinline__ void load_vec(const char* base, long long i, typename D::A (&v)[W]) {
+  using S = typename D::S;
+  const S* p = reinterpret_cast<const S*>(base) + i;
+  if constexpr (W * sizeof(S) == 16) {
+    uint4 raw = *reinterpret_cast<const uint4*>(p);
+    const S* s = reinterpret_cast<const S*>(&raw);
+#pragma unroll
+    for (int w = 0; w < W; ++w) v[w] = to_acc<D>(s[w]);
+  } else {
+#pragma unroll
+    for (int w = 0; w < W; ++w) v[w] = to_acc<D>(p[w]);
+  }
+}
+
+template <class D, int W>
+__device__ __forceinline__ void store_vec(char* base, long long i, const typename D::A (&v)[W]) {
+  using S = typename D::S;
+  S* p = reinterpret_cast<S*>(base) + i;
+  if constexpr (W * sizeof(S) == 16) {
+    uint4 raw;
+    S* s = reinterpret_cast<S*>(&raw);
+#pragma unroll
+    for (int w = 0; w < W; ++w) s[w] = from_acc<D>(v[w]);
+    *reinterpret_cast<uint4*>(p) = raw;
+  } else {
+#pragma unroll
+    for (int w = 0; w < W; ++w) p[w] = from_acc<D>(v[w]);
+  }
+}
+
+// ---- fold of p loaded operands in the reference order -------------------------
+// u[k] was loaded from seq[k]. LEFT: ((u0 op u1) op u2) ... (ring & flat).
+// TREE (collectives.py:178-229): leaves L_v = u[v] op u[M+v] for v < excess,
+// else u[v]; then a balanced tree, lower subtree first.
+template <int OP, int MP, int W, int M, typename A>
+__device__ __forceinline__ void tree_fold(A (&u)[MP][W], int excess) {
+#pragma unroll
+  for (int v = 0; v < M; ++v) {
+    constexpr int dummy = 0;
+    (void)dummy;
+    const int hi = (M + v < MP) ? M + v : MP - 1;
+    if (v < excess) {
+#pragma unroll
+      for (int w = 0; w < W; ++w) u[v][w] = op2<OP>(u[v][w], u[hi][w]);
+    }
+  }
+#pragma unroll
+  for (int s = 1; s < M; s *= 2) {
+#pragma unroll
+    for (int v = 0; v + s < M; v += 2 * s) {
+#pragma unroll
+      for (int w = 0; w < W; ++w) u[v][w] = op2<OP>(u[v][w], u[v + s][w]);
+    }
+  }
+}
+
+template <int OP, int MP, int W, bool TREE, typename A>
+__device__ __forceinline__ void fold(A (&u)[MP][W], int p, int m, int excess) {
+  if constexpr (!TREE) {
+#pragma unroll
+    for (int k = 1; k < MP; ++k)
+      if (k < p) {
+#pragma unroll
+        for (int w = 0; w < W; ++w) u[0][w] = op2<OP>(u[0][w], u[k][w]);
+      }
+  } else {
+    switch (m) {
+      case 1: tree_fold<OP, MP, W, 1>(u, excess); break;
+      case 2: tree_fold<OP, MP, W, 2>(u, excess); break;
+      case 4: tree_fold<OP, MP, W, (4 <= MP ? 4 : 1)>(u, excess); break;
+      case 8: tree_fold<OP, MP, W, (8 <= MP ? 8 : 1)>(u, excess); break;
+      default: tree_fold<OP, MP, W, (16 <= MP ? 16 : 1)>(u, excess); break;
+    }
+  }
+}
+
+// reduce U groups of W elements starting at element indices i0 + g*stride
+template <class D, int OP, int MP, int W, bool TREE>
+__device__ __forceinline__ void reduce_one(const char* const* seq, int p, int m, int excess,
+                                           long long i, int average, char* out,
+                                           long long out_shift, char* red, long long red_shift) {
+  using A = typename D::A;
+  A u[MP][W];
+#pragma unroll
+  for (int k = 0; k < MP; ++k)
+    if (k < p) load_vec<D, W>(seq[k], i, u[k]);
+  fold<OP, MP, W, TREE>(u, p, m, excess);
+  if (average) {
+#pragma unroll
+    for (int w = 0; w < W; ++w) u[0][w] = div_p<A>(u[0][w], p);
+  }
+  store_vec<D, W>(out, i - out_shift, u[0]);
+  if (red) store_vec<D, W>(red, i - red_shift, u[0]);
+}
+
+// Process [lo, hi) of one segment: scalar head/tail, W-wide body with 2-way
+// unrolling for memory-level parallelism over NVLink.
+template <class D, int OP, int MP, bool TREE>
+__device__ void reduce_range(const char* const* seq, int p, int m, int excess, long long lo,
+                             long long hi, bool vec, int average, char* out, long long out_shift,
+                             char* red, long long red_shift) {
+  using S = typename D::S;
+  constexpr int W = 16 / sizeof(S);
+  const int tid = threadIdx.x;
+  long long body_lo = lo, body_hi = lo;
+  if (vec) {
+    body_lo = ((lo + W - 1) / W) * W;
+    body_hi = (hi / W) * W;
+    if (body_hi < body_lo) body_hi = body_lo = hi;
+  }
+  // scalar head and tail
+  for (long long i = lo + tid; i < body_lo; i += blockDim.x)
+    reduce_one<D, OP, MP, 1, TREE>(seq, p, m, excess, i, average, out, out_shift, red, red_shift);
+  for (long long i = body_hi + tid; i < hi; i += blockDim.x)
+    reduce_one<D, OP, MP, 1, TREE>(seq, p, m, excess, i, average, out, out_shift, red, red_shift);
+  // vector body: vectors j in [body_lo/W, body_hi/W)
+  const long long v0 = body_lo / W, v1 = body_hi / W;
+  constexpr int U = (MP <= 8) ? 2 : 1;
+  long long j = v0 + tid;
+  for (; j + (U - 1) * (long long)blockDim.x < v1; j += U * (long long)blockDim.x) {
+    using A = typename D::A;
+    A u[U][MP][W];
+#pragma unroll
+    for (int g = 0; g < U; ++g)
+#pragma unroll
+      for (int k = 0; k < MP; ++k)
+        if (k < p) load_vec<D, W>(seq[k], (j + g * (long long)blockDim.x) * W, u[g][k]);
+#pragma unroll
+    for (int g = 0; g < U; ++g) {
+      fold<OP, MP, W, TREE>(u[g], p, m, excess);
+      if (average) {
+#pragma unroll
+        for (int w = 0; w < W; ++w) u[g][0][w] = div_p<A>(u[g][0][w], p);
+      }
+      const long long i = (j + g * (long long)blockDim.x) * W;
+      store_vec<D, W>(out, i - out_shift, u[g][0]);
+      if (red) store_vec<D, W>(red, i - red_shift, u[g][0]);
+    }
+  }
+  for (; j < v1; j += blockDim.x)
+    reduce_one<D, OP, MP, W, TREE>(seq, p, m, excess, j * W, average, out, out_shift, red,
+                                   red_shift);
+}
+
+// byte-level copy of elements [lo, hi): dst[i - dshift] = src[i - sshift]
+template <class D>
+__device__ void copy_range(const char* src, long long sshift, char* dst, long long dshift,
+                           long long lo, long long hi, bool vec) {
+  using S = typename D::S;
+  constexpr int W = 16 / sizeof(S);
+  const int tid = threadIdx.x;
+  const S* s = reinterpret_cast<const S*>(src);
+  S* d = reinterpret_cast<S*>(dst);
+  long long body_lo = lo, body_hi = lo;
+  if (vec) {
+    body_lo = ((lo + W - 1) / W) * W;
+    body_hi = (hi / W) * W;
+    if (body_hi < body_lo) body_hi = body_lo = hi;
+  }
+  for (long long i = lo + tid; i < body_lo; i += blockDim.x) d[i - dshift] = s[i - sshift];
+  for (long long i = body_hi + tid; i < hi; i += blockDim.x) d[i - dshift] = s[i - sshift];
+  const long long v0 = body_lo / W, v1 = body_hi / W;
+  constexpr int U = 4;
+  long long j = v0 + tid;
+  for (; j + (U - 1) * (long long)blockDim.x < v1; j += U * (long long)blockDim.x) {
+    uint4 r[U];
+#pragma unroll
+    for (int g = 0; g < U; ++g)
+      r[g] = *reinterpret_cast<const uint4*>(s + (j + g * (long long)blockDim.x) * W - sshift);
+#pragma unroll
+    for (int g = 0; g < U; ++g)
+      *reinterpret_cast<uint4*>(d + (j + g * (long long)blockDim.x) * W - dshift) = r[g];
+  }
+  for (; j < v1; j += blockDim.x)
+    *reinterpret_cast<uint4*>(d + j * W - dshift) = *reinterpret_cast<const uint4*>(s + j * W - sshift);
+}
+
+__device__ __forceinline__ bool al16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+__device__ __forceinline__ bool al16s(const char* base, long long shift_elems, int sz) {
+  return (((uintptr_t)base - (uintptr_t)(shift_elems * sz)) & 15u) == 0;
+}
+
+// ---- the collective kernel -------------------------------------------------------
+template <class D, int OP, int MP, bool TREE>
+__global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_constant__ CollParams P) {
+  using S = typename D::S;
+  constexpr int SZ = sizeof(S);
+  const int lr = P.virt ? blockIdx.y : 0;       // index into in/out
+  const int rank = P.virt ? (int)blockIdx.y : P.rank;
+  const int b = blockIdx.x, nb = gridDim.x, p = P.p, tid = threadIdx.x;
+  char* myheap = P.heap[rank];
+  Ctrl* ctrl = reinterpret_cast<Ctrl*>(myheap + CTRL_OFF);
+
+  __shared__ unsigned long long s_epoch;
+  __shared__ const char* s_src[MAXP];   // element 0 of rank q's input
+  __shared__ char* s_red[MAXP];         // element seg_off[q] of q's segment
+  __shared__ const char* s_seq[MAXP];   // fold sequence
+  __shared__ int s_err;
+
+  if (tid == 0) {
+    s_epoch = ctrl->epoch + 1;
+    s_err = 0;
+  }
+  __syncthreads();
+  const unsigned long long e = s_epoch;
+  const int par = (int)(e & 1);
+  const long long stage_off = (long long)STAGING_OFF + (long long)par * P.staging_bytes;
+  const char* in = P.in[lr];
+  char* out = P.out[lr];
+  const bool ag_only = !(P.phases & PH_RS);
+  const bool two_shot = !P.oneshot;
+
+  // my own src/red offsets (published to peers)
+  long long my_srcoff, my_redoff;
+  const long long mso = P.seg_off[rank];
+  if (P.srcmode == SRC_ZEROCOPY) {
+    my_srcoff = P.zc_srcoff[lr];
+    if (!ag_only)            // reduced segment goes to staging, vector-aligned like the source
+      my_redoff = stage_off + (mso % SLICE_ALIGN) * SZ;
+    else if (P.ag_in_rel)    // allgather: `in` holds only my segment
+      my_redoff = my_srcoff;
+    else
+      my_redoff = my_srcoff + mso * SZ;
+  } else {
+    my_srcoff = stage_off;
+    my_redoff = stage_off + mso * SZ;
+  }
+
+  // 1. copy-in: this CTA's slice of every segment peers will read from me
+  if (P.srcmode == SRC_COPYIN) {
+    char* stage = myheap + stage_off;
+    if (ag_only) {
+      const long long lo = slice_bound(mso, P.seg_len[rank], b, nb);
+      const long long hi = slice_bound(mso, P.seg_len[rank], b + 1, nb);
+      const long long ish = P.ag_in_rel ? mso : 0;
+      const bool v = al16s(in, ish, SZ);
+      copy_range<D>(in, ish, stage, 0, lo, hi, v);
+      copy_range<D>(in, ish, out, 0, lo, hi, v && al16(out));
+    } else {
+      const bool v = al16(in);
+      const int nseg = P.oneshot ? 1 : p;
+      for (int q = 0; q < nseg; ++q) {
+        const long long so = P.oneshot ? 0 : P.seg_off[q];
+        const long long sl = P.oneshot ? P.n : P.seg_len[q];
+        copy_range<D>(in, 0, stage, 0, slice_bound(so, sl, b, nb), slice_bound(so, sl, b + 1, nb), v);
+      }
+    }
+  }
+  __syncthreads();
+
+  // 2. publish my record to every peer, then collect theirs
+  if (tid < p) {
+    Rec* r = rec_slot(P.heap[tid], par, b, rank);
+    st_relaxed_sys(&r->hdr, P.hdr);
+    st_relaxed_sys_s64(&r->srcoff, my_srcoff);
+    st_relaxed_sys_s64(&r->redoff, my_redoff);
+    st_release_sys(&r->epoch, e);
+  }
+  if (tid < p) {
+    Rec* r = rec_slot(myheap, par, b, tid);
+    if (!wait_geq(&r->epoch, e, P.timeout_cycles)) {
+      atomicExch(&s_err, ERR_TRANSPORT);
+    } else {
+      if (ld_relaxed_sys(&r->hdr) != P.hdr) atomicExch(&s_err, ERR_SHAPE);
+      s_src[tid] = P.heap[tid] + ld_relaxed_sys_s64(&r->srcoff);
+      s_red[tid] = P.heap[tid] + ld_relaxed_sys_s64(&r->redoff);
+    }
+  }
+  __syncthreads();
+  if (s_err) goto finish;
+
+  // 3. reduce my segment (RS) — or the whole vector (one-shot)
+  if (P.phases & PH_RS) {
+    const long long so = P.oneshot ? 0 : mso;
+    const long long sl = P.oneshot ? P.n : P.seg_len[rank];
+    int m = 1;
+    while ((m << 1) <= p) m <<= 1;
+    const int excess = p - m;
+    if (tid == 0) {
+      if (P.order == ORD_RING) {          // chunk c folds x_{c-1}, x_{c-2}, ..., x_c
+        for (int k = 0; k < p; ++k) s_seq[k] = s_src[((rank - 1 - k) % p + p) % p];
+      } else if (P.order == ORD_TREE) {   // leaves real(v), partners 2v+1 at M+v
+        for (int v = 0; v < m; ++v) s_seq[v] = s_src[v < excess ? 2 * v : v + excess];
+        for (int v = 0; v < excess; ++v) s_seq[m + v] = s_src[2 * v + 1];
+      } else {
+        for (int k = 0; k < p; ++k) s_seq[k] = s_src[k];
+      }
+    }
+    __syncthreads();
+    bool vec = true;
+    for (int q = 0; q < p; ++q) vec = vec && al16(s_src[q]);
+    const long long out_shift = P.out_rel ? so : 0;
+    vec = vec && al16s(out, out_shift, SZ);
+    char* red = nullptr;
+    long long red_shift = 0;
+    if (two_shot && (P.phases & PH_AG)) {
+      red = s_red[rank];
+      red_shift = so;
+      vec = vec && al16s(red, red_shift, SZ);
+    }
+    const long long lo = slice_bound(so, sl, b, nb), hi = slice_bound(so, sl, b + 1, nb);
+    reduce_range<D, OP, MP, TREE>(s_seq, p, m, excess, lo, hi, vec, P.average, out, out_shift,
+                                  red, red_shift);
+  }
+
+  // 4. RS -> AG barrier (per CTA index) and 5. allgather
+  if (P.phases & PH_AG) {
+    if (!ag_only) {
+      __syncthreads();
+      if (tid < p) st_release_sys(mid_slot(P.heap[tid], b, rank), e);
+      if (tid < p && !wait_geq(mid_slot(myheap, b, tid), e, P.timeout_cycles))
+        atomicExch(&s_err, ERR_TRANSPORT);
+      __syncthreads();
+      if (s_err) goto finish;
+    }
+    for (int q = 0; q < p; ++q) {
+      if (q == rank && !(ag_only && P.srcmode == SRC_ZEROCOPY)) continue;
+      const long long so = P.seg_off[q], sl = P.seg_len[q];
+      const long long lo = slice_bound(so, sl, b, nb), hi = slice_bound(so, sl, b + 1, nb);
+      if (hi <= lo) continue;
+      const char* src = s_red[q];
+      copy_range<D>(src, so, out, 0, lo, hi, al16s(src, so, SZ) && al16(out));
+    }
+  }
+
+finish:
+  __syncthreads();
+  if (tid == 0) {
+    if (s_err) *reinterpret_cast<volatile unsigned*>(P.herr) = (unsigned)s_err;
+    __threadfence();
+    const unsigned old = atomicAdd(&ctrl->done, 1u);
+    if (old == (unsigned)nb - 1) {
+      ctrl->done = 0;
+      ctrl->epoch = e;
+      __threadfence();
+    }
+  }
+}
+
+// ---- batched copy (fusion pack / unfuse / cm_batched_copy) ---------------------
+constexpr int MAXCOPY = 128;
+struct CopyParams {
+  const char* src[MAXCOPY];
+  char* dst[MAXCOPY];          // absolute, or byte offset into staging[next parity] if staged
+  long long start[MAXCOPY + 1];  // prefix sums of bytes
+  int n;
+  int staged;                  // dst is relative to own staging[(epoch+1)&1]
+  char* heap;
+  long long staging_bytes;
+};
+
+__global__ void __launch_bounds__(THREADS) batched_copy_kernel(const __grid_constant__ CopyParams P) {
+  const long long total = P.start[P.n];
+  const int b = blockIdx.x, nb = gridDim.x, tid = threadIdx.x;
+  long long lo = (long long)(((__int128)total * b) / nb) & ~15ll;
+  long long hi = b == nb - 1 ? total : ((long long)(((__int128)total * (b + 1)) / nb) & ~15ll);
+  if (b == 0) lo = 0;
+  char* base = nullptr;
+  if (P.staged) {
+    const Ctrl* ctrl = reinterpret_cast<const Ctrl*>(P.heap + CTRL_OFF);
+    const unsigned long long e = ctrl->epoch + 1;
+    base = P.heap + STAGING_OFF + (long long)(e & 1) * P.staging_bytes;
+  }
+  // find the first member overlapping [lo, hi)
+  int k = 0;
+  while (k < P.n && P.start[k + 1] <= lo) ++k;
+  for (; k < P.n && P.start[k] < hi; ++k) {
+    const long long a = lo > P.start[k] ? lo : P.start[k];
+    const long long z = hi < P.start[k + 1] ? hi : P.start[k + 1];
+    const char* s = P.src[k] + (a - P.start[k]);
+    char* d = (P.staged ? base + (long long)(uintptr_t)P.dst[k] : P.dst[k]) + (a - P.start[k]);
+    const long long nbytes = z - a;
+    if ((((uintptr_t)s | (uintptr_t)d) & 15u) == 0) {
+      const long long nv = nbytes >> 4;
+      const uint4* s4 = reinterpret_cast<const uint4*>(s);
+      uint4* d4 = reinterpret_cast<uint4*>(d);
+      long long j = tid;
+      for (; j + 3 * THREADS < nv; j += 4 * THREADS) {
+        uint4 r0 = s4[j], r1 = s4[j + THREADS], r2 = s4[j + 2 * THREADS], r3 = s4[j + 3 * THREADS];
+        d4[j] = r0; d4[j + THREADS] = r1; d4[j + 2 * THREADS] = r2; d4[j + 3 * THREADS] = r3;
+      }
+      for (; j < nv; j += THREADS) d4[j] = s4[j];
+      for (long long t = (nv << 4) + tid; t < nbytes; t += THREADS) d[t] = s[t];
+    } else if ((((uintptr_t)s | (uintptr_t)d) & 3u) == 0) {
+      const long long nw = nbytes >> 2;
+      const uint32_t* s1 = reinterpret_cast<const uint32_t*>(s);
+      uint32_t* d1 = reinterpret_cast<uint32_t*>(d);
+      for (long long j = tid; j < nw; j += THREADS) d1[j] = s1[j];
+      for (long long t = (nw << 2) + tid; t < nbytes; t += THREADS) d[t] = s[t];
+    } else {
+      for (long long t = tid; t < nbytes; t += THREADS) d[t] = s[t];
+    }
+  }
+}
+
+// ---- local_reduce (core.py:94-110) -------------------------------------------------
+template <class D, int OP>
+__global__ void __launch_bounds__(THREADS) local_reduce_kernel(const char* a, const char* b, char* out,
+                                                              long long n, int vec) {
+  using S = typename D::S;
+  using A = typename D::A;
+  constexpr int W = 16 / sizeof(S);
+  const long long nvec = vec ? n / W : 0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < nvec; j += stride) {
+    A u[2][W];
+    load_vec<D, W>(a, j * W, u[0]);
+    load_vec<D, W>(b, j * W, u[1]);
+#pragma unroll
+    for (int w = 0; w < W; ++w) u[0][w] = op2<OP>(u[0][w], u[1][w]);
+    store_vec<D, W>(out, j * W, u[0]);
+  }
+  for (long long i = nvec * W + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride) {
+    A u[2][1];
+    load_vec<D, 1>(a, i, u[0]);
+    load_vec<D, 1>(b, i, u[1]);
+    u[0][0] = op2<OP>(u[0][0], u[1][0]);
+    store_vec<D, 1>(out, i, u[0]);
+  }
+}
+
+}  // namespace dev
+}  // namespace cm

@@ -1,0 +1,173 @@
+"""Per-rank parity program for the multi-GPU tier (one process per GPU).
+
+Launched by tests/test_gpu_multi.py as
+    torchrun --nproc-per-node N tests/mp_worker.py
+Each rank checks its results against the golden fixtures / CPU oracle and
+exits non-zero on the first mismatch (the message names rank and case).
+"""
+
+import hashlib
+import os
+import sys
+import traceback
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import paper_1810_11112_b200 as P  # noqa: E402
+from oracle import collectives as OC  # noqa: E402
+from tests.golden import inputs as I  # noqa: E402
+from tests.golden.load import of_kind  # noqa: E402
+
+OPS = {"sum": P.ReduceOp.SUM, "max": P.ReduceOp.MAX}
+
+
+def sha(b):
+    return hashlib.sha256(b).hexdigest()
+
+
+def main():
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo")
+    comm = P.Communicator(staging_bytes=256 << 20, pool_bytes=512 << 20, timeout_s=20.0)
+    group = P.GroupSpec(world)
+    checks = 0
+
+    def expect(cond, what):
+        nonlocal checks
+        checks += 1
+        if not cond:
+            raise AssertionError(f"rank {rank}: {what}")
+
+    # 1. golden allreduce cases for this group size (sum + max, f32/f64, all algos)
+    for case in of_kind("allreduce"):
+        if case["p"] != world:
+            continue
+        arrays = I.allreduce_inputs(world, case["n"], case["dtype"], case["op"])
+        t = P.Tensor("x", case["dtype"], torch.from_numpy(arrays[rank]).cuda())
+        out, st = P.allreduce(t, OPS[case["op"]], group, comm, algo=case["algo"])
+        expect(sha(out.to_bytes()) == case["sha"], f"golden {case['dtype']} {case['algo']} {case['op']} n={case['n']}")
+        expect([st.rounds, st.messages_per_rank, st.bytes_sent_per_rank] == case["stats"][rank],
+               f"stats {case['algo']} n={case['n']}")
+    if world == 4:
+        xs = I.c1_inputs()
+        for case in of_kind("c1"):
+            out, _ = P.allreduce(P.Tensor("x", "float32", torch.from_numpy(xs[rank]).cuda()),
+                                 P.ReduceOp.SUM, group, comm, algo=case["algo"])
+            expect(sha(out.to_bytes()) == case["sha"], f"C1 {case['algo']}")
+
+    # 2. large messages: copy-in, zero-copy (symmetric pool), in-place, host buffers
+    for n in (262145, 1 << 22, 5_000_011):
+        rng = np.random.default_rng([21, n])
+        xs = [(rng.standard_normal(n) * 10.0 ** rng.integers(-3, 4, size=n)).astype(np.float32)
+              for _ in range(world)]
+        for algo in ("ring_rsa", "rhd_rsa", "flat"):
+            want = OC.allreduce(xs, "sum", algo, "float32").tobytes()
+            x = torch.from_numpy(xs[rank]).cuda()
+            out, _ = P.allreduce(P.Tensor("x", "float32", x), P.ReduceOp.SUM, group, comm, algo=algo)
+            expect(out.to_bytes() == want, f"copy-in {algo} n={n}")
+            sym = comm.empty(n, "float32")
+            sym.copy_(x)
+            out, _ = P.allreduce(P.Tensor("x", "float32", sym), P.ReduceOp.SUM, group, comm, algo=algo)
+            expect(out.to_bytes() == want, f"zero-copy {algo} n={n}")
+            P.allreduce(P.Tensor("x", "float32", sym), P.ReduceOp.SUM, group, comm, algo=algo, out=sym)
+            expect(sym.cpu().numpy().tobytes() == want, f"zero-copy in-place {algo} n={n}")
+            comm.free(sym)
+            host = P.Tensor("x", "float32", xs[rank])           # numpy -> host tensor
+            out, _ = P.allreduce(host, P.ReduceOp.SUM, group, comm, algo=algo)
+            expect(not out.is_cuda and out.to_bytes() == want, f"host buffer {algo} n={n}")
+
+    # 3. reduce-scatter / allgather
+    for layout in ("ring", "rhd"):
+        for n in (0, 3, 1000, 1 << 20):
+            xs = I.allreduce_inputs(world, n, "float32", "sum") if n < 5000 else \
+                [np.random.default_rng([5, r]).standard_normal(n).astype(np.float32) for r in range(world)]
+            want = OC.reduce_scatter(xs, "sum", layout, "float32")
+            seg, _ = P.reduce_scatter(P.Tensor("x", "float32", torch.from_numpy(xs[rank]).cuda()),
+                                      P.ReduceOp.SUM, group, comm, layout=layout)
+            expect(seg.to_bytes() == want[rank].tobytes(), f"reduce_scatter {layout} n={n}")
+            full, _ = P.allgather(seg, n, group, comm, layout=layout)
+            expect(full.to_bytes() == OC.allgather(want, n, layout, "float32").tobytes(),
+                   f"allgather {layout} n={n}")
+
+    # 4. fused aggregate through cm_fused_allreduce (staged pack + fused mean)
+    for case in of_kind("aggregate"):
+        if case["p"] != world:
+            continue
+        schema = I.agg_schema(world)
+        mine = I.agg_inputs(schema, world, case["dtype"])[rank]
+        gs = P.GradientSet(tuple(P.Tensor(nm, case["dtype"], torch.from_numpy(a).cuda()) for nm, a in mine))
+        stats = []
+        res = P.aggregate(gs, group, comm, algo=case["algo"],
+                          cfg=P.FusionConfig(case["threshold"]), stats_out=stats)
+        expect(res.names == case["names"], "aggregate names")
+        expect([sha(t.to_bytes()) for t in res.tensors] == case["sha"],
+               f"aggregate {case['dtype']} {case['algo']} thr={case['threshold']}")
+        expect([[s.rounds, s.messages_per_rank, s.bytes_sent_per_rank] for s in stats]
+               == case["stats"][rank], "aggregate stats")
+    for case in of_kind("model"):
+        if case["p"] != world:
+            continue
+        layers = I.MODELS[case["model"]]
+        for host in (False, True):
+            grads = I.synth_gradients(0, 0, layers, rank)
+            gs = P.GradientSet(tuple(P.Tensor(nm, "float32", a if host else torch.from_numpy(a).cuda())
+                                     for nm, a in grads))
+            res = P.aggregate(gs, group, comm)
+            h = hashlib.sha256()
+            for t in res.tensors:
+                h.update(t.to_bytes())
+            expect(h.hexdigest() == case["sha"], f"model {case['model']} host={host}")
+
+    # 5. negotiation: partial intersection falls back to the control plane
+    ready = ["a", "b", "c"] if rank == 0 else ["b", "c", "d"]
+    expect(P.negotiate_ready(ready, group, comm) == ["b", "c"], "negotiate partial")
+    expect(P.negotiate_ready(["z", "y"], group, comm) == ["y", "z"], "negotiate full")
+
+    # 6. peer shape mismatch is detected on the device -> ShapeError everywhere
+    bad = torch.zeros(3 + rank, device="cuda")
+    try:
+        P.allreduce(P.Tensor("x", "float32", bad), P.ReduceOp.SUM, group, comm)
+        expect(False, "mismatched lengths did not raise")
+    except P.ShapeError:
+        checks += 1
+    # the communicator stays usable afterwards
+    x = torch.full((10,), float(rank), device="cuda")
+    out, _ = P.allreduce(P.Tensor("x", "float32", x), P.ReduceOp.SUM, group, comm)
+    expect(out.payload.cpu().tolist() == [float(sum(range(world)))] * 10, "usable after ShapeError")
+
+    # 7. back-to-back stress with changing sizes (epoch/parity reuse), async
+    comm.blocking = False
+    rng = np.random.default_rng(77)
+    sizes = [int(s) for s in rng.integers(0, 300000, size=200)]
+    outs = []
+    for i, n in enumerate(sizes):
+        x = torch.full((n,), float(rank + i), device="cuda")
+        algo = ("ring_rsa", "rhd_rsa", "auto", "flat")[i % 4]
+        out, _ = P.allreduce(P.Tensor("x", "float32", x), P.ReduceOp.SUM, group, comm, algo=algo)
+        outs.append((n, i, out.payload))
+    comm.synchronize()
+    for n, i, o in outs:
+        want = float(sum(r + i for r in range(world)))
+        expect(n == 0 or bool(torch.all(o == want)), f"stress call {i} n={n}")
+    comm.blocking = True
+
+    dist.barrier()
+    comm.close()
+    print(f"rank {rank}: {checks} checks passed", flush=True)
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    try:
+        main()
+    except Exception:
+        traceback.print_exc()
+        sys.stdout.flush()
+        os._exit(1)
