@@ -170,6 +170,13 @@ int cm_comm_counters(cm_comm_t* comm, int64_t* messages_sent, int64_t* bytes_sen
                      int64_t* nvlink_bytes_in, int64_t* calls);
 /* number of kernels this comm has launched (bench "gpu_launches") */
 int cm_comm_launches(cm_comm_t* comm, int64_t* launches);
+/* bracket every kernel this comm launches with CUDA events on its stream */
+int cm_comm_profile(cm_comm_t* comm, int enable);
+/* drain recorded launches of one kind (0 = collective kernel, 1 = pack/copy
+ * kernel): count, summed device ms, summed algorithmic bytes (collective:
+ * busBW bytes 2(p-1)/p*S; pack: bytes read + written) */
+int cm_comm_profile_read(cm_comm_t* comm, int kind, int64_t* launches, double* total_ms,
+                         int64_t* alg_bytes);
 
 /* allreduce collectives.py:250-260 (+ allreduce_ring :107, allreduce_rhd :155,
  * allreduce_flat :75 via `algo`). Results are bit-identical to the reference

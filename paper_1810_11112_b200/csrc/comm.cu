@@ -44,6 +44,15 @@ struct cm_comm {
   int max_ctas = 148;
   // counters
   int64_t messages = 0, bytes = 0, nvlink_in = 0, calls = 0, launches = 0;
+  // optional per-launch CUDA-event profiling (bench roofline)
+  struct Prof {
+    int kind;
+    cudaEvent_t e0, e1;
+    int64_t alg_bytes;
+  };
+  bool profiling = false;
+  std::vector<Prof> prof;
+  std::vector<cudaEvent_t> event_pool;
 };
 
 namespace {
@@ -60,6 +69,39 @@ int cuda_fail(cudaError_t e, const char* what) {
   } while (0)
 
 size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+cudaEvent_t take_event(cm_comm* c) {
+  if (!c->event_pool.empty()) {
+    cudaEvent_t e = c->event_pool.back();
+    c->event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// bracket one launch with events when profiling (kind 0 collective, 1 pack)
+struct ProfScope {
+  cm_comm* c;
+  cudaStream_t s;
+  int kind;
+  int64_t bytes;
+  cudaEvent_t e0 = nullptr;
+  ProfScope(cm_comm* c_, cudaStream_t s_, int k, int64_t b) : c(c_), s(s_), kind(k), bytes(b) {
+    if (c && c->profiling) {
+      e0 = take_event(c);
+      cudaEventRecord(e0, s);
+    }
+  }
+  ~ProfScope() {
+    if (e0) {
+      cudaEvent_t e1 = take_event(c);
+      cudaEventRecord(e1, s);
+      c->prof.push_back({kind, e0, e1, bytes});
+    }
+  }
+};
 
 using KFn = void (*)(CollParams);
 
@@ -202,6 +244,10 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
   KFn k = pick_kernel(L.dtype, L.op, p, L.order == ORD_TREE);
   if (!k) return fail(CM_ERR_SHAPE, "unsupported dtype");
   void* args[] = {&P};
+  int64_t alg = 0;   // busBW bytes of this launch (nccl-tests convention)
+  if (L.phases == (PH_RS | PH_AG) || L.oneshot) alg = 2 * (int64_t)(p - 1) * L.n * (int64_t)sz / p;
+  else alg = (int64_t)(p - 1) * L.n * (int64_t)sz / p;
+  ProfScope prof_scope(c, stream, 0, alg);
   if (c->virt) {
     int per_sm = 0;
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k, THREADS, 0));
@@ -448,6 +494,7 @@ int launch_batched_copy(cm_comm* c, int n, const void* const* srcs, void* const*
     int64_t nb = (P.start[m] + (128 << 10) - 1) / (128 << 10);
     nb = std::max<int64_t>(1, std::min<int64_t>(nb, 148 * 4));
     void* args[] = {&P};
+    ProfScope prof_scope(c, stream, 1, 2 * P.start[m]);
     CUDA_TRY(cudaLaunchKernel((const void*)batched_copy_kernel, dim3((unsigned)nb), dim3(THREADS),
                               args, 0, stream));
     if (c) c->launches += 1;
@@ -555,6 +602,8 @@ int cm_comm_destroy(cm_comm_t* c) {
   if (c->local) cudaFree(c->local);
   if (c->scratch) cudaFree(c->scratch);
   if (c->herr_host) cudaFreeHost(c->herr_host);
+  for (auto& pr : c->prof) { cudaEventDestroy(pr.e0); cudaEventDestroy(pr.e1); }
+  for (auto e : c->event_pool) cudaEventDestroy(e);
   cudaGetLastError();
   delete c;
   return CM_OK;
@@ -660,6 +709,34 @@ int cm_comm_counters(cm_comm_t* c, int64_t* messages_sent, int64_t* bytes_sent,
 
 int cm_comm_launches(cm_comm_t* c, int64_t* launches) {
   *launches = c->launches;
+  return CM_OK;
+}
+
+int cm_comm_profile(cm_comm_t* c, int enable) {
+  c->profiling = enable != 0;
+  return CM_OK;
+}
+
+int cm_comm_profile_read(cm_comm_t* c, int kind, int64_t* launches, double* total_ms,
+                         int64_t* alg_bytes) {
+  int64_t n = 0, b = 0;
+  double ms = 0;
+  std::vector<cm_comm::Prof> keep;
+  for (auto& pr : c->prof) {
+    if (pr.kind != kind) { keep.push_back(pr); continue; }
+    CUDA_TRY(cudaEventSynchronize(pr.e1));
+    float t = 0;
+    cudaEventElapsedTime(&t, pr.e0, pr.e1);
+    ms += t;
+    b += pr.alg_bytes;
+    ++n;
+    c->event_pool.push_back(pr.e0);
+    c->event_pool.push_back(pr.e1);
+  }
+  c->prof.swap(keep);
+  *launches = n;
+  *total_ms = ms;
+  *alg_bytes = b;
   return CM_OK;
 }
 

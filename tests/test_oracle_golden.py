@@ -158,3 +158,31 @@ def test_fuse_plan_reference_examples():
     assert OA.fuse_plan(mem[:3], 1) == [[0], [1], [2]]
     mixed = [("a", "float32", 8), ("b", "float64", 16)]
     assert OA.fuse_plan(mixed, 2**20) == [[0], [1]]
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 8])
+def test_threaded_port_matches_closed_forms(p):
+    """oracle/threaded.py (the CPU baseline / --impl reference path) is the
+    reference's message-passing schedule; it must equal the closed forms."""
+    from oracle import threaded as T
+    for n in (0, 1, 7, 64, 1001):
+        for dtype in ("float32", "float64"):
+            xs = I.allreduce_inputs(p, n, dtype, "sum")
+            for algo in ("flat", "ring_rsa", "rhd_rsa"):
+                outs = T.ThreadNet(p).run(lambda r, tp: T.allreduce_rank(xs[r], "sum", algo, tp))
+                want = OC.allreduce(xs, "sum", algo, dtype)
+                for o in outs:
+                    assert o.tobytes() == want.tobytes()
+
+
+def test_threaded_aggregate_matches_reference_model_golden():
+    from oracle import threaded as T
+    case = [c for c in of_kind("model") if c["model"] == "mobilenet_like"][0]
+    p = case["p"]
+    layers = I.MODELS[case["model"]]
+    grads = [I.synth_gradients(0, 0, layers, r) for r in range(p)]
+    outs = T.ThreadNet(p).run(lambda r, tp: T.aggregate_rank(grads[r], tp))
+    h = hashlib.sha256()
+    for nm in sorted(outs[0]):
+        h.update(outs[0][nm].tobytes())
+    assert h.hexdigest() == case["sha"]
