@@ -1,0 +1,590 @@
+#!/usr/bin/env python
+"""Benchmark of the CUDA-aware allreduce hot path on B200.
+
+Headline (default): BASELINE config 5 — the ResNet-50 gradient set
+(resnet50_like: 53 x 480,000 fp32 = 25.44 M params, 101.76 MB per rank) run
+through ``aggregate()`` every step: negotiation, tensor fusion under the
+64 MB threshold (2 fused buffers), the NVLink allreduce with the fused mean.
+One JSON line on rank 0.
+
+    python bench.py [--gpus N --steps K --warmup W]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+    python bench.py --impl reference ...   # the reference CPU path (threaded port)
+    torchrun ... bench.py --mode sweep      # C2/C3 latency + busBW sweep vs NCCL (CSV)
+    torchrun ... bench.py --mode tune       # measure the rhd/ring switch -> tuning.json
+
+value   = N x 101.76 MB / device step time (GB/s of gradients aggregated,
+          whole job); inputs resident in HBM, L2 flushed between steps.
+e2e     = same metric through the public API with pinned HOST gradients
+          (H2D + D2H inside the timed region).
+roofline: N>=2 the collective kernel (busBW vs the measured 770 GB/s NVLink
+          peer-copy rate); N=1 the fused pack kernel (HBM vs MEASURED_PEAKS).
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "allreduce latency (us) and bus GB/s vs message size at 1/2/4/8 B200"
+MODELS = {"resnet50_like": [480_000] * 53, "mobilenet_like": [150_000] * 28}
+NVLINK_PEAK_GBS = 770.0      # B200_PROFILING.md: measured NVLink peer copy per direction
+NVLINK_NOMINAL_GBS = 900.0
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# --------------------------------------------------------------------------- env
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+def init_dist(rank, world, local, nccl=True):
+    if world == 1:
+        return
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    backend = "cpu:gloo,cuda:nccl" if nccl else "gloo"
+    kw = {"device_id": torch.device("cuda", local)} if nccl else {}
+    dist.init_process_group(backend, rank=rank, world_size=world, **kw)
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    t = torch.tensor([x], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        dist.barrier()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+class ClockSampler(threading.Thread):
+    """Samples SM clock and throttle reasons (NVML) during the timed region."""
+
+    def __init__(self, device_index: int):
+        super().__init__(daemon=True)
+        self.idx = device_index
+        self.samples, self.reasons = [], set()
+        self.stop_flag = threading.Event()
+        self.max_mhz = None
+        self.ok = False
+
+    def run(self):
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.idx)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+            names = {
+                getattr(N, "nvmlClocksThrottleReasonHwSlowdown", 0x8): "hw_slowdown",
+                getattr(N, "nvmlClocksThrottleReasonHwThermalSlowdown", 0x40): "hw_thermal_slowdown",
+                getattr(N, "nvmlClocksThrottleReasonSwThermalSlowdown", 0x20): "sw_thermal_slowdown",
+                getattr(N, "nvmlClocksThrottleReasonSwPowerCap", 0x4): "sw_power_cap",
+                getattr(N, "nvmlClocksThrottleReasonHwPowerBrakeSlowdown", 0x80): "hw_power_brake",
+            }
+            self.ok = True
+            while not self.stop_flag.is_set():
+                self.samples.append(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM))
+                r = N.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                for bit, nm in names.items():
+                    if r & bit:
+                        self.reasons.add(nm)
+                time.sleep(0.002)
+        except Exception as exc:  # pragma: no cover
+            self.reasons.add(f"nvml_unavailable:{type(exc).__name__}")
+
+    def result(self):
+        self.stop_flag.set()
+        self.join(timeout=2)
+        med = statistics.median(self.samples) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "samples": len(self.samples),
+                "reasons": sorted(self.reasons)}
+
+
+# --------------------------------------------------------------------- workload
+def make_grads(model, rank, device, dtype="float32", pinned=False):
+    """Reference synth_gradients recipe (bench.py:224-232): default_rng([seed,
+    it, layer, rank]).standard_normal(n, float32); bf16 = RNE of those."""
+    import paper_1810_11112_b200 as P
+    from tests.golden.inputs import synth_gradients
+    ts = []
+    for nm, a in synth_gradients(0, 0, MODELS[model], rank):
+        t = torch.from_numpy(a)
+        if dtype == "bfloat16":
+            t = t.to(torch.bfloat16)
+        if device is not None:
+            t = t.to(device)
+        elif pinned:
+            t = t.pin_memory()
+        ts.append(P.Tensor(nm, dtype, t))
+    return P.GradientSet(tuple(ts))
+
+
+def oracle_check(model, world, rank, res, dtype):
+    """Rank 0: bit-exact comparison of this rank's aggregate with the CPU
+    oracle (reference fold order) on the same synthetic inputs."""
+    from oracle import aggregation as OA
+    from oracle import collectives as OC
+    from tests.golden.inputs import synth_gradients
+    per_rank = [synth_gradients(0, 0, MODELS[model], r) for r in range(world)]
+    if dtype == "bfloat16":
+        per_rank = [[(nm, OC.f32_to_bf16(a)) for nm, a in g] for g in per_rank]
+    want, _, _ = OA.aggregate(per_rank, dtype)
+    for t in res.tensors:
+        got = np.frombuffer(t.to_bytes(), dtype=OC.STORAGE[dtype])
+        if not np.array_equal(got.view(np.uint8), np.asarray(want[t.name]).view(np.uint8)):
+            return f"MISMATCH in {t.name}"
+    return "bit-exact vs oracle (reference fold order)"
+
+
+def cpu_baseline_sample(model, p, dtype="float32", max_s=20.0):
+    """The reference path (threaded message-passing port of collectives.py /
+    aggregation.py) on host cores, p ranks in-process."""
+    from oracle import threaded as T
+    from tests.golden.inputs import synth_gradients
+    grads = [synth_gradients(0, 0, MODELS[model], r) for r in range(p)]
+    times = []
+    t_end = time.perf_counter() + max_s
+    while True:
+        t0 = time.perf_counter()
+        T.ThreadNet(p).run(lambda r, tp: T.aggregate_rank(grads[r], tp))
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() > t_end or len(times) >= 3:
+            break
+    return times
+
+
+# ---------------------------------------------------------------------- headline
+def headline(args, rank, world, local):
+    import paper_1810_11112_b200 as P
+    from paper_1810_11112_b200 import _lib as L
+    device = torch.device("cuda", local)
+    torch.cuda.set_device(device)
+    layers = MODELS[args.model]
+    esz = 2 if args.dtype == "bfloat16" else 4
+    S = sum(layers) * esz
+    comm = P.Communicator(rank, world, local, staging_bytes=max(256 << 20, S + (8 << 20)),
+                          pool_bytes=64 << 20, blocking=False)
+    group = P.GroupSpec(world)
+    cfg = P.FusionConfig(args.fusion_threshold)
+    gs = make_grads(args.model, rank, device, args.dtype)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
+
+    state = {"out": None}
+
+    def step():   # persistent output buckets: aggregate(out=previous result)
+        state["out"] = P.aggregate(gs, group, comm, algo=args.algo, cfg=cfg,
+                                   switch_bytes=args.switch, out=state["out"])
+        return state["out"]
+
+    for _ in range(args.warmup):
+        res = step()
+    comm.synchronize()
+    parity = oracle_check(args.model, world, rank, res, args.dtype) if (rank == 0 and not args.no_check) else None
+    barrier(world)
+
+    nbuf = len(P.fuse_plan(list(gs.tensors), cfg))
+    L.check(L.lib.cm_comm_profile(comm._h, 1))
+    launches0 = comm.launches
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    sampler = ClockSampler(local)
+    sampler.start()
+    barrier(world)
+    torch.cuda.synchronize()
+    for i in range(args.steps):
+        flush.zero_()                       # L2 flush (256 MiB > 126 MB L2), untimed
+        evs[i][0].record()
+        step()
+        evs[i][1].record()
+    torch.cuda.synchronize()
+    barrier(world)
+    clocks = sampler.result()
+    comm.synchronize()
+    launches = comm.launches - launches0
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    ms_local = statistics.mean(step_ms)
+
+    def prof(kind):
+        n, ms, b = C.c_int64(), C.c_double(), C.c_int64()
+        L.check(L.lib.cm_comm_profile_read(comm._h, kind, C.byref(n), C.byref(ms), C.byref(b)))
+        return int(n.value), float(ms.value), int(b.value)
+    coll_n, coll_ms, coll_b = prof(0)
+    pack_n, pack_ms, pack_b = prof(1)
+    L.check(L.lib.cm_comm_profile(comm._h, 0))
+    ms = max_over_ranks(ms_local, world)
+
+    # NCCL comparator on the same fused buffers (N >= 2)
+    nccl = None
+    if world > 1 and not args.no_nccl:
+        sizes = []
+        for grp in P.fuse_plan(list(gs.tensors), cfg):
+            sizes.append(sum(layers[i] for i in grp))
+        bufs = [torch.randn(n, device=device).to(gs.tensors[0].payload.dtype) for n in sizes]
+        for _ in range(3):
+            for b in bufs:
+                dist.all_reduce(b)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        tot = 0.0
+        reps = max(5, min(args.steps, 50))
+        for _ in range(reps):
+            flush.zero_()
+            e0.record()
+            for b in bufs:
+                dist.all_reduce(b)
+                b.div_(world)
+            e1.record()
+            torch.cuda.synchronize()
+            tot += e0.elapsed_time(e1)
+        nccl_ms = max_over_ranks(tot / reps, world)
+        nccl = {"ms_per_step": round(nccl_ms, 4), "value": round(world * S / (nccl_ms * 1e-3) / 1e9, 2),
+                "what": f"torch.distributed NCCL all_reduce(SUM)+div on the same {len(sizes)} fused buffers"}
+
+    # end-to-end through the public API with pinned host gradients
+    e2e = None
+    if not args.no_e2e:
+        hgs = make_grads(args.model, rank, None, args.dtype, pinned=True)
+        comm.blocking = True
+        for _ in range(2):
+            P.aggregate(hgs, group, comm, algo=args.algo, cfg=cfg, switch_bytes=args.switch)
+        barrier(world)
+        k = max(3, min(args.steps, 20))
+        t0 = time.perf_counter()
+        for _ in range(k):
+            r = P.aggregate(hgs, group, comm, algo=args.algo, cfg=cfg, switch_bytes=args.switch)
+        torch.cuda.synchronize()
+        e2e_ms = max_over_ranks((time.perf_counter() - t0) / k * 1e3, world)
+        assert not r.tensors[0].is_cuda
+        e2e = {"value": round(world * S / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
+               "ms_per_step": round(e2e_ms, 4), "h2d_bytes_per_step": S, "d2h_bytes_per_step": S,
+               "what": "aggregate() on pinned host gradients: H2D into the device bounce buffer, "
+                       "fused allreduce+mean, D2H of the means, host wall clock, max over ranks"}
+
+    pk, pk_src = peaks()
+    if world > 1:
+        ach = coll_b / (coll_ms * 1e-3) / 1e9 if coll_ms > 0 else 0.0
+        ach = max_over_ranks(-ach, world) * -1  # min over ranks (slowest rank)
+        roofline = {"bound": "nvlink", "kernel": "collective_kernel (two-shot RS+AG, ring order)",
+                    "achieved": round(ach, 2), "peak": NVLINK_PEAK_GBS, "unit": "GB/s",
+                    "frac": round(ach / NVLINK_PEAK_GBS, 4),
+                    "peak_source": "B200_PROFILING.md measured NVLink peer copy (900 nominal)",
+                    "traffic": None,
+                    "algorithmic_bytes_per_launch": coll_b // max(coll_n, 1),
+                    "launches": coll_n, "avg_launch_us": round(coll_ms / max(coll_n, 1) * 1e3, 2)}
+    else:
+        ach = pack_b / (pack_ms * 1e-3) / 1e9 if pack_ms > 0 else 0.0
+        roofline = {"bound": "hbm", "kernel": "batched_copy_kernel (fused pack, p=1 identity allreduce)",
+                    "achieved": round(ach, 2), "peak": pk["hbm_gbs"], "unit": "GB/s",
+                    "frac": round(ach / pk["hbm_gbs"], 4), "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({pk_src})",
+                    "traffic": _ncu_traffic("batched_copy_kernel"),
+                    "algorithmic_bytes_per_launch": pack_b // max(pack_n, 1),
+                    "launches": pack_n, "avg_launch_us": round(pack_ms / max(pack_n, 1) * 1e3, 2)}
+
+    cpu = None
+    if world == 1 and rank == 0 and not args.no_cpu:
+        times = cpu_baseline_sample(args.model, 1, args.dtype)
+        t = statistics.median(times)
+        cpu = {"value": round(S / t / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "port",
+               "sample": f"{len(times)} full steps of the same workload at p=1 (oracle/threaded.py "
+                         f"aggregate: np.concatenate fuse, identity allreduce, float64 mean), "
+                         f"median {t * 1e3:.1f} ms/step"}
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": round(world * S / (ms * 1e-3) / 1e9, 2), "unit": "GB/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32" if args.dtype == "float32" else "bf16",
+            "data": "synthetic: reference synth_gradients recipe (seed 0, iteration 0)",
+            "config": {"workload": f"C5 {args.model} gradient set, tensor-fused allreduce + mean per "
+                                   f"step (aggregate)",
+                       "params_per_rank": sum(layers), "grad_bytes_per_rank": S,
+                       "tensors": len(layers), "fused_buffers": nbuf,
+                       "fusion_threshold": args.fusion_threshold, "algo": args.algo,
+                       "switch_bytes": args.switch, "parallelism": f"dp{world}",
+                       "l2": "flushed: 256 MiB memset between timed steps (outside the events)",
+                       "outputs": "persistent fused output buckets (aggregate(out=prev))"},
+            "latency_us": round(ms * 1e3, 2),
+            "bus_gbps": round(2 * (world - 1) / world * S / (ms * 1e-3) / 1e9, 2) if world > 1 else None,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "gpu_launches_per_step": launches / max(args.steps, 1),
+            "clocks": clocks, "nccl": nccl, "parity": parity,
+        }
+        print(json.dumps(out), flush=True)
+    comm.close()
+
+
+def _ncu_traffic(kernel: str):
+    """dram read+write bytes per launch from the committed ncu summary, if any."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            return json.load(fh).get(kernel)
+    except (OSError, ValueError):
+        return None
+
+
+# --------------------------------------------------------------- reference arm
+def reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    layers = MODELS[args.model]
+    S = sum(layers) * 4
+    from oracle import threaded as T
+    from tests.golden.inputs import synth_gradients
+    grads = [synth_gradients(0, 0, layers, r) for r in range(world)]
+
+    def step():
+        T.ThreadNet(world).run(lambda r, tp: T.aggregate_rank(grads[r], tp, algo=args.algo))
+
+    for _ in range(min(args.warmup, 1)):
+        step()
+    budget = args.ref_budget_s
+    times = []
+    t_start = time.perf_counter()
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        step()
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_start > budget:
+            break
+    ms = statistics.mean(times) * 1e3
+    val = round(world * S / (ms * 1e-3) / 1e9, 4)
+    cores = min(world, os.cpu_count() or 1)
+    out = {
+        "metric": METRIC, "value": val, "unit": "GB/s", "n_gpus": world, "steps": len(times),
+        "steps_requested": args.steps, "warmup": min(args.warmup, 1), "ms_per_step": round(ms, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic: reference synth_gradients recipe (seed 0, iteration 0)",
+        "config": {"workload": f"C5 {args.model} gradient set, tensor-fused allreduce + mean per step "
+                               f"(aggregate)", "params_per_rank": sum(layers), "grad_bytes_per_rank": S,
+                   "fusion_threshold": 67108864, "algo": args.algo, "parallelism": f"dp{world}"},
+        "impl": "reference",
+        "cpu_baseline": {"value": val, "unit": "GB/s", "cores": cores, "kind": "port",
+                         "sample": f"{len(times)} full steps; {world} rank threads of oracle/threaded.py "
+                                   f"(message-passing restatement of collectives.py ring/rhd + "
+                                   f"aggregation.py, numpy) on host cores"},
+        "e2e": {"value": val, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+# ------------------------------------------------------------------ sweep/tune
+def _time_calls(fn, iters, warmup, graph=False):
+    """Device ms per call: CUDA events around `iters` back-to-back calls, or a
+    CUDA graph of `iters` calls replayed once."""
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if graph:
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                for _ in range(iters):
+                    fn()
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        e0.record()
+        g.replay()
+        e1.record()
+    else:
+        e0.record()
+        for _ in range(iters):
+            fn()
+        e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / iters
+
+
+def sweep(args, rank, world, local):
+    import paper_1810_11112_b200 as P
+    from paper_1810_11112_b200 import _lib as L
+    device = torch.device("cuda", local)
+    torch.cuda.set_device(device)
+    maxb = args.sweep_max
+    comm = P.Communicator(rank, world, local, staging_bytes=max(64 << 20, maxb + (4 << 20)),
+                          pool_bytes=max(64 << 20, 2 * maxb + (4 << 20)), blocking=False)
+    st = L.Stats()
+    rows = []
+    sizes = []
+    b = args.sweep_min
+    while b <= maxb:
+        sizes.append(b)
+        b *= 2
+    src = comm.empty(maxb // 4, "float32")
+    dst = comm.empty(maxb // 4, "float32")
+    plain = torch.randn(maxb // 4, device=device)
+    plain_out = torch.empty_like(plain)
+    src.normal_()
+    stream = lambda: torch.cuda.current_stream().cuda_stream  # noqa: E731
+
+    def ours(n, algo, zc):
+        s, d = (src, dst) if zc else (plain, plain_out)
+        return lambda: L.check(L.lib.cm_allreduce(comm._h, s.data_ptr(), d.data_ptr(), n,
+                                                  0, 0, L.ALGO[algo], args.switch or 131072, 0,
+                                                  stream(), C.byref(st)))
+    for nbytes in sizes:
+        n = max(1, nbytes // 4)
+        iters = 200 if nbytes <= (1 << 20) else (50 if nbytes <= (64 << 20) else 10)
+        row = {"message_bytes": nbytes, "p": world}
+        for algo in ("rhd_rsa", "ring_rsa"):
+            barrier(world)
+            row[f"{algo}_us"] = max_over_ranks(_time_calls(ours(n, algo, False), iters, 5) * 1e3, world)
+            barrier(world)
+            row[f"{algo}_zc_us"] = max_over_ranks(_time_calls(ours(n, algo, True), iters, 5) * 1e3, world)
+            if nbytes <= (4 << 20):
+                barrier(world)
+                row[f"{algo}_graph_us"] = max_over_ranks(
+                    _time_calls(ours(n, algo, True), iters, 3, graph=True) * 1e3, world)
+        comm.synchronize()
+        if world > 1:
+            t = plain[:n]
+            barrier(world)
+            row["nccl_us"] = max_over_ranks(_time_calls(lambda: dist.all_reduce(t), iters, 5) * 1e3, world)
+            if nbytes <= (4 << 20):
+                barrier(world)
+                row["nccl_graph_us"] = max_over_ranks(
+                    _time_calls(lambda: dist.all_reduce(t), iters, 3, graph=True) * 1e3, world)
+        best = min(row[f"{a}{v}_us"] for a in ("rhd_rsa", "ring_rsa") for v in ("", "_zc"))
+        row["best_us"] = best
+        fac = 2 * (world - 1) / world if world > 1 else 0.0
+        row["bus_gbps"] = round(nbytes * fac / (best * 1e-6) / 1e9, 3)
+        row["roofline_frac"] = round(row["bus_gbps"] / NVLINK_PEAK_GBS, 4)
+        if "nccl_us" in row:
+            row["nccl_bus_gbps"] = round(nbytes * fac / (row["nccl_us"] * 1e-6) / 1e9, 3)
+        rows.append(row)
+        if rank == 0:
+            log(json.dumps(row))
+    if rank == 0:
+        os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+        path = args.out or os.path.join(ROOT, "gpurun_out", f"sweep_p{world}.csv")
+        keys = sorted({k for r in rows for k in r}, key=lambda k: (k != "message_bytes", k != "p", k))
+        with open(path, "w") as fh:
+            fh.write(",".join(keys) + "\n")
+            for r in rows:
+                fh.write(",".join(format(r.get(k, ""), ".6g") if isinstance(r.get(k), float)
+                                  else str(r.get(k, "")) for k in keys) + "\n")
+        print(json.dumps({"mode": "sweep", "p": world, "rows": rows}), flush=True)
+    comm.close()
+
+
+def tune(args, rank, world, local):
+    """Measure where ring_rsa (two-shot) starts to beat rhd_rsa and write the
+    per-p switch point into paper_1810_11112_b200/tuning.json."""
+    import paper_1810_11112_b200 as P
+    from paper_1810_11112_b200 import _lib as L
+    device = torch.device("cuda", local)
+    torch.cuda.set_device(device)
+    comm = P.Communicator(rank, world, local, staging_bytes=64 << 20, pool_bytes=64 << 20, blocking=False)
+    x = torch.randn(8 << 20, device=device)
+    y = torch.empty_like(x)
+    st = L.Stats()
+    res = {}
+    for nbytes in [1 << k for k in range(10, 24)]:
+        n = nbytes // 4
+        t = {}
+        for algo in ("rhd_rsa", "ring_rsa"):
+            fn = lambda a=algo: L.check(L.lib.cm_allreduce(comm._h, x.data_ptr(), y.data_ptr(), n, 0, 0,  # noqa: E731
+                                                           L.ALGO[a], 131072, 0,
+                                                           torch.cuda.current_stream().cuda_stream,
+                                                           C.byref(st)))
+            barrier(world)
+            t[algo] = max_over_ranks(_time_calls(fn, 100, 5, graph=True), world)
+        res[nbytes] = t
+    switch = None
+    for nbytes in sorted(res):
+        if res[nbytes]["ring_rsa"] < res[nbytes]["rhd_rsa"]:
+            switch = nbytes
+            break
+    if rank == 0:
+        path = os.path.join(ROOT, "paper_1810_11112_b200", "tuning.json")
+        try:
+            with open(path) as fh:
+                data = json.load(fh)
+        except (OSError, ValueError):
+            data = {}
+        data.setdefault("switch_bytes", {})[str(world)] = switch or (1 << 24)
+        data.setdefault("measured", {})[str(world)] = {str(k): {a: round(v * 1e3, 3) for a, v in t.items()}
+                                                       for k, t in res.items()}
+        with open(path, "w") as fh:
+            json.dump(data, fh, indent=1)
+        print(json.dumps({"mode": "tune", "p": world, "switch_bytes": switch}), flush=True)
+    comm.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=None)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--mode", choices=("headline", "sweep", "tune"), default="headline")
+    ap.add_argument("--model", choices=tuple(MODELS), default="resnet50_like")
+    ap.add_argument("--dtype", choices=("float32", "bfloat16"), default="float32")
+    ap.add_argument("--algo", default="auto")
+    ap.add_argument("--switch", type=int, default=None, help="switch_bytes (default: measured table)")
+    ap.add_argument("--fusion-threshold", type=int, default=67108864)
+    ap.add_argument("--sweep-min", type=int, default=4)
+    ap.add_argument("--sweep-max", type=int, default=1 << 30)
+    ap.add_argument("--ref-budget-s", type=float, default=90.0)
+    ap.add_argument("--out", default=None)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-nccl", action="store_true")
+    ap.add_argument("--no-check", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    rank, world, local = dist_env()
+    if args.gpus is not None and args.gpus != world:
+        log(f"note: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE")
+    if args.impl == "reference":
+        reference_arm(args, rank, world)
+        return
+    init_dist(rank, world, local, nccl=True)
+    try:
+        if args.mode == "headline":
+            headline(args, rank, world, local)
+        elif args.mode == "sweep":
+            sweep(args, rank, world, local)
+        else:
+            tune(args, rank, world, local)
+    finally:
+        if world > 1 and dist.is_initialized():
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -164,6 +164,10 @@ int cm_comm_free(cm_comm_t* comm, void* ptr);
 int cm_comm_sync(cm_comm_t* comm, void* stream);
 /* non-blocking error check of completed calls */
 int cm_comm_poll(cm_comm_t* comm);
+/* synchronous element-wise MAX over ranks of n <= 64 host int64 values (one
+ * one-shot NVLink kernel); control-plane primitive of negotiate_ready
+ * (aggregation.py:72-92) — equal (key, -key) maxima prove equal ready sets */
+int cm_agree(cm_comm_t* comm, const int64_t* values, int n, int64_t* maxes, void* stream);
 /* logical counters (Transport.messages_sent / bytes_sent, base.py:43-57) and
  * the real NVLink bytes this rank pulled from peers */
 int cm_comm_counters(cm_comm_t* comm, int64_t* messages_sent, int64_t* bytes_sent,

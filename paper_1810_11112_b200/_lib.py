@@ -90,6 +90,7 @@ _SIGS = {
     "cm_comm_free": ([_vp, _vp], _i),
     "cm_comm_sync": ([_vp, _vp], _i),
     "cm_comm_poll": ([_vp], _i),
+    "cm_agree": ([_vp, _P(_i64), _i, _P(_i64), _vp], _i),
     "cm_comm_counters": ([_vp, _P(_i64), _P(_i64), _P(_i64), _P(_i64)], _i),
     "cm_comm_launches": ([_vp, _P(_i64)], _i),
     "cm_comm_profile": ([_vp, _i], _i),

@@ -47,10 +47,11 @@ class GradientSet:
         return [t.name for t in self.tensors]
 
     def get(self, name: str) -> Tensor:
-        for t in self.tensors:
-            if t.name == name:
-                return t
-        raise KeyError(name)
+        idx = self.__dict__.get("_index")
+        if idx is None:
+            idx = {t.name: i for i, t in enumerate(self.tensors)}
+            object.__setattr__(self, "_index", idx)
+        return self.tensors[idx[name]]
 
 
 @dataclass(frozen=True)
@@ -82,31 +83,32 @@ def negotiate_ready(local_ready: list[str], group: GroupSpec, transport) -> list
     """Intersection of all ranks' ready sets in lexicographic order, identical
     on every rank (aggregation.py:72-92).
 
-    Fast path: one int64 MAX-allreduce over NVLink of (key, -key), key = a
-    hash of the sorted names; equal keys on every rank mean identical ready
-    sets, so the intersection is the local list. Otherwise the sets are
-    gathered to rank 0 over the torch.distributed control plane and the
-    intersection is broadcast, exactly as the reference does over its
-    transport."""
+    Fast path: ``cm_agree`` — one int64 MAX allreduce over NVLink of
+    (key, -key, count, -count), key = a hash of the sorted names; equal maxima
+    on every rank mean identical ready sets, so the intersection is the local
+    list. Otherwise the sets are gathered over the torch.distributed control
+    plane and the intersection is computed exactly as the reference does at
+    rank 0."""
     names = sorted(local_ready)
     if group.size == 1:
         return names
-    tp: Communicator = transport
-    key = _name_key(names)
-    probe = torch.tensor([key, -key, len(names), -len(names)], dtype=torch.int64, device=tp.device)
-    from .collectives import allreduce
-    got, _ = allreduce(Tensor("__negotiate__", "int64", probe), ReduceOp.MAX, group, tp,
-                       algo="rhd_rsa")
-    mx = got.payload.tolist()
-    if mx[0] == key and mx[1] == -key and mx[2] == len(names) and mx[3] == -len(names):
+    if _sets_agree(transport, _name_key(names), len(names)):
         return names
     import torch.distributed as dist
     gathered = [None] * group.size
-    dist.all_gather_object(gathered, names, group=tp._group)
+    dist.all_gather_object(gathered, names, group=transport._group)
     common = set(gathered[0])
     for g in gathered[1:]:
         common &= set(g)
     return sorted(common)
+
+
+def _sets_agree(tp: Communicator, key: int, count: int) -> bool:
+    vals = (C.c_int64 * 4)(key, -key, count, -count)
+    mx = (C.c_int64 * 4)()
+    with torch.cuda.device(tp.device):
+        L.check(L.lib.cm_agree(tp._h, vals, 4, mx, tp._stream()))
+    return list(mx) == [key, -key, count, -count]
 
 
 def fuse_plan(tensors: list[Tensor], cfg: FusionConfig) -> list[list[int]]:
@@ -160,66 +162,101 @@ def unfuse(buf: FusedBuffer) -> list[Tensor]:
             for name, off, length in buf.members]
 
 
+class _Plan:
+    """Per-(GradientSet, negotiated names, config) launch plan: member order,
+    same-dtype runs with their ctypes pointer/count arrays, and split sizes.
+    GradientSet is immutable, so the plan is cached on it."""
+
+    def __init__(self, grads: GradientSet, names: list[str]):
+        self.names = names
+        ready = [grads.get(nm) for nm in names]
+        self.runs = []
+        i = 0
+        while i < len(ready):
+            j = i
+            while j < len(ready) and ready[j].dtype == ready[i].dtype:
+                j += 1
+            run = ready[i:j]
+            for t in run:
+                if t.dtype not in ("float32", "float64", "bfloat16"):
+                    raise ShapeError(f"aggregate averages floating-point gradients, got {t.dtype}")
+            counts = [t.len for t in run]
+            self.runs.append(dict(
+                dtype=run[0].dtype, names=[t.name for t in run], counts=counts,
+                total=sum(counts), any_host=any(not t.is_cuda for t in run),
+                ptrs=L.ptr_array([t.payload.data_ptr() for t in run]),
+                counts_c=L.i64_array(counts), n=len(run),
+                stats=(L.Stats * len(run))()))
+            i = j
+        self.ready = ready
+
+
 def aggregate(grads: GradientSet, group: GroupSpec, transport: Communicator,
               algo: str = "auto", cfg: FusionConfig | None = None,
               switch_bytes: int | None = DEFAULT_SWITCH_BYTES,
               registry=None, handles: dict | None = None,
-              stats_out: list[CollectiveStats] | None = None) -> GradientSet:
+              stats_out: list[CollectiveStats] | None = None,
+              out: GradientSet | None = None) -> GradientSet:
     """Negotiate, fuse, allreduce-sum and average this iteration's gradients;
-    every rank returns the same mean tensors (aggregation.py:138-176)."""
+    every rank returns the same mean tensors (aggregation.py:138-176).
+
+    ``out``: a GradientSet previously returned by ``aggregate`` for the same
+    schema; its fused buffers are reused (stream-ordered overwrite, like
+    torch ``out=``) instead of allocating new ones — the persistent-bucket
+    mode of a training loop."""
     cfg = cfg or FusionConfig()
     tp = transport
     if group.size != tp.size:
         raise ShapeError(f"group size {group.size} does not match transport size {tp.size}")
+    if algo not in L.ALGO:
+        from .errors import ConfigError
+        raise ConfigError(f"unknown algorithm {algo!r}")
     ready_names = negotiate_ready(grads.names, group, tp)
     if not ready_names:
         return GradientSet((), grads.iteration)
-    ready = [grads.get(name) for name in ready_names]
-    for t in ready:
-        if t.dtype not in ("float32", "float64", "bfloat16"):
-            raise ShapeError(f"aggregate averages floating-point gradients, got {t.dtype}")
+    cache = grads.__dict__.setdefault("_plans", {})
+    key = tuple(ready_names)
+    plan = cache.get(key)
+    if plan is None:
+        plan = cache[key] = _Plan(grads, ready_names)
     sw = _switch(switch_bytes, tp.size)
-    plan = fuse_plan(ready, cfg)
     if registry is not None and handles is not None:
-        for grp in plan:                      # aggregation.py:159-161
+        for grp in fuse_plan(plan.ready, cfg):       # aggregation.py:159-161
             for i in grp:
-                registry.classify(handles[ready[i].name])
-    out: dict[str, Tensor] = {}
-    # a dtype change always closes a fused group, so consecutive same-dtype
-    # runs can be issued as independent cm_fused_allreduce calls
-    i = 0
-    while i < len(ready):
-        j = i
-        while j < len(ready) and ready[j].dtype == ready[i].dtype:
-            j += 1
-        run = ready[i:j]
-        dtype = run[0].dtype
-        any_host = any(not t.is_cuda for t in run)
-        dev = tp.device
-        total = sum(t.len for t in run)
-        fused = torch.empty(total, dtype=DTYPES[dtype], device=dev)
-        counts = [t.len for t in run]
-        st = (L.Stats * len(run))()
-        ncalls = C.c_int()
-        with torch.cuda.device(dev):
+                registry.classify(handles[plan.ready[i].name])
+    reuse = out.__dict__.get("_fused") if out is not None else None
+    if reuse is not None and [f.numel() for f in reuse] != [r["total"] for r in plan.runs]:
+        raise ShapeError("out= GradientSet does not match this gradient schema")
+    result: list[Tensor] = []
+    fused_bufs = []
+    stream = tp._stream()
+    with torch.cuda.device(tp.device):
+        for ri, run in enumerate(plan.runs):
+            dtype = run["dtype"]
+            fused = reuse[ri] if reuse is not None else \
+                torch.empty(run["total"], dtype=DTYPES[dtype], device=tp.device)
+            ncalls = C.c_int()
             L.check(L.lib.cm_fused_allreduce(
-                tp._h, len(run), L.ptr_array([t.payload.data_ptr() for t in run]),
-                L.i64_array(counts), L.DTYPE[dtype], fused.data_ptr(), L.ALGO[algo],
-                int(cfg.threshold_bytes), sw, 1, tp._stream(), st, C.byref(ncalls)))
-        if any_host:
-            fused = fused.cpu()
-        if tp.blocking or any_host:
-            tp.synchronize()
-        else:
-            tp.poll()
-        if stats_out is not None:
-            stats_out.extend(_stats(st[k]) for k in range(ncalls.value))
-        off = 0
-        for t in run:
-            out[t.name] = Tensor(t.name, dtype, fused[off:off + t.len])
-            off += t.len
-        i = j
-    return GradientSet(tuple(out[name] for name in ready_names), grads.iteration)
+                tp._h, run["n"], run["ptrs"], run["counts_c"], L.DTYPE[dtype], fused.data_ptr(),
+                L.ALGO[algo], int(cfg.threshold_bytes), sw, 1, stream, run["stats"],
+                C.byref(ncalls)))
+            if stats_out is not None:
+                stats_out.extend(_stats(run["stats"][k]) for k in range(ncalls.value))
+            fused_bufs.append(fused)
+            host = run["any_host"]
+            if host:
+                fused = fused.cpu()
+            for nm, view in zip(run["names"], fused.split_with_sizes(run["counts"])):
+                result.append(Tensor._wrap(nm, dtype, view))
+    if tp.blocking or any(r["any_host"] for r in plan.runs):
+        tp.synchronize()
+    else:
+        tp.poll()
+    gs = GradientSet.__new__(GradientSet)
+    object.__setattr__(gs, "tensors", tuple(result))
+    object.__setattr__(gs, "iteration", grads.iteration)
+    object.__setattr__(gs, "_fused", fused_bufs)
+    return gs
 
 
 def aggregate_group(per_rank: list[GradientSet], vg: VirtualGroup, algo: str = "auto",

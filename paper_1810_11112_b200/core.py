@@ -38,6 +38,9 @@ class ReduceOp(enum.Enum):
 
 
 def _as_payload(values, dtype: str) -> torch.Tensor:
+    if type(values) is torch.Tensor and values.dtype == DTYPES[dtype] and values.dim() == 1 \
+            and values.is_contiguous():
+        return values                                  # fast path: already a 1-D payload
     if isinstance(values, torch.Tensor):
         t = values
         if t.dtype != DTYPES[dtype]:
@@ -66,6 +69,16 @@ class Tensor:
         if self.dtype not in DTYPES:
             raise ShapeError(f"unsupported dtype {self.dtype!r}")
         object.__setattr__(self, "payload", _as_payload(self.payload, self.dtype))
+
+    @classmethod
+    def _wrap(cls, name: str, dtype: str, payload: torch.Tensor) -> "Tensor":
+        """Internal constructor for payloads the library produced itself
+        (already 1-D, contiguous, right dtype): skips validation."""
+        t = object.__new__(cls)
+        object.__setattr__(t, "name", name)
+        object.__setattr__(t, "dtype", dtype)
+        object.__setattr__(t, "payload", payload)
+        return t
 
     @property
     def len(self) -> int:

@@ -36,6 +36,8 @@ struct cm_comm {
   std::map<size_t, size_t> pool_free;  // offset -> bytes
   std::map<size_t, size_t> pool_used;
   char* scratch = nullptr;             // device bounce buffer for host-memory buffers
+  int64_t* agree_host = nullptr;       // pinned: cm_agree in/out
+  int64_t* agree_dev = nullptr;        // device: cm_agree in/out
   int sms = 148;
   // tuning knobs (cm_comm_set_param)
   int64_t oneshot_max_bytes = 256 * 1024;
@@ -602,6 +604,8 @@ int cm_comm_destroy(cm_comm_t* c) {
   if (c->local) cudaFree(c->local);
   if (c->scratch) cudaFree(c->scratch);
   if (c->herr_host) cudaFreeHost(c->herr_host);
+  if (c->agree_host) cudaFreeHost(c->agree_host);
+  if (c->agree_dev) cudaFree(c->agree_dev);
   for (auto& pr : c->prof) { cudaEventDestroy(pr.e0); cudaEventDestroy(pr.e1); }
   for (auto e : c->event_pool) cudaEventDestroy(e);
   cudaGetLastError();
@@ -697,6 +701,40 @@ int cm_comm_sync(cm_comm_t* c, void* stream) {
 }
 
 int cm_comm_poll(cm_comm_t* c) { return check_async_error(c); }
+
+// Element-wise MAX over ranks of n int64 host values, synchronously: the
+// control-plane primitive behind negotiate_ready's fast path (one one-shot
+// kernel over NVLink instead of a host gather/broadcast).
+int cm_agree(cm_comm_t* c, const int64_t* values, int n, int64_t* maxes, void* stream_) {
+  if (n < 1 || n > 64) return fail(CM_ERR_VALUE, "cm_agree takes 1..64 values");
+  if (c->virt) return fail(CM_ERR_UNSUPPORTED, "cm_agree needs a real communicator");
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  if (!c->agree_host) {
+    CUDA_TRY(cudaHostAlloc(&c->agree_host, 128 * sizeof(int64_t), cudaHostAllocDefault));
+    CUDA_TRY(cudaMalloc(&c->agree_dev, 128 * sizeof(int64_t)));
+  }
+  if (c->size == 1) {
+    memcpy(maxes, values, n * sizeof(int64_t));
+    return CM_OK;
+  }
+  memcpy(c->agree_host, values, n * sizeof(int64_t));
+  CUDA_TRY(cudaMemcpyAsync(c->agree_dev, c->agree_host, n * sizeof(int64_t), cudaMemcpyHostToDevice, stream));
+  Launch L;
+  L.n = n;
+  L.dtype = CM_INT64;
+  L.op = CM_MAX;
+  plan_algo(c, CM_ALGO_RHD, n * 8, &L);
+  L.srcmode = SRC_COPYIN;
+  L.in[0] = c->agree_dev;
+  L.out[0] = c->agree_dev + 64;
+  int st = launch_collective(c, L, stream);
+  if (st) return st;
+  CUDA_TRY(cudaMemcpyAsync(c->agree_host + 64, c->agree_dev + 64, n * sizeof(int64_t), cudaMemcpyDeviceToHost, stream));
+  CUDA_TRY(cudaStreamSynchronize(stream));
+  if ((st = check_async_error(c))) return st;
+  memcpy(maxes, c->agree_host + 64, n * sizeof(int64_t));
+  return CM_OK;
+}
 
 int cm_comm_counters(cm_comm_t* c, int64_t* messages_sent, int64_t* bytes_sent,
                      int64_t* nvlink_bytes_in, int64_t* calls) {

@@ -314,10 +314,11 @@ __device__ void reduce_range(const char* const* seq, int p, int m, int excess, l
     reduce_one<D, OP, MP, 1, TREE>(seq, p, m, excess, i, average, out, out_shift, red, red_shift);
   // vector body: vectors j in [body_lo/W, body_hi/W)
   const long long v0 = body_lo / W, v1 = body_hi / W;
-  constexpr int U = (MP <= 8) ? 2 : 1;
+  using A = typename D::A;
+  // two vector groups in flight per thread when the operand registers fit
+  constexpr int U = (MP * W * (int)(sizeof(A) / 4) <= 32) ? 2 : 1;
   long long j = v0 + tid;
   for (; j + (U - 1) * (long long)blockDim.x < v1; j += U * (long long)blockDim.x) {
-    using A = typename D::A;
     A u[U][MP][W];
 #pragma unroll
     for (int g = 0; g < U; ++g)
