@@ -194,6 +194,9 @@ def headline(args, rank, world, local):
     S = sum(layers) * esz
     comm = P.Communicator(rank, world, local, staging_bytes=max(256 << 20, S + (8 << 20)),
                           pool_bytes=64 << 20, blocking=False)
+    for kv in args.param:
+        k, v = kv.split("=")
+        comm.set_param(k, int(v))
     group = P.GroupSpec(world)
     cfg = P.FusionConfig(args.fusion_threshold)
     gs = make_grads(args.model, rank, device, args.dtype)
@@ -444,6 +447,9 @@ def sweep(args, rank, world, local):
     while b <= maxb:
         sizes.append(b)
         b *= 2
+    for kv in args.param:
+        k, v = kv.split("=")
+        comm.set_param(k, int(v))
     src = comm.empty(maxb // 4, "float32")
     dst = comm.empty(maxb // 4, "float32")
     plain = torch.randn(maxb // 4, device=device)
@@ -460,7 +466,7 @@ def sweep(args, rank, world, local):
         n = max(1, nbytes // 4)
         iters = 200 if nbytes <= (1 << 20) else (50 if nbytes <= (64 << 20) else 10)
         row = {"message_bytes": nbytes, "p": world}
-        for algo in ("rhd_rsa", "ring_rsa"):
+        for algo in args.algos.split(","):
             barrier(world)
             row[f"{algo}_us"] = max_over_ranks(_time_calls(ours(n, algo, False), iters, 5) * 1e3, world)
             barrier(world)
@@ -478,7 +484,7 @@ def sweep(args, rank, world, local):
                 barrier(world)
                 row["nccl_graph_us"] = max_over_ranks(
                     _time_calls(lambda: dist.all_reduce(t), iters, 3, graph=True) * 1e3, world)
-        best = min(row[f"{a}{v}_us"] for a in ("rhd_rsa", "ring_rsa") for v in ("", "_zc"))
+        best = min(row[f"{a}{v}_us"] for a in args.algos.split(",") for v in ("", "_zc"))
         row["best_us"] = best
         fac = 2 * (world - 1) / world if world > 1 else 0.0
         row["bus_gbps"] = round(nbytes * fac / (best * 1e-6) / 1e9, 3)
@@ -565,6 +571,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-nccl", action="store_true")
     ap.add_argument("--no-check", action="store_true")
+    ap.add_argument("--param", action="append", default=[],
+                    help="communicator tuning knob key=value (cm_comm_set_param)")
+    ap.add_argument("--algos", default="rhd_rsa,ring_rsa", help="sweep: algorithms to time")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank, world, local = dist_env()

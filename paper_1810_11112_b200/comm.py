@@ -167,6 +167,10 @@ class Communicator(_Base):
         self.set_policy(policy)
         if timeout_s is not None:
             self.set_timeout(timeout_s)
+        from .tuning import oneshot_max_for
+        osm = oneshot_max_for(self.size)
+        if osm:
+            self.set_param("oneshot_max_bytes", osm)
         self._sym: dict[int, int] = {}
 
     # -- symmetric allocation (zero-copy collectives) -------------------------

@@ -42,7 +42,7 @@ struct cm_comm {
   // tuning knobs (cm_comm_set_param)
   int64_t oneshot_max_bytes = 256 * 1024;
   int64_t oneshot_bytes_per_cta = 16 * 1024;
-  int64_t twoshot_bytes_per_cta = 64 * 1024;
+  int64_t twoshot_bytes_per_cta = 16 * 1024;
   int max_ctas = 148;
   // counters
   int64_t messages = 0, bytes = 0, nvlink_in = 0, calls = 0, launches = 0;
