@@ -342,37 +342,60 @@ __device__ void reduce_range(const char* const* seq, int p, int m, int excess, l
                                    red_shift);
 }
 
-// byte-level copy of elements [lo, hi): dst[i - dshift] = src[i - sshift]
-template <class D>
-__device__ void copy_range(const char* src, long long sshift, char* dst, long long dshift,
-                           long long lo, long long hi, bool vec) {
+// Several element ranges copied CONCURRENTLY: range r moves elements
+// [lo, hi) with dst[i - dshift] = src[i - sshift]. Every thread issues the
+// loads of all ranges before any store, so the allgather pulls from all
+// peers at once (balanced NVLink traffic, one round trip per iteration).
+struct CopyRange {
+  const char* src;
+  char* dst;
+  long long sshift, dshift, lo, hi;
+};
+
+struct VecRange {
+  const uint4* src;
+  uint4* dst;
+  long long nv;
+};
+
+// R[0..nr) in shared memory; V is shared scratch of the same size.
+template <class D, int MP>
+__device__ void multi_copy(const CopyRange* R, int nr, VecRange* V) {
   using S = typename D::S;
   constexpr int W = 16 / sizeof(S);
-  const int tid = threadIdx.x;
-  const S* s = reinterpret_cast<const S*>(src);
-  S* d = reinterpret_cast<S*>(dst);
-  long long body_lo = lo, body_hi = lo;
-  if (vec) {
-    body_lo = ((lo + W - 1) / W) * W;
-    body_hi = (hi / W) * W;
-    if (body_hi < body_lo) body_hi = body_lo = hi;
+  const int tid = threadIdx.x, bd = blockDim.x;
+  const int warp = tid >> 5, lane = tid & 31, nwarps = bd >> 5;
+  // scalar heads/tails (and misaligned ranges): one warp per range
+  for (int r = warp; r < nr; r += nwarps) {
+    const CopyRange c = R[r];
+    const S* s = reinterpret_cast<const S*>(c.src) - c.sshift;
+    S* d = reinterpret_cast<S*>(c.dst) - c.dshift;
+    long long blo = c.hi, bhi = c.hi;
+    if (((((uintptr_t)s) | ((uintptr_t)d)) & 15u) == 0) {
+      blo = ((c.lo + W - 1) / W) * W;
+      bhi = (c.hi / W) * W;
+      if (bhi < blo) blo = bhi = c.hi;
+    }
+    for (long long i = c.lo + lane; i < blo; i += 32) d[i] = s[i];
+    for (long long i = bhi + lane; i < c.hi; i += 32) d[i] = s[i];
+    if (lane == 0) {
+      V[r].src = reinterpret_cast<const uint4*>(s + blo);
+      V[r].dst = reinterpret_cast<uint4*>(d + blo);
+      V[r].nv = (bhi - blo) / W;
+    }
   }
-  for (long long i = lo + tid; i < body_lo; i += blockDim.x) d[i - dshift] = s[i - sshift];
-  for (long long i = body_hi + tid; i < hi; i += blockDim.x) d[i - dshift] = s[i - sshift];
-  const long long v0 = body_lo / W, v1 = body_hi / W;
-  constexpr int U = 4;
-  long long j = v0 + tid;
-  for (; j + (U - 1) * (long long)blockDim.x < v1; j += U * (long long)blockDim.x) {
-    uint4 r[U];
+  __syncthreads();
+  long long nvmax = 0;
+  for (int r = 0; r < nr; ++r) nvmax = V[r].nv > nvmax ? V[r].nv : nvmax;
+  for (long long j = tid; j < nvmax; j += bd) {
+    uint4 v[MP];
 #pragma unroll
-    for (int g = 0; g < U; ++g)
-      r[g] = *reinterpret_cast<const uint4*>(s + (j + g * (long long)blockDim.x) * W - sshift);
+    for (int r = 0; r < MP; ++r)
+      if (r < nr && j < V[r].nv) v[r] = V[r].src[j];
 #pragma unroll
-    for (int g = 0; g < U; ++g)
-      *reinterpret_cast<uint4*>(d + (j + g * (long long)blockDim.x) * W - dshift) = r[g];
+    for (int r = 0; r < MP; ++r)
+      if (r < nr && j < V[r].nv) V[r].dst[j] = v[r];
   }
-  for (; j < v1; j += blockDim.x)
-    *reinterpret_cast<uint4*>(d + j * W - dshift) = *reinterpret_cast<const uint4*>(s + j * W - sshift);
 }
 
 __device__ __forceinline__ bool al16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
@@ -427,24 +450,31 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
   }
 
   // 1. copy-in: this CTA's slice of every segment peers will read from me
+  __shared__ CopyRange s_cr[MAXP + 1];
+  __shared__ VecRange s_vr[MAXP + 1];
+  __shared__ int s_ncr;
   if (P.srcmode == SRC_COPYIN) {
     char* stage = myheap + stage_off;
     if (ag_only) {
-      const long long lo = slice_bound(mso, P.seg_len[rank], b, nb);
-      const long long hi = slice_bound(mso, P.seg_len[rank], b + 1, nb);
-      const long long ish = P.ag_in_rel ? mso : 0;
-      const bool v = al16s(in, ish, SZ);
-      copy_range<D>(in, ish, stage, 0, lo, hi, v);
-      copy_range<D>(in, ish, out, 0, lo, hi, v && al16(out));
-    } else {
-      const bool v = al16(in);
-      const int nseg = P.oneshot ? 1 : p;
-      for (int q = 0; q < nseg; ++q) {
-        const long long so = P.oneshot ? 0 : P.seg_off[q];
-        const long long sl = P.oneshot ? P.n : P.seg_len[q];
-        copy_range<D>(in, 0, stage, 0, slice_bound(so, sl, b, nb), slice_bound(so, sl, b + 1, nb), v);
+      if (tid == 0) {
+        const long long lo = slice_bound(mso, P.seg_len[rank], b, nb);
+        const long long hi = slice_bound(mso, P.seg_len[rank], b + 1, nb);
+        const long long ish = P.ag_in_rel ? mso : 0;
+        s_cr[0] = CopyRange{in, stage, ish, 0, lo, hi};
+        s_cr[1] = CopyRange{in, out, ish, 0, lo, hi};
+        s_ncr = 2;
       }
+    } else {
+      const int nseg = P.oneshot ? 1 : p;
+      if (tid < nseg) {
+        const long long so = P.oneshot ? 0 : P.seg_off[tid];
+        const long long sl = P.oneshot ? P.n : P.seg_len[tid];
+        s_cr[tid] = CopyRange{in, stage, 0, 0, slice_bound(so, sl, b, nb), slice_bound(so, sl, b + 1, nb)};
+      }
+      if (tid == 0) s_ncr = nseg;
     }
+    __syncthreads();
+    multi_copy<D, MP>(s_cr, s_ncr, s_vr);
   }
   __syncthreads();
 
@@ -513,14 +543,20 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
       __syncthreads();
       if (s_err) goto finish;
     }
-    for (int q = 0; q < p; ++q) {
-      if (q == rank && !(ag_only && P.srcmode == SRC_ZEROCOPY)) continue;
-      const long long so = P.seg_off[q], sl = P.seg_len[q];
-      const long long lo = slice_bound(so, sl, b, nb), hi = slice_bound(so, sl, b + 1, nb);
-      if (hi <= lo) continue;
-      const char* src = s_red[q];
-      copy_range<D>(src, so, out, 0, lo, hi, al16s(src, so, SZ) && al16(out));
+    // pull slice b of every other segment from all peers concurrently
+    if (tid == 0) {
+      int k = 0;
+      for (int q = 0; q < p; ++q) {
+        if (q == rank && !(ag_only && P.srcmode == SRC_ZEROCOPY)) continue;
+        const long long so = P.seg_off[q], sl = P.seg_len[q];
+        const long long lo = slice_bound(so, sl, b, nb), hi = slice_bound(so, sl, b + 1, nb);
+        if (hi <= lo) continue;
+        s_cr[k++] = CopyRange{s_red[q], out, so, 0, lo, hi};
+      }
+      s_ncr = k;
     }
+    __syncthreads();
+    multi_copy<D, MP>(s_cr, s_ncr, s_vr);
   }
 
 finish:
