@@ -41,8 +41,10 @@ struct cm_comm {
   int sms = 148;
   // tuning knobs (cm_comm_set_param)
   int64_t oneshot_max_bytes = 256 * 1024;
-  int64_t oneshot_bytes_per_cta = 16 * 1024;
-  int64_t twoshot_bytes_per_cta = 16 * 1024;
+  int64_t ll_max_bytes = 32 * 1024;           // one-shot via LL slots up to here
+  int64_t ll_units_per_cta = 512;
+  int64_t oneshot_bytes_per_cta = 8 * 1024;
+  int64_t twoshot_bytes_per_cta = 4 * 1024;
   int max_ctas = 148;
   // counters
   int64_t messages = 0, bytes = 0, nvlink_in = 0, calls = 0, launches = 0;
@@ -118,6 +120,26 @@ KFn pick_op(int op, int p, bool tree) {
   return op == CM_SUM ? pick_mp<D, CM_SUM>(p, tree) : pick_mp<D, CM_MAX>(p, tree);
 }
 
+template <class D, int OP>
+KFn pick_ll_mp(int p, bool tree) {
+  if (p <= 8) return tree ? ll_kernel<D, OP, 8, true> : ll_kernel<D, OP, 8, false>;
+  return tree ? ll_kernel<D, OP, 16, true> : ll_kernel<D, OP, 16, false>;
+}
+
+KFn pick_ll(int dtype, int op, int p, bool tree) {
+  switch (dtype) {
+#define LLCASE(T, D) \
+    case T: return op == CM_SUM ? pick_ll_mp<D, CM_SUM>(p, tree) : pick_ll_mp<D, CM_MAX>(p, tree);
+    LLCASE(CM_FLOAT32, F32)
+    LLCASE(CM_FLOAT64, F64)
+    LLCASE(CM_BFLOAT16, BF16)
+    LLCASE(CM_INT32, I32)
+    LLCASE(CM_INT64, I64)
+#undef LLCASE
+  }
+  return nullptr;
+}
+
 KFn pick_kernel(int dtype, int op, int p, bool tree) {
   switch (dtype) {
     case CM_FLOAT32: return pick_op<F32>(op, p, tree);
@@ -183,6 +205,7 @@ struct Launch {
   int dtype = 0, op = 0, order = ORD_SEQ, phases = PH_RS | PH_AG, oneshot = 0;
   int out_rel = 0, ag_in_rel = 0, average = 0, layout = CM_LAYOUT_RING;
   int srcmode = SRC_COPYIN;
+  int ll = 0;                       // one-shot through the LL slots
   const void* in[MAXP] = {};
   void* out[MAXP] = {};
   int64_t zc_srcoff[MAXP] = {};
@@ -217,7 +240,7 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
   // staging capacity
   const int64_t need = (L.srcmode == SRC_ZEROCOPY) ? (maxseg + SLICE_ALIGN) * (int64_t)sz
                                                   : L.n * (int64_t)sz;
-  if (need > (int64_t)c->staging_bytes)
+  if (!L.ll && need > (int64_t)c->staging_bytes)
     return fail(CM_ERR_CONFIG, "message of " + std::to_string(L.n * sz) + " B needs " +
                                    std::to_string(need) + " B of staging; the communicator has " +
                                    std::to_string(c->staging_bytes) +
@@ -242,8 +265,10 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
   const int64_t work = L.oneshot ? L.n * (int64_t)sz : maxseg * (int64_t)sz;
   const int64_t per = L.oneshot ? c->oneshot_bytes_per_cta : c->twoshot_bytes_per_cta;
   int64_t nb = (work + per - 1) / per;
+  if (L.ll) nb = ((L.n * (int64_t)sz + 7) / 8 + c->ll_units_per_cta - 1) / c->ll_units_per_cta;
   nb = std::max<int64_t>(1, std::min<int64_t>(nb, std::min(c->max_ctas, MAXBLK)));
-  KFn k = pick_kernel(L.dtype, L.op, p, L.order == ORD_TREE);
+  KFn k = L.ll ? pick_ll(L.dtype, L.op, p, L.order == ORD_TREE)
+               : pick_kernel(L.dtype, L.op, p, L.order == ORD_TREE);
   if (!k) return fail(CM_ERR_SHAPE, "unsupported dtype");
   void* args[] = {&P};
   int64_t alg = 0;   // busBW bytes of this launch (nccl-tests convention)
@@ -266,7 +291,8 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
   if (!c->virt) {
     const int r = c->rank;
     int64_t in_bytes = 0;
-    if (L.oneshot) in_bytes = (int64_t)(p - 1) * L.n * sz;
+    if (L.ll) in_bytes = (int64_t)(p - 1) * ((L.n * (int64_t)sz + 7) / 8) * 16;
+    else if (L.oneshot) in_bytes = (int64_t)(p - 1) * L.n * sz;
     else {
       if (L.phases & PH_RS) in_bytes += (int64_t)(p - 1) * len[r] * sz;
       if (L.phases & PH_AG)
@@ -342,6 +368,7 @@ void plan_algo(cm_comm* c, int concrete, int64_t nbytes, Launch* L) {
     L->layout = CM_LAYOUT_RING;
   }
   L->phases = L->oneshot ? PH_RS : (PH_RS | PH_AG);
+  L->ll = (L->oneshot && nbytes <= c->ll_max_bytes) ? 1 : 0;
 }
 
 int do_allreduce(cm_comm* c, const void* const* sends, void* const* recvs, int64_t count,
@@ -642,6 +669,8 @@ int cm_comm_set_param(cm_comm_t* c, const char* key, int64_t value) {
   const std::string k(key);
   if (value <= 0) return fail(CM_ERR_VALUE, "parameter must be positive");
   if (k == "oneshot_max_bytes") c->oneshot_max_bytes = value;
+  else if (k == "ll_max_bytes") c->ll_max_bytes = std::min<int64_t>(value, (int64_t)LL_MAX_BYTES);
+  else if (k == "ll_units_per_cta") c->ll_units_per_cta = value;
   else if (k == "oneshot_bytes_per_cta") c->oneshot_bytes_per_cta = value;
   else if (k == "twoshot_bytes_per_cta") c->twoshot_bytes_per_cta = value;
   else if (k == "max_ctas") c->max_ctas = (int)std::min<int64_t>(value, MAXBLK);
@@ -652,6 +681,8 @@ int cm_comm_set_param(cm_comm_t* c, const char* key, int64_t value) {
 int cm_comm_get_param(cm_comm_t* c, const char* key, int64_t* value) {
   const std::string k(key);
   if (k == "oneshot_max_bytes") *value = c->oneshot_max_bytes;
+  else if (k == "ll_max_bytes") *value = c->ll_max_bytes;
+  else if (k == "ll_units_per_cta") *value = c->ll_units_per_cta;
   else if (k == "oneshot_bytes_per_cta") *value = c->oneshot_bytes_per_cta;
   else if (k == "twoshot_bytes_per_cta") *value = c->twoshot_bytes_per_cta;
   else if (k == "max_ctas") *value = c->max_ctas;
