@@ -656,7 +656,10 @@ __global__ void __launch_bounds__(THREADS) ll_kernel(const __grid_constant__ Col
   const long long nbytes = P.n * (long long)sizeof(S);
   const long long nunits = (nbytes + 7) / 8;
   const long long u0 = nunits * b / nb, u1 = nunits * (b + 1) / nb;
-  const char* in = P.in[lr];
+  // prestaged input (fused pack) lives in staging[parity]
+  const char* in = P.srcmode == SRC_PRESTAGED
+                       ? myheap + STAGING_OFF + (long long)par * P.staging_bytes
+                       : P.in[lr];
   char* out = P.out[lr];
 
   // header units: this CTA's call signature to every rank
