@@ -174,6 +174,11 @@ int cm_comm_counters(cm_comm_t* comm, int64_t* messages_sent, int64_t* bytes_sen
                      int64_t* nvlink_bytes_in, int64_t* calls);
 /* number of kernels this comm has launched (bench "gpu_launches") */
 int cm_comm_launches(cm_comm_t* comm, int64_t* launches);
+/* diagnostics: every collective kernel writes globaltimer stamps of its
+ * phases (start, copied-in, start barrier, reduced, mid barrier, end) into
+ * device_buffer[(local_rank * ctas + cta) * 8 + phase] for ctas < `ctas`;
+ * NULL disables */
+int cm_comm_set_trace(cm_comm_t* comm, void* device_buffer, int ctas);
 /* bracket every kernel this comm launches with CUDA events on its stream */
 int cm_comm_profile(cm_comm_t* comm, int enable);
 /* drain recorded launches of one kind (0 = collective kernel, 1 = pack/copy

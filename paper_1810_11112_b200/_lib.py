@@ -94,6 +94,7 @@ _SIGS = {
     "cm_comm_counters": ([_vp, _P(_i64), _P(_i64), _P(_i64), _P(_i64)], _i),
     "cm_comm_launches": ([_vp, _P(_i64)], _i),
     "cm_comm_profile": ([_vp, _i], _i),
+    "cm_comm_set_trace": ([_vp, _vp, _i], _i),
     "cm_comm_profile_read": ([_vp, _i, _P(_i64), _P(C.c_double), _P(_i64)], _i),
     "cm_allreduce": ([_vp, _vp, _vp, _i64, _i, _i, _i, _i64, _i, _vp, _P(Stats)], _i),
     "cm_reduce_scatter": ([_vp, _vp, _vp, _i64, _i, _i, _i, _vp, _P(Stats)], _i),

@@ -54,6 +54,8 @@ struct cm_comm {
     cudaEvent_t e0, e1;
     int64_t alg_bytes;
   };
+  unsigned long long* trace = nullptr;  // cm_comm_set_trace
+  int trace_ctas = 0;
   bool profiling = false;
   std::vector<Prof> prof;
   std::vector<cudaEvent_t> event_pool;
@@ -260,6 +262,8 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
   P.out_rel = L.out_rel;
   P.ag_in_rel = L.ag_in_rel;
   P.average = L.average;
+  P.trace = c->trace;
+  P.trace_ctas = c->trace_ctas;
 
   // grid: CTAs per rank; identical on every rank (depends on n, p, dtype only)
   const int64_t work = L.oneshot ? L.n * (int64_t)sz : maxseg * (int64_t)sz;
@@ -778,6 +782,12 @@ int cm_comm_counters(cm_comm_t* c, int64_t* messages_sent, int64_t* bytes_sent,
 
 int cm_comm_launches(cm_comm_t* c, int64_t* launches) {
   *launches = c->launches;
+  return CM_OK;
+}
+
+int cm_comm_set_trace(cm_comm_t* c, void* device_buffer, int ctas) {
+  c->trace = static_cast<unsigned long long*>(device_buffer);
+  c->trace_ctas = device_buffer ? ctas : 0;
   return CM_OK;
 }
 

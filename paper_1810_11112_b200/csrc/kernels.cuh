@@ -97,7 +97,21 @@ struct CollParams {
   int out_rel;               // RS writes out[i - seg_off] (reduce_scatter API)
   int ag_in_rel;             // AG-only: `in` holds only my segment (in[i - seg_off])
   int average;               // divide the reduced value by p (aggregate mean)
+  unsigned long long* trace; // optional: per-CTA phase timestamps (globaltimer ns)
+  int trace_ctas;
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// phase stamp k (0 start, 1 copied-in, 2 start barrier, 3 reduced, 4 mid barrier, 5 end)
+#define CM_TRACE(P, lr, b, k)                                                   \
+  do {                                                                          \
+    if ((P).trace && threadIdx.x == 0 && (b) < (P).trace_ctas)                  \
+      (P).trace[((size_t)(lr) * (P).trace_ctas + (b)) * 8 + (k)] = gtimer();    \
+  } while (0)
 
 // ---- element types ----------------------------------------------------------
 struct F32 { using S = float;    using A = float; };
@@ -428,6 +442,7 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
   __shared__ const char* s_seq[MAXP];   // fold sequence
   __shared__ int s_err;
 
+  CM_TRACE(P, lr, b, 0);
   if (tid == 0) {
     s_epoch = ctrl->epoch + 1;
     s_err = 0;
@@ -485,6 +500,7 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
     multi_copy<D, MP>(s_cr, s_ncr, s_vr);
   }
   __syncthreads();
+  CM_TRACE(P, lr, b, 1);
 
   // 2. publish my record to every peer, then collect theirs
   if (tid < p) {
@@ -505,6 +521,7 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
     }
   }
   __syncthreads();
+  CM_TRACE(P, lr, b, 2);
   if (s_err) goto finish;
 
   // 3. reduce my segment (RS) — or the whole vector (one-shot)
@@ -542,6 +559,7 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
   }
 
   // 4. RS -> AG barrier (per CTA index) and 5. allgather
+  CM_TRACE(P, lr, b, 3);
   if (P.phases & PH_AG) {
     if (!ag_only) {
       __syncthreads();
@@ -549,6 +567,7 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
       if (tid < p && !wait_geq(mid_slot(myheap, b, tid), e, P.timeout_cycles))
         atomicExch(&s_err, ERR_TRANSPORT);
       __syncthreads();
+      CM_TRACE(P, lr, b, 4);
       if (s_err) goto finish;
     }
     // pull slice b of every other segment from all peers concurrently
@@ -569,6 +588,7 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
 
 finish:
   __syncthreads();
+  CM_TRACE(P, lr, b, 5);
   if (tid == 0) {
     if (s_err) *reinterpret_cast<volatile unsigned*>(P.herr) = (unsigned)s_err;
     __threadfence();
@@ -657,6 +677,7 @@ __global__ void __launch_bounds__(THREADS) ll_kernel(const __grid_constant__ Col
   const long long nunits = (nbytes + 7) / 8;
   const long long u0 = nunits * b / nb, u1 = nunits * (b + 1) / nb;
   // prestaged input (fused pack) lives in staging[parity]
+  CM_TRACE(P, lr, b, 0);
   const char* in = P.srcmode == SRC_PRESTAGED
                        ? myheap + STAGING_OFF + (long long)par * P.staging_bytes
                        : P.in[lr];
@@ -694,6 +715,7 @@ __global__ void __launch_bounds__(THREADS) ll_kernel(const __grid_constant__ Col
     }
   }
   __syncthreads();
+  CM_TRACE(P, lr, b, 2);
   if (s_err) goto ll_finish;
   // read + fold phase
   for (long long u = u0 + tid; u < u1; u += blockDim.x) {
@@ -730,6 +752,8 @@ __global__ void __launch_bounds__(THREADS) ll_kernel(const __grid_constant__ Col
   }
 ll_finish:
   __syncthreads();
+  CM_TRACE(P, lr, b, 5);
+  CM_TRACE(P, lr, b, 5);
   if (tid == 0) {
     if (s_err) *reinterpret_cast<volatile unsigned*>(P.herr) = (unsigned)s_err;
     __threadfence();

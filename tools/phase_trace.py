@@ -1,0 +1,70 @@
+"""Per-phase device timing of one collective kernel (diagnostics).
+
+    torchrun --nproc-per-node N tools/phase_trace.py --bytes 524288 --algo ring_rsa
+
+Every CTA stamps %globaltimer at: start, copied-in, start barrier, reduced,
+mid barrier, end (cm_comm_set_trace). Prints, for rank 0, the median over
+CTAs of each phase duration (us) averaged over iterations.
+"""
+import argparse
+import ctypes as C
+import os
+import sys
+
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1810_11112_b200 as P  # noqa: E402
+from paper_1810_11112_b200 import _lib as L  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--bytes", type=int, default=524288)
+ap.add_argument("--algo", default="ring_rsa")
+ap.add_argument("--iters", type=int, default=20)
+ap.add_argument("--zc", action="store_true")
+ap.add_argument("--param", action="append", default=[])
+a = ap.parse_args()
+rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+local = int(os.environ.get("LOCAL_RANK", rank))
+torch.cuda.set_device(local)
+dist.init_process_group("gloo")
+comm = P.Communicator(staging_bytes=max(64 << 20, a.bytes * 2), pool_bytes=max(64 << 20, a.bytes * 2),
+                      blocking=False)
+for kv in a.param:
+    k, v = kv.split("=")
+    comm.set_param(k, int(v))
+n = a.bytes // 4
+x = comm.empty(n) if a.zc else torch.empty(n, device="cuda")
+x.normal_()
+y = torch.empty(n, device="cuda")
+ctas = 1024
+tr = torch.zeros(ctas * 8, dtype=torch.int64, device="cuda")
+L.check(L.lib.cm_comm_set_trace(comm._h, tr.data_ptr(), ctas))
+st = L.Stats()
+phases = ["copyin", "start_barrier", "reduce", "mid_barrier", "allgather"]
+acc = [0.0] * 5
+tot = 0.0
+for it in range(a.iters + 3):
+    tr.zero_()
+    dist.barrier()
+    L.check(L.lib.cm_allreduce(comm._h, x.data_ptr(), y.data_ptr(), n, 0, 0, L.ALGO[a.algo], 131072, 0,
+                               torch.cuda.current_stream().cuda_stream, C.byref(st)))
+    comm.synchronize()
+    t = tr.view(ctas, 8).cpu()
+    used = t[:, 0] > 0
+    t = t[used].double()
+    if it < 3:
+        continue
+    for k in range(5):
+        d = (t[:, k + 1] - t[:, k])
+        d = d[(t[:, k + 1] > 0) & (t[:, k] > 0)]
+        acc[k] += float(d.median()) / 1e3 if len(d) else 0.0
+    tot += float((t[:, 5].max() - t[:, 0].min())) / 1e3
+if rank == 0:
+    print(f"p={world} bytes={a.bytes} algo={a.algo} zc={a.zc} ctas={int(used.sum())} "
+          f"kernel span {tot / a.iters:.2f} us | " +
+          " ".join(f"{ph} {v / a.iters:.2f}" for ph, v in zip(phases, acc)), flush=True)
+L.check(L.lib.cm_comm_set_trace(comm._h, None, 0))
+comm.close()
+dist.destroy_process_group()
