@@ -43,6 +43,8 @@ struct cm_comm {
   int64_t oneshot_max_bytes = 256 * 1024;
   int64_t ll_max_bytes = 32 * 1024;           // one-shot via LL slots up to here
   int64_t ll_units_per_cta = 512;
+  int64_t ll2_max_bytes = -1;                 // two-shot via LL slots up to here (-1: p x 512 KiB)
+  int64_t ll2_units_per_cta = 512;
   int64_t oneshot_bytes_per_cta = 8 * 1024;
   int64_t twoshot_bytes_per_cta = 4 * 1024;
   int max_ctas = 148;
@@ -132,6 +134,26 @@ KFn pick_ll(int dtype, int op, int p, bool tree) {
   switch (dtype) {
 #define LLCASE(T, D) \
     case T: return op == CM_SUM ? pick_ll_mp<D, CM_SUM>(p, tree) : pick_ll_mp<D, CM_MAX>(p, tree);
+    LLCASE(CM_FLOAT32, F32)
+    LLCASE(CM_FLOAT64, F64)
+    LLCASE(CM_BFLOAT16, BF16)
+    LLCASE(CM_INT32, I32)
+    LLCASE(CM_INT64, I64)
+#undef LLCASE
+  }
+  return nullptr;
+}
+
+template <class D, int OP>
+KFn pick_ll2_mp(int p, bool tree) {
+  if (p <= 8) return tree ? ll2_kernel<D, OP, 8, true> : ll2_kernel<D, OP, 8, false>;
+  return tree ? ll2_kernel<D, OP, 16, true> : ll2_kernel<D, OP, 16, false>;
+}
+
+KFn pick_ll2(int dtype, int op, int p, bool tree) {
+  switch (dtype) {
+#define LLCASE(T, D) \
+    case T: return op == CM_SUM ? pick_ll2_mp<D, CM_SUM>(p, tree) : pick_ll2_mp<D, CM_MAX>(p, tree);
     LLCASE(CM_FLOAT32, F32)
     LLCASE(CM_FLOAT64, F64)
     LLCASE(CM_BFLOAT16, BF16)
@@ -239,14 +261,6 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
     P.seg_len[q] = len[q];
     maxseg = std::max(maxseg, len[q]);
   }
-  // staging capacity
-  const int64_t need = (L.srcmode == SRC_ZEROCOPY) ? (maxseg + SLICE_ALIGN) * (int64_t)sz
-                                                  : L.n * (int64_t)sz;
-  if (!L.ll && need > (int64_t)c->staging_bytes)
-    return fail(CM_ERR_CONFIG, "message of " + std::to_string(L.n * sz) + " B needs " +
-                                   std::to_string(need) + " B of staging; the communicator has " +
-                                   std::to_string(c->staging_bytes) +
-                                   " (raise staging_bytes or allocate the buffers with comm.alloc)");
   P.n = L.n;
   P.hdr = make_hdr(L.n, L.dtype, L.op, L.order, L.phases, L.oneshot, L.average, L.layout);
   P.timeout_cycles = c->timeout_cycles;
@@ -269,10 +283,26 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
   const int64_t work = L.oneshot ? L.n * (int64_t)sz : maxseg * (int64_t)sz;
   const int64_t per = L.oneshot ? c->oneshot_bytes_per_cta : c->twoshot_bytes_per_cta;
   int64_t nb = (work + per - 1) / per;
-  if (L.ll) nb = ((L.n * (int64_t)sz + 7) / 8 + c->ll_units_per_cta - 1) / c->ll_units_per_cta;
+  int ll = L.ll;
+  if (ll == 2 && (maxseg * (int64_t)sz + 7) / 8 > (int64_t)LL_SRC_UNITS) ll = 0;  // rhd segments > n/p
+  // staging capacity (LL kernels read the input directly unless it is prestaged)
+  {
+    const int64_t need = (L.srcmode == SRC_ZEROCOPY) ? (maxseg + SLICE_ALIGN) * (int64_t)sz
+                                                    : L.n * (int64_t)sz;
+    const bool uses_staging = ll == 0 || L.srcmode == SRC_PRESTAGED;
+    if (uses_staging && need > (int64_t)c->staging_bytes)
+      return fail(CM_ERR_CONFIG, "message of " + std::to_string(L.n * sz) + " B needs " +
+                                     std::to_string(need) + " B of staging; the communicator has " +
+                                     std::to_string(c->staging_bytes) +
+                                     " (raise staging_bytes or allocate the buffers with comm.alloc)");
+  }
+  if (ll == 1) nb = ((L.n * (int64_t)sz + 7) / 8 + c->ll_units_per_cta - 1) / c->ll_units_per_cta;
+  if (ll == 2) nb = ((maxseg * (int64_t)sz + 7) / 8 + c->ll2_units_per_cta - 1) / c->ll2_units_per_cta;
   nb = std::max<int64_t>(1, std::min<int64_t>(nb, std::min(c->max_ctas, MAXBLK)));
-  KFn k = L.ll ? pick_ll(L.dtype, L.op, p, L.order == ORD_TREE)
-               : pick_kernel(L.dtype, L.op, p, L.order == ORD_TREE);
+  const bool tree = L.order == ORD_TREE;
+  KFn k = ll == 1 ? pick_ll(L.dtype, L.op, p, tree)
+        : ll == 2 ? pick_ll2(L.dtype, L.op, p, tree)
+                    : pick_kernel(L.dtype, L.op, p, tree);
   if (!k) return fail(CM_ERR_SHAPE, "unsupported dtype");
   void* args[] = {&P};
   int64_t alg = 0;   // busBW bytes of this launch (nccl-tests convention)
@@ -295,7 +325,8 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
   if (!c->virt) {
     const int r = c->rank;
     int64_t in_bytes = 0;
-    if (L.ll) in_bytes = (int64_t)(p - 1) * ((L.n * (int64_t)sz + 7) / 8) * 16;
+    if (ll == 1) in_bytes = (int64_t)(p - 1) * ((L.n * (int64_t)sz + 7) / 8) * 16;
+    else if (ll == 2) in_bytes = 2 * (int64_t)(p - 1) * ((maxseg * (int64_t)sz + 7) / 8) * 16;
     else if (L.oneshot) in_bytes = (int64_t)(p - 1) * L.n * sz;
     else {
       if (L.phases & PH_RS) in_bytes += (int64_t)(p - 1) * len[r] * sz;
@@ -372,7 +403,14 @@ void plan_algo(cm_comm* c, int concrete, int64_t nbytes, Launch* L) {
     L->layout = CM_LAYOUT_RING;
   }
   L->phases = L->oneshot ? PH_RS : (PH_RS | PH_AG);
-  L->ll = (L->oneshot && nbytes <= c->ll_max_bytes) ? 1 : 0;
+  const int64_t ll2_max = c->ll2_max_bytes >= 0 ? c->ll2_max_bytes : (int64_t)c->size * (int64_t)LL_MAX_BYTES;
+  if (L->oneshot) {
+    L->ll = nbytes <= std::min<int64_t>(c->ll_max_bytes, LL_MAX_BYTES) ? 1 : 0;
+  } else {
+    // a segment of ceil(n/p) elements must fit one source's LL slot range
+    const int64_t seg_bytes = (nbytes + c->size - 1) / c->size + 8;
+    L->ll = (nbytes <= ll2_max && seg_bytes <= (int64_t)LL_MAX_BYTES) ? 2 : 0;
+  }
 }
 
 int do_allreduce(cm_comm* c, const void* const* sends, void* const* recvs, int64_t count,
@@ -675,6 +713,8 @@ int cm_comm_set_param(cm_comm_t* c, const char* key, int64_t value) {
   if (k == "oneshot_max_bytes") c->oneshot_max_bytes = value;
   else if (k == "ll_max_bytes") c->ll_max_bytes = std::min<int64_t>(value, (int64_t)LL_MAX_BYTES);
   else if (k == "ll_units_per_cta") c->ll_units_per_cta = value;
+  else if (k == "ll2_max_bytes") c->ll2_max_bytes = value;
+  else if (k == "ll2_units_per_cta") c->ll2_units_per_cta = value;
   else if (k == "oneshot_bytes_per_cta") c->oneshot_bytes_per_cta = value;
   else if (k == "twoshot_bytes_per_cta") c->twoshot_bytes_per_cta = value;
   else if (k == "max_ctas") c->max_ctas = (int)std::min<int64_t>(value, MAXBLK);
@@ -687,6 +727,8 @@ int cm_comm_get_param(cm_comm_t* c, const char* key, int64_t* value) {
   if (k == "oneshot_max_bytes") *value = c->oneshot_max_bytes;
   else if (k == "ll_max_bytes") *value = c->ll_max_bytes;
   else if (k == "ll_units_per_cta") *value = c->ll_units_per_cta;
+  else if (k == "ll2_max_bytes") *value = c->ll2_max_bytes;
+  else if (k == "ll2_units_per_cta") *value = c->ll2_units_per_cta;
   else if (k == "oneshot_bytes_per_cta") *value = c->oneshot_bytes_per_cta;
   else if (k == "twoshot_bytes_per_cta") *value = c->twoshot_bytes_per_cta;
   else if (k == "max_ctas") *value = c->max_ctas;

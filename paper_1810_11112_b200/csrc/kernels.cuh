@@ -47,10 +47,12 @@ constexpr size_t MID_OFF = REC_OFF + REC_SIZE;
 constexpr size_t MID_SIZE = (size_t)MAXBLK * MAXP * 8;
 // LL (low-latency) one-shot slots: every 16-byte unit carries 8 payload bytes
 // and two copies of the epoch flag, so data and "ready" arrive in one store
-constexpr size_t LL_MAX_BYTES = 64 * 1024;              // payload per rank per call
-constexpr size_t LL_UNITS = LL_MAX_BYTES / 8;
+// layout [parity][phase][src][unit]; phase 0 = one-shot / reduce-scatter,
+// phase 1 = allgather of the two-shot LL kernel
+constexpr size_t LL_SRC_UNITS = 64 * 1024;               // 512 KiB payload per source
+constexpr size_t LL_MAX_BYTES = LL_SRC_UNITS * 8;
 constexpr size_t LL_OFF = MID_OFF + MID_SIZE;
-constexpr size_t LL_SIZE = 2ull * MAXP * LL_UNITS * 16;
+constexpr size_t LL_SIZE = 2ull * 2 * MAXP * LL_SRC_UNITS * 16;
 constexpr size_t LLH_OFF = LL_OFF + LL_SIZE;            // per-CTA header units
 constexpr size_t LLH_SIZE = 2ull * MAXBLK * MAXP * 16;
 constexpr size_t HEAP_ALIGN = 2ull << 20;
@@ -621,8 +623,8 @@ __device__ __forceinline__ uint4 ld_ll(const void* p) {
                : "memory");
   return v;
 }
-__device__ __forceinline__ char* ll_slot(char* heap, int par, int src, long long u) {
-  return heap + LL_OFF + (((size_t)par * MAXP + src) * LL_UNITS + (size_t)u) * 16;
+__device__ __forceinline__ char* ll_slot(char* heap, int par, int phase, int src, long long u) {
+  return heap + LL_OFF + ((((size_t)par * 2 + phase) * MAXP + src) * LL_SRC_UNITS + (size_t)u) * 16;
 }
 __device__ __forceinline__ char* llh_slot(char* heap, int par, int blk, int src) {
   return heap + LLH_OFF + (((size_t)par * MAXBLK + blk) * MAXP + src) * 16;
@@ -703,7 +705,7 @@ __global__ void __launch_bounds__(THREADS) ll_kernel(const __grid_constant__ Col
     }
 #pragma unroll
     for (int q = 0; q < MP; ++q)
-      if (q < p) st_ll(ll_slot(P.heap[q], par, rank, u), w0, w1, flag);
+      if (q < p) st_ll(ll_slot(P.heap[q], par, 0, rank, u), w0, w1, flag);
   }
   // header check before trusting the unit count
   if (tid < p) {
@@ -725,7 +727,7 @@ __global__ void __launch_bounds__(THREADS) ll_kernel(const __grid_constant__ Col
     for (int k = 0; k < MP; ++k) {
       if (k < p) {
         uint4 x;
-        if (!ll_wait(ll_slot(myheap, par, s_seq[k], u), flag, P.timeout_cycles, &x)) {
+        if (!ll_wait(ll_slot(myheap, par, 0, s_seq[k], u), flag, P.timeout_cycles, &x)) {
           ok = false;
           x = make_uint4(0, 0, 0, 0);
         }
@@ -753,6 +755,171 @@ __global__ void __launch_bounds__(THREADS) ll_kernel(const __grid_constant__ Col
 ll_finish:
   __syncthreads();
   CM_TRACE(P, lr, b, 5);
+  CM_TRACE(P, lr, b, 5);
+  if (tid == 0) {
+    if (s_err) *reinterpret_cast<volatile unsigned*>(P.herr) = (unsigned)s_err;
+    __threadfence();
+    const unsigned old = atomicAdd(&ctrl->done, 1u);
+    if (old == (unsigned)nb - 1) {
+      ctrl->done = 0;
+      ctrl->epoch = e;
+      __threadfence();
+    }
+  }
+}
+
+// ---- LL two-shot (medium messages) ----------------------------------------------
+// reduce-scatter by PUSH: every rank writes unit u of segment q of its input
+// into the owner q's LL slot [par][0][src][u]; the owner polls its own heap,
+// folds the p sources in the reference order (ring rotation or RHD tree) and
+// pushes the reduced unit to every peer's slot [par][1][owner][u]; readers
+// poll locally and write their output. No barriers and no fences: every
+// 16-byte unit carries its own epoch flags, so each hop costs one posted
+// NVLink store plus a local poll.
+template <class D>
+__device__ __forceinline__ uint2 pack_elems(const char* base, long long i, int cnt) {
+  using S = typename D::S;
+  constexpr int E = 8 / sizeof(S);
+  union { uint2 u; S s[E]; } w;
+  w.u = make_uint2(0, 0);
+  const S* src = reinterpret_cast<const S*>(base) + i;
+#pragma unroll
+  for (int t = 0; t < E; ++t)
+    if (t < cnt) w.s[t] = src[t];
+  return w.u;
+}
+
+template <class D>
+__device__ __forceinline__ void unpack_elems(char* base, long long i, int cnt, uint2 v) {
+  using S = typename D::S;
+  constexpr int E = 8 / sizeof(S);
+  union { uint2 u; S s[E]; } w;
+  w.u = v;
+  S* dst = reinterpret_cast<S*>(base) + i;
+#pragma unroll
+  for (int t = 0; t < E; ++t)
+    if (t < cnt) dst[t] = w.s[t];
+}
+
+template <class D, int OP, int MP, bool TREE>
+__global__ void __launch_bounds__(THREADS) ll2_kernel(const __grid_constant__ CollParams P) {
+  using S = typename D::S;
+  using A = typename D::A;
+  constexpr int E = 8 / sizeof(S);
+  const int lr = P.virt ? blockIdx.y : 0;
+  const int rank = P.virt ? (int)blockIdx.y : P.rank;
+  const int b = blockIdx.x, nb = gridDim.x, p = P.p, tid = threadIdx.x, bd = blockDim.x;
+  char* myheap = P.heap[rank];
+  Ctrl* ctrl = reinterpret_cast<Ctrl*>(myheap + CTRL_OFF);
+  __shared__ unsigned long long s_epoch;
+  __shared__ int s_err;
+  __shared__ int s_seq[MAXP];
+  CM_TRACE(P, lr, b, 0);
+  if (tid == 0) {
+    s_epoch = ctrl->epoch + 1;
+    s_err = 0;
+  }
+  int m = 1;
+  while ((m << 1) <= p) m <<= 1;
+  const int excess = p - m;
+  if (tid < p) {
+    int src;
+    if (P.order == ORD_TREE) src = tid < m ? (tid < excess ? 2 * tid : tid + excess) : 2 * (tid - m) + 1;
+    else if (P.order == ORD_RING) src = ((rank - 1 - tid) % p + p) % p;   // x_{r-1}, ..., x_r
+    else src = tid;
+    s_seq[tid] = src;
+  }
+  __syncthreads();
+  const unsigned long long e = s_epoch;
+  const int par = (int)(e & 1);
+  const unsigned flag = (unsigned)(e & 0x7fffffffu) | 0x80000000u;
+  const char* in = P.srcmode == SRC_PRESTAGED
+                       ? myheap + STAGING_OFF + (long long)par * P.staging_bytes
+                       : P.in[lr];
+  char* out = P.out[lr];
+
+  if (tid < p) st_ll(llh_slot(P.heap[tid], par, b, rank), (unsigned)P.hdr, (unsigned)(P.hdr >> 32), flag);
+  // 1. push slice b of every segment to its owner
+  for (int i = 0; i < p; ++i) {
+    const int q = (rank + 1 + i) % p;               // spread the first stores over peers
+    const long long so = P.seg_off[q], sl = P.seg_len[q];
+    const long long nu = (sl + E - 1) / E;
+    const long long u0 = nu * b / nb, u1 = nu * (b + 1) / nb;
+    char* dst = P.heap[q];
+    for (long long u = u0 + tid; u < u1; u += bd) {
+      const long long el = u * E;
+      const int cnt = (int)((sl - el) < E ? (sl - el) : E);
+      const uint2 w = pack_elems<D>(in, so + el, cnt);
+      st_ll(ll_slot(dst, par, 0, rank, u), w.x, w.y, flag);
+    }
+  }
+  if (tid < p) {
+    uint4 h;
+    if (!ll_wait(llh_slot(myheap, par, b, tid), flag, P.timeout_cycles, &h)) atomicExch(&s_err, ERR_TRANSPORT);
+    else if (((unsigned long long)h.z << 32 | h.x) != P.hdr) atomicExch(&s_err, ERR_SHAPE);
+  }
+  __syncthreads();
+  CM_TRACE(P, lr, b, 2);
+  if (s_err) goto ll2_finish;
+  {
+    // 2. reduce my segment, write it and push it to every peer
+    const long long so = P.seg_off[rank], sl = P.seg_len[rank];
+    const long long nu = (sl + E - 1) / E;
+    const long long u0 = nu * b / nb, u1 = nu * (b + 1) / nb;
+    for (long long u = u0 + tid; u < u1; u += bd) {
+      A v[MP][E];
+      bool ok = true;
+#pragma unroll
+      for (int k = 0; k < MP; ++k) {
+        if (k < p) {
+          uint4 x;
+          if (!ll_wait(ll_slot(myheap, par, 0, s_seq[k], u), flag, P.timeout_cycles, &x)) {
+            ok = false;
+            x = make_uint4(0, 0, 0, 0);
+          }
+          union { uint2 u; S s[E]; } w;
+          w.u = make_uint2(x.x, x.z);
+#pragma unroll
+          for (int t = 0; t < E; ++t) v[k][t] = to_acc<D>(w.s[t]);
+        }
+      }
+      if (!ok) {
+        atomicExch(&s_err, ERR_TRANSPORT);
+        break;
+      }
+      fold<OP, MP, E, TREE>(v, p, m, excess);
+      union { uint2 u; S s[E]; } r;
+#pragma unroll
+      for (int t = 0; t < E; ++t) r.s[t] = from_acc<D>(P.average ? div_p<A>(v[0][t], p) : v[0][t]);
+      const long long el = u * E;
+      const int cnt = (int)((sl - el) < E ? (sl - el) : E);
+      for (int i = 1; i < p; ++i) {
+        const int q = (rank + i) % p;
+        st_ll(ll_slot(P.heap[q], par, 1, rank, u), r.u.x, r.u.y, flag);
+      }
+      unpack_elems<D>(out, so + el, cnt, r.u);
+    }
+    CM_TRACE(P, lr, b, 3);
+    // 3. collect every other segment
+    for (int i = 1; i < p; ++i) {
+      const int q = (rank + i) % p;
+      const long long qo = P.seg_off[q], ql = P.seg_len[q];
+      const long long qn = (ql + E - 1) / E;
+      const long long q0 = qn * b / nb, q1 = qn * (b + 1) / nb;
+      for (long long u = q0 + tid; u < q1; u += bd) {
+        uint4 x;
+        if (!ll_wait(ll_slot(myheap, par, 1, q, u), flag, P.timeout_cycles, &x)) {
+          atomicExch(&s_err, ERR_TRANSPORT);
+          break;
+        }
+        const long long el = u * E;
+        const int cnt = (int)((ql - el) < E ? (ql - el) : E);
+        unpack_elems<D>(out, qo + el, cnt, make_uint2(x.x, x.z));
+      }
+    }
+  }
+ll2_finish:
+  __syncthreads();
   CM_TRACE(P, lr, b, 5);
   if (tid == 0) {
     if (s_err) *reinterpret_cast<volatile unsigned*>(P.herr) = (unsigned)s_err;
