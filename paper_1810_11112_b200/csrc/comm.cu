@@ -40,7 +40,7 @@ struct cm_comm {
   int64_t* agree_dev = nullptr;        // device: cm_agree in/out
   int sms = 148;
   // tuning knobs (cm_comm_set_param)
-  int64_t oneshot_max_bytes = 256 * 1024;
+  int64_t oneshot_max_bytes = 32 * 1024;
   int64_t ll_max_bytes = 32 * 1024;           // one-shot via LL slots up to here
   int64_t ll_units_per_cta = 512;
   int64_t ll2_max_bytes = -1;                 // two-shot via LL slots up to here (-1: p x 512 KiB)
