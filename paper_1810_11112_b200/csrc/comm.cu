@@ -26,6 +26,8 @@ struct cm_comm {
   int rank = 0, size = 1, device = 0;
   bool virt = false;
   size_t staging_bytes = 0, pool_bytes = 0, heap_bytes = 0;
+  size_t staging_off = 0;           // runtime heap layout (after the LL region)
+  int64_t ll_units = 0;             // LL units per (parity, phase, source)
   char* local = nullptr;            // own heap (virtual: all vranks' heaps)
   char* heap[MAXP] = {};
   bool connected = false;
@@ -77,6 +79,11 @@ int cuda_fail(cudaError_t e, const char* what) {
   } while (0)
 
 size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// LL payload capacity per source: 2 MiB on real communicators (two-shot LL up
+// to p x 2 MiB), 256 KiB per virtual rank (single-GPU emulation)
+constexpr int64_t CM_LL_UNITS_REAL = 256 * 1024;
+constexpr int64_t CM_LL_UNITS_VIRTUAL = 32 * 1024;
 
 cudaEvent_t take_event(cm_comm* c) {
   if (!c->event_pool.empty()) {
@@ -207,7 +214,7 @@ int classify(cm_comm* c, const void* ptr, int* kind) {
 bool in_pool(cm_comm* c, const void* ptr, int64_t bytes) {
   if (c->virt || !c->local) return false;
   const char* p = static_cast<const char*>(ptr);
-  const char* lo = c->local + STAGING_OFF + 2 * c->staging_bytes;
+  const char* lo = c->local + c->staging_off + 2 * c->staging_bytes;
   return p >= lo && p + bytes <= c->local + c->heap_bytes;
 }
 
@@ -276,6 +283,8 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
   P.out_rel = L.out_rel;
   P.ag_in_rel = L.ag_in_rel;
   P.average = L.average;
+  P.staging_off = (long long)c->staging_off;
+  P.ll_units = c->ll_units;
   P.trace = c->trace;
   P.trace_ctas = c->trace_ctas;
 
@@ -284,7 +293,8 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
   const int64_t per = L.oneshot ? c->oneshot_bytes_per_cta : c->twoshot_bytes_per_cta;
   int64_t nb = (work + per - 1) / per;
   int ll = L.ll;
-  if (ll == 2 && (maxseg * (int64_t)sz + 7) / 8 > (int64_t)LL_SRC_UNITS) ll = 0;  // rhd segments > n/p
+  if (ll == 1 && (L.n * (int64_t)sz + 7) / 8 > c->ll_units) ll = 0;
+  if (ll == 2 && (maxseg * (int64_t)sz + 7) / 8 > c->ll_units) ll = 0;  // rhd segments > n/p
   // staging capacity (LL kernels read the input directly unless it is prestaged)
   {
     const int64_t need = (L.srcmode == SRC_ZEROCOPY) ? (maxseg + SLICE_ALIGN) * (int64_t)sz
@@ -403,13 +413,14 @@ void plan_algo(cm_comm* c, int concrete, int64_t nbytes, Launch* L) {
     L->layout = CM_LAYOUT_RING;
   }
   L->phases = L->oneshot ? PH_RS : (PH_RS | PH_AG);
-  const int64_t ll2_max = c->ll2_max_bytes >= 0 ? c->ll2_max_bytes : (int64_t)c->size * (int64_t)LL_MAX_BYTES;
+  const int64_t cap = c->ll_units * 8;      // LL payload bytes per source
+  const int64_t ll2_max = c->ll2_max_bytes >= 0 ? c->ll2_max_bytes : (int64_t)c->size * cap;
   if (L->oneshot) {
-    L->ll = nbytes <= std::min<int64_t>(c->ll_max_bytes, LL_MAX_BYTES) ? 1 : 0;
+    L->ll = nbytes <= std::min<int64_t>(c->ll_max_bytes, cap) ? 1 : 0;
   } else {
     // a segment of ceil(n/p) elements must fit one source's LL slot range
     const int64_t seg_bytes = (nbytes + c->size - 1) / c->size + 8;
-    L->ll = (nbytes <= ll2_max && seg_bytes <= (int64_t)LL_MAX_BYTES) ? 2 : 0;
+    L->ll = (nbytes <= ll2_max && seg_bytes <= cap) ? 2 : 0;
   }
 }
 
@@ -561,6 +572,7 @@ int launch_batched_copy(cm_comm* c, int n, const void* const* srcs, void* const*
     if (c) {
       P.heap = c->local;
       P.staging_bytes = (long long)c->staging_bytes;
+      P.staging_off = (long long)c->staging_off;
     }
     int64_t nb = (P.start[m] + (128 << 10) - 1) / (128 << 10);
     nb = std::max<int64_t>(1, std::min<int64_t>(nb, 148 * 4));
@@ -589,7 +601,9 @@ int cm_comm_create(int rank, int size, int device, int64_t staging_bytes, int64_
   c->device = device;
   c->staging_bytes = round_up(std::max<int64_t>(staging_bytes, 1), HEAP_ALIGN);
   c->pool_bytes = round_up((size_t)pool_bytes, HEAP_ALIGN);
-  c->heap_bytes = STAGING_OFF + 2 * c->staging_bytes + c->pool_bytes;
+  c->ll_units = CM_LL_UNITS_REAL;
+  c->staging_off = round_up(LL_OFF + 4 * (size_t)size * (size_t)c->ll_units * 16, HEAP_ALIGN);
+  c->heap_bytes = c->staging_off + 2 * c->staging_bytes + c->pool_bytes;
   c->reg.policy = CM_LAZY_CACHE;
   c->reg.simulated = false;
   cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
@@ -603,7 +617,7 @@ int cm_comm_create(int rank, int size, int device, int64_t staging_bytes, int64_
   if (e != cudaSuccess) { cm_comm_destroy(c); return cuda_fail(e, "cm_comm_create"); }
   *c->herr_host = 0;
   c->heap[rank] = c->local;
-  if (c->pool_bytes) c->pool_free[STAGING_OFF + 2 * c->staging_bytes] = c->pool_bytes;
+  if (c->pool_bytes) c->pool_free[c->staging_off + 2 * c->staging_bytes] = c->pool_bytes;
   if (size == 1) c->connected = true;
   *out = c;
   return CM_OK;
@@ -643,7 +657,9 @@ int cm_comm_create_virtual(int size, int device, int64_t staging_bytes, cm_comm_
   c->size = size;
   c->device = device;
   c->staging_bytes = round_up(std::max<int64_t>(staging_bytes, 1), HEAP_ALIGN);
-  c->heap_bytes = STAGING_OFF + 2 * c->staging_bytes;
+  c->ll_units = CM_LL_UNITS_VIRTUAL;
+  c->staging_off = round_up(LL_OFF + 4 * (size_t)size * (size_t)c->ll_units * 16, HEAP_ALIGN);
+  c->heap_bytes = c->staging_off + 2 * c->staging_bytes;
   c->reg.policy = CM_LAZY_CACHE;
   c->reg.simulated = false;
   cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
@@ -711,7 +727,7 @@ int cm_comm_set_param(cm_comm_t* c, const char* key, int64_t value) {
   const std::string k(key);
   if (value <= 0) return fail(CM_ERR_VALUE, "parameter must be positive");
   if (k == "oneshot_max_bytes") c->oneshot_max_bytes = value;
-  else if (k == "ll_max_bytes") c->ll_max_bytes = std::min<int64_t>(value, (int64_t)LL_MAX_BYTES);
+  else if (k == "ll_max_bytes") c->ll_max_bytes = value;
   else if (k == "ll_units_per_cta") c->ll_units_per_cta = value;
   else if (k == "ll2_max_bytes") c->ll2_max_bytes = value;
   else if (k == "ll2_units_per_cta") c->ll2_units_per_cta = value;
@@ -733,6 +749,7 @@ int cm_comm_get_param(cm_comm_t* c, const char* key, int64_t* value) {
   else if (k == "twoshot_bytes_per_cta") *value = c->twoshot_bytes_per_cta;
   else if (k == "max_ctas") *value = c->max_ctas;
   else if (k == "staging_bytes") *value = (int64_t)c->staging_bytes;
+  else if (k == "ll_payload_per_source") *value = c->ll_units * 8;
   else if (k == "pool_bytes") *value = (int64_t)c->pool_bytes;
   else return fail(CM_ERR_CONFIG, "unknown parameter " + k);
   return CM_OK;

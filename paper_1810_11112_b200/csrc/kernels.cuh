@@ -45,19 +45,16 @@ constexpr size_t REC_BYTES = 32;
 constexpr size_t REC_SIZE = 2ull * MAXBLK * MAXP * REC_BYTES;
 constexpr size_t MID_OFF = REC_OFF + REC_SIZE;
 constexpr size_t MID_SIZE = (size_t)MAXBLK * MAXP * 8;
-// LL (low-latency) one-shot slots: every 16-byte unit carries 8 payload bytes
-// and two copies of the epoch flag, so data and "ready" arrive in one store
-// layout [parity][phase][src][unit]; phase 0 = one-shot / reduce-scatter,
-// phase 1 = allgather of the two-shot LL kernel
-constexpr size_t LL_SRC_UNITS = 64 * 1024;               // 512 KiB payload per source
-constexpr size_t LL_MAX_BYTES = LL_SRC_UNITS * 8;
-constexpr size_t LL_OFF = MID_OFF + MID_SIZE;
-constexpr size_t LL_SIZE = 2ull * 2 * MAXP * LL_SRC_UNITS * 16;
-constexpr size_t LLH_OFF = LL_OFF + LL_SIZE;            // per-CTA header units
+// LL (low-latency) slots: every 16-byte unit carries 8 payload bytes and two
+// copies of the epoch flag, so data and "ready" arrive in one store. Layout
+// [parity][phase][src < p][unit < ll_units] starting at LL_OFF; its size
+// depends on p and is chosen at communicator creation, so staging starts at a
+// runtime offset (CollParams::staging_off).
+constexpr size_t LLH_OFF = MID_OFF + MID_SIZE;          // per-CTA LL header units
 constexpr size_t LLH_SIZE = 2ull * MAXBLK * MAXP * 16;
 constexpr size_t HEAP_ALIGN = 2ull << 20;
-constexpr size_t CTRL_REGION = ((LLH_OFF + LLH_SIZE + HEAP_ALIGN - 1) / HEAP_ALIGN) * HEAP_ALIGN;
-constexpr size_t STAGING_OFF = CTRL_REGION;
+constexpr size_t LL_OFF = ((LLH_OFF + LLH_SIZE + HEAP_ALIGN - 1) / HEAP_ALIGN) * HEAP_ALIGN;
+constexpr size_t CTRL_REGION = LL_OFF;                  // zeroed at creation
 
 struct Ctrl {
   unsigned long long epoch;  // calls completed by this rank
@@ -99,6 +96,8 @@ struct CollParams {
   int out_rel;               // RS writes out[i - seg_off] (reduce_scatter API)
   int ag_in_rel;             // AG-only: `in` holds only my segment (in[i - seg_off])
   int average;               // divide the reduced value by p (aggregate mean)
+  long long staging_off;     // heap offset of staging[0]
+  long long ll_units;        // LL units per (parity, phase, source)
   unsigned long long* trace; // optional: per-CTA phase timestamps (globaltimer ns)
   int trace_ctas;
 };
@@ -452,7 +451,7 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
   __syncthreads();
   const unsigned long long e = s_epoch;
   const int par = (int)(e & 1);
-  const long long stage_off = (long long)STAGING_OFF + (long long)par * P.staging_bytes;
+  const long long stage_off = P.staging_off + (long long)par * P.staging_bytes;
   const char* in = P.in[lr];
   char* out = P.out[lr];
   const bool ag_only = !(P.phases & PH_RS);
@@ -623,9 +622,8 @@ __device__ __forceinline__ uint4 ld_ll(const void* p) {
                : "memory");
   return v;
 }
-__device__ __forceinline__ char* ll_slot(char* heap, int par, int phase, int src, long long u) {
-  return heap + LL_OFF + ((((size_t)par * 2 + phase) * MAXP + src) * LL_SRC_UNITS + (size_t)u) * 16;
-}
+#define LLSLOT(heap, par, phase, src, u) \
+  ((heap) + LL_OFF + ((((size_t)(par) * 2 + (phase)) * P.p + (src)) * (size_t)P.ll_units + (size_t)(u)) * 16)
 __device__ __forceinline__ char* llh_slot(char* heap, int par, int blk, int src) {
   return heap + LLH_OFF + (((size_t)par * MAXBLK + blk) * MAXP + src) * 16;
 }
@@ -681,7 +679,7 @@ __global__ void __launch_bounds__(THREADS) ll_kernel(const __grid_constant__ Col
   // prestaged input (fused pack) lives in staging[parity]
   CM_TRACE(P, lr, b, 0);
   const char* in = P.srcmode == SRC_PRESTAGED
-                       ? myheap + STAGING_OFF + (long long)par * P.staging_bytes
+                       ? myheap + P.staging_off + (long long)par * P.staging_bytes
                        : P.in[lr];
   char* out = P.out[lr];
 
@@ -705,7 +703,7 @@ __global__ void __launch_bounds__(THREADS) ll_kernel(const __grid_constant__ Col
     }
 #pragma unroll
     for (int q = 0; q < MP; ++q)
-      if (q < p) st_ll(ll_slot(P.heap[q], par, 0, rank, u), w0, w1, flag);
+      if (q < p) st_ll(LLSLOT(P.heap[q], par, 0, rank, u), w0, w1, flag);
   }
   // header check before trusting the unit count
   if (tid < p) {
@@ -727,7 +725,7 @@ __global__ void __launch_bounds__(THREADS) ll_kernel(const __grid_constant__ Col
     for (int k = 0; k < MP; ++k) {
       if (k < p) {
         uint4 x;
-        if (!ll_wait(ll_slot(myheap, par, 0, s_seq[k], u), flag, P.timeout_cycles, &x)) {
+        if (!ll_wait(LLSLOT(myheap, par, 0, s_seq[k], u), flag, P.timeout_cycles, &x)) {
           ok = false;
           x = make_uint4(0, 0, 0, 0);
         }
@@ -834,7 +832,7 @@ __global__ void __launch_bounds__(THREADS) ll2_kernel(const __grid_constant__ Co
   const int par = (int)(e & 1);
   const unsigned flag = (unsigned)(e & 0x7fffffffu) | 0x80000000u;
   const char* in = P.srcmode == SRC_PRESTAGED
-                       ? myheap + STAGING_OFF + (long long)par * P.staging_bytes
+                       ? myheap + P.staging_off + (long long)par * P.staging_bytes
                        : P.in[lr];
   char* out = P.out[lr];
 
@@ -850,7 +848,7 @@ __global__ void __launch_bounds__(THREADS) ll2_kernel(const __grid_constant__ Co
       const long long el = u * E;
       const int cnt = (int)((sl - el) < E ? (sl - el) : E);
       const uint2 w = pack_elems<D>(in, so + el, cnt);
-      st_ll(ll_slot(dst, par, 0, rank, u), w.x, w.y, flag);
+      st_ll(LLSLOT(dst, par, 0, rank, u), w.x, w.y, flag);
     }
   }
   if (tid < p) {
@@ -873,7 +871,7 @@ __global__ void __launch_bounds__(THREADS) ll2_kernel(const __grid_constant__ Co
       for (int k = 0; k < MP; ++k) {
         if (k < p) {
           uint4 x;
-          if (!ll_wait(ll_slot(myheap, par, 0, s_seq[k], u), flag, P.timeout_cycles, &x)) {
+          if (!ll_wait(LLSLOT(myheap, par, 0, s_seq[k], u), flag, P.timeout_cycles, &x)) {
             ok = false;
             x = make_uint4(0, 0, 0, 0);
           }
@@ -895,7 +893,7 @@ __global__ void __launch_bounds__(THREADS) ll2_kernel(const __grid_constant__ Co
       const int cnt = (int)((sl - el) < E ? (sl - el) : E);
       for (int i = 1; i < p; ++i) {
         const int q = (rank + i) % p;
-        st_ll(ll_slot(P.heap[q], par, 1, rank, u), r.u.x, r.u.y, flag);
+        st_ll(LLSLOT(P.heap[q], par, 1, rank, u), r.u.x, r.u.y, flag);
       }
       unpack_elems<D>(out, so + el, cnt, r.u);
     }
@@ -908,7 +906,7 @@ __global__ void __launch_bounds__(THREADS) ll2_kernel(const __grid_constant__ Co
       const long long q0 = qn * b / nb, q1 = qn * (b + 1) / nb;
       for (long long u = q0 + tid; u < q1; u += bd) {
         uint4 x;
-        if (!ll_wait(ll_slot(myheap, par, 1, q, u), flag, P.timeout_cycles, &x)) {
+        if (!ll_wait(LLSLOT(myheap, par, 1, q, u), flag, P.timeout_cycles, &x)) {
           atomicExch(&s_err, ERR_TRANSPORT);
           break;
         }
@@ -943,6 +941,7 @@ struct CopyParams {
   int staged;                  // dst is relative to own staging[(epoch+1)&1]
   char* heap;
   long long staging_bytes;
+  long long staging_off;
 };
 
 __global__ void __launch_bounds__(THREADS) batched_copy_kernel(const __grid_constant__ CopyParams P) {
@@ -955,7 +954,7 @@ __global__ void __launch_bounds__(THREADS) batched_copy_kernel(const __grid_cons
   if (P.staged) {
     const Ctrl* ctrl = reinterpret_cast<const Ctrl*>(P.heap + CTRL_OFF);
     const unsigned long long e = ctrl->epoch + 1;
-    base = P.heap + STAGING_OFF + (long long)(e & 1) * P.staging_bytes;
+    base = P.heap + P.staging_off + (long long)(e & 1) * P.staging_bytes;
   }
   // find the first member overlapping [lo, hi)
   int k = 0;
