@@ -231,6 +231,10 @@ int cm_local_reduce(const void* a, const void* b, void* out, int64_t count, int 
  * n (src, dst, bytes) triples */
 int cm_batched_copy(int n, const void* const* srcs, void* const* dsts, const int64_t* nbytes,
                     void* stream);
+/* diagnostics: all-to-all NVLink bandwidth, mode 0 = every rank pulls `bytes`
+ * from each peer, 1 = every rank pushes `bytes` to each peer; ms per round */
+int cm_bench_p2p(cm_comm_t* comm, int mode, int64_t bytes, int ctas, int iters, void* stream,
+                 double* ms_per_iter);
 /* device-timed loop of cm_allreduce (CUDA events on `stream`), ms per call */
 int cm_time_allreduce(cm_comm_t* comm, const void* send, void* recv, int64_t count, int dtype,
                       int op, int algo, int64_t switch_bytes, int iters, int warmup,

@@ -106,6 +106,7 @@ _SIGS = {
     "cm_allgather_v": ([_vp, _P(_vp), _P(_vp), _i64, _i, _i, _vp, _P(Stats)], _i),
     "cm_local_reduce": ([_vp, _vp, _vp, _i64, _i, _i, _vp], _i),
     "cm_batched_copy": ([_i, _P(_vp), _P(_vp), _P(_i64), _vp], _i),
+    "cm_bench_p2p": ([_vp, _i, _i64, _i, _i, _vp, _P(C.c_double)], _i),
     "cm_time_allreduce": ([_vp, _vp, _vp, _i64, _i, _i, _i, _i64, _i, _i, _vp,
                            _P(C.c_double)], _i),
 }

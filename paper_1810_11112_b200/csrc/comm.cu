@@ -1046,6 +1046,33 @@ int cm_batched_copy(int n, const void* const* srcs, void* const* dsts, const int
   return launch_batched_copy(nullptr, n, srcs, dsts, nbytes, false, static_cast<cudaStream_t>(stream));
 }
 
+int cm_bench_p2p(cm_comm_t* c, int mode, int64_t bytes, int ctas, int iters, void* stream_,
+                 double* ms_per_iter) {
+  if (c->virt || c->size < 2) return fail(CM_ERR_UNSUPPORTED, "needs a real group of >= 2 ranks");
+  if ((int64_t)bytes * c->size > (int64_t)c->staging_bytes) return fail(CM_ERR_CONFIG, "bytes too large");
+  cudaStream_t s = static_cast<cudaStream_t>(stream_);
+  CollParams P;
+  memset(&P, 0, sizeof P);
+  for (int q = 0; q < c->size; ++q) P.heap[q] = c->heap[q];
+  P.p = c->size;
+  P.rank = c->rank;
+  P.staging_off = (long long)c->staging_off;
+  cudaEvent_t e0, e1;
+  CUDA_TRY(cudaEventCreate(&e0));
+  CUDA_TRY(cudaEventCreate(&e1));
+  p2p_bw_kernel<<<ctas, THREADS, 0, s>>>(P, mode, bytes);
+  CUDA_TRY(cudaEventRecord(e0, s));
+  for (int i = 0; i < iters; ++i) p2p_bw_kernel<<<ctas, THREADS, 0, s>>>(P, mode, bytes);
+  CUDA_TRY(cudaEventRecord(e1, s));
+  CUDA_TRY(cudaEventSynchronize(e1));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  *ms_per_iter = ms / iters;
+  return CM_OK;
+}
+
 int cm_time_allreduce(cm_comm_t* c, const void* send, void* recv, int64_t count, int dtype, int op,
                       int algo, int64_t switch_bytes, int iters, int warmup, void* stream,
                       double* ms_per_call) {

@@ -931,6 +931,58 @@ ll2_finish:
   }
 }
 
+// ---- diagnostics: raw NVLink read / write bandwidth between all ranks --------
+// mode 0: pull — every rank reads `bytes` from each peer's staging into its own
+// mode 1: push — every rank writes `bytes` into each peer's staging
+// (all-to-all pattern of the two-shot phases; no synchronisation, data unused)
+__global__ void __launch_bounds__(THREADS) p2p_bw_kernel(const __grid_constant__ CollParams P, int mode,
+                                                         long long bytes) {
+  const int rank = P.rank, p = P.p, tid = threadIdx.x;
+  const long long nv = bytes / 16;
+  const long long per = (nv + gridDim.x - 1) / gridDim.x;
+  const long long v0 = per * blockIdx.x, v1 = min(nv, v0 + per);
+  char* mine = P.heap[rank] + P.staging_off;
+  if (mode >= 2) {  // all peers concurrently from every thread
+    const bool pull = mode == 2;
+    for (long long j = v0 + tid; j < v1; j += THREADS) {
+      uint4 v[MAXP];
+#pragma unroll
+      for (int i = 1; i < 8; ++i) {
+        if (i < p) {
+          const int q = (rank + i) % p;
+          const uint4* src = reinterpret_cast<const uint4*>(
+              pull ? P.heap[q] + P.staging_off + (long long)rank * bytes : mine + (long long)q * bytes);
+          v[i] = src[j];
+        }
+      }
+#pragma unroll
+      for (int i = 1; i < 8; ++i) {
+        if (i < p) {
+          const int q = (rank + i) % p;
+          uint4* dst = reinterpret_cast<uint4*>(pull ? mine + (long long)q * bytes
+                                                     : P.heap[q] + P.staging_off + (long long)rank * bytes);
+          dst[j] = v[i];
+        }
+      }
+    }
+    return;
+  }
+  for (int i = 1; i < p; ++i) {
+    const int q = (rank + i) % p;
+    char* peer = P.heap[q] + P.staging_off;
+    const uint4* src = reinterpret_cast<const uint4*>(mode == 0 ? peer + (long long)rank * bytes
+                                                                : mine + (long long)q * bytes);
+    uint4* dst = reinterpret_cast<uint4*>(mode == 0 ? mine + (long long)q * bytes
+                                                    : peer + (long long)rank * bytes);
+    long long j = v0 + tid;
+    for (; j + 3 * THREADS < v1; j += 4 * THREADS) {
+      uint4 a = src[j], b = src[j + THREADS], c = src[j + 2 * THREADS], d = src[j + 3 * THREADS];
+      dst[j] = a; dst[j + THREADS] = b; dst[j + 2 * THREADS] = c; dst[j + 3 * THREADS] = d;
+    }
+    for (; j < v1; j += THREADS) dst[j] = src[j];
+  }
+}
+
 // ---- batched copy (fusion pack / unfuse / cm_batched_copy) ---------------------
 constexpr int MAXCOPY = 128;
 struct CopyParams {
