@@ -278,20 +278,22 @@ def headline(args, rank, world, local):
     if not args.no_e2e:
         hgs = make_grads(args.model, rank, None, args.dtype, pinned=True)
         comm.blocking = True
+        r = None
         for _ in range(2):
-            P.aggregate(hgs, group, comm, algo=args.algo, cfg=cfg, switch_bytes=args.switch)
+            r = P.aggregate(hgs, group, comm, algo=args.algo, cfg=cfg, switch_bytes=args.switch, out=r)
         barrier(world)
         k = max(3, min(args.steps, 20))
         t0 = time.perf_counter()
         for _ in range(k):
-            r = P.aggregate(hgs, group, comm, algo=args.algo, cfg=cfg, switch_bytes=args.switch)
+            r = P.aggregate(hgs, group, comm, algo=args.algo, cfg=cfg, switch_bytes=args.switch, out=r)
         torch.cuda.synchronize()
         e2e_ms = max_over_ranks((time.perf_counter() - t0) / k * 1e3, world)
         assert not r.tensors[0].is_cuda
         e2e = {"value": round(world * S / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
                "ms_per_step": round(e2e_ms, 4), "h2d_bytes_per_step": S, "d2h_bytes_per_step": S,
                "what": "aggregate() on pinned host gradients: H2D into the device bounce buffer, "
-                       "fused allreduce+mean, D2H of the means, host wall clock, max over ranks"}
+                       "fused allreduce+mean, D2H of the means into pinned host buckets "
+                       "(aggregate(out=prev)), host wall clock, max over ranks"}
 
     pk, pk_src = peaks()
     if world > 1:
@@ -508,8 +510,11 @@ def sweep(args, rank, world, local):
 
 
 def tune(args, rank, world, local):
-    """Measure where ring_rsa (two-shot) starts to beat rhd_rsa and write the
-    per-p switch point into paper_1810_11112_b200/tuning.json."""
+    """Measure, per message size, rhd one-shot (LL), rhd two-shot and ring,
+    all CUDA-graph timed, and store per group size: the largest size worth
+    reducing one-shot (oneshot_max_bytes = ll_max_bytes) and the switch point
+    from which ring_rsa beats rhd_rsa (collectives.py:239-247's threshold,
+    measured on this box) in paper_1810_11112_b200/tuning.json."""
     import paper_1810_11112_b200 as P
     from paper_1810_11112_b200 import _lib as L
     device = torch.device("cuda", local)
@@ -518,23 +523,39 @@ def tune(args, rank, world, local):
     x = torch.randn(8 << 20, device=device)
     y = torch.empty_like(x)
     st = L.Stats()
+    sizes = [1 << k for k in range(10, 24)]
     res = {}
-    for nbytes in [1 << k for k in range(10, 24)]:
+    big = 1 << 40
+    for nbytes in sizes:
         n = nbytes // 4
         t = {}
-        for algo in ("rhd_rsa", "ring_rsa"):
-            fn = lambda a=algo: L.check(L.lib.cm_allreduce(comm._h, x.data_ptr(), y.data_ptr(), n, 0, 0,  # noqa: E731
-                                                           L.ALGO[a], 131072, 0,
-                                                           torch.cuda.current_stream().cuda_stream,
-                                                           C.byref(st)))
+        for name, algo, osm in (("rhd_oneshot", "rhd_rsa", big), ("rhd_twoshot", "rhd_rsa", 1),
+                                ("ring", "ring_rsa", big)):
+            comm.set_param("oneshot_max_bytes", osm)
+            comm.set_param("ll_max_bytes", osm)
+            fn = lambda a=algo: L.check(L.lib.cm_allreduce(  # noqa: E731
+                comm._h, x.data_ptr(), y.data_ptr(), n, 0, 0, L.ALGO[a], 131072, 0,
+                torch.cuda.current_stream().cuda_stream, C.byref(st)))
             barrier(world)
-            t[algo] = max_over_ranks(_time_calls(fn, 100, 5, graph=True), world)
+            t[name] = max_over_ranks(_time_calls(fn, 100, 5, graph=True) * 1e3, world)
         res[nbytes] = t
+        if rank == 0:
+            log(json.dumps({"bytes": nbytes, **{k: round(v, 2) for k, v in t.items()}}))
+    oneshot_max = 0
+    for nbytes in sizes:
+        if res[nbytes]["rhd_oneshot"] <= res[nbytes]["rhd_twoshot"]:
+            oneshot_max = nbytes
+        else:
+            break
+    def rhd_best(b):
+        return res[b]["rhd_oneshot"] if b <= oneshot_max else res[b]["rhd_twoshot"]
     switch = None
-    for nbytes in sorted(res):
-        if res[nbytes]["ring_rsa"] < res[nbytes]["rhd_rsa"]:
+    for nbytes in sizes:
+        if res[nbytes]["ring"] < rhd_best(nbytes):
             switch = nbytes
             break
+    if switch is None:
+        switch = 1 << 24
     if rank == 0:
         path = os.path.join(ROOT, "paper_1810_11112_b200", "tuning.json")
         try:
@@ -542,12 +563,15 @@ def tune(args, rank, world, local):
                 data = json.load(fh)
         except (OSError, ValueError):
             data = {}
-        data.setdefault("switch_bytes", {})[str(world)] = switch or (1 << 24)
-        data.setdefault("measured", {})[str(world)] = {str(k): {a: round(v * 1e3, 3) for a, v in t.items()}
-                                                       for k, t in res.items()}
+        data.setdefault("switch_bytes", {})[str(world)] = switch
+        data.setdefault("oneshot_max_bytes", {})[str(world)] = max(oneshot_max, 1024)
+        data.setdefault("measured_us_cuda_graph", {})[str(world)] = {
+            str(k): {a: round(v, 3) for a, v in t.items()} for k, t in res.items()}
+        data["how"] = "bench.py --mode tune on a B200 box: CUDA-graph timed, max over ranks"
         with open(path, "w") as fh:
             json.dump(data, fh, indent=1)
-        print(json.dumps({"mode": "tune", "p": world, "switch_bytes": switch}), flush=True)
+        print(json.dumps({"mode": "tune", "p": world, "switch_bytes": switch,
+                          "oneshot_max_bytes": oneshot_max}), flush=True)
     comm.close()
 
 

@@ -228,7 +228,7 @@ def aggregate(grads: GradientSet, group: GroupSpec, transport: Communicator,
     if reuse is not None and [f.numel() for f in reuse] != [r["total"] for r in plan.runs]:
         raise ShapeError("out= GradientSet does not match this gradient schema")
     result: list[Tensor] = []
-    fused_bufs = []
+    fused_bufs, host_bufs = [], []
     stream = tp._stream()
     with torch.cuda.device(tp.device):
         for ri, run in enumerate(plan.runs):
@@ -243,9 +243,15 @@ def aggregate(grads: GradientSet, group: GroupSpec, transport: Communicator,
             if stats_out is not None:
                 stats_out.extend(_stats(run["stats"][k]) for k in range(ncalls.value))
             fused_bufs.append(fused)
-            host = run["any_host"]
-            if host:
-                fused = fused.cpu()
+            if run["any_host"]:
+                # CUDA-aware semantics: host gradients get host means, copied
+                # into pinned memory on the communicator's stream
+                prev = out.__dict__.get("_host") if out is not None else None
+                hbuf = prev[ri] if prev is not None else \
+                    torch.empty(run["total"], dtype=DTYPES[dtype], pin_memory=True)
+                hbuf.copy_(fused, non_blocking=True)
+                host_bufs.append(hbuf)
+                fused = hbuf
             for nm, view in zip(run["names"], fused.split_with_sizes(run["counts"])):
                 result.append(Tensor._wrap(nm, dtype, view))
     if tp.blocking or any(r["any_host"] for r in plan.runs):
@@ -256,6 +262,7 @@ def aggregate(grads: GradientSet, group: GroupSpec, transport: Communicator,
     object.__setattr__(gs, "tensors", tuple(result))
     object.__setattr__(gs, "iteration", grads.iteration)
     object.__setattr__(gs, "_fused", fused_bufs)
+    object.__setattr__(gs, "_host", host_bufs if host_bufs else None)
     return gs
 
 

@@ -171,6 +171,7 @@ class Communicator(_Base):
         osm = oneshot_max_for(self.size)
         if osm:
             self.set_param("oneshot_max_bytes", osm)
+            self.set_param("ll_max_bytes", osm)
         self._sym: dict[int, int] = {}
 
     # -- symmetric allocation (zero-copy collectives) -------------------------

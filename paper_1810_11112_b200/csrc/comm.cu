@@ -574,8 +574,9 @@ int launch_batched_copy(cm_comm* c, int n, const void* const* srcs, void* const*
       P.staging_bytes = (long long)c->staging_bytes;
       P.staging_off = (long long)c->staging_off;
     }
-    int64_t nb = (P.start[m] + (128 << 10) - 1) / (128 << 10);
-    nb = std::max<int64_t>(1, std::min<int64_t>(nb, 148 * 4));
+    // >= 2 waves of 512-thread CTAs (4 resident per SM) for large packs
+    int64_t nb = (P.start[m] + (64 << 10) - 1) / (64 << 10);
+    nb = std::max<int64_t>(1, std::min<int64_t>(nb, 148 * 8));
     void* args[] = {&P};
     ProfScope prof_scope(c, stream, 1, 2 * P.start[m]);
     CUDA_TRY(cudaLaunchKernel((const void*)batched_copy_kernel, dim3((unsigned)nb), dim3(THREADS),
