@@ -49,6 +49,28 @@ def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
+_RESULT_FD = None
+
+
+def _isolate_stdout():
+    """Route fd 1 (NCCL/torch banners, C-level prints) to stderr so stdout
+    carries exactly the one JSON result line."""
+    global _RESULT_FD
+    if _RESULT_FD is None:
+        sys.stdout.flush()
+        _RESULT_FD = os.dup(1)
+        os.dup2(2, 1)
+
+
+def emit(obj) -> None:
+    line = json.dumps(obj) + "\n"
+    if _RESULT_FD is None:
+        sys.stdout.write(line)
+        sys.stdout.flush()
+    else:
+        os.write(_RESULT_FD, line.encode())
+
+
 # --------------------------------------------------------------------------- env
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -345,7 +367,7 @@ def headline(args, rank, world, local):
             "gpu_launches_per_step": launches / max(args.steps, 1),
             "clocks": clocks, "nccl": nccl, "parity": parity,
         }
-        print(json.dumps(out), flush=True)
+        emit(out)
     comm.close()
 
 
@@ -400,7 +422,7 @@ def reference_arm(args, rank, world):
                                    f"aggregation.py, numpy) on host cores"},
         "e2e": {"value": val, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(out), flush=True)
+    emit(out)
 
 
 # ------------------------------------------------------------------ sweep/tune
@@ -505,7 +527,7 @@ def sweep(args, rank, world, local):
             for r in rows:
                 fh.write(",".join(format(r.get(k, ""), ".6g") if isinstance(r.get(k), float)
                                   else str(r.get(k, "")) for k in keys) + "\n")
-        print(json.dumps({"mode": "sweep", "p": world, "rows": rows}), flush=True)
+        emit({"mode": "sweep", "p": world, "rows": rows})
     comm.close()
 
 
@@ -570,8 +592,7 @@ def tune(args, rank, world, local):
         data["how"] = "bench.py --mode tune on a B200 box: CUDA-graph timed, max over ranks"
         with open(path, "w") as fh:
             json.dump(data, fh, indent=1)
-        print(json.dumps({"mode": "tune", "p": world, "switch_bytes": switch,
-                          "oneshot_max_bytes": oneshot_max}), flush=True)
+        emit({"mode": "tune", "p": world, "switch_bytes": switch, "oneshot_max_bytes": oneshot_max})
     comm.close()
 
 
@@ -600,6 +621,7 @@ def main():
     ap.add_argument("--algos", default="rhd_rsa,ring_rsa", help="sweep: algorithms to time")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    _isolate_stdout()
     rank, world, local = dist_env()
     if args.gpus is not None and args.gpus != world:
         log(f"note: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE")
