@@ -110,15 +110,18 @@ def peaks():
 
 
 class ClockSampler(threading.Thread):
-    """Samples SM clock and throttle reasons (NVML) during the timed region."""
+    """Samples SM clock and throttle reasons (NVML) every ~2 ms; the summary
+    only uses samples taken inside the timed window (mark_start/mark_stop)."""
 
     def __init__(self, device_index: int):
         super().__init__(daemon=True)
         self.idx = device_index
-        self.samples, self.reasons = [], set()
+        self.samples = []            # (t, mhz, reasons)
         self.stop_flag = threading.Event()
+        self.ready = threading.Event()
         self.max_mhz = None
-        self.ok = False
+        self.t0 = self.t1 = None
+        self.error = None
 
     def run(self):
         try:
@@ -126,30 +129,37 @@ class ClockSampler(threading.Thread):
             N.nvmlInit()
             h = N.nvmlDeviceGetHandleByIndex(self.idx)
             self.max_mhz = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
-            names = {
-                getattr(N, "nvmlClocksThrottleReasonHwSlowdown", 0x8): "hw_slowdown",
-                getattr(N, "nvmlClocksThrottleReasonHwThermalSlowdown", 0x40): "hw_thermal_slowdown",
-                getattr(N, "nvmlClocksThrottleReasonSwThermalSlowdown", 0x20): "sw_thermal_slowdown",
-                getattr(N, "nvmlClocksThrottleReasonSwPowerCap", 0x4): "sw_power_cap",
-                getattr(N, "nvmlClocksThrottleReasonHwPowerBrakeSlowdown", 0x80): "hw_power_brake",
-            }
-            self.ok = True
+            names = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+                     0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
+            self.ready.set()
             while not self.stop_flag.is_set():
-                self.samples.append(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM))
+                mhz = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
                 r = N.nvmlDeviceGetCurrentClocksThrottleReasons(h)
-                for bit, nm in names.items():
-                    if r & bit:
-                        self.reasons.add(nm)
+                self.samples.append((time.perf_counter(), mhz, [nm for bit, nm in names.items() if r & bit]))
                 time.sleep(0.002)
         except Exception as exc:  # pragma: no cover
-            self.reasons.add(f"nvml_unavailable:{type(exc).__name__}")
+            self.error = f"nvml_unavailable:{type(exc).__name__}"
+            self.ready.set()
+
+    def start_and_wait(self):
+        self.start()
+        self.ready.wait(timeout=30)
+
+    def mark_start(self):
+        self.t0 = time.perf_counter()
+
+    def mark_stop(self):
+        self.t1 = time.perf_counter()
 
     def result(self):
         self.stop_flag.set()
         self.join(timeout=2)
-        med = statistics.median(self.samples) if self.samples else None
-        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "samples": len(self.samples),
-                "reasons": sorted(self.reasons)}
+        win = [s for s in self.samples if self.t0 is not None and self.t0 <= s[0] <= (self.t1 or 1e30)]
+        if not win and self.samples:     # very short timed window: nearest samples
+            win = sorted(self.samples, key=lambda s: abs(s[0] - (self.t0 or 0)))[:3]
+        reasons = sorted({r for s in win for r in s[2]} | ({self.error} if self.error else set()))
+        med = statistics.median([s[1] for s in win]) if win else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "samples": len(win), "reasons": reasons}
 
 
 # --------------------------------------------------------------------- workload
@@ -231,6 +241,8 @@ def headline(args, rank, world, local):
                                    switch_bytes=args.switch, out=state["out"])
         return state["out"]
 
+    sampler = ClockSampler(local)
+    sampler.start_and_wait()
     for _ in range(args.warmup):
         res = step()
     comm.synchronize()
@@ -242,16 +254,16 @@ def headline(args, rank, world, local):
     launches0 = comm.launches
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
-    sampler = ClockSampler(local)
-    sampler.start()
     barrier(world)
     torch.cuda.synchronize()
+    sampler.mark_start()
     for i in range(args.steps):
         flush.zero_()                       # L2 flush (256 MiB > 126 MB L2), untimed
         evs[i][0].record()
         step()
         evs[i][1].record()
     torch.cuda.synchronize()
+    sampler.mark_stop()
     barrier(world)
     clocks = sampler.result()
     comm.synchronize()
