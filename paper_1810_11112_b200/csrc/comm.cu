@@ -47,6 +47,7 @@ struct cm_comm {
   int64_t ll_units_per_cta = 512;
   int64_t ll2_max_bytes = -1;                 // two-shot via LL slots up to here (-1: p x 512 KiB)
   int64_t ll2_units_per_cta = 512;
+  int64_t stream_chunk = 8192;                // elements; 0 disables the pipelined two-shot
   int64_t oneshot_bytes_per_cta = 8 * 1024;
   int64_t twoshot_bytes_per_cta = 4 * 1024;
   int max_ctas = 148;
@@ -120,15 +121,15 @@ struct ProfScope {
 
 using KFn = void (*)(CollParams);
 
-template <class D, int OP>
+template <class D, int OP, bool ST>
 KFn pick_mp(int p, bool tree) {
-  if (p <= 8) return tree ? collective_kernel<D, OP, 8, true> : collective_kernel<D, OP, 8, false>;
-  return tree ? collective_kernel<D, OP, 16, true> : collective_kernel<D, OP, 16, false>;
+  if (p <= 8) return tree ? collective_kernel<D, OP, 8, true, ST> : collective_kernel<D, OP, 8, false, ST>;
+  return tree ? collective_kernel<D, OP, 16, true, ST> : collective_kernel<D, OP, 16, false, ST>;
 }
 
-template <class D>
+template <class D, bool ST>
 KFn pick_op(int op, int p, bool tree) {
-  return op == CM_SUM ? pick_mp<D, CM_SUM>(p, tree) : pick_mp<D, CM_MAX>(p, tree);
+  return op == CM_SUM ? pick_mp<D, CM_SUM, ST>(p, tree) : pick_mp<D, CM_MAX, ST>(p, tree);
 }
 
 template <class D, int OP>
@@ -171,15 +172,20 @@ KFn pick_ll2(int dtype, int op, int p, bool tree) {
   return nullptr;
 }
 
-KFn pick_kernel(int dtype, int op, int p, bool tree) {
+template <bool ST>
+KFn pick_kernel_t(int dtype, int op, int p, bool tree) {
   switch (dtype) {
-    case CM_FLOAT32: return pick_op<F32>(op, p, tree);
-    case CM_FLOAT64: return pick_op<F64>(op, p, tree);
-    case CM_BFLOAT16: return pick_op<BF16>(op, p, tree);
-    case CM_INT32: return pick_op<I32>(op, p, tree);
-    case CM_INT64: return pick_op<I64>(op, p, tree);
+    case CM_FLOAT32: return pick_op<F32, ST>(op, p, tree);
+    case CM_FLOAT64: return pick_op<F64, ST>(op, p, tree);
+    case CM_BFLOAT16: return pick_op<BF16, ST>(op, p, tree);
+    case CM_INT32: return pick_op<I32, ST>(op, p, tree);
+    case CM_INT64: return pick_op<I64, ST>(op, p, tree);
   }
   return nullptr;
+}
+
+KFn pick_kernel(int dtype, int op, int p, bool tree, bool stream) {
+  return stream ? pick_kernel_t<true>(dtype, op, p, tree) : pick_kernel_t<false>(dtype, op, p, tree);
 }
 
 int check_dtype_op(int dtype, int op) {
@@ -310,9 +316,13 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
   if (ll == 2) nb = ((maxseg * (int64_t)sz + 7) / 8 + c->ll2_units_per_cta - 1) / c->ll2_units_per_cta;
   nb = std::max<int64_t>(1, std::min<int64_t>(nb, std::min(c->max_ctas, MAXBLK)));
   const bool tree = L.order == ORD_TREE;
+  // pipelined two-shot when every CTA's slice spans >= 2 chunks
+  const bool pipelined = ll == 0 && !L.oneshot && L.phases == (PH_RS | PH_AG) &&
+                         c->stream_chunk > 0 && maxseg / std::max<int64_t>(nb, 1) >= 2 * c->stream_chunk;
+  P.stream_chunk = c->stream_chunk;
   KFn k = ll == 1 ? pick_ll(L.dtype, L.op, p, tree)
         : ll == 2 ? pick_ll2(L.dtype, L.op, p, tree)
-                    : pick_kernel(L.dtype, L.op, p, tree);
+                    : pick_kernel(L.dtype, L.op, p, tree, pipelined);
   if (!k) return fail(CM_ERR_SHAPE, "unsupported dtype");
   void* args[] = {&P};
   int64_t alg = 0;   // busBW bytes of this launch (nccl-tests convention)
@@ -732,6 +742,7 @@ int cm_comm_set_param(cm_comm_t* c, const char* key, int64_t value) {
   else if (k == "ll_units_per_cta") c->ll_units_per_cta = value;
   else if (k == "ll2_max_bytes") c->ll2_max_bytes = value;
   else if (k == "ll2_units_per_cta") c->ll2_units_per_cta = value;
+  else if (k == "stream_chunk") c->stream_chunk = value == 1 ? 0 : ((value + 63) / 64) * 64;
   else if (k == "oneshot_bytes_per_cta") c->oneshot_bytes_per_cta = value;
   else if (k == "twoshot_bytes_per_cta") c->twoshot_bytes_per_cta = value;
   else if (k == "max_ctas") c->max_ctas = (int)std::min<int64_t>(value, MAXBLK);
@@ -746,6 +757,7 @@ int cm_comm_get_param(cm_comm_t* c, const char* key, int64_t* value) {
   else if (k == "ll_units_per_cta") *value = c->ll_units_per_cta;
   else if (k == "ll2_max_bytes") *value = c->ll2_max_bytes;
   else if (k == "ll2_units_per_cta") *value = c->ll2_units_per_cta;
+  else if (k == "stream_chunk") *value = c->stream_chunk;
   else if (k == "oneshot_bytes_per_cta") *value = c->oneshot_bytes_per_cta;
   else if (k == "twoshot_bytes_per_cta") *value = c->twoshot_bytes_per_cta;
   else if (k == "max_ctas") *value = c->max_ctas;

@@ -50,7 +50,9 @@ constexpr size_t MID_SIZE = (size_t)MAXBLK * MAXP * 8;
 // [parity][phase][src < p][unit < ll_units] starting at LL_OFF; its size
 // depends on p and is chosen at communicator creation, so staging starts at a
 // runtime offset (CollParams::staging_off).
-constexpr size_t LLH_OFF = MID_OFF + MID_SIZE;          // per-CTA LL header units
+constexpr size_t WMID_OFF = MID_OFF + MID_SIZE;         // per-warp progress of the pipelined two-shot
+constexpr size_t WMID_SIZE = (size_t)MAXBLK * MAXP * 8 * 8;
+constexpr size_t LLH_OFF = WMID_OFF + WMID_SIZE;        // per-CTA LL header units
 constexpr size_t LLH_SIZE = 2ull * MAXBLK * MAXP * 16;
 constexpr size_t HEAP_ALIGN = 2ull << 20;
 constexpr size_t LL_OFF = ((LLH_OFF + LLH_SIZE + HEAP_ALIGN - 1) / HEAP_ALIGN) * HEAP_ALIGN;
@@ -97,6 +99,7 @@ struct CollParams {
   int ag_in_rel;             // AG-only: `in` holds only my segment (in[i - seg_off])
   int average;               // divide the reduced value by p (aggregate mean)
   long long staging_off;     // heap offset of staging[0]
+  long long stream_chunk;    // elements per chunk of the pipelined two-shot
   long long ll_units;        // LL units per (parity, phase, source)
   unsigned long long* trace; // optional: per-CTA phase timestamps (globaltimer ns)
   int trace_ctas;
@@ -320,10 +323,9 @@ __device__ __forceinline__ void reduce_one(const char* const* seq, int p, int m,
 template <class D, int OP, int MP, bool TREE>
 __device__ void reduce_range(const char* const* seq, int p, int m, int excess, long long lo,
                              long long hi, bool vec, int average, char* out, long long out_shift,
-                             char* red, long long red_shift) {
+                             char* red, long long red_shift, int tid, int nthr) {
   using S = typename D::S;
   constexpr int W = 16 / sizeof(S);
-  const int tid = threadIdx.x;
   long long body_lo = lo, body_hi = lo;
   if (vec) {
     body_lo = ((lo + W - 1) / W) * W;
@@ -331,9 +333,9 @@ __device__ void reduce_range(const char* const* seq, int p, int m, int excess, l
     if (body_hi < body_lo) body_hi = body_lo = hi;
   }
   // scalar head and tail
-  for (long long i = lo + tid; i < body_lo; i += blockDim.x)
+  for (long long i = lo + tid; i < body_lo; i += nthr)
     reduce_one<D, OP, MP, 1, TREE>(seq, p, m, excess, i, average, out, out_shift, red, red_shift);
-  for (long long i = body_hi + tid; i < hi; i += blockDim.x)
+  for (long long i = body_hi + tid; i < hi; i += nthr)
     reduce_one<D, OP, MP, 1, TREE>(seq, p, m, excess, i, average, out, out_shift, red, red_shift);
   // vector body: vectors j in [body_lo/W, body_hi/W)
   const long long v0 = body_lo / W, v1 = body_hi / W;
@@ -341,13 +343,13 @@ __device__ void reduce_range(const char* const* seq, int p, int m, int excess, l
   // two vector groups in flight per thread when the operand registers fit
   constexpr int U = (MP * W * (int)(sizeof(A) / 4) <= 32) ? 2 : 1;
   long long j = v0 + tid;
-  for (; j + (U - 1) * (long long)blockDim.x < v1; j += U * (long long)blockDim.x) {
+  for (; j + (U - 1) * (long long)nthr < v1; j += U * (long long)nthr) {
     A u[U][MP][W];
 #pragma unroll
     for (int g = 0; g < U; ++g)
 #pragma unroll
       for (int k = 0; k < MP; ++k)
-        if (k < p) load_vec<D, W>(seq[k], (j + g * (long long)blockDim.x) * W, u[g][k]);
+        if (k < p) load_vec<D, W>(seq[k], (j + g * (long long)nthr) * W, u[g][k]);
 #pragma unroll
     for (int g = 0; g < U; ++g) {
       fold<OP, MP, W, TREE>(u[g], p, m, excess);
@@ -355,12 +357,12 @@ __device__ void reduce_range(const char* const* seq, int p, int m, int excess, l
 #pragma unroll
         for (int w = 0; w < W; ++w) u[g][0][w] = div_p<A>(u[g][0][w], p);
       }
-      const long long i = (j + g * (long long)blockDim.x) * W;
+      const long long i = (j + g * (long long)nthr) * W;
       store_vec<D, W>(out, i - out_shift, u[g][0]);
       if (red) store_vec<D, W>(red, i - red_shift, u[g][0]);
     }
   }
-  for (; j < v1; j += blockDim.x)
+  for (; j < v1; j += nthr)
     reduce_one<D, OP, MP, W, TREE>(seq, p, m, excess, j * W, average, out, out_shift, red,
                                    red_shift);
 }
@@ -427,7 +429,129 @@ __device__ __forceinline__ bool al16s(const char* base, long long shift_elems, i
 }
 
 // ---- the collective kernel -------------------------------------------------------
+constexpr int RS_WARPS = 8;                      // reducer warps of the pipelined two-shot
+__device__ __forceinline__ unsigned long long* wmid_slot(char* heap, int blk, int src, int warp) {
+  return reinterpret_cast<unsigned long long*>(heap + WMID_OFF +
+                                               (((size_t)blk * MAXP + src) * RS_WARPS + warp) * 8);
+}
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+
+// chunk k of slice [lo, hi): the first chunk ends at the first 64-aligned
+// boundary + C, later chunks are C elements on 64-aligned boundaries
+__device__ __forceinline__ void chunk_of(long long lo, long long hi, long long C, long long k,
+                                         long long* a, long long* z) {
+  const long long base = ((lo + SLICE_ALIGN - 1) / SLICE_ALIGN) * SLICE_ALIGN;
+  long long x = k == 0 ? lo : base + k * C;
+  long long y = base + (k + 1) * C;
+  if (x > hi) x = hi;
+  if (y > hi) y = hi;
+  if (y < x) y = x;
+  *a = x;
+  *z = y;
+}
+__device__ __forceinline__ long long chunks_of(long long lo, long long hi, long long C) {
+  const long long base = ((lo + SLICE_ALIGN - 1) / SLICE_ALIGN) * SLICE_ALIGN;
+  return hi <= base ? 1 : (hi - base + C - 1) / C;
+}
+
 template <class D, int OP, int MP, bool TREE>
+__device__ void stream_body(const CollParams& P, int rank, int b, int nb, unsigned long long e,
+                            const char* const* s_src, char* const* s_red, const char* const* s_seq,
+                            int* s_err, char* out, char* myheap) {
+  using S = typename D::S;
+  constexpr int SZ = sizeof(S);
+  constexpr int W = 16 / SZ;
+  constexpr int NR = RS_WARPS * 32;                // threads per role
+  const int p = P.p, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const long long C = P.stream_chunk;
+  // common chunk count (identical on every rank and for every segment)
+  long long K = 1;
+  for (int q = 0; q < p; ++q) {
+    const long long lo = slice_bound(P.seg_off[q], P.seg_len[q], b, nb);
+    const long long hi = slice_bound(P.seg_off[q], P.seg_len[q], b + 1, nb);
+    const long long kq = chunks_of(lo, hi, C);
+    K = kq > K ? kq : K;
+  }
+  const unsigned long long tag0 = e << 20;
+  if (warp < RS_WARPS) {
+    // ---------------- reducer warps
+    int m = 1;
+    while ((m << 1) <= p) m <<= 1;
+    const int excess = p - m;
+    const long long so = P.seg_off[rank], sl = P.seg_len[rank];
+    const long long lo = slice_bound(so, sl, b, nb), hi = slice_bound(so, sl, b + 1, nb);
+    bool vec = true;
+    for (int q = 0; q < p; ++q) vec = vec && al16(s_src[q]);
+    char* red = s_red[rank];
+    vec = vec && al16(out) && al16s(red, so, SZ);
+    for (long long k = 0; k < K; ++k) {
+      long long a, z;
+      chunk_of(lo, hi, C, k, &a, &z);
+      reduce_range<D, OP, MP, TREE>(s_seq, p, m, excess, a, z, vec, P.average, out, 0, red, so, tid, NR);
+      __syncwarp();
+      if (lane == 0) {
+        fence_acq_rel_sys();
+        for (int q = 0; q < p; ++q)
+          if (q != rank) st_relaxed_sys(wmid_slot(P.heap[q], b, rank, warp), tag0 | (unsigned long long)(k + 1));
+      }
+    }
+  } else {
+    // ---------------- gather warps
+    const int rt = tid - NR;
+    __shared__ VecRange s_av[MAXP];
+    for (long long k = 0; k < K; ++k) {
+      const unsigned long long want = tag0 | (unsigned long long)(k + 1);
+      if (rt < p * RS_WARPS) {
+        const int q = rt / RS_WARPS, w = rt % RS_WARPS;
+        if (q != rank && !wait_geq(wmid_slot(myheap, b, q, w), want, P.timeout_cycles))
+          atomicExch(s_err, ERR_TRANSPORT);
+      }
+      named_sync(1, NR);
+      if (*s_err) break;
+      if (rt < p) {                                  // ranges + scalar head/tail of peer rt
+        const int q = rt;
+        VecRange v{nullptr, nullptr, 0};
+        if (q != rank) {
+          const long long qo = P.seg_off[q], ql = P.seg_len[q];
+          long long a, z;
+          chunk_of(slice_bound(qo, ql, b, nb), slice_bound(qo, ql, b + 1, nb), C, k, &a, &z);
+          const S* src = reinterpret_cast<const S*>(s_red[q]) - qo;
+          S* dst = reinterpret_cast<S*>(out);
+          long long blo = z, bhi = z;
+          if (((((uintptr_t)src) | ((uintptr_t)dst)) & 15u) == 0) {
+            blo = ((a + W - 1) / W) * W;
+            bhi = (z / W) * W;
+            if (bhi < blo) blo = bhi = z;
+          }
+          for (long long i = a; i < blo; ++i) dst[i] = src[i];
+          for (long long i = bhi; i < z; ++i) dst[i] = src[i];
+          v.src = reinterpret_cast<const uint4*>(src + blo);
+          v.dst = reinterpret_cast<uint4*>(dst + blo);
+          v.nv = (bhi - blo) / W;
+        }
+        s_av[q] = v;
+      }
+      named_sync(1, NR);
+      long long nvmax = 0;
+      for (int q = 0; q < p; ++q) nvmax = s_av[q].nv > nvmax ? s_av[q].nv : nvmax;
+      for (long long j = rt; j < nvmax; j += NR) {
+        uint4 v[MP];
+#pragma unroll
+        for (int q = 0; q < MP; ++q)
+          if (q < p && j < s_av[q].nv) v[q] = s_av[q].src[j];
+#pragma unroll
+        for (int q = 0; q < MP; ++q)
+          if (q < p && j < s_av[q].nv) s_av[q].dst[j] = v[q];
+      }
+      named_sync(1, NR);                             // s_av reuse
+    }
+  }
+}
+
+template <class D, int OP, int MP, bool TREE, bool STREAM>
 __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_constant__ CollParams P) {
   using S = typename D::S;
   constexpr int SZ = sizeof(S);
@@ -525,6 +649,16 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
   CM_TRACE(P, lr, b, 2);
   if (s_err) goto finish;
 
+  if constexpr (STREAM) {
+    // Pipelined two-shot: warps 0..7 reduce chunk after chunk of my segment
+    // slice and publish per-warp progress to every peer; warps 8..15 pull
+    // chunk k of every other segment as soon as all peers' reducer warps have
+    // published it. Reduce-scatter of chunk k+1 overlaps allgather of chunk k,
+    // so there is no CTA-wide mid barrier and no idle link between phases.
+    stream_body<D, OP, MP, TREE>(P, rank, b, nb, e, s_src, s_red, s_seq, &s_err, out, myheap);
+    goto finish;
+  }
+
   // 3. reduce my segment (RS) — or the whole vector (one-shot)
   if (P.phases & PH_RS) {
     const long long so = P.oneshot ? 0 : mso;
@@ -556,7 +690,7 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
     }
     const long long lo = slice_bound(so, sl, b, nb), hi = slice_bound(so, sl, b + 1, nb);
     reduce_range<D, OP, MP, TREE>(s_seq, p, m, excess, lo, hi, vec, P.average, out, out_shift,
-                                  red, red_shift);
+                                  red, red_shift, tid, blockDim.x);
   }
 
   // 4. RS -> AG barrier (per CTA index) and 5. allgather

@@ -63,7 +63,7 @@ def main():
             expect(sha(out.to_bytes()) == case["sha"], f"C1 {case['algo']}")
 
     # 2. large messages: copy-in, zero-copy (symmetric pool), in-place, host buffers
-    for n in (262145, 1 << 22, 5_000_011):
+    for n in (262145, 1 << 22, 5_000_011, 20_000_003):
         rng = np.random.default_rng([21, n])
         xs = [(rng.standard_normal(n) * 10.0 ** rng.integers(-3, 4, size=n)).astype(np.float32)
               for _ in range(world)]

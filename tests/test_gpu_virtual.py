@@ -85,6 +85,25 @@ def test_large_fp32_vs_oracle(p, algo, n):
         assert t.to_bytes() == want.tobytes()
 
 
+@pytest.mark.parametrize("p", [2, 3, 4, 8])
+@pytest.mark.parametrize("algo", ["ring_rsa", "rhd_rsa"])
+def test_pipelined_two_shot_vs_oracle(p, algo):
+    """Large messages take the pipelined two-shot (reducer/gather warps with
+    per-warp progress flags); force small chunks so every CTA runs many."""
+    g = vg(p)
+    n = 6_000_007
+    rng = np.random.default_rng([p, 99])
+    xs = [(rng.standard_normal(n) * 10.0 ** rng.integers(-3, 4, size=n)).astype(np.float32)
+          for _ in range(p)]
+    want = OC.allreduce(xs, "sum", algo, "float32")
+    for chunk in (1024, 8192):
+        g.set_param("stream_chunk", chunk)
+        res = P.allreduce_group(dev_tensors(xs, "float32"), P.ReduceOp.SUM, g, algo=algo)
+        for t, _ in res:
+            assert t.to_bytes() == want.tobytes(), chunk
+    g.set_param("stream_chunk", 8192)
+
+
 @pytest.mark.parametrize("dtype", ["int32", "int64"])
 @pytest.mark.parametrize("p", [2, 3, 7, 8])
 def test_int_bit_exact(dtype, p):
