@@ -121,71 +121,20 @@ struct ProfScope {
 
 using KFn = void (*)(CollParams);
 
-template <class D, int OP, bool ST>
-KFn pick_mp(int p, bool tree) {
-  if (p <= 8) return tree ? collective_kernel<D, OP, 8, true, ST> : collective_kernel<D, OP, 8, false, ST>;
-  return tree ? collective_kernel<D, OP, 16, true, ST> : collective_kernel<D, OP, 16, false, ST>;
-}
+// kernel tables live in one translation unit per element type (csrc/inst_*.cu)
+// so the instantiations compile in parallel
+enum KernelKind { K_COLL = 0, K_STREAM = 1, K_LL = 2, K_LL2 = 3 };
 
-template <class D, bool ST>
-KFn pick_op(int op, int p, bool tree) {
-  return op == CM_SUM ? pick_mp<D, CM_SUM, ST>(p, tree) : pick_mp<D, CM_MAX, ST>(p, tree);
-}
-
-template <class D, int OP>
-KFn pick_ll_mp(int p, bool tree) {
-  if (p <= 8) return tree ? ll_kernel<D, OP, 8, true> : ll_kernel<D, OP, 8, false>;
-  return tree ? ll_kernel<D, OP, 16, true> : ll_kernel<D, OP, 16, false>;
-}
-
-KFn pick_ll(int dtype, int op, int p, bool tree) {
+KFn pick(int kind, int dtype, int op, int p, bool tree) {
+  const bool mp16 = p > 8;
   switch (dtype) {
-#define LLCASE(T, D) \
-    case T: return op == CM_SUM ? pick_ll_mp<D, CM_SUM>(p, tree) : pick_ll_mp<D, CM_MAX>(p, tree);
-    LLCASE(CM_FLOAT32, F32)
-    LLCASE(CM_FLOAT64, F64)
-    LLCASE(CM_BFLOAT16, BF16)
-    LLCASE(CM_INT32, I32)
-    LLCASE(CM_INT64, I64)
-#undef LLCASE
+    case CM_FLOAT32: return cm_kernels_f32(kind, op, mp16, tree);
+    case CM_FLOAT64: return cm_kernels_f64(kind, op, mp16, tree);
+    case CM_BFLOAT16: return cm_kernels_bf16(kind, op, mp16, tree);
+    case CM_INT32: return cm_kernels_i32(kind, op, mp16, tree);
+    case CM_INT64: return cm_kernels_i64(kind, op, mp16, tree);
   }
   return nullptr;
-}
-
-template <class D, int OP>
-KFn pick_ll2_mp(int p, bool tree) {
-  if (p <= 8) return tree ? ll2_kernel<D, OP, 8, true> : ll2_kernel<D, OP, 8, false>;
-  return tree ? ll2_kernel<D, OP, 16, true> : ll2_kernel<D, OP, 16, false>;
-}
-
-KFn pick_ll2(int dtype, int op, int p, bool tree) {
-  switch (dtype) {
-#define LLCASE(T, D) \
-    case T: return op == CM_SUM ? pick_ll2_mp<D, CM_SUM>(p, tree) : pick_ll2_mp<D, CM_MAX>(p, tree);
-    LLCASE(CM_FLOAT32, F32)
-    LLCASE(CM_FLOAT64, F64)
-    LLCASE(CM_BFLOAT16, BF16)
-    LLCASE(CM_INT32, I32)
-    LLCASE(CM_INT64, I64)
-#undef LLCASE
-  }
-  return nullptr;
-}
-
-template <bool ST>
-KFn pick_kernel_t(int dtype, int op, int p, bool tree) {
-  switch (dtype) {
-    case CM_FLOAT32: return pick_op<F32, ST>(op, p, tree);
-    case CM_FLOAT64: return pick_op<F64, ST>(op, p, tree);
-    case CM_BFLOAT16: return pick_op<BF16, ST>(op, p, tree);
-    case CM_INT32: return pick_op<I32, ST>(op, p, tree);
-    case CM_INT64: return pick_op<I64, ST>(op, p, tree);
-  }
-  return nullptr;
-}
-
-KFn pick_kernel(int dtype, int op, int p, bool tree, bool stream) {
-  return stream ? pick_kernel_t<true>(dtype, op, p, tree) : pick_kernel_t<false>(dtype, op, p, tree);
 }
 
 int check_dtype_op(int dtype, int op) {
@@ -320,9 +269,7 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
   const bool pipelined = ll == 0 && !L.oneshot && L.phases == (PH_RS | PH_AG) &&
                          c->stream_chunk > 0 && maxseg / std::max<int64_t>(nb, 1) >= 2 * c->stream_chunk;
   P.stream_chunk = c->stream_chunk;
-  KFn k = ll == 1 ? pick_ll(L.dtype, L.op, p, tree)
-        : ll == 2 ? pick_ll2(L.dtype, L.op, p, tree)
-                    : pick_kernel(L.dtype, L.op, p, tree, pipelined);
+  KFn k = pick(ll == 1 ? K_LL : ll == 2 ? K_LL2 : pipelined ? K_STREAM : K_COLL, L.dtype, L.op, p, tree);
   if (!k) return fail(CM_ERR_SHAPE, "unsupported dtype");
   void* args[] = {&P};
   int64_t alg = 0;   // busBW bytes of this launch (nccl-tests convention)

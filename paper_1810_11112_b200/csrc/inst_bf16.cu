@@ -1,0 +1,16 @@
+// Kernel instantiations for element type BF16 (one translation unit per type so
+// nvcc compiles them in parallel; see csrc/kernels.cuh).
+#include "kernels.cuh"
+
+namespace cm {
+namespace dev {
+CM_KERNEL_TABLE(BF16)
+}  // namespace dev
+}  // namespace cm
+
+cm_kfn_t cm_kernels_bf16(int kind, int op, bool mp16, bool tree) {
+  using namespace cm::dev;
+  void* f = op == CM_SUM ? (mp16 ? cm_table_op_BF16<CM_SUM, true>(kind, tree) : cm_table_op_BF16<CM_SUM, false>(kind, tree))
+                         : (mp16 ? cm_table_op_BF16<CM_MAX, true>(kind, tree) : cm_table_op_BF16<CM_MAX, false>(kind, tree));
+  return reinterpret_cast<cm_kfn_t>(f);
+}

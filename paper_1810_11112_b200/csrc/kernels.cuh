@@ -645,6 +645,20 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
       s_red[tid] = P.heap[tid] + ld_relaxed_sys_s64(&r->redoff);
     }
   }
+  // fold sequence of my segment's sources (reference order)
+  if (tid == 0 && (P.phases & PH_RS)) {
+    int m = 1;
+    while ((m << 1) <= p) m <<= 1;
+    const int excess = p - m;
+    if (P.order == ORD_RING) {            // chunk c folds x_{c-1}, x_{c-2}, ..., x_c
+      for (int k = 0; k < p; ++k) s_seq[k] = s_src[((rank - 1 - k) % p + p) % p];
+    } else if (P.order == ORD_TREE) {     // leaves real(v), partners 2v+1 at M+v
+      for (int v = 0; v < m; ++v) s_seq[v] = s_src[v < excess ? 2 * v : v + excess];
+      for (int v = 0; v < excess; ++v) s_seq[m + v] = s_src[2 * v + 1];
+    } else {
+      for (int k = 0; k < p; ++k) s_seq[k] = s_src[k];
+    }
+  }
   __syncthreads();
   CM_TRACE(P, lr, b, 2);
   if (s_err) goto finish;
@@ -666,17 +680,6 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
     int m = 1;
     while ((m << 1) <= p) m <<= 1;
     const int excess = p - m;
-    if (tid == 0) {
-      if (P.order == ORD_RING) {          // chunk c folds x_{c-1}, x_{c-2}, ..., x_c
-        for (int k = 0; k < p; ++k) s_seq[k] = s_src[((rank - 1 - k) % p + p) % p];
-      } else if (P.order == ORD_TREE) {   // leaves real(v), partners 2v+1 at M+v
-        for (int v = 0; v < m; ++v) s_seq[v] = s_src[v < excess ? 2 * v : v + excess];
-        for (int v = 0; v < excess; ++v) s_seq[m + v] = s_src[2 * v + 1];
-      } else {
-        for (int k = 0; k < p; ++k) s_seq[k] = s_src[k];
-      }
-    }
-    __syncthreads();
     bool vec = true;
     for (int q = 0; q < p; ++q) vec = vec && al16(s_src[q]);
     const long long out_shift = P.out_rel ? so : 0;
@@ -1069,7 +1072,7 @@ ll2_finish:
 // mode 0: pull — every rank reads `bytes` from each peer's staging into its own
 // mode 1: push — every rank writes `bytes` into each peer's staging
 // (all-to-all pattern of the two-shot phases; no synchronisation, data unused)
-__global__ void __launch_bounds__(THREADS) p2p_bw_kernel(const __grid_constant__ CollParams P, int mode,
+static __global__ void __launch_bounds__(THREADS) p2p_bw_kernel(const __grid_constant__ CollParams P, int mode,
                                                          long long bytes) {
   const int rank = P.rank, p = P.p, tid = threadIdx.x;
   const long long nv = bytes / 16;
@@ -1130,7 +1133,7 @@ struct CopyParams {
   long long staging_off;
 };
 
-__global__ void __launch_bounds__(THREADS) batched_copy_kernel(const __grid_constant__ CopyParams P) {
+static __global__ void __launch_bounds__(THREADS) batched_copy_kernel(const __grid_constant__ CopyParams P) {
   const long long total = P.start[P.n];
   const int b = blockIdx.x, nb = gridDim.x, tid = threadIdx.x;
   long long lo = (long long)(((__int128)total * b) / nb) & ~15ll;
@@ -1200,5 +1203,28 @@ __global__ void __launch_bounds__(THREADS) local_reduce_kernel(const char* a, co
   }
 }
 
+// kernel table of one element type: kind 0 collective, 1 pipelined two-shot,
+// 2 LL one-shot, 3 LL two-shot (defined in csrc/inst_<type>.cu)
+#define CM_KERNEL_TABLE(D)                                                          \
+  template <int OP, bool MP16>                                                      \
+  static void* cm_table_op_##D(int kind, bool tree) {                               \
+    constexpr int MP = MP16 ? 16 : 8;                                               \
+    switch (kind) {                                                                 \
+      case 0: return tree ? (void*)collective_kernel<D, OP, MP, true, false>        \
+                          : (void*)collective_kernel<D, OP, MP, false, false>;      \
+      case 1: return tree ? (void*)collective_kernel<D, OP, MP, true, true>         \
+                          : (void*)collective_kernel<D, OP, MP, false, true>;       \
+      case 2: return tree ? (void*)ll_kernel<D, OP, MP, true> : (void*)ll_kernel<D, OP, MP, false>;   \
+      default: return tree ? (void*)ll2_kernel<D, OP, MP, true> : (void*)ll2_kernel<D, OP, MP, false>; \
+    }                                                                               \
+  }
+
 }  // namespace dev
 }  // namespace cm
+
+using cm_kfn_t = void (*)(cm::dev::CollParams);
+cm_kfn_t cm_kernels_f32(int kind, int op, bool mp16, bool tree);
+cm_kfn_t cm_kernels_f64(int kind, int op, bool mp16, bool tree);
+cm_kfn_t cm_kernels_bf16(int kind, int op, bool mp16, bool tree);
+cm_kfn_t cm_kernels_i32(int kind, int op, bool mp16, bool tree);
+cm_kfn_t cm_kernels_i64(int kind, int op, bool mp16, bool tree);
