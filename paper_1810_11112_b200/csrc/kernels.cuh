@@ -645,6 +645,7 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
       s_red[tid] = P.heap[tid] + ld_relaxed_sys_s64(&r->redoff);
     }
   }
+  __syncthreads();                       // s_src / s_red / s_err complete
   // fold sequence of my segment's sources (reference order)
   if (tid == 0 && (P.phases & PH_RS)) {
     int m = 1;

@@ -4,22 +4,20 @@ import numpy as np, torch
 import paper_1810_11112_b200 as P
 from oracle import collectives as OC
 torch.cuda.set_device(0)
-g = P.VirtualGroup(4, 0, staging_bytes=128 << 20)
-for n in (16_320_000, 6_000_007):
+p = int(os.environ.get("P", 4))
+g = P.VirtualGroup(p, 0, staging_bytes=128 << 20)
+for n in [int(v) for v in os.environ.get("NS", "20000003,16320000,6000007").split(",")]:
     rng = np.random.default_rng(1)
-    xs = [rng.standard_normal(n).astype(np.float32) for _ in range(4)]
-    want = OC.allreduce(xs, "sum", "ring_rsa", "float32")
-    for chunk in (1024, 8192, 1):
-        for avg in (False, True):
+    xs = [rng.standard_normal(n).astype(np.float32) for _ in range(p)]
+    for algo in ("ring_rsa", "rhd_rsa"):
+        want = OC.allreduce(xs, "sum", algo, "float32")
+        for chunk in (8192, 1):
             g.set_param("stream_chunk", chunk)
-            res = P.allreduce_group([P.Tensor("x", "float32", torch.from_numpy(x).cuda()) for x in xs],
-                                    P.ReduceOp.SUM, g, algo="ring_rsa", average=avg)
-            w = want / np.float32(4) if avg else want
-            for r, (t, _) in enumerate(res):
-                got = t.numpy()
-                bad = np.nonzero(got.view(np.uint32) != w.astype(np.float32).view(np.uint32))[0]
-                if len(bad):
-                    print(f"n={n} chunk={chunk} avg={avg} rank={r}: {len(bad)} bad, first {bad[:5]}, last {bad[-3:]}")
-                    break
-            else:
-                print(f"n={n} chunk={chunk} avg={avg}: ok")
+            try:
+                res = P.allreduce_group([P.Tensor("x", "float32", torch.from_numpy(x).cuda()) for x in xs],
+                                        P.ReduceOp.SUM, g, algo=algo)
+            except Exception as exc:
+                print(f"n={n} {algo} chunk={chunk}: EXC {exc}", flush=True)
+                sys.exit(1)
+            bad = [r for r, (t, _) in enumerate(res) if t.to_bytes() != want.tobytes()]
+            print(f"n={n} {algo} chunk={chunk}: {'ok' if not bad else 'BAD ranks ' + str(bad)}", flush=True)
