@@ -47,7 +47,7 @@ struct cm_comm {
   int64_t ll_units_per_cta = 512;
   int64_t ll2_max_bytes = -1;                 // two-shot via LL slots up to here (-1: p x 512 KiB)
   int64_t ll2_units_per_cta = 512;
-  int64_t stream_chunk = 8192;                // elements; 0 disables the pipelined two-shot
+  int64_t stream_chunk = 0;                   // elements; 0 disables the pipelined two-shot
   int64_t oneshot_bytes_per_cta = 8 * 1024;
   int64_t twoshot_bytes_per_cta = 4 * 1024;
   int max_ctas = 148;
@@ -126,13 +126,12 @@ using KFn = void (*)(CollParams);
 enum KernelKind { K_COLL = 0, K_STREAM = 1, K_LL = 2, K_LL2 = 3 };
 
 KFn pick(int kind, int dtype, int op, int p, bool tree) {
-  const bool mp16 = p > 8;
   switch (dtype) {
-    case CM_FLOAT32: return cm_kernels_f32(kind, op, mp16, tree);
-    case CM_FLOAT64: return cm_kernels_f64(kind, op, mp16, tree);
-    case CM_BFLOAT16: return cm_kernels_bf16(kind, op, mp16, tree);
-    case CM_INT32: return cm_kernels_i32(kind, op, mp16, tree);
-    case CM_INT64: return cm_kernels_i64(kind, op, mp16, tree);
+    case CM_FLOAT32: return cm_kernels_f32(kind, op, p, tree);
+    case CM_FLOAT64: return cm_kernels_f64(kind, op, p, tree);
+    case CM_BFLOAT16: return cm_kernels_bf16(kind, op, p, tree);
+    case CM_INT32: return cm_kernels_i32(kind, op, p, tree);
+    case CM_INT64: return cm_kernels_i64(kind, op, p, tree);
   }
   return nullptr;
 }

@@ -8,9 +8,8 @@ CM_KERNEL_TABLE(F32)
 }  // namespace dev
 }  // namespace cm
 
-cm_kfn_t cm_kernels_f32(int kind, int op, bool mp16, bool tree) {
+cm_kfn_t cm_kernels_f32(int kind, int op, int p, bool tree) {
   using namespace cm::dev;
-  void* f = op == CM_SUM ? (mp16 ? cm_table_op_F32<CM_SUM, true>(kind, tree) : cm_table_op_F32<CM_SUM, false>(kind, tree))
-                         : (mp16 ? cm_table_op_F32<CM_MAX, true>(kind, tree) : cm_table_op_F32<CM_MAX, false>(kind, tree));
+  void* f = op == CM_SUM ? cm_table_op_F32<CM_SUM>(kind, p, tree) : cm_table_op_F32<CM_MAX>(kind, p, tree);
   return reinterpret_cast<cm_kfn_t>(f);
 }

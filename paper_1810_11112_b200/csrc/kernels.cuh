@@ -340,8 +340,9 @@ __device__ void reduce_range(const char* const* seq, int p, int m, int excess, l
   // vector body: vectors j in [body_lo/W, body_hi/W)
   const long long v0 = body_lo / W, v1 = body_hi / W;
   using A = typename D::A;
-  // two vector groups in flight per thread when the operand registers fit
-  constexpr int U = (MP * W * (int)(sizeof(A) / 4) <= 32) ? 2 : 1;
+  // vector groups in flight per thread: ~64 operand registers whatever MP is
+  constexpr int OPR = MP * W * (int)(sizeof(A) / 4);
+  constexpr int U = OPR >= 64 ? 1 : 64 / OPR;
   long long j = v0 + tid;
   for (; j + (U - 1) * (long long)nthr < v1; j += U * (long long)nthr) {
     A u[U][MP][W];
@@ -412,14 +413,30 @@ __device__ void multi_copy(const CopyRange* R, int nr, VecRange* V) {
   __syncthreads();
   long long nvmax = 0;
   for (int r = 0; r < nr; ++r) nvmax = V[r].nv > nvmax ? V[r].nv : nvmax;
-  for (long long j = tid; j < nvmax; j += bd) {
-    uint4 v[MP];
+  // NS 16-byte loads in flight per thread whatever the number of ranges:
+  // slot s copies range s % nr at vector offset (s / nr) * bd
+  constexpr int NS = MP > 8 ? MP : 8;
+  if (nr < 1) return;
+  const int G = NS / nr > 1 ? NS / nr : 1;
+  const int act = nr * G < NS ? nr * G : NS;
+  int sr[NS], sg[NS];
 #pragma unroll
-    for (int r = 0; r < MP; ++r)
-      if (r < nr && j < V[r].nv) v[r] = V[r].src[j];
+  for (int k = 0; k < NS; ++k) {
+    sr[k] = k % nr;
+    sg[k] = k / nr;
+  }
+  for (long long j0 = tid; j0 < nvmax; j0 += (long long)bd * G) {
+    uint4 v[NS];
 #pragma unroll
-    for (int r = 0; r < MP; ++r)
-      if (r < nr && j < V[r].nv) V[r].dst[j] = v[r];
+    for (int k = 0; k < NS; ++k) {
+      const long long j = j0 + (long long)sg[k] * bd;
+      if (k < act && j < V[sr[k]].nv) v[k] = V[sr[k]].src[j];
+    }
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+      const long long j = j0 + (long long)sg[k] * bd;
+      if (k < act && j < V[sr[k]].nv) V[sr[k]].dst[j] = v[k];
+    }
   }
 }
 
@@ -1207,25 +1224,33 @@ __global__ void __launch_bounds__(THREADS) local_reduce_kernel(const char* a, co
 // kernel table of one element type: kind 0 collective, 1 pipelined two-shot,
 // 2 LL one-shot, 3 LL two-shot (defined in csrc/inst_<type>.cu)
 #define CM_KERNEL_TABLE(D)                                                          \
-  template <int OP, bool MP16>                                                      \
-  static void* cm_table_op_##D(int kind, bool tree) {                               \
-    constexpr int MP = MP16 ? 16 : 8;                                               \
-    switch (kind) {                                                                 \
-      case 0: return tree ? (void*)collective_kernel<D, OP, MP, true, false>        \
-                          : (void*)collective_kernel<D, OP, MP, false, false>;      \
-      case 1: return tree ? (void*)collective_kernel<D, OP, MP, true, true>         \
-                          : (void*)collective_kernel<D, OP, MP, false, true>;       \
-      case 2: return tree ? (void*)ll_kernel<D, OP, MP, true> : (void*)ll_kernel<D, OP, MP, false>;   \
-      default: return tree ? (void*)ll2_kernel<D, OP, MP, true> : (void*)ll2_kernel<D, OP, MP, false>; \
-    }                                                                               \
+  template <int OP, int MP>                                                         \
+  static void* cm_table_coll_##D(int kind, bool tree) {                             \
+    if (kind == 1) return tree ? (void*)collective_kernel<D, OP, MP, true, true>    \
+                               : (void*)collective_kernel<D, OP, MP, false, true>;  \
+    return tree ? (void*)collective_kernel<D, OP, MP, true, false>                  \
+                : (void*)collective_kernel<D, OP, MP, false, false>;                \
+  }                                                                                 \
+  template <int OP, int MP>                                                         \
+  static void* cm_table_ll_##D(int kind, bool tree) {                               \
+    if (kind == 2) return tree ? (void*)ll_kernel<D, OP, MP, true> : (void*)ll_kernel<D, OP, MP, false>; \
+    return tree ? (void*)ll2_kernel<D, OP, MP, true> : (void*)ll2_kernel<D, OP, MP, false>;              \
+  }                                                                                 \
+  template <int OP>                                                                 \
+  static void* cm_table_op_##D(int kind, int p, bool tree) {                        \
+    if (kind >= 2) return p <= 8 ? cm_table_ll_##D<OP, 8>(kind, tree) : cm_table_ll_##D<OP, 16>(kind, tree); \
+    if (p <= 2) return cm_table_coll_##D<OP, 2>(kind, tree);                        \
+    if (p <= 4) return cm_table_coll_##D<OP, 4>(kind, tree);                        \
+    if (p <= 8) return cm_table_coll_##D<OP, 8>(kind, tree);                        \
+    return cm_table_coll_##D<OP, 16>(kind, tree);                                   \
   }
 
 }  // namespace dev
 }  // namespace cm
 
 using cm_kfn_t = void (*)(cm::dev::CollParams);
-cm_kfn_t cm_kernels_f32(int kind, int op, bool mp16, bool tree);
-cm_kfn_t cm_kernels_f64(int kind, int op, bool mp16, bool tree);
-cm_kfn_t cm_kernels_bf16(int kind, int op, bool mp16, bool tree);
-cm_kfn_t cm_kernels_i32(int kind, int op, bool mp16, bool tree);
-cm_kfn_t cm_kernels_i64(int kind, int op, bool mp16, bool tree);
+cm_kfn_t cm_kernels_f32(int kind, int op, int p, bool tree);
+cm_kfn_t cm_kernels_f64(int kind, int op, int p, bool tree);
+cm_kfn_t cm_kernels_bf16(int kind, int op, int p, bool tree);
+cm_kfn_t cm_kernels_i32(int kind, int op, int p, bool tree);
+cm_kfn_t cm_kernels_i64(int kind, int op, int p, bool tree);
