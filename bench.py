@@ -608,13 +608,39 @@ def tune(args, rank, world, local):
     comm.close()
 
 
+def refsweep(args):
+    """Reference CPU path per message size: oracle/threaded.py (the
+    reference's message-passing ring/rhd programs, numpy, one thread per
+    rank) for p = --ranks, float32, timed on this host. CSV to stdout."""
+    from oracle import threaded as T
+    p = args.ranks
+    rows = ["message_bytes,p,algo,mean_ms,min_ms,iters"]
+    b = args.sweep_min
+    while b <= args.sweep_max:
+        n = max(1, b // 4)
+        rng = np.random.default_rng([0, b])
+        xs = [rng.standard_normal(n).astype(np.float32) for _ in range(p)]
+        algo = "rhd_rsa" if b < 131072 else "ring_rsa"
+        times = []
+        t_end = time.perf_counter() + 3.0
+        while len(times) < 50 and (time.perf_counter() < t_end or len(times) < 2):
+            t0 = time.perf_counter()
+            T.ThreadNet(p).run(lambda r, tp: T.allreduce_rank(xs[r], "sum", algo, tp))
+            times.append(time.perf_counter() - t0)
+        rows.append(f"{b},{p},{algo},{statistics.mean(times) * 1e3:.4f},{min(times) * 1e3:.4f},{len(times)}")
+        log(rows[-1])
+        b *= 4
+    emit({"mode": "refsweep", "p": p, "csv": rows})
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=None)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--mode", choices=("headline", "sweep", "tune"), default="headline")
+    ap.add_argument("--mode", choices=("headline", "sweep", "tune", "refsweep"), default="headline")
+    ap.add_argument("--ranks", type=int, default=4, help="refsweep: simulated ranks")
     ap.add_argument("--model", choices=tuple(MODELS), default="resnet50_like")
     ap.add_argument("--dtype", choices=("float32", "bfloat16"), default="float32")
     ap.add_argument("--algo", default="auto")
@@ -639,6 +665,10 @@ def main():
         log(f"note: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE")
     if args.impl == "reference":
         reference_arm(args, rank, world)
+        return
+    if args.mode == "refsweep":
+        if rank == 0:
+            refsweep(args)
         return
     init_dist(rank, world, local, nccl=True)
     try:
