@@ -84,19 +84,22 @@ def negotiate_ready(local_ready: list[str], group: GroupSpec, transport) -> list
     on every rank (aggregation.py:72-92).
 
     Fast path: ``cm_agree`` — one int64 MAX allreduce over NVLink of
-    (key, -key, count, -count), key = a hash of the sorted names; equal maxima
+    (key, count, -key, -count), key = a hash of the sorted names; equal maxima
     on every rank mean identical ready sets, so the intersection is the local
     list. Otherwise the sets are gathered over the torch.distributed control
-    plane and the intersection is computed exactly as the reference does at
-    rank 0."""
+    plane and intersected exactly as the reference does at rank 0."""
     names = sorted(local_ready)
     if group.size == 1:
         return names
     if _sets_agree(transport, _name_key(names), len(names)):
         return names
+    return _negotiate_gather(names, group, transport)
+
+
+def _negotiate_gather(names: list[str], group: GroupSpec, tp) -> list[str]:
     import torch.distributed as dist
     gathered = [None] * group.size
-    dist.all_gather_object(gathered, names, group=transport._group)
+    dist.all_gather_object(gathered, list(names), group=tp._group)
     common = set(gathered[0])
     for g in gathered[1:]:
         common &= set(g)
@@ -104,11 +107,11 @@ def negotiate_ready(local_ready: list[str], group: GroupSpec, transport) -> list
 
 
 def _sets_agree(tp: Communicator, key: int, count: int) -> bool:
-    vals = (C.c_int64 * 4)(key, -key, count, -count)
+    vals = (C.c_int64 * 4)(key, count, -key, -count)
     mx = (C.c_int64 * 4)()
     with torch.cuda.device(tp.device):
         L.check(L.lib.cm_agree(tp._h, vals, 4, mx, tp._stream()))
-    return list(mx) == [key, -key, count, -count]
+    return list(mx) == [key, count, -key, -count]
 
 
 def fuse_plan(tensors: list[Tensor], cfg: FusionConfig) -> list[list[int]]:
@@ -200,6 +203,12 @@ def aggregate(grads: GradientSet, group: GroupSpec, transport: Communicator,
     """Negotiate, fuse, allreduce-sum and average this iteration's gradients;
     every rank returns the same mean tensors (aggregation.py:138-176).
 
+    Negotiation is folded into the first fused call: every rank passes a hash
+    of its sorted ready names and ``cm_fused_allreduce_agreed`` checks them
+    with one NVLink MAX-allreduce before launching, in the same C call (no
+    Python between the check and the launches). If the sets differ, the
+    intersection is negotiated over the control plane as in the reference.
+
     ``out``: a GradientSet previously returned by ``aggregate`` for the same
     schema; its fused buffers are reused (stream-ordered overwrite, like
     torch ``out=``) instead of allocating new ones — the persistent-bucket
@@ -211,15 +220,32 @@ def aggregate(grads: GradientSet, group: GroupSpec, transport: Communicator,
     if algo not in L.ALGO:
         from .errors import ConfigError
         raise ConfigError(f"unknown algorithm {algo!r}")
-    ready_names = negotiate_ready(grads.names, group, tp)
-    if not ready_names:
+    local = grads.__dict__.get("_sorted_names")
+    if local is None:
+        local = sorted(grads.names)
+        object.__setattr__(grads, "_sorted_names", local)
+        object.__setattr__(grads, "_name_key", _name_key(local))
+    sw = _switch(switch_bytes, tp.size)
+    if tp.size == 1:
+        return _aggregate_names(grads, local, tp, algo, cfg, sw, registry, handles, stats_out, out, None)
+    if not local:               # nothing to fuse: plain agree + gather
+        names = negotiate_ready([], group, tp)
+        return _aggregate_names(grads, names, tp, algo, cfg, sw, registry, handles, stats_out, out, None)
+    agree = (C.c_int64 * 2)(grads.__dict__["_name_key"], len(local))
+    res = _aggregate_names(grads, local, tp, algo, cfg, sw, registry, handles, stats_out, out, agree)
+    if res is None:             # ready sets differ across ranks
+        names = _negotiate_gather(local, group, tp)
+        res = _aggregate_names(grads, names, tp, algo, cfg, sw, registry, handles, stats_out, out, None)
+    return res
+
+
+def _aggregate_names(grads, names, tp, algo, cfg, sw, registry, handles, stats_out, out, agree):
+    if not names:
         return GradientSet((), grads.iteration)
     cache = grads.__dict__.setdefault("_plans", {})
-    key = tuple(ready_names)
-    plan = cache.get(key)
+    plan = cache.get(tuple(names))
     if plan is None:
-        plan = cache[key] = _Plan(grads, ready_names)
-    sw = _switch(switch_bytes, tp.size)
+        plan = cache[tuple(names)] = _Plan(grads, names)
     if registry is not None and handles is not None:
         for grp in fuse_plan(plan.ready, cfg):       # aggregation.py:159-161
             for i in grp:
@@ -236,10 +262,14 @@ def aggregate(grads: GradientSet, group: GroupSpec, transport: Communicator,
             fused = reuse[ri] if reuse is not None else \
                 torch.empty(run["total"], dtype=DTYPES[dtype], device=tp.device)
             ncalls = C.c_int()
-            L.check(L.lib.cm_fused_allreduce(
+            agreed = C.c_int(1)
+            L.check(L.lib.cm_fused_allreduce_agreed(
                 tp._h, run["n"], run["ptrs"], run["counts_c"], L.DTYPE[dtype], fused.data_ptr(),
-                L.ALGO[algo], int(cfg.threshold_bytes), sw, 1, stream, run["stats"],
-                C.byref(ncalls)))
+                L.ALGO[algo], int(cfg.threshold_bytes), sw, 1, agree, 2 if agree is not None else 0,
+                C.byref(agreed), stream, run["stats"], C.byref(ncalls)))
+            if not agreed.value:
+                return None             # nothing was launched
+            agree = None
             if stats_out is not None:
                 stats_out.extend(_stats(run["stats"][k]) for k in range(ncalls.value))
             fused_bufs.append(fused)

@@ -878,6 +878,16 @@ int cm_fused_allreduce(cm_comm_t* c, int n, const void* const* sends, const int6
                        int dtype, void* recv_fused, int algo, int64_t threshold,
                        int64_t switch_bytes, int average, void* stream_, cm_stats_t* stats,
                        int* n_calls) {
+  return cm_fused_allreduce_agreed(c, n, sends, counts, dtype, recv_fused, algo, threshold,
+                                   switch_bytes, average, nullptr, 0, nullptr, stream_, stats,
+                                   n_calls);
+}
+
+int cm_fused_allreduce_agreed(cm_comm_t* c, int n, const void* const* sends,
+                              const int64_t* counts, int dtype, void* recv_fused, int algo,
+                              int64_t threshold, int64_t switch_bytes, int average,
+                              const int64_t* agree_values, int n_agree, int* agreed,
+                              void* stream_, cm_stats_t* stats, int* n_calls) {
   if (c->virt) return fail(CM_ERR_UNSUPPORTED, "fused allreduce needs a real communicator");
   int st = check_dtype_op(dtype, CM_SUM);
   if (st) return st;
@@ -886,6 +896,20 @@ int cm_fused_allreduce(cm_comm_t* c, int n, const void* const* sends, const int6
   if ((st = check_async_error(c))) return st;
   if (threshold <= 0) return fail(CM_ERR_VALUE, "fusion threshold must be positive");
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  *n_calls = 0;
+  if (n_agree > 0) {
+    // negotiation fast path (aggregation.py:72-92): every rank must hold the
+    // same values, checked as max(v) == v and max(-v) == -v in one one-shot
+    // MAX allreduce; the fused launches follow without returning to Python
+    if (n_agree > 32) return fail(CM_ERR_VALUE, "at most 32 agreement values");
+    int64_t vals[64], mx[64];
+    for (int i = 0; i < n_agree; ++i) { vals[i] = agree_values[i]; vals[n_agree + i] = -agree_values[i]; }
+    if ((st = cm_agree(c, vals, 2 * n_agree, mx, stream_))) return st;
+    bool same = true;
+    for (int i = 0; i < 2 * n_agree; ++i) same = same && mx[i] == vals[i];
+    *agreed = same ? 1 : 0;
+    if (!same) return CM_OK;
+  }
   const int64_t sz = (int64_t)dtype_size(dtype);
   std::vector<int64_t> nbytes(n);
   std::vector<int> dts(n, dtype), group(n);

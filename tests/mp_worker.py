@@ -125,6 +125,17 @@ def main():
                 h.update(t.to_bytes())
             expect(h.hexdigest() == case["sha"], f"model {case['model']} host={host}")
 
+    # 4b. aggregate with differing ready sets: the device-side agreement check
+    # fails and the intersection is negotiated (aggregation.py:152-155)
+    schema = I.agg_schema(world)
+    mine = I.agg_inputs(schema, world, "float32")[rank]
+    extra = [("zz_only_rank0", np.ones(7, np.float32))] if rank == 0 else []
+    gs = P.GradientSet(tuple(P.Tensor(nm, "float32", torch.from_numpy(a).cuda()) for nm, a in mine + extra))
+    res = P.aggregate(gs, group, comm)
+    expect(res.names == sorted(nm for nm, _ in schema), "aggregate partial readiness intersection")
+    res2 = P.aggregate(gs, group, comm)          # second call takes the same fallback
+    expect([t.to_bytes() for t in res2.tensors] == [t.to_bytes() for t in res.tensors], "fallback repeatable")
+
     # 5. negotiation: partial intersection falls back to the control plane
     ready = ["a", "b", "c"] if rank == 0 else ["b", "c", "d"]
     expect(P.negotiate_ready(ready, group, comm) == ["b", "c"], "negotiate partial")
