@@ -164,7 +164,7 @@ int cm_comm_free(cm_comm_t* comm, void* ptr);
 int cm_comm_sync(cm_comm_t* comm, void* stream);
 /* non-blocking error check of completed calls */
 int cm_comm_poll(cm_comm_t* comm);
-/* synchronous element-wise MAX over ranks of n <= 64 host int64 values (one
+/* synchronous element-wise MAX over ranks of n <= 8 host int64 values (one
  * one-shot NVLink kernel); control-plane primitive of negotiate_ready
  * (aggregation.py:72-92) — equal (key, -key) maxima prove equal ready sets */
 int cm_agree(cm_comm_t* comm, const int64_t* values, int n, int64_t* maxes, void* stream);
@@ -212,7 +212,7 @@ int cm_fused_allreduce(cm_comm_t* comm, int n, const void* const* sends, const i
                        int* n_calls);
 
 /* cm_fused_allreduce preceded by the negotiation check: every rank passes the
- * same n_agree (<= 32) values (e.g. a hash of its ready names) when its ready
+ * same n_agree (<= 4) values (e.g. a hash of its ready names) when its ready
  * set is identical; *agreed = 1 and the fused launches follow in the same call,
  * or *agreed = 0 and nothing is launched (the caller negotiates the
  * intersection, aggregation.py:72-92, and calls again). */

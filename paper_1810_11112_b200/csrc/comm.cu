@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -38,8 +39,9 @@ struct cm_comm {
   std::map<size_t, size_t> pool_free;  // offset -> bytes
   std::map<size_t, size_t> pool_used;
   char* scratch = nullptr;             // device bounce buffer for host-memory buffers
-  int64_t* agree_host = nullptr;       // pinned: cm_agree in/out
-  int64_t* agree_dev = nullptr;        // device: cm_agree in/out
+  int64_t* agree_host = nullptr;       // mapped pinned: cm_agree result + completion word
+  int64_t* agree_dev = nullptr;        // device alias of agree_host
+  unsigned long long agree_ticket = 0;
   int sms = 148;
   // tuning knobs (cm_comm_set_param)
   int64_t oneshot_max_bytes = 32 * 1024;
@@ -190,6 +192,9 @@ struct Launch {
   int dtype = 0, op = 0, order = ORD_SEQ, phases = PH_RS | PH_AG, oneshot = 0;
   int out_rel = 0, ag_in_rel = 0, average = 0, layout = CM_LAYOUT_RING;
   int srcmode = SRC_COPYIN;
+  const long long* inl = nullptr;   // SRC_INLINE payload (<= 8 words)
+  unsigned long long* done_flag = nullptr;
+  unsigned long long done_value = 0;
   int ll = 0;                       // one-shot through the LL slots
   const void* in[MAXP] = {};
   void* out[MAXP] = {};
@@ -239,6 +244,9 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
   P.average = L.average;
   P.staging_off = (long long)c->staging_off;
   P.ll_units = c->ll_units;
+  if (L.inl) for (int i = 0; i < 8; ++i) P.inl[i] = L.inl[i];
+  P.done_flag = L.done_flag;
+  P.done_value = L.done_value;
   P.trace = c->trace;
   P.trace_ctas = c->trace_ctas;
 
@@ -647,7 +655,6 @@ int cm_comm_destroy(cm_comm_t* c) {
   if (c->scratch) cudaFree(c->scratch);
   if (c->herr_host) cudaFreeHost(c->herr_host);
   if (c->agree_host) cudaFreeHost(c->agree_host);
-  if (c->agree_dev) cudaFree(c->agree_dev);
   for (auto& pr : c->prof) { cudaEventDestroy(pr.e0); cudaEventDestroy(pr.e1); }
   for (auto e : c->event_pool) cudaEventDestroy(e);
   cudaGetLastError();
@@ -759,33 +766,49 @@ int cm_comm_poll(cm_comm_t* c) { return check_async_error(c); }
 // control-plane primitive behind negotiate_ready's fast path (one one-shot
 // kernel over NVLink instead of a host gather/broadcast).
 int cm_agree(cm_comm_t* c, const int64_t* values, int n, int64_t* maxes, void* stream_) {
-  if (n < 1 || n > 64) return fail(CM_ERR_VALUE, "cm_agree takes 1..64 values");
+  if (n < 1 || n > 8) return fail(CM_ERR_VALUE, "cm_agree takes 1..8 values");
   if (c->virt) return fail(CM_ERR_UNSUPPORTED, "cm_agree needs a real communicator");
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
-  if (!c->agree_host) {
-    CUDA_TRY(cudaHostAlloc(&c->agree_host, 128 * sizeof(int64_t), cudaHostAllocDefault));
-    CUDA_TRY(cudaMalloc(&c->agree_dev, 128 * sizeof(int64_t)));
-  }
   if (c->size == 1) {
     memcpy(maxes, values, n * sizeof(int64_t));
     return CM_OK;
   }
-  memcpy(c->agree_host, values, n * sizeof(int64_t));
-  CUDA_TRY(cudaMemcpyAsync(c->agree_dev, c->agree_host, n * sizeof(int64_t), cudaMemcpyHostToDevice, stream));
+  if (!c->agree_host) {      // mapped pinned: kernel writes result + completion word
+    CUDA_TRY(cudaHostAlloc(&c->agree_host, 16 * sizeof(int64_t), cudaHostAllocMapped));
+    CUDA_TRY(cudaHostGetDevicePointer((void**)&c->agree_dev, c->agree_host, 0));
+    memset(c->agree_host, 0, 16 * sizeof(int64_t));
+  }
+  // values travel in the kernel parameters, the result lands in pinned host
+  // memory, and the host spins on a completion word: one launch, no memcpy
+  long long inl[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int i = 0; i < n; ++i) inl[i] = values[i];
+  volatile unsigned long long* flag = reinterpret_cast<volatile unsigned long long*>(c->agree_host + 8);
+  const unsigned long long ticket = ++c->agree_ticket;
   Launch L;
   L.n = n;
   L.dtype = CM_INT64;
   L.op = CM_MAX;
   plan_algo(c, CM_ALGO_RHD, n * 8, &L);
-  L.srcmode = SRC_COPYIN;
-  L.in[0] = c->agree_dev;
-  L.out[0] = c->agree_dev + 64;
+  L.ll = 1;
+  L.oneshot = 1;
+  L.srcmode = SRC_INLINE;
+  L.inl = inl;
+  L.out[0] = c->agree_dev;
+  L.done_flag = reinterpret_cast<unsigned long long*>(c->agree_dev + 8);
+  L.done_value = ticket;
   int st = launch_collective(c, L, stream);
   if (st) return st;
-  CUDA_TRY(cudaMemcpyAsync(c->agree_host + 64, c->agree_dev + 64, n * sizeof(int64_t), cudaMemcpyDeviceToHost, stream));
-  CUDA_TRY(cudaStreamSynchronize(stream));
+  const auto t0 = std::chrono::steady_clock::now();
+  while (*flag != ticket) {
+    if (*reinterpret_cast<volatile unsigned*>(c->herr_host)) break;
+    if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(60)) {
+      cudaError_t e = cudaStreamQuery(stream);
+      if (e != cudaErrorNotReady && e != cudaSuccess) return cuda_fail(e, "cm_agree");
+      return fail(CM_ERR_TRANSPORT, "cm_agree: peers did not answer within 60 s");
+    }
+  }
   if ((st = check_async_error(c))) return st;
-  memcpy(maxes, c->agree_host + 64, n * sizeof(int64_t));
+  for (int i = 0; i < n; ++i) maxes[i] = reinterpret_cast<volatile int64_t*>(c->agree_host)[i];
   return CM_OK;
 }
 
@@ -901,7 +924,7 @@ int cm_fused_allreduce_agreed(cm_comm_t* c, int n, const void* const* sends,
     // negotiation fast path (aggregation.py:72-92): every rank must hold the
     // same values, checked as max(v) == v and max(-v) == -v in one one-shot
     // MAX allreduce; the fused launches follow without returning to Python
-    if (n_agree > 32) return fail(CM_ERR_VALUE, "at most 32 agreement values");
+    if (n_agree > 4) return fail(CM_ERR_VALUE, "at most 4 agreement values");
     int64_t vals[64], mx[64];
     for (int i = 0; i < n_agree; ++i) { vals[i] = agree_values[i]; vals[n_agree + i] = -agree_values[i]; }
     if ((st = cm_agree(c, vals, 2 * n_agree, mx, stream_))) return st;

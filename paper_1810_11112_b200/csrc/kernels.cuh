@@ -71,7 +71,7 @@ struct Rec {
   long long redoff;  // element i of the sender's segment at heap + redoff + (i-seg_off)*sz
 };
 
-enum SrcMode { SRC_COPYIN = 0, SRC_PRESTAGED = 1, SRC_ZEROCOPY = 2 };
+enum SrcMode { SRC_COPYIN = 0, SRC_PRESTAGED = 1, SRC_ZEROCOPY = 2, SRC_INLINE = 3 };
 enum Order { ORD_SEQ = 0, ORD_RING = 1, ORD_TREE = 2 };
 enum Phase { PH_RS = 1, PH_AG = 2 };
 enum Err { ERR_SHAPE = 1, ERR_TRANSPORT = 4 };
@@ -103,6 +103,9 @@ struct CollParams {
   long long ll_units;        // LL units per (parity, phase, source)
   unsigned long long* trace; // optional: per-CTA phase timestamps (globaltimer ns)
   int trace_ctas;
+  long long inl[8];          // SRC_INLINE: the input travels in the parameters (cm_agree)
+  unsigned long long* done_flag;  // optional: written with done_value when the call completes
+  unsigned long long done_value;
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -835,7 +838,7 @@ __global__ void __launch_bounds__(THREADS) ll_kernel(const __grid_constant__ Col
   CM_TRACE(P, lr, b, 0);
   const char* in = P.srcmode == SRC_PRESTAGED
                        ? myheap + P.staging_off + (long long)par * P.staging_bytes
-                       : P.in[lr];
+                       : P.srcmode == SRC_INLINE ? reinterpret_cast<const char*>(P.inl) : P.in[lr];
   char* out = P.out[lr];
 
   // header units: this CTA's call signature to every rank
@@ -908,7 +911,6 @@ __global__ void __launch_bounds__(THREADS) ll_kernel(const __grid_constant__ Col
 ll_finish:
   __syncthreads();
   CM_TRACE(P, lr, b, 5);
-  CM_TRACE(P, lr, b, 5);
   if (tid == 0) {
     if (s_err) *reinterpret_cast<volatile unsigned*>(P.herr) = (unsigned)s_err;
     __threadfence();
@@ -917,6 +919,10 @@ ll_finish:
       ctrl->done = 0;
       ctrl->epoch = e;
       __threadfence();
+      if (P.done_flag) {                 // host spins on this (cm_agree)
+        __threadfence_system();
+        *reinterpret_cast<volatile unsigned long long*>(P.done_flag) = P.done_value;
+      }
     }
   }
 }
