@@ -253,6 +253,10 @@ def _aggregate_names(grads, names, tp, algo, cfg, sw, registry, handles, stats_o
     reuse = out.__dict__.get("_fused") if out is not None else None
     if reuse is not None and [f.numel() for f in reuse] != [r["total"] for r in plan.runs]:
         raise ShapeError("out= GradientSet does not match this gradient schema")
+    # out= with the same schema: the result tensors are views of the reused
+    # buckets already, so `out` itself is refilled and returned (torch out=)
+    refill = reuse is not None and out.names == list(names) and \
+        out.__dict__.get("_host") is None and not any(r["any_host"] for r in plan.runs)
     result: list[Tensor] = []
     fused_bufs, host_bufs = [], []
     stream = tp._stream()
@@ -273,6 +277,8 @@ def _aggregate_names(grads, names, tp, algo, cfg, sw, registry, handles, stats_o
             if stats_out is not None:
                 stats_out.extend(_stats(run["stats"][k]) for k in range(ncalls.value))
             fused_bufs.append(fused)
+            if refill:
+                continue
             if run["any_host"]:
                 # CUDA-aware semantics: host gradients get host means, copied
                 # into pinned memory on the communicator's stream
@@ -288,6 +294,9 @@ def _aggregate_names(grads, names, tp, algo, cfg, sw, registry, handles, stats_o
         tp.synchronize()
     else:
         tp.poll()
+    if refill:
+        object.__setattr__(out, "iteration", grads.iteration)
+        return out
     gs = GradientSet.__new__(GradientSet)
     object.__setattr__(gs, "tensors", tuple(result))
     object.__setattr__(gs, "iteration", grads.iteration)

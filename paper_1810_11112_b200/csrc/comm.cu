@@ -943,6 +943,37 @@ int cm_fused_allreduce_agreed(cm_comm_t* c, int n, const void* const* sends,
   if ((st = classify(c, recv_fused, &rk))) return st;
   if (rk != CM_KIND_DEVICE) return fail(CM_ERR_UNSUPPORTED, "fused output must be device memory");
   const int p = c->size;
+  if (p == 1) {
+    // single rank: every allreduce is the identity and the mean divides by 1
+    // (collectives.py:119-120), so all fused groups collapse into ONE batched
+    // copy of the members into the concatenated output
+    bool any_host = false;
+    std::vector<const void*> srcs(n);
+    std::vector<void*> dsts(n);
+    std::vector<int64_t> bytes(n);
+    int64_t off = 0;
+    for (int k = 0; k < n; ++k) {
+      int kind = CM_KIND_DEVICE;
+      if (counts[k] > 0 && (st = classify(c, sends[k], &kind))) return st;
+      any_host = any_host || kind == CM_KIND_HOST;
+      srcs[k] = sends[k];
+      dsts[k] = static_cast<char*>(recv_fused) + off;
+      bytes[k] = counts[k] * sz;
+      off += bytes[k];
+    }
+    for (int g = 0; g < ngroups; ++g) {
+      stats[g] = cm_stats_t{0, 0, 0};
+      count_stats(c, stats[g]);
+    }
+    if (any_host) {
+      for (int k = 0; k < n; ++k)
+        if (bytes[k]) CUDA_TRY(cudaMemcpyAsync(dsts[k], srcs[k], bytes[k], cudaMemcpyDefault, stream));
+    } else if ((st = launch_batched_copy(c, n, srcs.data(), dsts.data(), bytes.data(), false, stream))) {
+      return st;
+    }
+    *n_calls = ngroups;
+    return CM_OK;
+  }
   int64_t fused_off = 0;  // elements
   int i = 0;
   for (int g = 0; g < ngroups; ++g) {

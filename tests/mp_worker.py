@@ -125,6 +125,17 @@ def main():
                 h.update(t.to_bytes())
             expect(h.hexdigest() == case["sha"], f"model {case['model']} host={host}")
 
+    # 4a. out= refill: persistent buckets are overwritten with the next step's means
+    layers = I.MODELS["mobilenet_like"]
+    g1 = I.synth_gradients(0, 0, layers, rank)
+    gs1 = P.GradientSet(tuple(P.Tensor(nm, "float32", torch.from_numpy(a).cuda()) for nm, a in g1))
+    gs2 = P.GradientSet(tuple(P.Tensor(nm, "float32", torch.from_numpy(a * 2).cuda()) for nm, a in g1))
+    r1 = P.aggregate(gs1, group, comm)
+    first = [t.payload.clone() for t in r1.tensors]
+    r2 = P.aggregate(gs2, group, comm, out=r1)
+    expect(r2 is r1, "out= returns the refilled GradientSet")
+    expect(all(torch.equal(t.payload, 2 * f) for t, f in zip(r2.tensors, first)), "out= refill values")
+
     # 4b. aggregate with differing ready sets: the device-side agreement check
     # fails and the intersection is negotiated (aggregation.py:152-155)
     schema = I.agg_schema(world)
