@@ -50,6 +50,7 @@ struct cm_comm {
   int64_t ll2_max_bytes = -1;                 // two-shot via LL slots up to here (-1: p x 512 KiB)
   int64_t ll2_units_per_cta = 512;
   int64_t stream_chunk = 0;                   // elements; 0 disables the pipelined two-shot
+  int multi_buffer = 1;                       // batch fused buffers into one launch
   int64_t oneshot_bytes_per_cta = 8 * 1024;
   int64_t twoshot_bytes_per_cta = 4 * 1024;
   int max_ctas = 148;
@@ -193,6 +194,10 @@ struct Launch {
   int out_rel = 0, ag_in_rel = 0, average = 0, layout = CM_LAYOUT_RING;
   int srcmode = SRC_COPYIN;
   const long long* inl = nullptr;   // SRC_INLINE payload (<= 8 words)
+  int nbuf = 1;                     // multi-buffer launch (prestaged, two-shot pull)
+  int64_t bn[MAXBUF] = {};
+  int64_t bboff[MAXBUF] = {};
+  void* bout[MAXBUF] = {};
   unsigned long long* done_flag = nullptr;
   unsigned long long done_value = 0;
   int ll = 0;                       // one-shot through the LL slots
@@ -228,7 +233,30 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
     maxseg = std::max(maxseg, len[q]);
   }
   P.n = L.n;
-  P.hdr = make_hdr(L.n, L.dtype, L.op, L.order, L.phases, L.oneshot, L.average, L.layout);
+  unsigned long long multi_hash = 0;
+  if (L.nbuf > 1) {
+    P.nbuf = L.nbuf;
+    maxseg = 0;
+    multi_hash = 1469598103934665603ull;
+    for (int k = 0; k < L.nbuf; ++k) {
+      int64_t bo[MAXP], bl[MAXP];
+      if (L.layout == CM_LAYOUT_RHD) rhd_layout(L.bn[k], p, bo, bl);
+      else chunk_partition(L.bn[k], p, bo, bl);
+      int64_t mk = 0;
+      for (int q = 0; q < p; ++q) {
+        P.bseg_off[k][q] = bo[q];
+        P.bseg_len[k][q] = bl[q];
+        mk = std::max(mk, bl[q]);
+      }
+      maxseg += mk;                    // per-CTA work spans every buffer
+      P.bn[k] = L.bn[k];
+      P.bboff[k] = L.bboff[k];
+      P.bout[k] = static_cast<char*>(L.bout[k]);
+      multi_hash = (multi_hash ^ (unsigned long long)L.bn[k]) * 1099511628211ull;
+    }
+  }
+  P.hdr = make_hdr(L.nbuf > 1 ? (int64_t)(multi_hash >> 24) : L.n, L.dtype, L.op, L.order, L.phases,
+                   L.oneshot, L.average, L.layout) ^ ((unsigned long long)(L.nbuf - 1) << 51);
   P.timeout_cycles = c->timeout_cycles;
   P.staging_bytes = (long long)c->staging_bytes;
   P.herr = c->herr_dev;
@@ -259,8 +287,9 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
   if (ll == 2 && (maxseg * (int64_t)sz + 7) / 8 > c->ll_units) ll = 0;  // rhd segments > n/p
   // staging capacity (LL kernels read the input directly unless it is prestaged)
   {
-    const int64_t need = (L.srcmode == SRC_ZEROCOPY) ? (maxseg + SLICE_ALIGN) * (int64_t)sz
-                                                    : L.n * (int64_t)sz;
+    int64_t need = (L.srcmode == SRC_ZEROCOPY) ? (maxseg + SLICE_ALIGN) * (int64_t)sz
+                                              : L.n * (int64_t)sz;
+    if (L.nbuf > 1) need = (L.bboff[L.nbuf - 1] + L.bn[L.nbuf - 1]) * (int64_t)sz;
     const bool uses_staging = ll == 0 || L.srcmode == SRC_PRESTAGED;
     if (uses_staging && need > (int64_t)c->staging_bytes)
       return fail(CM_ERR_CONFIG, "message of " + std::to_string(L.n * sz) + " B needs " +
@@ -273,14 +302,16 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
   nb = std::max<int64_t>(1, std::min<int64_t>(nb, std::min(c->max_ctas, MAXBLK)));
   const bool tree = L.order == ORD_TREE;
   // pipelined two-shot when every CTA's slice spans >= 2 chunks
-  const bool pipelined = ll == 0 && !L.oneshot && L.phases == (PH_RS | PH_AG) &&
+  const bool pipelined = ll == 0 && L.nbuf == 1 && !L.oneshot && L.phases == (PH_RS | PH_AG) &&
                          c->stream_chunk > 0 && maxseg / std::max<int64_t>(nb, 1) >= 2 * c->stream_chunk;
   P.stream_chunk = c->stream_chunk;
   KFn k = pick(ll == 1 ? K_LL : ll == 2 ? K_LL2 : pipelined ? K_STREAM : K_COLL, L.dtype, L.op, p, tree);
   if (!k) return fail(CM_ERR_SHAPE, "unsupported dtype");
   void* args[] = {&P};
   int64_t alg = 0;   // busBW bytes of this launch (nccl-tests convention)
-  if (L.phases == (PH_RS | PH_AG) || L.oneshot) alg = 2 * (int64_t)(p - 1) * L.n * (int64_t)sz / p;
+  int64_t ntot = L.n;
+  if (L.nbuf > 1) { ntot = 0; for (int k = 0; k < L.nbuf; ++k) ntot += L.bn[k]; }
+  if (L.phases == (PH_RS | PH_AG) || L.oneshot) alg = 2 * (int64_t)(p - 1) * ntot * (int64_t)sz / p;
   else alg = (int64_t)(p - 1) * L.n * (int64_t)sz / p;
   ProfScope prof_scope(c, stream, 0, alg);
   if (c->virt) {
@@ -303,10 +334,16 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
     else if (ll == 2) in_bytes = 2 * (int64_t)(p - 1) * ((maxseg * (int64_t)sz + 7) / 8) * 16;
     else if (L.oneshot) in_bytes = (int64_t)(p - 1) * L.n * sz;
     else {
-      if (L.phases & PH_RS) in_bytes += (int64_t)(p - 1) * len[r] * sz;
-      if (L.phases & PH_AG)
-        for (int q = 0; q < p; ++q)
-          if (q != r) in_bytes += len[q] * sz;
+      if (L.nbuf > 1) {
+        for (int k = 0; k < L.nbuf; ++k)
+          for (int q = 0; q < p; ++q)
+            in_bytes += (q == r ? (int64_t)(p - 1) : 1) * P.bseg_len[k][q] * (int64_t)sz;
+      } else {
+        if (L.phases & PH_RS) in_bytes += (int64_t)(p - 1) * len[r] * sz;
+        if (L.phases & PH_AG)
+          for (int q = 0; q < p; ++q)
+            if (q != r) in_bytes += len[q] * sz;
+      }
     }
     c->nvlink_in += in_bytes;
   }
@@ -696,6 +733,7 @@ int cm_comm_set_param(cm_comm_t* c, const char* key, int64_t value) {
   else if (k == "ll2_max_bytes") c->ll2_max_bytes = value;
   else if (k == "ll2_units_per_cta") c->ll2_units_per_cta = value;
   else if (k == "stream_chunk") c->stream_chunk = value == 1 ? 0 : ((value + 63) / 64) * 64;
+  else if (k == "multi_buffer") c->multi_buffer = value > 1 ? 1 : 0;
   else if (k == "oneshot_bytes_per_cta") c->oneshot_bytes_per_cta = value;
   else if (k == "twoshot_bytes_per_cta") c->twoshot_bytes_per_cta = value;
   else if (k == "max_ctas") c->max_ctas = (int)std::min<int64_t>(value, MAXBLK);
@@ -711,6 +749,7 @@ int cm_comm_get_param(cm_comm_t* c, const char* key, int64_t* value) {
   else if (k == "ll2_max_bytes") *value = c->ll2_max_bytes;
   else if (k == "ll2_units_per_cta") *value = c->ll2_units_per_cta;
   else if (k == "stream_chunk") *value = c->stream_chunk;
+  else if (k == "multi_buffer") *value = c->multi_buffer ? 2 : 1;
   else if (k == "oneshot_bytes_per_cta") *value = c->oneshot_bytes_per_cta;
   else if (k == "twoshot_bytes_per_cta") *value = c->twoshot_bytes_per_cta;
   else if (k == "max_ctas") *value = c->max_ctas;
@@ -974,77 +1013,126 @@ int cm_fused_allreduce_agreed(cm_comm_t* c, int n, const void* const* sends,
     *n_calls = ngroups;
     return CM_OK;
   }
-  int64_t fused_off = 0;  // elements
-  int i = 0;
-  for (int g = 0; g < ngroups; ++g) {
-    int j = i;
-    int64_t ng = 0;
-    bool any_host = false;
-    while (j < n && group[j] == g) {
-      int k = CM_KIND_DEVICE;
-      // aggregation.py:159-161: classify every member once per allreduce call
-      if (counts[j] > 0 && (st = classify(c, sends[j], &k))) return st;
-      any_host = any_host || (k == CM_KIND_HOST);
-      ng += counts[j];
-      ++j;
+  // Pass 1: per fused group, members, size, algorithm and launch plan
+  struct Grp {
+    int i, j;
+    int64_t ng, off;   // elements, offset in recv_fused
+    bool any_host;
+    Launch L;
+    bool batchable;
+  };
+  std::vector<Grp> gr;
+  {
+    int i = 0;
+    int64_t fused_off = 0;
+    for (int g = 0; g < ngroups; ++g) {
+      Grp G;
+      G.i = i;
+      G.ng = 0;
+      G.any_host = false;
+      int j = i;
+      while (j < n && group[j] == g) {
+        int k = CM_KIND_DEVICE;
+        // aggregation.py:159-161: classify every member once per allreduce call
+        if (counts[j] > 0 && (st = classify(c, sends[j], &k))) return st;
+        G.any_host = G.any_host || (k == CM_KIND_HOST);
+        G.ng += counts[j];
+        ++j;
+      }
+      G.j = j;
+      G.off = fused_off;
+      int concrete;
+      if ((st = cm_resolve_algorithm(algo, G.ng * sz, switch_bytes, &concrete))) return st;
+      cm_algo_stats(concrete, p, c->rank, G.ng, dtype, switch_bytes, &stats[g]);
+      count_stats(c, stats[g]);
+      if (G.ng * sz > (int64_t)c->staging_bytes)
+        return fail(CM_ERR_CONFIG, "fused buffer of " + std::to_string(G.ng * sz) +
+                                       " B exceeds the staging area; lower the fusion threshold");
+      G.L.n = G.ng;
+      G.L.dtype = dtype;
+      G.L.op = CM_SUM;
+      G.L.average = average;
+      plan_algo(c, concrete, G.ng * sz, &G.L);
+      G.L.out[0] = static_cast<char*>(recv_fused) + fused_off * sz;
+      G.batchable = c->multi_buffer && !G.any_host && G.L.ll == 0 && !G.L.oneshot &&
+                    G.L.phases == (PH_RS | PH_AG);
+      gr.push_back(G);
+      fused_off += G.ng;
+      i = j;
     }
-    char* out = static_cast<char*>(recv_fused) + fused_off * sz;
-    int concrete;
-    if ((st = cm_resolve_algorithm(algo, ng * sz, switch_bytes, &concrete))) return st;
-    cm_algo_stats(concrete, p, c->rank, ng, dtype, switch_bytes, &stats[g]);
-    count_stats(c, stats[g]);
+  }
+  // Pass 2: launches. Consecutive two-shot groups with the same layout share
+  // one pack + one multi-buffer launch (up to MAXBUF); others go one by one.
+  size_t g = 0;
+  while (g < gr.size()) {
+    size_t h = g + 1;
+    if (gr[g].batchable) {
+      int64_t tot = gr[g].ng;
+      while (h < gr.size() && h - g < (size_t)MAXBUF && gr[h].batchable &&
+             gr[h].L.order == gr[g].L.order && gr[h].L.layout == gr[g].L.layout &&
+             (tot + gr[h].ng) * sz <= (int64_t)c->staging_bytes) {
+        tot += gr[h].ng;
+        ++h;
+      }
+    }
+    if (h - g > 1) {
+      std::vector<const void*> srcs;
+      std::vector<void*> dsts;
+      std::vector<int64_t> bytes;
+      Launch L = gr[g].L;
+      L.nbuf = (int)(h - g);
+      int64_t boff = 0;
+      for (size_t t = g; t < h; ++t) {
+        for (int k = gr[t].i; k < gr[t].j; ++k) {
+          srcs.push_back(sends[k]);
+          dsts.push_back(reinterpret_cast<void*>((uintptr_t)((boff + 0) * sz)));
+          bytes.push_back(counts[k] * sz);
+          boff += counts[k];
+        }
+        L.bn[t - g] = gr[t].ng;
+        L.bboff[t - g] = boff - gr[t].ng;
+        L.bout[t - g] = gr[t].L.out[0];
+      }
+      // staged pack offsets are byte offsets; members of all groups are consecutive
+      {
+        int64_t o = 0;
+        for (size_t q = 0; q < dsts.size(); ++q) { dsts[q] = reinterpret_cast<void*>((uintptr_t)o); o += bytes[q]; }
+      }
+      if ((st = launch_batched_copy(c, (int)srcs.size(), srcs.data(), dsts.data(), bytes.data(), true, stream)))
+        return st;
+      L.srcmode = SRC_PRESTAGED;
+      L.n = L.bn[0];
+      if ((st = launch_collective(c, L, stream))) return st;
+      g = h;
+      continue;
+    }
+    Grp& G = gr[g];
     std::vector<const void*> srcs;
     std::vector<void*> dsts;
     std::vector<int64_t> bytes;
     int64_t off = 0;
-    for (int k = i; k < j; ++k) {
+    for (int k = G.i; k < G.j; ++k) {
       srcs.push_back(sends[k]);
       bytes.push_back(counts[k] * sz);
-      dsts.push_back(nullptr);
+      dsts.push_back(reinterpret_cast<void*>((uintptr_t)off));
       off += counts[k] * sz;
     }
-    if (ng * sz > (int64_t)c->staging_bytes)
-      return fail(CM_ERR_CONFIG, "fused buffer of " + std::to_string(ng * sz) +
-                                     " B exceeds the staging area; lower the fusion threshold");
-    if (p == 1) {  // allreduce is the identity; the mean divides by 1
+    Launch L = G.L;
+    if (G.any_host) {  // bounce through device scratch, then copy-in
       off = 0;
-      for (int k = i; k < j; ++k) { dsts[k - i] = out + off; off += counts[k] * sz; }
-      if (any_host) {
-        for (int k = i; k < j; ++k)
-          if (counts[k]) CUDA_TRY(cudaMemcpyAsync(dsts[k - i], srcs[k - i], bytes[k - i], cudaMemcpyDefault, stream));
-      } else if ((st = launch_batched_copy(c, j - i, srcs.data(), dsts.data(), bytes.data(), false, stream))) {
+      for (int k = G.i; k < G.j; ++k) {
+        if (counts[k]) CUDA_TRY(cudaMemcpyAsync(c->scratch + off, sends[k], counts[k] * sz, cudaMemcpyDefault, stream));
+        off += counts[k] * sz;
+      }
+      L.srcmode = SRC_COPYIN;
+      L.in[0] = c->scratch;
+    } else {         // pack straight into the IPC staging area (no extra copy)
+      if ((st = launch_batched_copy(c, G.j - G.i, srcs.data(), dsts.data(), bytes.data(), true, stream)))
         return st;
-      }
-    } else {
-      Launch L;
-      L.n = ng;
-      L.dtype = dtype;
-      L.op = CM_SUM;
-      L.average = average;
-      plan_algo(c, concrete, ng * sz, &L);
-      L.out[0] = out;
-      if (any_host) {  // bounce through device scratch, then copy-in
-        off = 0;
-        for (int k = i; k < j; ++k) {
-          if (counts[k]) CUDA_TRY(cudaMemcpyAsync(c->scratch + off, sends[k], counts[k] * sz, cudaMemcpyDefault, stream));
-          off += counts[k] * sz;
-        }
-        L.srcmode = SRC_COPYIN;
-        L.in[0] = c->scratch;
-      } else {         // pack straight into the IPC staging area (no extra copy)
-        off = 0;
-        for (int k = i; k < j; ++k) {
-          dsts[k - i] = reinterpret_cast<void*>((uintptr_t)off);
-          off += counts[k] * sz;
-        }
-        if ((st = launch_batched_copy(c, j - i, srcs.data(), dsts.data(), bytes.data(), true, stream)))
-          return st;
-        L.srcmode = SRC_PRESTAGED;
-      }
-      if ((st = launch_collective(c, L, stream))) return st;
+      L.srcmode = SRC_PRESTAGED;
     }
-    fused_off += ng;
-    i = j;
+    if ((st = launch_collective(c, L, stream))) return st;
+    ++g;
   }
   *n_calls = ngroups;
   return CM_OK;

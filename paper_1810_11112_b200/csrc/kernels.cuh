@@ -37,6 +37,7 @@ constexpr int MAXP = CM_MAX_RANKS;
 constexpr int MAXBLK = 1024;
 constexpr int THREADS = 512;
 constexpr int SLICE_ALIGN = 64;  // elements; slice boundaries are multiples of this
+constexpr int MAXBUF = 4;        // fused buffers per multi-buffer launch
 
 // ---- heap layout (identical on every rank) ---------------------------------
 constexpr size_t CTRL_OFF = 0;
@@ -103,6 +104,16 @@ struct CollParams {
   long long ll_units;        // LL units per (parity, phase, source)
   unsigned long long* trace; // optional: per-CTA phase timestamps (globaltimer ns)
   int trace_ctas;
+  // several fused buffers in ONE launch (aggregate): buffer k holds bn[k]
+  // elements at staging element offset bboff[k] and is written to bout[k];
+  // each keeps its own reduce-scatter layout (so ring chunking, and therefore
+  // the fold order, is exactly that of one allreduce per buffer)
+  int nbuf;
+  long long bn[MAXBUF];
+  long long bboff[MAXBUF];
+  char* bout[MAXBUF];
+  long long bseg_off[MAXBUF][MAXP];
+  long long bseg_len[MAXBUF][MAXP];
   long long inl[8];          // SRC_INLINE: the input travels in the parameters (cm_agree)
   unsigned long long* done_flag;  // optional: written with done_value when the call completes
   unsigned long long done_value;
@@ -420,27 +431,36 @@ __device__ void multi_copy(const CopyRange* R, int nr, VecRange* V) {
   // slot s copies range s % nr at vector offset (s / nr) * bd
   constexpr int NS = MP > 8 ? MP : 8;
   if (nr < 1) return;
-  const int G = NS / nr > 1 ? NS / nr : 1;
-  const int act = nr * G < NS ? nr * G : NS;
-  int sr[NS], sg[NS];
-#pragma unroll
-  for (int k = 0; k < NS; ++k) {
-    sr[k] = k % nr;
-    sg[k] = k / nr;
-  }
-  for (long long j0 = tid; j0 < nvmax; j0 += (long long)bd * G) {
-    uint4 v[NS];
-#pragma unroll
-    for (int k = 0; k < NS; ++k) {
-      const long long j = j0 + (long long)sg[k] * bd;
-      if (k < act && j < V[sr[k]].nv) v[k] = V[sr[k]].src[j];
-    }
+  // ranges are processed in blocks of at most NS (multi-buffer launches have
+  // up to MAXBUF * (p - 1) ranges)
+  for (int r0 = 0; r0 < nr; r0 += NS) {
+    const int nrb = nr - r0 < NS ? nr - r0 : NS;
+    const VecRange* VB = V + r0;
+    long long nvb = 0;
+    for (int r = 0; r < nrb; ++r) nvb = VB[r].nv > nvb ? VB[r].nv : nvb;
+    const int G = NS / nrb > 1 ? NS / nrb : 1;
+    const int act = nrb * G < NS ? nrb * G : NS;
+    int sr[NS], sg[NS];
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
-      const long long j = j0 + (long long)sg[k] * bd;
-      if (k < act && j < V[sr[k]].nv) V[sr[k]].dst[j] = v[k];
+      sr[k] = k % nrb;
+      sg[k] = k / nrb;
+    }
+    for (long long j0 = tid; j0 < nvb; j0 += (long long)bd * G) {
+      uint4 v[NS];
+#pragma unroll
+      for (int k = 0; k < NS; ++k) {
+        const long long j = j0 + (long long)sg[k] * bd;
+        if (k < act && j < VB[sr[k]].nv) v[k] = VB[sr[k]].src[j];
+      }
+#pragma unroll
+      for (int k = 0; k < NS; ++k) {
+        const long long j = j0 + (long long)sg[k] * bd;
+        if (k < act && j < VB[sr[k]].nv) VB[sr[k]].dst[j] = v[k];
+      }
     }
   }
+  (void)nvmax;
 }
 
 __device__ __forceinline__ bool al16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
@@ -618,8 +638,8 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
   }
 
   // 1. copy-in: this CTA's slice of every segment peers will read from me
-  __shared__ CopyRange s_cr[MAXP + 1];
-  __shared__ VecRange s_vr[MAXP + 1];
+  __shared__ CopyRange s_cr[MAXBUF * MAXP + 1];
+  __shared__ VecRange s_vr[MAXBUF * MAXP + 1];
   __shared__ int s_ncr;
   if (P.srcmode == SRC_COPYIN) {
     char* stage = myheap + stage_off;
@@ -691,6 +711,50 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
     // published it. Reduce-scatter of chunk k+1 overlaps allgather of chunk k,
     // so there is no CTA-wide mid barrier and no idle link between phases.
     stream_body<D, OP, MP, TREE>(P, rank, b, nb, e, s_src, s_red, s_seq, &s_err, out, myheap);
+    goto finish;
+  }
+
+  if (P.nbuf > 1) {
+    // ---- several fused buffers, one launch: RS of every buffer, ONE
+    // RS->AG barrier, AG of every buffer (input prestaged in staging)
+    __shared__ const char* s_seqk[MAXP];
+    int m = 1;
+    while ((m << 1) <= p) m <<= 1;
+    const int excess = p - m;
+    char* mystage = myheap + stage_off;
+    for (int k = 0; k < P.nbuf; ++k) {
+      if (tid < p) s_seqk[tid] = s_seq[tid] + P.bboff[k] * SZ;
+      __syncthreads();
+      const long long so = P.bseg_off[k][rank], sl = P.bseg_len[k][rank];
+      char* bo = P.bout[k];
+      char* red = mystage + P.bboff[k] * SZ;           // in place, element 0 of buffer k
+      bool vec = al16(bo) && al16(red);
+      for (int q = 0; q < p; ++q) vec = vec && al16(s_seqk[q]);
+      const long long lo = slice_bound(so, sl, b, nb), hi = slice_bound(so, sl, b + 1, nb);
+      reduce_range<D, OP, MP, TREE>(s_seqk, p, m, excess, lo, hi, vec, P.average, bo, 0, red, 0,
+                                    tid, blockDim.x);
+      __syncthreads();
+    }
+    CM_TRACE(P, lr, b, 3);
+    if (tid < p) st_release_sys(mid_slot(P.heap[tid], b, rank), e);
+    if (tid < p && !wait_geq(mid_slot(myheap, b, tid), e, P.timeout_cycles)) atomicExch(&s_err, ERR_TRANSPORT);
+    __syncthreads();
+    CM_TRACE(P, lr, b, 4);
+    if (s_err) goto finish;
+    if (tid == 0) {
+      int r = 0;
+      for (int k = 0; k < P.nbuf; ++k)
+        for (int q = 0; q < p; ++q) {
+          if (q == rank) continue;
+          const long long so = P.bseg_off[k][q], sl = P.bseg_len[k][q];
+          const long long lo = slice_bound(so, sl, b, nb), hi = slice_bound(so, sl, b + 1, nb);
+          if (hi <= lo) continue;
+          s_cr[r++] = CopyRange{s_src[q] + P.bboff[k] * SZ, P.bout[k], 0, 0, lo, hi};
+        }
+      s_ncr = r;
+    }
+    __syncthreads();
+    multi_copy<D, MP>(s_cr, s_ncr, s_vr);
     goto finish;
   }
 

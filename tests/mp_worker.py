@@ -125,6 +125,24 @@ def main():
                 h.update(t.to_bytes())
             expect(h.hexdigest() == case["sha"], f"model {case['model']} host={host}")
 
+    # 4c. multi-buffer launches: many large fused groups (threshold 8 MB) share
+    # one pack + one launch per MAXBUF groups; results vs the oracle
+    from oracle import aggregation as OA
+    layers = [480_000] * 12 + [1_000_003, 77]
+    per_rank = [I.synth_gradients(3, 0, layers, r) for r in range(world)]
+    for algo in ("ring_rsa", "rhd_rsa", "auto"):
+        want, groups, _ = OA.aggregate(per_rank, "float32", algo, 8 << 20)
+        for mb in (2, 1):
+            comm.set_param("multi_buffer", mb)
+            gs = P.GradientSet(tuple(P.Tensor(nm, "float32", torch.from_numpy(a).cuda())
+                                     for nm, a in per_rank[rank]))
+            stats = []
+            res = P.aggregate(gs, group, comm, algo=algo, cfg=P.FusionConfig(8 << 20), stats_out=stats)
+            expect(len(stats) == len(groups), "multi-buffer call count")
+            expect(all(t.to_bytes() == want[t.name].tobytes() for t in res.tensors),
+                   f"multi-buffer aggregate {algo} mb={mb}")
+    comm.set_param("multi_buffer", 2)
+
     # 4a. out= refill: persistent buckets are overwritten with the next step's means
     layers = I.MODELS["mobilenet_like"]
     g1 = I.synth_gradients(0, 0, layers, rank)
