@@ -804,24 +804,20 @@ int cm_comm_poll(cm_comm_t* c) { return check_async_error(c); }
 // Element-wise MAX over ranks of n int64 host values, synchronously: the
 // control-plane primitive behind negotiate_ready's fast path (one one-shot
 // kernel over NVLink instead of a host gather/broadcast).
-int cm_agree(cm_comm_t* c, const int64_t* values, int n, int64_t* maxes, void* stream_) {
-  if (n < 1 || n > 8) return fail(CM_ERR_VALUE, "cm_agree takes 1..8 values");
-  if (c->virt) return fail(CM_ERR_UNSUPPORTED, "cm_agree needs a real communicator");
-  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
-  if (c->size == 1) {
-    memcpy(maxes, values, n * sizeof(int64_t));
-    return CM_OK;
-  }
-  if (!c->agree_host) {      // mapped pinned: kernel writes result + completion word
+}  // extern "C"
+
+namespace {
+// launch half of cm_agree: values travel in the kernel parameters, the result
+// lands in mapped host memory with a completion ticket
+int agree_launch(cm_comm* c, const int64_t* values, int n, cudaStream_t stream,
+                 unsigned long long* ticket_out) {
+  if (!c->agree_host) {
     CUDA_TRY(cudaHostAlloc(&c->agree_host, 16 * sizeof(int64_t), cudaHostAllocMapped));
     CUDA_TRY(cudaHostGetDevicePointer((void**)&c->agree_dev, c->agree_host, 0));
     memset(c->agree_host, 0, 16 * sizeof(int64_t));
   }
-  // values travel in the kernel parameters, the result lands in pinned host
-  // memory, and the host spins on a completion word: one launch, no memcpy
   long long inl[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   for (int i = 0; i < n; ++i) inl[i] = values[i];
-  volatile unsigned long long* flag = reinterpret_cast<volatile unsigned long long*>(c->agree_host + 8);
   const unsigned long long ticket = ++c->agree_ticket;
   Launch L;
   L.n = n;
@@ -837,6 +833,13 @@ int cm_agree(cm_comm_t* c, const int64_t* values, int n, int64_t* maxes, void* s
   L.done_value = ticket;
   int st = launch_collective(c, L, stream);
   if (st) return st;
+  *ticket_out = ticket;
+  return CM_OK;
+}
+
+// wait half: host spin on the completion word
+int agree_wait(cm_comm* c, unsigned long long ticket, int n, int64_t* maxes, cudaStream_t stream) {
+  volatile unsigned long long* flag = reinterpret_cast<volatile unsigned long long*>(c->agree_host + 8);
   const auto t0 = std::chrono::steady_clock::now();
   while (*flag != ticket) {
     if (*reinterpret_cast<volatile unsigned*>(c->herr_host)) break;
@@ -846,9 +849,27 @@ int cm_agree(cm_comm_t* c, const int64_t* values, int n, int64_t* maxes, void* s
       return fail(CM_ERR_TRANSPORT, "cm_agree: peers did not answer within 60 s");
     }
   }
-  if ((st = check_async_error(c))) return st;
+  int st = check_async_error(c);
+  if (st) return st;
   for (int i = 0; i < n; ++i) maxes[i] = reinterpret_cast<volatile int64_t*>(c->agree_host)[i];
   return CM_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int cm_agree(cm_comm_t* c, const int64_t* values, int n, int64_t* maxes, void* stream_) {
+  if (n < 1 || n > 8) return fail(CM_ERR_VALUE, "cm_agree takes 1..8 values");
+  if (c->virt) return fail(CM_ERR_UNSUPPORTED, "cm_agree needs a real communicator");
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  if (c->size == 1) {
+    memcpy(maxes, values, n * sizeof(int64_t));
+    return CM_OK;
+  }
+  unsigned long long ticket;
+  int st = agree_launch(c, values, n, stream, &ticket);
+  if (st) return st;
+  return agree_wait(c, ticket, n, maxes, stream);
 }
 
 int cm_comm_counters(cm_comm_t* c, int64_t* messages_sent, int64_t* bytes_sent,
@@ -959,19 +980,34 @@ int cm_fused_allreduce_agreed(cm_comm_t* c, int n, const void* const* sends,
   if (threshold <= 0) return fail(CM_ERR_VALUE, "fusion threshold must be positive");
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
   *n_calls = 0;
+  // negotiation fast path (aggregation.py:72-92): every rank must hold the
+  // same values, checked as max(v) == v and max(-v) == -v in one one-shot MAX
+  // allreduce. The check is launched first; the first pack (local only) is
+  // queued behind it before the host waits, and the first collective is
+  // launched only once agreement is known.
+  int64_t agree_vals[8];
+  unsigned long long ticket = 0;
+  bool pending = false;
   if (n_agree > 0) {
-    // negotiation fast path (aggregation.py:72-92): every rank must hold the
-    // same values, checked as max(v) == v and max(-v) == -v in one one-shot
-    // MAX allreduce; the fused launches follow without returning to Python
     if (n_agree > 4) return fail(CM_ERR_VALUE, "at most 4 agreement values");
-    int64_t vals[64], mx[64];
-    for (int i = 0; i < n_agree; ++i) { vals[i] = agree_values[i]; vals[n_agree + i] = -agree_values[i]; }
-    if ((st = cm_agree(c, vals, 2 * n_agree, mx, stream_))) return st;
-    bool same = true;
-    for (int i = 0; i < 2 * n_agree; ++i) same = same && mx[i] == vals[i];
-    *agreed = same ? 1 : 0;
-    if (!same) return CM_OK;
+    if (c->size > 1) {
+      for (int i = 0; i < n_agree; ++i) { agree_vals[i] = agree_values[i]; agree_vals[n_agree + i] = -agree_values[i]; }
+      if ((st = agree_launch(c, agree_vals, 2 * n_agree, stream, &ticket))) return st;
+      pending = true;
+    }
+    *agreed = 1;
   }
+  auto resolve_agree = [&]() -> int {
+    if (!pending) return CM_OK;
+    pending = false;
+    int64_t mx[8];
+    int s2 = agree_wait(c, ticket, 2 * n_agree, mx, stream);
+    if (s2) return s2;
+    bool same = true;
+    for (int i = 0; i < 2 * n_agree; ++i) same = same && mx[i] == agree_vals[i];
+    *agreed = same ? 1 : 0;
+    return CM_OK;
+  };
   const int64_t sz = (int64_t)dtype_size(dtype);
   std::vector<int64_t> nbytes(n);
   std::vector<int> dts(n, dtype), group(n);
@@ -1044,7 +1080,6 @@ int cm_fused_allreduce_agreed(cm_comm_t* c, int n, const void* const* sends,
       int concrete;
       if ((st = cm_resolve_algorithm(algo, G.ng * sz, switch_bytes, &concrete))) return st;
       cm_algo_stats(concrete, p, c->rank, G.ng, dtype, switch_bytes, &stats[g]);
-      count_stats(c, stats[g]);
       if (G.ng * sz > (int64_t)c->staging_bytes)
         return fail(CM_ERR_CONFIG, "fused buffer of " + std::to_string(G.ng * sz) +
                                        " B exceeds the staging area; lower the fusion threshold");
@@ -1102,6 +1137,8 @@ int cm_fused_allreduce_agreed(cm_comm_t* c, int n, const void* const* sends,
         return st;
       L.srcmode = SRC_PRESTAGED;
       L.n = L.bn[0];
+      if ((st = resolve_agree())) return st;
+      if (!*agreed) return CM_OK;            // the queued pack only touched local staging
       if ((st = launch_collective(c, L, stream))) return st;
       g = h;
       continue;
@@ -1131,9 +1168,12 @@ int cm_fused_allreduce_agreed(cm_comm_t* c, int n, const void* const* sends,
         return st;
       L.srcmode = SRC_PRESTAGED;
     }
+    if ((st = resolve_agree())) return st;
+    if (!*agreed) return CM_OK;
     if ((st = launch_collective(c, L, stream))) return st;
     ++g;
   }
+  for (int q = 0; q < ngroups; ++q) count_stats(c, stats[q]);
   *n_calls = ngroups;
   return CM_OK;
 }
