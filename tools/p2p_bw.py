@@ -17,9 +17,10 @@ rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
 torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
 dist.init_process_group("gloo")
 comm = P.Communicator(staging_bytes=1 << 30, pool_bytes=2 << 20, blocking=False)
-for ctas in (148, 296, 592):
-    for mode, name in ((0, "pull"), (1, "push"), (2, "pull-concurrent"), (3, "push-concurrent")):
-        for nb in (4 << 20, 64 << 20):
+SIZES = [int(x) for x in os.environ.get("SIZES", str(64 << 20)).split(",")]
+for ctas in [int(x) for x in os.environ.get("CTAS", "148,296").split(",")]:
+    for mode, name in ((2, "pull-concurrent"), (3, "push-concurrent")):
+        for nb in SIZES:
             per = nb // (world - 1)
             per -= per % 16
             ms = C.c_double()
