@@ -160,6 +160,19 @@ int cm_comm_get_param(cm_comm_t* comm, const char* key, int64_t* value);
  * on every rank). Buffers from here are read by peers in place (zero copy). */
 int cm_comm_alloc(cm_comm_t* comm, int64_t bytes, void** ptr);
 int cm_comm_free(cm_comm_t* comm, void* ptr);
+/* Registered buffers — the pointer cache's IPC side (PAPER §V-B; NCCL-style
+ * user-buffer registration). Collective: every rank exports the buffer it
+ * passes at this registration (allocation handle + offset, cm_comm_export),
+ * the 64-byte handles and offsets are all-gathered over any host channel, and
+ * cm_comm_register opens every peer allocation once (cached) and records the
+ * peer pointers under one id. Later collectives whose send buffer lies inside
+ * a registered range are read by peers in place (no staging copy). Buffers
+ * must stay allocated until cm_comm_deregister. */
+int cm_comm_export(cm_comm_t* comm, const void* ptr, int64_t bytes, void* handle_out,
+                   int64_t* offset);
+int cm_comm_register(cm_comm_t* comm, const void* ptr, int64_t bytes, const void* all_handles,
+                     const int64_t* all_offsets, int64_t* reg_id);
+int cm_comm_deregister(cm_comm_t* comm, const void* ptr);
 /* wait for `stream`, then report any device-side error of earlier calls */
 int cm_comm_sync(cm_comm_t* comm, void* stream);
 /* non-blocking error check of completed calls */

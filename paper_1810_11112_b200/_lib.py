@@ -88,6 +88,9 @@ _SIGS = {
     "cm_comm_get_param": ([_vp, C.c_char_p, _P(_i64)], _i),
     "cm_comm_alloc": ([_vp, _i64, _P(_vp)], _i),
     "cm_comm_free": ([_vp, _vp], _i),
+    "cm_comm_export": ([_vp, _vp, _i64, _vp, _P(_i64)], _i),
+    "cm_comm_register": ([_vp, _vp, _i64, _vp, _P(_i64), _P(_i64)], _i),
+    "cm_comm_deregister": ([_vp, _vp], _i),
     "cm_comm_sync": ([_vp, _vp], _i),
     "cm_comm_poll": ([_vp], _i),
     "cm_agree": ([_vp, _P(_i64), _i, _P(_i64), _vp], _i),

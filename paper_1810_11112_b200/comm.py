@@ -194,6 +194,41 @@ class Communicator(_Base):
         del self._sym[p]
         L.check(L.lib.cm_comm_free(self._h, p))
 
+    def register_buffers(self, tensors) -> list[int]:
+        """Collective: register device tensors for zero-copy collectives (every
+        rank passes its own tensors, same count and order). Each rank exports
+        the CUDA-IPC handle of the allocation holding the tensor plus the
+        offset; handles are all-gathered on the control plane and every peer
+        allocation is opened once (cached). Afterwards, collectives whose send
+        buffer lies inside a registered tensor are read by peers in place. The
+        tensors must stay alive until ``deregister_buffers``."""
+        import torch.distributed as dist
+        mine = []
+        for t in tensors:
+            h = (C.c_char * L.IPC_HANDLE_BYTES)()
+            off = C.c_int64()
+            L.check(L.lib.cm_comm_export(self._h, t.data_ptr(), t.numel() * t.element_size(), h,
+                                         C.byref(off)))
+            mine.append((bytes(h), int(off.value)))
+        gathered = [None] * self.size
+        if self.size > 1:
+            dist.all_gather_object(gathered, mine, group=self._group)
+        else:
+            gathered = [mine]
+        ids = []
+        for i, t in enumerate(tensors):
+            handles = b"".join(gathered[q][i][0] for q in range(self.size))
+            offs = L.i64_array([gathered[q][i][1] for q in range(self.size)])
+            rid = C.c_int64()
+            L.check(L.lib.cm_comm_register(self._h, t.data_ptr(), t.numel() * t.element_size(),
+                                           handles, offs, C.byref(rid)))
+            ids.append(int(rid.value))
+        return ids
+
+    def deregister_buffers(self, tensors) -> None:
+        for t in tensors:
+            L.check(L.lib.cm_comm_deregister(self._h, t.data_ptr()))
+
     def barrier(self) -> None:
         import torch.distributed as dist
         if self.size > 1:

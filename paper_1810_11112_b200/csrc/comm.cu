@@ -6,6 +6,7 @@
 //   pointer cache (no driver query on a cache hit, PAPER §V-B) -> pick the
 //   source mode (zero-copy from the symmetric pool, copy-in, or host staging)
 //   -> ONE kernel launch (one-shot or two-shot) -> logical CollectiveStats.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -42,6 +43,15 @@ struct cm_comm {
   int64_t* agree_host = nullptr;       // mapped pinned: cm_agree result + completion word
   int64_t* agree_dev = nullptr;        // device alias of agree_host
   unsigned long long agree_ticket = 0;
+  // registered buffers (cm_comm_register): local start -> {bytes, id}; opened
+  // peer allocations cached by (peer, handle bytes) -> mapped base
+  struct Reg {
+    int64_t bytes;
+    int64_t id;
+  };
+  std::map<uintptr_t, Reg> regs;
+  std::map<std::string, char*> opened;
+  int64_t next_reg = 0;
   int sms = 148;
   // tuning knobs (cm_comm_set_param)
   int64_t oneshot_max_bytes = 32 * 1024;
@@ -377,6 +387,18 @@ int place(cm_comm* c, const void* send, int64_t send_bytes, void* recv, int64_t 
   } else if (in_pool(c, send, send_bytes)) {
     pl->srcmode = SRC_ZEROCOPY;
     pl->zc = static_cast<const char*>(send) - c->local;
+  } else if (!c->regs.empty() && send_bytes > 0) {
+    // pointer cache: is the send buffer inside a collectively registered range?
+    const uintptr_t a = reinterpret_cast<uintptr_t>(send);
+    auto it = c->regs.upper_bound(a);
+    if (it != c->regs.begin()) {
+      --it;
+      if (a + (uintptr_t)send_bytes <= it->first + (uintptr_t)it->second.bytes) {
+        pl->srcmode = SRC_REGISTERED;
+        pl->zc = (int64_t)(REG_FLAG | ((unsigned long long)it->second.id << 40) |
+                           (unsigned long long)(a - it->first));
+      }
+    }
   }
   if (kr == CM_KIND_HOST) {
     pl->out = c->scratch;
@@ -463,6 +485,11 @@ int do_allreduce(cm_comm* c, const void* const* sends, void* const* recvs, int64
     L.zc_srcoff[0] = pl.zc;
   } else {
     for (int q = 0; q < p; ++q) { L.in[q] = sends[q]; L.out[q] = recvs[q]; }
+  }
+  // a one-shot pull kernel has no barrier after peers read my input, so user
+  // buffers must not be read in place there: stage them
+  if (L.oneshot && !L.ll && (L.srcmode == SRC_ZEROCOPY || L.srcmode == SRC_REGISTERED)) {
+    L.srcmode = SRC_COPYIN;
   }
   if ((st = launch_collective(c, L, stream))) return st;
   if (pl.recv_host) CUDA_TRY(cudaMemcpyAsync(recvs[0], pl.out, nbytes, cudaMemcpyDeviceToHost, stream));
@@ -688,6 +715,7 @@ int cm_comm_destroy(cm_comm_t* c) {
   if (!c->virt)
     for (int q = 0; q < c->size; ++q)
       if (q != c->rank && c->heap[q]) cudaIpcCloseMemHandle(c->heap[q]);
+  for (auto& kv : c->opened) cudaIpcCloseMemHandle(kv.second);
   if (c->local) cudaFree(c->local);
   if (c->scratch) cudaFree(c->scratch);
   if (c->herr_host) cudaFreeHost(c->herr_host);
@@ -791,6 +819,73 @@ int cm_comm_free(cm_comm_t* c, void* ptr) {
     if (pv->first + pv->second == o) { o = pv->first; len += pv->second; c->pool_free.erase(pv); }
   }
   c->pool_free[o] = len;
+  return CM_OK;
+}
+
+int cm_comm_export(cm_comm_t* c, const void* ptr, int64_t bytes, void* handle_out, int64_t* offset) {
+  if (c->virt) return fail(CM_ERR_UNSUPPORTED, "virtual groups do not register buffers");
+  static CUresult (*get_range)(CUdeviceptr*, size_t*, CUdeviceptr) = nullptr;
+  if (!get_range) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) {
+      cudaGetLastError();
+      return fail(CM_ERR_UNSUPPORTED, "cuMemGetAddressRange unavailable");
+    }
+    get_range = reinterpret_cast<CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr)>(fn);
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (get_range(&base, &size, reinterpret_cast<CUdeviceptr>(ptr)) != CUDA_SUCCESS)
+    return fail(CM_ERR_UNKNOWN_BUFFER, "not device memory of this process (cuMemGetAddressRange)");
+  if (reinterpret_cast<uintptr_t>(ptr) + (uintptr_t)bytes > (uintptr_t)base + size)
+    return fail(CM_ERR_SHAPE, "buffer crosses the end of its allocation");
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+  memcpy(handle_out, &h, sizeof h);
+  *offset = (int64_t)(reinterpret_cast<uintptr_t>(ptr) - (uintptr_t)base);
+  return CM_OK;
+}
+
+int cm_comm_register(cm_comm_t* c, const void* ptr, int64_t bytes, const void* all_handles,
+                     const int64_t* all_offsets, int64_t* reg_id) {
+  if (c->virt) return fail(CM_ERR_UNSUPPORTED, "virtual groups do not register buffers");
+  if (c->next_reg >= MAXREG) return fail(CM_ERR_CONFIG, "registered-buffer table is full");
+  const int p = c->size;
+  char* table[MAXP] = {};
+  const char* hs = static_cast<const char*>(all_handles);
+  for (int q = 0; q < p; ++q) {
+    if (q == c->rank) { table[q] = static_cast<char*>(const_cast<void*>(ptr)); continue; }
+    const std::string key = std::to_string(q) + ":" + std::string(hs + (size_t)q * CM_IPC_HANDLE_BYTES, CM_IPC_HANDLE_BYTES);
+    auto it = c->opened.find(key);
+    char* base;
+    if (it != c->opened.end()) {
+      base = it->second;
+    } else {
+      cudaIpcMemHandle_t h;
+      memcpy(&h, hs + (size_t)q * CM_IPC_HANDLE_BYTES, sizeof h);
+      void* mapped = nullptr;
+      CUDA_TRY(cudaIpcOpenMemHandle(&mapped, h, cudaIpcMemLazyEnablePeerAccess));
+      base = static_cast<char*>(mapped);
+      c->opened[key] = base;
+    }
+    table[q] = base + all_offsets[q];
+  }
+  const int64_t id = c->next_reg++;
+  CUDA_TRY(cudaMemcpy(c->local + REG_OFF + (size_t)id * MAXP * 8, table, sizeof(char*) * MAXP,
+                      cudaMemcpyHostToDevice));
+  c->regs[reinterpret_cast<uintptr_t>(ptr)] = cm_comm::Reg{bytes, id};
+  // the pointer cache now knows this range (intercept-style insert)
+  c->reg.register_range(reinterpret_cast<uint64_t>(ptr), bytes, CM_KIND_DEVICE);
+  *reg_id = id;
+  return CM_OK;
+}
+
+int cm_comm_deregister(cm_comm_t* c, const void* ptr) {
+  auto it = c->regs.find(reinterpret_cast<uintptr_t>(ptr));
+  if (it == c->regs.end()) return fail(CM_ERR_INVALID_HANDLE, "buffer is not registered");
+  c->regs.erase(it);
+  c->reg.unregister_range(reinterpret_cast<uint64_t>(ptr));
   return CM_OK;
 }
 

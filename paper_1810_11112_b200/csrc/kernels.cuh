@@ -55,8 +55,15 @@ constexpr size_t WMID_OFF = MID_OFF + MID_SIZE;         // per-warp progress of 
 constexpr size_t WMID_SIZE = (size_t)MAXBLK * MAXP * 8 * 8;
 constexpr size_t LLH_OFF = WMID_OFF + WMID_SIZE;        // per-CTA LL header units
 constexpr size_t LLH_SIZE = 2ull * MAXBLK * MAXP * 16;
+// registered-buffer table: REGTAB[id][q] = rank q's registered buffer start,
+// mapped in THIS process (cm_comm_register, the IPC side of the pointer cache)
+constexpr int MAXREG = 4096;
+constexpr size_t REG_OFF = LLH_OFF + LLH_SIZE;
+constexpr size_t REG_SIZE = (size_t)MAXREG * MAXP * 8;
 constexpr size_t HEAP_ALIGN = 2ull << 20;
-constexpr size_t LL_OFF = ((LLH_OFF + LLH_SIZE + HEAP_ALIGN - 1) / HEAP_ALIGN) * HEAP_ALIGN;
+constexpr size_t LL_OFF = ((REG_OFF + REG_SIZE + HEAP_ALIGN - 1) / HEAP_ALIGN) * HEAP_ALIGN;
+// record source encoding for registered inputs: bit 62 | id << 40 | byte delta
+constexpr unsigned long long REG_FLAG = 1ull << 62;
 constexpr size_t CTRL_REGION = LL_OFF;                  // zeroed at creation
 
 struct Ctrl {
@@ -72,7 +79,7 @@ struct Rec {
   long long redoff;  // element i of the sender's segment at heap + redoff + (i-seg_off)*sz
 };
 
-enum SrcMode { SRC_COPYIN = 0, SRC_PRESTAGED = 1, SRC_ZEROCOPY = 2, SRC_INLINE = 3 };
+enum SrcMode { SRC_COPYIN = 0, SRC_PRESTAGED = 1, SRC_ZEROCOPY = 2, SRC_INLINE = 3, SRC_REGISTERED = 4 };
 enum Order { ORD_SEQ = 0, ORD_RING = 1, ORD_TREE = 2 };
 enum Phase { PH_RS = 1, PH_AG = 2 };
 enum Err { ERR_SHAPE = 1, ERR_TRANSPORT = 4 };
@@ -624,8 +631,8 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
   // my own src/red offsets (published to peers)
   long long my_srcoff, my_redoff;
   const long long mso = P.seg_off[rank];
-  if (P.srcmode == SRC_ZEROCOPY) {
-    my_srcoff = P.zc_srcoff[lr];
+  if (P.srcmode == SRC_ZEROCOPY || P.srcmode == SRC_REGISTERED) {
+    my_srcoff = P.zc_srcoff[lr];           // heap offset, or REG_FLAG | id | delta
     if (!ag_only)            // reduced segment goes to staging, vector-aligned like the source
       my_redoff = stage_off + (mso % SLICE_ALIGN) * SZ;
     else if (P.ag_in_rel)    // allgather: `in` holds only my segment
@@ -681,7 +688,14 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
       atomicExch(&s_err, ERR_TRANSPORT);
     } else {
       if (ld_relaxed_sys(&r->hdr) != P.hdr) atomicExch(&s_err, ERR_SHAPE);
-      s_src[tid] = P.heap[tid] + ld_relaxed_sys_s64(&r->srcoff);
+      const long long so = ld_relaxed_sys_s64(&r->srcoff);
+      if ((unsigned long long)so & REG_FLAG) {   // peer's registered buffer, mapped here
+        const long long id = (so >> 40) & 0x3FFFFF, delta = so & ((1ll << 40) - 1);
+        const char* base = *reinterpret_cast<char* const*>(myheap + REG_OFF + ((size_t)id * MAXP + tid) * 8);
+        s_src[tid] = base + delta;
+      } else {
+        s_src[tid] = P.heap[tid] + so;
+      }
       s_red[tid] = P.heap[tid] + ld_relaxed_sys_s64(&r->redoff);
     }
   }

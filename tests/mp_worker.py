@@ -83,6 +83,27 @@ def main():
             out, _ = P.allreduce(host, P.ReduceOp.SUM, group, comm, algo=algo)
             expect(not out.is_cuda and out.to_bytes() == want, f"host buffer {algo} n={n}")
 
+    # 2b. registered buffers: peers read ordinary torch tensors in place after a
+    # collective registration (pointer cache of IPC handles); views inside a
+    # registered tensor resolve to it with an offset; mixed modes interoperate
+    n = 9_000_011
+    rng = np.random.default_rng([22, n])
+    xs = [rng.standard_normal(n).astype(np.float32) for _ in range(world)]
+    big = torch.from_numpy(xs[rank]).cuda()
+    comm.register_buffers([big])
+    for algo in ("ring_rsa", "rhd_rsa", "flat"):
+        want = OC.allreduce(xs, "sum", algo, "float32").tobytes()
+        out, _ = P.allreduce(P.Tensor("x", "float32", big), P.ReduceOp.SUM, group, comm, algo=algo)
+        expect(out.to_bytes() == want, f"registered {algo}")
+        sub = [x[1000:5_000_000] for x in xs]
+        out, _ = P.allreduce(P.Tensor("x", "float32", big[1000:5_000_000]), P.ReduceOp.SUM, group, comm,
+                             algo=algo)
+        expect(out.to_bytes() == OC.allreduce(sub, "sum", algo, "float32").tobytes(), f"registered view {algo}")
+        other = big.clone() if rank % 2 else big        # odd ranks: unregistered copy
+        out, _ = P.allreduce(P.Tensor("x", "float32", other), P.ReduceOp.SUM, group, comm, algo=algo)
+        expect(out.to_bytes() == want, f"mixed registered/copy-in {algo}")
+    comm.deregister_buffers([big])
+
     # 3. reduce-scatter / allgather
     for layout in ("ring", "rhd"):
         for n in (0, 3, 1000, 1 << 20):
