@@ -234,12 +234,37 @@ def headline(args, rank, world, local):
     gs = make_grads(args.model, rank, device, args.dtype)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
 
-    state = {"out": None}
+    state = {"out": None, "gs": gs}
 
     def step():   # persistent output buckets: aggregate(out=previous result)
-        state["out"] = P.aggregate(gs, group, comm, algo=args.algo, cfg=cfg,
+        state["out"] = P.aggregate(state["gs"], group, comm, algo=args.algo, cfg=cfg,
                                    switch_bytes=args.switch, out=state["out"])
         return state["out"]
+
+    def timed_steps(k):
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(k)]
+        barrier(world)
+        torch.cuda.synchronize()
+        for i in range(k):
+            flush.zero_()
+            ev[i][0].record()
+            step()
+            ev[i][1].record()
+        torch.cuda.synchronize()
+        barrier(world)
+        return max_over_ranks(statistics.mean(a.elapsed_time(b) for a, b in ev), world)
+
+    # unregistered gradients first (pack into the IPC staging heap every step)
+    ms_unreg = None
+    if world > 1 and not args.no_register:
+        for _ in range(args.warmup):
+            step()
+        ms_unreg = timed_steps(max(10, args.steps // 4))
+        # then register the gradient tensors once (collective, outside the
+        # timed region): peers read them in place, the pack disappears
+        P.register_gradients(gs, comm)
+        state["out"] = None
 
     sampler = ClockSampler(local)
     sampler.start_and_wait()
@@ -372,7 +397,11 @@ def headline(args, rank, world, local):
                        "fusion_threshold": args.fusion_threshold, "algo": args.algo,
                        "switch_bytes": args.switch, "parallelism": f"dp{world}",
                        "l2": "flushed: 256 MiB memset between timed steps (outside the events)",
-                       "outputs": "persistent fused output buckets (aggregate(out=prev))"},
+                       "outputs": "persistent fused output buckets (aggregate(out=prev))",
+                       "gradients": ("registered once with register_gradients (outside the timed "
+                                     "region): peers read them in place, no pack")
+                       if (world > 1 and not args.no_register) else "unregistered: packed every step"},
+            "ms_per_step_unregistered": None if ms_unreg is None else round(ms_unreg, 4),
             "latency_us": round(ms * 1e3, 2),
             "bus_gbps": round(2 * (world - 1) / world * S / (ms * 1e-3) / 1e9, 2) if world > 1 else None,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
@@ -654,6 +683,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-nccl", action="store_true")
     ap.add_argument("--no-check", action="store_true")
+    ap.add_argument("--no-register", action="store_true",
+                    help="do not register the gradient tensors (pack them every step)")
     ap.add_argument("--param", action="append", default=[],
                     help="communicator tuning knob key=value (cm_comm_set_param)")
     ap.add_argument("--algos", default="rhd_rsa,ring_rsa", help="sweep: algorithms to time")

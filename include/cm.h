@@ -228,12 +228,16 @@ int cm_fused_allreduce(cm_comm_t* comm, int n, const void* const* sends, const i
  * same n_agree (<= 4) values (e.g. a hash of its ready names) when its ready
  * set is identical; *agreed = 1 and the fused launches follow in the same call,
  * or *agreed = 0 and nothing is launched (the caller negotiates the
- * intersection, aggregation.py:72-92, and calls again). */
+ * intersection, aggregation.py:72-92, and calls again). reg_ids (nullable):
+ * per member, its cm_comm_register id (same on every rank) or -1; fused groups
+ * whose members are all registered skip the pack — peers read the member
+ * tensors in place. */
 int cm_fused_allreduce_agreed(cm_comm_t* comm, int n, const void* const* sends,
                               const int64_t* counts, int dtype, void* recv_fused, int algo,
                               int64_t threshold, int64_t switch_bytes, int average,
-                              const int64_t* agree_values, int n_agree, int* agreed, void* stream,
-                              cm_stats_t* stats, int* n_calls);
+                              const int64_t* agree_values, int n_agree, int* agreed,
+                              const int64_t* reg_ids, void* stream, cm_stats_t* stats,
+                              int* n_calls);
 
 /* virtual-group variants: arrays of `size` per-rank pointers */
 int cm_allreduce_v(cm_comm_t* comm, const void* const* sends, void* const* recvs, int64_t count,

@@ -105,7 +105,7 @@ _SIGS = {
     "cm_fused_allreduce": ([_vp, _i, _P(_vp), _P(_i64), _i, _vp, _i, _i64, _i64, _i, _vp,
                             _P(Stats), _P(_i)], _i),
     "cm_fused_allreduce_agreed": ([_vp, _i, _P(_vp), _P(_i64), _i, _vp, _i, _i64, _i64, _i,
-                                   _P(_i64), _i, _P(_i), _vp, _P(Stats), _P(_i)], _i),
+                                   _P(_i64), _i, _P(_i), _P(_i64), _vp, _P(Stats), _P(_i)], _i),
     "cm_allreduce_v": ([_vp, _P(_vp), _P(_vp), _i64, _i, _i, _i, _i64, _i, _vp, _P(Stats)], _i),
     "cm_reduce_scatter_v": ([_vp, _P(_vp), _P(_vp), _i64, _i, _i, _i, _vp, _P(Stats)], _i),
     "cm_allgather_v": ([_vp, _P(_vp), _P(_vp), _i64, _i, _i, _vp, _P(Stats)], _i),

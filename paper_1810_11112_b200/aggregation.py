@@ -184,7 +184,12 @@ class _Plan:
                 if t.dtype not in ("float32", "float64", "bfloat16"):
                     raise ShapeError(f"aggregate averages floating-point gradients, got {t.dtype}")
             counts = [t.len for t in run]
+            regmap = grads.__dict__.get("_reg_ids")
+            reg = None
+            if regmap is not None and all(t.name in regmap for t in run):
+                reg = L.i64_array([regmap[t.name] for t in run])
             self.runs.append(dict(
+                reg=reg,
                 dtype=run[0].dtype, names=[t.name for t in run], counts=counts,
                 total=sum(counts), any_host=any(not t.is_cuda for t in run),
                 ptrs=L.ptr_array([t.payload.data_ptr() for t in run]),
@@ -239,6 +244,23 @@ def aggregate(grads: GradientSet, group: GroupSpec, transport: Communicator,
     return res
 
 
+def register_gradients(grads: GradientSet, transport: Communicator) -> None:
+    """Collective: register every gradient tensor of ``grads`` (sorted by
+    name, so ids agree across ranks) for zero-copy aggregation. Later
+    ``aggregate`` calls on this GradientSet skip the pack: peers read the
+    member tensors in place through the registered IPC mappings (the pointer
+    cache of PAPER §V-B applied to peer mappings). The tensors must stay
+    allocated for the lifetime of the registration."""
+    tp = transport
+    ordered = sorted(grads.tensors, key=lambda t: t.name)
+    for t in ordered:
+        if not t.is_cuda:
+            raise ShapeError(f"{t.name}: only device tensors can be registered")
+    ids = tp.register_buffers([t.payload for t in ordered]) if ordered else []
+    object.__setattr__(grads, "_reg_ids", {t.name: i for t, i in zip(ordered, ids)})
+    grads.__dict__.pop("_plans", None)
+
+
 def _aggregate_names(grads, names, tp, algo, cfg, sw, registry, handles, stats_out, out, agree):
     if not names:
         return GradientSet((), grads.iteration)
@@ -270,7 +292,7 @@ def _aggregate_names(grads, names, tp, algo, cfg, sw, registry, handles, stats_o
             L.check(L.lib.cm_fused_allreduce_agreed(
                 tp._h, run["n"], run["ptrs"], run["counts_c"], L.DTYPE[dtype], fused.data_ptr(),
                 L.ALGO[algo], int(cfg.threshold_bytes), sw, 1, agree, 2 if agree is not None else 0,
-                C.byref(agreed), stream, run["stats"], C.byref(ncalls)))
+                C.byref(agreed), run["reg"], stream, run["stats"], C.byref(ncalls)))
             if not agreed.value:
                 return None             # nothing was launched
             agree = None

@@ -51,6 +51,7 @@ struct cm_comm {
   };
   std::map<uintptr_t, Reg> regs;
   std::map<std::string, char*> opened;
+  std::map<std::string, long long*> gtabs;   // member tables of registered fused batches
   int64_t next_reg = 0;
   int sms = 148;
   // tuning knobs (cm_comm_set_param)
@@ -204,6 +205,9 @@ struct Launch {
   int out_rel = 0, ag_in_rel = 0, average = 0, layout = CM_LAYOUT_RING;
   int srcmode = SRC_COPYIN;
   const long long* inl = nullptr;   // SRC_INLINE payload (<= 8 words)
+  const long long* gtab = nullptr;  // SRC_GATHER member table (device)
+  int gmem = 0;
+  unsigned long long gsig = 0;      // member-table signature (checked across ranks)
   int nbuf = 1;                     // multi-buffer launch (prestaged, two-shot pull)
   int64_t bn[MAXBUF] = {};
   int64_t bboff[MAXBUF] = {};
@@ -244,7 +248,9 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
   }
   P.n = L.n;
   unsigned long long multi_hash = 0;
-  if (L.nbuf > 1) {
+  P.gtab = L.gtab;
+  P.gmem = L.gmem;
+  if (L.nbuf > 1 || L.srcmode == SRC_GATHER) {
     P.nbuf = L.nbuf;
     maxseg = 0;
     multi_hash = 1469598103934665603ull;
@@ -264,8 +270,9 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
       P.bout[k] = static_cast<char*>(L.bout[k]);
       multi_hash = (multi_hash ^ (unsigned long long)L.bn[k]) * 1099511628211ull;
     }
+    multi_hash = (multi_hash ^ L.gsig) * 1099511628211ull;
   }
-  P.hdr = make_hdr(L.nbuf > 1 ? (int64_t)(multi_hash >> 24) : L.n, L.dtype, L.op, L.order, L.phases,
+  P.hdr = make_hdr(P.nbuf >= 1 && (L.nbuf > 1 || L.srcmode == SRC_GATHER) ? (int64_t)(multi_hash >> 24) : L.n, L.dtype, L.op, L.order, L.phases,
                    L.oneshot, L.average, L.layout) ^ ((unsigned long long)(L.nbuf - 1) << 51);
   P.timeout_cycles = c->timeout_cycles;
   P.staging_bytes = (long long)c->staging_bytes;
@@ -299,7 +306,7 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
   {
     int64_t need = (L.srcmode == SRC_ZEROCOPY) ? (maxseg + SLICE_ALIGN) * (int64_t)sz
                                               : L.n * (int64_t)sz;
-    if (L.nbuf > 1) need = (L.bboff[L.nbuf - 1] + L.bn[L.nbuf - 1]) * (int64_t)sz;
+    if (L.nbuf > 1 || L.srcmode == SRC_GATHER) need = (L.bboff[L.nbuf - 1] + L.bn[L.nbuf - 1]) * (int64_t)sz;
     const bool uses_staging = ll == 0 || L.srcmode == SRC_PRESTAGED;
     if (uses_staging && need > (int64_t)c->staging_bytes)
       return fail(CM_ERR_CONFIG, "message of " + std::to_string(L.n * sz) + " B needs " +
@@ -312,7 +319,8 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
   nb = std::max<int64_t>(1, std::min<int64_t>(nb, std::min(c->max_ctas, MAXBLK)));
   const bool tree = L.order == ORD_TREE;
   // pipelined two-shot when every CTA's slice spans >= 2 chunks
-  const bool pipelined = ll == 0 && L.nbuf == 1 && !L.oneshot && L.phases == (PH_RS | PH_AG) &&
+  const bool pipelined = ll == 0 && L.nbuf == 1 && L.srcmode != SRC_GATHER && !L.oneshot &&
+                         L.phases == (PH_RS | PH_AG) &&
                          c->stream_chunk > 0 && maxseg / std::max<int64_t>(nb, 1) >= 2 * c->stream_chunk;
   P.stream_chunk = c->stream_chunk;
   KFn k = pick(ll == 1 ? K_LL : ll == 2 ? K_LL2 : pipelined ? K_STREAM : K_COLL, L.dtype, L.op, p, tree);
@@ -320,7 +328,7 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
   void* args[] = {&P};
   int64_t alg = 0;   // busBW bytes of this launch (nccl-tests convention)
   int64_t ntot = L.n;
-  if (L.nbuf > 1) { ntot = 0; for (int k = 0; k < L.nbuf; ++k) ntot += L.bn[k]; }
+  if (L.nbuf > 1 || L.srcmode == SRC_GATHER) { ntot = 0; for (int k = 0; k < L.nbuf; ++k) ntot += L.bn[k]; }
   if (L.phases == (PH_RS | PH_AG) || L.oneshot) alg = 2 * (int64_t)(p - 1) * ntot * (int64_t)sz / p;
   else alg = (int64_t)(p - 1) * L.n * (int64_t)sz / p;
   ProfScope prof_scope(c, stream, 0, alg);
@@ -344,7 +352,7 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
     else if (ll == 2) in_bytes = 2 * (int64_t)(p - 1) * ((maxseg * (int64_t)sz + 7) / 8) * 16;
     else if (L.oneshot) in_bytes = (int64_t)(p - 1) * L.n * sz;
     else {
-      if (L.nbuf > 1) {
+      if (L.nbuf > 1 || L.srcmode == SRC_GATHER) {
         for (int k = 0; k < L.nbuf; ++k)
           for (int q = 0; q < p; ++q)
             in_bytes += (q == r ? (int64_t)(p - 1) : 1) * P.bseg_len[k][q] * (int64_t)sz;
@@ -716,6 +724,7 @@ int cm_comm_destroy(cm_comm_t* c) {
     for (int q = 0; q < c->size; ++q)
       if (q != c->rank && c->heap[q]) cudaIpcCloseMemHandle(c->heap[q]);
   for (auto& kv : c->opened) cudaIpcCloseMemHandle(kv.second);
+  for (auto& kv : c->gtabs) cudaFree(kv.second);
   if (c->local) cudaFree(c->local);
   if (c->scratch) cudaFree(c->scratch);
   if (c->herr_host) cudaFreeHost(c->herr_host);
@@ -1057,15 +1066,16 @@ int cm_fused_allreduce(cm_comm_t* c, int n, const void* const* sends, const int6
                        int64_t switch_bytes, int average, void* stream_, cm_stats_t* stats,
                        int* n_calls) {
   return cm_fused_allreduce_agreed(c, n, sends, counts, dtype, recv_fused, algo, threshold,
-                                   switch_bytes, average, nullptr, 0, nullptr, stream_, stats,
-                                   n_calls);
+                                   switch_bytes, average, nullptr, 0, nullptr, nullptr, stream_,
+                                   stats, n_calls);
 }
 
 int cm_fused_allreduce_agreed(cm_comm_t* c, int n, const void* const* sends,
                               const int64_t* counts, int dtype, void* recv_fused, int algo,
                               int64_t threshold, int64_t switch_bytes, int average,
                               const int64_t* agree_values, int n_agree, int* agreed,
-                              void* stream_, cm_stats_t* stats, int* n_calls) {
+                              const int64_t* reg_ids, void* stream_, cm_stats_t* stats,
+                              int* n_calls) {
   if (c->virt) return fail(CM_ERR_UNSUPPORTED, "fused allreduce needs a real communicator");
   int st = check_dtype_op(dtype, CM_SUM);
   if (st) return st;
@@ -1204,6 +1214,53 @@ int cm_fused_allreduce_agreed(cm_comm_t* c, int n, const void* const* sends,
         tot += gr[h].ng;
         ++h;
       }
+    }
+    bool gather_ok = reg_ids != nullptr && gr[g].batchable;
+    if (gather_ok)
+      for (size_t t = g; t < h && gather_ok; ++t)
+        for (int k = gr[t].i; k < gr[t].j; ++k) gather_ok = gather_ok && reg_ids[k] >= 0;
+    if (gather_ok) {
+      // registered gradients: peers' members are read in place, no pack
+      Launch L = gr[g].L;
+      L.nbuf = (int)(h - g);
+      std::vector<long long> tab;
+      std::vector<long long> ids;
+      int64_t boff = 0;
+      tab.push_back(0);
+      for (size_t t = g; t < h; ++t) {
+        L.bn[t - g] = gr[t].ng;
+        L.bboff[t - g] = boff;
+        L.bout[t - g] = gr[t].L.out[0];
+        for (int k = gr[t].i; k < gr[t].j; ++k) {
+          boff += counts[k];
+          tab.push_back(boff);
+          ids.push_back(reg_ids[k]);
+        }
+      }
+      const int gm = (int)ids.size();
+      tab.insert(tab.end(), ids.begin(), ids.end());
+      std::string key(reinterpret_cast<const char*>(tab.data()), tab.size() * sizeof(long long));
+      auto it = c->gtabs.find(key);
+      long long* dtab;
+      if (it != c->gtabs.end()) {
+        dtab = it->second;
+      } else {
+        CUDA_TRY(cudaMalloc(&dtab, tab.size() * sizeof(long long)));
+        CUDA_TRY(cudaMemcpy(dtab, tab.data(), tab.size() * sizeof(long long), cudaMemcpyHostToDevice));
+        c->gtabs[key] = dtab;
+      }
+      unsigned long long sig = 1469598103934665603ull;
+      for (long long v : tab) sig = (sig ^ (unsigned long long)v) * 1099511628211ull;
+      L.gtab = dtab;
+      L.gmem = gm;
+      L.gsig = sig;
+      L.srcmode = SRC_GATHER;
+      L.n = L.bn[0];
+      if ((st = resolve_agree())) return st;
+      if (!*agreed) return CM_OK;
+      if ((st = launch_collective(c, L, stream))) return st;
+      g = h;
+      continue;
     }
     if (h - g > 1) {
       std::vector<const void*> srcs;

@@ -79,7 +79,8 @@ struct Rec {
   long long redoff;  // element i of the sender's segment at heap + redoff + (i-seg_off)*sz
 };
 
-enum SrcMode { SRC_COPYIN = 0, SRC_PRESTAGED = 1, SRC_ZEROCOPY = 2, SRC_INLINE = 3, SRC_REGISTERED = 4 };
+enum SrcMode { SRC_COPYIN = 0, SRC_PRESTAGED = 1, SRC_ZEROCOPY = 2, SRC_INLINE = 3, SRC_REGISTERED = 4,
+               SRC_GATHER = 5 };
 enum Order { ORD_SEQ = 0, ORD_RING = 1, ORD_TREE = 2 };
 enum Phase { PH_RS = 1, PH_AG = 2 };
 enum Err { ERR_SHAPE = 1, ERR_TRANSPORT = 4 };
@@ -121,6 +122,12 @@ struct CollParams {
   char* bout[MAXBUF];
   long long bseg_off[MAXBUF][MAXP];
   long long bseg_len[MAXBUF][MAXP];
+  // SRC_GATHER (aggregate on registered gradients): the fused buffers are the
+  // concatenation of registered member tensors; gtab = {gstart[0..gmem],
+  // id[0..gmem)} in device memory; peers' members are read in place through
+  // REGTAB[id][q] (no pack, no staging copy)
+  const long long* gtab;
+  int gmem;
   long long inl[8];          // SRC_INLINE: the input travels in the parameters (cm_agree)
   unsigned long long* done_flag;  // optional: written with done_value when the call completes
   unsigned long long done_value;
@@ -612,6 +619,7 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
   __shared__ const char* s_src[MAXP];   // element 0 of rank q's input
   __shared__ char* s_red[MAXP];         // element seg_off[q] of q's segment
   __shared__ const char* s_seq[MAXP];   // fold sequence
+  __shared__ int s_rord[MAXP];          // fold sequence as source ranks
   __shared__ int s_err;
 
   CM_TRACE(P, lr, b, 0);
@@ -706,13 +714,14 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
     while ((m << 1) <= p) m <<= 1;
     const int excess = p - m;
     if (P.order == ORD_RING) {            // chunk c folds x_{c-1}, x_{c-2}, ..., x_c
-      for (int k = 0; k < p; ++k) s_seq[k] = s_src[((rank - 1 - k) % p + p) % p];
+      for (int k = 0; k < p; ++k) s_rord[k] = ((rank - 1 - k) % p + p) % p;
     } else if (P.order == ORD_TREE) {     // leaves real(v), partners 2v+1 at M+v
-      for (int v = 0; v < m; ++v) s_seq[v] = s_src[v < excess ? 2 * v : v + excess];
-      for (int v = 0; v < excess; ++v) s_seq[m + v] = s_src[2 * v + 1];
+      for (int v = 0; v < m; ++v) s_rord[v] = v < excess ? 2 * v : v + excess;
+      for (int v = 0; v < excess; ++v) s_rord[m + v] = 2 * v + 1;
     } else {
-      for (int k = 0; k < p; ++k) s_seq[k] = s_src[k];
+      for (int k = 0; k < p; ++k) s_rord[k] = k;
     }
+    for (int k = 0; k < p; ++k) s_seq[k] = s_src[s_rord[k]];
   }
   __syncthreads();
   CM_TRACE(P, lr, b, 2);
@@ -728,26 +737,64 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
     goto finish;
   }
 
-  if (P.nbuf > 1) {
+  if (P.nbuf > 1 || P.srcmode == SRC_GATHER) {
     // ---- several fused buffers, one launch: RS of every buffer, ONE
-    // RS->AG barrier, AG of every buffer (input prestaged in staging)
+    // RS->AG barrier, AG of every buffer. Input prestaged in staging, or
+    // (SRC_GATHER) read in place from every rank's registered member tensors.
     __shared__ const char* s_seqk[MAXP];
+    __shared__ long long s_piece[2];
     int m = 1;
     while ((m << 1) <= p) m <<= 1;
     const int excess = p - m;
     char* mystage = myheap + stage_off;
+    const bool gather = P.srcmode == SRC_GATHER;
     for (int k = 0; k < P.nbuf; ++k) {
-      if (tid < p) s_seqk[tid] = s_seq[tid] + P.bboff[k] * SZ;
-      __syncthreads();
       const long long so = P.bseg_off[k][rank], sl = P.bseg_len[k][rank];
       char* bo = P.bout[k];
-      char* red = mystage + P.bboff[k] * SZ;           // in place, element 0 of buffer k
-      bool vec = al16(bo) && al16(red);
-      for (int q = 0; q < p; ++q) vec = vec && al16(s_seqk[q]);
+      char* red = mystage + P.bboff[k] * SZ;           // element 0 of buffer k (AG source)
       const long long lo = slice_bound(so, sl, b, nb), hi = slice_bound(so, sl, b + 1, nb);
-      reduce_range<D, OP, MP, TREE>(s_seqk, p, m, excess, lo, hi, vec, P.average, bo, 0, red, 0,
-                                    tid, blockDim.x);
-      __syncthreads();
+      if (!gather) {
+        if (tid < p) s_seqk[tid] = s_seq[tid] + P.bboff[k] * SZ;
+        __syncthreads();
+        bool vec = al16(bo) && al16(red);
+        for (int q = 0; q < p; ++q) vec = vec && al16(s_seqk[q]);
+        reduce_range<D, OP, MP, TREE>(s_seqk, p, m, excess, lo, hi, vec, P.average, bo, 0, red, 0,
+                                      tid, blockDim.x);
+        __syncthreads();
+        continue;
+      }
+      // gather: walk the members overlapping [lo, hi) of buffer k
+      const long long* gstart = P.gtab;
+      const long long* gid = P.gtab + P.gmem + 1;
+      long long i = lo;
+      while (i < hi) {
+        if (tid == 0) {                              // member holding global index bboff + i
+          const long long g = P.bboff[k] + i;
+          int a = 0, z = P.gmem;                     // gstart[a] <= g < gstart[z]
+          while (z - a > 1) {
+            const int mid = (a + z) >> 1;
+            if (gstart[mid] <= g) a = mid; else z = mid;
+          }
+          s_piece[0] = a;
+          const long long mend = gstart[a + 1] - P.bboff[k];
+          s_piece[1] = mend < hi ? mend : hi;
+        }
+        __syncthreads();
+        const int mi = (int)s_piece[0];
+        const long long pe = s_piece[1];
+        if (tid < p) {
+          const char* base = *reinterpret_cast<char* const*>(
+              myheap + REG_OFF + ((size_t)gid[mi] * MAXP + s_rord[tid]) * 8);
+          s_seqk[tid] = base - (gstart[mi] - P.bboff[k]) * SZ;   // element i of buffer k
+        }
+        __syncthreads();
+        bool vec = al16(bo) && al16(red);
+        for (int q = 0; q < p; ++q) vec = vec && al16(s_seqk[q]);
+        reduce_range<D, OP, MP, TREE>(s_seqk, p, m, excess, i, pe, vec, P.average, bo, 0, red, 0,
+                                      tid, blockDim.x);
+        __syncthreads();
+        i = pe;
+      }
     }
     CM_TRACE(P, lr, b, 3);
     if (tid < p) st_release_sys(mid_slot(P.heap[tid], b, rank), e);

@@ -163,6 +163,29 @@ def main():
             expect(all(t.to_bytes() == want[t.name].tobytes() for t in res.tensors),
                    f"multi-buffer aggregate {algo} mb={mb}")
     comm.set_param("multi_buffer", 2)
+    # registered gradients: peers' member tensors are read in place (no pack)
+    for algo in ("ring_rsa", "rhd_rsa"):
+        want, groups, _ = OA.aggregate(per_rank, "float32", algo, 8 << 20)
+        gs = P.GradientSet(tuple(P.Tensor(nm, "float32", torch.from_numpy(a).cuda())
+                                 for nm, a in per_rank[rank]))
+        P.register_gradients(gs, comm)
+        for _ in range(2):
+            res = P.aggregate(gs, group, comm, algo=algo, cfg=P.FusionConfig(8 << 20))
+            expect(all(t.to_bytes() == want[t.name].tobytes() for t in res.tensors),
+                   f"registered-gradient aggregate {algo}")
+        comm.deregister_buffers([t.payload for t in gs.tensors])
+    for case in of_kind("model"):
+        if case["p"] != world:
+            continue
+        grads = I.synth_gradients(0, 0, I.MODELS[case["model"]], rank)
+        gs = P.GradientSet(tuple(P.Tensor(nm, "float32", torch.from_numpy(a).cuda()) for nm, a in grads))
+        P.register_gradients(gs, comm)
+        res = P.aggregate(gs, group, comm)
+        h = hashlib.sha256()
+        for t in res.tensors:
+            h.update(t.to_bytes())
+        expect(h.hexdigest() == case["sha"], f"registered model {case['model']}")
+        comm.deregister_buffers([t.payload for t in gs.tensors])
 
     # 4a. out= refill: persistent buckets are overwritten with the next step's means
     layers = I.MODELS["mobilenet_like"]
