@@ -104,6 +104,25 @@ def main():
         expect(out.to_bytes() == want, f"mixed registered/copy-in {algo}")
     comm.deregister_buffers([big])
 
+    # 2c. other element types: int32/int64 wrap-around (bit-exact), bf16 (fp32
+    # accumulation, one rounding; bit-identical to the oracle's definition)
+    for dtype in ("int32", "int64"):
+        info = np.iinfo(dtype)
+        for n in (5, 70_001, 3_000_017):
+            rng = np.random.default_rng([31, n])
+            xs = [rng.integers(info.min, info.max, size=n, dtype=dtype) for _ in range(world)]
+            for algo in ("ring_rsa", "rhd_rsa"):
+                out, _ = P.allreduce(P.Tensor("x", dtype, torch.from_numpy(xs[rank]).cuda()), P.ReduceOp.SUM,
+                                     group, comm, algo=algo)
+                expect(out.to_bytes() == OC.allreduce(xs, "sum", algo, dtype).tobytes(), f"{dtype} {algo} n={n}")
+    for n in (9, 70_001, 3_000_017):
+        rng = np.random.default_rng([32, n])
+        xs = [OC.f32_to_bf16(rng.standard_normal(n).astype(np.float32)) for _ in range(world)]
+        for algo in ("ring_rsa", "rhd_rsa"):
+            t = torch.from_numpy(xs[rank].view(np.int16)).view(torch.bfloat16).cuda()
+            out, _ = P.allreduce(P.Tensor("x", "bfloat16", t), P.ReduceOp.SUM, group, comm, algo=algo)
+            expect(out.to_bytes() == OC.allreduce(xs, "sum", algo, "bfloat16").tobytes(), f"bf16 {algo} n={n}")
+
     # 3. reduce-scatter / allgather
     for layout in ("ring", "rhd"):
         for n in (0, 3, 1000, 1 << 20):
