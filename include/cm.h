@@ -151,9 +151,18 @@ int cm_comm_set_timeout(cm_comm_t* comm, double seconds);
 /* pointer-cache policy used to classify send/recv on every call */
 int cm_comm_set_policy(cm_comm_t* comm, int policy);
 int cm_comm_registry(cm_comm_t* comm, cm_registry_t** reg);
-/* tuning knobs: "oneshot_max_bytes" (largest message reduced one-shot),
- * "oneshot_bytes_per_cta", "twoshot_bytes_per_cta", "max_ctas";
- * get also reads "staging_bytes" and "pool_bytes" */
+/* tuning knobs (values must be > 0):
+ *   "oneshot_max_bytes"   largest message reduced one-shot
+ *   "ll_max_bytes"        one-shot through the low-latency slots up to here
+ *   "ll2_max_bytes"       two-shot through the low-latency slots up to here
+ *   "ll_units_per_cta", "ll2_units_per_cta", "oneshot_bytes_per_cta",
+ *   "twoshot_bytes_per_cta", "max_ctas"   grid sizing
+ *   "stream_chunk"        elements per chunk of the pipelined two-shot (1 = off)
+ *   "multi_buffer"        2 = batch fused buffers into one launch, 1 = off
+ *   "rhd_logp"            2 = rhd_rsa runs the literal log2(p)-step recursive
+ *                         halving/doubling kernel (pairwise flags), 1 = off
+ *                         (default: one-/two-shot kernels with the same tree)
+ * get also reads "staging_bytes", "pool_bytes" and "ll_payload_per_source" */
 int cm_comm_set_param(cm_comm_t* comm, const char* key, int64_t value);
 int cm_comm_get_param(cm_comm_t* comm, const char* key, int64_t* value);
 /* symmetric allocation from the IPC heap (collective: same sizes, same order

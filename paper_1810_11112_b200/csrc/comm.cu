@@ -62,6 +62,7 @@ struct cm_comm {
   int64_t ll2_units_per_cta = 512;
   int64_t stream_chunk = 0;                   // elements; 0 disables the pipelined two-shot
   int multi_buffer = 1;                       // batch fused buffers into one launch
+  int rhd_logp = 0;                           // 1: rhd_rsa runs the log2(p)-step halving/doubling kernel
   int64_t oneshot_bytes_per_cta = 8 * 1024;
   int64_t twoshot_bytes_per_cta = 4 * 1024;
   int max_ctas = 148;
@@ -137,7 +138,7 @@ using KFn = void (*)(CollParams);
 
 // kernel tables live in one translation unit per element type (csrc/inst_*.cu)
 // so the instantiations compile in parallel
-enum KernelKind { K_COLL = 0, K_STREAM = 1, K_LL = 2, K_LL2 = 3 };
+enum KernelKind { K_COLL = 0, K_STREAM = 1, K_LL = 2, K_LL2 = 3, K_RHD = 4 };
 
 KFn pick(int kind, int dtype, int op, int p, bool tree) {
   switch (dtype) {
@@ -300,6 +301,11 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
   const int64_t per = L.oneshot ? c->oneshot_bytes_per_cta : c->twoshot_bytes_per_cta;
   int64_t nb = (work + per - 1) / per;
   int ll = L.ll;
+  // literal recursive halving/doubling (log2 p pairwise steps) for rhd_rsa allreduce
+  const bool logp = c->rhd_logp && L.order == ORD_TREE && L.nbuf == 1 && L.dtype != CM_BFLOAT16 &&
+                    !L.out_rel && (L.oneshot || L.phases == (PH_RS | PH_AG)) &&
+                    (L.srcmode == SRC_COPYIN || L.srcmode == SRC_ZEROCOPY || L.srcmode == SRC_REGISTERED);
+  if (logp) ll = 0;
   if (ll == 1 && (L.n * (int64_t)sz + 7) / 8 > c->ll_units) ll = 0;
   if (ll == 2 && (maxseg * (int64_t)sz + 7) / 8 > c->ll_units) ll = 0;  // rhd segments > n/p
   // staging capacity (LL kernels read the input directly unless it is prestaged)
@@ -307,6 +313,7 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
     int64_t need = (L.srcmode == SRC_ZEROCOPY) ? (maxseg + SLICE_ALIGN) * (int64_t)sz
                                               : L.n * (int64_t)sz;
     if (L.nbuf > 1 || L.srcmode == SRC_GATHER) need = (L.bboff[L.nbuf - 1] + L.bn[L.nbuf - 1]) * (int64_t)sz;
+    if (logp) need = L.n * (int64_t)sz;
     const bool uses_staging = ll == 0 || L.srcmode == SRC_PRESTAGED;
     if (uses_staging && need > (int64_t)c->staging_bytes)
       return fail(CM_ERR_CONFIG, "message of " + std::to_string(L.n * sz) + " B needs " +
@@ -316,6 +323,7 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
   }
   if (ll == 1) nb = ((L.n * (int64_t)sz + 7) / 8 + c->ll_units_per_cta - 1) / c->ll_units_per_cta;
   if (ll == 2) nb = ((maxseg * (int64_t)sz + 7) / 8 + c->ll2_units_per_cta - 1) / c->ll2_units_per_cta;
+  if (logp) nb = (L.n * (int64_t)sz + c->twoshot_bytes_per_cta - 1) / c->twoshot_bytes_per_cta;
   nb = std::max<int64_t>(1, std::min<int64_t>(nb, std::min(c->max_ctas, MAXBLK)));
   const bool tree = L.order == ORD_TREE;
   // pipelined two-shot when every CTA's slice spans >= 2 chunks
@@ -323,7 +331,8 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
                          L.phases == (PH_RS | PH_AG) &&
                          c->stream_chunk > 0 && maxseg / std::max<int64_t>(nb, 1) >= 2 * c->stream_chunk;
   P.stream_chunk = c->stream_chunk;
-  KFn k = pick(ll == 1 ? K_LL : ll == 2 ? K_LL2 : pipelined ? K_STREAM : K_COLL, L.dtype, L.op, p, tree);
+  KFn k = pick(logp ? K_RHD : ll == 1 ? K_LL : ll == 2 ? K_LL2 : pipelined ? K_STREAM : K_COLL, L.dtype, L.op, p,
+               tree);
   if (!k) return fail(CM_ERR_SHAPE, "unsupported dtype");
   void* args[] = {&P};
   int64_t alg = 0;   // busBW bytes of this launch (nccl-tests convention)
@@ -348,7 +357,15 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
   if (!c->virt) {
     const int r = c->rank;
     int64_t in_bytes = 0;
-    if (ll == 1) in_bytes = (int64_t)(p - 1) * ((L.n * (int64_t)sz + 7) / 8) * 16;
+    if (logp) {
+      // halving moves n/2 + n/4 + ..., doubling the same again; +n for a fold partner
+      int m = 1;
+      while ((m << 1) <= p) m <<= 1;
+      const int excess = p - m;
+      const bool odd = r < 2 * excess && (r & 1), even = r < 2 * excess && !(r & 1);
+      if (odd) in_bytes = L.n * (int64_t)sz;
+      else in_bytes = 2 * (L.n - L.n / m) * (int64_t)sz + (even ? L.n * (int64_t)sz : 0);
+    } else if (ll == 1) in_bytes = (int64_t)(p - 1) * ((L.n * (int64_t)sz + 7) / 8) * 16;
     else if (ll == 2) in_bytes = 2 * (int64_t)(p - 1) * ((maxseg * (int64_t)sz + 7) / 8) * 16;
     else if (L.oneshot) in_bytes = (int64_t)(p - 1) * L.n * sz;
     else {
@@ -771,6 +788,7 @@ int cm_comm_set_param(cm_comm_t* c, const char* key, int64_t value) {
   else if (k == "ll2_units_per_cta") c->ll2_units_per_cta = value;
   else if (k == "stream_chunk") c->stream_chunk = value == 1 ? 0 : ((value + 63) / 64) * 64;
   else if (k == "multi_buffer") c->multi_buffer = value > 1 ? 1 : 0;
+  else if (k == "rhd_logp") c->rhd_logp = value > 1 ? 1 : 0;
   else if (k == "oneshot_bytes_per_cta") c->oneshot_bytes_per_cta = value;
   else if (k == "twoshot_bytes_per_cta") c->twoshot_bytes_per_cta = value;
   else if (k == "max_ctas") c->max_ctas = (int)std::min<int64_t>(value, MAXBLK);
@@ -787,6 +805,7 @@ int cm_comm_get_param(cm_comm_t* c, const char* key, int64_t* value) {
   else if (k == "ll2_units_per_cta") *value = c->ll2_units_per_cta;
   else if (k == "stream_chunk") *value = c->stream_chunk;
   else if (k == "multi_buffer") *value = c->multi_buffer ? 2 : 1;
+  else if (k == "rhd_logp") *value = c->rhd_logp ? 2 : 1;
   else if (k == "oneshot_bytes_per_cta") *value = c->oneshot_bytes_per_cta;
   else if (k == "twoshot_bytes_per_cta") *value = c->twoshot_bytes_per_cta;
   else if (k == "max_ctas") *value = c->max_ctas;

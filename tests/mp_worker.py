@@ -62,6 +62,32 @@ def main():
                                  P.ReduceOp.SUM, group, comm, algo=case["algo"])
             expect(sha(out.to_bytes()) == case["sha"], f"C1 {case['algo']}")
 
+    # 1b. the literal log2(p)-step recursive halving/doubling kernel (rhd_logp):
+    # golden rhd cases, then large vectors copy-in / zero-copy / in-place
+    comm.set_param("rhd_logp", 2)
+    for case in of_kind("allreduce"):
+        if case["p"] != world or case["algo"] != "rhd_rsa":
+            continue
+        arrays = I.allreduce_inputs(world, case["n"], case["dtype"], case["op"])
+        t = P.Tensor("x", case["dtype"], torch.from_numpy(arrays[rank]).cuda())
+        out, _ = P.allreduce(t, OPS[case["op"]], group, comm, algo="rhd_rsa")
+        expect(sha(out.to_bytes()) == case["sha"], f"rhd log-p golden {case['dtype']} {case['op']} n={case['n']}")
+    for n in (1, 262145, 5_000_011):
+        rng = np.random.default_rng([23, n])
+        xs = [(rng.standard_normal(n) * 10.0 ** rng.integers(-3, 4, size=n)).astype(np.float32)
+              for _ in range(world)]
+        want = OC.allreduce(xs, "sum", "rhd_rsa", "float32").tobytes()
+        x = torch.from_numpy(xs[rank]).cuda()
+        for _ in range(2):
+            out, _ = P.allreduce(P.Tensor("x", "float32", x), P.ReduceOp.SUM, group, comm, algo="rhd_rsa")
+            expect(out.to_bytes() == want, f"rhd log-p copy-in n={n}")
+        sym = comm.empty(n, "float32")
+        sym.copy_(x)
+        P.allreduce(P.Tensor("x", "float32", sym), P.ReduceOp.SUM, group, comm, algo="rhd_rsa", out=sym)
+        expect(sym.cpu().numpy().tobytes() == want, f"rhd log-p zero-copy in-place n={n}")
+        comm.free(sym)
+    comm.set_param("rhd_logp", 1)
+
     # 2. large messages: copy-in, zero-copy (symmetric pool), in-place, host buffers
     for n in (262145, 1 << 22, 5_000_011, 20_000_003):
         rng = np.random.default_rng([21, n])

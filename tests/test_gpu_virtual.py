@@ -101,7 +101,53 @@ def test_pipelined_two_shot_vs_oracle(p, algo):
         res = P.allreduce_group(dev_tensors(xs, "float32"), P.ReduceOp.SUM, g, algo=algo)
         for t, _ in res:
             assert t.to_bytes() == want.tobytes(), chunk
-    g.set_param("stream_chunk", 8192)
+    g.set_param("stream_chunk", 1)   # back to the default (off)
+
+
+_VGL = {}
+
+
+def vg_logp(p):
+    """A virtual group whose rhd_rsa runs the literal log2(p)-step recursive
+    halving/doubling kernel (pairwise flags) instead of the direct kernels."""
+    if p not in _VGL:
+        g = P.VirtualGroup(p, 0, staging_bytes=128 << 20, timeout_s=5.0)
+        g.set_param("rhd_logp", 2)
+        _VGL[p] = g
+    return _VGL[p]
+
+
+RHD_GOLDEN = [c for c in ALLREDUCE if c["algo"] == "rhd_rsa"]
+
+
+@pytest.mark.parametrize("case", RHD_GOLDEN,
+                         ids=[f"{c['dtype']}-{c['op']}-p{c['p']}-n{c['n']}" for c in RHD_GOLDEN])
+def test_rhd_logp_kernel_bit_exact_vs_reference_golden(case):
+    p, n, dtype, op = case["p"], case["n"], case["dtype"], case["op"]
+    arrays = I.allreduce_inputs(p, n, dtype, op)
+    res = P.allreduce_group(dev_tensors(arrays, dtype), OPS[op], vg_logp(p), algo="rhd_rsa")
+    for r, (t, st) in enumerate(res):
+        assert sha(t.to_bytes()) == case["sha"], r
+        assert [st.rounds, st.messages_per_rank, st.bytes_sent_per_rank] == case["stats"][r]
+
+
+@pytest.mark.parametrize("p", [2, 3, 5, 6, 7, 8, 12, 16])
+@pytest.mark.parametrize("n", [1, 1000, 262145, 3_000_001])
+def test_rhd_logp_kernel_vs_oracle(p, n):
+    rng = np.random.default_rng([p, n, 5])
+    xs = [(rng.standard_normal(n) * 10.0 ** rng.integers(-3, 4, size=n)).astype(np.float32)
+          for _ in range(p)]
+    want = OC.allreduce(xs, "sum", "rhd_rsa", "float32")
+    g = vg_logp(p)
+    for _ in range(2):                     # both staging parities
+        res = P.allreduce_group(dev_tensors(xs, "float32"), P.ReduceOp.SUM, g, algo="rhd_rsa")
+        for t, _ in res:
+            assert t.to_bytes() == want.tobytes()
+    ints = [rng.integers(-2**31, 2**31 - 1, size=n, dtype=np.int64) for _ in range(p)]
+    res = P.allreduce_group(dev_tensors(ints, "int64"), P.ReduceOp.SUM, g, algo="rhd_rsa")
+    want = OC.allreduce(ints, "sum", "rhd_rsa", "int64")
+    for t, _ in res:
+        assert t.to_bytes() == want.tobytes()
 
 
 @pytest.mark.parametrize("dtype", ["int32", "int64"])

@@ -45,6 +45,7 @@ st = L.Stats()
 phases = ["copyin", "start_barrier", "reduce", "mid_barrier", "allgather"]
 acc = [0.0] * 5
 tot = 0.0
+skew = [0.0] * 6
 for it in range(a.iters + 3):
     tr.zero_()
     dist.barrier()
@@ -61,10 +62,15 @@ for it in range(a.iters + 3):
         d = d[(t[:, k + 1] > 0) & (t[:, k] > 0)]
         acc[k] += float(d.median()) / 1e3 if len(d) else 0.0
     tot += float((t[:, 5].max() - t[:, 0].min())) / 1e3
+    for k in range(6):
+        col = t[:, k][t[:, k] > 0]
+        skew[k] += float(col.max() - t[:, 0].min()) / 1e3 if len(col) else 0.0
 if rank == 0:
     print(f"p={world} bytes={a.bytes} algo={a.algo} zc={a.zc} ctas={int(used.sum())} "
           f"kernel span {tot / a.iters:.2f} us | " +
-          " ".join(f"{ph} {v / a.iters:.2f}" for ph, v in zip(phases, acc)), flush=True)
+          " ".join(f"{ph} {v / a.iters:.2f}" for ph, v in zip(phases, acc)) +
+          " | last CTA past stamp k (from first start): " + " ".join(f"{v / a.iters:.1f}" for v in skew),
+          flush=True)
 L.check(L.lib.cm_comm_set_trace(comm._h, None, 0))
 comm.close()
 dist.destroy_process_group()
