@@ -272,21 +272,30 @@ def _aggregate_names(grads, names, tp, algo, cfg, sw, registry, handles, stats_o
         for grp in fuse_plan(plan.ready, cfg):       # aggregation.py:159-161
             for i in grp:
                 registry.classify(handles[plan.ready[i].name])
-    reuse = out.__dict__.get("_fused") if out is not None else None
-    if reuse is not None and [f.numel() for f in reuse] != [r["total"] for r in plan.runs]:
+    # out= reuses the previous result's buckets (device, or pinned host for
+    # host gradients) when the schema matches
+    reuse = out.__dict__.get("_bufs") if out is not None else None
+    if reuse is not None and [(f.numel(), f.is_cuda) for f in reuse] != \
+            [(r["total"], not r["any_host"]) for r in plan.runs]:
         raise ShapeError("out= GradientSet does not match this gradient schema")
-    # out= with the same schema: the result tensors are views of the reused
+    # same schema and names: the result tensors are views of the reused
     # buckets already, so `out` itself is refilled and returned (torch out=)
-    refill = reuse is not None and out.names == list(names) and \
-        out.__dict__.get("_host") is None and not any(r["any_host"] for r in plan.runs)
+    refill = reuse is not None and out.names == list(names)
     result: list[Tensor] = []
-    fused_bufs, host_bufs = [], []
+    bufs = []
     stream = tp._stream()
     with torch.cuda.device(tp.device):
         for ri, run in enumerate(plan.runs):
             dtype = run["dtype"]
-            fused = reuse[ri] if reuse is not None else \
-                torch.empty(run["total"], dtype=DTYPES[dtype], device=tp.device)
+            if reuse is not None:
+                fused = reuse[ri]
+            elif run["any_host"]:
+                # CUDA-aware semantics: host gradients get host means. The C
+                # call streams H2D / collectives / D2H on separate streams
+                # straight into this pinned bucket.
+                fused = torch.empty(run["total"], dtype=DTYPES[dtype], pin_memory=True)
+            else:
+                fused = torch.empty(run["total"], dtype=DTYPES[dtype], device=tp.device)
             ncalls = C.c_int()
             agreed = C.c_int(1)
             L.check(L.lib.cm_fused_allreduce_agreed(
@@ -298,18 +307,9 @@ def _aggregate_names(grads, names, tp, algo, cfg, sw, registry, handles, stats_o
             agree = None
             if stats_out is not None:
                 stats_out.extend(_stats(run["stats"][k]) for k in range(ncalls.value))
-            fused_bufs.append(fused)
+            bufs.append(fused)
             if refill:
                 continue
-            if run["any_host"]:
-                # CUDA-aware semantics: host gradients get host means, copied
-                # into pinned memory on the communicator's stream
-                prev = out.__dict__.get("_host") if out is not None else None
-                hbuf = prev[ri] if prev is not None else \
-                    torch.empty(run["total"], dtype=DTYPES[dtype], pin_memory=True)
-                hbuf.copy_(fused, non_blocking=True)
-                host_bufs.append(hbuf)
-                fused = hbuf
             for nm, view in zip(run["names"], fused.split_with_sizes(run["counts"])):
                 result.append(Tensor._wrap(nm, dtype, view))
     if tp.blocking or any(r["any_host"] for r in plan.runs):
@@ -322,8 +322,7 @@ def _aggregate_names(grads, names, tp, algo, cfg, sw, registry, handles, stats_o
     gs = GradientSet.__new__(GradientSet)
     object.__setattr__(gs, "tensors", tuple(result))
     object.__setattr__(gs, "iteration", grads.iteration)
-    object.__setattr__(gs, "_fused", fused_bufs)
-    object.__setattr__(gs, "_host", host_bufs if host_bufs else None)
+    object.__setattr__(gs, "_bufs", bufs)
     return gs
 
 

@@ -40,6 +40,13 @@ struct cm_comm {
   std::map<size_t, size_t> pool_free;  // offset -> bytes
   std::map<size_t, size_t> pool_used;
   char* scratch = nullptr;             // device bounce buffer for host-memory buffers
+  // host-memory aggregate pipeline: inputs land in `indev` on the h2d stream,
+  // results leave `outdev` on the d2h stream, overlapping both PCIe directions
+  char* indev = nullptr;
+  char* outdev = nullptr;
+  int64_t indev_bytes = 0, outdev_bytes = 0;
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  std::vector<cudaEvent_t> sync_events;
   int64_t* agree_host = nullptr;       // mapped pinned: cm_agree result + completion word
   int64_t* agree_dev = nullptr;        // device alias of agree_host
   unsigned long long agree_ticket = 0;
@@ -639,6 +646,71 @@ int launch_batched_copy(cm_comm* c, int n, const void* const* srcs, void* const*
   return CM_OK;
 }
 
+// Host-memory aggregate pipeline (CUDA-aware semantics for host gradients).
+// Stream roles: h2d copies inputs into `indev`, the caller's stream runs the
+// collectives, d2h copies results out of `outdev`. Every hand-off is an
+// event, so H2D of group g+1 and D2H of group g run concurrently (PCIe is
+// full duplex) and overlap the NVLink collectives; the caller's stream joins
+// both copy streams before the call returns (stream-ordered semantics kept).
+struct HostPipe {
+  cm_comm* c;
+  cudaStream_t main;
+  bool active = false;
+  size_t next_ev = 0;
+  explicit HostPipe(cm_comm* c_, cudaStream_t s) : c(c_), main(s) {}
+  int ev(cudaEvent_t* out) {
+    if (next_ev == c->sync_events.size()) {
+      cudaEvent_t e;
+      CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      c->sync_events.push_back(e);
+    }
+    *out = c->sync_events[next_ev++];
+    return CM_OK;
+  }
+  // order `to` after everything queued so far on `from`
+  int link(cudaStream_t from, cudaStream_t to) {
+    cudaEvent_t e;
+    int st = ev(&e);
+    if (st) return st;
+    CUDA_TRY(cudaEventRecord(e, from));
+    CUDA_TRY(cudaStreamWaitEvent(to, e, 0));
+    return CM_OK;
+  }
+  static int grow(char** buf, int64_t* have, int64_t need) {
+    if (*have >= need) return CM_OK;
+    if (*buf) {
+      CUDA_TRY(cudaDeviceSynchronize());
+      CUDA_TRY(cudaFree(*buf));
+      *buf = nullptr;
+      *have = 0;
+    }
+    CUDA_TRY(cudaMalloc(buf, need));
+    *have = need;
+    return CM_OK;
+  }
+  int start(int64_t in_bytes, int64_t out_bytes) {
+    if (!c->h2d) CUDA_TRY(cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
+    if (!c->d2h) CUDA_TRY(cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
+    int st;
+    if ((st = grow(&c->indev, &c->indev_bytes, std::max<int64_t>(in_bytes, 1)))) return st;
+    if ((st = grow(&c->outdev, &c->outdev_bytes, std::max<int64_t>(out_bytes, 1)))) return st;
+    // copy streams start after all earlier work of the caller's stream (which
+    // produced device inputs and last read indev/outdev)
+    if ((st = link(main, c->h2d))) return st;
+    if ((st = link(main, c->d2h))) return st;
+    active = true;
+    return CM_OK;
+  }
+  int join() {
+    if (!active) return CM_OK;
+    active = false;
+    int st;
+    if ((st = link(c->h2d, main))) return st;
+    return link(c->d2h, main);
+  }
+  ~HostPipe() { join(); }
+};
+
 }  // namespace
 
 extern "C" {
@@ -744,6 +816,11 @@ int cm_comm_destroy(cm_comm_t* c) {
   for (auto& kv : c->gtabs) cudaFree(kv.second);
   if (c->local) cudaFree(c->local);
   if (c->scratch) cudaFree(c->scratch);
+  if (c->indev) cudaFree(c->indev);
+  if (c->outdev) cudaFree(c->outdev);
+  if (c->h2d) cudaStreamDestroy(c->h2d);
+  if (c->d2h) cudaStreamDestroy(c->d2h);
+  for (auto e : c->sync_events) cudaEventDestroy(e);
   if (c->herr_host) cudaFreeHost(c->herr_host);
   if (c->agree_host) cudaFreeHost(c->agree_host);
   for (auto& pr : c->prof) { cudaEventDestroy(pr.e0); cudaEventDestroy(pr.e1); }
@@ -1140,8 +1217,10 @@ int cm_fused_allreduce_agreed(cm_comm_t* c, int n, const void* const* sends,
   cm_fuse_plan(n, nbytes.data(), dts.data(), threshold, group.data(), &ngroups);
   int rk;
   if ((st = classify(c, recv_fused, &rk))) return st;
-  if (rk != CM_KIND_DEVICE) return fail(CM_ERR_UNSUPPORTED, "fused output must be device memory");
+  const bool out_host = rk == CM_KIND_HOST;
+  if (out_host && c->virt) return fail(CM_ERR_UNSUPPORTED, "virtual groups need device buffers");
   const int p = c->size;
+  HostPipe hp(c, stream);
   if (p == 1) {
     // single rank: every allreduce is the identity and the mean divides by 1
     // (collectives.py:119-120), so all fused groups collapse into ONE batched
@@ -1150,11 +1229,13 @@ int cm_fused_allreduce_agreed(cm_comm_t* c, int n, const void* const* sends,
     std::vector<const void*> srcs(n);
     std::vector<void*> dsts(n);
     std::vector<int64_t> bytes(n);
+    std::vector<int> kinds(n, CM_KIND_DEVICE);
     int64_t off = 0;
     for (int k = 0; k < n; ++k) {
       int kind = CM_KIND_DEVICE;
       if (counts[k] > 0 && (st = classify(c, sends[k], &kind))) return st;
       any_host = any_host || kind == CM_KIND_HOST;
+      kinds[k] = kind;
       srcs[k] = sends[k];
       dsts[k] = static_cast<char*>(recv_fused) + off;
       bytes[k] = counts[k] * sz;
@@ -1164,15 +1245,43 @@ int cm_fused_allreduce_agreed(cm_comm_t* c, int n, const void* const* sends,
       stats[g] = cm_stats_t{0, 0, 0};
       count_stats(c, stats[g]);
     }
-    if (any_host) {
-      for (int k = 0; k < n; ++k)
-        if (bytes[k]) CUDA_TRY(cudaMemcpyAsync(dsts[k], srcs[k], bytes[k], cudaMemcpyDefault, stream));
+    if (any_host || out_host) {
+      // H2D into the device (h2d stream) and, for host outputs, D2H back out
+      // (d2h stream) in ~16 MiB chunks so both PCIe directions stream at once
+      if ((st = hp.start(out_host ? off : 0, 0))) return st;
+      // the fused result is contiguous in indev, so each chunk leaves in ONE D2H
+      int64_t soff = 0, chunk_lo = 0;
+      for (int k = 0; k < n; ++k) {
+        if (bytes[k])
+          CUDA_TRY(cudaMemcpyAsync(out_host ? c->indev + soff : dsts[k], srcs[k], bytes[k], cudaMemcpyDefault,
+                                   c->h2d));
+        soff += bytes[k];
+        if (out_host && soff > chunk_lo && (soff - chunk_lo >= (16 << 20) || k == n - 1)) {
+          if ((st = hp.link(c->h2d, c->d2h))) return st;
+          CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(recv_fused) + chunk_lo, c->indev + chunk_lo, soff - chunk_lo,
+                                   cudaMemcpyDeviceToHost, c->d2h));
+          chunk_lo = soff;
+        }
+      }
+      if ((st = hp.join())) return st;
     } else if ((st = launch_batched_copy(c, n, srcs.data(), dsts.data(), bytes.data(), false, stream))) {
       return st;
     }
     *n_calls = ngroups;
     return CM_OK;
   }
+  // host inputs or outputs: start the copy-stream pipeline (device buffers
+  // sized for the whole call) before the plan takes outdev addresses
+  bool any_host_in = false;
+  int64_t total_bytes = 0;
+  std::vector<int> kinds(n, CM_KIND_DEVICE);
+  for (int k = 0; k < n; ++k) {
+    if (counts[k] > 0 && (st = classify(c, sends[k], &kinds[k]))) return st;
+    any_host_in = any_host_in || kinds[k] == CM_KIND_HOST;
+    total_bytes += counts[k] * sz;
+  }
+  if ((any_host_in || out_host) && (st = hp.start(any_host_in ? total_bytes : 0, out_host ? total_bytes : 0)))
+    return st;
   // Pass 1: per fused group, members, size, algorithm and launch plan
   struct Grp {
     int i, j;
@@ -1192,10 +1301,8 @@ int cm_fused_allreduce_agreed(cm_comm_t* c, int n, const void* const* sends,
       G.any_host = false;
       int j = i;
       while (j < n && group[j] == g) {
-        int k = CM_KIND_DEVICE;
-        // aggregation.py:159-161: classify every member once per allreduce call
-        if (counts[j] > 0 && (st = classify(c, sends[j], &k))) return st;
-        G.any_host = G.any_host || (k == CM_KIND_HOST);
+        // aggregation.py:159-161: every member classified once per call (above)
+        G.any_host = G.any_host || (kinds[j] == CM_KIND_HOST);
         G.ng += counts[j];
         ++j;
       }
@@ -1212,7 +1319,7 @@ int cm_fused_allreduce_agreed(cm_comm_t* c, int n, const void* const* sends,
       G.L.op = CM_SUM;
       G.L.average = average;
       plan_algo(c, concrete, G.ng * sz, &G.L);
-      G.L.out[0] = static_cast<char*>(recv_fused) + fused_off * sz;
+      G.L.out[0] = (out_host ? c->outdev : static_cast<char*>(recv_fused)) + fused_off * sz;
       G.batchable = c->multi_buffer && !G.any_host && G.L.ll == 0 && !G.L.oneshot &&
                     G.L.phases == (PH_RS | PH_AG);
       gr.push_back(G);
@@ -1220,6 +1327,31 @@ int cm_fused_allreduce_agreed(cm_comm_t* c, int n, const void* const* sends,
       i = j;
     }
   }
+  // host-input groups: every group's H2D is queued up front on the h2d stream
+  // (into indev at the group's fused offset); each collective waits only for
+  // its own group's event
+  std::vector<cudaEvent_t> in_ready(gr.size(), nullptr);
+  for (size_t t = 0; t < gr.size(); ++t) {
+    if (!gr[t].any_host) continue;
+    int64_t o = gr[t].off * sz;
+    for (int k = gr[t].i; k < gr[t].j; ++k) {
+      if (counts[k]) CUDA_TRY(cudaMemcpyAsync(c->indev + o, sends[k], counts[k] * sz, cudaMemcpyDefault, c->h2d));
+      o += counts[k] * sz;
+    }
+    if ((st = hp.ev(&in_ready[t]))) return st;
+    CUDA_TRY(cudaEventRecord(in_ready[t], c->h2d));
+  }
+  // host outputs: after the launch of groups [a, b), copy their results out
+  auto drain = [&](size_t a, size_t b) -> int {
+    if (!out_host) return CM_OK;
+    int s2 = hp.link(stream, c->d2h);
+    if (s2) return s2;
+    for (size_t t = a; t < b; ++t)
+      if (gr[t].ng)
+        CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(recv_fused) + gr[t].off * sz, c->outdev + gr[t].off * sz,
+                                 gr[t].ng * sz, cudaMemcpyDeviceToHost, c->d2h));
+    return CM_OK;
+  };
   // Pass 2: launches. Consecutive two-shot groups with the same layout share
   // one pack + one multi-buffer launch (up to MAXBUF); others go one by one.
   size_t g = 0;
@@ -1278,6 +1410,7 @@ int cm_fused_allreduce_agreed(cm_comm_t* c, int n, const void* const* sends,
       if ((st = resolve_agree())) return st;
       if (!*agreed) return CM_OK;
       if ((st = launch_collective(c, L, stream))) return st;
+      if ((st = drain(g, h))) return st;
       g = h;
       continue;
     }
@@ -1311,6 +1444,7 @@ int cm_fused_allreduce_agreed(cm_comm_t* c, int n, const void* const* sends,
       if ((st = resolve_agree())) return st;
       if (!*agreed) return CM_OK;            // the queued pack only touched local staging
       if ((st = launch_collective(c, L, stream))) return st;
+      if ((st = drain(g, h))) return st;
       g = h;
       continue;
     }
@@ -1326,14 +1460,10 @@ int cm_fused_allreduce_agreed(cm_comm_t* c, int n, const void* const* sends,
       off += counts[k] * sz;
     }
     Launch L = G.L;
-    if (G.any_host) {  // bounce through device scratch, then copy-in
-      off = 0;
-      for (int k = G.i; k < G.j; ++k) {
-        if (counts[k]) CUDA_TRY(cudaMemcpyAsync(c->scratch + off, sends[k], counts[k] * sz, cudaMemcpyDefault, stream));
-        off += counts[k] * sz;
-      }
+    if (G.any_host) {  // inputs arrive in indev on the h2d stream, then copy-in
+      CUDA_TRY(cudaStreamWaitEvent(stream, in_ready[g], 0));
       L.srcmode = SRC_COPYIN;
-      L.in[0] = c->scratch;
+      L.in[0] = c->indev + G.off * sz;
     } else {         // pack straight into the IPC staging area (no extra copy)
       if ((st = launch_batched_copy(c, G.j - G.i, srcs.data(), dsts.data(), bytes.data(), true, stream)))
         return st;
@@ -1342,8 +1472,10 @@ int cm_fused_allreduce_agreed(cm_comm_t* c, int n, const void* const* sends,
     if ((st = resolve_agree())) return st;
     if (!*agreed) return CM_OK;
     if ((st = launch_collective(c, L, stream))) return st;
+    if ((st = drain(g, g + 1))) return st;
     ++g;
   }
+  if ((st = hp.join())) return st;
   for (int q = 0; q < ngroups; ++q) count_stats(c, stats[q]);
   *n_calls = ngroups;
   return CM_OK;

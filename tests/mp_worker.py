@@ -232,6 +232,30 @@ def main():
         expect(h.hexdigest() == case["sha"], f"registered model {case['model']}")
         comm.deregister_buffers([t.payload for t in gs.tensors])
 
+    # 4b. host gradients through the copy-stream pipeline (H2D / collectives /
+    # D2H overlapped): pinned, pageable and mixed host/device members, many
+    # fused groups, persistent pinned output buckets refilled by out=
+    for algo in ("ring_rsa", "auto"):
+        want, groups, _ = OA.aggregate(per_rank, "float32", algo, 8 << 20)
+        want2, _, _ = OA.aggregate([[(nm, a * 2) for nm, a in pr] for pr in per_rank], "float32", algo, 8 << 20)
+        for kind in ("pinned", "pageable", "mixed"):
+            def mk(scale):
+                ts = []
+                for i, (nm, a) in enumerate(per_rank[rank]):
+                    x = torch.from_numpy(a * scale)
+                    if kind == "pinned" or (kind == "mixed" and i % 2 == 0):
+                        x = x.pin_memory()
+                    elif kind == "mixed":
+                        x = x.cuda()
+                    ts.append(P.Tensor(nm, "float32", x))
+                return P.GradientSet(tuple(ts))
+            res = P.aggregate(mk(1), group, comm, algo=algo, cfg=P.FusionConfig(8 << 20))
+            expect(all(not t.is_cuda for t in res.tensors), f"host means stay on the host {kind}")
+            expect(all(t.to_bytes() == want[t.name].tobytes() for t in res.tensors), f"host aggregate {algo} {kind}")
+            res2 = P.aggregate(mk(2), group, comm, algo=algo, cfg=P.FusionConfig(8 << 20), out=res)
+            expect(res2 is res and all(t.to_bytes() == want2[t.name].tobytes() for t in res2.tensors),
+                   f"host aggregate out= refill {algo} {kind}")
+
     # 4a. out= refill: persistent buckets are overwritten with the next step's means
     layers = I.MODELS["mobilenet_like"]
     g1 = I.synth_gradients(0, 0, layers, rank)

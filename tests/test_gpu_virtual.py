@@ -327,3 +327,30 @@ def test_p1_identity_and_errors():
     with pytest.raises(P.ConfigError):
         P.allreduce_group([P.Tensor("x", "float32", torch.zeros(3, device="cuda"))] * 2,
                           P.ReduceOp.SUM, vg(2), switch_bytes=0)
+
+
+def test_single_rank_communicator_aggregate_host_and_device():
+    """p = 1 real communicator (BASELINE C5 at N=1): device gradients -> one
+    batched copy; pinned / pageable / mixed host gradients -> chunked H2D + D2H
+    on the copy streams into pinned host buckets (refilled with out=)."""
+    comm = P.Communicator(rank=0, size=1, device=0, staging_bytes=64 << 20, pool_bytes=2 << 20)
+    layers = [480_000] * 40 + [1_000_003, 77]
+    g = I.synth_gradients(0, 0, layers, 0)
+    for kind in ("device", "pinned", "pageable", "mixed"):
+        def mk(scale):
+            ts = []
+            for i, (nm, a) in enumerate(g):
+                x = torch.from_numpy(a * scale)
+                if kind == "device" or (kind == "mixed" and i % 3 == 0):
+                    x = x.cuda()
+                elif kind in ("pinned", "mixed"):
+                    x = x.pin_memory()
+                ts.append(P.Tensor(nm, "float32", x))
+            return P.GradientSet(tuple(ts))
+        res = P.aggregate(mk(1), P.GroupSpec(1), comm)
+        assert all(t.to_bytes() == (a * 1).tobytes() for t, (_, a) in zip(res.tensors, sorted(g)))
+        res2 = P.aggregate(mk(3), P.GroupSpec(1), comm, out=res)
+        assert res2 is res
+        assert all(t.to_bytes() == (a * 3).tobytes() for t, (_, a) in zip(res.tensors, sorted(g)))
+        assert all(t.is_cuda == (kind == "device") for t in res.tensors)
+    comm.close()
