@@ -162,6 +162,10 @@ int cm_comm_registry(cm_comm_t* comm, cm_registry_t** reg);
  *   "rhd_logp"            2 = rhd_rsa runs the literal log2(p)-step recursive
  *                         halving/doubling kernel (pairwise flags), 1 = off
  *                         (default: one-/two-shot kernels with the same tree)
+ *   "bulk_copy"           2 = fusion pack through the TMA bulk-copy engine when
+ *                         every member is 16-byte aligned, 1 = SM copy (default:
+ *                         same kernel time, but its 96 KiB shared-memory carve-out
+ *                         costs ~5 us of reconfiguration per step in the bench)
  * get also reads "staging_bytes", "pool_bytes" and "ll_payload_per_source" */
 int cm_comm_set_param(cm_comm_t* comm, const char* key, int64_t value);
 int cm_comm_get_param(cm_comm_t* comm, const char* key, int64_t* value);

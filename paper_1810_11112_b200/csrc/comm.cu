@@ -70,6 +70,7 @@ struct cm_comm {
   int64_t stream_chunk = 0;                   // elements; 0 disables the pipelined two-shot
   int multi_buffer = 1;                       // batch fused buffers into one launch
   int rhd_logp = 0;                           // 1: rhd_rsa runs the log2(p)-step halving/doubling kernel
+  int bulk_copy = 0;                          // fusion pack through the TMA bulk-copy engine (opt-in)
   int64_t oneshot_bytes_per_cta = 8 * 1024;
   int64_t twoshot_bytes_per_cta = 4 * 1024;
   int max_ctas = 148;
@@ -614,6 +615,8 @@ int do_ag(cm_comm* c, const void* const* sends, void* const* recvs, int64_t coun
   return CM_OK;
 }
 
+bool g_bulk_copy_default = true;   // cm_batched_copy without a communicator (fuse/unfuse)
+
 int launch_batched_copy(cm_comm* c, int n, const void* const* srcs, void* const* dsts,
                         const int64_t* nbytes, bool staged, cudaStream_t stream) {
   for (int base = 0; base < n; base += MAXCOPY) {
@@ -633,6 +636,27 @@ int launch_batched_copy(cm_comm* c, int n, const void* const* srcs, void* const*
       P.heap = c->local;
       P.staging_bytes = (long long)c->staging_bytes;
       P.staging_off = (long long)c->staging_off;
+    }
+    // TMA bulk-copy engine when every piece is 16-byte aligned (addresses and sizes)
+    bool aligned = P.start[m] >= (256 << 10) && (c ? c->bulk_copy : g_bulk_copy_default);
+    for (int i = 0; i < m && aligned; ++i)
+      aligned = ((((uintptr_t)P.src[i]) | ((uintptr_t)P.dst[i]) | (uintptr_t)nbytes[base + i]) & 15u) == 0;
+    if (aligned) {
+      static bool attr_set = false;
+      if (!attr_set) {
+        CUDA_TRY(cudaFuncSetAttribute((const void*)bulk_copy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)BULK_SMEM));
+        attr_set = true;
+      }
+      const int sms = c ? c->sms : 148;
+      int64_t nb = (P.start[m] + 4 * BULK_CHUNK - 1) / (4 * BULK_CHUNK);
+      nb = std::max<int64_t>(1, std::min<int64_t>(nb, 2 * (int64_t)sms));
+      void* args[] = {&P};
+      ProfScope prof_scope(c, stream, 1, 2 * P.start[m]);
+      CUDA_TRY(cudaLaunchKernel((const void*)bulk_copy_kernel, dim3((unsigned)nb), dim3(BULK_THREADS), args,
+                                BULK_SMEM, stream));
+      if (c) c->launches += 1;
+      continue;
     }
     // >= 2 waves of 512-thread CTAs (4 resident per SM) for large packs
     int64_t nb = (P.start[m] + (64 << 10) - 1) / (64 << 10);
@@ -866,6 +890,7 @@ int cm_comm_set_param(cm_comm_t* c, const char* key, int64_t value) {
   else if (k == "stream_chunk") c->stream_chunk = value == 1 ? 0 : ((value + 63) / 64) * 64;
   else if (k == "multi_buffer") c->multi_buffer = value > 1 ? 1 : 0;
   else if (k == "rhd_logp") c->rhd_logp = value > 1 ? 1 : 0;
+  else if (k == "bulk_copy") c->bulk_copy = value > 1 ? 1 : 0;
   else if (k == "oneshot_bytes_per_cta") c->oneshot_bytes_per_cta = value;
   else if (k == "twoshot_bytes_per_cta") c->twoshot_bytes_per_cta = value;
   else if (k == "max_ctas") c->max_ctas = (int)std::min<int64_t>(value, MAXBLK);
@@ -883,6 +908,7 @@ int cm_comm_get_param(cm_comm_t* c, const char* key, int64_t* value) {
   else if (k == "stream_chunk") *value = c->stream_chunk;
   else if (k == "multi_buffer") *value = c->multi_buffer ? 2 : 1;
   else if (k == "rhd_logp") *value = c->rhd_logp ? 2 : 1;
+  else if (k == "bulk_copy") *value = c->bulk_copy ? 2 : 1;
   else if (k == "oneshot_bytes_per_cta") *value = c->oneshot_bytes_per_cta;
   else if (k == "twoshot_bytes_per_cta") *value = c->twoshot_bytes_per_cta;
   else if (k == "max_ctas") *value = c->max_ctas;

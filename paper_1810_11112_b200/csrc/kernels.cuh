@@ -1536,6 +1536,107 @@ static __global__ void __launch_bounds__(THREADS) batched_copy_kernel(const __gr
   }
 }
 
+// ---- TMA bulk copy (same CopyParams; every member 16-byte aligned) ----------------
+// One elected thread per CTA streams its contiguous byte range through a ring
+// of BULK_STAGES shared-memory stages with the bulk-copy engine:
+// cp.async.bulk global->shared (completion counted on an mbarrier), then
+// cp.async.bulk shared->global (bulk group). Loads run BULK_STAGES-1 chunks
+// ahead of the stores; no SM load/store instructions touch the payload.
+constexpr int BULK_STAGES = 6;
+constexpr int BULK_CHUNK = 16384;
+constexpr int BULK_THREADS = 32;
+constexpr size_t BULK_SMEM = (size_t)BULK_STAGES * BULK_CHUNK + BULK_STAGES * 8;
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+
+static __global__ void __launch_bounds__(BULK_THREADS) bulk_copy_kernel(const __grid_constant__ CopyParams P) {
+  extern __shared__ __align__(128) unsigned char bulk_smem[];
+  if (threadIdx.x != 0) return;
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(bulk_smem + (size_t)BULK_STAGES * BULK_CHUNK);
+  const long long total = P.start[P.n];
+  const int b = blockIdx.x, nb = gridDim.x;
+  long long lo = (long long)(((__int128)total * b) / nb) & ~15ll;
+  long long hi = b == nb - 1 ? total : ((long long)(((__int128)total * (b + 1)) / nb) & ~15ll);
+  if (b == 0) lo = 0;
+  if (hi <= lo) return;
+  char* base = nullptr;
+  if (P.staged) {
+    const Ctrl* ctrl = reinterpret_cast<const Ctrl*>(P.heap + CTRL_OFF);
+    base = P.heap + P.staging_off + (long long)((ctrl->epoch + 1) & 1) * P.staging_bytes;
+  }
+  for (int s = 0; s < BULK_STAGES; ++s)
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[s])));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+
+  // chunk cursor over [lo, hi): pieces of <= BULK_CHUNK bytes inside one member
+  struct Cur {
+    int k;
+    long long pos;
+  };
+  auto first = [&](long long at) {
+    Cur c{0, at};
+    while (c.k < P.n && P.start[c.k + 1] <= at) ++c.k;
+    return c;
+  };
+  auto piece = [&](const Cur& c, const char** src, char** dst) -> int {
+    const long long mend = P.start[c.k + 1] < hi ? P.start[c.k + 1] : hi;
+    long long len = mend - c.pos;
+    if (len > BULK_CHUNK) len = BULK_CHUNK;
+    const long long off = c.pos - P.start[c.k];
+    *src = P.src[c.k] + off;
+    *dst = (P.staged ? base + (long long)(uintptr_t)P.dst[c.k] : P.dst[c.k]) + off;
+    return (int)len;
+  };
+  auto advance = [&](Cur& c, int len) {
+    c.pos += len;
+    while (c.k < P.n && P.start[c.k + 1] <= c.pos) ++c.k;
+  };
+  char* dsts[BULK_STAGES];
+  int lens[BULK_STAGES];
+  Cur ld = first(lo);
+  int issued = 0;
+  auto issue_load = [&](int i) {
+    const int s = i % BULK_STAGES;
+    const char* src;
+    char* dst;
+    const int len = piece(ld, &src, &dst);
+    dsts[s] = dst;
+    lens[s] = len;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar[s])), "r"(len)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(bulk_smem + (size_t)s * BULK_CHUNK)),
+        "l"(src), "r"(len), "r"(smem_u32(&bar[s]))
+        : "memory");
+    advance(ld, len);
+  };
+  while (issued < BULK_STAGES && ld.pos < hi) issue_load(issued++);
+  for (int i = 0; i < issued; ++i) {
+    const int s = i % BULK_STAGES;
+    const unsigned parity = (unsigned)((i / BULK_STAGES) & 1);
+    unsigned ok = 0;
+    while (!ok)
+      asm volatile(
+          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+          : "=r"(ok)
+          : "r"(smem_u32(&bar[s])), "r"(parity)
+          : "memory");
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dsts[s]),
+                 "r"(smem_u32(bulk_smem + (size_t)s * BULK_CHUNK)), "r"(lens[s])
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    // the previous stage's store has finished reading shared memory: refill it
+    if (i >= 1 && ld.pos < hi) {
+      asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      issue_load(issued++);
+    }
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 // ---- local_reduce (core.py:94-110) -------------------------------------------------
 template <class D, int OP>
 __global__ void __launch_bounds__(THREADS) local_reduce_kernel(const char* a, const char* b, char* out,

@@ -314,6 +314,17 @@ def test_local_reduce_and_batched_copy():
         assert torch.equal(a.payload, b.payload)
 
 
+@pytest.mark.parametrize("sizes", [(480_000,) * 53, (65_536, 4, 1_000_000, 262_144), (1_000_003, 77, 5, 999_999)])
+def test_large_fuse_unfuse_bulk_and_sm_copy(sizes):
+    """Large packs: 16-byte aligned members go through the TMA bulk-copy
+    kernel, others through the SM copy; both must equal torch.cat."""
+    ts = [P.Tensor(f"t{i:03d}", "float32", torch.randn(n, device="cuda")) for i, n in enumerate(sizes)]
+    (buf,) = P.fuse(ts, P.FusionConfig(1 << 40))
+    assert torch.equal(buf.payload, torch.cat([t.payload for t in ts]))
+    for a, b in zip(ts, P.unfuse(buf)):
+        assert torch.equal(a.payload, b.payload)
+
+
 def test_p1_identity_and_errors():
     x = torch.randn(17, device="cuda")
     (t, st), = P.allreduce_group([P.Tensor("x", "float32", x)], P.ReduceOp.SUM, vg(1))
