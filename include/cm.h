@@ -166,6 +166,9 @@ int cm_comm_registry(cm_comm_t* comm, cm_registry_t** reg);
  *                         every member is 16-byte aligned, 1 = SM copy (default:
  *                         same kernel time, but its 96 KiB shared-memory carve-out
  *                         costs ~5 us of reconfiguration per step in the bench)
+ *   "bulk_rs"             2..6 = the reduce phase streams its sources into this
+ *                         many 32 KiB shared-memory stages with the bulk-copy
+ *                         engine (default 6), 1 = SM loads
  * get also reads "staging_bytes", "pool_bytes" and "ll_payload_per_source" */
 int cm_comm_set_param(cm_comm_t* comm, const char* key, int64_t value);
 int cm_comm_get_param(cm_comm_t* comm, const char* key, int64_t* value);

@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -71,6 +72,7 @@ struct cm_comm {
   int multi_buffer = 1;                       // batch fused buffers into one launch
   int rhd_logp = 0;                           // 1: rhd_rsa runs the log2(p)-step halving/doubling kernel
   int bulk_copy = 0;                          // fusion pack through the TMA bulk-copy engine (opt-in)
+  int bulk_rs = 6;                            // reduce phase: bulk-engine stages in smem (0: SM loads)
   int64_t oneshot_bytes_per_cta = 8 * 1024;
   int64_t twoshot_bytes_per_cta = 4 * 1024;
   int max_ctas = 148;
@@ -342,6 +344,18 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
   KFn k = pick(logp ? K_RHD : ll == 1 ? K_LL : ll == 2 ? K_LL2 : pipelined ? K_STREAM : K_COLL, L.dtype, L.op, p,
                tree);
   if (!k) return fail(CM_ERR_SHAPE, "unsupported dtype");
+  // reduce phase through the bulk-copy engine (shared-memory stage ring)
+  const bool bulk = c->bulk_rs > 0 && !logp && ll == 0 && !pipelined && (L.phases & PH_RS);
+  P.bulk_rs = bulk ? c->bulk_rs : 0;
+  const size_t dsm = bulk ? rs_smem_bytes(c->bulk_rs) : 0;
+  if (bulk) {
+    static std::set<const void*> configured;
+    if (!configured.count((const void*)k)) {
+      CUDA_TRY(cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)rs_smem_bytes(RS_MAX_STAGES)));
+      configured.insert((const void*)k);
+    }
+  }
   void* args[] = {&P};
   int64_t alg = 0;   // busBW bytes of this launch (nccl-tests convention)
   int64_t ntot = L.n;
@@ -351,14 +365,14 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
   ProfScope prof_scope(c, stream, 0, alg);
   if (c->virt) {
     int per_sm = 0;
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k, THREADS, 0));
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k, THREADS, dsm));
     const int64_t cap = (int64_t)per_sm * c->sms / p;
     if (cap < 1) return fail(CM_ERR_CONFIG, "virtual group too large for one GPU");
     nb = std::min(nb, cap);
     CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k, dim3((unsigned)nb, (unsigned)p),
-                                         dim3(THREADS), args, 0, stream));
+                                         dim3(THREADS), args, dsm, stream));
   } else {
-    CUDA_TRY(cudaLaunchKernel((const void*)k, dim3((unsigned)nb), dim3(THREADS), args, 0, stream));
+    CUDA_TRY(cudaLaunchKernel((const void*)k, dim3((unsigned)nb), dim3(THREADS), args, dsm, stream));
   }
   c->launches += 1;
   // real bytes pulled over NVLink by this rank
@@ -891,6 +905,7 @@ int cm_comm_set_param(cm_comm_t* c, const char* key, int64_t value) {
   else if (k == "multi_buffer") c->multi_buffer = value > 1 ? 1 : 0;
   else if (k == "rhd_logp") c->rhd_logp = value > 1 ? 1 : 0;
   else if (k == "bulk_copy") c->bulk_copy = value > 1 ? 1 : 0;
+  else if (k == "bulk_rs") c->bulk_rs = value == 1 ? 0 : (int)std::min<int64_t>(value, RS_MAX_STAGES);
   else if (k == "oneshot_bytes_per_cta") c->oneshot_bytes_per_cta = value;
   else if (k == "twoshot_bytes_per_cta") c->twoshot_bytes_per_cta = value;
   else if (k == "max_ctas") c->max_ctas = (int)std::min<int64_t>(value, MAXBLK);
@@ -909,6 +924,7 @@ int cm_comm_get_param(cm_comm_t* c, const char* key, int64_t* value) {
   else if (k == "multi_buffer") *value = c->multi_buffer ? 2 : 1;
   else if (k == "rhd_logp") *value = c->rhd_logp ? 2 : 1;
   else if (k == "bulk_copy") *value = c->bulk_copy ? 2 : 1;
+  else if (k == "bulk_rs") *value = c->bulk_rs ? c->bulk_rs : 1;
   else if (k == "oneshot_bytes_per_cta") *value = c->oneshot_bytes_per_cta;
   else if (k == "twoshot_bytes_per_cta") *value = c->twoshot_bytes_per_cta;
   else if (k == "max_ctas") *value = c->max_ctas;
@@ -1543,7 +1559,8 @@ int cm_batched_copy(int n, const void* const* srcs, void* const* dsts, const int
 int cm_bench_p2p(cm_comm_t* c, int mode, int64_t bytes, int ctas, int iters, void* stream_,
                  double* ms_per_iter) {
   if (c->virt || c->size < 2) return fail(CM_ERR_UNSUPPORTED, "needs a real group of >= 2 ranks");
-  if ((int64_t)bytes * c->size > (int64_t)c->staging_bytes) return fail(CM_ERR_CONFIG, "bytes too large");
+  const int64_t need = (int64_t)bytes * ((mode >= 6 && mode <= 9) ? 6 : c->size);
+  if (need > (int64_t)c->staging_bytes) return fail(CM_ERR_CONFIG, "bytes too large");
   cudaStream_t s = static_cast<cudaStream_t>(stream_);
   CollParams P;
   memset(&P, 0, sizeof P);
@@ -1554,9 +1571,29 @@ int cm_bench_p2p(cm_comm_t* c, int mode, int64_t bytes, int ctas, int iters, voi
   cudaEvent_t e0, e1;
   CUDA_TRY(cudaEventCreate(&e0));
   CUDA_TRY(cudaEventCreate(&e1));
-  p2p_bw_kernel<<<ctas, THREADS, 0, s>>>(P, mode, bytes);
+  CopyParams B;
+  memset(&B, 0, sizeof B);
+  if (mode == 4) {
+    CUDA_TRY(cudaFuncSetAttribute((const void*)bulk_copy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)BULK_SMEM));
+    int m = 0;
+    B.start[0] = 0;
+    for (int i = 1; i < c->size; ++i) {
+      const int q = (c->rank + i) % c->size;
+      B.src[m] = c->heap[q] + c->staging_off + (int64_t)c->rank * bytes;
+      B.dst[m] = c->local + c->staging_off + (int64_t)q * bytes;
+      B.start[m + 1] = B.start[m] + bytes;
+      ++m;
+    }
+    B.n = m;
+  }
+  auto launch = [&]() {
+    if (mode == 4) bulk_copy_kernel<<<ctas, BULK_THREADS, BULK_SMEM, s>>>(B);
+    else p2p_bw_kernel<<<ctas, THREADS, 0, s>>>(P, mode, bytes);
+  };
+  launch();
   CUDA_TRY(cudaEventRecord(e0, s));
-  for (int i = 0; i < iters; ++i) p2p_bw_kernel<<<ctas, THREADS, 0, s>>>(P, mode, bytes);
+  for (int i = 0; i < iters; ++i) launch();
   CUDA_TRY(cudaEventRecord(e1, s));
   CUDA_TRY(cudaEventSynchronize(e1));
   float ms = 0;

@@ -135,6 +135,7 @@ struct CollParams {
   long long inl[8];          // SRC_INLINE: the input travels in the parameters (cm_agree)
   unsigned long long* done_flag;  // optional: written with done_value when the call completes
   unsigned long long done_value;
+  int bulk_rs;               // >0: reduce through the bulk-copy engine with this many smem stages
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -372,9 +373,10 @@ __device__ void reduce_range(const char* const* seq, int p, int m, int excess, l
   // vector body: vectors j in [body_lo/W, body_hi/W)
   const long long v0 = body_lo / W, v1 = body_hi / W;
   using A = typename D::A;
-  // vector groups in flight per thread: ~64 operand registers whatever MP is
+  // vector groups in flight per thread: ~32 operand registers whatever MP is (the
+  // bulk-engine path carries the large-message traffic; this one stays spill-free)
   constexpr int OPR = MP * W * (int)(sizeof(A) / 4);
-  constexpr int U = OPR >= 64 ? 1 : 64 / OPR;
+  constexpr int U = OPR >= 32 ? 1 : 32 / OPR;
   // Groups are predicated rather than peeled: the last partial round still
   // keeps every remaining load in flight at once (a peeled one-group tail
   // would pay one NVLink round trip per group).
@@ -484,6 +486,131 @@ __device__ void multi_copy(const CopyRange* R, int nr, VecRange* V) {
 }
 
 __device__ __forceinline__ bool al16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  unsigned ok = 0;
+  while (!ok)
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+}
+
+// ---- reduce through the bulk-copy engine ----------------------------------------
+// The reduce-scatter's sources (p - 1 of them across NVLink) are streamed into
+// a ring of shared-memory stages by ONE producer thread with cp.async.bulk
+// (completion counted on a `full` mbarrier per stage), so the bytes in flight
+// no longer depend on registers: stages x 32 KiB per SM. Warps 0..14 fold
+// each stage (sources in the reference order) and write out / staging; each
+// warp then arrives on the stage's `empty` mbarrier so the producer can refill.
+constexpr int RS_MAX_STAGES = 6;
+constexpr int RS_STAGE_BYTES = 32768;
+constexpr int RS_CONSUMERS = THREADS - 32;
+__host__ __device__ constexpr size_t rs_smem_bytes(int stages) {
+  return (size_t)stages * RS_STAGE_BYTES + (2 * (size_t)stages + 2) * 8;
+}
+
+struct BulkRS {
+  unsigned char* smem;        // stages x RS_STAGE_BYTES
+  unsigned long long* full;   // [stages], 1 arrival + tx bytes
+  unsigned long long* empty;  // [stages], RS_CONSUMERS / 32 arrivals
+  unsigned long long* seqno;  // stage uses so far in this launch
+  int stages;
+};
+
+__device__ __forceinline__ BulkRS bulk_rs_setup(unsigned char* dyn, int stages, int tid) {
+  BulkRS B;
+  B.stages = stages;
+  B.smem = dyn;
+  B.full = reinterpret_cast<unsigned long long*>(dyn + (size_t)stages * RS_STAGE_BYTES);
+  B.empty = B.full + stages;
+  B.seqno = B.empty + stages;
+  if (tid == 0) {
+    for (int s = 0; s < stages; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&B.full[s])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&B.empty[s])), "r"(RS_CONSUMERS / 32));
+    }
+    *B.seqno = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  return B;
+}
+
+// Same contract as reduce_range (sources 16-byte aligned at vector boundaries).
+template <class D, int OP, int MP, bool TREE>
+__device__ void reduce_range_bulk(const BulkRS& B, const char* const* seq, int p, int m, int excess,
+                                  long long lo, long long hi, int average, char* out, long long out_shift,
+                                  char* red, long long red_shift, int tid) {
+  using S = typename D::S;
+  using A = typename D::A;
+  constexpr int W = 16 / sizeof(S);
+  constexpr int SZ = sizeof(S);
+  long long body_lo = ((lo + W - 1) / W) * W, body_hi = (hi / W) * W;
+  if (body_hi < body_lo) body_lo = body_hi = hi;
+  for (long long i = lo + tid; i < body_lo; i += THREADS)
+    reduce_one<D, OP, MP, 1, TREE>(seq, p, m, excess, i, average, out, out_shift, red, red_shift);
+  for (long long i = body_hi + tid; i < hi; i += THREADS)
+    reduce_one<D, OP, MP, 1, TREE>(seq, p, m, excess, i, average, out, out_shift, red, red_shift);
+  const long long nbytes = (body_hi - body_lo) * SZ;
+  if (nbytes <= 0) return;
+  const int ch = (RS_STAGE_BYTES / p) & ~15;            // bytes per source per stage
+  const long long C = (nbytes + ch - 1) / ch;
+  const unsigned long long base = *B.seqno;
+  if (tid == RS_CONSUMERS) {                            // producer: warp 15, lane 0
+    asm volatile("fence.proxy.async;" ::: "memory");
+    for (long long c = 0; c < C; ++c) {
+      const unsigned long long g = base + (unsigned long long)c;
+      const int s = (int)(g % B.stages);
+      if (g >= (unsigned long long)B.stages) mbar_wait(&B.empty[s], (unsigned)(((g / B.stages) - 1) & 1));
+      const long long off = body_lo * SZ + c * ch;
+      const int len = (int)((nbytes - c * ch) < ch ? (nbytes - c * ch) : ch);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&B.full[s])),
+                   "r"(len * p)
+                   : "memory");
+      for (int k = 0; k < p; ++k)
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_u32(B.smem + (size_t)s * RS_STAGE_BYTES + (size_t)k * ch)),
+            "l"(seq[k] + off), "r"(len), "r"(smem_u32(&B.full[s]))
+            : "memory");
+    }
+  } else if (tid < RS_CONSUMERS) {
+    for (long long c = 0; c < C; ++c) {
+      const unsigned long long g = base + (unsigned long long)c;
+      const int s = (int)(g % B.stages);
+      mbar_wait(&B.full[s], (unsigned)((g / B.stages) & 1));
+      const int len = (int)((nbytes - c * ch) < ch ? (nbytes - c * ch) : ch);
+      const int nv = len / 16;
+      const char* st = reinterpret_cast<const char*>(B.smem + (size_t)s * RS_STAGE_BYTES);
+      const long long e0 = body_lo + c * (ch / SZ);
+      for (int v = tid; v < nv; v += RS_CONSUMERS) {
+        A u[MP][W];
+#pragma unroll
+        for (int k = 0; k < MP; ++k)
+          if (k < p) load_vec<D, W>(st + (size_t)k * ch, (long long)v * W, u[k]);
+        fold<OP, MP, W, TREE>(u, p, m, excess);
+        if (average) {
+#pragma unroll
+          for (int w = 0; w < W; ++w) u[0][w] = div_p<A>(u[0][w], p);
+        }
+        const long long i = e0 + (long long)v * W;
+        store_vec<D, W>(out, i - out_shift, u[0]);
+        if (red) store_vec<D, W>(red, i - red_shift, u[0]);
+      }
+      __syncwarp();
+      if ((tid & 31) == 0)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&B.empty[s])) : "memory");
+    }
+  }
+  __syncthreads();
+  if (tid == 0) *B.seqno = base + (unsigned long long)C;
+  __syncthreads();
+}
 __device__ __forceinline__ bool al16s(const char* base, long long shift_elems, int sz) {
   return (((uintptr_t)base - (uintptr_t)(shift_elems * sz)) & 15u) == 0;
 }
@@ -628,7 +755,10 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
   __shared__ int s_rord[MAXP];          // fold sequence as source ranks
   __shared__ int s_err;
 
+  extern __shared__ __align__(128) unsigned char coll_dyn[];
   CM_TRACE(P, lr, b, 0);
+  BulkRS BR{};
+  if (!STREAM && P.bulk_rs) BR = bulk_rs_setup(coll_dyn, P.bulk_rs, tid);
   if (tid == 0) {
     s_epoch = ctrl->epoch + 1;
     s_err = 0;
@@ -764,8 +894,11 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
         __syncthreads();
         bool vec = al16(bo) && al16(red);
         for (int q = 0; q < p; ++q) vec = vec && al16(s_seqk[q]);
-        reduce_range<D, OP, MP, TREE>(s_seqk, p, m, excess, lo, hi, vec, P.average, bo, 0, red, 0,
-                                      tid, blockDim.x);
+        if (P.bulk_rs && vec)
+          reduce_range_bulk<D, OP, MP, TREE>(BR, s_seqk, p, m, excess, lo, hi, P.average, bo, 0, red, 0, tid);
+        else
+          reduce_range<D, OP, MP, TREE>(s_seqk, p, m, excess, lo, hi, vec, P.average, bo, 0, red, 0,
+                                        tid, blockDim.x);
         __syncthreads();
         continue;
       }
@@ -796,8 +929,11 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
         __syncthreads();
         bool vec = al16(bo) && al16(red);
         for (int q = 0; q < p; ++q) vec = vec && al16(s_seqk[q]);
-        reduce_range<D, OP, MP, TREE>(s_seqk, p, m, excess, i, pe, vec, P.average, bo, 0, red, 0,
-                                      tid, blockDim.x);
+        if (P.bulk_rs && vec)
+          reduce_range_bulk<D, OP, MP, TREE>(BR, s_seqk, p, m, excess, i, pe, P.average, bo, 0, red, 0, tid);
+        else
+          reduce_range<D, OP, MP, TREE>(s_seqk, p, m, excess, i, pe, vec, P.average, bo, 0, red, 0,
+                                        tid, blockDim.x);
         __syncthreads();
         i = pe;
       }
@@ -844,8 +980,12 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
       vec = vec && al16s(red, red_shift, SZ);
     }
     const long long lo = slice_bound(so, sl, b, nb), hi = slice_bound(so, sl, b + 1, nb);
-    reduce_range<D, OP, MP, TREE>(s_seq, p, m, excess, lo, hi, vec, P.average, out, out_shift,
-                                  red, red_shift, tid, blockDim.x);
+    if (P.bulk_rs && vec)
+      reduce_range_bulk<D, OP, MP, TREE>(BR, s_seq, p, m, excess, lo, hi, P.average, out, out_shift, red,
+                                         red_shift, tid);
+    else
+      reduce_range<D, OP, MP, TREE>(s_seq, p, m, excess, lo, hi, vec, P.average, out, out_shift,
+                                    red, red_shift, tid, blockDim.x);
   }
 
   // 4. RS -> AG barrier (per CTA index) and 5. allgather
@@ -1546,10 +1686,6 @@ constexpr int BULK_STAGES = 6;
 constexpr int BULK_CHUNK = 16384;
 constexpr int BULK_THREADS = 32;
 constexpr size_t BULK_SMEM = (size_t)BULK_STAGES * BULK_CHUNK + BULK_STAGES * 8;
-
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return (unsigned)__cvta_generic_to_shared(p);
-}
 
 static __global__ void __launch_bounds__(BULK_THREADS) bulk_copy_kernel(const __grid_constant__ CopyParams P) {
   extern __shared__ __align__(128) unsigned char bulk_smem[];
