@@ -225,6 +225,7 @@ struct Launch {
   void* bout[MAXBUF] = {};
   unsigned long long* done_flag = nullptr;
   unsigned long long done_value = 0;
+  unsigned long long agree_gate = 0;  // run only if agreement check `agree_gate` succeeded
   int ll = 0;                       // one-shot through the LL slots
   const void* in[MAXP] = {};
   void* out[MAXP] = {};
@@ -303,6 +304,7 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
   if (L.inl) for (int i = 0; i < 8; ++i) P.inl[i] = L.inl[i];
   P.done_flag = L.done_flag;
   P.done_value = L.done_value;
+  P.agree_gate = L.agree_gate;
   P.trace = c->trace;
   P.trace_ctas = c->trace_ctas;
 
@@ -341,6 +343,8 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
                          L.phases == (PH_RS | PH_AG) &&
                          c->stream_chunk > 0 && maxseg / std::max<int64_t>(nb, 1) >= 2 * c->stream_chunk;
   P.stream_chunk = c->stream_chunk;
+  if (L.agree_gate && (logp || ll != 0))
+    return fail(CM_ERR_CONFIG, "internal: agreement gate needs the pull collective kernel");
   KFn k = pick(logp ? K_RHD : ll == 1 ? K_LL : ll == 2 ? K_LL2 : pipelined ? K_STREAM : K_COLL, L.dtype, L.op, p,
                tree);
   if (!k) return fail(CM_ERR_SHAPE, "unsupported dtype");
@@ -1449,8 +1453,7 @@ int cm_fused_allreduce_agreed(cm_comm_t* c, int n, const void* const* sends,
       L.gsig = sig;
       L.srcmode = SRC_GATHER;
       L.n = L.bn[0];
-      if ((st = resolve_agree())) return st;
-      if (!*agreed) return CM_OK;
+      L.agree_gate = pending ? ticket : 0;   // device-side gate: no host wait before the launch
       if ((st = launch_collective(c, L, stream))) return st;
       if ((st = drain(g, h))) return st;
       g = h;
@@ -1483,8 +1486,7 @@ int cm_fused_allreduce_agreed(cm_comm_t* c, int n, const void* const* sends,
         return st;
       L.srcmode = SRC_PRESTAGED;
       L.n = L.bn[0];
-      if ((st = resolve_agree())) return st;
-      if (!*agreed) return CM_OK;            // the queued pack only touched local staging
+      L.agree_gate = pending ? ticket : 0;   // the queued pack only touched local staging
       if ((st = launch_collective(c, L, stream))) return st;
       if ((st = drain(g, h))) return st;
       g = h;
@@ -1511,13 +1513,21 @@ int cm_fused_allreduce_agreed(cm_comm_t* c, int n, const void* const* sends,
         return st;
       L.srcmode = SRC_PRESTAGED;
     }
-    if ((st = resolve_agree())) return st;
-    if (!*agreed) return CM_OK;
+    if (L.ll != 0 || c->rhd_logp) {          // LL / log-p kernels have no gate: wait on the host
+      if ((st = resolve_agree())) return st;
+      if (!*agreed) return CM_OK;
+    } else {
+      L.agree_gate = pending ? ticket : 0;
+    }
     if ((st = launch_collective(c, L, stream))) return st;
     if ((st = drain(g, g + 1))) return st;
     ++g;
   }
   if ((st = hp.join())) return st;
+  // the agreement result arrives while the gated collectives run; on a
+  // mismatch they were no-ops on every rank and the caller negotiates
+  if ((st = resolve_agree())) return st;
+  if (!*agreed) return CM_OK;
   for (int q = 0; q < ngroups; ++q) count_stats(c, stats[q]);
   *n_calls = ngroups;
   return CM_OK;

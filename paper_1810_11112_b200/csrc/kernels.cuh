@@ -71,9 +71,11 @@ constexpr unsigned long long REG_FLAG = 1ull << 62;
 constexpr size_t CTRL_REGION = LL_OFF;                  // zeroed at creation
 
 struct Ctrl {
-  unsigned long long epoch;  // calls completed by this rank
-  unsigned int done;         // CTAs finished in the current call
+  unsigned long long epoch;      // calls completed by this rank
+  unsigned int done;             // CTAs finished in the current call
   unsigned int pad;
+  unsigned long long agree_tag;  // ticket of the last agreement check (cm_agree)
+  long long agree_ok;            // its outcome: every rank held the same values
 };
 
 struct Rec {
@@ -136,6 +138,9 @@ struct CollParams {
   unsigned long long* done_flag;  // optional: written with done_value when the call completes
   unsigned long long done_value;
   int bulk_rs;               // >0: reduce through the bulk-copy engine with this many smem stages
+  // >0: run only if the agreement check with this ticket (queued before on the
+  // same stream) succeeded; otherwise every rank skips the call identically
+  unsigned long long agree_gate;
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -754,6 +759,7 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
   __shared__ const char* s_seq[MAXP];   // fold sequence
   __shared__ int s_rord[MAXP];          // fold sequence as source ranks
   __shared__ int s_err;
+  __shared__ int s_skip;                // agreement gate failed: the call is a no-op
 
   extern __shared__ __align__(128) unsigned char coll_dyn[];
   CM_TRACE(P, lr, b, 0);
@@ -762,6 +768,9 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
   if (tid == 0) {
     s_epoch = ctrl->epoch + 1;
     s_err = 0;
+    // the agreement kernel ran before this one on the stream; its outcome is
+    // identical on every rank, so every rank skips (or runs) consistently
+    s_skip = P.agree_gate && !(ctrl->agree_tag == P.agree_gate && ctrl->agree_ok) ? 1 : 0;
   }
   __syncthreads();
   const unsigned long long e = s_epoch;
@@ -792,7 +801,7 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
   __shared__ CopyRange s_cr[MAXBUF * MAXP + 1];
   __shared__ VecRange s_vr[MAXBUF * MAXP + 1];
   __shared__ int s_ncr;
-  if (P.srcmode == SRC_COPYIN) {
+  if (P.srcmode == SRC_COPYIN && !s_skip) {
     char* stage = myheap + stage_off;
     if (ag_only) {
       if (tid == 0) {
@@ -819,14 +828,14 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
   CM_TRACE(P, lr, b, 1);
 
   // 2. publish my record to every peer, then collect theirs
-  if (tid < p) {
+  if (tid < p && !s_skip) {
     Rec* r = rec_slot(P.heap[tid], par, b, rank);
     st_relaxed_sys(&r->hdr, P.hdr);
     st_relaxed_sys_s64(&r->srcoff, my_srcoff);
     st_relaxed_sys_s64(&r->redoff, my_redoff);
     st_release_sys(&r->epoch, e);
   }
-  if (tid < p) {
+  if (tid < p && !s_skip) {
     Rec* r = rec_slot(myheap, par, b, tid);
     if (!wait_geq(&r->epoch, e, P.timeout_cycles)) {
       atomicExch(&s_err, ERR_TRANSPORT);
@@ -861,7 +870,7 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
   }
   __syncthreads();
   CM_TRACE(P, lr, b, 2);
-  if (s_err) goto finish;
+  if (s_err || s_skip) goto finish;
 
   if constexpr (STREAM) {
     // Pipelined two-shot: warps 0..7 reduce chunk after chunk of my segment
@@ -1085,9 +1094,11 @@ __global__ void __launch_bounds__(THREADS) ll_kernel(const __grid_constant__ Col
   __shared__ unsigned long long s_epoch;
   __shared__ int s_err;
   __shared__ int s_seq[MAXP];
+  __shared__ int s_disagree;
   if (tid == 0) {
     s_epoch = ctrl->epoch + 1;
     s_err = 0;
+    s_disagree = 0;
   }
   int m = 1;
   while ((m << 1) <= p) m <<= 1;
@@ -1172,6 +1183,10 @@ __global__ void __launch_bounds__(THREADS) ll_kernel(const __grid_constant__ Col
     union { uint2 u; S s[E]; unsigned char c[8]; } res;
 #pragma unroll
     for (int t = 0; t < E; ++t) res.s[t] = from_acc<D>(P.average ? div_p<A>(v[0][t], p) : v[0][t]);
+    // agreement check (cm_agree): the MAX of every rank's values equals mine
+    // for all values on every rank iff all ranks hold the same values
+    if (P.done_flag && u < 8 && (long long)(((unsigned long long)res.u.y << 32) | res.u.x) != P.inl[u])
+      s_disagree = 1;
     const long long boff = u * 8;
     if (boff + 8 <= nbytes && ((((uintptr_t)out) & 7u) == 0)) {
       *reinterpret_cast<uint2*>(out + boff) = res.u;
@@ -1191,6 +1206,8 @@ ll_finish:
       ctrl->epoch = e;
       __threadfence();
       if (P.done_flag) {                 // host spins on this (cm_agree)
+        ctrl->agree_ok = s_disagree ? 0 : 1;   // read by gated collectives queued behind
+        ctrl->agree_tag = P.done_value;
         __threadfence_system();
         *reinterpret_cast<volatile unsigned long long*>(P.done_flag) = P.done_value;
       }

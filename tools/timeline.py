@@ -26,6 +26,8 @@ gs = bench.make_grads("resnet50_like", rank, None if HOST else dev, pinned=HOST)
     bench.make_grads("resnet50_like", rank, dev)
 if HOST:
     comm.blocking = True
+if os.environ.get("REG") == "1":
+    P.register_gradients(gs, comm)
 group = P.GroupSpec(world)
 out = None
 for _ in range(5):
