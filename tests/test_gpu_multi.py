@@ -47,3 +47,38 @@ def test_four_gpus():
 @pytest.mark.multigpu(8)
 def test_eight_gpus():
     _run(min(8, torch.cuda.device_count()))
+
+
+@pytest.mark.gpu
+@pytest.mark.multigpu(2)
+def test_cli_microbench_and_train_two_gpus(tmp_path):
+    """The reference-format harness (cli.py) under torchrun: CSV header and
+    rows as collectium writes them, plus the B200 columns."""
+    out = tmp_path / "micro.csv"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           "-m", "paper_1810_11112_b200.cli", "--mode", "microbench", "--msg-min-bytes", "8",
+           "--msg-max-bytes", "1048576", "--warmup-iters", "2", "--timed-iters", "5", "--output", str(out)]
+    env = dict(os.environ, OMP_NUM_THREADS="1")
+    proc = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert proc.returncode == 0, (proc.stdout + proc.stderr)[-4000:]
+    rows = out.read_text().splitlines()
+    assert rows[0] == ("message_bytes,algo,p,mean_latency_s,min_latency_s,max_latency_s,messages_per_rank,"
+                       "device_latency_s,bus_gbps,roofline_frac")
+    assert len(rows) == 1 + 18                       # 8 B .. 1 MiB
+    for r in rows[1:]:
+        f = r.split(",")
+        size, algo, p = int(f[0]), f[1], int(f[2])
+        assert p == 2 and algo == ("rhd_rsa" if size < 131072 else "ring_rsa")
+        assert int(f[6]) == 2                        # messages_per_rank, reference schedule at p=2
+        assert 0 < float(f[4]) <= float(f[3]) <= float(f[5])
+    out2 = tmp_path / "train.csv"
+    cmd = cmd[:cmd.index("--mode")] + ["--mode", "train", "--model", "mobilenet_like", "--warmup-iters", "1",
+                                        "--timed-iters", "2", "--output", str(out2)]
+    cmd[cmd.index("--master-port") + 1] = str(_free_port())
+    proc = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert proc.returncode == 0, (proc.stdout + proc.stderr)[-4000:]
+    rows = out2.read_text().splitlines()
+    assert rows[0] == "model,strategy,p,images_per_sec,ideal,efficiency"
+    f = rows[1].split(",")
+    assert f[:3] == ["mobilenet_like", "horovod_allreduce", "2"] and 0 < float(f[5]) <= 1.0
