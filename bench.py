@@ -675,13 +675,93 @@ def refsweep(args):
     emit({"mode": "refsweep", "p": p, "csv": rows})
 
 
+def overlap(args, rank, world, local):
+    """Caller-side study: a synthetic backward pass (one
+    bf16 GEMM per layer on the producer stream, last layer first) producing the
+    C5 gradients, aggregated (A) after the backward pass with aggregate() or
+    (B) overlapped with it through OverlappedAggregator. Step = backward +
+    aggregation, CUDA events, max over ranks; results checked equal."""
+    import paper_1810_11112_b200 as P
+    device = torch.device("cuda", local)
+    torch.cuda.set_device(device)
+    layers = MODELS[args.model]
+    S = sum(layers) * 4
+    comm = P.Communicator(rank, world, local, staging_bytes=max(256 << 20, S + (8 << 20)),
+                          pool_bytes=64 << 20, blocking=False)
+    for kv in args.param:
+        k, v = kv.split("=")
+        comm.set_param(k, int(v))
+    group = P.GroupSpec(world)
+    cfg = P.FusionConfig(args.fusion_threshold)
+    src = make_grads(args.model, rank, device)
+    names = [t.name for t in src.tensors]
+    grads = [torch.empty_like(t.payload) for t in src.tensors]
+    gdim = args.gemm
+    wts = [torch.randn(gdim, gdim, device=device, dtype=torch.bfloat16) for _ in range(2)]
+
+    def layer_compute():
+        torch.matmul(wts[0], wts[1])
+
+    def backward(ov=None):
+        for i in reversed(range(len(grads))):
+            layer_compute()
+            grads[i].copy_(src.tensors[i].payload)
+            if ov is not None:
+                ov.ready(names[i], grads[i])
+
+    gs_view = P.GradientSet(tuple(P.Tensor(nm, "float32", g) for nm, g in zip(names, grads)))
+    ov = P.OverlappedAggregator(gs_view, comm, algo=args.algo, cfg=cfg, max_ctas=args.ov_ctas or None,
+                                priority=args.ov_priority)
+
+    def step_seq():
+        backward()
+        return P.aggregate(gs_view, group, comm, algo=args.algo, cfg=cfg)
+
+    def step_ovl():
+        backward(ov)
+        return ov.finish()
+
+    def step_bwd():
+        backward()
+
+    def timed(fn, k):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        barrier(world)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(k):
+            r = fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return max_over_ranks(e0.elapsed_time(e1) / k, world), r
+
+    k = max(5, min(args.steps, 30))
+    t_bwd, _ = timed(step_bwd, k)
+    t_seq, r_seq = timed(step_seq, k)
+    t_ovl, r_ovl = timed(step_ovl, k)
+    same = all(a.to_bytes() == b.to_bytes() for a, b in zip(r_seq.tensors, r_ovl.tensors))
+    comm.synchronize()
+    if rank == 0:
+        emit({"mode": "overlap", "n_gpus": world, "model": args.model, "gemm": gdim,
+              "backward_ms": round(t_bwd, 4), "sequential_ms": round(t_seq, 4), "overlapped_ms": round(t_ovl, 4),
+              "hidden_frac": round((t_seq - t_ovl) / max(t_seq - t_bwd, 1e-9), 3),
+              "groups": len(ov.groups), "ov_ctas": args.ov_ctas, "ov_priority": args.ov_priority,
+              "bit_identical": same})
+    comm.close()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=None)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--mode", choices=("headline", "sweep", "tune", "refsweep"), default="headline")
+    ap.add_argument("--mode", choices=("headline", "sweep", "tune", "refsweep", "overlap"), default="headline")
+    ap.add_argument("--gemm", type=int, default=2048, help="overlap: per-layer bf16 GEMM size")
+    ap.add_argument("--ov-ctas", type=int, default=64, help="overlap: CTA cap of overlapped collectives (0: none)")
+    ap.add_argument("--ov-priority", type=int, default=-1, help="overlap: communication stream priority")
     ap.add_argument("--ranks", type=int, default=4, help="refsweep: simulated ranks")
     ap.add_argument("--model", choices=tuple(MODELS), default="resnet50_like")
     ap.add_argument("--dtype", choices=("float32", "bfloat16"), default="float32")
@@ -720,6 +800,8 @@ def main():
             headline(args, rank, world, local)
         elif args.mode == "sweep":
             sweep(args, rank, world, local)
+        elif args.mode == "overlap":
+            overlap(args, rank, world, local)
         else:
             tune(args, rank, world, local)
     finally:

@@ -23,6 +23,7 @@ from .collectives import (ALGORITHMS, DEFAULT_SWITCH_BYTES, CollectiveStats,  # 
 from .aggregation import (DEFAULT_FUSION_THRESHOLD, FusedBuffer, FusionConfig,  # noqa: F401
                           GradientSet, aggregate, aggregate_group, fuse,
                           fuse_plan, negotiate_ready, register_gradients, unfuse)
+from .overlap import OverlappedAggregator  # noqa: F401
 from .registry import (BufferHandle, BufferKind, BufferRegistry, Policy,  # noqa: F401
                        RegistryStats)
 

@@ -1,0 +1,184 @@
+"""Overlapped gradient aggregation (the caller side of
+the path): fused allreduces start while the backward pass is still producing
+gradients, as Horovod's background coordinator and PyTorch DDP's buckets do.
+
+The fusion plan is the reference's (aggregation.py:95-130: canonical sorted
+names, greedy first-fit under the threshold) computed ONCE over the full
+gradient schema, so every fused group, its ring chunking and therefore every
+result bit are identical to ``aggregate`` over the complete set
+(aggregation.py:138-176). Groups are launched in a fixed order that is the
+same on every rank (reverse plan order by default: backward produces the
+last layers first), each as soon as it and every group before it in that
+order are complete, on a communication stream that waits only for the
+producer-stream event of the group's last gradient. ``finish`` joins the
+communication stream into the caller's stream and returns the means.
+
+Ranks may mark gradients ready in different orders; the launch order is
+static, so the collectives still match one to one across ranks (no
+negotiation round per step).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from collections import namedtuple
+
+import torch
+
+from . import _lib as L
+from .aggregation import FusionConfig, GradientSet, fuse_plan
+from .collectives import DEFAULT_SWITCH_BYTES, CollectiveStats
+from .comm import Communicator
+from .core import DTYPES, Tensor
+from .errors import ConfigError, ShapeError
+from .tuning import switch_bytes_for
+
+_Spec = namedtuple("_Spec", "name len dtype nbytes")
+
+
+class OverlappedAggregator:
+    """``ready(name, grad)`` per gradient as the backward pass produces it,
+    then ``finish()`` -> GradientSet of means (canonical order), identical
+    to ``aggregate(all gradients)``.
+
+    ``schema``: a GradientSet (used as a template) or ``[(name, numel,
+    dtype), ...]``. ``launch_order``: "reverse" (default, last layers first)
+    or "forward". ``max_ctas`` caps the CTAs of each overlapped collective
+    (None: the communicator's setting); ``priority`` is the communication
+    stream's priority (-1: high).
+
+    Stream rules (as for NCCL communicators): the means are views of
+    persistent per-group buckets that the next step overwrites once its
+    group's gradients are ready on the producer stream, so consume them on
+    that stream before producing the next gradients; while a step is in
+    flight, issue no other collective on the same communicator from another
+    stream."""
+
+    def __init__(self, schema, comm: Communicator, algo: str = "auto", cfg: FusionConfig | None = None,
+                 switch_bytes: int | None = DEFAULT_SWITCH_BYTES, launch_order: str = "reverse",
+                 max_ctas: int | None = 64, priority: int = -1):
+        if isinstance(schema, GradientSet):
+            specs = [(t.name, t.len, t.dtype) for t in schema.tensors]
+        else:
+            specs = list(schema)
+        if len({nm for nm, _, _ in specs}) != len(specs):
+            raise ShapeError("duplicate gradient names in the schema")
+        self.comm = comm
+        self.algo = algo
+        self.cfg = cfg or FusionConfig()
+        self.switch = switch_bytes_for(comm.size) if switch_bytes is None else int(switch_bytes)
+        self.specs = sorted((_Spec(nm, int(n), dt, int(n) * torch.empty((), dtype=DTYPES[dt]).element_size())
+                             for nm, n, dt in specs), key=lambda s: s.name)       # aggregation.py:77,85
+        for s in self.specs:
+            if s.dtype not in ("float32", "float64", "bfloat16"):
+                raise ShapeError(f"aggregate averages floating-point gradients, got {s.dtype}")
+        self.groups = fuse_plan(self.specs, self.cfg)
+        self.by_name = {s.name: s for s in self.specs}
+        self.group_of = {}
+        for g, members in enumerate(self.groups):
+            for i in members:
+                self.group_of[self.specs[i].name] = g
+        if launch_order == "reverse":
+            self.order = list(range(len(self.groups)))[::-1]
+        elif launch_order == "forward":
+            self.order = list(range(len(self.groups)))
+        else:
+            raise ConfigError(f"launch_order must be 'reverse' or 'forward', got {launch_order!r}")
+        dev = comm.device
+        # high-priority communication stream: its CTAs are scheduled first as
+        # the producer's kernels drain, and a CTA cap leaves SMs to the
+        # backward pass (the collective is NVLink-bound well below 148 CTAs)
+        self.stream = torch.cuda.Stream(dev, priority=priority)
+        self.max_ctas = max_ctas
+        self.buckets = [torch.empty(sum(self.specs[i].len for i in m), dtype=DTYPES[self.specs[m[0]].dtype],
+                                    device=dev) for m in self.groups]
+        self.stats = [(L.Stats * 1)() for _ in self.groups]
+        self.step_stats: list[CollectiveStats] = []
+        self.iteration = 0
+        self._reset()
+
+    # -- per step ---------------------------------------------------------------
+    def _reset(self):
+        self._tensors = {}
+        self._missing = [len(m) for m in self.groups]
+        self._events = [None] * len(self.groups)
+        self._next = 0
+        self.step_stats = []
+
+    def ready(self, name: str, grad) -> None:
+        """Hand over one gradient (torch CUDA tensor or Tensor) produced on
+        the current stream; launches every fused group that became due."""
+        t = grad.payload if isinstance(grad, Tensor) else grad
+        g = self.group_of.get(name)
+        if g is None:
+            raise ShapeError(f"{name!r} is not in the gradient schema")
+        if name in self._tensors:
+            raise ShapeError(f"{name!r} marked ready twice in one step")
+        spec = self.by_name[name]
+        if not t.is_cuda or t.numel() != spec.len or t.dtype != DTYPES[spec.dtype] or not t.is_contiguous():
+            raise ShapeError(f"{name!r}: expected a contiguous CUDA {spec.dtype} tensor of {spec.len} elements")
+        t.record_stream(self.stream)              # kept alive until the collective has read it
+        self._tensors[name] = t
+        self._missing[g] -= 1
+        if self._missing[g] == 0:
+            ev = torch.cuda.Event()
+            ev.record(torch.cuda.current_stream(t.device))
+            self._events[g] = ev
+            self._launch_due()
+
+    def _launch_due(self):
+        while self._next < len(self.order) and self._missing[self.order[self._next]] == 0:
+            self._launch(self.order[self._next])
+            self._next += 1
+
+    def _launch(self, g: int):
+        members = [self.specs[i] for i in self.groups[g]]
+        ts = [self._tensors[s.name] for s in members]
+        n = len(ts)
+        ncalls = C.c_int()
+        agreed = C.c_int(1)
+        self.stream.wait_event(self._events[g])
+        saved = None
+        if self.max_ctas:
+            saved = self.comm.get_param("max_ctas")
+            self.comm.set_param("max_ctas", self.max_ctas)
+        try:
+            self._call(g, members, ts, n, ncalls, agreed)
+        finally:
+            if saved is not None:
+                self.comm.set_param("max_ctas", saved)
+        if ncalls.value != 1:
+            raise ShapeError("internal: an overlapped group split into several fused buffers")
+
+    def _call(self, g, members, ts, n, ncalls, agreed):
+        with torch.cuda.device(self.comm.device):
+            L.check(L.lib.cm_fused_allreduce_agreed(
+                self.comm._h, n, L.ptr_array([t.data_ptr() for t in ts]), L.i64_array([s.len for s in members]),
+                L.DTYPE[members[0].dtype], self.buckets[g].data_ptr(), L.ALGO[self.algo],
+                int(self.cfg.threshold_bytes), self.switch, 1, None, 0, C.byref(agreed), None,
+                self.stream.cuda_stream, self.stats[g], C.byref(ncalls)))
+
+    def finish(self) -> GradientSet:
+        """Join the communication stream into the caller's stream and return
+        the means of this step (views of persistent per-group buckets)."""
+        if self._next != len(self.order):
+            missing = sorted(s.name for s in self.specs if s.name not in self._tensors)
+            raise ShapeError(f"finish() before every gradient was ready: missing {missing[:8]}")
+        torch.cuda.current_stream(self.comm.device).wait_stream(self.stream)
+        if self.comm.blocking:
+            L.check(L.lib.cm_comm_sync(self.comm._h, self.stream.cuda_stream))
+        else:
+            L.check(L.lib.cm_comm_poll(self.comm._h))
+        views = {}
+        for g, m in enumerate(self.groups):
+            for s, v in zip((self.specs[i] for i in m), self.buckets[g].split([self.specs[i].len for i in m])):
+                views[s.name] = Tensor._wrap(s.name, s.dtype, v)
+        stats = [CollectiveStats(int(self.stats[g][0].rounds), int(self.stats[g][0].messages_per_rank),
+                                 int(self.stats[g][0].bytes_sent_per_rank)) for g in self.order]
+        gs = GradientSet.__new__(GradientSet)
+        object.__setattr__(gs, "tensors", tuple(views[s.name] for s in self.specs))
+        object.__setattr__(gs, "iteration", self.iteration)
+        self.iteration += 1
+        self._reset()
+        self.step_stats = stats
+        return gs

@@ -256,6 +256,27 @@ def main():
             expect(res2 is res and all(t.to_bytes() == want2[t.name].tobytes() for t in res2.tensors),
                    f"host aggregate out= refill {algo} {kind}")
 
+    # 4d. overlapped aggregation: groups launched from a communication stream
+    # while "backward" still produces gradients; every rank marks them ready
+    # in a different order; results equal aggregate() of the full set
+    for algo in ("auto", "ring_rsa"):
+        want, groups, _ = OA.aggregate(per_rank, "float32", algo, 8 << 20)
+        schema = [(nm, a.size, "float32") for nm, a in per_rank[rank]]
+        ov = P.OverlappedAggregator(schema, comm, algo=algo, cfg=P.FusionConfig(8 << 20))
+        expect(len(ov.groups) == len(groups), "overlap group count")
+        rng = np.random.default_rng([77, rank])
+        for step in range(2):
+            order = list(rng.permutation(len(per_rank[rank])))
+            spin = torch.randn(1024, 1024, device="cuda")
+            for i in order:
+                nm, a = per_rank[rank][i]
+                spin = spin @ spin.T * 1e-3                      # producer-stream work in between
+                ov.ready(nm, torch.from_numpy(a).cuda())
+            res = ov.finish()
+            expect(all(t.to_bytes() == want[t.name].tobytes() for t in res.tensors),
+                   f"overlapped aggregate {algo} step {step}")
+            expect(len(ov.step_stats) == len(groups), "overlap stats")
+
     # 4a. out= refill: persistent buckets are overwritten with the next step's means
     layers = I.MODELS["mobilenet_like"]
     g1 = I.synth_gradients(0, 0, layers, rank)

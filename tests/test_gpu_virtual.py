@@ -365,3 +365,24 @@ def test_single_rank_communicator_aggregate_host_and_device():
         assert all(t.to_bytes() == (a * 3).tobytes() for t, (_, a) in zip(res.tensors, sorted(g)))
         assert all(t.is_cuda == (kind == "device") for t in res.tensors)
     comm.close()
+
+
+def test_overlapped_aggregator_single_rank():
+    comm = P.Communicator(rank=0, size=1, device=0, staging_bytes=64 << 20, pool_bytes=2 << 20)
+    layers = [480_000] * 20 + [77, 1_000_003]
+    g = I.synth_gradients(0, 0, layers, 0)
+    ov = P.OverlappedAggregator([(nm, a.size, "float32") for nm, a in g], comm, cfg=P.FusionConfig(8 << 20))
+    assert len(ov.groups) > 2
+    for nm, a in reversed(g):
+        ov.ready(nm, torch.from_numpy(a).cuda())
+    res = ov.finish()
+    assert res.names == sorted(nm for nm, _ in g)
+    assert all(t.to_bytes() == dict(g)[t.name].tobytes() for t in res.tensors)
+    with pytest.raises(P.ShapeError):
+        ov.ready("nope", torch.zeros(3, device="cuda"))
+    ov.ready(g[0][0], torch.from_numpy(g[0][1]).cuda())
+    with pytest.raises(P.ShapeError):
+        ov.ready(g[0][0], torch.from_numpy(g[0][1]).cuda())
+    with pytest.raises(P.ShapeError):
+        ov.finish()
+    comm.close()
