@@ -256,6 +256,17 @@ def main():
             expect(res2 is res and all(t.to_bytes() == want2[t.name].tobytes() for t in res2.tensors),
                    f"host aggregate out= refill {algo} {kind}")
 
+    # 4e. a fused group larger than the staging area is a ConfigError on every rank
+    small = P.Communicator(staging_bytes=16 << 20, pool_bytes=2 << 20, timeout_s=20.0)
+    gbig = P.GradientSet(tuple(P.Tensor(nm, "float32", torch.from_numpy(a).cuda())
+                               for nm, a in I.synth_gradients(0, 0, [3_000_000] * 4, rank)))
+    try:
+        P.aggregate(gbig, group, small)
+        expect(False, "oversized fused group must raise ConfigError")
+    except P.ConfigError:
+        pass
+    small.close()
+
     # 4d. overlapped aggregation: groups launched from a communication stream
     # while "backward" still produces gradients; every rank marks them ready
     # in a different order; results equal aggregate() of the full set

@@ -24,12 +24,13 @@ ap.add_argument("--algo", default="ring_rsa")
 ap.add_argument("--iters", type=int, default=20)
 ap.add_argument("--zc", action="store_true")
 ap.add_argument("--param", action="append", default=[])
+ap.add_argument("--agg", action="store_true", help="trace the C5 aggregate step (registered gradients)")
 a = ap.parse_args()
 rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
 local = int(os.environ.get("LOCAL_RANK", rank))
 torch.cuda.set_device(local)
 dist.init_process_group("gloo")
-comm = P.Communicator(staging_bytes=max(64 << 20, a.bytes * 2), pool_bytes=max(64 << 20, a.bytes * 2),
+comm = P.Communicator(staging_bytes=max(256 << 20 if a.agg else 64 << 20, a.bytes * 2), pool_bytes=max(64 << 20, a.bytes * 2),
                       blocking=False)
 for kv in a.param:
     k, v = kv.split("=")
@@ -46,11 +47,25 @@ phases = ["copyin", "start_barrier", "reduce", "mid_barrier", "allgather"]
 acc = [0.0] * 5
 tot = 0.0
 skew = [0.0] * 6
+if a.agg:
+    import bench  # noqa: E402
+    gs = bench.make_grads("resnet50_like", rank, torch.device("cuda", local))
+    P.register_gradients(gs, comm)
+    agg_out = [None]
+    for _ in range(3):
+        agg_out[0] = P.aggregate(gs, P.GroupSpec(world), comm, out=agg_out[0])
+    comm.synchronize()
 for it in range(a.iters + 3):
     tr.zero_()
     dist.barrier()
-    L.check(L.lib.cm_allreduce(comm._h, x.data_ptr(), y.data_ptr(), n, 0, 0, L.ALGO[a.algo], 131072, 0,
-                               torch.cuda.current_stream().cuda_stream, C.byref(st)))
+    if a.agg:
+        # back-to-back pair: the second call is traced without the host barrier skew
+        agg_out[0] = P.aggregate(gs, P.GroupSpec(world), comm, out=agg_out[0])
+        tr.zero_()
+        agg_out[0] = P.aggregate(gs, P.GroupSpec(world), comm, out=agg_out[0])
+    else:
+        L.check(L.lib.cm_allreduce(comm._h, x.data_ptr(), y.data_ptr(), n, 0, 0, L.ALGO[a.algo], 131072, 0,
+                                   torch.cuda.current_stream().cuda_stream, C.byref(st)))
     comm.synchronize()
     t = tr.view(ctas, 8).cpu()
     used = t[:, 0] > 0
