@@ -169,6 +169,9 @@ int cm_comm_registry(cm_comm_t* comm, cm_registry_t** reg);
  *   "bulk_rs"             2..6 = the reduce phase streams its sources into this
  *                         many 32 KiB shared-memory stages with the bulk-copy
  *                         engine (default 6), 1 = SM loads
+ *   "dyn_ag"              2 = the allgather is a (slice, peer) task queue shared
+ *                         by the CTAs, 1 = each CTA pulls its own slice index
+ *                         after a per-index barrier (default; measured equal)
  * get also reads "staging_bytes", "pool_bytes" and "ll_payload_per_source" */
 int cm_comm_set_param(cm_comm_t* comm, const char* key, int64_t value);
 int cm_comm_get_param(cm_comm_t* comm, const char* key, int64_t* value);

@@ -73,6 +73,7 @@ struct cm_comm {
   int rhd_logp = 0;                           // 1: rhd_rsa runs the log2(p)-step halving/doubling kernel
   int bulk_copy = 0;                          // fusion pack through the TMA bulk-copy engine (opt-in)
   int bulk_rs = 6;                            // reduce phase: bulk-engine stages in smem (0: SM loads)
+  int dyn_ag = 0;                             // allgather as a shared (slice, peer) task queue (opt-in)
   int64_t oneshot_bytes_per_cta = 8 * 1024;
   int64_t twoshot_bytes_per_cta = 4 * 1024;
   int max_ctas = 148;
@@ -305,6 +306,7 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
   P.done_flag = L.done_flag;
   P.done_value = L.done_value;
   P.agree_gate = L.agree_gate;
+  P.dyn_ag = c->dyn_ag;
   P.trace = c->trace;
   P.trace_ctas = c->trace_ctas;
 
@@ -910,6 +912,7 @@ int cm_comm_set_param(cm_comm_t* c, const char* key, int64_t value) {
   else if (k == "rhd_logp") c->rhd_logp = value > 1 ? 1 : 0;
   else if (k == "bulk_copy") c->bulk_copy = value > 1 ? 1 : 0;
   else if (k == "bulk_rs") c->bulk_rs = value == 1 ? 0 : (int)std::min<int64_t>(value, RS_MAX_STAGES);
+  else if (k == "dyn_ag") c->dyn_ag = value > 1 ? 1 : 0;
   else if (k == "oneshot_bytes_per_cta") c->oneshot_bytes_per_cta = value;
   else if (k == "twoshot_bytes_per_cta") c->twoshot_bytes_per_cta = value;
   else if (k == "max_ctas") c->max_ctas = (int)std::min<int64_t>(value, MAXBLK);
@@ -929,6 +932,7 @@ int cm_comm_get_param(cm_comm_t* c, const char* key, int64_t* value) {
   else if (k == "rhd_logp") *value = c->rhd_logp ? 2 : 1;
   else if (k == "bulk_copy") *value = c->bulk_copy ? 2 : 1;
   else if (k == "bulk_rs") *value = c->bulk_rs ? c->bulk_rs : 1;
+  else if (k == "dyn_ag") *value = c->dyn_ag ? 2 : 1;
   else if (k == "oneshot_bytes_per_cta") *value = c->oneshot_bytes_per_cta;
   else if (k == "twoshot_bytes_per_cta") *value = c->twoshot_bytes_per_cta;
   else if (k == "max_ctas") *value = c->max_ctas;

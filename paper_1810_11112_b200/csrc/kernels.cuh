@@ -76,6 +76,7 @@ struct Ctrl {
   unsigned int pad;
   unsigned long long agree_tag;  // ticket of the last agreement check (cm_agree)
   long long agree_ok;            // its outcome: every rank held the same values
+  unsigned long long ag_next;    // next allgather task of the current call (dynamic allgather)
 };
 
 struct Rec {
@@ -141,6 +142,7 @@ struct CollParams {
   // >0: run only if the agreement check with this ticket (queued before on the
   // same stream) succeeded; otherwise every rank skips the call identically
   unsigned long long agree_gate;
+  int dyn_ag;                // allgather as a queue of (slice, peer) tasks shared by the CTAs
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -743,6 +745,49 @@ __device__ void stream_body(const CollParams& P, int rank, int b, int nb, unsign
   }
 }
 
+// Allgather as a task queue: after its reduce-scatter slice, every CTA takes
+// (slice s, peer q) tasks in order from a per-rank counter, waits for peer q's
+// CTA s to have published its reduced slice, and pulls it. CTAs that finish
+// their reduce early start pulling whatever is ready instead of waiting for
+// the peers' CTA of their own index (no per-index RS->AG barrier skew).
+template <class D, int MP>
+__device__ void dynamic_allgather(const CollParams& P, int rank, int nb, unsigned long long e, char* myheap,
+                                  Ctrl* ctrl, const char* const* s_src, char* const* s_red, char* out, bool multi,
+                                  CopyRange* s_cr, VecRange* s_vr, int* s_ncr, int* s_err) {
+  constexpr int SZ = sizeof(typename D::S);
+  __shared__ long long s_task;
+  const int tid = threadIdx.x, p = P.p, np1 = p - 1;
+  const long long ntask = (long long)nb * np1;
+  while (true) {
+    if (tid == 0) s_task = (long long)atomicAdd(&ctrl->ag_next, 1ull);
+    __syncthreads();
+    const long long t = s_task;
+    if (t >= ntask) break;
+    const int s = (int)(t / np1);
+    const int q = (rank + 1 + (int)(t % np1)) % p;
+    if (tid == 0) {
+      if (!wait_geq(mid_slot(myheap, s, q), e, P.timeout_cycles)) atomicExch(s_err, ERR_TRANSPORT);
+      int r = 0;
+      if (multi) {
+        for (int k = 0; k < P.nbuf; ++k) {
+          const long long so = P.bseg_off[k][q], sl = P.bseg_len[k][q];
+          const long long lo = slice_bound(so, sl, s, nb), hi = slice_bound(so, sl, s + 1, nb);
+          if (hi > lo) s_cr[r++] = CopyRange{s_src[q] + P.bboff[k] * SZ, P.bout[k], 0, 0, lo, hi};
+        }
+      } else {
+        const long long so = P.seg_off[q], sl = P.seg_len[q];
+        const long long lo = slice_bound(so, sl, s, nb), hi = slice_bound(so, sl, s + 1, nb);
+        if (hi > lo) s_cr[r++] = CopyRange{s_red[q], out, so, 0, lo, hi};
+      }
+      *s_ncr = r;
+    }
+    __syncthreads();
+    if (*s_err) break;
+    multi_copy<D, MP>(s_cr, *s_ncr, s_vr);
+    __syncthreads();
+  }
+}
+
 template <class D, int OP, int MP, bool TREE, bool STREAM>
 __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_constant__ CollParams P) {
   using S = typename D::S;
@@ -949,6 +994,10 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
     }
     CM_TRACE(P, lr, b, 3);
     if (tid < p) st_release_sys(mid_slot(P.heap[tid], b, rank), e);
+    if (P.dyn_ag) {
+      dynamic_allgather<D, MP>(P, rank, nb, e, myheap, ctrl, s_src, s_red, out, true, s_cr, s_vr, &s_ncr, &s_err);
+      goto finish;
+    }
     if (tid < p && !wait_geq(mid_slot(myheap, b, tid), e, P.timeout_cycles)) atomicExch(&s_err, ERR_TRANSPORT);
     __syncthreads();
     CM_TRACE(P, lr, b, 4);
@@ -1003,6 +1052,11 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
     if (!ag_only) {
       __syncthreads();
       if (tid < p) st_release_sys(mid_slot(P.heap[tid], b, rank), e);
+      if (P.dyn_ag) {
+        dynamic_allgather<D, MP>(P, rank, nb, e, myheap, ctrl, s_src, s_red, out, false, s_cr, s_vr, &s_ncr,
+                                 &s_err);
+        goto finish;
+      }
       if (tid < p && !wait_geq(mid_slot(myheap, b, tid), e, P.timeout_cycles))
         atomicExch(&s_err, ERR_TRANSPORT);
       __syncthreads();
@@ -1034,6 +1088,7 @@ finish:
     const unsigned old = atomicAdd(&ctrl->done, 1u);
     if (old == (unsigned)nb - 1) {
       ctrl->done = 0;
+      ctrl->ag_next = 0;
       ctrl->epoch = e;
       __threadfence();
     }

@@ -386,3 +386,24 @@ def test_overlapped_aggregator_single_rank():
     with pytest.raises(P.ShapeError):
         ov.finish()
     comm.close()
+
+
+@pytest.mark.parametrize("p", [2, 3, 4, 8])
+def test_dynamic_allgather_and_sm_reduce_variants(p):
+    """Opt-in kernel variants must stay bit-identical: the task-queue allgather
+    (dyn_ag) and the SM-load reduce (bulk_rs off)."""
+    g = P.VirtualGroup(p, 0, staging_bytes=64 << 20, timeout_s=5.0)
+    n = 3_000_017
+    rng = np.random.default_rng([p, 123])
+    xs = [(rng.standard_normal(n) * 10.0 ** rng.integers(-3, 4, size=n)).astype(np.float32) for _ in range(p)]
+    for algo in ("ring_rsa", "rhd_rsa"):
+        want = OC.allreduce(xs, "sum", algo, "float32").tobytes()
+        for knobs in ({"dyn_ag": 2}, {"bulk_rs": 1}, {"bulk_rs": 3, "dyn_ag": 2}):
+            for k, v in knobs.items():
+                g.set_param(k, v)
+            for _ in range(2):
+                res = P.allreduce_group(dev_tensors(xs, "float32"), P.ReduceOp.SUM, g, algo=algo)
+                assert all(t.to_bytes() == want for t, _ in res), knobs
+            g.set_param("dyn_ag", 1)
+            g.set_param("bulk_rs", 6)
+    g.close()
