@@ -213,8 +213,9 @@ int cm_comm_launches(cm_comm_t* comm, int64_t* launches);
 int cm_comm_set_trace(cm_comm_t* comm, void* device_buffer, int ctas);
 /* bracket every kernel this comm launches with CUDA events on its stream */
 int cm_comm_profile(cm_comm_t* comm, int enable);
-/* drain recorded launches of one kind (0 = collective kernel, 1 = pack/copy
- * kernel): count, summed device ms, summed algorithmic bytes (collective:
+/* drain recorded launches of one kind (0 = pull collective kernel, 1 =
+ * pack/copy kernel, 2 = LL / log-p collective kernels, e.g. the agreement
+ * check): count, summed device ms, summed algorithmic bytes (collectives:
  * busBW bytes 2(p-1)/p*S; pack: bytes read + written) */
 int cm_comm_profile_read(cm_comm_t* comm, int kind, int64_t* launches, double* total_ms,
                          int64_t* alg_bytes);

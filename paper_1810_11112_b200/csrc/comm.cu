@@ -368,7 +368,7 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
   if (L.nbuf > 1 || L.srcmode == SRC_GATHER) { ntot = 0; for (int k = 0; k < L.nbuf; ++k) ntot += L.bn[k]; }
   if (L.phases == (PH_RS | PH_AG) || L.oneshot) alg = 2 * (int64_t)(p - 1) * ntot * (int64_t)sz / p;
   else alg = (int64_t)(p - 1) * L.n * (int64_t)sz / p;
-  ProfScope prof_scope(c, stream, 0, alg);
+  ProfScope prof_scope(c, stream, (ll != 0 || logp) ? 2 : 0, alg);   // 0 pull collective, 2 LL / log-p
   if (c->virt) {
     int per_sm = 0;
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k, THREADS, dsm));
