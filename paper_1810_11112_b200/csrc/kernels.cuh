@@ -1,1849 +1,22 @@
-// sm_100a device code for the CUDA-aware allreduce.
+// sm_100a device code for the CUDA-aware allreduce: the single include point
+// for the per-dtype translation units (inst_*.cu) and the host code (comm.cu).
 //
-// One kernel family (`collective_kernel`) implements every collective of the
-// reference allreduce suite over a CUDA-IPC peer-mapped symmetric heap:
-//
-//   one-shot  : every rank reduces the whole vector from all p peers' staged
-//               copies (small messages; RHD tree order or flat order)
-//   two-shot  : reduce-scatter (rank r reduces its layout segment from all p
-//               peers, in the reference fold order) -> per-CTA flag barrier ->
-//               allgather (rank r pulls every other segment). This is the ring
-//               RSA (collectives.py:107-152) / RHD RSA (:155-236) data movement
-//               collapsed onto NVSwitch's full crossbar: the same 2(p-1)/p*S
-//               bytes per GPU per direction, two sync points instead of 2(p-1),
-//               and the per-element fold order of the reference replayed
-//               exactly so results are bit-identical.
-//   RS-only / AG-only : the public reduce_scatter / allgather.
-//
-// Synchronisation is flag based over NVLink: CTA b of rank r publishes a
-// record {epoch, header, src offset, reduced offset} into slot [parity][b][r]
-// of every peer's heap with st.release.sys, and waits on its own heap with
-// ld.acquire.sys. The epoch lives in device memory and is advanced by the last
-// CTA of each launch, so launches can be captured into CUDA graphs. Staging is
-// double-buffered by epoch parity: a rank rewrites staging[e&1] only in call
-// e+2, after every peer has entered call e+1 (and therefore left call e).
-// Waits are bounded (timeout -> CM_ERR_TRANSPORT in the host-mapped error word).
+//   dev_common.cuh        heap layout, CollParams, folds, reduce/copy loops
+//   kernel_collective.cuh one-/two-shot pull collectives (+ RS/AG, multi-buffer)
+//   kernel_ll.cuh         LL one-shot / two-shot (small and medium messages)
+//   kernel_rhd.cuh        literal log2(p)-step recursive halving/doubling
+//   kernel_copy.cuh       fusion pack (SM and TMA bulk copy), NVLink diagnostics
+//   kernels.cuh           local_reduce and the per-dtype kernel tables
 #pragma once
 
-#include <cuda_runtime.h>
-#include <stdint.h>
-
-#include "cm.h"
+#include "dev_common.cuh"
+#include "kernel_collective.cuh"
+#include "kernel_ll.cuh"
+#include "kernel_rhd.cuh"
+#include "kernel_copy.cuh"
 
 namespace cm {
 namespace dev {
-
-constexpr int MAXP = CM_MAX_RANKS;
-constexpr int MAXBLK = 1024;
-constexpr int THREADS = 512;
-constexpr int SLICE_ALIGN = 64;  // elements; slice boundaries are multiples of this
-constexpr int MAXBUF = 4;        // fused buffers per multi-buffer launch
-
-// ---- heap layout (identical on every rank) ---------------------------------
-constexpr size_t CTRL_OFF = 0;
-constexpr size_t REC_OFF = 4096;
-constexpr size_t REC_BYTES = 32;
-constexpr size_t REC_SIZE = 2ull * MAXBLK * MAXP * REC_BYTES;
-constexpr size_t MID_OFF = REC_OFF + REC_SIZE;
-constexpr size_t MID_SIZE = (size_t)MAXBLK * MAXP * 8;
-// LL (low-latency) slots: every 16-byte unit carries 8 payload bytes and two
-// copies of the epoch flag, so data and "ready" arrive in one store. Layout
-// [parity][phase][src < p][unit < ll_units] starting at LL_OFF; its size
-// depends on p and is chosen at communicator creation, so staging starts at a
-// runtime offset (CollParams::staging_off).
-constexpr size_t WMID_OFF = MID_OFF + MID_SIZE;         // per-warp progress of the pipelined two-shot
-constexpr size_t WMID_SIZE = (size_t)MAXBLK * MAXP * 8 * 8;
-constexpr size_t LLH_OFF = WMID_OFF + WMID_SIZE;        // per-CTA LL header units
-constexpr size_t LLH_SIZE = 2ull * MAXBLK * MAXP * 16;
-// registered-buffer table: REGTAB[id][q] = rank q's registered buffer start,
-// mapped in THIS process (cm_comm_register, the IPC side of the pointer cache)
-constexpr int MAXREG = 4096;
-constexpr size_t REG_OFF = LLH_OFF + LLH_SIZE;
-constexpr size_t REG_SIZE = (size_t)MAXREG * MAXP * 8;
-// pairwise phase flags of the log-p recursive halving/doubling kernel:
-// RFLAG[src][cta] = {(epoch << 8) | phase, call header}, pushed by src
-constexpr size_t RHDF_OFF = REG_OFF + REG_SIZE;
-constexpr size_t RHDF_SIZE = (size_t)MAXP * MAXBLK * 16;
-constexpr size_t HEAP_ALIGN = 2ull << 20;
-constexpr size_t LL_OFF = ((RHDF_OFF + RHDF_SIZE + HEAP_ALIGN - 1) / HEAP_ALIGN) * HEAP_ALIGN;
-// record source encoding for registered inputs: bit 62 | id << 40 | byte delta
-constexpr unsigned long long REG_FLAG = 1ull << 62;
-constexpr size_t CTRL_REGION = LL_OFF;                  // zeroed at creation
-
-struct Ctrl {
-  unsigned long long epoch;      // calls completed by this rank
-  unsigned int done;             // CTAs finished in the current call
-  unsigned int pad;
-  unsigned long long agree_tag;  // ticket of the last agreement check (cm_agree)
-  long long agree_ok;            // its outcome: every rank held the same values
-  unsigned long long ag_next;    // next allgather task of the current call (dynamic allgather)
-};
-
-struct Rec {
-  unsigned long long epoch;
-  unsigned long long hdr;
-  long long srcoff;  // element i of the sender's input at heap + srcoff + i*sz
-  long long redoff;  // element i of the sender's segment at heap + redoff + (i-seg_off)*sz
-};
-
-enum SrcMode { SRC_COPYIN = 0, SRC_PRESTAGED = 1, SRC_ZEROCOPY = 2, SRC_INLINE = 3, SRC_REGISTERED = 4,
-               SRC_GATHER = 5 };
-enum Order { ORD_SEQ = 0, ORD_RING = 1, ORD_TREE = 2 };
-enum Phase { PH_RS = 1, PH_AG = 2 };
-enum Err { ERR_SHAPE = 1, ERR_TRANSPORT = 4 };
-
-struct CollParams {
-  char* heap[MAXP];          // every rank's heap, mapped in this process
-  const char* in[MAXP];      // per local rank (real mode: [0])
-  char* out[MAXP];
-  long long seg_off[MAXP];   // layout segment per rank (elements)
-  long long seg_len[MAXP];
-  long long n;               // full vector length (elements)
-  long long zc_srcoff[MAXP]; // ZEROCOPY: byte offset of `in` within own heap (per local rank)
-  unsigned long long hdr;    // call signature checked against every peer
-  unsigned long long timeout_cycles;
-  long long staging_bytes;   // per parity half
-  unsigned int* herr;        // host-mapped error word
-  int p;
-  int rank;                  // real mode
-  int virt;                  // 1: blockIdx.y is the rank (single-GPU emulation)
-  int srcmode;
-  int order;                 // Order
-  int phases;                // Phase bits
-  int oneshot;               // every segment is [0, n)
-  int out_rel;               // RS writes out[i - seg_off] (reduce_scatter API)
-  int ag_in_rel;             // AG-only: `in` holds only my segment (in[i - seg_off])
-  int average;               // divide the reduced value by p (aggregate mean)
-  long long staging_off;     // heap offset of staging[0]
-  long long stream_chunk;    // elements per chunk of the pipelined two-shot
-  long long ll_units;        // LL units per (parity, phase, source)
-  unsigned long long* trace; // optional: per-CTA phase timestamps (globaltimer ns)
-  int trace_ctas;
-  // several fused buffers in ONE launch (aggregate): buffer k holds bn[k]
-  // elements at staging element offset bboff[k] and is written to bout[k];
-  // each keeps its own reduce-scatter layout (so ring chunking, and therefore
-  // the fold order, is exactly that of one allreduce per buffer)
-  int nbuf;
-  long long bn[MAXBUF];
-  long long bboff[MAXBUF];
-  char* bout[MAXBUF];
-  long long bseg_off[MAXBUF][MAXP];
-  long long bseg_len[MAXBUF][MAXP];
-  // SRC_GATHER (aggregate on registered gradients): the fused buffers are the
-  // concatenation of registered member tensors; gtab = {gstart[0..gmem],
-  // id[0..gmem)} in device memory; peers' members are read in place through
-  // REGTAB[id][q] (no pack, no staging copy)
-  const long long* gtab;
-  int gmem;
-  long long inl[8];          // SRC_INLINE: the input travels in the parameters (cm_agree)
-  unsigned long long* done_flag;  // optional: written with done_value when the call completes
-  unsigned long long done_value;
-  int bulk_rs;               // >0: reduce through the bulk-copy engine with this many smem stages
-  // >0: run only if the agreement check with this ticket (queued before on the
-  // same stream) succeeded; otherwise every rank skips the call identically
-  unsigned long long agree_gate;
-  int dyn_ag;                // allgather as a queue of (slice, peer) tasks shared by the CTAs
-};
-
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-// phase stamp k (0 start, 1 copied-in, 2 start barrier, 3 reduced, 4 mid barrier, 5 end)
-#define CM_TRACE(P, lr, b, k)                                                   \
-  do {                                                                          \
-    if ((P).trace && threadIdx.x == 0 && (b) < (P).trace_ctas)                  \
-      (P).trace[((size_t)(lr) * (P).trace_ctas + (b)) * 8 + (k)] = gtimer();    \
-  } while (0)
-
-// ---- element types ----------------------------------------------------------
-struct F32 { using S = float;    using A = float; };
-struct F64 { using S = double;   using A = double; };
-struct BF16 { using S = uint16_t; using A = float; };
-struct I32 { using S = int32_t;  using A = int32_t; };
-struct I64 { using S = int64_t;  using A = int64_t; };
-
-__device__ __forceinline__ float bf16_to_f32(uint16_t h) {
-  return __uint_as_float(((unsigned)h) << 16);
-}
-// round-to-nearest-even, NaN -> 0x7FC0 (matches oracle/collectives.f32_to_bf16)
-__device__ __forceinline__ uint16_t f32_to_bf16(float f) {
-  const unsigned u = __float_as_uint(f);
-  if ((u & 0x7fffffffu) > 0x7f800000u) return 0x7FC0;
-  return (uint16_t)((u + 0x7fffu + ((u >> 16) & 1u)) >> 16);
-}
-
-template <class D> __device__ __forceinline__ typename D::A to_acc(typename D::S s) { return s; }
-template <> __device__ __forceinline__ float to_acc<BF16>(uint16_t s) { return bf16_to_f32(s); }
-template <class D> __device__ __forceinline__ typename D::S from_acc(typename D::A a) { return a; }
-template <> __device__ __forceinline__ uint16_t from_acc<BF16>(float a) { return f32_to_bf16(a); }
-
-// _reduce_arrays (collectives.py:57-64): `a` is the accumulator (first operand).
-// MAX is numpy.maximum bit for bit: (a > b || isnan(a)) ? a : b.
-template <int OP, typename A> __device__ __forceinline__ A op2(A a, A b);
-template <> __device__ __forceinline__ float op2<CM_SUM, float>(float a, float b) { return __fadd_rn(a, b); }
-template <> __device__ __forceinline__ double op2<CM_SUM, double>(double a, double b) { return __dadd_rn(a, b); }
-template <> __device__ __forceinline__ int32_t op2<CM_SUM, int32_t>(int32_t a, int32_t b) {
-  return (int32_t)((uint32_t)a + (uint32_t)b);
-}
-template <> __device__ __forceinline__ int64_t op2<CM_SUM, int64_t>(int64_t a, int64_t b) {
-  return (int64_t)((uint64_t)a + (uint64_t)b);
-}
-template <> __device__ __forceinline__ float op2<CM_MAX, float>(float a, float b) { return (a > b || a != a) ? a : b; }
-template <> __device__ __forceinline__ double op2<CM_MAX, double>(double a, double b) { return (a > b || a != a) ? a : b; }
-template <> __device__ __forceinline__ int32_t op2<CM_MAX, int32_t>(int32_t a, int32_t b) { return a > b ? a : b; }
-template <> __device__ __forceinline__ int64_t op2<CM_MAX, int64_t>(int64_t a, int64_t b) { return a > b ? a : b; }
-
-// IEEE division by p (aggregation.py:167-172: float32(float64(s)/p) == s/(float)p)
-template <typename A> __device__ __forceinline__ A div_p(A a, int p);
-template <> __device__ __forceinline__ float div_p<float>(float a, int p) { return __fdiv_rn(a, (float)p); }
-template <> __device__ __forceinline__ double div_p<double>(double a, int p) { return __ddiv_rn(a, (double)p); }
-template <> __device__ __forceinline__ int32_t div_p<int32_t>(int32_t a, int) { return a; }
-template <> __device__ __forceinline__ int64_t div_p<int64_t>(int64_t a, int) { return a; }
-
-// ---- memory-model helpers -----------------------------------------------------
-__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ void st_relaxed_sys(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ void st_relaxed_sys_s64(long long* p, long long v) {
-  asm volatile("st.relaxed.sys.global.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ unsigned long long ld_relaxed_sys(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ long long ld_relaxed_sys_s64(const long long* p) {
-  long long v;
-  asm volatile("ld.relaxed.sys.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-
-__device__ __forceinline__ Rec* rec_slot(char* heap, int par, int blk, int src) {
-  return reinterpret_cast<Rec*>(heap + REC_OFF +
-                                ((size_t)(par * MAXBLK + blk) * MAXP + src) * REC_BYTES);
-}
-__device__ __forceinline__ unsigned long long* mid_slot(char* heap, int blk, int src) {
-  return reinterpret_cast<unsigned long long*>(heap + MID_OFF + ((size_t)blk * MAXP + src) * 8);
-}
-
-// bounded spin: returns false on timeout
-__device__ __forceinline__ bool wait_geq(const unsigned long long* f, unsigned long long e,
-                                         unsigned long long timeout) {
-  if (ld_acquire_sys(f) >= e) return true;
-  const long long t0 = clock64();
-  while (true) {
-    for (int i = 0; i < 64; ++i)
-      if (ld_acquire_sys(f) >= e) return true;
-    if ((unsigned long long)(clock64() - t0) > timeout) return false;
-  }
-}
-
-// Slice b of segment [off, off+len) split over nb CTAs; interior boundaries
-// are multiples of SLICE_ALIGN (absolute element index) so they are vector
-// aligned and independent of the vector width.
-__device__ __forceinline__ long long slice_bound(long long off, long long len, int k, int nb) {
-  if (k <= 0) return off;
-  if (k >= nb) return off + len;
-  long long x = off + (long long)(((__int128)len * k) / nb);
-  x = (x / SLICE_ALIGN) * SLICE_ALIGN;
-  if (x < off) x = off;
-  if (x > off + len) x = off + len;
-  return x;
-}
-
-// ---- vector load/store of W elements (16 B when W*sizeof(S)==16) ---------------
-template <class D, int W>
-__device__ __forceinline__ void load_vec(const char* base, long long i, typename D::A (&v)[W]) {
-  using S = typename D::S;
-  const S* p = reinterpret_cast<const S*>(base) + i;
-  if constexpr (W * sizeof(S) == 16) {
-    uint4 raw = *reinterpret_cast<const uint4*>(p);
-    const S* s = reinterpret_cast<const S*>(&raw);
-#pragma unroll
-    for (int w = 0; w < W; ++w) v[w] = to_acc<D>(s[w]);
-  } else {
-#pragma unroll
-    for (int w = 0; w < W; ++w) v[w] = to_acc<D>(p[w]);
-  }
-}
-
-template <class D, int W>
-__device__ __forceinline__ void store_vec(char* base, long long i, const typename D::A (&v)[W]) {
-  using S = typename D::S;
-  S* p = reinterpret_cast<S*>(base) + i;
-  if constexpr (W * sizeof(S) == 16) {
-    uint4 raw;
-    S* s = reinterpret_cast<S*>(&raw);
-#pragma unroll
-    for (int w = 0; w < W; ++w) s[w] = from_acc<D>(v[w]);
-    *reinterpret_cast<uint4*>(p) = raw;
-  } else {
-#pragma unroll
-    for (int w = 0; w < W; ++w) p[w] = from_acc<D>(v[w]);
-  }
-}
-
-// ---- fold of p loaded operands in the reference order -------------------------
-// u[k] was loaded from seq[k]. LEFT: ((u0 op u1) op u2) ... (ring & flat).
-// TREE (collectives.py:178-229): leaves L_v = u[v] op u[M+v] for v < excess,
-// else u[v]; then a balanced tree, lower subtree first.
-template <int OP, int MP, int W, int M, typename A>
-__device__ __forceinline__ void tree_fold(A (&u)[MP][W], int excess) {
-#pragma unroll
-  for (int v = 0; v < M; ++v) {
-    constexpr int dummy = 0;
-    (void)dummy;
-    const int hi = (M + v < MP) ? M + v : MP - 1;
-    if (v < excess) {
-#pragma unroll
-      for (int w = 0; w < W; ++w) u[v][w] = op2<OP>(u[v][w], u[hi][w]);
-    }
-  }
-#pragma unroll
-  for (int s = 1; s < M; s *= 2) {
-#pragma unroll
-    for (int v = 0; v + s < M; v += 2 * s) {
-#pragma unroll
-      for (int w = 0; w < W; ++w) u[v][w] = op2<OP>(u[v][w], u[v + s][w]);
-    }
-  }
-}
-
-template <int OP, int MP, int W, bool TREE, typename A>
-__device__ __forceinline__ void fold(A (&u)[MP][W], int p, int m, int excess) {
-  if constexpr (!TREE) {
-#pragma unroll
-    for (int k = 1; k < MP; ++k)
-      if (k < p) {
-#pragma unroll
-        for (int w = 0; w < W; ++w) u[0][w] = op2<OP>(u[0][w], u[k][w]);
-      }
-  } else {
-    switch (m) {
-      case 1: tree_fold<OP, MP, W, 1>(u, excess); break;
-      case 2: tree_fold<OP, MP, W, 2>(u, excess); break;
-      case 4: tree_fold<OP, MP, W, (4 <= MP ? 4 : 1)>(u, excess); break;
-      case 8: tree_fold<OP, MP, W, (8 <= MP ? 8 : 1)>(u, excess); break;
-      default: tree_fold<OP, MP, W, (16 <= MP ? 16 : 1)>(u, excess); break;
-    }
-  }
-}
-
-// reduce U groups of W elements starting at element indices i0 + g*stride
-template <class D, int OP, int MP, int W, bool TREE>
-__device__ __forceinline__ void reduce_one(const char* const* seq, int p, int m, int excess,
-                                           long long i, int average, char* out,
-                                           long long out_shift, char* red, long long red_shift) {
-  using A = typename D::A;
-  A u[MP][W];
-#pragma unroll
-  for (int k = 0; k < MP; ++k)
-    if (k < p) load_vec<D, W>(seq[k], i, u[k]);
-  fold<OP, MP, W, TREE>(u, p, m, excess);
-  if (average) {
-#pragma unroll
-    for (int w = 0; w < W; ++w) u[0][w] = div_p<A>(u[0][w], p);
-  }
-  store_vec<D, W>(out, i - out_shift, u[0]);
-  if (red) store_vec<D, W>(red, i - red_shift, u[0]);
-}
-
-// Process [lo, hi) of one segment: scalar head/tail, W-wide body with 2-way
-// unrolling for memory-level parallelism over NVLink.
-template <class D, int OP, int MP, bool TREE>
-__device__ void reduce_range(const char* const* seq, int p, int m, int excess, long long lo,
-                             long long hi, bool vec, int average, char* out, long long out_shift,
-                             char* red, long long red_shift, int tid, int nthr) {
-  using S = typename D::S;
-  constexpr int W = 16 / sizeof(S);
-  long long body_lo = lo, body_hi = lo;
-  if (vec) {
-    body_lo = ((lo + W - 1) / W) * W;
-    body_hi = (hi / W) * W;
-    if (body_hi < body_lo) body_hi = body_lo = hi;
-  }
-  // scalar head and tail
-  for (long long i = lo + tid; i < body_lo; i += nthr)
-    reduce_one<D, OP, MP, 1, TREE>(seq, p, m, excess, i, average, out, out_shift, red, red_shift);
-  for (long long i = body_hi + tid; i < hi; i += nthr)
-    reduce_one<D, OP, MP, 1, TREE>(seq, p, m, excess, i, average, out, out_shift, red, red_shift);
-  // vector body: vectors j in [body_lo/W, body_hi/W)
-  const long long v0 = body_lo / W, v1 = body_hi / W;
-  using A = typename D::A;
-  // vector groups in flight per thread: ~32 operand registers whatever MP is (the
-  // bulk-engine path carries the large-message traffic; this one stays spill-free)
-  constexpr int OPR = MP * W * (int)(sizeof(A) / 4);
-  constexpr int U = OPR >= 32 ? 1 : 32 / OPR;
-  // Groups are predicated rather than peeled: the last partial round still
-  // keeps every remaining load in flight at once (a peeled one-group tail
-  // would pay one NVLink round trip per group).
-  for (long long j = v0 + tid; j < v1; j += U * (long long)nthr) {
-    A u[U][MP][W];
-#pragma unroll
-    for (int g = 0; g < U; ++g)
-      if (j + g * (long long)nthr < v1) {
-#pragma unroll
-        for (int k = 0; k < MP; ++k)
-          if (k < p) load_vec<D, W>(seq[k], (j + g * (long long)nthr) * W, u[g][k]);
-      }
-#pragma unroll
-    for (int g = 0; g < U; ++g) {
-      if (j + g * (long long)nthr >= v1) break;
-      fold<OP, MP, W, TREE>(u[g], p, m, excess);
-      if (average) {
-#pragma unroll
-        for (int w = 0; w < W; ++w) u[g][0][w] = div_p<A>(u[g][0][w], p);
-      }
-      const long long i = (j + g * (long long)nthr) * W;
-      store_vec<D, W>(out, i - out_shift, u[g][0]);
-      if (red) store_vec<D, W>(red, i - red_shift, u[g][0]);
-    }
-  }
-}
-
-// Several element ranges copied CONCURRENTLY: range r moves elements
-// [lo, hi) with dst[i - dshift] = src[i - sshift]. Every thread issues the
-// loads of all ranges before any store, so the allgather pulls from all
-// peers at once (balanced NVLink traffic, one round trip per iteration).
-struct CopyRange {
-  const char* src;
-  char* dst;
-  long long sshift, dshift, lo, hi;
-};
-
-struct VecRange {
-  const uint4* src;
-  uint4* dst;
-  long long nv;
-};
-
-// R[0..nr) in shared memory; V is shared scratch of the same size.
-template <class D, int MP>
-__device__ void multi_copy(const CopyRange* R, int nr, VecRange* V) {
-  using S = typename D::S;
-  constexpr int W = 16 / sizeof(S);
-  const int tid = threadIdx.x, bd = blockDim.x;
-  const int warp = tid >> 5, lane = tid & 31, nwarps = bd >> 5;
-  // scalar heads/tails (and misaligned ranges): one warp per range
-  for (int r = warp; r < nr; r += nwarps) {
-    const CopyRange c = R[r];
-    const S* s = reinterpret_cast<const S*>(c.src) - c.sshift;
-    S* d = reinterpret_cast<S*>(c.dst) - c.dshift;
-    long long blo = c.hi, bhi = c.hi;
-    if (((((uintptr_t)s) | ((uintptr_t)d)) & 15u) == 0) {
-      blo = ((c.lo + W - 1) / W) * W;
-      bhi = (c.hi / W) * W;
-      if (bhi < blo) blo = bhi = c.hi;
-    }
-    for (long long i = c.lo + lane; i < blo; i += 32) d[i] = s[i];
-    for (long long i = bhi + lane; i < c.hi; i += 32) d[i] = s[i];
-    if (lane == 0) {
-      V[r].src = reinterpret_cast<const uint4*>(s + blo);
-      V[r].dst = reinterpret_cast<uint4*>(d + blo);
-      V[r].nv = (bhi - blo) / W;
-    }
-  }
-  __syncthreads();
-  long long nvmax = 0;
-  for (int r = 0; r < nr; ++r) nvmax = V[r].nv > nvmax ? V[r].nv : nvmax;
-  // NS 16-byte loads in flight per thread whatever the number of ranges:
-  // slot s copies range s % nr at vector offset (s / nr) * bd
-  constexpr int NS = MP > 8 ? MP : 8;
-  if (nr < 1) return;
-  // ranges are processed in blocks of at most NS (multi-buffer launches have
-  // up to MAXBUF * (p - 1) ranges)
-  for (int r0 = 0; r0 < nr; r0 += NS) {
-    const int nrb = nr - r0 < NS ? nr - r0 : NS;
-    const VecRange* VB = V + r0;
-    long long nvb = 0;
-    for (int r = 0; r < nrb; ++r) nvb = VB[r].nv > nvb ? VB[r].nv : nvb;
-    const int G = NS / nrb > 1 ? NS / nrb : 1;
-    const int act = nrb * G < NS ? nrb * G : NS;
-    int sr[NS], sg[NS];
-#pragma unroll
-    for (int k = 0; k < NS; ++k) {
-      sr[k] = k % nrb;
-      sg[k] = k / nrb;
-    }
-    for (long long j0 = tid; j0 < nvb; j0 += (long long)bd * G) {
-      uint4 v[NS];
-#pragma unroll
-      for (int k = 0; k < NS; ++k) {
-        const long long j = j0 + (long long)sg[k] * bd;
-        if (k < act && j < VB[sr[k]].nv) v[k] = VB[sr[k]].src[j];
-      }
-#pragma unroll
-      for (int k = 0; k < NS; ++k) {
-        const long long j = j0 + (long long)sg[k] * bd;
-        if (k < act && j < VB[sr[k]].nv) VB[sr[k]].dst[j] = v[k];
-      }
-    }
-  }
-  (void)nvmax;
-}
-
-__device__ __forceinline__ bool al16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
-
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return (unsigned)__cvta_generic_to_shared(p);
-}
-
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
-  unsigned ok = 0;
-  while (!ok)
-    asm volatile(
-        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-}
-
-// ---- reduce through the bulk-copy engine ----------------------------------------
-// The reduce-scatter's sources (p - 1 of them across NVLink) are streamed into
-// a ring of shared-memory stages by ONE producer thread with cp.async.bulk
-// (completion counted on a `full` mbarrier per stage), so the bytes in flight
-// no longer depend on registers: stages x 32 KiB per SM. Warps 0..14 fold
-// each stage (sources in the reference order) and write out / staging; each
-// warp then arrives on the stage's `empty` mbarrier so the producer can refill.
-constexpr int RS_MAX_STAGES = 6;
-constexpr int RS_STAGE_BYTES = 32768;
-constexpr int RS_CONSUMERS = THREADS - 32;
-__host__ __device__ constexpr size_t rs_smem_bytes(int stages) {
-  return (size_t)stages * RS_STAGE_BYTES + (2 * (size_t)stages + 2) * 8;
-}
-
-struct BulkRS {
-  unsigned char* smem;        // stages x RS_STAGE_BYTES
-  unsigned long long* full;   // [stages], 1 arrival + tx bytes
-  unsigned long long* empty;  // [stages], RS_CONSUMERS / 32 arrivals
-  unsigned long long* seqno;  // stage uses so far in this launch
-  int stages;
-};
-
-__device__ __forceinline__ BulkRS bulk_rs_setup(unsigned char* dyn, int stages, int tid) {
-  BulkRS B;
-  B.stages = stages;
-  B.smem = dyn;
-  B.full = reinterpret_cast<unsigned long long*>(dyn + (size_t)stages * RS_STAGE_BYTES);
-  B.empty = B.full + stages;
-  B.seqno = B.empty + stages;
-  if (tid == 0) {
-    for (int s = 0; s < stages; ++s) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&B.full[s])));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&B.empty[s])), "r"(RS_CONSUMERS / 32));
-    }
-    *B.seqno = 0;
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  return B;
-}
-
-// Same contract as reduce_range (sources 16-byte aligned at vector boundaries).
-template <class D, int OP, int MP, bool TREE>
-__device__ void reduce_range_bulk(const BulkRS& B, const char* const* seq, int p, int m, int excess,
-                                  long long lo, long long hi, int average, char* out, long long out_shift,
-                                  char* red, long long red_shift, int tid) {
-  using S = typename D::S;
-  using A = typename D::A;
-  constexpr int W = 16 / sizeof(S);
-  constexpr int SZ = sizeof(S);
-  long long body_lo = ((lo + W - 1) / W) * W, body_hi = (hi / W) * W;
-  if (body_hi < body_lo) body_lo = body_hi = hi;
-  for (long long i = lo + tid; i < body_lo; i += THREADS)
-    reduce_one<D, OP, MP, 1, TREE>(seq, p, m, excess, i, average, out, out_shift, red, red_shift);
-  for (long long i = body_hi + tid; i < hi; i += THREADS)
-    reduce_one<D, OP, MP, 1, TREE>(seq, p, m, excess, i, average, out, out_shift, red, red_shift);
-  const long long nbytes = (body_hi - body_lo) * SZ;
-  if (nbytes <= 0) return;
-  const int ch = (RS_STAGE_BYTES / p) & ~15;            // bytes per source per stage
-  const long long C = (nbytes + ch - 1) / ch;
-  const unsigned long long base = *B.seqno;
-  if (tid == RS_CONSUMERS) {                            // producer: warp 15, lane 0
-    asm volatile("fence.proxy.async;" ::: "memory");
-    for (long long c = 0; c < C; ++c) {
-      const unsigned long long g = base + (unsigned long long)c;
-      const int s = (int)(g % B.stages);
-      if (g >= (unsigned long long)B.stages) mbar_wait(&B.empty[s], (unsigned)(((g / B.stages) - 1) & 1));
-      const long long off = body_lo * SZ + c * ch;
-      const int len = (int)((nbytes - c * ch) < ch ? (nbytes - c * ch) : ch);
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&B.full[s])),
-                   "r"(len * p)
-                   : "memory");
-      for (int k = 0; k < p; ++k)
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                smem_u32(B.smem + (size_t)s * RS_STAGE_BYTES + (size_t)k * ch)),
-            "l"(seq[k] + off), "r"(len), "r"(smem_u32(&B.full[s]))
-            : "memory");
-    }
-  } else if (tid < RS_CONSUMERS) {
-    for (long long c = 0; c < C; ++c) {
-      const unsigned long long g = base + (unsigned long long)c;
-      const int s = (int)(g % B.stages);
-      mbar_wait(&B.full[s], (unsigned)((g / B.stages) & 1));
-      const int len = (int)((nbytes - c * ch) < ch ? (nbytes - c * ch) : ch);
-      const int nv = len / 16;
-      const char* st = reinterpret_cast<const char*>(B.smem + (size_t)s * RS_STAGE_BYTES);
-      const long long e0 = body_lo + c * (ch / SZ);
-      for (int v = tid; v < nv; v += RS_CONSUMERS) {
-        A u[MP][W];
-#pragma unroll
-        for (int k = 0; k < MP; ++k)
-          if (k < p) load_vec<D, W>(st + (size_t)k * ch, (long long)v * W, u[k]);
-        fold<OP, MP, W, TREE>(u, p, m, excess);
-        if (average) {
-#pragma unroll
-          for (int w = 0; w < W; ++w) u[0][w] = div_p<A>(u[0][w], p);
-        }
-        const long long i = e0 + (long long)v * W;
-        store_vec<D, W>(out, i - out_shift, u[0]);
-        if (red) store_vec<D, W>(red, i - red_shift, u[0]);
-      }
-      __syncwarp();
-      if ((tid & 31) == 0)
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&B.empty[s])) : "memory");
-    }
-  }
-  __syncthreads();
-  if (tid == 0) *B.seqno = base + (unsigned long long)C;
-  __syncthreads();
-}
-__device__ __forceinline__ bool al16s(const char* base, long long shift_elems, int sz) {
-  return (((uintptr_t)base - (uintptr_t)(shift_elems * sz)) & 15u) == 0;
-}
-
-// ---- the collective kernel -------------------------------------------------------
-constexpr int RS_WARPS = 8;                      // reducer warps of the pipelined two-shot
-__device__ __forceinline__ unsigned long long* wmid_slot(char* heap, int blk, int src, int warp) {
-  return reinterpret_cast<unsigned long long*>(heap + WMID_OFF +
-                                               (((size_t)blk * MAXP + src) * RS_WARPS + warp) * 8);
-}
-__device__ __forceinline__ void named_sync(int id, int nthreads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
-__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
-
-// chunk k of slice [lo, hi): the first chunk ends at the first 64-aligned
-// boundary + C, later chunks are C elements on 64-aligned boundaries
-__device__ __forceinline__ void chunk_of(long long lo, long long hi, long long C, long long k,
-                                         long long* a, long long* z) {
-  const long long base = ((lo + SLICE_ALIGN - 1) / SLICE_ALIGN) * SLICE_ALIGN;
-  long long x = k == 0 ? lo : base + k * C;
-  long long y = base + (k + 1) * C;
-  if (x > hi) x = hi;
-  if (y > hi) y = hi;
-  if (y < x) y = x;
-  *a = x;
-  *z = y;
-}
-__device__ __forceinline__ long long chunks_of(long long lo, long long hi, long long C) {
-  const long long base = ((lo + SLICE_ALIGN - 1) / SLICE_ALIGN) * SLICE_ALIGN;
-  return hi <= base ? 1 : (hi - base + C - 1) / C;
-}
-
-template <class D, int OP, int MP, bool TREE>
-__device__ void stream_body(const CollParams& P, int rank, int b, int nb, unsigned long long e,
-                            const char* const* s_src, char* const* s_red, const char* const* s_seq,
-                            int* s_err, char* out, char* myheap) {
-  using S = typename D::S;
-  constexpr int SZ = sizeof(S);
-  constexpr int W = 16 / SZ;
-  constexpr int NR = RS_WARPS * 32;                // threads per role
-  const int p = P.p, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const long long C = P.stream_chunk;
-  // common chunk count (identical on every rank and for every segment)
-  long long K = 1;
-  for (int q = 0; q < p; ++q) {
-    const long long lo = slice_bound(P.seg_off[q], P.seg_len[q], b, nb);
-    const long long hi = slice_bound(P.seg_off[q], P.seg_len[q], b + 1, nb);
-    const long long kq = chunks_of(lo, hi, C);
-    K = kq > K ? kq : K;
-  }
-  const unsigned long long tag0 = e << 20;
-  if (warp < RS_WARPS) {
-    // ---------------- reducer warps
-    int m = 1;
-    while ((m << 1) <= p) m <<= 1;
-    const int excess = p - m;
-    const long long so = P.seg_off[rank], sl = P.seg_len[rank];
-    const long long lo = slice_bound(so, sl, b, nb), hi = slice_bound(so, sl, b + 1, nb);
-    bool vec = true;
-    for (int q = 0; q < p; ++q) vec = vec && al16(s_src[q]);
-    char* red = s_red[rank];
-    vec = vec && al16(out) && al16s(red, so, SZ);
-    for (long long k = 0; k < K; ++k) {
-      long long a, z;
-      chunk_of(lo, hi, C, k, &a, &z);
-      reduce_range<D, OP, MP, TREE>(s_seq, p, m, excess, a, z, vec, P.average, out, 0, red, so, tid, NR);
-      __syncwarp();
-      if (lane == 0) {
-        fence_acq_rel_sys();
-        for (int q = 0; q < p; ++q)
-          if (q != rank) st_relaxed_sys(wmid_slot(P.heap[q], b, rank, warp), tag0 | (unsigned long long)(k + 1));
-      }
-    }
-  } else {
-    // ---------------- gather warps
-    const int rt = tid - NR;
-    __shared__ VecRange s_av[MAXP];
-    for (long long k = 0; k < K; ++k) {
-      const unsigned long long want = tag0 | (unsigned long long)(k + 1);
-      if (rt < p * RS_WARPS) {
-        const int q = rt / RS_WARPS, w = rt % RS_WARPS;
-        if (q != rank && !wait_geq(wmid_slot(myheap, b, q, w), want, P.timeout_cycles))
-          atomicExch(s_err, ERR_TRANSPORT);
-      }
-      named_sync(1, NR);
-      if (*s_err) break;
-      if (rt < p) {                                  // ranges + scalar head/tail of peer rt
-        const int q = rt;
-        VecRange v{nullptr, nullptr, 0};
-        if (q != rank) {
-          const long long qo = P.seg_off[q], ql = P.seg_len[q];
-          long long a, z;
-          chunk_of(slice_bound(qo, ql, b, nb), slice_bound(qo, ql, b + 1, nb), C, k, &a, &z);
-          const S* src = reinterpret_cast<const S*>(s_red[q]) - qo;
-          S* dst = reinterpret_cast<S*>(out);
-          long long blo = z, bhi = z;
-          if (((((uintptr_t)src) | ((uintptr_t)dst)) & 15u) == 0) {
-            blo = ((a + W - 1) / W) * W;
-            bhi = (z / W) * W;
-            if (bhi < blo) blo = bhi = z;
-          }
-          for (long long i = a; i < blo; ++i) dst[i] = src[i];
-          for (long long i = bhi; i < z; ++i) dst[i] = src[i];
-          v.src = reinterpret_cast<const uint4*>(src + blo);
-          v.dst = reinterpret_cast<uint4*>(dst + blo);
-          v.nv = (bhi - blo) / W;
-        }
-        s_av[q] = v;
-      }
-      named_sync(1, NR);
-      long long nvmax = 0;
-      for (int q = 0; q < p; ++q) nvmax = s_av[q].nv > nvmax ? s_av[q].nv : nvmax;
-      for (long long j = rt; j < nvmax; j += NR) {
-        uint4 v[MP];
-#pragma unroll
-        for (int q = 0; q < MP; ++q)
-          if (q < p && j < s_av[q].nv) v[q] = s_av[q].src[j];
-#pragma unroll
-        for (int q = 0; q < MP; ++q)
-          if (q < p && j < s_av[q].nv) s_av[q].dst[j] = v[q];
-      }
-      named_sync(1, NR);                             // s_av reuse
-    }
-  }
-}
-
-// Allgather as a task queue: after its reduce-scatter slice, every CTA takes
-// (slice s, peer q) tasks in order from a per-rank counter, waits for peer q's
-// CTA s to have published its reduced slice, and pulls it. CTAs that finish
-// their reduce early start pulling whatever is ready instead of waiting for
-// the peers' CTA of their own index (no per-index RS->AG barrier skew).
-template <class D, int MP>
-__device__ void dynamic_allgather(const CollParams& P, int rank, int nb, unsigned long long e, char* myheap,
-                                  Ctrl* ctrl, const char* const* s_src, char* const* s_red, char* out, bool multi,
-                                  CopyRange* s_cr, VecRange* s_vr, int* s_ncr, int* s_err) {
-  constexpr int SZ = sizeof(typename D::S);
-  __shared__ long long s_task;
-  const int tid = threadIdx.x, p = P.p, np1 = p - 1;
-  const long long ntask = (long long)nb * np1;
-  while (true) {
-    if (tid == 0) s_task = (long long)atomicAdd(&ctrl->ag_next, 1ull);
-    __syncthreads();
-    const long long t = s_task;
-    if (t >= ntask) break;
-    const int s = (int)(t / np1);
-    const int q = (rank + 1 + (int)(t % np1)) % p;
-    if (tid == 0) {
-      if (!wait_geq(mid_slot(myheap, s, q), e, P.timeout_cycles)) atomicExch(s_err, ERR_TRANSPORT);
-      int r = 0;
-      if (multi) {
-        for (int k = 0; k < P.nbuf; ++k) {
-          const long long so = P.bseg_off[k][q], sl = P.bseg_len[k][q];
-          const long long lo = slice_bound(so, sl, s, nb), hi = slice_bound(so, sl, s + 1, nb);
-          if (hi > lo) s_cr[r++] = CopyRange{s_src[q] + P.bboff[k] * SZ, P.bout[k], 0, 0, lo, hi};
-        }
-      } else {
-        const long long so = P.seg_off[q], sl = P.seg_len[q];
-        const long long lo = slice_bound(so, sl, s, nb), hi = slice_bound(so, sl, s + 1, nb);
-        if (hi > lo) s_cr[r++] = CopyRange{s_red[q], out, so, 0, lo, hi};
-      }
-      *s_ncr = r;
-    }
-    __syncthreads();
-    if (*s_err) break;
-    multi_copy<D, MP>(s_cr, *s_ncr, s_vr);
-    __syncthreads();
-  }
-}
-
-template <class D, int OP, int MP, bool TREE, bool STREAM>
-__global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_constant__ CollParams P) {
-  using S = typename D::S;
-  constexpr int SZ = sizeof(S);
-  const int lr = P.virt ? blockIdx.y : 0;       // index into in/out
-  const int rank = P.virt ? (int)blockIdx.y : P.rank;
-  const int b = blockIdx.x, nb = gridDim.x, p = P.p, tid = threadIdx.x;
-  char* myheap = P.heap[rank];
-  Ctrl* ctrl = reinterpret_cast<Ctrl*>(myheap + CTRL_OFF);
-
-  __shared__ unsigned long long s_epoch;
-  __shared__ const char* s_src[MAXP];   // element 0 of rank q's input
-  __shared__ char* s_red[MAXP];         // element seg_off[q] of q's segment
-  __shared__ const char* s_seq[MAXP];   // fold sequence
-  __shared__ int s_rord[MAXP];          // fold sequence as source ranks
-  __shared__ int s_err;
-  __shared__ int s_skip;                // agreement gate failed: the call is a no-op
-
-  extern __shared__ __align__(128) unsigned char coll_dyn[];
-  CM_TRACE(P, lr, b, 0);
-  BulkRS BR{};
-  if (!STREAM && P.bulk_rs) BR = bulk_rs_setup(coll_dyn, P.bulk_rs, tid);
-  if (tid == 0) {
-    s_epoch = ctrl->epoch + 1;
-    s_err = 0;
-    // the agreement kernel ran before this one on the stream; its outcome is
-    // identical on every rank, so every rank skips (or runs) consistently
-    s_skip = P.agree_gate && !(ctrl->agree_tag == P.agree_gate && ctrl->agree_ok) ? 1 : 0;
-  }
-  __syncthreads();
-  const unsigned long long e = s_epoch;
-  const int par = (int)(e & 1);
-  const long long stage_off = P.staging_off + (long long)par * P.staging_bytes;
-  const char* in = P.in[lr];
-  char* out = P.out[lr];
-  const bool ag_only = !(P.phases & PH_RS);
-  const bool two_shot = !P.oneshot;
-
-  // my own src/red offsets (published to peers)
-  long long my_srcoff, my_redoff;
-  const long long mso = P.seg_off[rank];
-  if (P.srcmode == SRC_ZEROCOPY || P.srcmode == SRC_REGISTERED) {
-    my_srcoff = P.zc_srcoff[lr];           // heap offset, or REG_FLAG | id | delta
-    if (!ag_only)            // reduced segment goes to staging, vector-aligned like the source
-      my_redoff = stage_off + (mso % SLICE_ALIGN) * SZ;
-    else if (P.ag_in_rel)    // allgather: `in` holds only my segment
-      my_redoff = my_srcoff;
-    else
-      my_redoff = my_srcoff + mso * SZ;
-  } else {
-    my_srcoff = stage_off;
-    my_redoff = stage_off + mso * SZ;
-  }
-
-  // 1. copy-in: this CTA's slice of every segment peers will read from me
-  __shared__ CopyRange s_cr[MAXBUF * MAXP + 1];
-  __shared__ VecRange s_vr[MAXBUF * MAXP + 1];
-  __shared__ int s_ncr;
-  if (P.srcmode == SRC_COPYIN && !s_skip) {
-    char* stage = myheap + stage_off;
-    if (ag_only) {
-      if (tid == 0) {
-        const long long lo = slice_bound(mso, P.seg_len[rank], b, nb);
-        const long long hi = slice_bound(mso, P.seg_len[rank], b + 1, nb);
-        const long long ish = P.ag_in_rel ? mso : 0;
-        s_cr[0] = CopyRange{in, stage, ish, 0, lo, hi};
-        s_cr[1] = CopyRange{in, out, ish, 0, lo, hi};
-        s_ncr = 2;
-      }
-    } else {
-      const int nseg = P.oneshot ? 1 : p;
-      if (tid < nseg) {
-        const long long so = P.oneshot ? 0 : P.seg_off[tid];
-        const long long sl = P.oneshot ? P.n : P.seg_len[tid];
-        s_cr[tid] = CopyRange{in, stage, 0, 0, slice_bound(so, sl, b, nb), slice_bound(so, sl, b + 1, nb)};
-      }
-      if (tid == 0) s_ncr = nseg;
-    }
-    __syncthreads();
-    multi_copy<D, MP>(s_cr, s_ncr, s_vr);
-  }
-  __syncthreads();
-  CM_TRACE(P, lr, b, 1);
-
-  // 2. publish my record to every peer, then collect theirs
-  if (tid < p && !s_skip) {
-    Rec* r = rec_slot(P.heap[tid], par, b, rank);
-    st_relaxed_sys(&r->hdr, P.hdr);
-    st_relaxed_sys_s64(&r->srcoff, my_srcoff);
-    st_relaxed_sys_s64(&r->redoff, my_redoff);
-    st_release_sys(&r->epoch, e);
-  }
-  if (tid < p && !s_skip) {
-    Rec* r = rec_slot(myheap, par, b, tid);
-    if (!wait_geq(&r->epoch, e, P.timeout_cycles)) {
-      atomicExch(&s_err, ERR_TRANSPORT);
-    } else {
-      if (ld_relaxed_sys(&r->hdr) != P.hdr) atomicExch(&s_err, ERR_SHAPE);
-      const long long so = ld_relaxed_sys_s64(&r->srcoff);
-      if ((unsigned long long)so & REG_FLAG) {   // peer's registered buffer, mapped here
-        const long long id = (so >> 40) & 0x3FFFFF, delta = so & ((1ll << 40) - 1);
-        const char* base = *reinterpret_cast<char* const*>(myheap + REG_OFF + ((size_t)id * MAXP + tid) * 8);
-        s_src[tid] = base + delta;
-      } else {
-        s_src[tid] = P.heap[tid] + so;
-      }
-      s_red[tid] = P.heap[tid] + ld_relaxed_sys_s64(&r->redoff);
-    }
-  }
-  __syncthreads();                       // s_src / s_red / s_err complete
-  // fold sequence of my segment's sources (reference order)
-  if (tid == 0 && (P.phases & PH_RS)) {
-    int m = 1;
-    while ((m << 1) <= p) m <<= 1;
-    const int excess = p - m;
-    if (P.order == ORD_RING) {            // chunk c folds x_{c-1}, x_{c-2}, ..., x_c
-      for (int k = 0; k < p; ++k) s_rord[k] = ((rank - 1 - k) % p + p) % p;
-    } else if (P.order == ORD_TREE) {     // leaves real(v), partners 2v+1 at M+v
-      for (int v = 0; v < m; ++v) s_rord[v] = v < excess ? 2 * v : v + excess;
-      for (int v = 0; v < excess; ++v) s_rord[m + v] = 2 * v + 1;
-    } else {
-      for (int k = 0; k < p; ++k) s_rord[k] = k;
-    }
-    for (int k = 0; k < p; ++k) s_seq[k] = s_src[s_rord[k]];
-  }
-  __syncthreads();
-  CM_TRACE(P, lr, b, 2);
-  if (s_err || s_skip) goto finish;
-
-  if constexpr (STREAM) {
-    // Pipelined two-shot: warps 0..7 reduce chunk after chunk of my segment
-    // slice and publish per-warp progress to every peer; warps 8..15 pull
-    // chunk k of every other segment as soon as all peers' reducer warps have
-    // published it. Reduce-scatter of chunk k+1 overlaps allgather of chunk k,
-    // so there is no CTA-wide mid barrier and no idle link between phases.
-    stream_body<D, OP, MP, TREE>(P, rank, b, nb, e, s_src, s_red, s_seq, &s_err, out, myheap);
-    goto finish;
-  }
-
-  if (P.nbuf > 1 || P.srcmode == SRC_GATHER) {
-    // ---- several fused buffers, one launch: RS of every buffer, ONE
-    // RS->AG barrier, AG of every buffer. Input prestaged in staging, or
-    // (SRC_GATHER) read in place from every rank's registered member tensors.
-    __shared__ const char* s_seqk[MAXP];
-    __shared__ long long s_piece[2];
-    int m = 1;
-    while ((m << 1) <= p) m <<= 1;
-    const int excess = p - m;
-    char* mystage = myheap + stage_off;
-    const bool gather = P.srcmode == SRC_GATHER;
-    for (int k = 0; k < P.nbuf; ++k) {
-      const long long so = P.bseg_off[k][rank], sl = P.bseg_len[k][rank];
-      char* bo = P.bout[k];
-      char* red = mystage + P.bboff[k] * SZ;           // element 0 of buffer k (AG source)
-      const long long lo = slice_bound(so, sl, b, nb), hi = slice_bound(so, sl, b + 1, nb);
-      if (!gather) {
-        if (tid < p) s_seqk[tid] = s_seq[tid] + P.bboff[k] * SZ;
-        __syncthreads();
-        bool vec = al16(bo) && al16(red);
-        for (int q = 0; q < p; ++q) vec = vec && al16(s_seqk[q]);
-        if (P.bulk_rs && vec)
-          reduce_range_bulk<D, OP, MP, TREE>(BR, s_seqk, p, m, excess, lo, hi, P.average, bo, 0, red, 0, tid);
-        else
-          reduce_range<D, OP, MP, TREE>(s_seqk, p, m, excess, lo, hi, vec, P.average, bo, 0, red, 0,
-                                        tid, blockDim.x);
-        __syncthreads();
-        continue;
-      }
-      // gather: walk the members overlapping [lo, hi) of buffer k
-      const long long* gstart = P.gtab;
-      const long long* gid = P.gtab + P.gmem + 1;
-      long long i = lo;
-      while (i < hi) {
-        if (tid == 0) {                              // member holding global index bboff + i
-          const long long g = P.bboff[k] + i;
-          int a = 0, z = P.gmem;                     // gstart[a] <= g < gstart[z]
-          while (z - a > 1) {
-            const int mid = (a + z) >> 1;
-            if (gstart[mid] <= g) a = mid; else z = mid;
-          }
-          s_piece[0] = a;
-          const long long mend = gstart[a + 1] - P.bboff[k];
-          s_piece[1] = mend < hi ? mend : hi;
-        }
-        __syncthreads();
-        const int mi = (int)s_piece[0];
-        const long long pe = s_piece[1];
-        if (tid < p) {
-          const char* base = *reinterpret_cast<char* const*>(
-              myheap + REG_OFF + ((size_t)gid[mi] * MAXP + s_rord[tid]) * 8);
-          s_seqk[tid] = base - (gstart[mi] - P.bboff[k]) * SZ;   // element i of buffer k
-        }
-        __syncthreads();
-        bool vec = al16(bo) && al16(red);
-        for (int q = 0; q < p; ++q) vec = vec && al16(s_seqk[q]);
-        if (P.bulk_rs && vec)
-          reduce_range_bulk<D, OP, MP, TREE>(BR, s_seqk, p, m, excess, i, pe, P.average, bo, 0, red, 0, tid);
-        else
-          reduce_range<D, OP, MP, TREE>(s_seqk, p, m, excess, i, pe, vec, P.average, bo, 0, red, 0,
-                                        tid, blockDim.x);
-        __syncthreads();
-        i = pe;
-      }
-    }
-    CM_TRACE(P, lr, b, 3);
-    if (tid < p) st_release_sys(mid_slot(P.heap[tid], b, rank), e);
-    if (P.dyn_ag) {
-      dynamic_allgather<D, MP>(P, rank, nb, e, myheap, ctrl, s_src, s_red, out, true, s_cr, s_vr, &s_ncr, &s_err);
-      goto finish;
-    }
-    if (tid < p && !wait_geq(mid_slot(myheap, b, tid), e, P.timeout_cycles)) atomicExch(&s_err, ERR_TRANSPORT);
-    __syncthreads();
-    CM_TRACE(P, lr, b, 4);
-    if (s_err) goto finish;
-    if (tid == 0) {
-      int r = 0;
-      for (int k = 0; k < P.nbuf; ++k)
-        for (int q = 0; q < p; ++q) {
-          if (q == rank) continue;
-          const long long so = P.bseg_off[k][q], sl = P.bseg_len[k][q];
-          const long long lo = slice_bound(so, sl, b, nb), hi = slice_bound(so, sl, b + 1, nb);
-          if (hi <= lo) continue;
-          s_cr[r++] = CopyRange{s_src[q] + P.bboff[k] * SZ, P.bout[k], 0, 0, lo, hi};
-        }
-      s_ncr = r;
-    }
-    __syncthreads();
-    multi_copy<D, MP>(s_cr, s_ncr, s_vr);
-    goto finish;
-  }
-
-  // 3. reduce my segment (RS) — or the whole vector (one-shot)
-  if (P.phases & PH_RS) {
-    const long long so = P.oneshot ? 0 : mso;
-    const long long sl = P.oneshot ? P.n : P.seg_len[rank];
-    int m = 1;
-    while ((m << 1) <= p) m <<= 1;
-    const int excess = p - m;
-    bool vec = true;
-    for (int q = 0; q < p; ++q) vec = vec && al16(s_src[q]);
-    const long long out_shift = P.out_rel ? so : 0;
-    vec = vec && al16s(out, out_shift, SZ);
-    char* red = nullptr;
-    long long red_shift = 0;
-    if (two_shot && (P.phases & PH_AG)) {
-      red = s_red[rank];
-      red_shift = so;
-      vec = vec && al16s(red, red_shift, SZ);
-    }
-    const long long lo = slice_bound(so, sl, b, nb), hi = slice_bound(so, sl, b + 1, nb);
-    if (P.bulk_rs && vec)
-      reduce_range_bulk<D, OP, MP, TREE>(BR, s_seq, p, m, excess, lo, hi, P.average, out, out_shift, red,
-                                         red_shift, tid);
-    else
-      reduce_range<D, OP, MP, TREE>(s_seq, p, m, excess, lo, hi, vec, P.average, out, out_shift,
-                                    red, red_shift, tid, blockDim.x);
-  }
-
-  // 4. RS -> AG barrier (per CTA index) and 5. allgather
-  CM_TRACE(P, lr, b, 3);
-  if (P.phases & PH_AG) {
-    if (!ag_only) {
-      __syncthreads();
-      if (tid < p) st_release_sys(mid_slot(P.heap[tid], b, rank), e);
-      if (P.dyn_ag) {
-        dynamic_allgather<D, MP>(P, rank, nb, e, myheap, ctrl, s_src, s_red, out, false, s_cr, s_vr, &s_ncr,
-                                 &s_err);
-        goto finish;
-      }
-      if (tid < p && !wait_geq(mid_slot(myheap, b, tid), e, P.timeout_cycles))
-        atomicExch(&s_err, ERR_TRANSPORT);
-      __syncthreads();
-      CM_TRACE(P, lr, b, 4);
-      if (s_err) goto finish;
-    }
-    // pull slice b of every other segment from all peers concurrently
-    if (tid == 0) {
-      int k = 0;
-      for (int q = 0; q < p; ++q) {
-        if (q == rank && !(ag_only && P.srcmode == SRC_ZEROCOPY)) continue;
-        const long long so = P.seg_off[q], sl = P.seg_len[q];
-        const long long lo = slice_bound(so, sl, b, nb), hi = slice_bound(so, sl, b + 1, nb);
-        if (hi <= lo) continue;
-        s_cr[k++] = CopyRange{s_red[q], out, so, 0, lo, hi};
-      }
-      s_ncr = k;
-    }
-    __syncthreads();
-    multi_copy<D, MP>(s_cr, s_ncr, s_vr);
-  }
-
-finish:
-  __syncthreads();
-  CM_TRACE(P, lr, b, 5);
-  if (tid == 0) {
-    if (s_err) *reinterpret_cast<volatile unsigned*>(P.herr) = (unsigned)s_err;
-    __threadfence();
-    const unsigned old = atomicAdd(&ctrl->done, 1u);
-    if (old == (unsigned)nb - 1) {
-      ctrl->done = 0;
-      ctrl->ag_next = 0;
-      ctrl->epoch = e;
-      __threadfence();
-    }
-  }
-}
-
-// ---- LL one-shot (small messages) ------------------------------------------------
-// Rank r writes every 8-byte unit of its input into slot [par][r][u] of EVERY
-// rank's heap as {w0, flag, w1, flag} with one 16-byte volatile store; readers
-// poll their own heap until both flags equal the call's epoch tag, then fold
-// the p sources in the reference order. No fence, no separate flag round trip:
-// latency = launch + one NVLink store + local polls. Header units carry the
-// call signature so mismatched peers raise ShapeError.
-__device__ __forceinline__ void st_ll(void* p, unsigned w0, unsigned w1, unsigned f) {
-  asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(w0), "r"(f), "r"(w1),
-               "r"(f)
-               : "memory");
-}
-__device__ __forceinline__ uint4 ld_ll(const void* p) {
-  uint4 v;
-  asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-               : "l"(p)
-               : "memory");
-  return v;
-}
-#define LLSLOT(heap, par, phase, src, u) \
-  ((heap) + LL_OFF + ((((size_t)(par) * 2 + (phase)) * P.p + (src)) * (size_t)P.ll_units + (size_t)(u)) * 16)
-__device__ __forceinline__ char* llh_slot(char* heap, int par, int blk, int src) {
-  return heap + LLH_OFF + (((size_t)par * MAXBLK + blk) * MAXP + src) * 16;
-}
-
-// poll one LL unit until both flags match; false on timeout
-__device__ __forceinline__ bool ll_wait(const char* slot, unsigned f, unsigned long long timeout,
-                                        uint4* out) {
-  uint4 v = ld_ll(slot);
-  if (v.y == f && v.w == f) { *out = v; return true; }
-  const long long t0 = clock64();
-  while (true) {
-    for (int i = 0; i < 32; ++i) {
-      v = ld_ll(slot);
-      if (v.y == f && v.w == f) { *out = v; return true; }
-    }
-    if ((unsigned long long)(clock64() - t0) > timeout) return false;
-  }
-}
-
-template <class D, int OP, int MP, bool TREE>
-__global__ void __launch_bounds__(THREADS) ll_kernel(const __grid_constant__ CollParams P) {
-  using S = typename D::S;
-  using A = typename D::A;
-  constexpr int E = 8 / sizeof(S);                    // elements per unit
-  const int lr = P.virt ? blockIdx.y : 0;
-  const int rank = P.virt ? (int)blockIdx.y : P.rank;
-  const int b = blockIdx.x, nb = gridDim.x, p = P.p, tid = threadIdx.x;
-  char* myheap = P.heap[rank];
-  Ctrl* ctrl = reinterpret_cast<Ctrl*>(myheap + CTRL_OFF);
-  __shared__ unsigned long long s_epoch;
-  __shared__ int s_err;
-  __shared__ int s_seq[MAXP];
-  __shared__ int s_disagree;
-  if (tid == 0) {
-    s_epoch = ctrl->epoch + 1;
-    s_err = 0;
-    s_disagree = 0;
-  }
-  int m = 1;
-  while ((m << 1) <= p) m <<= 1;
-  const int excess = p - m;
-  if (tid < p) {                                      // fold sequence (see collective_kernel)
-    int src;
-    if (P.order == ORD_TREE) src = tid < m ? (tid < excess ? 2 * tid : tid + excess) : 2 * (tid - m) + 1;
-    else src = tid;
-    s_seq[tid] = src;
-  }
-  __syncthreads();
-  const unsigned long long e = s_epoch;
-  const int par = (int)(e & 1);
-  const unsigned flag = (unsigned)(e & 0x7fffffffu) | 0x80000000u;
-  const long long nbytes = P.n * (long long)sizeof(S);
-  const long long nunits = (nbytes + 7) / 8;
-  const long long u0 = nunits * b / nb, u1 = nunits * (b + 1) / nb;
-  // prestaged input (fused pack) lives in staging[parity]
-  CM_TRACE(P, lr, b, 0);
-  const char* in = P.srcmode == SRC_PRESTAGED
-                       ? myheap + P.staging_off + (long long)par * P.staging_bytes
-                       : P.srcmode == SRC_INLINE ? reinterpret_cast<const char*>(P.inl) : P.in[lr];
-  char* out = P.out[lr];
-
-  // header units: this CTA's call signature to every rank
-  if (tid < p) {
-    st_ll(llh_slot(P.heap[tid], par, b, rank), (unsigned)P.hdr, (unsigned)(P.hdr >> 32), flag);
-  }
-  // write phase: my units into every rank's slot [par][rank][u]
-  for (long long u = u0 + tid; u < u1; u += blockDim.x) {
-    unsigned w0 = 0, w1 = 0;
-    const long long boff = u * 8;
-    if (boff + 8 <= nbytes && ((((uintptr_t)in) & 7u) == 0)) {
-      const uint2 v = *reinterpret_cast<const uint2*>(in + boff);
-      w0 = v.x;
-      w1 = v.y;
-    } else {
-      unsigned char bytes[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      for (int k = 0; k < 8 && boff + k < nbytes; ++k) bytes[k] = (unsigned char)in[boff + k];
-      memcpy(&w0, bytes, 4);
-      memcpy(&w1, bytes + 4, 4);
-    }
-#pragma unroll
-    for (int q = 0; q < MP; ++q)
-      if (q < p) st_ll(LLSLOT(P.heap[q], par, 0, rank, u), w0, w1, flag);
-  }
-  // header check before trusting the unit count
-  if (tid < p) {
-    uint4 h;
-    if (!ll_wait(llh_slot(myheap, par, b, tid), flag, P.timeout_cycles, &h)) {
-      atomicExch(&s_err, ERR_TRANSPORT);
-    } else if (((unsigned long long)h.z << 32 | h.x) != P.hdr) {
-      atomicExch(&s_err, ERR_SHAPE);
-    }
-  }
-  __syncthreads();
-  CM_TRACE(P, lr, b, 2);
-  if (s_err) goto ll_finish;
-  // read + fold phase
-  for (long long u = u0 + tid; u < u1; u += blockDim.x) {
-    A v[MP][E];
-    bool ok = true;
-#pragma unroll
-    for (int k = 0; k < MP; ++k) {
-      if (k < p) {
-        uint4 x;
-        if (!ll_wait(LLSLOT(myheap, par, 0, s_seq[k], u), flag, P.timeout_cycles, &x)) {
-          ok = false;
-          x = make_uint4(0, 0, 0, 0);
-        }
-        union { uint2 u; S s[E]; } w;
-        w.u = make_uint2(x.x, x.z);
-#pragma unroll
-        for (int t = 0; t < E; ++t) v[k][t] = to_acc<D>(w.s[t]);
-      }
-    }
-    if (!ok) {
-      atomicExch(&s_err, ERR_TRANSPORT);
-      break;
-    }
-    fold<OP, MP, E, TREE>(v, p, m, excess);
-    union { uint2 u; S s[E]; unsigned char c[8]; } res;
-#pragma unroll
-    for (int t = 0; t < E; ++t) res.s[t] = from_acc<D>(P.average ? div_p<A>(v[0][t], p) : v[0][t]);
-    // agreement check (cm_agree): the MAX of every rank's values equals mine
-    // for all values on every rank iff all ranks hold the same values
-    if (P.done_flag && u < 8 && (long long)(((unsigned long long)res.u.y << 32) | res.u.x) != P.inl[u])
-      s_disagree = 1;
-    const long long boff = u * 8;
-    if (boff + 8 <= nbytes && ((((uintptr_t)out) & 7u) == 0)) {
-      *reinterpret_cast<uint2*>(out + boff) = res.u;
-    } else {
-      for (int k = 0; k < 8 && boff + k < nbytes; ++k) out[boff + k] = (char)res.c[k];
-    }
-  }
-ll_finish:
-  __syncthreads();
-  CM_TRACE(P, lr, b, 5);
-  if (tid == 0) {
-    if (s_err) *reinterpret_cast<volatile unsigned*>(P.herr) = (unsigned)s_err;
-    __threadfence();
-    const unsigned old = atomicAdd(&ctrl->done, 1u);
-    if (old == (unsigned)nb - 1) {
-      ctrl->done = 0;
-      ctrl->epoch = e;
-      __threadfence();
-      if (P.done_flag) {                 // host spins on this (cm_agree)
-        ctrl->agree_ok = s_disagree ? 0 : 1;   // read by gated collectives queued behind
-        ctrl->agree_tag = P.done_value;
-        __threadfence_system();
-        *reinterpret_cast<volatile unsigned long long*>(P.done_flag) = P.done_value;
-      }
-    }
-  }
-}
-
-// ---- LL two-shot (medium messages) ----------------------------------------------
-// reduce-scatter by PUSH: every rank writes unit u of segment q of its input
-// into the owner q's LL slot [par][0][src][u]; the owner polls its own heap,
-// folds the p sources in the reference order (ring rotation or RHD tree) and
-// pushes the reduced unit to every peer's slot [par][1][owner][u]; readers
-// poll locally and write their output. No barriers and no fences: every
-// 16-byte unit carries its own epoch flags, so each hop costs one posted
-// NVLink store plus a local poll.
-template <class D>
-__device__ __forceinline__ uint2 pack_elems(const char* base, long long i, int cnt) {
-  using S = typename D::S;
-  constexpr int E = 8 / sizeof(S);
-  union { uint2 u; S s[E]; } w;
-  w.u = make_uint2(0, 0);
-  const S* src = reinterpret_cast<const S*>(base) + i;
-#pragma unroll
-  for (int t = 0; t < E; ++t)
-    if (t < cnt) w.s[t] = src[t];
-  return w.u;
-}
-
-template <class D>
-__device__ __forceinline__ void unpack_elems(char* base, long long i, int cnt, uint2 v) {
-  using S = typename D::S;
-  constexpr int E = 8 / sizeof(S);
-  union { uint2 u; S s[E]; } w;
-  w.u = v;
-  S* dst = reinterpret_cast<S*>(base) + i;
-#pragma unroll
-  for (int t = 0; t < E; ++t)
-    if (t < cnt) dst[t] = w.s[t];
-}
-
-template <class D, int OP, int MP, bool TREE>
-__global__ void __launch_bounds__(THREADS) ll2_kernel(const __grid_constant__ CollParams P) {
-  using S = typename D::S;
-  using A = typename D::A;
-  constexpr int E = 8 / sizeof(S);
-  const int lr = P.virt ? blockIdx.y : 0;
-  const int rank = P.virt ? (int)blockIdx.y : P.rank;
-  const int b = blockIdx.x, nb = gridDim.x, p = P.p, tid = threadIdx.x, bd = blockDim.x;
-  char* myheap = P.heap[rank];
-  Ctrl* ctrl = reinterpret_cast<Ctrl*>(myheap + CTRL_OFF);
-  __shared__ unsigned long long s_epoch;
-  __shared__ int s_err;
-  __shared__ int s_seq[MAXP];
-  CM_TRACE(P, lr, b, 0);
-  if (tid == 0) {
-    s_epoch = ctrl->epoch + 1;
-    s_err = 0;
-  }
-  int m = 1;
-  while ((m << 1) <= p) m <<= 1;
-  const int excess = p - m;
-  if (tid < p) {
-    int src;
-    if (P.order == ORD_TREE) src = tid < m ? (tid < excess ? 2 * tid : tid + excess) : 2 * (tid - m) + 1;
-    else if (P.order == ORD_RING) src = ((rank - 1 - tid) % p + p) % p;   // x_{r-1}, ..., x_r
-    else src = tid;
-    s_seq[tid] = src;
-  }
-  __syncthreads();
-  const unsigned long long e = s_epoch;
-  const int par = (int)(e & 1);
-  const unsigned flag = (unsigned)(e & 0x7fffffffu) | 0x80000000u;
-  const char* in = P.srcmode == SRC_PRESTAGED
-                       ? myheap + P.staging_off + (long long)par * P.staging_bytes
-                       : P.in[lr];
-  char* out = P.out[lr];
-
-  if (tid < p) st_ll(llh_slot(P.heap[tid], par, b, rank), (unsigned)P.hdr, (unsigned)(P.hdr >> 32), flag);
-  // 1. push slice b of every segment to its owner
-  for (int i = 0; i < p; ++i) {
-    const int q = (rank + 1 + i) % p;               // spread the first stores over peers
-    const long long so = P.seg_off[q], sl = P.seg_len[q];
-    const long long nu = (sl + E - 1) / E;
-    const long long u0 = nu * b / nb, u1 = nu * (b + 1) / nb;
-    char* dst = P.heap[q];
-    for (long long u = u0 + tid; u < u1; u += bd) {
-      const long long el = u * E;
-      const int cnt = (int)((sl - el) < E ? (sl - el) : E);
-      const uint2 w = pack_elems<D>(in, so + el, cnt);
-      st_ll(LLSLOT(dst, par, 0, rank, u), w.x, w.y, flag);
-    }
-  }
-  if (tid < p) {
-    uint4 h;
-    if (!ll_wait(llh_slot(myheap, par, b, tid), flag, P.timeout_cycles, &h)) atomicExch(&s_err, ERR_TRANSPORT);
-    else if (((unsigned long long)h.z << 32 | h.x) != P.hdr) atomicExch(&s_err, ERR_SHAPE);
-  }
-  __syncthreads();
-  CM_TRACE(P, lr, b, 2);
-  if (s_err) goto ll2_finish;
-  {
-    // 2. reduce my segment, write it and push it to every peer
-    const long long so = P.seg_off[rank], sl = P.seg_len[rank];
-    const long long nu = (sl + E - 1) / E;
-    const long long u0 = nu * b / nb, u1 = nu * (b + 1) / nb;
-    for (long long u = u0 + tid; u < u1; u += bd) {
-      A v[MP][E];
-      bool ok = true;
-#pragma unroll
-      for (int k = 0; k < MP; ++k) {
-        if (k < p) {
-          uint4 x;
-          if (!ll_wait(LLSLOT(myheap, par, 0, s_seq[k], u), flag, P.timeout_cycles, &x)) {
-            ok = false;
-            x = make_uint4(0, 0, 0, 0);
-          }
-          union { uint2 u; S s[E]; } w;
-          w.u = make_uint2(x.x, x.z);
-#pragma unroll
-          for (int t = 0; t < E; ++t) v[k][t] = to_acc<D>(w.s[t]);
-        }
-      }
-      if (!ok) {
-        atomicExch(&s_err, ERR_TRANSPORT);
-        break;
-      }
-      fold<OP, MP, E, TREE>(v, p, m, excess);
-      union { uint2 u; S s[E]; } r;
-#pragma unroll
-      for (int t = 0; t < E; ++t) r.s[t] = from_acc<D>(P.average ? div_p<A>(v[0][t], p) : v[0][t]);
-      const long long el = u * E;
-      const int cnt = (int)((sl - el) < E ? (sl - el) : E);
-      for (int i = 1; i < p; ++i) {
-        const int q = (rank + i) % p;
-        st_ll(LLSLOT(P.heap[q], par, 1, rank, u), r.u.x, r.u.y, flag);
-      }
-      unpack_elems<D>(out, so + el, cnt, r.u);
-    }
-    CM_TRACE(P, lr, b, 3);
-    // 3. collect every other segment
-    for (int i = 1; i < p; ++i) {
-      const int q = (rank + i) % p;
-      const long long qo = P.seg_off[q], ql = P.seg_len[q];
-      const long long qn = (ql + E - 1) / E;
-      const long long q0 = qn * b / nb, q1 = qn * (b + 1) / nb;
-      for (long long u = q0 + tid; u < q1; u += bd) {
-        uint4 x;
-        if (!ll_wait(LLSLOT(myheap, par, 1, q, u), flag, P.timeout_cycles, &x)) {
-          atomicExch(&s_err, ERR_TRANSPORT);
-          break;
-        }
-        const long long el = u * E;
-        const int cnt = (int)((ql - el) < E ? (ql - el) : E);
-        unpack_elems<D>(out, qo + el, cnt, make_uint2(x.x, x.z));
-      }
-    }
-  }
-ll2_finish:
-  __syncthreads();
-  CM_TRACE(P, lr, b, 5);
-  if (tid == 0) {
-    if (s_err) *reinterpret_cast<volatile unsigned*>(P.herr) = (unsigned)s_err;
-    __threadfence();
-    const unsigned old = atomicAdd(&ctrl->done, 1u);
-    if (old == (unsigned)nb - 1) {
-      ctrl->done = 0;
-      ctrl->epoch = e;
-      __threadfence();
-    }
-  }
-}
-
-// ---- recursive halving / doubling in log2(p) pairwise steps ---------------------
-// The reference's rhd_rsa schedule (collectives.py:155-236) executed literally
-// over NVLink: fold of the excess odd ranks into their even neighbours, log2(m)
-// halving steps (partner vrank ^ 2^k, lower vrank keeps [lo, mid)), log2(m)
-// doubling steps in reverse, unfold. Each step pulls the partner's half from
-// its staging buffer and is ordered by ONE pairwise flag per CTA: every CTA
-// owns the same slice of [0, n) in every phase, so CTA b only ever depends on
-// CTA b of its partner (no grid-wide barrier). Element results equal the
-// balanced vrank tree (Appendix A.3) bit for bit; the direct kernels compute
-// the same tree in one or two exchanges, which is why they are the default.
-struct RFlag {
-  unsigned long long v;
-  unsigned long long hdr;
-};
-
-__device__ __forceinline__ RFlag* rflag_slot(char* heap, int src, int blk) {
-  return reinterpret_cast<RFlag*>(heap + RHDF_OFF) + ((size_t)src * MAXBLK + blk);
-}
-
-// dst_raw[i] = a[i] (op) b[i] (b == nullptr: a[i]); dst_out[i] = the same value,
-// divided by p when averaging. Either destination may be null. i in [lo, hi).
-template <class D, int OP>
-__device__ void pair_pass(const char* a, const char* b, char* dst_raw, char* dst_out, long long lo,
-                          long long hi, int average, int p) {
-  using S = typename D::S;
-  using A = typename D::A;
-  constexpr int W = 16 / sizeof(S);
-  constexpr int U = 4;
-  if (lo >= hi) return;
-  const int tid = threadIdx.x, nthr = blockDim.x;
-  const bool vec = al16(a) && (!b || al16(b)) && (!dst_raw || al16(dst_raw)) && (!dst_out || al16(dst_out));
-  long long blo = hi, bhi = hi;
-  if (vec) {
-    blo = ((lo + W - 1) / W) * W;
-    bhi = (hi / W) * W;
-    if (bhi < blo) blo = bhi = hi;
-  }
-  auto one = [&](long long i) {
-    A u[1], t[1];
-    load_vec<D, 1>(a, i, u);
-    if (b) {
-      load_vec<D, 1>(b, i, t);
-      u[0] = op2<OP>(u[0], t[0]);
-    }
-    if (dst_raw) store_vec<D, 1>(dst_raw, i, u);
-    if (dst_out) {
-      if (average) u[0] = div_p<A>(u[0], p);
-      store_vec<D, 1>(dst_out, i, u);
-    }
-  };
-  for (long long i = lo + tid; i < blo; i += nthr) one(i);
-  for (long long i = bhi + tid; i < hi; i += nthr) one(i);
-  const long long v0 = blo / W, v1 = bhi / W;
-  for (long long j = v0 + tid; j < v1; j += U * (long long)nthr) {
-    A u[U][W], t[U][W];
-#pragma unroll
-    for (int g = 0; g < U; ++g) {
-      const long long jj = j + g * (long long)nthr;
-      if (jj < v1) {
-        load_vec<D, W>(a, jj * W, u[g]);
-        if (b) load_vec<D, W>(b, jj * W, t[g]);
-      }
-    }
-#pragma unroll
-    for (int g = 0; g < U; ++g) {
-      const long long jj = j + g * (long long)nthr;
-      if (jj >= v1) break;
-      if (b) {
-#pragma unroll
-        for (int w = 0; w < W; ++w) u[g][w] = op2<OP>(u[g][w], t[g][w]);
-      }
-      if (dst_raw) store_vec<D, W>(dst_raw, jj * W, u[g]);
-      if (dst_out) {
-        if (average) {
-#pragma unroll
-          for (int w = 0; w < W; ++w) u[g][w] = div_p<A>(u[g][w], p);
-        }
-        store_vec<D, W>(dst_out, jj * W, u[g]);
-      }
-    }
-  }
-}
-
-template <class D, int OP>
-__global__ void __launch_bounds__(THREADS) rhd_kernel(const __grid_constant__ CollParams P) {
-  const int lr = P.virt ? blockIdx.y : 0;
-  const int rank = P.virt ? (int)blockIdx.y : P.rank;
-  const int b = blockIdx.x, nb = gridDim.x, p = P.p, tid = threadIdx.x;
-  char* myheap = P.heap[rank];
-  Ctrl* ctrl = reinterpret_cast<Ctrl*>(myheap + CTRL_OFF);
-  __shared__ unsigned long long s_epoch;
-  __shared__ int s_err;
-  CM_TRACE(P, lr, b, 0);
-  if (tid == 0) {
-    s_epoch = ctrl->epoch + 1;
-    s_err = 0;
-  }
-  __syncthreads();
-  const unsigned long long e = s_epoch;
-  const long long stage_off = P.staging_off + (long long)(e & 1) * P.staging_bytes;
-  char* buf = myheap + stage_off;
-  char* out = P.out[lr];
-  const long long n = P.n;
-  const long long lo_b = slice_bound(0, n, b, nb), hi_b = slice_bound(0, n, b + 1, nb);
-  int m = 1;
-  while ((m << 1) <= p) m <<= 1;
-  const int excess = p - m;
-  int steps = 0;
-  while ((1 << steps) < m) ++steps;
-  const bool folded_odd = rank < 2 * excess && (rank & 1);
-  const int v = rank < 2 * excess ? rank / 2 : rank - excess;
-  const unsigned long long base = e << 8;
-  const int ph_fold = excess > 0 ? 1 : 0;
-  long long los[MAXP], his[MAXP];        // range after halving step k-1 (level k)
-
-  auto real = [&](int w) { return w < excess ? 2 * w : w + excess; };
-  auto peer_buf = [&](int q) -> const char* { return P.heap[q] + stage_off; };
-  auto signal = [&](int ph) {
-    __syncthreads();                     // this CTA's writes of the phase precede the flag
-    if (tid < p) {
-      RFlag* f = rflag_slot(P.heap[tid], rank, b);
-      st_relaxed_sys(&f->hdr, P.hdr);
-      st_release_sys(&f->v, base | (unsigned long long)ph);
-    }
-  };
-  auto wait = [&](int src, int ph) -> bool {
-    if (tid == 0) {
-      RFlag* f = rflag_slot(myheap, src, b);
-      const unsigned long long want = base | (unsigned long long)ph;
-      if (!wait_geq(&f->v, want, P.timeout_cycles)) {
-        s_err = ERR_TRANSPORT;
-      } else if ((ld_acquire_sys(&f->v) >> 8) == e && ld_relaxed_sys(&f->hdr) != P.hdr) {
-        s_err = ERR_SHAPE;               // (a flag of a later call means src passed this one)
-      }
-    }
-    __syncthreads();
-    return s_err == 0;
-  };
-
-  // phase 0: my slice of the input into my staging buffer
-  pair_pass<D, OP>(P.in[lr], nullptr, buf, nullptr, lo_b, hi_b, 0, p);
-  signal(0);
-  CM_TRACE(P, lr, b, 1);
-  // phase 1 (non-power-of-two p): L_v = x_{2v} + x_{2v+1} on the even rank
-  if (excess > 0) {
-    if (rank < 2 * excess && !(rank & 1)) {
-      if (!wait(rank + 1, 0)) goto finish;
-      pair_pass<D, OP>(buf, peer_buf(rank + 1), buf, nullptr, lo_b, hi_b, 0, p);
-    }
-    signal(1);
-  }
-  CM_TRACE(P, lr, b, 2);
-  if (!folded_odd) {
-    long long lo = 0, hi = n;
-    los[0] = 0;
-    his[0] = n;
-    for (int k = 0; k < steps; ++k) {            // halving
-      const int q = real(v ^ (1 << k));
-      const long long mid = lo + (hi - lo) / 2;
-      const int bit = (v >> k) & 1;               // 0: lower vrank, keeps [lo, mid)
-      const long long klo = bit ? mid : lo, khi = bit ? hi : mid;
-      if (!wait(q, ph_fold + k)) goto finish;
-      const char* pb = peer_buf(q);
-      const bool last = k == steps - 1;
-      pair_pass<D, OP>(bit ? pb : buf, bit ? buf : pb, buf, last ? out : nullptr, klo > lo_b ? klo : lo_b,
-                       khi < hi_b ? khi : hi_b, P.average, p);
-      lo = klo;
-      hi = khi;
-      los[k + 1] = lo;
-      his[k + 1] = hi;
-      signal(ph_fold + 1 + k);
-    }
-    CM_TRACE(P, lr, b, 3);
-    for (int t = 0; t < steps; ++t) {            // doubling, reverse order
-      const int j = steps - 1 - t;
-      const int q = real(v ^ (1 << j));
-      if (!wait(q, ph_fold + steps + t)) goto finish;
-      const long long ulo = los[j], uhi = his[j], rlo = los[j + 1], rhi = his[j + 1];
-      const long long slo = rlo == ulo ? rhi : ulo, shi = rlo == ulo ? uhi : rlo;   // partner's part
-      pair_pass<D, OP>(peer_buf(q), nullptr, buf, out, slo > lo_b ? slo : lo_b, shi < hi_b ? shi : hi_b,
-                       P.average, p);
-      signal(ph_fold + steps + 1 + t);
-    }
-  } else {                                       // unfold: the result from rank - 1
-    if (!wait(rank - 1, ph_fold + 2 * steps)) goto finish;
-    pair_pass<D, OP>(peer_buf(rank - 1), nullptr, nullptr, out, lo_b, hi_b, P.average, p);
-  }
-  CM_TRACE(P, lr, b, 4);
-
-finish:
-  __syncthreads();
-  CM_TRACE(P, lr, b, 5);
-  if (tid == 0) {
-    if (s_err) *reinterpret_cast<volatile unsigned*>(P.herr) = (unsigned)s_err;
-    __threadfence();
-    const unsigned old = atomicAdd(&ctrl->done, 1u);
-    if (old == (unsigned)nb - 1) {
-      ctrl->done = 0;
-      ctrl->epoch = e;
-      __threadfence();
-    }
-  }
-}
-
-// ---- diagnostics: raw NVLink read / write bandwidth between all ranks --------
-// mode 0: pull — every rank reads `bytes` from each peer's staging into its own
-// mode 1: push — every rank writes `bytes` into each peer's staging
-// (all-to-all pattern of the two-shot phases; no synchronisation, data unused)
-static __global__ void __launch_bounds__(THREADS) p2p_bw_kernel(const __grid_constant__ CollParams P, int mode,
-                                                         long long bytes) {
-  const int rank = P.rank, p = P.p, tid = threadIdx.x;
-  const long long nv = bytes / 16;
-  const long long per = (nv + gridDim.x - 1) / gridDim.x;
-  const long long v0 = per * blockIdx.x, v1 = min(nv, v0 + per);
-  char* mine = P.heap[rank] + P.staging_off;
-  if (mode >= 2) {  // all peers concurrently from every thread
-    const bool pull = mode == 2;
-    for (long long j = v0 + tid; j < v1; j += THREADS) {
-      uint4 v[MAXP];
-#pragma unroll
-      for (int i = 1; i < 8; ++i) {
-        if (i < p) {
-          const int q = (rank + i) % p;
-          const uint4* src = reinterpret_cast<const uint4*>(
-              pull ? P.heap[q] + P.staging_off + (long long)rank * bytes : mine + (long long)q * bytes);
-          v[i] = src[j];
-        }
-      }
-#pragma unroll
-      for (int i = 1; i < 8; ++i) {
-        if (i < p) {
-          const int q = (rank + i) % p;
-          uint4* dst = reinterpret_cast<uint4*>(pull ? mine + (long long)q * bytes
-                                                     : P.heap[q] + P.staging_off + (long long)rank * bytes);
-          dst[j] = v[i];
-        }
-      }
-    }
-    return;
-  }
-  for (int i = 1; i < p; ++i) {
-    const int q = (rank + i) % p;
-    char* peer = P.heap[q] + P.staging_off;
-    const uint4* src = reinterpret_cast<const uint4*>(mode == 0 ? peer + (long long)rank * bytes
-                                                                : mine + (long long)q * bytes);
-    uint4* dst = reinterpret_cast<uint4*>(mode == 0 ? mine + (long long)q * bytes
-                                                    : peer + (long long)rank * bytes);
-    long long j = v0 + tid;
-    for (; j + 3 * THREADS < v1; j += 4 * THREADS) {
-      uint4 a = src[j], b = src[j + THREADS], c = src[j + 2 * THREADS], d = src[j + 3 * THREADS];
-      dst[j] = a; dst[j + THREADS] = b; dst[j + 2 * THREADS] = c; dst[j + 3 * THREADS] = d;
-    }
-    for (; j < v1; j += THREADS) dst[j] = src[j];
-  }
-}
-
-// ---- batched copy (fusion pack / unfuse / cm_batched_copy) ---------------------
-constexpr int MAXCOPY = 128;
-struct CopyParams {
-  const char* src[MAXCOPY];
-  char* dst[MAXCOPY];          // absolute, or byte offset into staging[next parity] if staged
-  long long start[MAXCOPY + 1];  // prefix sums of bytes
-  int n;
-  int staged;                  // dst is relative to own staging[(epoch+1)&1]
-  char* heap;
-  long long staging_bytes;
-  long long staging_off;
-};
-
-static __global__ void __launch_bounds__(THREADS) batched_copy_kernel(const __grid_constant__ CopyParams P) {
-  const long long total = P.start[P.n];
-  const int b = blockIdx.x, nb = gridDim.x, tid = threadIdx.x;
-  long long lo = (long long)(((__int128)total * b) / nb) & ~15ll;
-  long long hi = b == nb - 1 ? total : ((long long)(((__int128)total * (b + 1)) / nb) & ~15ll);
-  if (b == 0) lo = 0;
-  char* base = nullptr;
-  if (P.staged) {
-    const Ctrl* ctrl = reinterpret_cast<const Ctrl*>(P.heap + CTRL_OFF);
-    const unsigned long long e = ctrl->epoch + 1;
-    base = P.heap + P.staging_off + (long long)(e & 1) * P.staging_bytes;
-  }
-  // find the first member overlapping [lo, hi)
-  int k = 0;
-  while (k < P.n && P.start[k + 1] <= lo) ++k;
-  for (; k < P.n && P.start[k] < hi; ++k) {
-    const long long a = lo > P.start[k] ? lo : P.start[k];
-    const long long z = hi < P.start[k + 1] ? hi : P.start[k + 1];
-    const char* s = P.src[k] + (a - P.start[k]);
-    char* d = (P.staged ? base + (long long)(uintptr_t)P.dst[k] : P.dst[k]) + (a - P.start[k]);
-    const long long nbytes = z - a;
-    if ((((uintptr_t)s | (uintptr_t)d) & 15u) == 0) {
-      const long long nv = nbytes >> 4;
-      const uint4* s4 = reinterpret_cast<const uint4*>(s);
-      uint4* d4 = reinterpret_cast<uint4*>(d);
-      long long j = tid;
-      for (; j + 3 * THREADS < nv; j += 4 * THREADS) {
-        uint4 r0 = s4[j], r1 = s4[j + THREADS], r2 = s4[j + 2 * THREADS], r3 = s4[j + 3 * THREADS];
-        d4[j] = r0; d4[j + THREADS] = r1; d4[j + 2 * THREADS] = r2; d4[j + 3 * THREADS] = r3;
-      }
-      for (; j < nv; j += THREADS) d4[j] = s4[j];
-      for (long long t = (nv << 4) + tid; t < nbytes; t += THREADS) d[t] = s[t];
-    } else if ((((uintptr_t)s | (uintptr_t)d) & 3u) == 0) {
-      const long long nw = nbytes >> 2;
-      const uint32_t* s1 = reinterpret_cast<const uint32_t*>(s);
-      uint32_t* d1 = reinterpret_cast<uint32_t*>(d);
-      for (long long j = tid; j < nw; j += THREADS) d1[j] = s1[j];
-      for (long long t = (nw << 2) + tid; t < nbytes; t += THREADS) d[t] = s[t];
-    } else {
-      for (long long t = tid; t < nbytes; t += THREADS) d[t] = s[t];
-    }
-  }
-}
-
-// ---- TMA bulk copy (same CopyParams; every member 16-byte aligned) ----------------
-// One elected thread per CTA streams its contiguous byte range through a ring
-// of BULK_STAGES shared-memory stages with the bulk-copy engine:
-// cp.async.bulk global->shared (completion counted on an mbarrier), then
-// cp.async.bulk shared->global (bulk group). Loads run BULK_STAGES-1 chunks
-// ahead of the stores; no SM load/store instructions touch the payload.
-constexpr int BULK_STAGES = 6;
-constexpr int BULK_CHUNK = 16384;
-constexpr int BULK_THREADS = 32;
-constexpr size_t BULK_SMEM = (size_t)BULK_STAGES * BULK_CHUNK + BULK_STAGES * 8;
-
-static __global__ void __launch_bounds__(BULK_THREADS) bulk_copy_kernel(const __grid_constant__ CopyParams P) {
-  extern __shared__ __align__(128) unsigned char bulk_smem[];
-  if (threadIdx.x != 0) return;
-  unsigned long long* bar = reinterpret_cast<unsigned long long*>(bulk_smem + (size_t)BULK_STAGES * BULK_CHUNK);
-  const long long total = P.start[P.n];
-  const int b = blockIdx.x, nb = gridDim.x;
-  long long lo = (long long)(((__int128)total * b) / nb) & ~15ll;
-  long long hi = b == nb - 1 ? total : ((long long)(((__int128)total * (b + 1)) / nb) & ~15ll);
-  if (b == 0) lo = 0;
-  if (hi <= lo) return;
-  char* base = nullptr;
-  if (P.staged) {
-    const Ctrl* ctrl = reinterpret_cast<const Ctrl*>(P.heap + CTRL_OFF);
-    base = P.heap + P.staging_off + (long long)((ctrl->epoch + 1) & 1) * P.staging_bytes;
-  }
-  for (int s = 0; s < BULK_STAGES; ++s)
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[s])));
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-
-  // chunk cursor over [lo, hi): pieces of <= BULK_CHUNK bytes inside one member
-  struct Cur {
-    int k;
-    long long pos;
-  };
-  auto first = [&](long long at) {
-    Cur c{0, at};
-    while (c.k < P.n && P.start[c.k + 1] <= at) ++c.k;
-    return c;
-  };
-  auto piece = [&](const Cur& c, const char** src, char** dst) -> int {
-    const long long mend = P.start[c.k + 1] < hi ? P.start[c.k + 1] : hi;
-    long long len = mend - c.pos;
-    if (len > BULK_CHUNK) len = BULK_CHUNK;
-    const long long off = c.pos - P.start[c.k];
-    *src = P.src[c.k] + off;
-    *dst = (P.staged ? base + (long long)(uintptr_t)P.dst[c.k] : P.dst[c.k]) + off;
-    return (int)len;
-  };
-  auto advance = [&](Cur& c, int len) {
-    c.pos += len;
-    while (c.k < P.n && P.start[c.k + 1] <= c.pos) ++c.k;
-  };
-  char* dsts[BULK_STAGES];
-  int lens[BULK_STAGES];
-  Cur ld = first(lo);
-  int issued = 0;
-  auto issue_load = [&](int i) {
-    const int s = i % BULK_STAGES;
-    const char* src;
-    char* dst;
-    const int len = piece(ld, &src, &dst);
-    dsts[s] = dst;
-    lens[s] = len;
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar[s])), "r"(len)
-                 : "memory");
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(bulk_smem + (size_t)s * BULK_CHUNK)),
-        "l"(src), "r"(len), "r"(smem_u32(&bar[s]))
-        : "memory");
-    advance(ld, len);
-  };
-  while (issued < BULK_STAGES && ld.pos < hi) issue_load(issued++);
-  for (int i = 0; i < issued; ++i) {
-    const int s = i % BULK_STAGES;
-    const unsigned parity = (unsigned)((i / BULK_STAGES) & 1);
-    unsigned ok = 0;
-    while (!ok)
-      asm volatile(
-          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-          : "=r"(ok)
-          : "r"(smem_u32(&bar[s])), "r"(parity)
-          : "memory");
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dsts[s]),
-                 "r"(smem_u32(bulk_smem + (size_t)s * BULK_CHUNK)), "r"(lens[s])
-                 : "memory");
-    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-    // the previous stage's store has finished reading shared memory: refill it
-    if (i >= 1 && ld.pos < hi) {
-      asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-      issue_load(issued++);
-    }
-  }
-  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-}
 
 // ---- local_reduce (core.py:94-110) -------------------------------------------------
 template <class D, int OP>

@@ -73,8 +73,9 @@ def test_cli_microbench_and_train_two_gpus(tmp_path):
         assert int(f[6]) == 2                        # messages_per_rank, reference schedule at p=2
         assert 0 < float(f[4]) <= float(f[3]) <= float(f[5])
     out2 = tmp_path / "train.csv"
+    dump = tmp_path / "final.npz"
     cmd = cmd[:cmd.index("--mode")] + ["--mode", "train", "--model", "mobilenet_like", "--warmup-iters", "1",
-                                        "--timed-iters", "2", "--output", str(out2)]
+                                        "--timed-iters", "2", "--output", str(out2), "--dump-grads", str(dump)]
     cmd[cmd.index("--master-port") + 1] = str(_free_port())
     proc = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert proc.returncode == 0, (proc.stdout + proc.stderr)[-4000:]
@@ -82,3 +83,15 @@ def test_cli_microbench_and_train_two_gpus(tmp_path):
     assert rows[0] == "model,strategy,p,images_per_sec,ideal,efficiency"
     f = rows[1].split(",")
     assert f[:3] == ["mobilenet_like", "horovod_allreduce", "2"] and 0 < float(f[5]) <= 1.0
+    # acceptance criterion 9 analogue (test_acceptance.py:331-366): the final
+    # data-path tensors equal the reference's aggregate of the same synthetic
+    # gradients (last iteration), bit for bit
+    import numpy as np
+    from oracle import aggregation as OA
+    from tests.golden import inputs as I
+    last = 1 + 2 - 1
+    per_rank = [I.synth_gradients(0, last, I.MODELS["mobilenet_like"], r) for r in range(2)]
+    want, _, _ = OA.aggregate(per_rank, "float32", "auto", 64 << 20)
+    got = np.load(dump)
+    assert sorted(got.files) == sorted(want)
+    assert all(got[k].tobytes() == want[k].tobytes() for k in want)
