@@ -18,11 +18,16 @@ communicator so results can be emitted in the reference's own format:
   ``aggregate`` (``horovod_allreduce`` with ``algo``, ``baidu_ring`` with
   ring_rsa). CSV ``TRAIN_CSV_HEADER`` (bench.py:40).
 
+* ``sweep`` (bench.py:287-291): the analytic alpha-beta-gamma model
+  (costmodel.py, a restatement of simcost.py), with the reference's default
+  costs, a JSON cost model, or ``--cost-model b200`` (fitted to this
+  framework's measured latencies).
+
 Group identity comes from torchrun's ``RANK``/``WORLD_SIZE`` or the
 reference's ``COLLECTIUM_RANK``/``COLLECTIUM_NPROCS`` (bench.py:32-33,
-316-334). The simulator, socket transport, parameter server and analytic
-cost-model sweep are not part of this framework: asking for
-them is a ``ConfigError`` (exit 2).
+316-334). The simulator, socket transport and parameter-server data path are
+not part of this framework: asking for them is a
+``ConfigError`` (exit 2).
 """
 
 from __future__ import annotations
@@ -126,6 +131,7 @@ class BenchConfig:
     strategies: list = field(default_factory=lambda: list(STRATEGIES))
     p_list: list = field(default_factory=lambda: [1, 2, 4, 8])
     dump_grads: str | None = None
+    cost_model: object = None          # CostModel, or "b200" (measured calibration per p)
 
     def validate(self) -> None:
         if self.mode not in _MODES:
@@ -150,12 +156,11 @@ class BenchConfig:
             raise ConfigError("msg_min_bytes must be a multiple of 8, >= 8")
         if self.msg_max_bytes < self.msg_min_bytes:
             raise ConfigError("msg_max_bytes must be >= msg_min_bytes")
+        if self.mode == "sweep":            # analytic: no transport involved
+            return
         if self.transport != "nvlink":
             raise ConfigError(f"transport {self.transport!r} (the reference's simulator / TCP "
                               f"sockets) is not part of this framework; use transport 'nvlink'")
-        if self.mode == "sweep":
-            raise ConfigError("sweep mode is the reference's analytic cost model (simcost.py), "
-                              "which is not part of this framework")
         if self.mode == "train" and self.strategy == "ps_pull":
             raise ConfigError("strategy ps_pull (parameter server, paramserver.py) is not part "
                               "of this framework")
@@ -169,11 +174,13 @@ class BenchConfig:
             raise ConfigError(f"cannot read config {path}: {exc}") from exc
         except json.JSONDecodeError as exc:
             raise ConfigError(f"{path}:{exc.lineno}: invalid JSON: {exc.msg}") from exc
-        known = {f.name for f in fields(cls)} | {"cost_model"}
+        known = {f.name for f in fields(cls)}
         unknown = set(data) - known
         if unknown:
             raise ConfigError(f"{path}: unknown fields {sorted(unknown)}")
-        data = {k: v for k, v in data.items() if k != "cost_model"}
+        if isinstance(data.get("cost_model"), dict):
+            from .costmodel import CostModel
+            data = dict(data, cost_model=CostModel.from_dict(data["cost_model"]))
         try:
             return cls(**data)
         except TypeError as exc:
@@ -336,9 +343,24 @@ def write_output(cfg: BenchConfig, rows: list) -> None:
         print(text, end="")
 
 
+def run_sweep(cfg: BenchConfig) -> list:
+    """bench.py:287-291 / simcost.py:265-290: analytic images/sec and
+    scaling efficiency per (model, strategy, p); ``cost_model="b200"`` uses
+    the alpha/beta/gamma fitted to this framework's measured latencies."""
+    from .costmodel import CostModel, sweep, sweep_csv_rows
+    cfg.validate()
+    calibrated = cfg.cost_model == "b200"
+    costs = cfg.cost_model if isinstance(cfg.cost_model, CostModel) else CostModel()
+    return sweep_csv_rows(sweep(cfg.models, cfg.strategies, cfg.p_list, costs, cfg.fusion_threshold,
+                                calibrated=calibrated))
+
+
 def run_bench(cfg: BenchConfig) -> None:
     """bench.py:337-361."""
     cfg.validate()
+    if cfg.mode == "sweep":
+        write_output(cfg, run_sweep(cfg))
+        return
     rank, _ = resolve_identity(cfg)
     if cfg.mode == "microbench":
         rows = run_microbench(cfg)

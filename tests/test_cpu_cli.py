@@ -11,7 +11,6 @@ from paper_1810_11112_b200 import cli, harness
 
 
 @pytest.mark.parametrize("argv,msg", [
-    (["--mode", "sweep"], "cost model"),
     (["--transport", "socket"], "not part of this framework"),
     (["--transport", "sim"], "not part of this framework"),
     (["--mode", "train", "--strategy", "ps_pull"], "ps_pull"),
@@ -65,3 +64,34 @@ def test_models_sizes_and_identity(monkeypatch, tmp_path):
     monkeypatch.setenv("COLLECTIUM_RANK", "4")
     with pytest.raises(harness.ConfigError):
         harness.resolve_identity(cfg)
+
+
+def test_cost_model_sweep_matches_reference_golden():
+    """costmodel.py restates simcost.py: the sweep CSV rows and the closed-form
+    predictions equal the unmodified reference's (tests/golden/gen_sweep.py)."""
+    import os
+    from paper_1810_11112_b200 import costmodel as CM
+    cases = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "sweep.json")))
+    for c in cases:
+        if "predict" in c:
+            algo, n, p = c["predict"]
+            assert CM.predict_allreduce_time(algo, n, p, CM.CostModel()) == c["seconds"]
+            continue
+        costs = CM.CostModel.from_dict(c["cost"])
+        rows = CM.sweep_csv_rows(CM.sweep(c["models"], c["strategies"], c["p_list"], costs, c["threshold"]))
+        assert rows == c["csv"]
+
+
+def test_cli_sweep_mode_and_b200_calibration(tmp_path, capsys):
+    out = tmp_path / "sweep.csv"
+    assert cli.main(["--mode", "sweep", "--models", "resnet50_like", "--strategies", "horovod_allreduce",
+                     "--p-list", "1,2,4,8", "--output", str(out)]) == 0
+    rows = out.read_text().splitlines()
+    assert rows[0] == "model,strategy,p,images_per_sec,ideal,efficiency,exposed_comm_s" and len(rows) == 5
+    assert cli.main(["--mode", "sweep", "--cost-model", "b200", "--p-list", "2,4", "--output", str(out)]) == 0
+    from paper_1810_11112_b200 import costmodel as CM
+    m = CM.b200_cost_model(4)
+    assert 0 < m.alpha < 25e-6 and 0 < m.beta < 2e-9       # B200 NVLink: far below the reference defaults
+    spec = tmp_path / "cost.json"
+    spec.write_text(json.dumps({"alpha": 1e-5, "beta": 1e-10, "gamma": 0, "bogus": 1}))
+    assert cli.main(["--mode", "sweep", "--cost-model", str(spec)]) == 2
