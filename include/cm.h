@@ -273,6 +273,19 @@ int cm_allgather_v(cm_comm_t* comm, const void* const* sends, void* const* recvs
  * Local kernels
  * ------------------------------------------------------------------------- */
 /* local_reduce core.py:94-110: out = a op b (a is the accumulator) */
+/* parameter-server pull step paramserver.py:171-271 (round-robin shard map
+ * :159-165 given as owners[], tensors in sorted-name order): worker ranks
+ * (worker_mask bit q) stage their gradients; each owner sums the workers'
+ * shards in worker-rank order in float64, divides by the worker count and
+ * applies params -= lr * mean (float64, then rounded to the dtype); workers
+ * then pull every other owner's updated shards into `params` (a fused
+ * device buffer, in/out). float32 / float64. Stream-ordered. */
+int cm_ps_step(cm_comm_t* comm, int n, const void* const* grads, void* params, const int64_t* counts,
+               int dtype, const int* owners, uint32_t worker_mask, double lr, void* stream);
+int cm_ps_step_v(cm_comm_t* comm, int n, const void* const* grads, void* const* params,
+                 const int64_t* counts, int dtype, const int* owners, uint32_t worker_mask, double lr,
+                 void* stream);
+
 int cm_local_reduce(const void* a, const void* b, void* out, int64_t count, int dtype, int op,
                     void* stream);
 /* fuse/unfuse payload moves aggregation.py:110-111,133-135: one launch copies

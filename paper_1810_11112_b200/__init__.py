@@ -24,6 +24,7 @@ from .aggregation import (DEFAULT_FUSION_THRESHOLD, FusedBuffer, FusionConfig,  
                           GradientSet, aggregate, aggregate_group, fuse,
                           fuse_plan, negotiate_ready, register_gradients, unfuse)
 from .overlap import OverlappedAggregator  # noqa: F401
+from .paramserver import PsTopology, run_ps_step, run_ps_step_group  # noqa: F401
 from .registry import (BufferHandle, BufferKind, BufferRegistry, Policy,  # noqa: F401
                        RegistryStats)
 

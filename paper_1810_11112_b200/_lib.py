@@ -1,7 +1,7 @@
 """ctypes binding of libcm.so (include/cm.h).
 
 The library is built in-tree by ``__graft_entry__.build()`` /
-``python -m paper_1810_11112_b200._build``. There is no fallback: importing
+``python paper_1810_11112_b200/_build.py``. There is no fallback: importing
 this module without the built library raises immediately.
 """
 
@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(_HERE, "libcm.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
-        f"{LIB_PATH} is missing: build it with `python -m paper_1810_11112_b200._build` "
+        f"{LIB_PATH} is missing: build it with `python paper_1810_11112_b200/_build.py` "
         "(there is no CPU fallback for the allreduce path)")
 
 lib = C.CDLL(LIB_PATH)
@@ -110,12 +110,18 @@ _SIGS = {
     "cm_reduce_scatter_v": ([_vp, _P(_vp), _P(_vp), _i64, _i, _i, _i, _vp, _P(Stats)], _i),
     "cm_allgather_v": ([_vp, _P(_vp), _P(_vp), _i64, _i, _i, _vp, _P(Stats)], _i),
     "cm_local_reduce": ([_vp, _vp, _vp, _i64, _i, _i, _vp], _i),
+    "cm_ps_step": ([_vp, _i, _P(_vp), _vp, _P(_i64), _i, _P(_i), C.c_uint32, C.c_double, _vp], _i),
+    "cm_ps_step_v": ([_vp, _i, _P(_vp), _P(_vp), _P(_i64), _i, _P(_i), C.c_uint32, C.c_double, _vp], _i),
     "cm_batched_copy": ([_i, _P(_vp), _P(_vp), _P(_i64), _vp], _i),
     "cm_bench_p2p": ([_vp, _i, _i64, _i, _i, _vp, _P(C.c_double)], _i),
     "cm_time_allreduce": ([_vp, _vp, _vp, _i64, _i, _i, _i, _i64, _i, _i, _vp,
                            _P(C.c_double)], _i),
 }
 
+_missing = [n for n in _SIGS if not hasattr(lib, n)]
+if _missing:
+    raise ImportError(f"{LIB_PATH} is stale (missing {', '.join(_missing[:4])}): rebuild it with "
+                      f"`python paper_1810_11112_b200/_build.py`")
 for _name, (_args, _res) in _SIGS.items():
     _fn = getattr(lib, _name)
     _fn.argtypes = _args

@@ -638,7 +638,7 @@ int do_ag(cm_comm* c, const void* const* sends, void* const* recvs, int64_t coun
 bool g_bulk_copy_default = true;   // cm_batched_copy without a communicator (fuse/unfuse)
 
 int launch_batched_copy(cm_comm* c, int n, const void* const* srcs, void* const* dsts,
-                        const int64_t* nbytes, bool staged, cudaStream_t stream) {
+                        const int64_t* nbytes, bool staged, cudaStream_t stream, char* heap = nullptr) {
   for (int base = 0; base < n; base += MAXCOPY) {
     const int m = std::min(MAXCOPY, n - base);
     CopyParams P;
@@ -653,7 +653,7 @@ int launch_batched_copy(cm_comm* c, int n, const void* const* srcs, void* const*
     if (P.start[m] == 0) continue;
     P.staged = staged ? 1 : 0;
     if (c) {
-      P.heap = c->local;
+      P.heap = heap ? heap : c->local;      // staged: whose staging (virtual ranks share one process)
       P.staging_bytes = (long long)c->staging_bytes;
       P.staging_off = (long long)c->staging_off;
     }
@@ -1535,6 +1535,120 @@ int cm_fused_allreduce_agreed(cm_comm_t* c, int n, const void* const* sends,
   for (int q = 0; q < ngroups; ++q) count_stats(c, stats[q]);
   *n_calls = ngroups;
   return CM_OK;
+}
+
+// Parameter-server step (paramserver.py:171-271) on the NVLink heap: workers
+// stage their gradients, owners update their shards in float64, workers pull
+// the others'. `grads`: nloc * n pointers (rank-major; ignored for non-workers),
+// `params`: nloc fused parameter buffers (in/out, sorted-name layout).
+int cm_ps_step_v(cm_comm_t* c, int n, const void* const* grads, void* const* params, const int64_t* counts,
+                 int dtype, const int* owners, uint32_t worker_mask, double lr, void* stream_) {
+  if (dtype != CM_FLOAT32 && dtype != CM_FLOAT64)
+    return fail(CM_ERR_SHAPE, "the parameter server handles float32 / float64 (core.py:18-21)");
+  const int p = c->size;
+  if (n < 1) return fail(CM_ERR_VALUE, "no tensors");
+  if (worker_mask == 0 || (p < 32 && (worker_mask >> p) != 0)) return fail(CM_ERR_VALUE, "bad worker mask");
+  int st;
+  if ((st = check_async_error(c))) return st;
+  const int64_t sz = (int64_t)dtype_size(dtype);
+  int64_t gtot = 0;
+  std::vector<int64_t> goff(n);
+  for (int t = 0; t < n; ++t) {
+    if (counts[t] < 0) return fail(CM_ERR_SHAPE, "negative element count");
+    if (owners[t] < 0 || owners[t] >= p) return fail(CM_ERR_VALUE, "shard owner outside the group");
+    goff[t] = gtot;
+    gtot += counts[t];
+  }
+  if (2 * gtot * sz > (int64_t)c->staging_bytes)
+    return fail(CM_ERR_CONFIG, "parameter-server step needs 2 x " + std::to_string(gtot * sz) +
+                                   " B of staging; the communicator has " + std::to_string(c->staging_bytes));
+  // owner table: own_first[0..p], then {prefix, goff, len} per owned tensor
+  std::vector<long long> tab(p + 1, 0);
+  std::vector<long long> ent;
+  int64_t maxown = 0;
+  for (int q = 0; q < p; ++q) {
+    tab[q] = (long long)(ent.size() / 3);
+    int64_t pre = 0;
+    for (int t = 0; t < n; ++t)
+      if (owners[t] == q && counts[t] > 0) {
+        ent.push_back(pre);
+        ent.push_back(goff[t]);
+        ent.push_back(counts[t]);
+        pre += counts[t];
+      }
+    maxown = std::max(maxown, pre);
+  }
+  tab[p] = (long long)(ent.size() / 3);
+  tab.insert(tab.end(), ent.begin(), ent.end());
+  std::string key = "ps:" + std::string(reinterpret_cast<const char*>(tab.data()), tab.size() * sizeof(long long));
+  long long* dtab;
+  auto it = c->gtabs.find(key);
+  if (it != c->gtabs.end()) {
+    dtab = it->second;
+  } else {
+    CUDA_TRY(cudaMalloc(&dtab, tab.size() * sizeof(long long)));
+    CUDA_TRY(cudaMemcpy(dtab, tab.data(), tab.size() * sizeof(long long), cudaMemcpyHostToDevice));
+    c->gtabs[key] = dtab;
+  }
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  const int nloc = c->virt ? p : 1;
+  // 1. workers stage their gradients (sorted-name layout) into staging[next parity]
+  for (int l = 0; l < nloc; ++l) {
+    const int r = c->virt ? l : c->rank;
+    if (!((worker_mask >> r) & 1u)) continue;
+    std::vector<const void*> srcs(n);
+    std::vector<void*> dsts(n);
+    std::vector<int64_t> bytes(n);
+    for (int t = 0; t < n; ++t) {
+      srcs[t] = grads[(size_t)l * n + t];
+      dsts[t] = reinterpret_cast<void*>((uintptr_t)(goff[t] * sz));
+      bytes[t] = counts[t] * sz;
+    }
+    if ((st = launch_batched_copy(c, n, srcs.data(), dsts.data(), bytes.data(), true, stream, c->heap[r])))
+      return st;
+  }
+  // 2. the step kernel
+  PsParams P;
+  memset(&P, 0, sizeof P);
+  for (int q = 0; q < p; ++q) P.heap[q] = c->heap[q];
+  for (int l = 0; l < nloc; ++l) P.params[l] = static_cast<char*>(params[l]);
+  P.table = dtab;
+  P.p = p;
+  P.rank = c->rank;
+  P.virt = c->virt ? 1 : 0;
+  for (int q = 0; q < p; ++q)
+    if ((worker_mask >> q) & 1u) P.workers[P.nworkers++] = q;
+  P.worker_mask = worker_mask;
+  P.gtot = gtot;
+  P.lr = lr;
+  unsigned long long h = make_hdr(gtot, dtype, 0, 0, 3, 0, 0, 0) ^ ((unsigned long long)worker_mask << 52);
+  for (long long v : tab) h = (h ^ (unsigned long long)v) * 1099511628211ull;
+  P.hdr = h;
+  P.timeout_cycles = c->timeout_cycles;
+  P.staging_off = (long long)c->staging_off;
+  P.staging_bytes = (long long)c->staging_bytes;
+  P.herr = c->herr_dev;
+  int64_t nb = (maxown * sz + c->twoshot_bytes_per_cta - 1) / c->twoshot_bytes_per_cta;
+  nb = std::max<int64_t>(1, std::min<int64_t>(nb, std::min(c->max_ctas, MAXBLK)));
+  const void* k = dtype == CM_FLOAT32 ? (const void*)ps_kernel<F32> : (const void*)ps_kernel<F64>;
+  void* args[] = {&P};
+  if (c->virt) {
+    int per_sm = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, THREADS, 0));
+    nb = std::min<int64_t>(nb, std::max<int64_t>(1, (int64_t)per_sm * c->sms / p));
+    CUDA_TRY(cudaLaunchCooperativeKernel(k, dim3((unsigned)nb, (unsigned)p), dim3(THREADS), args, 0, stream));
+  } else {
+    CUDA_TRY(cudaLaunchKernel(k, dim3((unsigned)nb), dim3(THREADS), args, 0, stream));
+  }
+  c->launches += 1;
+  c->calls += 1;
+  return CM_OK;
+}
+
+int cm_ps_step(cm_comm_t* c, int n, const void* const* grads, void* params, const int64_t* counts, int dtype,
+               const int* owners, uint32_t worker_mask, double lr, void* stream) {
+  void* pv[1] = {params};
+  return cm_ps_step_v(c, n, grads, pv, counts, dtype, owners, worker_mask, lr, stream);
 }
 
 int cm_local_reduce(const void* a, const void* b, void* out, int64_t count, int dtype, int op,

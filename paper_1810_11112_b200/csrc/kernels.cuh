@@ -6,6 +6,7 @@
 //   kernel_ll.cuh         LL one-shot / two-shot (small and medium messages)
 //   kernel_rhd.cuh        literal log2(p)-step recursive halving/doubling
 //   kernel_copy.cuh       fusion pack (SM and TMA bulk copy), NVLink diagnostics
+//   kernel_ps.cuh         parameter-server step (owner update + pull)
 //   kernels.cuh           local_reduce and the per-dtype kernel tables
 #pragma once
 
@@ -14,6 +15,7 @@
 #include "kernel_ll.cuh"
 #include "kernel_rhd.cuh"
 #include "kernel_copy.cuh"
+#include "kernel_ps.cuh"
 
 namespace cm {
 namespace dev {

@@ -41,3 +41,36 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def ps_cases():
+    """Parameter-server steps run by the unmodified reference on its simulated
+    network (paramserver.py:274-298): co-located and split topologies."""
+    import numpy as np
+    ref = reference.load()
+    from collectium import paramserver as PS
+    from collectium.core import Tensor
+    cases = []
+    specs = [((0, 1, 2, 3), (0, 1, 2, 3), "float32", [5, 1, 1000, 37, 64, 3, 129]),
+             ((0, 1, 2), (0, 1, 2), "float64", [7, 100, 2, 33]),
+             ((0, 1, 2, 3), (1, 3), "float32", [16, 9, 250, 4, 1]),
+             ((1, 2, 3), (0,), "float32", [8, 12, 1001])]
+    for workers, ps, dtype, sizes in specs:
+        names = [f"w{i:02d}" for i in range(len(sizes))]
+        rng = np.random.default_rng([len(workers), len(ps), len(sizes)])
+        params = [Tensor(nm, dtype, rng.standard_normal(n).astype(dtype)) for nm, n in zip(names, sizes)]
+        grads = [[Tensor(nm, dtype, rng.standard_normal(n).astype(dtype)) for nm, n in zip(names, sizes)]
+                 for _ in workers]
+        topo = PS.PsTopology.create(workers, ps, names)
+        res, _ = PS.ps_training_step(topo, grads, params, 0.05)
+        cases.append({"workers": list(workers), "ps": list(ps), "dtype": dtype, "sizes": sizes, "lr": 0.05,
+                      "seed": [len(workers), len(ps), len(sizes)],
+                      "sha": {t.name: __import__("hashlib").sha256(t.to_bytes()).hexdigest() for t in res[0]},
+                      "same_on_all_workers": all([t.to_bytes() for t in r] == [t.to_bytes() for t in res[0]]
+                                                 for r in res)})
+    json.dump(cases, open(os.path.join(HERE, "ps.json"), "w"), indent=1)
+    print("wrote", len(cases), "ps cases", ref.__name__)
+
+
+if __name__ == "__main__" and "--ps" in sys.argv:
+    ps_cases()

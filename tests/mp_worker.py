@@ -288,6 +288,36 @@ def main():
                    f"overlapped aggregate {algo} step {step}")
             expect(len(ov.step_stats) == len(groups), "overlap stats")
 
+    # 4f. parameter-server pull step (paramserver.py:171-271): co-located and
+    # split topologies, two steps each, bit-exact vs the oracle restatement
+    from oracle import paramserver as OPS
+    sizes = [300_001, 17, 1 << 20, 4096, 99_999, 2, 65_536]
+    pnames = [f"p{i:02d}" for i in range(len(sizes))]
+    rngp = np.random.default_rng([41, world])
+    params0 = {nm: rngp.standard_normal(n).astype(np.float32) for nm, n in zip(pnames, sizes)}
+    for workers, ps in ((list(range(world)), list(range(world))),
+                        (list(range(world)), [world - 1]),
+                        (list(range(1, world)), [0])):
+        topo = P.PsTopology.create(workers, ps, pnames)
+        cur = dict(params0)
+        mine = [P.Tensor(nm, "float32", torch.from_numpy(cur[nm]).cuda()) for nm in pnames]
+        for step in range(2):
+            gr = [{nm: np.random.default_rng([42, step, w, i]).standard_normal(n).astype(np.float32)
+                   for i, (nm, n) in enumerate(zip(pnames, sizes))} for w in workers]
+            want = OPS.ps_step(gr, cur, workers, 0.05)
+            my_g = None
+            if rank in workers:
+                my_g = [P.Tensor(nm, "float32", torch.from_numpy(gr[workers.index(rank)][nm]).cuda()) for nm in pnames]
+            res = P.run_ps_step(rank, comm, topo, my_g, mine, 0.05)
+            if rank in workers:
+                expect(all(t.to_bytes() == want[t.name].tobytes() for t in res),
+                       f"ps step workers={workers} ps={ps} step={step}")
+                mine = res
+            else:
+                expect(res is None, "pure PS rank returns None")
+                mine = [P.Tensor(nm, "float32", torch.from_numpy(want[nm]).cuda()) for nm in pnames]
+            cur = want
+
     # 4a. out= refill: persistent buckets are overwritten with the next step's means
     layers = I.MODELS["mobilenet_like"]
     g1 = I.synth_gradients(0, 0, layers, rank)
