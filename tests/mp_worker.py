@@ -290,7 +290,7 @@ def main():
 
     # 4f. parameter-server pull step (paramserver.py:171-271): co-located and
     # split topologies, two steps each, bit-exact vs the oracle restatement
-    from oracle import paramserver as OPS
+    from oracle import paramserver as OPSV
     sizes = [300_001, 17, 1 << 20, 4096, 99_999, 2, 65_536]
     pnames = [f"p{i:02d}" for i in range(len(sizes))]
     rngp = np.random.default_rng([41, world])
@@ -304,7 +304,7 @@ def main():
         for step in range(2):
             gr = [{nm: np.random.default_rng([42, step, w, i]).standard_normal(n).astype(np.float32)
                    for i, (nm, n) in enumerate(zip(pnames, sizes))} for w in workers]
-            want = OPS.ps_step(gr, cur, workers, 0.05)
+            want = OPSV.ps_step(gr, cur, workers, 0.05)
             my_g = None
             if rank in workers:
                 my_g = [P.Tensor(nm, "float32", torch.from_numpy(gr[workers.index(rank)][nm]).cuda()) for nm in pnames]
