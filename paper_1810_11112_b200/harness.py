@@ -16,7 +16,8 @@ communicator so results can be emitted in the reference's own format:
   layer, rank) (bench.py:224-232), the modeled forward+backward time spent
   for real as the socket transport does (sockets.py:206-210, a sleep), then
   ``aggregate`` (``horovod_allreduce`` with ``algo``, ``baidu_ring`` with
-  ring_rsa). CSV ``TRAIN_CSV_HEADER`` (bench.py:40).
+  ring_rsa) or the parameter-server step (``ps_pull``, paramserver.py via
+  ``run_ps_step``). CSV ``TRAIN_CSV_HEADER`` (bench.py:40).
 
 * ``sweep`` (bench.py:287-291): the analytic alpha-beta-gamma model
   (costmodel.py, a restatement of simcost.py), with the reference's default
@@ -25,9 +26,8 @@ communicator so results can be emitted in the reference's own format:
 
 Group identity comes from torchrun's ``RANK``/``WORLD_SIZE`` or the
 reference's ``COLLECTIUM_RANK``/``COLLECTIUM_NPROCS`` (bench.py:32-33,
-316-334). The simulator, socket transport and parameter-server data path are
-not part of this framework: asking for them is a
-``ConfigError`` (exit 2).
+316-334). The simulator and socket transport are not part of this framework
+(DESIGN.md section 7): asking for them is a ``ConfigError`` (exit 2).
 """
 
 from __future__ import annotations
@@ -161,9 +161,6 @@ class BenchConfig:
         if self.transport != "nvlink":
             raise ConfigError(f"transport {self.transport!r} (the reference's simulator / TCP "
                               f"sockets) is not part of this framework; use transport 'nvlink'")
-        if self.mode == "train" and self.strategy == "ps_pull":
-            raise ConfigError("strategy ps_pull (parameter server, paramserver.py) is not part "
-                              "of this framework")
 
     @classmethod
     def from_file(cls, path: str) -> "BenchConfig":
@@ -309,18 +306,30 @@ def run_train_bench(cfg: BenchConfig) -> tuple:
     cfg.validate()
     model = resolve_model(cfg.model)
     grad_bytes = sum(b for b, _ in model.layers)
-    g = _Group(cfg, staging_bytes=max(64 << 20, min(grad_bytes, cfg.fusion_threshold) + (8 << 20)))
+    ps = cfg.strategy == "ps_pull"
+    need = 2 * grad_bytes if ps else min(grad_bytes, cfg.fusion_threshold)
+    g = _Group(cfg, staging_bytes=max(64 << 20, need + (8 << 20)))
     try:
         fusion = FusionConfig(cfg.fusion_threshold)
         algo = "ring_rsa" if cfg.strategy == "baidu_ring" else cfg.algo
         device = torch.device("cuda", g.local)
         times, final = [], None
+        if ps:                                   # bench.py:239-243: zero parameters, round-robin shards
+            from .paramserver import PsTopology, run_ps_step
+            names = [f"layer{idx:04d}" for idx in range(len(model.layers))]
+            topology = PsTopology.create(range(g.size), range(g.size), names)
+            params = [Tensor(nm, "float32", torch.zeros(nb // 4, dtype=torch.float32, device=device))
+                      for nm, (nb, _) in zip(names, model.layers)]
         for it in range(cfg.warmup_iters + cfg.timed_iters):
             t0 = time.perf_counter()
             time.sleep(model.forward_s + model.backward_s)   # modeled compute (sockets.py:206-210)
             grads = synth_gradients(cfg.seed, it, model, g.rank, device)
-            result = aggregate(grads, g.group, g.comm, algo=algo, cfg=fusion, switch_bytes=cfg.switch_bytes)
-            final = list(result.tensors)
+            if ps:
+                params = run_ps_step(g.rank, g.comm, topology, list(grads.tensors), params, cfg.learning_rate)
+                final = params
+            else:
+                result = aggregate(grads, g.group, g.comm, algo=algo, cfg=fusion, switch_bytes=cfg.switch_bytes)
+                final = list(result.tensors)
             t1 = time.perf_counter()
             if it >= cfg.warmup_iters:
                 times.append(t1 - t0)

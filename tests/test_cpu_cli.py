@@ -13,7 +13,6 @@ from paper_1810_11112_b200 import cli, harness
 @pytest.mark.parametrize("argv,msg", [
     (["--transport", "socket"], "not part of this framework"),
     (["--transport", "sim"], "not part of this framework"),
-    (["--mode", "train", "--strategy", "ps_pull"], "ps_pull"),
     (["--timed-iters", "0"], "timed_iters"),
     (["--warmup-iters", "-1"], "warmup_iters"),
     (["--switch-bytes", "0"], "switch_bytes"),

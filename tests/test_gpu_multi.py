@@ -95,3 +95,18 @@ def test_cli_microbench_and_train_two_gpus(tmp_path):
     got = np.load(dump)
     assert sorted(got.files) == sorted(want)
     assert all(got[k].tobytes() == want[k].tobytes() for k in want)
+    # ps_pull strategy: the parameter-server path, params from zeros, lr 0.1
+    from oracle import paramserver as OPS
+    cmd[cmd.index("--master-port") + 1] = str(_free_port())
+    i = cmd.index("--output")
+    cmd = cmd[:i] + ["--output", str(out2), "--dump-grads", str(dump), "--strategy", "ps_pull"]
+    proc = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert proc.returncode == 0, (proc.stdout + proc.stderr)[-4000:]
+    assert out2.read_text().splitlines()[1].split(",")[1] == "ps_pull"
+    names = [nm for nm, _ in per_rank[0]]
+    cur = {nm: np.zeros(a.size, np.float32) for nm, a in per_rank[0]}
+    for it in range(3):
+        grads = [dict(I.synth_gradients(0, it, I.MODELS["mobilenet_like"], r)) for r in range(2)]
+        cur = OPS.ps_step(grads, cur, [0, 1], 0.1)
+    got = np.load(dump)
+    assert all(got[k].tobytes() == cur[k].tobytes() for k in names)
