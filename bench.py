@@ -169,14 +169,23 @@ def make_grads(model, rank, device, dtype="float32", pinned=False):
     import paper_1810_11112_b200 as P
     from tests.golden.inputs import synth_gradients
     ts = []
-    for nm, a in synth_gradients(0, 0, MODELS[model], rank):
+    grads = synth_gradients(0, 0, MODELS[model], rank)
+    flat = None
+    if device is None and pinned:     # host gradients: views of ONE flat pinned buffer, as a
+        tdt = torch.bfloat16 if dtype == "bfloat16" else torch.float32   # framework's flat grads
+        flat = torch.empty(sum(a.size for _, a in grads), dtype=tdt).pin_memory()
+    off = 0
+    for nm, a in grads:
         t = torch.from_numpy(a)
         if dtype == "bfloat16":
             t = t.to(torch.bfloat16)
         if device is not None:
             t = t.to(device)
-        elif pinned:
-            t = t.pin_memory()
+        elif flat is not None:
+            v = flat[off:off + a.size]
+            v.copy_(t)
+            t = v
+            off += a.size
         ts.append(P.Tensor(nm, dtype, t))
     return P.GradientSet(tuple(ts))
 
@@ -374,7 +383,7 @@ def headline(args, rank, world, local):
         assert not r.tensors[0].is_cuda
         e2e = {"value": round(world * S / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
                "ms_per_step": round(e2e_ms, 4), "h2d_bytes_per_step": S, "d2h_bytes_per_step": S,
-               "what": "aggregate() on pinned host gradients: H2D on a copy stream, fused "
+               "what": "aggregate() on pinned host gradients (views of one flat pinned buffer): H2D on a copy stream, fused "
                        "allreduce+mean on the compute stream, D2H on a second copy stream straight "
                        "into pinned host buckets (aggregate(out=prev)), overlapped per fused group; "
                        "host wall clock, max over ranks"}

@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <chrono>
 #include <cstdlib>
 #include <cstring>
@@ -690,6 +691,33 @@ int launch_batched_copy(cm_comm* c, int n, const void* const* srcs, void* const*
   return CM_OK;
 }
 
+// Consecutive members whose sources are adjacent in memory (a flat gradient
+// buffer viewed as tensors) become one copy: {source, offset in the fused
+// layout, bytes}, cut into pieces of at most `piece` bytes.
+struct Run {
+  const char* src;
+  int64_t off, bytes;
+};
+
+std::vector<Run> coalesce(const void* const* srcs, const int64_t* bytes, int n, int64_t piece) {
+  std::vector<Run> runs;
+  int64_t off = 0;
+  for (int k = 0; k < n; ++k) {
+    const char* s = static_cast<const char*>(srcs[k]);
+    if (bytes[k] > 0) {
+      if (!runs.empty() && runs.back().src + runs.back().bytes == s && runs.back().off + runs.back().bytes == off)
+        runs.back().bytes += bytes[k];
+      else
+        runs.push_back(Run{s, off, bytes[k]});
+    }
+    off += bytes[k];
+  }
+  std::vector<Run> out;
+  for (const Run& r : runs)
+    for (int64_t a = 0; a < r.bytes; a += piece) out.push_back(Run{r.src + a, r.off + a, std::min(piece, r.bytes - a)});
+  return out;
+}
+
 // Host-memory aggregate pipeline (CUDA-aware semantics for host gradients).
 // Stream roles: h2d copies inputs into `indev`, the caller's stream runs the
 // collectives, d2h copies results out of `outdev`. Every hand-off is an
@@ -1299,18 +1327,21 @@ int cm_fused_allreduce_agreed(cm_comm_t* c, int n, const void* const* sends,
       // H2D into the device (h2d stream) and, for host outputs, D2H back out
       // (d2h stream) in ~16 MiB chunks so both PCIe directions stream at once
       if ((st = hp.start(out_host ? off : 0, 0))) return st;
-      // the fused result is contiguous in indev, so each chunk leaves in ONE D2H
-      int64_t soff = 0, chunk_lo = 0;
-      for (int k = 0; k < n; ++k) {
-        if (bytes[k])
-          CUDA_TRY(cudaMemcpyAsync(out_host ? c->indev + soff : dsts[k], srcs[k], bytes[k], cudaMemcpyDefault,
-                                   c->h2d));
-        soff += bytes[k];
-        if (out_host && soff > chunk_lo && (soff - chunk_lo >= (16 << 20) || k == n - 1)) {
+      // members adjacent in memory are copied as one run (one DMA), runs are
+      // cut into 16 MiB pieces, and the fused result (contiguous) leaves in
+      // one D2H per piece
+      std::vector<Run> runs = coalesce(srcs.data(), bytes.data(), n, 16 << 20);
+      int64_t chunk_lo = 0;
+      for (size_t k = 0; k < runs.size(); ++k) {
+        const Run& r = runs[k];
+        CUDA_TRY(cudaMemcpyAsync((out_host ? c->indev : static_cast<char*>(recv_fused)) + r.off, r.src, r.bytes,
+                                 cudaMemcpyDefault, c->h2d));
+        const int64_t end = r.off + r.bytes;
+        if (out_host && (end - chunk_lo >= (16 << 20) || k + 1 == runs.size())) {
           if ((st = hp.link(c->h2d, c->d2h))) return st;
-          CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(recv_fused) + chunk_lo, c->indev + chunk_lo, soff - chunk_lo,
+          CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(recv_fused) + chunk_lo, c->indev + chunk_lo, end - chunk_lo,
                                    cudaMemcpyDeviceToHost, c->d2h));
-          chunk_lo = soff;
+          chunk_lo = end;
         }
       }
       if ((st = hp.join())) return st;
@@ -1383,11 +1414,10 @@ int cm_fused_allreduce_agreed(cm_comm_t* c, int n, const void* const* sends,
   std::vector<cudaEvent_t> in_ready(gr.size(), nullptr);
   for (size_t t = 0; t < gr.size(); ++t) {
     if (!gr[t].any_host) continue;
-    int64_t o = gr[t].off * sz;
-    for (int k = gr[t].i; k < gr[t].j; ++k) {
-      if (counts[k]) CUDA_TRY(cudaMemcpyAsync(c->indev + o, sends[k], counts[k] * sz, cudaMemcpyDefault, c->h2d));
-      o += counts[k] * sz;
-    }
+    std::vector<int64_t> gb;
+    for (int k = gr[t].i; k < gr[t].j; ++k) gb.push_back(counts[k] * sz);
+    for (const Run& r : coalesce(sends + gr[t].i, gb.data(), gr[t].j - gr[t].i, INT64_MAX))
+      CUDA_TRY(cudaMemcpyAsync(c->indev + gr[t].off * sz + r.off, r.src, r.bytes, cudaMemcpyDefault, c->h2d));
     if ((st = hp.ev(&in_ready[t]))) return st;
     CUDA_TRY(cudaEventRecord(in_ready[t], c->h2d));
   }
