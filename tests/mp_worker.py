@@ -238,15 +238,21 @@ def main():
     for algo in ("ring_rsa", "auto"):
         want, groups, _ = OA.aggregate(per_rank, "float32", algo, 8 << 20)
         want2, _, _ = OA.aggregate([[(nm, a * 2) for nm, a in pr] for pr in per_rank], "float32", algo, 8 << 20)
-        for kind in ("pinned", "pageable", "mixed"):
+        flat = torch.empty(sum(a.size for _, a in per_rank[rank]), dtype=torch.float32).pin_memory()
+        for kind in ("pinned", "pageable", "mixed", "flat"):
             def mk(scale):
-                ts = []
+                ts, off = [], 0
                 for i, (nm, a) in enumerate(per_rank[rank]):
                     x = torch.from_numpy(a * scale)
                     if kind == "pinned" or (kind == "mixed" and i % 2 == 0):
                         x = x.pin_memory()
                     elif kind == "mixed":
                         x = x.cuda()
+                    elif kind == "flat":
+                        v = flat[off:off + a.size]
+                        v.copy_(x)
+                        x = v
+                    off += a.size
                     ts.append(P.Tensor(nm, "float32", x))
                 return P.GradientSet(tuple(ts))
             res = P.aggregate(mk(1), group, comm, algo=algo, cfg=P.FusionConfig(8 << 20))

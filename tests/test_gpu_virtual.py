@@ -347,15 +347,21 @@ def test_single_rank_communicator_aggregate_host_and_device():
     comm = P.Communicator(rank=0, size=1, device=0, staging_bytes=64 << 20, pool_bytes=2 << 20)
     layers = [480_000] * 40 + [1_000_003, 77]
     g = I.synth_gradients(0, 0, layers, 0)
-    for kind in ("device", "pinned", "pageable", "mixed"):
+    flat = torch.empty(sum(a.size for _, a in g), dtype=torch.float32).pin_memory()
+    for kind in ("device", "pinned", "pageable", "mixed", "flat"):
         def mk(scale):
-            ts = []
+            ts, off = [], 0
             for i, (nm, a) in enumerate(g):
                 x = torch.from_numpy(a * scale)
                 if kind == "device" or (kind == "mixed" and i % 3 == 0):
                     x = x.cuda()
                 elif kind in ("pinned", "mixed"):
                     x = x.pin_memory()
+                elif kind == "flat":              # views of one pinned buffer: coalesced copies
+                    v = flat[off:off + a.size]
+                    v.copy_(x)
+                    x = v
+                off += a.size
                 ts.append(P.Tensor(nm, "float32", x))
             return P.GradientSet(tuple(ts))
         res = P.aggregate(mk(1), P.GroupSpec(1), comm)
