@@ -208,6 +208,16 @@ def main():
             expect(all(t.to_bytes() == want[t.name].tobytes() for t in res.tensors),
                    f"multi-buffer aggregate {algo} mb={mb}")
     comm.set_param("multi_buffer", 2)
+    # opt-in TMA bulk-copy pack (bulk_copy) into the staging heap
+    comm.set_param("bulk_copy", 2)
+    aligned = [I.synth_gradients(5, 0, [480_000] * 12 + [1_000_004, 76], r) for r in range(world)]
+    for algo in ("ring_rsa", "rhd_rsa"):
+        want, groups, _ = OA.aggregate(aligned, "float32", algo, 8 << 20)
+        gs = P.GradientSet(tuple(P.Tensor(nm, "float32", torch.from_numpy(a).cuda())
+                                 for nm, a in aligned[rank]))
+        res = P.aggregate(gs, group, comm, algo=algo, cfg=P.FusionConfig(8 << 20))
+        expect(all(t.to_bytes() == want[t.name].tobytes() for t in res.tensors), f"bulk-copy pack {algo}")
+    comm.set_param("bulk_copy", 1)
     # registered gradients: peers' member tensors are read in place (no pack)
     for algo in ("ring_rsa", "rhd_rsa"):
         want, groups, _ = OA.aggregate(per_rank, "float32", algo, 8 << 20)
