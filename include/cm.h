@@ -172,6 +172,9 @@ int cm_comm_registry(cm_comm_t* comm, cm_registry_t** reg);
  *   "dyn_ag"              2 = the allgather is a (slice, peer) task queue shared
  *                         by the CTAs, 1 = each CTA pulls its own slice index
  *                         after a per-index barrier (default; measured equal)
+ *   "inline_agree"        2 = aggregate's ready-set agreement travels in the fused
+ *                         collective's start-barrier records (default), 1 = a
+ *                         separate LL agreement kernel gates the collective
  * get also reads "staging_bytes", "pool_bytes" and "ll_payload_per_source" */
 int cm_comm_set_param(cm_comm_t* comm, const char* key, int64_t value);
 int cm_comm_get_param(cm_comm_t* comm, const char* key, int64_t* value);

@@ -75,6 +75,7 @@ struct cm_comm {
   int bulk_copy = 0;                          // fusion pack through the TMA bulk-copy engine (opt-in)
   int bulk_rs = 6;                            // reduce phase: bulk-engine stages in smem (0: SM loads)
   int dyn_ag = 0;                             // allgather as a shared (slice, peer) task queue (opt-in)
+  int inline_agree = 1;                       // aggregate's agreement inside the collective's records
   int64_t oneshot_bytes_per_cta = 8 * 1024;
   int64_t twoshot_bytes_per_cta = 4 * 1024;
   int max_ctas = 148;
@@ -228,6 +229,10 @@ struct Launch {
   unsigned long long* done_flag = nullptr;
   unsigned long long done_value = 0;
   unsigned long long agree_gate = 0;  // run only if agreement check `agree_gate` succeeded
+  int agree_inline = 0;               // agreement values travel in the start-barrier records
+  long long akey = 0, acnt = 0;
+  unsigned long long* agree_out = nullptr;
+  unsigned long long agree_ticket = 0;
   int ll = 0;                       // one-shot through the LL slots
   const void* in[MAXP] = {};
   void* out[MAXP] = {};
@@ -307,6 +312,11 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
   P.done_flag = L.done_flag;
   P.done_value = L.done_value;
   P.agree_gate = L.agree_gate;
+  P.agree_inline = L.agree_inline;
+  P.akey = L.akey;
+  P.acnt = L.acnt;
+  P.agree_out = L.agree_out;
+  P.agree_ticket = L.agree_ticket;
   P.dyn_ag = c->dyn_ag;
   P.trace = c->trace;
   P.trace_ctas = c->trace_ctas;
@@ -346,7 +356,7 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
                          L.phases == (PH_RS | PH_AG) &&
                          c->stream_chunk > 0 && maxseg / std::max<int64_t>(nb, 1) >= 2 * c->stream_chunk;
   P.stream_chunk = c->stream_chunk;
-  if (L.agree_gate && (logp || ll != 0))
+  if ((L.agree_gate || L.agree_inline) && (logp || ll != 0))
     return fail(CM_ERR_CONFIG, "internal: agreement gate needs the pull collective kernel");
   KFn k = pick(logp ? K_RHD : ll == 1 ? K_LL : ll == 2 ? K_LL2 : pipelined ? K_STREAM : K_COLL, L.dtype, L.op, p,
                tree);
@@ -941,6 +951,7 @@ int cm_comm_set_param(cm_comm_t* c, const char* key, int64_t value) {
   else if (k == "bulk_copy") c->bulk_copy = value > 1 ? 1 : 0;
   else if (k == "bulk_rs") c->bulk_rs = value == 1 ? 0 : (int)std::min<int64_t>(value, RS_MAX_STAGES);
   else if (k == "dyn_ag") c->dyn_ag = value > 1 ? 1 : 0;
+  else if (k == "inline_agree") c->inline_agree = value > 1 ? 1 : 0;
   else if (k == "oneshot_bytes_per_cta") c->oneshot_bytes_per_cta = value;
   else if (k == "twoshot_bytes_per_cta") c->twoshot_bytes_per_cta = value;
   else if (k == "max_ctas") c->max_ctas = (int)std::min<int64_t>(value, MAXBLK);
@@ -961,6 +972,7 @@ int cm_comm_get_param(cm_comm_t* c, const char* key, int64_t* value) {
   else if (k == "bulk_copy") *value = c->bulk_copy ? 2 : 1;
   else if (k == "bulk_rs") *value = c->bulk_rs ? c->bulk_rs : 1;
   else if (k == "dyn_ag") *value = c->dyn_ag ? 2 : 1;
+  else if (k == "inline_agree") *value = c->inline_agree ? 2 : 1;
   else if (k == "oneshot_bytes_per_cta") *value = c->oneshot_bytes_per_cta;
   else if (k == "twoshot_bytes_per_cta") *value = c->twoshot_bytes_per_cta;
   else if (k == "max_ctas") *value = c->max_ctas;
@@ -1087,13 +1099,38 @@ int cm_comm_poll(cm_comm_t* c) { return check_async_error(c); }
 namespace {
 // launch half of cm_agree: values travel in the kernel parameters, the result
 // lands in mapped host memory with a completion ticket
-int agree_launch(cm_comm* c, const int64_t* values, int n, cudaStream_t stream,
-                 unsigned long long* ticket_out) {
+int ensure_agree_buf(cm_comm* c) {
   if (!c->agree_host) {
     CUDA_TRY(cudaHostAlloc(&c->agree_host, 16 * sizeof(int64_t), cudaHostAllocMapped));
     CUDA_TRY(cudaHostGetDevicePointer((void**)&c->agree_dev, c->agree_host, 0));
     memset(c->agree_host, 0, 16 * sizeof(int64_t));
   }
+  return CM_OK;
+}
+
+// inline agreement: CTA 0 of the first collective writes {ticket, ok} to
+// agree_host[12..13] right after its start barrier
+int inline_agree_wait(cm_comm* c, unsigned long long ticket, cudaStream_t stream, int* agreed) {
+  volatile unsigned long long* flag = reinterpret_cast<volatile unsigned long long*>(c->agree_host + 12);
+  const auto t0 = std::chrono::steady_clock::now();
+  while (*flag != ticket) {
+    if (*reinterpret_cast<volatile unsigned*>(c->herr_host)) break;
+    if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(60)) {
+      cudaError_t e = cudaStreamQuery(stream);
+      if (e != cudaErrorNotReady && e != cudaSuccess) return cuda_fail(e, "aggregate agreement");
+      return fail(CM_ERR_TRANSPORT, "aggregate agreement: peers did not answer within 60 s");
+    }
+  }
+  int st = check_async_error(c);
+  if (st) return st;
+  *agreed = reinterpret_cast<volatile unsigned long long*>(c->agree_host)[13] ? 1 : 0;
+  return CM_OK;
+}
+
+int agree_launch(cm_comm* c, const int64_t* values, int n, cudaStream_t stream,
+                 unsigned long long* ticket_out) {
+  int st0 = ensure_agree_buf(c);
+  if (st0) return st0;
   long long inl[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   for (int i = 0; i < n; ++i) inl[i] = values[i];
   const unsigned long long ticket = ++c->agree_ticket;
@@ -1266,19 +1303,42 @@ int cm_fused_allreduce_agreed(cm_comm_t* c, int n, const void* const* sends,
   // launched only once agreement is known.
   int64_t agree_vals[8];
   unsigned long long ticket = 0;
-  bool pending = false;
-  if (n_agree > 0) {
-    if (n_agree > 4) return fail(CM_ERR_VALUE, "at most 4 agreement values");
-    if (c->size > 1) {
-      for (int i = 0; i < n_agree; ++i) { agree_vals[i] = agree_values[i]; agree_vals[n_agree + i] = -agree_values[i]; }
-      if ((st = agree_launch(c, agree_vals, 2 * n_agree, stream, &ticket))) return st;
-      pending = true;
+  bool pending = false, inline_agree = false;
+  if (n_agree > 4) return fail(CM_ERR_VALUE, "at most 4 agreement values");
+  if (n_agree > 0) *agreed = 1;
+  // started after the plan is known (below): either inline in the collectives'
+  // records, or as a separate LL check kernel when a group takes an LL kernel
+  auto start_agree = [&](bool all_pull) -> int {
+    if (n_agree <= 0 || c->size == 1) return CM_OK;
+    if (all_pull && n_agree == 2 && !c->rhd_logp && c->inline_agree) {
+      int s2 = ensure_agree_buf(c);
+      if (s2) return s2;
+      ticket = ++c->agree_ticket;
+      inline_agree = pending = true;
+      return CM_OK;
     }
-    *agreed = 1;
-  }
+    for (int i = 0; i < n_agree; ++i) { agree_vals[i] = agree_values[i]; agree_vals[n_agree + i] = -agree_values[i]; }
+    int s2 = agree_launch(c, agree_vals, 2 * n_agree, stream, &ticket);
+    if (s2) return s2;
+    pending = true;
+    return CM_OK;
+  };
+  auto tag_launch = [&](Launch& L) {
+    if (!inline_agree) return;
+    L.agree_inline = 1;
+    L.akey = agree_values[0];
+    L.acnt = agree_values[1];
+    L.agree_out = reinterpret_cast<unsigned long long*>(c->agree_dev + 12);
+    L.agree_ticket = ticket;
+  };
   auto resolve_agree = [&]() -> int {
     if (!pending) return CM_OK;
     pending = false;
+    if (inline_agree) {
+      int s2 = inline_agree_wait(c, ticket, stream, agreed);
+      inline_agree = false;
+      return s2;
+    }
     int64_t mx[8];
     int s2 = agree_wait(c, ticket, 2 * n_agree, mx, stream);
     if (s2) return s2;
@@ -1408,6 +1468,11 @@ int cm_fused_allreduce_agreed(cm_comm_t* c, int n, const void* const* sends,
       i = j;
     }
   }
+  {
+    bool all_pull = true;
+    for (const Grp& G : gr) all_pull = all_pull && G.L.ll == 0;
+    if ((st = start_agree(all_pull))) return st;
+  }
   // host-input groups: every group's H2D is queued up front on the h2d stream
   // (into indev at the group's fused offset); each collective waits only for
   // its own group's event
@@ -1487,7 +1552,8 @@ int cm_fused_allreduce_agreed(cm_comm_t* c, int n, const void* const* sends,
       L.gsig = sig;
       L.srcmode = SRC_GATHER;
       L.n = L.bn[0];
-      L.agree_gate = pending ? ticket : 0;   // device-side gate: no host wait before the launch
+      L.agree_gate = (pending && !inline_agree) ? ticket : 0;   // device-side gate: no host wait
+      tag_launch(L);
       if ((st = launch_collective(c, L, stream))) return st;
       if ((st = drain(g, h))) return st;
       g = h;
@@ -1520,7 +1586,8 @@ int cm_fused_allreduce_agreed(cm_comm_t* c, int n, const void* const* sends,
         return st;
       L.srcmode = SRC_PRESTAGED;
       L.n = L.bn[0];
-      L.agree_gate = pending ? ticket : 0;   // the queued pack only touched local staging
+      L.agree_gate = (pending && !inline_agree) ? ticket : 0;   // the pack only touched local staging
+      tag_launch(L);
       if ((st = launch_collective(c, L, stream))) return st;
       if ((st = drain(g, h))) return st;
       g = h;
@@ -1551,7 +1618,8 @@ int cm_fused_allreduce_agreed(cm_comm_t* c, int n, const void* const* sends,
       if ((st = resolve_agree())) return st;
       if (!*agreed) return CM_OK;
     } else {
-      L.agree_gate = pending ? ticket : 0;
+      L.agree_gate = (pending && !inline_agree) ? ticket : 0;
+      tag_launch(L);
     }
     if ((st = launch_collective(c, L, stream))) return st;
     if ((st = drain(g, g + 1))) return st;

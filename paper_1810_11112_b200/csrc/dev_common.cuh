@@ -45,7 +45,7 @@ constexpr int MAXBUF = 4;        // fused buffers per multi-buffer launch
 // ---- heap layout (identical on every rank) ---------------------------------
 constexpr size_t CTRL_OFF = 0;
 constexpr size_t REC_OFF = 4096;
-constexpr size_t REC_BYTES = 32;
+constexpr size_t REC_BYTES = 64;
 constexpr size_t REC_SIZE = 2ull * MAXBLK * MAXP * REC_BYTES;
 constexpr size_t MID_OFF = REC_OFF + REC_SIZE;
 constexpr size_t MID_SIZE = (size_t)MAXBLK * MAXP * 8;
@@ -87,6 +87,9 @@ struct Rec {
   unsigned long long hdr;
   long long srcoff;  // element i of the sender's input at heap + srcoff + i*sz
   long long redoff;  // element i of the sender's segment at heap + redoff + (i-seg_off)*sz
+  long long akey;    // inline agreement (aggregate's ready-set hash and count)
+  long long acnt;
+  long long pad[2];
 };
 
 enum SrcMode { SRC_COPYIN = 0, SRC_PRESTAGED = 1, SRC_ZEROCOPY = 2, SRC_INLINE = 3, SRC_REGISTERED = 4,
@@ -145,6 +148,13 @@ struct CollParams {
   // >0: run only if the agreement check with this ticket (queued before on the
   // same stream) succeeded; otherwise every rank skips the call identically
   unsigned long long agree_gate;
+  // inline agreement: every rank publishes {akey, acnt} in its records; if any
+  // peer's differ, every rank skips the call identically and CTA 0 reports
+  // it through agree_out = {ok, ticket} (host-mapped)
+  int agree_inline;
+  long long akey, acnt;
+  unsigned long long* agree_out;
+  unsigned long long agree_ticket;
   int dyn_ag;                // allgather as a queue of (slice, peer) tasks shared by the CTAs
 };
 

@@ -262,6 +262,10 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
     st_relaxed_sys(&r->hdr, P.hdr);
     st_relaxed_sys_s64(&r->srcoff, my_srcoff);
     st_relaxed_sys_s64(&r->redoff, my_redoff);
+    if (P.agree_inline) {
+      st_relaxed_sys_s64(&r->akey, P.akey);
+      st_relaxed_sys_s64(&r->acnt, P.acnt);
+    }
     st_release_sys(&r->epoch, e);
   }
   if (tid < p && !s_skip) {
@@ -269,6 +273,8 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
     if (!wait_geq(&r->epoch, e, P.timeout_cycles)) {
       atomicExch(&s_err, ERR_TRANSPORT);
     } else {
+      if (P.agree_inline && (ld_relaxed_sys_s64(&r->akey) != P.akey || ld_relaxed_sys_s64(&r->acnt) != P.acnt))
+        atomicExch(&s_skip, 2);            // ready sets differ: nobody moves data
       if (ld_relaxed_sys(&r->hdr) != P.hdr) atomicExch(&s_err, ERR_SHAPE);
       const long long so = ld_relaxed_sys_s64(&r->srcoff);
       if ((unsigned long long)so & REG_FLAG) {   // peer's registered buffer, mapped here
@@ -282,6 +288,20 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
     }
   }
   __syncthreads();                       // s_src / s_red / s_err complete
+  if (P.agree_inline && s_err != ERR_TRANSPORT) {
+    // every rank compared every peer: a disagreement is seen by all ranks, so
+    // all skip; the plans (and headers) of disagreeing ranks may differ, which
+    // is then not an error
+    const bool agreed = s_skip != 2;
+    __syncthreads();
+    if (tid == 0 && !agreed) s_err = 0;
+    if (tid == 0 && b == 0 && P.agree_out) {
+      reinterpret_cast<volatile unsigned long long*>(P.agree_out)[1] = agreed ? 1ull : 0ull;
+      __threadfence_system();
+      reinterpret_cast<volatile unsigned long long*>(P.agree_out)[0] = P.agree_ticket;
+    }
+    __syncthreads();
+  }
   // fold sequence of my segment's sources (reference order)
   if (tid == 0 && (P.phases & PH_RS)) {
     int m = 1;
