@@ -76,6 +76,7 @@ struct cm_comm {
   int bulk_rs = 6;                            // reduce phase: bulk-engine stages in smem (0: SM loads)
   int dyn_ag = 0;                             // allgather as a shared (slice, peer) task queue (opt-in)
   int inline_agree = 1;                       // aggregate's agreement inside the collective's records
+  int bulk_local = 0;                         // reduce: own source loaded directly (opt-in; measured slower)
   int64_t oneshot_bytes_per_cta = 8 * 1024;
   int64_t twoshot_bytes_per_cta = 4 * 1024;
   int max_ctas = 148;
@@ -318,6 +319,7 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
   P.agree_out = L.agree_out;
   P.agree_ticket = L.agree_ticket;
   P.dyn_ag = c->dyn_ag;
+  P.bulk_local = c->bulk_local;
   P.trace = c->trace;
   P.trace_ctas = c->trace_ctas;
 
@@ -952,6 +954,7 @@ int cm_comm_set_param(cm_comm_t* c, const char* key, int64_t value) {
   else if (k == "bulk_rs") c->bulk_rs = value == 1 ? 0 : (int)std::min<int64_t>(value, RS_MAX_STAGES);
   else if (k == "dyn_ag") c->dyn_ag = value > 1 ? 1 : 0;
   else if (k == "inline_agree") c->inline_agree = value > 1 ? 1 : 0;
+  else if (k == "bulk_local") c->bulk_local = value > 1 ? 1 : 0;
   else if (k == "oneshot_bytes_per_cta") c->oneshot_bytes_per_cta = value;
   else if (k == "twoshot_bytes_per_cta") c->twoshot_bytes_per_cta = value;
   else if (k == "max_ctas") c->max_ctas = (int)std::min<int64_t>(value, MAXBLK);
@@ -973,6 +976,7 @@ int cm_comm_get_param(cm_comm_t* c, const char* key, int64_t* value) {
   else if (k == "bulk_rs") *value = c->bulk_rs ? c->bulk_rs : 1;
   else if (k == "dyn_ag") *value = c->dyn_ag ? 2 : 1;
   else if (k == "inline_agree") *value = c->inline_agree ? 2 : 1;
+  else if (k == "bulk_local") *value = c->bulk_local ? 2 : 1;
   else if (k == "oneshot_bytes_per_cta") *value = c->oneshot_bytes_per_cta;
   else if (k == "twoshot_bytes_per_cta") *value = c->twoshot_bytes_per_cta;
   else if (k == "max_ctas") *value = c->max_ctas;

@@ -145,6 +145,7 @@ struct CollParams {
   unsigned long long* done_flag;  // optional: written with done_value when the call completes
   unsigned long long done_value;
   int bulk_rs;               // >0: reduce through the bulk-copy engine with this many smem stages
+  int bulk_local;            // the reduce's own-rank source is loaded directly, not staged
   // >0: run only if the agreement check with this ticket (queued before on the
   // same stream) succeeded; otherwise every rank skips the call identically
   unsigned long long agree_gate;
@@ -565,7 +566,9 @@ __device__ __forceinline__ BulkRS bulk_rs_setup(unsigned char* dyn, int stages, 
 template <class D, int OP, int MP, bool TREE>
 __device__ void reduce_range_bulk(const BulkRS& B, const char* const* seq, int p, int m, int excess,
                                   long long lo, long long hi, int average, char* out, long long out_shift,
-                                  char* red, long long red_shift, int tid) {
+                                  char* red, long long red_shift, int tid, int local_k = -1) {
+  // local_k >= 0: source local_k is this rank's own (HBM) buffer; the
+  // consumers load it directly, so every stage byte carries NVLink traffic
   using S = typename D::S;
   using A = typename D::A;
   constexpr int W = 16 / sizeof(S);
@@ -578,7 +581,8 @@ __device__ void reduce_range_bulk(const BulkRS& B, const char* const* seq, int p
     reduce_one<D, OP, MP, 1, TREE>(seq, p, m, excess, i, average, out, out_shift, red, red_shift);
   const long long nbytes = (body_hi - body_lo) * SZ;
   if (nbytes <= 0) return;
-  const int ch = (RS_STAGE_BYTES / p) & ~15;            // bytes per source per stage
+  const int nstaged = local_k >= 0 ? p - 1 : p;
+  const int ch = (RS_STAGE_BYTES / nstaged) & ~15;      // bytes per staged source per stage
   const long long C = (nbytes + ch - 1) / ch;
   const unsigned long long base = *B.seqno;
   if (tid == RS_CONSUMERS) {                            // producer: warp 15, lane 0
@@ -590,14 +594,17 @@ __device__ void reduce_range_bulk(const BulkRS& B, const char* const* seq, int p
       const long long off = body_lo * SZ + c * ch;
       const int len = (int)((nbytes - c * ch) < ch ? (nbytes - c * ch) : ch);
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&B.full[s])),
-                   "r"(len * p)
+                   "r"(len * nstaged)
                    : "memory");
-      for (int k = 0; k < p; ++k)
+      for (int k = 0; k < p; ++k) {
+        if (k == local_k) continue;
+        const int slot = (local_k >= 0 && k > local_k) ? k - 1 : k;
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                smem_u32(B.smem + (size_t)s * RS_STAGE_BYTES + (size_t)k * ch)),
+                smem_u32(B.smem + (size_t)s * RS_STAGE_BYTES + (size_t)slot * ch)),
             "l"(seq[k] + off), "r"(len), "r"(smem_u32(&B.full[s]))
             : "memory");
+      }
     }
   } else if (tid < RS_CONSUMERS) {
     for (long long c = 0; c < C; ++c) {
@@ -611,8 +618,15 @@ __device__ void reduce_range_bulk(const BulkRS& B, const char* const* seq, int p
       for (int v = tid; v < nv; v += RS_CONSUMERS) {
         A u[MP][W];
 #pragma unroll
-        for (int k = 0; k < MP; ++k)
-          if (k < p) load_vec<D, W>(st + (size_t)k * ch, (long long)v * W, u[k]);
+        for (int k = 0; k < MP; ++k) {
+          if (k >= p) continue;
+          if (k == local_k) {
+            load_vec<D, W>(seq[k], e0 + (long long)v * W, u[k]);
+          } else {
+            const int slot = (local_k >= 0 && k > local_k) ? k - 1 : k;
+            load_vec<D, W>(st + (size_t)slot * ch, (long long)v * W, u[k]);
+          }
+        }
         fold<OP, MP, W, TREE>(u, p, m, excess);
         if (average) {
 #pragma unroll

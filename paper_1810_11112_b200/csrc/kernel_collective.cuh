@@ -317,6 +317,13 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
     }
     for (int k = 0; k < p; ++k) s_seq[k] = s_src[s_rord[k]];
   }
+  __shared__ int s_localk;
+  if (tid == 0) {
+    s_localk = -1;
+    if (P.bulk_local && (P.phases & PH_RS))
+      for (int k = 0; k < p; ++k)
+        if (s_rord[k] == rank) s_localk = k;
+  }
   __syncthreads();
   CM_TRACE(P, lr, b, 2);
   if (s_err || s_skip) goto finish;
@@ -353,7 +360,8 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
         bool vec = al16(bo) && al16(red);
         for (int q = 0; q < p; ++q) vec = vec && al16(s_seqk[q]);
         if (P.bulk_rs && vec)
-          reduce_range_bulk<D, OP, MP, TREE>(BR, s_seqk, p, m, excess, lo, hi, P.average, bo, 0, red, 0, tid);
+          reduce_range_bulk<D, OP, MP, TREE>(BR, s_seqk, p, m, excess, lo, hi, P.average, bo, 0, red, 0, tid,
+                                             s_localk);
         else
           reduce_range<D, OP, MP, TREE>(s_seqk, p, m, excess, lo, hi, vec, P.average, bo, 0, red, 0,
                                         tid, blockDim.x);
@@ -388,7 +396,8 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
         bool vec = al16(bo) && al16(red);
         for (int q = 0; q < p; ++q) vec = vec && al16(s_seqk[q]);
         if (P.bulk_rs && vec)
-          reduce_range_bulk<D, OP, MP, TREE>(BR, s_seqk, p, m, excess, i, pe, P.average, bo, 0, red, 0, tid);
+          reduce_range_bulk<D, OP, MP, TREE>(BR, s_seqk, p, m, excess, i, pe, P.average, bo, 0, red, 0, tid,
+                                             s_localk);
         else
           reduce_range<D, OP, MP, TREE>(s_seqk, p, m, excess, i, pe, vec, P.average, bo, 0, red, 0,
                                         tid, blockDim.x);
@@ -444,7 +453,7 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
     const long long lo = slice_bound(so, sl, b, nb), hi = slice_bound(so, sl, b + 1, nb);
     if (P.bulk_rs && vec)
       reduce_range_bulk<D, OP, MP, TREE>(BR, s_seq, p, m, excess, lo, hi, P.average, out, out_shift, red,
-                                         red_shift, tid);
+                                         red_shift, tid, s_localk);
     else
       reduce_range<D, OP, MP, TREE>(s_seq, p, m, excess, lo, hi, vec, P.average, out, out_shift,
                                     red, red_shift, tid, blockDim.x);
