@@ -77,6 +77,7 @@ struct cm_comm {
   int dyn_ag = 0;                             // allgather as a shared (slice, peer) task queue (opt-in)
   int inline_agree = 1;                       // aggregate's agreement inside the collective's records
   int bulk_local = 0;                         // reduce: own source loaded directly (opt-in; measured slower)
+  int bulk_stage = 2 * RS_STAGE_BYTES;        // bytes per bulk-reduce stage (64 KiB: 3 stages fit)
   int64_t oneshot_bytes_per_cta = 8 * 1024;
   int64_t twoshot_bytes_per_cta = 4 * 1024;
   int max_ctas = 148;
@@ -365,16 +366,23 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
   if (!k) return fail(CM_ERR_SHAPE, "unsupported dtype");
   // reduce phase through the bulk-copy engine (shared-memory stage ring)
   const bool bulk = c->bulk_rs > 0 && !logp && ll == 0 && !pipelined && (L.phases & PH_RS);
-  P.bulk_rs = bulk ? c->bulk_rs : 0;
-  const size_t dsm = bulk ? rs_smem_bytes(c->bulk_rs) : 0;
-  if (bulk) {
-    static std::set<const void*> configured;
-    if (!configured.count((const void*)k)) {
-      CUDA_TRY(cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)rs_smem_bytes(RS_MAX_STAGES)));
-      configured.insert((const void*)k);
-    }
+  // dynamic shared memory available next to the kernel's static arrays
+  static std::map<const void*, int> max_dyn;
+  if (bulk && !max_dyn.count((const void*)k)) {
+    int optin = 0;
+    CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
+    cudaFuncAttributes fa;
+    CUDA_TRY(cudaFuncGetAttributes(&fa, (const void*)k));
+    const int avail = optin - (int)fa.sharedSizeBytes;
+    CUDA_TRY(cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, avail));
+    max_dyn[(const void*)k] = avail;
   }
+  int stages = c->bulk_rs;
+  if (bulk)
+    while (stages > 1 && rs_smem_bytes(stages, c->bulk_stage) > (size_t)max_dyn[(const void*)k]) --stages;
+  P.bulk_rs = bulk ? stages : 0;
+  P.bulk_stage = c->bulk_stage;
+  const size_t dsm = bulk ? rs_smem_bytes(stages, c->bulk_stage) : 0;
   void* args[] = {&P};
   int64_t alg = 0;   // busBW bytes of this launch (nccl-tests convention)
   int64_t ntot = L.n;
@@ -955,6 +963,7 @@ int cm_comm_set_param(cm_comm_t* c, const char* key, int64_t value) {
   else if (k == "dyn_ag") c->dyn_ag = value > 1 ? 1 : 0;
   else if (k == "inline_agree") c->inline_agree = value > 1 ? 1 : 0;
   else if (k == "bulk_local") c->bulk_local = value > 1 ? 1 : 0;
+  else if (k == "bulk_stage_kb") c->bulk_stage = (int)std::max<int64_t>(4, std::min<int64_t>(value, 112)) * 1024;
   else if (k == "oneshot_bytes_per_cta") c->oneshot_bytes_per_cta = value;
   else if (k == "twoshot_bytes_per_cta") c->twoshot_bytes_per_cta = value;
   else if (k == "max_ctas") c->max_ctas = (int)std::min<int64_t>(value, MAXBLK);
@@ -977,6 +986,7 @@ int cm_comm_get_param(cm_comm_t* c, const char* key, int64_t* value) {
   else if (k == "dyn_ag") *value = c->dyn_ag ? 2 : 1;
   else if (k == "inline_agree") *value = c->inline_agree ? 2 : 1;
   else if (k == "bulk_local") *value = c->bulk_local ? 2 : 1;
+  else if (k == "bulk_stage_kb") *value = c->bulk_stage / 1024;
   else if (k == "oneshot_bytes_per_cta") *value = c->oneshot_bytes_per_cta;
   else if (k == "twoshot_bytes_per_cta") *value = c->twoshot_bytes_per_cta;
   else if (k == "max_ctas") *value = c->max_ctas;

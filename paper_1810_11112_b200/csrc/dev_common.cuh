@@ -146,6 +146,7 @@ struct CollParams {
   unsigned long long done_value;
   int bulk_rs;               // >0: reduce through the bulk-copy engine with this many smem stages
   int bulk_local;            // the reduce's own-rank source is loaded directly, not staged
+  int bulk_stage;            // bytes per shared-memory stage of the bulk reduce
   // >0: run only if the agreement check with this ticket (queued before on the
   // same stream) succeeded; otherwise every rank skips the call identically
   unsigned long long agree_gate;
@@ -530,25 +531,27 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
 // each stage (sources in the reference order) and write out / staging; each
 // warp then arrives on the stage's `empty` mbarrier so the producer can refill.
 constexpr int RS_MAX_STAGES = 6;
-constexpr int RS_STAGE_BYTES = 32768;
+constexpr int RS_STAGE_BYTES = 32768;         // default stage size (knob bulk_stage_kb)
 constexpr int RS_CONSUMERS = THREADS - 32;
-__host__ __device__ constexpr size_t rs_smem_bytes(int stages) {
-  return (size_t)stages * RS_STAGE_BYTES + (2 * (size_t)stages + 2) * 8;
+__host__ __device__ constexpr size_t rs_smem_bytes(int stages, int stage_bytes = RS_STAGE_BYTES) {
+  return (size_t)stages * stage_bytes + (2 * (size_t)stages + 2) * 8;
 }
 
 struct BulkRS {
-  unsigned char* smem;        // stages x RS_STAGE_BYTES
+  unsigned char* smem;        // stages x stage_bytes
   unsigned long long* full;   // [stages], 1 arrival + tx bytes
   unsigned long long* empty;  // [stages], RS_CONSUMERS / 32 arrivals
   unsigned long long* seqno;  // stage uses so far in this launch
   int stages;
+  int stage_bytes;
 };
 
-__device__ __forceinline__ BulkRS bulk_rs_setup(unsigned char* dyn, int stages, int tid) {
+__device__ __forceinline__ BulkRS bulk_rs_setup(unsigned char* dyn, int stages, int stage_bytes, int tid) {
   BulkRS B;
   B.stages = stages;
+  B.stage_bytes = stage_bytes;
   B.smem = dyn;
-  B.full = reinterpret_cast<unsigned long long*>(dyn + (size_t)stages * RS_STAGE_BYTES);
+  B.full = reinterpret_cast<unsigned long long*>(dyn + (size_t)stages * stage_bytes);
   B.empty = B.full + stages;
   B.seqno = B.empty + stages;
   if (tid == 0) {
@@ -582,7 +585,7 @@ __device__ void reduce_range_bulk(const BulkRS& B, const char* const* seq, int p
   const long long nbytes = (body_hi - body_lo) * SZ;
   if (nbytes <= 0) return;
   const int nstaged = local_k >= 0 ? p - 1 : p;
-  const int ch = (RS_STAGE_BYTES / nstaged) & ~15;      // bytes per staged source per stage
+  const int ch = (B.stage_bytes / nstaged) & ~15;       // bytes per staged source per stage
   const long long C = (nbytes + ch - 1) / ch;
   const unsigned long long base = *B.seqno;
   if (tid == RS_CONSUMERS) {                            // producer: warp 15, lane 0
@@ -601,7 +604,7 @@ __device__ void reduce_range_bulk(const BulkRS& B, const char* const* seq, int p
         const int slot = (local_k >= 0 && k > local_k) ? k - 1 : k;
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                smem_u32(B.smem + (size_t)s * RS_STAGE_BYTES + (size_t)slot * ch)),
+                smem_u32(B.smem + (size_t)s * B.stage_bytes + (size_t)slot * ch)),
             "l"(seq[k] + off), "r"(len), "r"(smem_u32(&B.full[s]))
             : "memory");
       }
@@ -613,7 +616,7 @@ __device__ void reduce_range_bulk(const BulkRS& B, const char* const* seq, int p
       mbar_wait(&B.full[s], (unsigned)((g / B.stages) & 1));
       const int len = (int)((nbytes - c * ch) < ch ? (nbytes - c * ch) : ch);
       const int nv = len / 16;
-      const char* st = reinterpret_cast<const char*>(B.smem + (size_t)s * RS_STAGE_BYTES);
+      const char* st = reinterpret_cast<const char*>(B.smem + (size_t)s * B.stage_bytes);
       const long long e0 = body_lo + c * (ch / SZ);
       for (int v = tid; v < nv; v += RS_CONSUMERS) {
         A u[MP][W];

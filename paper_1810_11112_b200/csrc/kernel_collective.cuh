@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
   extern __shared__ __align__(128) unsigned char coll_dyn[];
   CM_TRACE(P, lr, b, 0);
   BulkRS BR{};
-  if (!STREAM && P.bulk_rs) BR = bulk_rs_setup(coll_dyn, P.bulk_rs, tid);
+  if (!STREAM && P.bulk_rs) BR = bulk_rs_setup(coll_dyn, P.bulk_rs, P.bulk_stage, tid);
   if (tid == 0) {
     s_epoch = ctrl->epoch + 1;
     s_err = 0;
