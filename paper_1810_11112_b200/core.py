@@ -117,13 +117,6 @@ class Tensor:
         return Tensor(self.name, self.dtype, values)
 
 
-def dtype_of(t: torch.Tensor) -> str:
-    try:
-        return _TORCH_NAME[t.dtype]
-    except KeyError:
-        raise ShapeError(f"unsupported dtype {t.dtype}") from None
-
-
 @dataclass(frozen=True)
 class GroupSpec:
     """A process group of ``size`` ranks numbered densely 0..size-1 (core.py:73-91)."""
