@@ -6,6 +6,18 @@
 //   pointer cache (no driver query on a cache hit, PAPER §V-B) -> pick the
 //   source mode (zero-copy from the symmetric pool, copy-in, or host staging)
 //   -> ONE kernel launch (one-shot or two-shot) -> logical CollectiveStats.
+//
+// Sections:
+//   struct cm_comm                      per-rank state (heap, staging, knobs, counters)
+//   launch_collective / plan_algo       grid sizing, kernel choice, parameters
+//   place / do_allreduce / do_rs / do_ag  buffer placement and the single collectives
+//   launch_batched_copy / coalesce / HostPipe   packs and the host-gradient pipeline
+//   cm_comm_* (extern "C")              lifecycle, IPC bootstrap, registration, knobs
+//   agreement helpers, cm_agree         ready-set agreement (LL kernel / inline)
+//   cm_allreduce..cm_allgather_v        the C ABI of the collectives
+//   cm_fused_allreduce_agreed           aggregate(): plan, agreement, launches, pipeline
+//   cm_ps_step(_v)                      parameter-server step
+//   cm_local_reduce, cm_batched_copy, cm_bench_p2p, cm_time_allreduce
 #include <cuda.h>
 #include <cuda_runtime.h>
 
