@@ -81,7 +81,8 @@ for it in range(a.iters + 3):
         col = t[:, k][t[:, k] > 0]
         skew[k] += float(col.max() - t[:, 0].min()) / 1e3 if len(col) else 0.0
 if rank == 0:
-    print(f"p={world} bytes={a.bytes} algo={a.algo} zc={a.zc} ctas={int(used.sum())} "
+    what = "C5 aggregate (registered, 2 fused groups)" if a.agg else f"bytes={a.bytes} algo={a.algo} zc={a.zc}"
+    print(f"p={world} {what} ctas={int(used.sum())} "
           f"kernel span {tot / a.iters:.2f} us | " +
           " ".join(f"{ph} {v / a.iters:.2f}" for ph, v in zip(phases, acc)) +
           " | last CTA past stamp k (from first start): " + " ".join(f"{v / a.iters:.1f}" for v in skew),
