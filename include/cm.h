@@ -172,6 +172,8 @@ int cm_comm_registry(cm_comm_t* comm, cm_registry_t** reg);
  *   "dyn_ag"              2 = the allgather is a (slice, peer) task queue shared
  *                         by the CTAs, 1 = each CTA pulls its own slice index
  *                         after a per-index barrier (default; measured equal)
+ *   "host_chunk_kb"       KiB per H2D/D2H piece of the single-rank host-gradient
+ *                         pipeline (default 8192; 2048/4096/16384 measured slower)
  *   "bulk_stage_kb"       KiB per bulk-reduce stage (default 64; the stage count
  *                         is clamped to the shared memory available)
  *   "bulk_local"          2 = the reduce loads its own rank's source directly and

@@ -90,6 +90,7 @@ struct cm_comm {
   int inline_agree = 1;                       // aggregate's agreement inside the collective's records
   int bulk_local = 0;                         // reduce: own source loaded directly (opt-in; measured slower)
   int bulk_stage = 2 * RS_STAGE_BYTES;        // bytes per bulk-reduce stage (64 KiB: 3 stages fit)
+  int64_t host_chunk = 8 << 20;               // host-gradient pipeline: bytes per H2D/D2H piece (p = 1)
   int64_t oneshot_bytes_per_cta = 8 * 1024;
   int64_t twoshot_bytes_per_cta = 4 * 1024;
   int max_ctas = 148;
@@ -975,6 +976,7 @@ int cm_comm_set_param(cm_comm_t* c, const char* key, int64_t value) {
   else if (k == "dyn_ag") c->dyn_ag = value > 1 ? 1 : 0;
   else if (k == "inline_agree") c->inline_agree = value > 1 ? 1 : 0;
   else if (k == "bulk_local") c->bulk_local = value > 1 ? 1 : 0;
+  else if (k == "host_chunk_kb") c->host_chunk = std::max<int64_t>(64, value) * 1024;
   else if (k == "bulk_stage_kb") c->bulk_stage = (int)std::max<int64_t>(4, std::min<int64_t>(value, 112)) * 1024;
   else if (k == "oneshot_bytes_per_cta") c->oneshot_bytes_per_cta = value;
   else if (k == "twoshot_bytes_per_cta") c->twoshot_bytes_per_cta = value;
@@ -999,6 +1001,7 @@ int cm_comm_get_param(cm_comm_t* c, const char* key, int64_t* value) {
   else if (k == "inline_agree") *value = c->inline_agree ? 2 : 1;
   else if (k == "bulk_local") *value = c->bulk_local ? 2 : 1;
   else if (k == "bulk_stage_kb") *value = c->bulk_stage / 1024;
+  else if (k == "host_chunk_kb") *value = c->host_chunk / 1024;
   else if (k == "oneshot_bytes_per_cta") *value = c->oneshot_bytes_per_cta;
   else if (k == "twoshot_bytes_per_cta") *value = c->twoshot_bytes_per_cta;
   else if (k == "max_ctas") *value = c->max_ctas;
@@ -1416,14 +1419,14 @@ int cm_fused_allreduce_agreed(cm_comm_t* c, int n, const void* const* sends,
       // members adjacent in memory are copied as one run (one DMA), runs are
       // cut into 16 MiB pieces, and the fused result (contiguous) leaves in
       // one D2H per piece
-      std::vector<Run> runs = coalesce(srcs.data(), bytes.data(), n, 16 << 20);
+      std::vector<Run> runs = coalesce(srcs.data(), bytes.data(), n, c->host_chunk);
       int64_t chunk_lo = 0;
       for (size_t k = 0; k < runs.size(); ++k) {
         const Run& r = runs[k];
         CUDA_TRY(cudaMemcpyAsync((out_host ? c->indev : static_cast<char*>(recv_fused)) + r.off, r.src, r.bytes,
                                  cudaMemcpyDefault, c->h2d));
         const int64_t end = r.off + r.bytes;
-        if (out_host && (end - chunk_lo >= (16 << 20) || k + 1 == runs.size())) {
+        if (out_host && (end - chunk_lo >= c->host_chunk || k + 1 == runs.size())) {
           if ((st = hp.link(c->h2d, c->d2h))) return st;
           CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(recv_fused) + chunk_lo, c->indev + chunk_lo, end - chunk_lo,
                                    cudaMemcpyDeviceToHost, c->d2h));
