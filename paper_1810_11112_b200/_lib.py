@@ -13,7 +13,8 @@ import os
 from . import errors as E
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcm.so")
+# CM_LIB selects another build of the same ABI (A/B studies under tools/)
+LIB_PATH = os.environ.get("CM_LIB") or os.path.join(_HERE, "libcm.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

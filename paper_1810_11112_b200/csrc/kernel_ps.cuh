@@ -7,13 +7,15 @@
 //   1. start barrier (per-CTA records, as in collective_kernel)
 //   2. owner phase: CTA b takes slice b of the rank's owned elements; per
 //      element: acc = (double)g_w0 + g_w1 + ... in worker-rank order, read from
-//      every worker's staging over NVLink; mean = acc / W; updated =
+//      every worker's staging over NVLink (PS_U elements per thread in
+//      flight); mean = acc / W; updated =
 //      (T)((double)param - lr * mean) with separately rounded multiply and
 //      subtract (no FMA contraction, as numpy evaluates it). The result goes
 //      to the rank's parameter buffer and to its "served" area (staging +
 //      Gtot elements, same global offsets).
 //   3. per-CTA mid flag, then pull phase (workers): slice b of every other
-//      owner's owned elements is copied from that owner's served area.
+//      owner's owned elements is copied from that owner's served area
+//      (16-byte vectors where the offsets allow).
 #pragma once
 
 #include "dev_common.cuh"
@@ -61,6 +63,8 @@ __device__ __forceinline__ void ps_pieces(const long long* table, int p, int q, 
   }
 }
 
+constexpr int PS_U = 4;
+
 template <class D>
 __global__ void __launch_bounds__(THREADS) ps_kernel(const __grid_constant__ PsParams P) {
   using S = typename D::S;
@@ -107,7 +111,37 @@ __global__ void __launch_bounds__(THREADS) ps_kernel(const __grid_constant__ PsP
     S* served = reinterpret_cast<S*>(myheap + stage_off + P.gtot * SZ);
     const double wcount = (double)P.nworkers;
     ps_pieces(P.table, p, rank, lo, hi, [&](long long g0, long long cnt) {
-      for (long long i = tid; i < cnt; i += THREADS) {
+      // PS_U independent elements per thread (strided by THREADS so every
+      // load stays coalesced): the NVLink loads of one worker are issued
+      // together before the adds; each element keeps its own fold in
+      // worker-rank order, so the result is unchanged.
+      long long i = tid;
+      for (; i + (PS_U - 1) * THREADS < cnt; i += PS_U * THREADS) {
+        const long long g = g0 + i;
+        double acc[PS_U];
+        const S* s0 = reinterpret_cast<const S*>(P.heap[P.workers[0]] + stage_off) + g;
+#pragma unroll
+        for (int u = 0; u < PS_U; ++u) acc[u] = (double)s0[u * THREADS];
+        for (int w = 1; w < P.nworkers; ++w) {
+          const S* sw = reinterpret_cast<const S*>(P.heap[P.workers[w]] + stage_off) + g;
+          S v[PS_U];
+#pragma unroll
+          for (int u = 0; u < PS_U; ++u) v[u] = sw[u * THREADS];
+#pragma unroll
+          for (int u = 0; u < PS_U; ++u) acc[u] = __dadd_rn(acc[u], (double)v[u]);
+        }
+        S pv[PS_U];
+#pragma unroll
+        for (int u = 0; u < PS_U; ++u) pv[u] = prm[g + u * THREADS];
+#pragma unroll
+        for (int u = 0; u < PS_U; ++u) {
+          const double mean = __ddiv_rn(acc[u], wcount);
+          const S v = (S)__dsub_rn((double)pv[u], __dmul_rn(P.lr, mean));
+          prm[g + u * THREADS] = v;
+          served[g + u * THREADS] = v;
+        }
+      }
+      for (; i < cnt; i += THREADS) {
         const long long g = g0 + i;
         double acc = (double)reinterpret_cast<const S*>(P.heap[P.workers[0]] + stage_off)[g];
         for (int w = 1; w < P.nworkers; ++w)
@@ -133,7 +167,25 @@ __global__ void __launch_bounds__(THREADS) ps_kernel(const __grid_constant__ PsP
       const long long lo = slice_bound(0, own, b, nb), hi = slice_bound(0, own, b + 1, nb);
       const S* src = reinterpret_cast<const S*>(P.heap[q] + stage_off + P.gtot * SZ);
       ps_pieces(P.table, p, q, lo, hi, [&](long long g0, long long cnt) {
-        for (long long i = tid; i < cnt; i += THREADS) prm[g0 + i] = src[g0 + i];
+        // served area and parameters share the element offset, so they share
+        // 16-byte alignment: scalar head, uint4 body, scalar tail
+        constexpr long long VE = 16 / SZ;
+        const long long head = ((VE - ((reinterpret_cast<uintptr_t>(prm + g0) & 15) / SZ)) % VE);
+        const bool vec = ((reinterpret_cast<uintptr_t>(src + g0) ^ reinterpret_cast<uintptr_t>(prm + g0)) & 15) == 0;
+        const long long h = vec ? (head < cnt ? head : cnt) : cnt;
+        for (long long i = tid; i < h; i += THREADS) prm[g0 + i] = src[g0 + i];
+        if (vec) {
+          const long long nv = (cnt - h) / VE;
+          const uint4* vs = reinterpret_cast<const uint4*>(src + g0 + h);
+          uint4* vd = reinterpret_cast<uint4*>(prm + g0 + h);
+          long long i = tid;
+          for (; i + 3 * THREADS < nv; i += 4 * THREADS) {
+            const uint4 a = vs[i], b2 = vs[i + THREADS], c = vs[i + 2 * THREADS], d = vs[i + 3 * THREADS];
+            vd[i] = a; vd[i + THREADS] = b2; vd[i + 2 * THREADS] = c; vd[i + 3 * THREADS] = d;
+          }
+          for (; i < nv; i += THREADS) vd[i] = vs[i];
+          for (long long j = h + nv * VE + tid; j < cnt; j += THREADS) prm[g0 + j] = src[g0 + j];
+        }
       });
     }
   }
