@@ -34,6 +34,15 @@ case "$1" in
   overlap)    # overlapped aggregation study (profiles/r01_overlap_n4.txt)
     python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 \
       --master-port 29591 bench.py --gpus 4 --mode overlap --fusion-threshold 16777216 ;;
+  ps)         # parameter-server step: virtual p=2/4/8, real p=2, kernel launch list (profiles/r01_ps_ab.txt)
+    for p in 2 4 8; do python tools/ps_bench.py --p $p; done
+    python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 \
+      --master-port 29533 tools/ps_bench.py
+    ncu --metrics gpu__time_duration.sum --clock-control none -k regex:ps_kernel --csv \
+      --log-file gpurun_out/ps_launches.csv python tools/ps_bench.py --p 4 --iters 3 > /dev/null ;;
+  hostov)     # small-allreduce host submission vs device drain (profiles/r01_host_overhead_p2.txt)
+    python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 \
+      --master-port 29561 tools/host_overhead.py ;;
   pcie)       # host copy ceilings behind the e2e number
     python tools/pcie_bw.py
     python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 \
