@@ -7,7 +7,7 @@
 //   1. start barrier (per-CTA records, as in collective_kernel)
 //   2. owner phase: CTA b takes slice b of the rank's owned elements; per
 //      element: acc = (double)g_w0 + g_w1 + ... in worker-rank order, read from
-//      every worker's staging over NVLink (PS_U elements per thread in
+//      every worker's staging over NVLink (PS_U = 8 elements per thread in
 //      flight); mean = acc / W; updated =
 //      (T)((double)param - lr * mean) with separately rounded multiply and
 //      subtract (no FMA contraction, as numpy evaluates it). The result goes
@@ -63,7 +63,7 @@ __device__ __forceinline__ void ps_pieces(const long long* table, int p, int q, 
   }
 }
 
-constexpr int PS_U = 4;
+constexpr int PS_U = 8;
 
 template <class D>
 __global__ void __launch_bounds__(THREADS) ps_kernel(const __grid_constant__ PsParams P) {
