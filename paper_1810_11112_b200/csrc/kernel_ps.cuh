@@ -7,7 +7,7 @@
 //   1. start barrier (per-CTA records, as in collective_kernel)
 //   2. owner phase: CTA b takes slice b of the rank's owned elements; per
 //      element: acc = (double)g_w0 + g_w1 + ... in worker-rank order, read from
-//      every worker's staging over NVLink (PS_U = 8 elements per thread in
+//      every worker's staging over NVLink (PS_U = 8 f32 / 4 f64 elements per thread in
 //      flight); mean = acc / W; updated =
 //      (T)((double)param - lr * mean) with separately rounded multiply and
 //      subtract (no FMA contraction, as numpy evaluates it). The result goes
@@ -63,12 +63,13 @@ __device__ __forceinline__ void ps_pieces(const long long* table, int p, int q, 
   }
 }
 
-constexpr int PS_U = 8;
+
 
 template <class D>
 __global__ void __launch_bounds__(THREADS) ps_kernel(const __grid_constant__ PsParams P) {
   using S = typename D::S;
   constexpr int SZ = sizeof(S);
+  constexpr int PS_U = SZ == 8 ? 4 : 8;   // elements in flight per thread (f64: keeps 2 CTAs/SM)
   const int lr_ = P.virt ? blockIdx.y : 0;
   const int rank = P.virt ? (int)blockIdx.y : P.rank;
   const int b = blockIdx.x, nb = gridDim.x, p = P.p, tid = threadIdx.x;

@@ -28,6 +28,7 @@ def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--p", type=int, default=4)
     ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--dtype", choices=("float32", "float64"), default="float32")
     a = ap.parse_args()
     import numpy as np
     import torch
@@ -37,8 +38,9 @@ def main() -> None:
     n_layers, count = 53, 480_000
     names = [f"layer{i:03d}" for i in range(n_layers)]
     rng = np.random.default_rng(0)
-    params = {nm: rng.standard_normal(count).astype(np.float32) for nm in names}
-    grads = [{nm: rng.standard_normal(count).astype(np.float32) for nm in names} for _ in range(a.p)]
+    params = {nm: rng.standard_normal(count).astype(a.dtype) for nm in names}
+    grads = [{nm: rng.standard_normal(count).astype(a.dtype) for nm in names} for _ in range(a.p)]
+    staging = max(256 << 20, 2 * n_layers * count * np.dtype(a.dtype).itemsize + (8 << 20))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if world > 1:
         import torch.distributed as dist
@@ -46,10 +48,10 @@ def main() -> None:
         torch.cuda.set_device(local)
         dist.init_process_group("gloo")
         a.p = world
-        comm = P.Communicator(staging_bytes=256 << 20, pool_bytes=64 << 20, timeout_s=10.0)
+        comm = P.Communicator(staging_bytes=staging, pool_bytes=64 << 20, timeout_s=10.0)
         topo = P.PsTopology.create(range(world), range(world), names)
-        pt = [P.Tensor(nm, "float32", torch.from_numpy(params[nm]).cuda()) for nm in names]
-        my_g = [P.Tensor(nm, "float32", torch.from_numpy(grads[rank % len(grads)][nm]).cuda()) for nm in names]
+        pt = [P.Tensor(nm, a.dtype, torch.from_numpy(params[nm]).cuda()) for nm in names]
+        my_g = [P.Tensor(nm, a.dtype, torch.from_numpy(grads[rank % len(grads)][nm]).cuda()) for nm in names]
         step = lambda: P.run_ps_step(rank, comm, topo, my_g, pt, 0.1)
         res0 = step()
         for _ in range(2):
@@ -69,10 +71,10 @@ def main() -> None:
         if rank != 0:
             return
     else:
-        vg = P.VirtualGroup(a.p, 0, staging_bytes=256 << 20, timeout_s=10.0)
+        vg = P.VirtualGroup(a.p, 0, staging_bytes=staging, timeout_s=10.0)
         topo = P.PsTopology.create(range(a.p), range(a.p), names)
-        pt = [P.Tensor(nm, "float32", torch.from_numpy(params[nm]).cuda()) for nm in names]
-        gper = [[P.Tensor(nm, "float32", torch.from_numpy(grads[r][nm]).cuda()) for nm in names]
+        pt = [P.Tensor(nm, a.dtype, torch.from_numpy(params[nm]).cuda()) for nm in names]
+        gper = [[P.Tensor(nm, a.dtype, torch.from_numpy(grads[r][nm]).cuda()) for nm in names]
                 for r in range(a.p)]
         res = None
         for _ in range(3):
@@ -87,7 +89,7 @@ def main() -> None:
             ts.append((time.perf_counter() - t0) * 1e3)
         vg.close()
     print(json.dumps({"tool": "ps_bench", "lib": os.path.basename(L.LIB_PATH), "p": a.p, "ranks": "real (one process per GPU)" if world > 1 else "virtual (one GPU)",
-                      "elements": n_layers * count, "ms_per_call_median": round(statistics.median(ts), 4),
+                      "dtype": a.dtype, "elements": n_layers * count, "ms_per_call_median": round(statistics.median(ts), 4),
                       "rank0_params_sha256_16": digest}))
 
 
