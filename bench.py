@@ -224,6 +224,120 @@ def cpu_baseline_sample(model, p, dtype="float32", max_s=20.0):
     return times
 
 
+# ----------------------------------------------------- virtual-group evidence
+def virtual_block(args, local, steps):
+    """N = 1 only: the reduction / allgather kernels the N >= 2 headline runs,
+    driven as p virtual ranks on this GPU (one cooperative launch holds every
+    rank's CTAs; flags, staging and fold order exactly as over NVLink).
+
+    * C1 (BASELINE config 1): 4 ranks, 1 MiB fp32, auto (= ring_rsa), sum —
+      device latency per call (L2-warm) and bit-exactness vs the reference
+      golden SHA.
+    * The headline kernel configuration (registered gradients, ONE
+      multi-buffer two-shot launch with the fused mean) on the C5
+      resnet50_like gradient set at p = 4 and p = 8: per-launch CUDA-event
+      time of the collective kernel and its algorithmic HBM bytes. On one GPU
+      every "peer" byte is an HBM byte: per rank the kernel reads the p
+      sources of its segment (S) and the p-1 reduced peer segments
+      ((p-1)S/p), and writes its output (S) and its staged reduced segment
+      (S/p): 3S per rank, 3pS per launch."""
+    import hashlib
+
+    import paper_1810_11112_b200 as P
+    from paper_1810_11112_b200 import _lib as L
+    from tests.golden import inputs as I
+    from tests.golden.load import of_kind
+    device = torch.device("cuda", local)
+    pk, pk_src = peaks()
+    out = {"what": "p virtual ranks on this GPU (cooperative launch), the kernels of the N>=2 path",
+           "peak": pk["hbm_gbs"], "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({pk_src})"}
+
+    def prof(vg, kind):
+        n, ms, b = C.c_int64(), C.c_double(), C.c_int64()
+        L.check(L.lib.cm_comm_profile_read(vg._h, kind, C.byref(n), C.byref(ms), C.byref(b)))
+        return int(n.value), float(ms.value)
+
+    # C1
+    vg = P.VirtualGroup(4, local, staging_bytes=64 << 20)
+    xs = I.c1_inputs()
+    ts = [P.Tensor("x", "float32", torch.from_numpy(x).to(device)) for x in xs]
+    sha = {c["algo"]: c["sha"] for c in of_kind("c1")}
+    res = P.allreduce_group(ts, P.ReduceOp.SUM, vg, algo="auto")
+    exact = all(hashlib.sha256(t.to_bytes()).hexdigest() == sha["ring_rsa"] for t, _ in res)
+    outs = [torch.empty_like(t.payload) for t in ts]
+    st = (L.Stats * 4)()
+    ins_a, outs_a = L.ptr_array([t.payload.data_ptr() for t in ts]), L.ptr_array([o.data_ptr() for o in outs])
+    stream = torch.cuda.current_stream(device).cuda_stream
+
+    def call():
+        L.check(L.lib.cm_allreduce_v(vg._h, ins_a, outs_a, 262144, 0, 0, 0, 131072, 0, stream, st))
+    for _ in range(20):
+        call()
+    torch.cuda.synchronize()
+    iters = 200
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(iters):
+        call()
+    e1.record()
+    torch.cuda.synchronize()
+    vg.poll()
+    out["c1"] = {"config": "4 ranks x 1 MiB fp32, auto -> ring_rsa, sum", "us_per_call": round(
+        e0.elapsed_time(e1) / iters * 1e3, 2), "timing": f"{iters} back-to-back calls, CUDA events, L2-warm",
+        "parity": "bit-exact vs reference golden SHA" if exact else "MISMATCH"}
+    vg.close()
+
+    # headline kernel configuration at p = 4 and 8
+    layers = MODELS["resnet50_like"]
+    S = sum(layers) * 4
+    for p in (4, 8):
+        vg = P.VirtualGroup(p, local, staging_bytes=S + (8 << 20))
+        sets = [P.GradientSet(tuple(P.Tensor(nm, "float32", torch.from_numpy(a).to(device))
+                                    for nm, a in I.synth_gradients(0, 0, layers, r))) for r in range(p)]
+        P.register_gradients_group(sets, vg)
+        res = P.aggregate_group(sets, vg)
+        parity = None
+        for case in of_kind("model"):
+            if case["model"] == "resnet50_like" and case["p"] == p:
+                h = hashlib.sha256()
+                for t in res[0].tensors:
+                    h.update(t.to_bytes())
+                parity = "bit-exact vs reference golden SHA" if h.hexdigest() == case["sha"] else "MISMATCH"
+        if parity is None:
+            from oracle import aggregation as OA
+            want, _, _ = OA.aggregate([I.synth_gradients(0, 0, layers, r) for r in range(p)], "float32")
+            ok = all(t.to_bytes() == want[t.name].tobytes() for t in res[p - 1].tensors)
+            parity = "bit-exact vs oracle (reference fold order)" if ok else "MISMATCH"
+        for _ in range(3):
+            P.aggregate_group(sets, vg)
+        torch.cuda.synchronize()
+        L.check(L.lib.cm_comm_profile(vg._h, 1))
+        k = max(5, min(steps, 20))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(k):
+            P.aggregate_group(sets, vg)
+        e1.record()
+        torch.cuda.synchronize()
+        n, ms = prof(vg, 0)
+        L.check(L.lib.cm_comm_profile(vg._h, 0))
+        us = ms / max(n, 1) * 1e3
+        alg = 3 * p * S
+        ach = alg / (us * 1e-6) / 1e9
+        out[f"aggregate_p{p}"] = {
+            "config": f"C5 resnet50_like ({S} B fp32 per rank), registered gradients, {p} virtual ranks, "
+                      f"one multi-buffer two-shot launch with the fused mean",
+            "kernel": "collective_kernel<F32,SUM,MP,ring,MULTI> (SRC_GATHER, bulk-engine reduce)",
+            "launches": n, "avg_launch_us": round(us, 2), "step_ms": round(e0.elapsed_time(e1) / k, 4),
+            "algorithmic_bytes_per_launch": alg, "achieved": round(ach, 1), "unit": "GB/s",
+            "frac": round(ach / pk["hbm_gbs"], 4), "parity": parity,
+            "bytes_model": "3*p*S: per rank reads S (RS sources) + (p-1)S/p (AG), writes S (output) + S/p (staged segment)"}
+        del sets, res
+        vg.close()
+        torch.cuda.empty_cache()
+    return out
+
+
 # ---------------------------------------------------------------------- headline
 def headline(args, rank, world, local):
     import paper_1810_11112_b200 as P
@@ -423,6 +537,10 @@ def headline(args, rank, world, local):
                          f"aggregate: np.concatenate fuse, identity allreduce, float64 mean), "
                          f"median {t * 1e3:.1f} ms/step"}
 
+    virt = None
+    if world == 1 and rank == 0 and not args.no_virtual:
+        virt = virtual_block(args, local, args.steps)
+
     if rank == 0:
         out = {
             "metric": METRIC, "value": round(world * S / (ms * 1e-3) / 1e9, 2), "unit": "GB/s",
@@ -449,6 +567,8 @@ def headline(args, rank, world, local):
             "gpu_launches_per_step": launches / max(args.steps, 1),
             "clocks": clocks, "nccl": nccl, "parity": parity,
         }
+        if virt is not None:
+            out["virtual"] = virt
         emit(out)
     comm.close()
 
@@ -804,6 +924,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-nccl", action="store_true")
     ap.add_argument("--no-check", action="store_true")
+    ap.add_argument("--no-virtual", action="store_true", help="N=1: skip the virtual-group kernel block")
     ap.add_argument("--no-register", action="store_true",
                     help="do not register the gradient tensors (pack them every step)")
     ap.add_argument("--param", action="append", default=[],

@@ -75,6 +75,17 @@ typedef struct {
   int64_t invalidations;
 } cm_registry_stats_t;
 
+/* what the pointer cache records about an address (real backend: memory type,
+ * device ordinal, allocation range and buffer id from one
+ * cuPointerGetAttributes; intercept cache: the registered range) */
+typedef struct {
+  int32_t kind;          /* cm_kind */
+  int32_t device;        /* device ordinal, -1 for host memory / unknown */
+  uint64_t range_start;  /* allocation holding the address (0 if unknown) */
+  int64_t range_size;
+  uint64_t buffer_id;    /* unique per allocation (0 if unknown) */
+} cm_buffer_info_t;
+
 typedef struct cm_comm cm_comm_t;
 typedef struct cm_registry cm_registry_t;
 
@@ -118,6 +129,8 @@ int cm_registry_free(cm_registry_t* reg, uint64_t address);
 int cm_registry_register(cm_registry_t* reg, uint64_t address, int64_t size, int kind);
 int cm_registry_unregister(cm_registry_t* reg, uint64_t address);
 int cm_registry_classify(cm_registry_t* reg, uint64_t address, int* kind);
+/* classify through the policy and return the cache entry's details */
+int cm_registry_info(cm_registry_t* reg, uint64_t address, cm_buffer_info_t* out);
 int cm_registry_ground_truth(cm_registry_t* reg, uint64_t address, int* kind);
 int cm_registry_stats(cm_registry_t* reg, cm_registry_stats_t* out);
 int cm_registry_policy(cm_registry_t* reg, int* policy);
@@ -176,11 +189,17 @@ int cm_comm_registry(cm_comm_t* comm, cm_registry_t** reg);
  *                         pipeline (default 8192; 2048/4096/16384 measured slower)
  *   "bulk_stage_kb"       KiB per bulk-reduce stage (default 64; the stage count
  *                         is clamped to the shared memory available)
- *   "bulk_local"          2 = the reduce loads its own rank's source directly and
- *                         stages only remote ones (measured slower), 1 = all staged
  *   "inline_agree"        2 = aggregate's ready-set agreement travels in the fused
  *                         collective's start-barrier records (default), 1 = a
  *                         separate LL agreement kernel gates the collective
+ *   "auto_register"       2 = (default) the pointer cache registers the allocation
+ *                         behind a plain device send buffer on first sight: its
+ *                         CUDA-IPC handle goes into this rank's heap mailbox,
+ *                         peers map it when their kernels report the new slot
+ *                         and acknowledge in this heap; from then on peers read
+ *                         the buffer in place (no copy into staging). 1 = off.
+ * get also reads the counters "auto_published", "auto_mapped",
+ * "auto_zero_copy_calls" and "auto_buffer_checks" (allocation-id re-checks)
  * get also reads "staging_bytes", "pool_bytes" and "ll_payload_per_source" */
 int cm_comm_set_param(cm_comm_t* comm, const char* key, int64_t value);
 int cm_comm_get_param(cm_comm_t* comm, const char* key, int64_t* value);
@@ -201,6 +220,10 @@ int cm_comm_export(cm_comm_t* comm, const void* ptr, int64_t bytes, void* handle
 int cm_comm_register(cm_comm_t* comm, const void* ptr, int64_t bytes, const void* all_handles,
                      const int64_t* all_offsets, int64_t* reg_id);
 int cm_comm_deregister(cm_comm_t* comm, const void* ptr);
+/* virtual group (single-GPU emulation): register every virtual rank's buffer
+ * (ptrs[size]) under one id; fused aggregates whose members all carry ids read
+ * the members in place (the SRC_GATHER path of real communicators) */
+int cm_comm_register_v(cm_comm_t* comm, const void* const* ptrs, int64_t bytes, int64_t* reg_id);
 /* wait for `stream`, then report any device-side error of earlier calls */
 int cm_comm_sync(cm_comm_t* comm, void* stream);
 /* non-blocking error check of completed calls */
@@ -209,6 +232,8 @@ int cm_comm_poll(cm_comm_t* comm);
  * one-shot NVLink kernel); control-plane primitive of negotiate_ready
  * (aggregation.py:72-92) — equal (key, -key) maxima prove equal ready sets */
 int cm_agree(cm_comm_t* comm, const int64_t* values, int n, int64_t* maxes, void* stream);
+/* virtual group: values[size * n] (rank-major) -> maxes[size * n] */
+int cm_agree_v(cm_comm_t* comm, const int64_t* values, int n, int64_t* maxes, void* stream);
 /* logical counters (Transport.messages_sent / bytes_sent, base.py:43-57) and
  * the real NVLink bytes this rank pulled from peers */
 int cm_comm_counters(cm_comm_t* comm, int64_t* messages_sent, int64_t* bytes_sent,
@@ -256,11 +281,16 @@ int cm_fused_allreduce(cm_comm_t* comm, int n, const void* const* sends, const i
 /* cm_fused_allreduce preceded by the negotiation check: every rank passes the
  * same n_agree (<= 4) values (e.g. a hash of its ready names) when its ready
  * set is identical; *agreed = 1 and the fused launches follow in the same call,
- * or *agreed = 0 and nothing is launched (the caller negotiates the
- * intersection, aggregation.py:72-92, and calls again). reg_ids (nullable):
- * per member, its cm_comm_register id (same on every rank) or -1; fused groups
- * whose members are all registered skip the pack — peers read the member
- * tensors in place. */
+ * or *agreed = 0 and no data moves on any rank (the caller negotiates the
+ * intersection, aggregation.py:72-92, and calls again). The call's structure
+ * does not depend on the rank's plan while the agreement is pending: with
+ * n_agree == 2 the first collective carries the values in its start-barrier
+ * records on the full grid, otherwise an LL agreement kernel goes first; all
+ * later collectives are gated and skip (no barrier, no epoch advance) on a
+ * mismatch, so ranks whose ready sets — and launch counts — differ stay in
+ * step. reg_ids (nullable): per member, its cm_comm_register id (same on every
+ * rank) or -1; fused groups whose members are all registered skip the pack —
+ * peers read the member tensors in place. */
 int cm_fused_allreduce_agreed(cm_comm_t* comm, int n, const void* const* sends,
                               const int64_t* counts, int dtype, void* recv_fused, int algo,
                               int64_t threshold, int64_t switch_bytes, int average,
@@ -269,6 +299,14 @@ int cm_fused_allreduce_agreed(cm_comm_t* comm, int n, const void* const* sends,
                               int* n_calls);
 
 /* virtual-group variants: arrays of `size` per-rank pointers */
+/* sends[size * n] (rank-major), recvs_fused[size], agree_values[size * n_agree],
+ * agreed[size], stats[size * n] (rank r's group g at r * n + g) */
+int cm_fused_allreduce_agreed_v(cm_comm_t* comm, int n, const void* const* sends,
+                                const int64_t* counts, int dtype, void* const* recvs_fused, int algo,
+                                int64_t threshold, int64_t switch_bytes, int average,
+                                const int64_t* agree_values, int n_agree, int* agreed,
+                                const int64_t* reg_ids, void* stream, cm_stats_t* stats,
+                                int* n_calls);
 int cm_allreduce_v(cm_comm_t* comm, const void* const* sends, void* const* recvs, int64_t count,
                    int dtype, int op, int algo, int64_t switch_bytes, int average, void* stream,
                    cm_stats_t* stats);

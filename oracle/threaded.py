@@ -17,7 +17,6 @@ from __future__ import annotations
 
 import queue
 import threading
-from collections import defaultdict
 
 import numpy as np
 
@@ -44,7 +43,10 @@ class ThreadTransport:
 class ThreadNet:
     def __init__(self, size: int):
         self.size = size
-        self.box = defaultdict(queue.Queue)
+        # every (src, dst) FIFO exists before the rank threads start: creating
+        # them lazily from several threads (defaultdict) can lose a queue and
+        # the message in it
+        self.box = {(s, d): queue.Queue() for s in range(size) for d in range(size)}
 
     def run(self, fn):
         out = [None] * self.size

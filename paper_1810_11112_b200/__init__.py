@@ -22,6 +22,7 @@ from .collectives import (ALGORITHMS, DEFAULT_SWITCH_BYTES, CollectiveStats,  # 
                           resolve_algorithm)
 from .aggregation import (DEFAULT_FUSION_THRESHOLD, FusedBuffer, FusionConfig,  # noqa: F401
                           GradientSet, aggregate, aggregate_group, fuse,
+                          negotiate_ready_group, register_gradients_group,
                           fuse_plan, negotiate_ready, register_gradients, unfuse)
 from .overlap import OverlappedAggregator  # noqa: F401
 from .paramserver import PsTopology, run_ps_step, run_ps_step_group  # noqa: F401

@@ -21,40 +21,67 @@ FLAGS = [
 ]
 
 
+# csrc/inst.cu is compiled once per (element type, reduce op): the kernel
+# tables are the long pole of the build, so they are split ten ways
+INST = [(t, tl, o, ol) for t, tl in (("BF16", "bf16"), ("F32", "f32"), ("F64", "f64"), ("I64", "i64"), ("I32", "i32"))
+        for o, ol in (("CM_SUM", "sum"), ("CM_MAX", "max"))]
+
+
 def sources():
-    return sorted(glob.glob(os.path.join(HERE, "csrc", "*.cu")) +
-                  glob.glob(os.path.join(HERE, "csrc", "*.cpp")))
+    return sorted(f for f in glob.glob(os.path.join(HERE, "csrc", "*.cu")) if not f.endswith("inst.cu")) + \
+        sorted(glob.glob(os.path.join(HERE, "csrc", "*.cpp")))
+
+
+def units():
+    """(source, object name, extra defines) for every translation unit."""
+    inst = os.path.join(HERE, "csrc", "inst.cu")
+    out = [(inst, f"inst_{tl}_{ol}.o", [f"-DCM_INST_T={t}", f"-DCM_INST_OP={o}",
+                                        f"-DCM_INST_FN=cm_kernels_{tl}_{ol}"])
+           for t, tl, o, ol in INST]
+    return out + [(s, os.path.basename(s) + ".o", []) for s in sources()]
 
 
 def stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = sources() + glob.glob(os.path.join(HERE, "csrc", "*.h*")) + \
+    deps = sources() + [os.path.join(HERE, "csrc", "inst.cu")] + glob.glob(os.path.join(HERE, "csrc", "*.h*")) + \
         glob.glob(os.path.join(HERE, "csrc", "*.cuh")) + [os.path.join(ROOT, "include", "cm.h")]
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, extra=()) -> str:
+def build(verbose: bool = False, extra=(), ptxas_log: str | None = None) -> str:
     """Compile every translation unit in parallel (the per-dtype kernel
-    tables dominate), then link libcm.so."""
+    tables dominate), then link libcm.so. ``ptxas_log``: also write the
+    `-Xptxas -v` register/spill report of every kernel to this file."""
     from concurrent.futures import ThreadPoolExecutor
     objdir = os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
     inc = ["-I", os.path.join(ROOT, "include"), "-I", os.path.join(HERE, "csrc")]
     cflags = [f for f in FLAGS if f != "-shared"]
 
-    def compile_one(src):
-        obj = os.path.join(objdir, os.path.basename(src) + ".o")
-        cmd = [NVCC, *cflags, *extra, *inc, "-c", src, "-o", obj]
+    def compile_one(unit):
+        src, name, defs = unit
+        obj = os.path.join(objdir, name)
+        cmd = [NVCC, *cflags, *extra, *defs, *inc, "-c", src, "-o", obj]
+        if ptxas_log:
+            cmd += ["-Xptxas", "-v"]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
-        subprocess.run(cmd, check=True)
-        return obj
+        r = subprocess.run(cmd, capture_output=bool(ptxas_log), text=True)
+        if r.returncode:
+            sys.stderr.write((r.stderr or "") if ptxas_log else "")
+            raise subprocess.CalledProcessError(r.returncode, cmd)
+        return obj, (r.stderr or "") if ptxas_log else ""
 
-    srcs = sources()
-    with ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 4)) as ex:
-        objs = list(ex.map(compile_one, srcs))
+    todo = units()
+    with ThreadPoolExecutor(max_workers=min(len(todo), os.cpu_count() or 4)) as ex:
+        res = list(ex.map(compile_one, todo))
+    objs = [o for o, _ in res]
+    if ptxas_log:
+        with open(ptxas_log, "w") as fh:
+            for (_, name, _), (_, log) in zip(todo, res):
+                fh.write(f"==== {name}\n{log}")
     cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", LIB + ".tmp"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
@@ -64,4 +91,8 @@ def build(verbose: bool = False, extra=()) -> str:
 
 
 if __name__ == "__main__":
-    print(build(verbose=True, extra=sys.argv[1:]))
+    args = sys.argv[1:]
+    log = None
+    if args and args[0].startswith("--ptxas-log="):
+        log = args.pop(0).split("=", 1)[1]
+    print(build(verbose=True, extra=args, ptxas_log=log))

@@ -47,6 +47,11 @@ class RegStats(C.Structure):
                 ("inserts", C.c_int64), ("invalidations", C.c_int64)]
 
 
+class BufferInfo(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("device", C.c_int32), ("range_start", C.c_uint64),
+                ("range_size", C.c_int64), ("buffer_id", C.c_uint64)]
+
+
 _vp = C.c_void_p
 _i64 = C.c_int64
 _i = C.c_int
@@ -70,6 +75,7 @@ _SIGS = {
     "cm_registry_register": ([_vp, C.c_uint64, _i64, _i], _i),
     "cm_registry_unregister": ([_vp, C.c_uint64], _i),
     "cm_registry_classify": ([_vp, C.c_uint64, _P(_i)], _i),
+    "cm_registry_info": ([_vp, C.c_uint64, _P(BufferInfo)], _i),
     "cm_registry_ground_truth": ([_vp, C.c_uint64, _P(_i)], _i),
     "cm_registry_stats": ([_vp, _P(RegStats)], _i),
     "cm_registry_policy": ([_vp, _P(_i)], _i),
@@ -92,9 +98,11 @@ _SIGS = {
     "cm_comm_export": ([_vp, _vp, _i64, _vp, _P(_i64)], _i),
     "cm_comm_register": ([_vp, _vp, _i64, _vp, _P(_i64), _P(_i64)], _i),
     "cm_comm_deregister": ([_vp, _vp], _i),
+    "cm_comm_register_v": ([_vp, _P(_vp), _i64, _P(_i64)], _i),
     "cm_comm_sync": ([_vp, _vp], _i),
     "cm_comm_poll": ([_vp], _i),
     "cm_agree": ([_vp, _P(_i64), _i, _P(_i64), _vp], _i),
+    "cm_agree_v": ([_vp, _P(_i64), _i, _P(_i64), _vp], _i),
     "cm_comm_counters": ([_vp, _P(_i64), _P(_i64), _P(_i64), _P(_i64)], _i),
     "cm_comm_launches": ([_vp, _P(_i64)], _i),
     "cm_comm_profile": ([_vp, _i], _i),
@@ -107,6 +115,8 @@ _SIGS = {
                             _P(Stats), _P(_i)], _i),
     "cm_fused_allreduce_agreed": ([_vp, _i, _P(_vp), _P(_i64), _i, _vp, _i, _i64, _i64, _i,
                                    _P(_i64), _i, _P(_i), _P(_i64), _vp, _P(Stats), _P(_i)], _i),
+    "cm_fused_allreduce_agreed_v": ([_vp, _i, _P(_vp), _P(_i64), _i, _P(_vp), _i, _i64, _i64, _i,
+                                     _P(_i64), _i, _P(_i), _P(_i64), _vp, _P(Stats), _P(_i)], _i),
     "cm_allreduce_v": ([_vp, _P(_vp), _P(_vp), _i64, _i, _i, _i, _i64, _i, _vp, _P(Stats)], _i),
     "cm_reduce_scatter_v": ([_vp, _P(_vp), _P(_vp), _i64, _i, _i, _i, _vp, _P(Stats)], _i),
     "cm_allgather_v": ([_vp, _P(_vp), _P(_vp), _i64, _i, _i, _vp, _P(Stats)], _i),

@@ -274,10 +274,13 @@ def _aggregate_names(grads, names, tp, algo, cfg, sw, registry, handles, stats_o
                 registry.classify(handles[plan.ready[i].name])
     # out= reuses the previous result's buckets (device, or pinned host for
     # host gradients) when the schema matches
+    # (checked locally but never raised: this rank's plan may be the one that
+    # disagrees, and the agreement inside the call must still run on every
+    # rank — a non-matching out= just gets fresh buckets)
     reuse = out.__dict__.get("_bufs") if out is not None else None
     if reuse is not None and [(f.numel(), f.is_cuda) for f in reuse] != \
             [(r["total"], not r["any_host"]) for r in plan.runs]:
-        raise ShapeError("out= GradientSet does not match this gradient schema")
+        reuse = None
     # same schema and names: the result tensors are views of the reused
     # buckets already, so `out` itself is refilled and returned (torch out=)
     refill = reuse is not None and out.names == list(names)
@@ -326,41 +329,144 @@ def _aggregate_names(grads, names, tp, algo, cfg, sw, registry, handles, stats_o
     return gs
 
 
+def negotiate_ready_group(per_rank_ready: list[list[str]], vg: VirtualGroup) -> list[list[str]]:
+    """``negotiate_ready`` for every rank of a VirtualGroup: the same fast path
+    (``cm_agree_v``: one int64 MAX-allreduce of (key, count, -key, -count)
+    over the virtual ranks) and, on a mismatch, the reference's intersection
+    (aggregation.py:72-92)."""
+    p = vg.size
+    if len(per_rank_ready) != p:
+        raise ShapeError(f"{len(per_rank_ready)} ready sets for a group of {p}")
+    names = [sorted(r) for r in per_rank_ready]
+    if p == 1:
+        return names
+    vals = []
+    for nm in names:
+        k = _name_key(nm)
+        vals += [k, len(nm), -k, -len(nm)]
+    mx = (C.c_int64 * (4 * p))()
+    with torch.cuda.device(vg.device):
+        L.check(L.lib.cm_agree_v(vg._h, L.i64_array(vals), 4, mx, vg._stream()))
+    if all(list(mx[4 * r:4 * r + 4]) == vals[4 * r:4 * r + 4] for r in range(p)):
+        return names
+    common = set(names[0])
+    for nm in names[1:]:
+        common &= set(nm)
+    return [sorted(common)] * p
+
+
+def register_gradients_group(per_rank: list[GradientSet], vg: VirtualGroup) -> None:
+    """``register_gradients`` for every rank of a VirtualGroup: every
+    gradient (sorted by name; every rank must hold the same names) gets one
+    registered-buffer id, so ``aggregate_group`` reads the members in place
+    (SRC_GATHER, the registered path of real communicators)."""
+    names = sorted(per_rank[0].names)
+    for g in per_rank[1:]:
+        if sorted(g.names) != names:
+            raise ShapeError("every rank must register the same gradient names")
+    for g in per_rank:
+        for nm in names:
+            if not g.get(nm).is_cuda:
+                raise ShapeError(f"{nm}: only device tensors can be registered")
+    ids = vg.register_buffers([[g.get(nm).payload for g in per_rank] for nm in names]) if names else []
+    for g in per_rank:
+        object.__setattr__(g, "_reg_ids", dict(zip(names, ids)))
+
+
 def aggregate_group(per_rank: list[GradientSet], vg: VirtualGroup, algo: str = "auto",
                     cfg: FusionConfig | None = None,
                     switch_bytes: int | None = DEFAULT_SWITCH_BYTES,
-                    stats_out: list[list[CollectiveStats]] | None = None) -> list[GradientSet]:
-    """``aggregate`` for every rank of a single-GPU VirtualGroup: negotiation
-    (local intersection), fusion with the batched-copy kernel, then one
-    averaged allreduce launch per fused buffer."""
-    from .collectives import allreduce_group
+                    stats_out: list[list[CollectiveStats]] | None = None,
+                    agree: bool = True) -> list[GradientSet]:
+    """``aggregate`` for every rank of a single-GPU VirtualGroup through the
+    same C path as a real communicator (``cm_fused_allreduce_agreed_v``):
+    inline ready-set agreement in the first fused collective, packs into each
+    rank's staging (or in-place reads of registered gradients), multi-buffer
+    two-shot launches with the fused mean, host gradients through the copy
+    streams. If the ranks' ready sets differ, the intersection is negotiated
+    as in the reference (aggregation.py:72-92) and the call repeats.
+
+    One launch covers all virtual ranks, so the first (agreed) attempt needs
+    every rank's schema to have the same shape; otherwise the intersection is
+    taken up front."""
     cfg = cfg or FusionConfig()
     p = vg.size
     if len(per_rank) != p:
         raise ShapeError(f"{len(per_rank)} gradient sets for a group of {p}")
-    common = set(per_rank[0].names)
-    for g in per_rank[1:]:
-        common &= set(g.names)
-    names = sorted(common)
-    outs = [dict() for _ in range(p)]
+    if algo not in L.ALGO:
+        from .errors import ConfigError
+        raise ConfigError(f"unknown algorithm {algo!r}")
+    sw = _switch(switch_bytes, p)
+    local = [sorted(g.names) for g in per_rank]
     if stats_out is not None:
         stats_out.extend([] for _ in range(p))
-    ready0 = [per_rank[0].get(nm) for nm in names]
-    for grp in fuse_plan(ready0, cfg):
-        bufs = []
+
+    def shape(r):
+        return [(per_rank[r].get(nm).dtype, per_rank[r].get(nm).len) for nm in local[r]]
+    res = None
+    if agree and p > 1 and local[0] and all(shape(r) == shape(0) for r in range(1, p)):
+        vals = []
+        for nm in local:
+            vals += [_name_key(nm), len(nm)]
+        res = _aggregate_group_names(per_rank, local, vg, algo, cfg, sw, stats_out, vals)
+    if res is None:
+        common = set(local[0])
+        for nm in local[1:]:
+            common &= set(nm)
+        names = sorted(common)
+        res = _aggregate_group_names(per_rank, [names] * p, vg, algo, cfg, sw, stats_out, None)
+    return res
+
+
+def _aggregate_group_names(per_rank, names, vg, algo, cfg, sw, stats_out, agree_vals):
+    p = vg.size
+    ready = [[per_rank[r].get(nm) for nm in names[r]] for r in range(p)]
+    for r in range(1, p):
+        if [(t.dtype, t.len) for t in ready[r]] != [(t.dtype, t.len) for t in ready[0]]:
+            raise ShapeError("collective shape error: ranks disagree on the negotiated gradient shapes")
+    outs: list[list[Tensor]] = [[] for _ in range(p)]
+    stats: list[list[CollectiveStats]] = [[] for _ in range(p)]
+    regmaps = [g.__dict__.get("_reg_ids") for g in per_rank]
+    agree = L.i64_array(agree_vals) if agree_vals is not None else None
+    i = 0
+    stream = vg._stream()
+    with torch.cuda.device(vg.device):
+        while i < len(ready[0]):
+            j = i
+            while j < len(ready[0]) and ready[0][j].dtype == ready[0][i].dtype:
+                j += 1
+            dtype = ready[0][i].dtype
+            if dtype not in ("float32", "float64", "bfloat16"):
+                raise ShapeError(f"aggregate averages floating-point gradients, got {dtype}")
+            run = [ready[r][i:j] for r in range(p)]
+            n = j - i
+            counts = [t.len for t in run[0]]
+            any_host = any(not t.is_cuda for rr in run for t in rr)
+            fused = [torch.empty(sum(counts), dtype=DTYPES[dtype], pin_memory=True) if any_host
+                     else torch.empty(sum(counts), dtype=DTYPES[dtype], device=vg.device) for _ in range(p)]
+            reg = None
+            if all(m is not None and all(t.name in m for t in rr) for m, rr in zip(regmaps, run)):
+                ids = [regmaps[0][t.name] for t in run[0]]
+                if all([m[t.name] for t in rr] == ids for m, rr in zip(regmaps, run)):
+                    reg = L.i64_array(ids)
+            st = (L.Stats * (p * max(1, n)))()
+            ncalls = C.c_int()
+            agreed = (C.c_int * p)(*([1] * p))
+            L.check(L.lib.cm_fused_allreduce_agreed_v(
+                vg._h, n, L.ptr_array([t.payload.data_ptr() for rr in run for t in rr]), L.i64_array(counts),
+                L.DTYPE[dtype], L.ptr_array([f.data_ptr() for f in fused]), L.ALGO[algo],
+                int(cfg.threshold_bytes), sw, 1, agree, 2 if agree is not None else 0, agreed, reg,
+                stream, st, C.byref(ncalls)))
+            if agree is not None and not all(agreed):
+                return None             # nothing moved on any rank
+            agree = None
+            for r in range(p):
+                stats[r].extend(_stats(st[r * n + k]) for k in range(ncalls.value))
+                for t, view in zip(run[r], fused[r].split_with_sizes(counts)):
+                    outs[r].append(Tensor._wrap(t.name, dtype, view))
+            i = j
+    vg.synchronize()
+    if stats_out is not None:
         for r in range(p):
-            ts = [per_rank[r].get(names[i]) for i in grp]
-            ts = [Tensor(t.name, t.dtype, t.payload.to(vg.device)) for t in ts]
-            (fb,) = fuse(ts, FusionConfig(1 << 62))
-            bufs.append(fb)
-        res = allreduce_group([Tensor("__fused__", b.dtype, b.payload) for b in bufs],
-                              ReduceOp.SUM, vg, algo=algo, switch_bytes=switch_bytes,
-                              average=True)
-        for r in range(p):
-            mean, st = res[r]
-            if stats_out is not None:
-                stats_out[r].append(st)
-            for name, off, ln in bufs[r].members:
-                outs[r][name] = Tensor(name, mean.dtype, mean.payload[off:off + ln])
-    return [GradientSet(tuple(outs[r][nm] for nm in names), per_rank[r].iteration)
-            for r in range(p)]
+            stats_out[r].extend(stats[r])
+    return [GradientSet(tuple(outs[r]), per_rank[r].iteration) for r in range(p)]

@@ -264,6 +264,21 @@ class VirtualGroup(_Base):
         if timeout_s is not None:
             self.set_timeout(timeout_s)
 
+    def register_buffers(self, per_rank_tensors) -> list[int]:
+        """Register buffers for zero-copy aggregation: ``per_rank_tensors[i]``
+        lists every virtual rank's i-th tensor (device memory); returns one id
+        per i, the same id for all ranks (as ``Communicator.register_buffers``
+        returns on every rank of a real group)."""
+        ids = []
+        for ts in per_rank_tensors:
+            if len(ts) != self.size:
+                raise InvalidGroupError(f"{len(ts)} tensors for a group of {self.size}")
+            rid = C.c_int64()
+            L.check(L.lib.cm_comm_register_v(self._h, L.ptr_array([t.data_ptr() for t in ts]),
+                                             ts[0].numel() * ts[0].element_size(), C.byref(rid)))
+            ids.append(int(rid.value))
+        return ids
+
 
 def _tensor_from_ptr(ptr: int, numel: int, dtype: torch.dtype, device: torch.device) -> torch.Tensor:
     """Wrap comm-owned device memory as a torch tensor (no copy, not owned)."""

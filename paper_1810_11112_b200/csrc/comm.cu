@@ -27,6 +27,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <set>
 #include <string>
 #include <vector>
@@ -61,8 +62,9 @@ struct cm_comm {
   int64_t indev_bytes = 0, outdev_bytes = 0;
   cudaStream_t h2d = nullptr, d2h = nullptr;
   std::vector<cudaEvent_t> sync_events;
-  int64_t* agree_host = nullptr;       // mapped pinned: cm_agree result + completion word
+  int64_t* agree_host = nullptr;       // mapped pinned agreement words (AGH_* layout below)
   int64_t* agree_dev = nullptr;        // device alias of agree_host
+  int64_t* agree_in = nullptr;         // device copy of the virtual ranks' agreement inputs
   unsigned long long agree_ticket = 0;
   // registered buffers (cm_comm_register): local start -> {bytes, id}; opened
   // peer allocations cached by (peer, handle bytes) -> mapped base
@@ -74,6 +76,22 @@ struct cm_comm {
   std::map<std::string, char*> opened;
   std::map<std::string, long long*> gtabs;   // member tables of registered fused batches
   int64_t next_reg = 0;
+  // automatic registration of user allocations (dev_common.cuh MAILBOX/AUTOTAB/ACK):
+  // allocation base -> {bytes, mailbox slot (-1: not IPC-exportable), buffer id}
+  struct AutoReg {
+    size_t size;
+    int64_t slot;
+    unsigned long long buffer_id;
+  };
+  int auto_reg = 1;
+  std::map<uintptr_t, AutoReg> autoregs;
+  int64_t reg_seq = 0;                      // slots published in my mailbox
+  int64_t mapped_seq[MAXP] = {};            // peers' slots mapped into AUTOTAB
+  unsigned long long* areg_host = nullptr;  // mapped pinned: notice[MAXP], acked
+  unsigned long long* areg_dev = nullptr;
+  unsigned char* areg_pin = nullptr;        // pinned scratch for mailbox reads / table writes
+  cudaStream_t reg_stream = nullptr;
+  int64_t auto_published = 0, auto_mapped = 0, auto_zc_calls = 0, auto_checks = 0;
   int sms = 148;
   // tuning knobs (cm_comm_set_param)
   int64_t oneshot_max_bytes = 32 * 1024;
@@ -88,7 +106,6 @@ struct cm_comm {
   int bulk_rs = 6;                            // reduce phase: bulk-engine stages in smem (0: SM loads)
   int dyn_ag = 0;                             // allgather as a shared (slice, peer) task queue (opt-in)
   int inline_agree = 1;                       // aggregate's agreement inside the collective's records
-  int bulk_local = 0;                         // reduce: own source loaded directly (opt-in; measured slower)
   int bulk_stage = 2 * RS_STAGE_BYTES;        // bytes per bulk-reduce stage (64 KiB: 3 stages fit)
   int64_t host_chunk = 8 << 20;               // host-gradient pipeline: bytes per H2D/D2H piece (p = 1)
   int64_t oneshot_bytes_per_cta = 8 * 1024;
@@ -164,17 +181,40 @@ struct ProfScope {
 
 using KFn = void (*)(CollParams);
 
+// cudaFuncAttributeMaxDynamicSharedMemorySize is set per (device, kernel):
+// `want` < 0 opts in to everything next to the static shared memory and
+// returns that amount in *avail
+std::mutex g_attr_mu;
+std::map<std::pair<int, const void*>, int> g_attr;
+
+int dyn_smem_optin(int device, const void* k, int* avail, int want = -1) {
+  std::lock_guard<std::mutex> g(g_attr_mu);
+  auto key = std::make_pair(device, k);
+  auto it = g_attr.find(key);
+  if (it != g_attr.end()) { *avail = it->second; return CM_OK; }
+  int optin = 0;
+  CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+  cudaFuncAttributes fa;
+  CUDA_TRY(cudaFuncGetAttributes(&fa, k));
+  const int a = want >= 0 ? want : optin - (int)fa.sharedSizeBytes;
+  CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, a));
+  g_attr[key] = a;
+  *avail = a;
+  return CM_OK;
+}
+
 // kernel tables live in one translation unit per element type (csrc/inst_*.cu)
 // so the instantiations compile in parallel
-enum KernelKind { K_COLL = 0, K_STREAM = 1, K_LL = 2, K_LL2 = 3, K_RHD = 4 };
+enum KernelKind { K_COLL = 0, K_STREAM = 1, K_LL = 2, K_LL2 = 3, K_RHD = 4, K_MULTI = 5 };
 
 KFn pick(int kind, int dtype, int op, int p, bool tree) {
+  const bool sum = op == CM_SUM;
   switch (dtype) {
-    case CM_FLOAT32: return cm_kernels_f32(kind, op, p, tree);
-    case CM_FLOAT64: return cm_kernels_f64(kind, op, p, tree);
-    case CM_BFLOAT16: return cm_kernels_bf16(kind, op, p, tree);
-    case CM_INT32: return cm_kernels_i32(kind, op, p, tree);
-    case CM_INT64: return cm_kernels_i64(kind, op, p, tree);
+    case CM_FLOAT32: return sum ? cm_kernels_f32_sum(kind, p, tree) : cm_kernels_f32_max(kind, p, tree);
+    case CM_FLOAT64: return sum ? cm_kernels_f64_sum(kind, p, tree) : cm_kernels_f64_max(kind, p, tree);
+    case CM_BFLOAT16: return sum ? cm_kernels_bf16_sum(kind, p, tree) : cm_kernels_bf16_max(kind, p, tree);
+    case CM_INT32: return sum ? cm_kernels_i32_sum(kind, p, tree) : cm_kernels_i32_max(kind, p, tree);
+    case CM_INT64: return sum ? cm_kernels_i64_sum(kind, p, tree) : cm_kernels_i64_max(kind, p, tree);
   }
   return nullptr;
 }
@@ -240,14 +280,16 @@ struct Launch {
   int nbuf = 1;                     // multi-buffer launch (prestaged, two-shot pull)
   int64_t bn[MAXBUF] = {};
   int64_t bboff[MAXBUF] = {};
-  void* bout[MAXBUF] = {};
+  int64_t bout_off[MAXBUF] = {};    // element offset of buffer k's output in out[lr]
   unsigned long long* done_flag = nullptr;
   unsigned long long done_value = 0;
   unsigned long long agree_gate = 0;  // run only if agreement check `agree_gate` succeeded
   int agree_inline = 0;               // agreement values travel in the start-barrier records
-  long long akey = 0, acnt = 0;
+  long long akey[MAXP] = {}, acnt[MAXP] = {};
   unsigned long long* agree_out = nullptr;
   unsigned long long agree_ticket = 0;
+  int force_pull = 0;               // pull collective kernel on the full grid (inline agreement:
+                                    // the launch must have the same shape on every rank)
   int ll = 0;                       // one-shot through the LL slots
   const void* in[MAXP] = {};
   void* out[MAXP] = {};
@@ -301,7 +343,7 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
       maxseg += mk;                    // per-CTA work spans every buffer
       P.bn[k] = L.bn[k];
       P.bboff[k] = L.bboff[k];
-      P.bout[k] = static_cast<char*>(L.bout[k]);
+      P.bout_off[k] = L.bout_off[k];
       multi_hash = (multi_hash ^ (unsigned long long)L.bn[k]) * 1099511628211ull;
     }
     multi_hash = (multi_hash ^ L.gsig) * 1099511628211ull;
@@ -328,12 +370,16 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
   P.done_value = L.done_value;
   P.agree_gate = L.agree_gate;
   P.agree_inline = L.agree_inline;
-  P.akey = L.akey;
-  P.acnt = L.acnt;
+  for (int q = 0; q < MAXP; ++q) { P.akey[q] = L.akey[q]; P.acnt[q] = L.acnt[q]; }
   P.agree_out = L.agree_out;
   P.agree_ticket = L.agree_ticket;
   P.dyn_ag = c->dyn_ag;
-  P.bulk_local = c->bulk_local;
+  if (!c->virt && c->areg_dev) {
+    P.reg_seq = c->reg_seq;
+    for (int q = 0; q < p; ++q) P.mapped_seq[q] = c->mapped_seq[q];
+    P.notice = c->areg_dev;
+    P.acked = c->areg_dev + MAXP;
+  }
   P.trace = c->trace;
   P.trace_ctas = c->trace_ctas;
 
@@ -343,10 +389,10 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
   int64_t nb = (work + per - 1) / per;
   int ll = L.ll;
   // literal recursive halving/doubling (log2 p pairwise steps) for rhd_rsa allreduce
-  const bool logp = c->rhd_logp && L.order == ORD_TREE && L.nbuf == 1 && L.dtype != CM_BFLOAT16 &&
+  const bool logp = !L.force_pull && c->rhd_logp && L.order == ORD_TREE && L.nbuf == 1 && L.dtype != CM_BFLOAT16 &&
                     !L.out_rel && (L.oneshot || L.phases == (PH_RS | PH_AG)) &&
                     (L.srcmode == SRC_COPYIN || L.srcmode == SRC_ZEROCOPY || L.srcmode == SRC_REGISTERED);
-  if (logp) ll = 0;
+  if (logp || L.force_pull) ll = 0;
   if (ll == 1 && (L.n * (int64_t)sz + 7) / 8 > c->ll_units) ll = 0;
   if (ll == 2 && (maxseg * (int64_t)sz + 7) / 8 > c->ll_units) ll = 0;  // rhd segments > n/p
   // staging capacity (LL kernels read the input directly unless it is prestaged)
@@ -365,6 +411,7 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
   if (ll == 1) nb = ((L.n * (int64_t)sz + 7) / 8 + c->ll_units_per_cta - 1) / c->ll_units_per_cta;
   if (ll == 2) nb = ((maxseg * (int64_t)sz + 7) / 8 + c->ll2_units_per_cta - 1) / c->ll2_units_per_cta;
   if (logp) nb = (L.n * (int64_t)sz + c->twoshot_bytes_per_cta - 1) / c->twoshot_bytes_per_cta;
+  if (L.force_pull) nb = MAXBLK;      // the full grid: independent of the (rank-local) plan
   nb = std::max<int64_t>(1, std::min<int64_t>(nb, std::min(c->max_ctas, MAXBLK)));
   const bool tree = L.order == ORD_TREE;
   // pipelined two-shot when every CTA's slice spans >= 2 chunks
@@ -372,27 +419,24 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
                          L.phases == (PH_RS | PH_AG) &&
                          c->stream_chunk > 0 && maxseg / std::max<int64_t>(nb, 1) >= 2 * c->stream_chunk;
   P.stream_chunk = c->stream_chunk;
-  if ((L.agree_gate || L.agree_inline) && (logp || ll != 0))
-    return fail(CM_ERR_CONFIG, "internal: agreement gate needs the pull collective kernel");
-  KFn k = pick(logp ? K_RHD : ll == 1 ? K_LL : ll == 2 ? K_LL2 : pipelined ? K_STREAM : K_COLL, L.dtype, L.op, p,
-               tree);
+  if (L.agree_inline && (logp || ll != 0))
+    return fail(CM_ERR_CONFIG, "internal: inline agreement needs the pull collective kernel");
+  const bool multi = L.nbuf > 1 || L.srcmode == SRC_GATHER;
+  KFn k = pick(logp ? K_RHD : ll == 1 ? K_LL : ll == 2 ? K_LL2 : pipelined ? K_STREAM : multi ? K_MULTI : K_COLL,
+               L.dtype, L.op, p, tree);
   if (!k) return fail(CM_ERR_SHAPE, "unsupported dtype");
   // reduce phase through the bulk-copy engine (shared-memory stage ring)
   const bool bulk = c->bulk_rs > 0 && !logp && ll == 0 && !pipelined && (L.phases & PH_RS);
-  // dynamic shared memory available next to the kernel's static arrays
-  static std::map<const void*, int> max_dyn;
-  if (bulk && !max_dyn.count((const void*)k)) {
-    int optin = 0;
-    CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
-    cudaFuncAttributes fa;
-    CUDA_TRY(cudaFuncGetAttributes(&fa, (const void*)k));
-    const int avail = optin - (int)fa.sharedSizeBytes;
-    CUDA_TRY(cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, avail));
-    max_dyn[(const void*)k] = avail;
+  // dynamic shared memory available next to the kernel's static arrays (the
+  // opt-in is a per-device function attribute)
+  int avail = 0;
+  if (bulk) {
+    int st = dyn_smem_optin(c->device, (const void*)k, &avail);
+    if (st) return st;
   }
   int stages = c->bulk_rs;
   if (bulk)
-    while (stages > 1 && rs_smem_bytes(stages, c->bulk_stage) > (size_t)max_dyn[(const void*)k]) --stages;
+    while (stages > 1 && rs_smem_bytes(stages, c->bulk_stage) > (size_t)avail) --stages;
   P.bulk_rs = bulk ? stages : 0;
   P.bulk_stage = c->bulk_stage;
   const size_t dsm = bulk ? rs_smem_bytes(stages, c->bulk_stage) : 0;
@@ -457,8 +501,121 @@ struct Placement {
   bool recv_host = false;
 };
 
+// ---- automatic registration (the pointer cache's IPC side) ----------------
+typedef CUresult (*GetRangeFn)(CUdeviceptr*, size_t*, CUdeviceptr);
+typedef CUresult (*GetAttrFn)(void*, CUpointer_attribute, CUdeviceptr);
+
+template <class F>
+F driver_fn(const char* name) {
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return reinterpret_cast<F>(fn);
+}
+
+unsigned long long buffer_id_of(cm_comm* c, const void* ptr) {
+  static GetAttrFn get_attr = driver_fn<GetAttrFn>("cuPointerGetAttribute");
+  unsigned long long id = 0;
+  c->auto_checks += 1;
+  if (!get_attr || get_attr(&id, CU_POINTER_ATTRIBUTE_BUFFER_ID, reinterpret_cast<CUdeviceptr>(ptr)) != CUDA_SUCCESS)
+    return 0;
+  return id;
+}
+
+// Map the allocation slots peers have published since the last call (their
+// kernels report the counts in c->areg_host[q]): read the mailbox entries over
+// NVLink, open the IPC handles (cached), write AUTOTAB[slot][q] in my heap and
+// acknowledge in the peer's heap. Synchronous on a private stream; runs only
+// when a peer published something new.
+int service_autoreg(cm_comm* c) {
+  if (!c->areg_host) return CM_OK;
+  for (int q = 0; q < c->size; ++q) {
+    if (q == c->rank) continue;
+    const int64_t n = (int64_t) reinterpret_cast<volatile unsigned long long*>(c->areg_host)[q];
+    if (n <= c->mapped_seq[q]) continue;
+    const int64_t lo = c->mapped_seq[q], cnt = std::min<int64_t>(n, MAXAUTO) - lo;
+    if (cnt <= 0) continue;
+    unsigned char* mb = c->areg_pin;
+    unsigned long long* vals = reinterpret_cast<unsigned long long*>(c->areg_pin + MAXAUTO * MAILBOX_BYTES);
+    CUDA_TRY(cudaMemcpyAsync(mb, c->heap[q] + MAILBOX_OFF + lo * MAILBOX_BYTES, cnt * MAILBOX_BYTES,
+                             cudaMemcpyDeviceToHost, c->reg_stream));
+    CUDA_TRY(cudaStreamSynchronize(c->reg_stream));
+    for (int64_t i = 0; i < cnt; ++i) {
+      const std::string key = std::to_string(q) + ":" +
+                              std::string(reinterpret_cast<const char*>(mb + i * MAILBOX_BYTES), CM_IPC_HANDLE_BYTES);
+      auto it = c->opened.find(key);
+      char* base;
+      if (it != c->opened.end()) {
+        base = it->second;
+      } else {
+        cudaIpcMemHandle_t h;
+        memcpy(&h, mb + i * MAILBOX_BYTES, sizeof h);
+        void* mapped = nullptr;
+        CUDA_TRY(cudaIpcOpenMemHandle(&mapped, h, cudaIpcMemLazyEnablePeerAccess));
+        base = static_cast<char*>(mapped);
+        c->opened[key] = base;
+      }
+      vals[i] = reinterpret_cast<unsigned long long>(base);
+      CUDA_TRY(cudaMemcpyAsync(c->local + AUTOTAB_OFF + ((size_t)(lo + i) * MAXP + q) * 8, &vals[i], 8,
+                               cudaMemcpyHostToDevice, c->reg_stream));
+    }
+    vals[MAXAUTO] = (unsigned long long)(lo + cnt);
+    CUDA_TRY(cudaMemcpyAsync(c->heap[q] + ACK_OFF + (size_t)c->rank * 8, &vals[MAXAUTO], 8,
+                             cudaMemcpyHostToDevice, c->reg_stream));
+    CUDA_TRY(cudaStreamSynchronize(c->reg_stream));
+    c->mapped_seq[q] = lo + cnt;
+    c->auto_mapped += cnt;
+  }
+  return CM_OK;
+}
+
+// Mailbox slot of the allocation holding [ptr, ptr+bytes) (publishing it on
+// first sight), or -1 if it cannot be shared (not cudaMalloc memory, or the
+// mailbox is full). The allocation's buffer id is re-checked on every use so
+// a freed and re-allocated range at the same address gets a new slot.
+int64_t auto_slot(cm_comm* c, const void* ptr, int64_t bytes) {
+  static GetRangeFn get_range = driver_fn<GetRangeFn>("cuMemGetAddressRange");
+  const uintptr_t a = reinterpret_cast<uintptr_t>(ptr);
+  const unsigned long long bid = buffer_id_of(c, ptr);
+  auto it = c->autoregs.upper_bound(a);
+  if (it != c->autoregs.begin()) {
+    --it;
+    if (a + (uintptr_t)bytes <= it->first + it->second.size && it->second.buffer_id == bid && bid)
+      return it->second.slot;
+    if (a < it->first + it->second.size) c->autoregs.erase(it);     // stale: the range was re-allocated
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (!get_range || !bid || get_range(&base, &size, reinterpret_cast<CUdeviceptr>(ptr)) != CUDA_SUCCESS) return -1;
+  if (a + (uintptr_t)bytes > (uintptr_t)base + size) return -1;
+  cm_comm::AutoReg r{size, -1, bid};
+  cudaIpcMemHandle_t h;
+  if (c->reg_seq < MAXAUTO && cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)) == cudaSuccess) {
+    unsigned char* e = c->areg_pin;
+    memset(e, 0, MAILBOX_BYTES);
+    memcpy(e, &h, sizeof h);
+    memcpy(e + 64, &size, 8);
+    memcpy(e + 72, &bid, 8);
+    memcpy(e + 80, &base, 8);     // own entry of the slot table: the kernels resolve every rank's record
+    if (cudaMemcpyAsync(c->local + MAILBOX_OFF + (size_t)c->reg_seq * MAILBOX_BYTES, e, MAILBOX_BYTES,
+                        cudaMemcpyHostToDevice, c->reg_stream) == cudaSuccess &&
+        cudaMemcpyAsync(c->local + AUTOTAB_OFF + ((size_t)c->reg_seq * MAXP + c->rank) * 8, e + 80, 8,
+                        cudaMemcpyHostToDevice, c->reg_stream) == cudaSuccess &&
+        cudaStreamSynchronize(c->reg_stream) == cudaSuccess) {
+      r.slot = c->reg_seq++;
+      c->auto_published += 1;
+    }
+  }
+  cudaGetLastError();
+  c->autoregs[(uintptr_t)base] = r;
+  return r.slot;
+}
+
 int place(cm_comm* c, const void* send, int64_t send_bytes, void* recv, int64_t recv_bytes,
-          cudaStream_t stream, Placement* pl) {
+          cudaStream_t stream, Placement* pl, bool peers_read_send = false) {
   int ks = CM_KIND_DEVICE, kr = CM_KIND_DEVICE;
   int st;
   if (send_bytes > 0 && (st = classify(c, send, &ks))) return st;
@@ -485,6 +642,21 @@ int place(cm_comm* c, const void* send, int64_t send_bytes, void* recv, int64_t 
         pl->zc = (int64_t)(REG_FLAG | ((unsigned long long)it->second.id << 40) |
                            (unsigned long long)(a - it->first));
       }
+    }
+  }
+  if (pl->srcmode == SRC_COPYIN && ks == CM_KIND_DEVICE && peers_read_send && c->auto_reg && c->areg_host &&
+      send_bytes > 0) {
+    // automatic registration: peers read this allocation in place once every
+    // peer has mapped its mailbox slot; until then it is copied in
+    const int64_t slot = auto_slot(c, send, send_bytes);
+    const int64_t acked = (int64_t) reinterpret_cast<volatile unsigned long long*>(c->areg_host)[MAXP];
+    if (slot >= 0 && slot < acked) {
+      auto it = c->autoregs.upper_bound(reinterpret_cast<uintptr_t>(send));
+      --it;
+      pl->srcmode = SRC_REGISTERED;
+      pl->zc = (int64_t)(REG_FLAG | AUTO_FLAG | ((unsigned long long)slot << 40) |
+                         (unsigned long long)(reinterpret_cast<uintptr_t>(send) - it->first));
+      c->auto_zc_calls += 1;
     }
   }
   if (kr == CM_KIND_HOST) {
@@ -565,7 +737,9 @@ int do_allreduce(cm_comm* c, const void* const* sends, void* const* recvs, int64
   plan_algo(c, concrete, nbytes, &L);
   Placement pl;
   if (!c->virt) {
-    if ((st = place(c, sends[0], nbytes, recvs[0], nbytes, stream, &pl))) return st;
+    if ((st = service_autoreg(c))) return st;
+    const bool peers_read = !L.ll && !L.oneshot;    // the two-shot pull reads inputs in place
+    if ((st = place(c, sends[0], nbytes, recvs[0], nbytes, stream, &pl, peers_read))) return st;
     L.srcmode = pl.srcmode;
     L.in[0] = pl.in;
     L.out[0] = pl.out;
@@ -612,7 +786,8 @@ int do_rs(cm_comm* c, const void* const* sends, void* const* recvs, int64_t coun
   L.out_rel = 1;
   Placement pl;
   if (!c->virt) {
-    if ((st = place(c, sends[0], count * sz, recvs[0], len[c->rank] * sz, stream, &pl))) return st;
+    if ((st = service_autoreg(c))) return st;
+    if ((st = place(c, sends[0], count * sz, recvs[0], len[c->rank] * sz, stream, &pl, true))) return st;
     L.srcmode = pl.srcmode;
     L.in[0] = pl.in;
     L.out[0] = pl.out;
@@ -655,7 +830,8 @@ int do_ag(cm_comm* c, const void* const* sends, void* const* recvs, int64_t coun
   L.ag_in_rel = 1;
   Placement pl;
   if (!c->virt) {
-    if ((st = place(c, sends[0], len[c->rank] * sz, recvs[0], count * sz, stream, &pl))) return st;
+    if ((st = service_autoreg(c))) return st;
+    if ((st = place(c, sends[0], len[c->rank] * sz, recvs[0], count * sz, stream, &pl, true))) return st;
     L.srcmode = pl.srcmode;
     L.in[0] = pl.in;
     L.out[0] = pl.out;
@@ -696,12 +872,10 @@ int launch_batched_copy(cm_comm* c, int n, const void* const* srcs, void* const*
     for (int i = 0; i < m && aligned; ++i)
       aligned = ((((uintptr_t)P.src[i]) | ((uintptr_t)P.dst[i]) | (uintptr_t)nbytes[base + i]) & 15u) == 0;
     if (aligned) {
-      static bool attr_set = false;
-      if (!attr_set) {
-        CUDA_TRY(cudaFuncSetAttribute((const void*)bulk_copy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)BULK_SMEM));
-        attr_set = true;
-      }
+      int dev = 0, avail = 0;
+      CUDA_TRY(cudaGetDevice(&dev));
+      int st = dyn_smem_optin(dev, (const void*)bulk_copy_kernel, &avail, (int)BULK_SMEM);
+      if (st) return st;
       const int sms = c ? c->sms : 148;
       int64_t nb = (P.start[m] + 4 * BULK_CHUNK - 1) / (4 * BULK_CHUNK);
       nb = std::max<int64_t>(1, std::min<int64_t>(nb, 2 * (int64_t)sms));
@@ -876,6 +1050,13 @@ int cm_comm_connect(cm_comm_t* c, const void* all_handles) {
     if (e != cudaSuccess) return cuda_fail(e, ("cudaIpcOpenMemHandle(peer " + std::to_string(q) + ")").c_str());
     c->heap[q] = static_cast<char*>(ptr);
   }
+  if (c->size > 1) {
+    CUDA_TRY(cudaHostAlloc(&c->areg_host, (MAXP + 1) * sizeof(unsigned long long), cudaHostAllocMapped));
+    CUDA_TRY(cudaHostGetDevicePointer((void**)&c->areg_dev, c->areg_host, 0));
+    memset(c->areg_host, 0, (MAXP + 1) * sizeof(unsigned long long));
+    CUDA_TRY(cudaHostAlloc(&c->areg_pin, MAXAUTO * MAILBOX_BYTES + (MAXAUTO + 1) * 8, cudaHostAllocDefault));
+    CUDA_TRY(cudaStreamCreateWithFlags(&c->reg_stream, cudaStreamNonBlocking));
+  }
   c->connected = true;
   return CM_OK;
 }
@@ -921,6 +1102,10 @@ int cm_comm_destroy(cm_comm_t* c) {
   for (auto& kv : c->gtabs) cudaFree(kv.second);
   if (c->local) cudaFree(c->local);
   if (c->scratch) cudaFree(c->scratch);
+  if (c->agree_in) cudaFree(c->agree_in);
+  if (c->areg_host) cudaFreeHost(c->areg_host);
+  if (c->areg_pin) cudaFreeHost(c->areg_pin);
+  if (c->reg_stream) cudaStreamDestroy(c->reg_stream);
   if (c->indev) cudaFree(c->indev);
   if (c->outdev) cudaFree(c->outdev);
   if (c->h2d) cudaStreamDestroy(c->h2d);
@@ -975,7 +1160,7 @@ int cm_comm_set_param(cm_comm_t* c, const char* key, int64_t value) {
   else if (k == "bulk_rs") c->bulk_rs = value == 1 ? 0 : (int)std::min<int64_t>(value, RS_MAX_STAGES);
   else if (k == "dyn_ag") c->dyn_ag = value > 1 ? 1 : 0;
   else if (k == "inline_agree") c->inline_agree = value > 1 ? 1 : 0;
-  else if (k == "bulk_local") c->bulk_local = value > 1 ? 1 : 0;
+  else if (k == "auto_register") c->auto_reg = value > 1 ? 1 : 0;
   else if (k == "host_chunk_kb") c->host_chunk = std::max<int64_t>(64, value) * 1024;
   else if (k == "bulk_stage_kb") c->bulk_stage = (int)std::max<int64_t>(4, std::min<int64_t>(value, 112)) * 1024;
   else if (k == "oneshot_bytes_per_cta") c->oneshot_bytes_per_cta = value;
@@ -999,7 +1184,11 @@ int cm_comm_get_param(cm_comm_t* c, const char* key, int64_t* value) {
   else if (k == "bulk_rs") *value = c->bulk_rs ? c->bulk_rs : 1;
   else if (k == "dyn_ag") *value = c->dyn_ag ? 2 : 1;
   else if (k == "inline_agree") *value = c->inline_agree ? 2 : 1;
-  else if (k == "bulk_local") *value = c->bulk_local ? 2 : 1;
+  else if (k == "auto_register") *value = c->auto_reg ? 2 : 1;
+  else if (k == "auto_published") *value = c->auto_published;
+  else if (k == "auto_mapped") *value = c->auto_mapped;
+  else if (k == "auto_zero_copy_calls") *value = c->auto_zc_calls;
+  else if (k == "auto_buffer_checks") *value = c->auto_checks;
   else if (k == "bulk_stage_kb") *value = c->bulk_stage / 1024;
   else if (k == "host_chunk_kb") *value = c->host_chunk / 1024;
   else if (k == "oneshot_bytes_per_cta") *value = c->oneshot_bytes_per_cta;
@@ -1105,6 +1294,22 @@ int cm_comm_register(cm_comm_t* c, const void* ptr, int64_t bytes, const void* a
   return CM_OK;
 }
 
+// virtual group: every local rank's buffer under one id (the registered-buffer
+// table of every virtual rank's heap holds all of them; no IPC involved)
+int cm_comm_register_v(cm_comm_t* c, const void* const* ptrs, int64_t bytes, int64_t* reg_id) {
+  if (!c->virt) return fail(CM_ERR_UNSUPPORTED, "cm_comm_register_v needs a virtual group");
+  if (c->next_reg >= MAXREG) return fail(CM_ERR_CONFIG, "registered-buffer table is full");
+  if (bytes < 0) return fail(CM_ERR_VALUE, "negative size");
+  const char* table[MAXP] = {};
+  for (int q = 0; q < c->size; ++q) table[q] = static_cast<const char*>(ptrs[q]);
+  const int64_t id = c->next_reg++;
+  for (int q = 0; q < c->size; ++q)
+    CUDA_TRY(cudaMemcpy(c->heap[q] + REG_OFF + (size_t)id * MAXP * 8, table, sizeof(char*) * MAXP,
+                        cudaMemcpyHostToDevice));
+  *reg_id = id;
+  return CM_OK;
+}
+
 int cm_comm_deregister(cm_comm_t* c, const void* ptr) {
   auto it = c->regs.find(reinterpret_cast<uintptr_t>(ptr));
   if (it == c->regs.end()) return fail(CM_ERR_INVALID_HANDLE, "buffer is not registered");
@@ -1120,48 +1325,66 @@ int cm_comm_sync(cm_comm_t* c, void* stream) {
 
 int cm_comm_poll(cm_comm_t* c) { return check_async_error(c); }
 
+}  // extern "C"
+
 // Element-wise MAX over ranks of n int64 host values, synchronously: the
 // control-plane primitive behind negotiate_ready's fast path (one one-shot
 // kernel over NVLink instead of a host gather/broadcast).
-}  // extern "C"
-
 namespace {
-// launch half of cm_agree: values travel in the kernel parameters, the result
-// lands in mapped host memory with a completion ticket
+// Agreement words in mapped pinned memory (int64 indices):
+//   AGH_RES + 8*lr   cm_agree maxima of local rank lr
+//   AGH_DONE + lr    completion ticket of the LL agreement kernel (per local rank)
+//   AGH_INL + 2*lr   inline agreement {ticket, ok} written by CTA 0 of the first collective
+//   AGH_IN + 8*lr    staging of the virtual ranks' agreement inputs
+constexpr int AGH_RES = 0, AGH_DONE = 8 * MAXP, AGH_INL = 9 * MAXP, AGH_IN = 11 * MAXP, AGH_WORDS = 19 * MAXP;
+
 int ensure_agree_buf(cm_comm* c) {
   if (!c->agree_host) {
-    CUDA_TRY(cudaHostAlloc(&c->agree_host, 16 * sizeof(int64_t), cudaHostAllocMapped));
+    CUDA_TRY(cudaHostAlloc(&c->agree_host, AGH_WORDS * sizeof(int64_t), cudaHostAllocMapped));
     CUDA_TRY(cudaHostGetDevicePointer((void**)&c->agree_dev, c->agree_host, 0));
-    memset(c->agree_host, 0, 16 * sizeof(int64_t));
+    memset(c->agree_host, 0, AGH_WORDS * sizeof(int64_t));
   }
+  if (c->virt && !c->agree_in) CUDA_TRY(cudaMalloc(&c->agree_in, 8 * MAXP * sizeof(int64_t)));
   return CM_OK;
 }
 
-// inline agreement: CTA 0 of the first collective writes {ticket, ok} to
-// agree_host[12..13] right after its start barrier
-int inline_agree_wait(cm_comm* c, unsigned long long ticket, cudaStream_t stream, int* agreed) {
-  volatile unsigned long long* flag = reinterpret_cast<volatile unsigned long long*>(c->agree_host + 12);
+// host spin on a mapped completion word (bounded; device errors end it early)
+int spin_ticket(cm_comm* c, int64_t idx, unsigned long long ticket, cudaStream_t stream, const char* what) {
+  volatile unsigned long long* flag = reinterpret_cast<volatile unsigned long long*>(c->agree_host + idx);
   const auto t0 = std::chrono::steady_clock::now();
   while (*flag != ticket) {
     if (*reinterpret_cast<volatile unsigned*>(c->herr_host)) break;
     if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(60)) {
       cudaError_t e = cudaStreamQuery(stream);
-      if (e != cudaErrorNotReady && e != cudaSuccess) return cuda_fail(e, "aggregate agreement");
-      return fail(CM_ERR_TRANSPORT, "aggregate agreement: peers did not answer within 60 s");
+      if (e != cudaErrorNotReady && e != cudaSuccess) return cuda_fail(e, what);
+      return fail(CM_ERR_TRANSPORT, std::string(what) + ": peers did not answer within 60 s");
     }
   }
-  int st = check_async_error(c);
-  if (st) return st;
-  *agreed = reinterpret_cast<volatile unsigned long long*>(c->agree_host)[13] ? 1 : 0;
+  return check_async_error(c);
+}
+
+// inline agreement: CTA 0 of the first collective of every local rank writes
+// {ticket, ok} right after its start barrier
+int inline_agree_wait(cm_comm* c, unsigned long long ticket, cudaStream_t stream, int* agreed) {
+  const int nloc = c->virt ? c->size : 1;
+  for (int lr = 0; lr < nloc; ++lr) {
+    int st = spin_ticket(c, AGH_INL + 2 * lr, ticket, stream, "aggregate agreement");
+    if (st) return st;
+    agreed[lr] = reinterpret_cast<volatile int64_t*>(c->agree_host)[AGH_INL + 2 * lr + 1] ? 1 : 0;
+  }
   return CM_OK;
 }
 
+// launch half of cm_agree: an LL one-shot MAX over the ranks' n values (same
+// shape on every rank); the result lands in mapped host memory with a
+// completion ticket, and the last CTA leaves {agree_tag, agree_ok} in Ctrl for
+// gated collectives queued behind it. values: nloc * n (local-rank major).
 int agree_launch(cm_comm* c, const int64_t* values, int n, cudaStream_t stream,
                  unsigned long long* ticket_out) {
   int st0 = ensure_agree_buf(c);
   if (st0) return st0;
+  const int nloc = c->virt ? c->size : 1;
   long long inl[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  for (int i = 0; i < n; ++i) inl[i] = values[i];
   const unsigned long long ticket = ++c->agree_ticket;
   Launch L;
   L.n = n;
@@ -1170,10 +1393,22 @@ int agree_launch(cm_comm* c, const int64_t* values, int n, cudaStream_t stream,
   plan_algo(c, CM_ALGO_RHD, n * 8, &L);
   L.ll = 1;
   L.oneshot = 1;
-  L.srcmode = SRC_INLINE;
-  L.inl = inl;
-  L.out[0] = c->agree_dev;
-  L.done_flag = reinterpret_cast<unsigned long long*>(c->agree_dev + 8);
+  if (!c->virt) {
+    for (int i = 0; i < n; ++i) inl[i] = values[i];
+    L.srcmode = SRC_INLINE;
+    L.inl = inl;
+  } else {
+    // every local rank's values: pinned staging -> device (the host does not
+    // touch the staging again before this call's completion word is seen)
+    for (int lr = 0; lr < nloc; ++lr)
+      for (int i = 0; i < 8; ++i) c->agree_host[AGH_IN + 8 * lr + i] = i < n ? values[lr * n + i] : 0;
+    CUDA_TRY(cudaMemcpyAsync(c->agree_in, c->agree_host + AGH_IN, 8 * nloc * sizeof(int64_t),
+                             cudaMemcpyHostToDevice, stream));
+    L.srcmode = SRC_COPYIN;
+    for (int lr = 0; lr < nloc; ++lr) L.in[lr] = c->agree_in + 8 * lr;
+  }
+  for (int lr = 0; lr < nloc; ++lr) L.out[lr] = c->agree_dev + AGH_RES + 8 * lr;
+  L.done_flag = reinterpret_cast<unsigned long long*>(c->agree_dev + AGH_DONE);
   L.done_value = ticket;
   int st = launch_collective(c, L, stream);
   if (st) return st;
@@ -1181,39 +1416,42 @@ int agree_launch(cm_comm* c, const int64_t* values, int n, cudaStream_t stream,
   return CM_OK;
 }
 
-// wait half: host spin on the completion word
+// wait half: host spin on every local rank's completion word; maxes: nloc * n
 int agree_wait(cm_comm* c, unsigned long long ticket, int n, int64_t* maxes, cudaStream_t stream) {
-  volatile unsigned long long* flag = reinterpret_cast<volatile unsigned long long*>(c->agree_host + 8);
-  const auto t0 = std::chrono::steady_clock::now();
-  while (*flag != ticket) {
-    if (*reinterpret_cast<volatile unsigned*>(c->herr_host)) break;
-    if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(60)) {
-      cudaError_t e = cudaStreamQuery(stream);
-      if (e != cudaErrorNotReady && e != cudaSuccess) return cuda_fail(e, "cm_agree");
-      return fail(CM_ERR_TRANSPORT, "cm_agree: peers did not answer within 60 s");
-    }
+  const int nloc = c->virt ? c->size : 1;
+  for (int lr = 0; lr < nloc; ++lr) {
+    int st = spin_ticket(c, AGH_DONE + lr, ticket, stream, "cm_agree");
+    if (st) return st;
+    for (int i = 0; i < n; ++i)
+      maxes[lr * n + i] = reinterpret_cast<volatile int64_t*>(c->agree_host)[AGH_RES + 8 * lr + i];
   }
-  int st = check_async_error(c);
-  if (st) return st;
-  for (int i = 0; i < n; ++i) maxes[i] = reinterpret_cast<volatile int64_t*>(c->agree_host)[i];
   return CM_OK;
 }
-}  // namespace
 
-extern "C" {
-
-int cm_agree(cm_comm_t* c, const int64_t* values, int n, int64_t* maxes, void* stream_) {
+int agree_impl(cm_comm* c, const int64_t* values, int n, int64_t* maxes, cudaStream_t stream) {
   if (n < 1 || n > 8) return fail(CM_ERR_VALUE, "cm_agree takes 1..8 values");
-  if (c->virt) return fail(CM_ERR_UNSUPPORTED, "cm_agree needs a real communicator");
-  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  int st = check_async_error(c);
+  if (st) return st;
   if (c->size == 1) {
     memcpy(maxes, values, n * sizeof(int64_t));
     return CM_OK;
   }
   unsigned long long ticket;
-  int st = agree_launch(c, values, n, stream, &ticket);
-  if (st) return st;
+  if ((st = agree_launch(c, values, n, stream, &ticket))) return st;
   return agree_wait(c, ticket, n, maxes, stream);
+}
+}  // namespace
+
+extern "C" {
+
+int cm_agree(cm_comm_t* c, const int64_t* values, int n, int64_t* maxes, void* stream) {
+  if (c->virt) return fail(CM_ERR_UNSUPPORTED, "use cm_agree_v on a virtual group");
+  return agree_impl(c, values, n, maxes, static_cast<cudaStream_t>(stream));
+}
+
+int cm_agree_v(cm_comm_t* c, const int64_t* values, int n, int64_t* maxes, void* stream) {
+  if (!c->virt) return fail(CM_ERR_UNSUPPORTED, "cm_agree_v needs a virtual group");
+  return agree_impl(c, values, n, maxes, static_cast<cudaStream_t>(stream));
 }
 
 int cm_comm_counters(cm_comm_t* c, int64_t* messages_sent, int64_t* bytes_sent,
@@ -1301,161 +1539,117 @@ int cm_allgather_v(cm_comm_t* c, const void* const* sends, void* const* recvs, i
   return do_ag(c, sends, recvs, count, dtype, layout, stream, stats);
 }
 
-int cm_fused_allreduce(cm_comm_t* c, int n, const void* const* sends, const int64_t* counts,
-                       int dtype, void* recv_fused, int algo, int64_t threshold,
-                       int64_t switch_bytes, int average, void* stream_, cm_stats_t* stats,
-                       int* n_calls) {
-  return cm_fused_allreduce_agreed(c, n, sends, counts, dtype, recv_fused, algo, threshold,
-                                   switch_bytes, average, nullptr, 0, nullptr, nullptr, stream_,
-                                   stats, n_calls);
-}
+}  // extern "C"
 
-int cm_fused_allreduce_agreed(cm_comm_t* c, int n, const void* const* sends,
-                              const int64_t* counts, int dtype, void* recv_fused, int algo,
-                              int64_t threshold, int64_t switch_bytes, int average,
-                              const int64_t* agree_values, int n_agree, int* agreed,
-                              const int64_t* reg_ids, void* stream_, cm_stats_t* stats,
-                              int* n_calls) {
-  if (c->virt) return fail(CM_ERR_UNSUPPORTED, "fused allreduce needs a real communicator");
+namespace {
+
+// aggregate() hot loop (aggregation.py:138-176) for every local rank of the
+// communicator (nloc = size on a virtual group, else 1):
+//   sends[lr * n + k]   member k of local rank lr (device, pinned or pageable host)
+//   recvs[lr]           its concatenated means (device or host)
+//   agree_values[lr * n_agree + i], agreed[lr], stats[lr * n + g]
+// Call structure under a pending agreement is the same on every rank whatever
+// its plan: the first launch either is the LL agreement kernel or carries the
+// agreement inline on the full grid (force_pull); every later collective is
+// gated and, on a mismatch, returns without a barrier or an epoch advance.
+int fused_impl(cm_comm* c, int n, const void* const* sends, const int64_t* counts, int dtype,
+               void* const* recvs, int algo, int64_t threshold, int64_t switch_bytes, int average,
+               const int64_t* agree_values, int n_agree, int* agreed, const int64_t* reg_ids,
+               cudaStream_t stream, cm_stats_t* stats, int* n_calls) {
   int st = check_dtype_op(dtype, CM_SUM);
   if (st) return st;
   if (average && (dtype == CM_INT32 || dtype == CM_INT64))
     return fail(CM_ERR_SHAPE, "averaging needs a floating-point dtype");
   if ((st = check_async_error(c))) return st;
   if (threshold <= 0) return fail(CM_ERR_VALUE, "fusion threshold must be positive");
-  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  if (n < 0) return fail(CM_ERR_VALUE, "negative member count");
+  if (n_agree < 0 || n_agree > 4) return fail(CM_ERR_VALUE, "at most 4 agreement values");
+  for (int k = 0; k < n; ++k)
+    if (counts[k] < 0) return fail(CM_ERR_SHAPE, "negative element count");
+  const int p = c->size;
+  const int nloc = c->virt ? p : 1;
   *n_calls = 0;
-  // negotiation fast path (aggregation.py:72-92): every rank must hold the
-  // same values, checked as max(v) == v and max(-v) == -v in one one-shot MAX
-  // allreduce. The check is launched first; the first pack (local only) is
-  // queued behind it before the host waits, and the first collective is
-  // launched only once agreement is known.
-  int64_t agree_vals[8];
-  unsigned long long ticket = 0;
-  bool pending = false, inline_agree = false;
-  if (n_agree > 4) return fail(CM_ERR_VALUE, "at most 4 agreement values");
-  if (n_agree > 0) *agreed = 1;
-  // started after the plan is known (below): either inline in the collectives'
-  // records, or as a separate LL check kernel when a group takes an LL kernel
-  auto start_agree = [&](bool all_pull) -> int {
-    if (n_agree <= 0 || c->size == 1) return CM_OK;
-    if (all_pull && n_agree == 2 && !c->rhd_logp && c->inline_agree) {
-      int s2 = ensure_agree_buf(c);
-      if (s2) return s2;
-      ticket = ++c->agree_ticket;
-      inline_agree = pending = true;
-      return CM_OK;
-    }
-    for (int i = 0; i < n_agree; ++i) { agree_vals[i] = agree_values[i]; agree_vals[n_agree + i] = -agree_values[i]; }
-    int s2 = agree_launch(c, agree_vals, 2 * n_agree, stream, &ticket);
-    if (s2) return s2;
-    pending = true;
-    return CM_OK;
-  };
-  auto tag_launch = [&](Launch& L) {
-    if (!inline_agree) return;
-    L.agree_inline = 1;
-    L.akey = agree_values[0];
-    L.acnt = agree_values[1];
-    L.agree_out = reinterpret_cast<unsigned long long*>(c->agree_dev + 12);
-    L.agree_ticket = ticket;
-  };
-  auto resolve_agree = [&]() -> int {
-    if (!pending) return CM_OK;
-    pending = false;
-    if (inline_agree) {
-      int s2 = inline_agree_wait(c, ticket, stream, agreed);
-      inline_agree = false;
-      return s2;
-    }
-    int64_t mx[8];
-    int s2 = agree_wait(c, ticket, 2 * n_agree, mx, stream);
-    if (s2) return s2;
-    bool same = true;
-    for (int i = 0; i < 2 * n_agree; ++i) same = same && mx[i] == agree_vals[i];
-    *agreed = same ? 1 : 0;
-    return CM_OK;
-  };
+  if (n_agree > 0)
+    for (int lr = 0; lr < nloc; ++lr) agreed[lr] = 1;
   const int64_t sz = (int64_t)dtype_size(dtype);
   std::vector<int64_t> nbytes(n);
   std::vector<int> dts(n, dtype), group(n);
-  for (int i = 0; i < n; ++i) nbytes[i] = counts[i] * sz;
+  int64_t total_bytes = 0;
+  for (int i = 0; i < n; ++i) {
+    nbytes[i] = counts[i] * sz;
+    total_bytes += nbytes[i];
+  }
   int ngroups = 0;
-  cm_fuse_plan(n, nbytes.data(), dts.data(), threshold, group.data(), &ngroups);
-  int rk;
-  if ((st = classify(c, recv_fused, &rk))) return st;
-  const bool out_host = rk == CM_KIND_HOST;
-  if (out_host && c->virt) return fail(CM_ERR_UNSUPPORTED, "virtual groups need device buffers");
-  const int p = c->size;
+  if (n > 0) cm_fuse_plan(n, nbytes.data(), dts.data(), threshold, group.data(), &ngroups);
+  auto rank_of = [&](int lr) { return c->virt ? lr : c->rank; };
+  // every member of every local rank is classified once per call through the
+  // pointer cache (aggregation.py:159-161), and so is every output
+  std::vector<int> kinds((size_t)nloc * n, CM_KIND_DEVICE);
+  bool any_host_in = false, out_host = false, out_dev = false;
+  for (int lr = 0; lr < nloc; ++lr) {
+    for (int k = 0; k < n; ++k)
+      if (counts[k] > 0 && (st = classify(c, sends[(size_t)lr * n + k], &kinds[(size_t)lr * n + k]))) return st;
+    int rk = CM_KIND_DEVICE;
+    if (total_bytes > 0 && (st = classify(c, recvs[lr], &rk))) return st;
+    (rk == CM_KIND_HOST ? out_host : out_dev) = true;
+  }
+  for (int v : kinds) any_host_in = any_host_in || v == CM_KIND_HOST;
+  if (out_host && out_dev) return fail(CM_ERR_UNSUPPORTED, "local ranks mix host and device outputs");
   HostPipe hp(c, stream);
   if (p == 1) {
     // single rank: every allreduce is the identity and the mean divides by 1
     // (collectives.py:119-120), so all fused groups collapse into ONE batched
     // copy of the members into the concatenated output
-    bool any_host = false;
     std::vector<const void*> srcs(n);
     std::vector<void*> dsts(n);
-    std::vector<int64_t> bytes(n);
-    std::vector<int> kinds(n, CM_KIND_DEVICE);
     int64_t off = 0;
     for (int k = 0; k < n; ++k) {
-      int kind = CM_KIND_DEVICE;
-      if (counts[k] > 0 && (st = classify(c, sends[k], &kind))) return st;
-      any_host = any_host || kind == CM_KIND_HOST;
-      kinds[k] = kind;
       srcs[k] = sends[k];
-      dsts[k] = static_cast<char*>(recv_fused) + off;
-      bytes[k] = counts[k] * sz;
-      off += bytes[k];
+      dsts[k] = static_cast<char*>(recvs[0]) + off;
+      off += nbytes[k];
     }
     for (int g = 0; g < ngroups; ++g) {
       stats[g] = cm_stats_t{0, 0, 0};
       count_stats(c, stats[g]);
     }
-    if (any_host || out_host) {
+    if (any_host_in || out_host) {
       // H2D into the device (h2d stream) and, for host outputs, D2H back out
-      // (d2h stream) in ~16 MiB chunks so both PCIe directions stream at once
+      // (d2h stream) in host_chunk pieces so both PCIe directions stream at
+      // once; members adjacent in memory are copied as one run (one DMA)
       if ((st = hp.start(out_host ? off : 0, 0))) return st;
-      // members adjacent in memory are copied as one run (one DMA), runs are
-      // cut into 16 MiB pieces, and the fused result (contiguous) leaves in
-      // one D2H per piece
-      std::vector<Run> runs = coalesce(srcs.data(), bytes.data(), n, c->host_chunk);
+      std::vector<Run> runs = coalesce(srcs.data(), nbytes.data(), n, c->host_chunk);
       int64_t chunk_lo = 0;
       for (size_t k = 0; k < runs.size(); ++k) {
         const Run& r = runs[k];
-        CUDA_TRY(cudaMemcpyAsync((out_host ? c->indev : static_cast<char*>(recv_fused)) + r.off, r.src, r.bytes,
+        CUDA_TRY(cudaMemcpyAsync((out_host ? c->indev : static_cast<char*>(recvs[0])) + r.off, r.src, r.bytes,
                                  cudaMemcpyDefault, c->h2d));
         const int64_t end = r.off + r.bytes;
         if (out_host && (end - chunk_lo >= c->host_chunk || k + 1 == runs.size())) {
           if ((st = hp.link(c->h2d, c->d2h))) return st;
-          CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(recv_fused) + chunk_lo, c->indev + chunk_lo, end - chunk_lo,
+          CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(recvs[0]) + chunk_lo, c->indev + chunk_lo, end - chunk_lo,
                                    cudaMemcpyDeviceToHost, c->d2h));
           chunk_lo = end;
         }
       }
       if ((st = hp.join())) return st;
-    } else if ((st = launch_batched_copy(c, n, srcs.data(), dsts.data(), bytes.data(), false, stream))) {
+    } else if ((st = launch_batched_copy(c, n, srcs.data(), dsts.data(), nbytes.data(), false, stream))) {
       return st;
     }
     *n_calls = ngroups;
     return CM_OK;
   }
-  // host inputs or outputs: start the copy-stream pipeline (device buffers
-  // sized for the whole call) before the plan takes outdev addresses
-  bool any_host_in = false;
-  int64_t total_bytes = 0;
-  std::vector<int> kinds(n, CM_KIND_DEVICE);
-  for (int k = 0; k < n; ++k) {
-    if (counts[k] > 0 && (st = classify(c, sends[k], &kinds[k]))) return st;
-    any_host_in = any_host_in || kinds[k] == CM_KIND_HOST;
-    total_bytes += counts[k] * sz;
-  }
-  if ((any_host_in || out_host) && (st = hp.start(any_host_in ? total_bytes : 0, out_host ? total_bytes : 0)))
+  // host inputs or outputs: the copy-stream pipeline (device buffers sized for
+  // every local rank's whole call) starts before the plan takes their addresses
+  if ((any_host_in || out_host) &&
+      (st = hp.start(any_host_in ? nloc * total_bytes : 0, out_host ? nloc * total_bytes : 0)))
     return st;
+  auto outbase = [&](int lr) -> char* {
+    return out_host ? c->outdev + (int64_t)lr * total_bytes : static_cast<char*>(recvs[lr]);
+  };
   // Pass 1: per fused group, members, size, algorithm and launch plan
   struct Grp {
     int i, j;
-    int64_t ng, off;   // elements, offset in recv_fused
+    int64_t ng, off;   // elements, offset in the fused output
     bool any_host;
     Launch L;
     bool batchable;
@@ -1471,8 +1665,7 @@ int cm_fused_allreduce_agreed(cm_comm_t* c, int n, const void* const* sends,
       G.any_host = false;
       int j = i;
       while (j < n && group[j] == g) {
-        // aggregation.py:159-161: every member classified once per call (above)
-        G.any_host = G.any_host || (kinds[j] == CM_KIND_HOST);
+        for (int lr = 0; lr < nloc; ++lr) G.any_host = G.any_host || kinds[(size_t)lr * n + j] == CM_KIND_HOST;
         G.ng += counts[j];
         ++j;
       }
@@ -1480,7 +1673,8 @@ int cm_fused_allreduce_agreed(cm_comm_t* c, int n, const void* const* sends,
       G.off = fused_off;
       int concrete;
       if ((st = cm_resolve_algorithm(algo, G.ng * sz, switch_bytes, &concrete))) return st;
-      cm_algo_stats(concrete, p, c->rank, G.ng, dtype, switch_bytes, &stats[g]);
+      for (int lr = 0; lr < nloc; ++lr)
+        cm_algo_stats(concrete, p, rank_of(lr), G.ng, dtype, switch_bytes, &stats[(size_t)lr * n + g]);
       if (G.ng * sz > (int64_t)c->staging_bytes)
         return fail(CM_ERR_CONFIG, "fused buffer of " + std::to_string(G.ng * sz) +
                                        " B exceeds the staging area; lower the fusion threshold");
@@ -1489,7 +1683,7 @@ int cm_fused_allreduce_agreed(cm_comm_t* c, int n, const void* const* sends,
       G.L.op = CM_SUM;
       G.L.average = average;
       plan_algo(c, concrete, G.ng * sz, &G.L);
-      G.L.out[0] = (out_host ? c->outdev : static_cast<char*>(recv_fused)) + fused_off * sz;
+      for (int lr = 0; lr < nloc; ++lr) G.L.out[lr] = outbase(lr) + fused_off * sz;
       G.batchable = c->multi_buffer && !G.any_host && G.L.ll == 0 && !G.L.oneshot &&
                     G.L.phases == (PH_RS | PH_AG);
       gr.push_back(G);
@@ -1497,21 +1691,52 @@ int cm_fused_allreduce_agreed(cm_comm_t* c, int n, const void* const* sends,
       i = j;
     }
   }
-  {
-    bool all_pull = true;
-    for (const Grp& G : gr) all_pull = all_pull && G.L.ll == 0;
-    if ((st = start_agree(all_pull))) return st;
+  // agreement (negotiate_ready fast path, aggregation.py:72-92)
+  const bool want_agree = n_agree > 0;
+  const bool inline_mode = want_agree && n_agree == 2 && c->inline_agree && !gr.empty();
+  unsigned long long ticket = 0;
+  if (want_agree) {
+    if ((st = ensure_agree_buf(c))) return st;
+    if (inline_mode) {
+      ticket = ++c->agree_ticket;
+    } else {
+      std::vector<int64_t> vals((size_t)nloc * 2 * n_agree);
+      for (int lr = 0; lr < nloc; ++lr)
+        for (int i = 0; i < n_agree; ++i) {
+          vals[(size_t)lr * 2 * n_agree + i] = agree_values[lr * n_agree + i];
+          vals[(size_t)lr * 2 * n_agree + n_agree + i] = -agree_values[lr * n_agree + i];
+        }
+      if ((st = agree_launch(c, vals.data(), 2 * n_agree, stream, &ticket))) return st;
+    }
   }
+  bool first_launch = true;
+  auto tag_launch = [&](Launch& L) {
+    if (!want_agree) return;
+    if (inline_mode && first_launch) {
+      L.agree_inline = 1;
+      L.force_pull = 1;
+      for (int lr = 0; lr < nloc; ++lr) {
+        L.akey[lr] = agree_values[lr * n_agree];
+        L.acnt[lr] = agree_values[lr * n_agree + 1];
+      }
+      L.agree_out = reinterpret_cast<unsigned long long*>(c->agree_dev + AGH_INL);
+      L.agree_ticket = ticket;
+    } else {
+      L.agree_gate = ticket;
+    }
+    first_launch = false;
+  };
   // host-input groups: every group's H2D is queued up front on the h2d stream
-  // (into indev at the group's fused offset); each collective waits only for
-  // its own group's event
+  // (into indev at the local rank's and the group's offset); each collective
+  // waits only for its own group's event
   std::vector<cudaEvent_t> in_ready(gr.size(), nullptr);
+  auto indev_at = [&](int lr, const Grp& G) { return c->indev + (int64_t)lr * total_bytes + G.off * sz; };
   for (size_t t = 0; t < gr.size(); ++t) {
     if (!gr[t].any_host) continue;
-    std::vector<int64_t> gb;
-    for (int k = gr[t].i; k < gr[t].j; ++k) gb.push_back(counts[k] * sz);
-    for (const Run& r : coalesce(sends + gr[t].i, gb.data(), gr[t].j - gr[t].i, INT64_MAX))
-      CUDA_TRY(cudaMemcpyAsync(c->indev + gr[t].off * sz + r.off, r.src, r.bytes, cudaMemcpyDefault, c->h2d));
+    std::vector<int64_t> gb(nbytes.begin() + gr[t].i, nbytes.begin() + gr[t].j);
+    for (int lr = 0; lr < nloc; ++lr)
+      for (const Run& r : coalesce(sends + (size_t)lr * n + gr[t].i, gb.data(), gr[t].j - gr[t].i, INT64_MAX))
+        CUDA_TRY(cudaMemcpyAsync(indev_at(lr, gr[t]) + r.off, r.src, r.bytes, cudaMemcpyDefault, c->h2d));
     if ((st = hp.ev(&in_ready[t]))) return st;
     CUDA_TRY(cudaEventRecord(in_ready[t], c->h2d));
   }
@@ -1522,8 +1747,24 @@ int cm_fused_allreduce_agreed(cm_comm_t* c, int n, const void* const* sends,
     if (s2) return s2;
     for (size_t t = a; t < b; ++t)
       if (gr[t].ng)
-        CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(recv_fused) + gr[t].off * sz, c->outdev + gr[t].off * sz,
-                                 gr[t].ng * sz, cudaMemcpyDeviceToHost, c->d2h));
+        for (int lr = 0; lr < nloc; ++lr)
+          CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(recvs[lr]) + gr[t].off * sz, outbase(lr) + gr[t].off * sz,
+                                   gr[t].ng * sz, cudaMemcpyDeviceToHost, c->d2h));
+    return CM_OK;
+  };
+  // pack members [i, j) of every local rank into its staging (byte offsets from `base`)
+  auto pack = [&](int i, int j) -> int {
+    std::vector<void*> dsts;
+    int64_t o = 0;
+    for (int k = i; k < j; ++k) {
+      dsts.push_back(reinterpret_cast<void*>((uintptr_t)o));
+      o += nbytes[k];
+    }
+    for (int lr = 0; lr < nloc; ++lr) {
+      int s2 = launch_batched_copy(c, j - i, sends + (size_t)lr * n + i, dsts.data(), nbytes.data() + i, true, stream,
+                                   c->virt ? c->heap[lr] : nullptr);
+      if (s2) return s2;
+    }
     return CM_OK;
   };
   // Pass 2: launches. Consecutive two-shot groups with the same layout share
@@ -1544,78 +1785,51 @@ int cm_fused_allreduce_agreed(cm_comm_t* c, int n, const void* const* sends,
     if (gather_ok)
       for (size_t t = g; t < h && gather_ok; ++t)
         for (int k = gr[t].i; k < gr[t].j; ++k) gather_ok = gather_ok && reg_ids[k] >= 0;
-    if (gather_ok) {
-      // registered gradients: peers' members are read in place, no pack
+    if (gather_ok || h - g > 1) {
       Launch L = gr[g].L;
       L.nbuf = (int)(h - g);
-      std::vector<long long> tab;
-      std::vector<long long> ids;
+      for (int lr = 0; lr < nloc; ++lr) L.out[lr] = outbase(lr);
       int64_t boff = 0;
-      tab.push_back(0);
       for (size_t t = g; t < h; ++t) {
         L.bn[t - g] = gr[t].ng;
         L.bboff[t - g] = boff;
-        L.bout[t - g] = gr[t].L.out[0];
-        for (int k = gr[t].i; k < gr[t].j; ++k) {
-          boff += counts[k];
-          tab.push_back(boff);
-          ids.push_back(reg_ids[k]);
-        }
+        L.bout_off[t - g] = gr[t].off;
+        boff += gr[t].ng;
       }
-      const int gm = (int)ids.size();
-      tab.insert(tab.end(), ids.begin(), ids.end());
-      std::string key(reinterpret_cast<const char*>(tab.data()), tab.size() * sizeof(long long));
-      auto it = c->gtabs.find(key);
-      long long* dtab;
-      if (it != c->gtabs.end()) {
-        dtab = it->second;
+      L.n = L.bn[0];
+      if (gather_ok) {
+        // registered gradients: peers' members are read in place, no pack
+        std::vector<long long> tab(1, 0), ids;
+        int64_t e = 0;
+        for (size_t t = g; t < h; ++t)
+          for (int k = gr[t].i; k < gr[t].j; ++k) {
+            e += counts[k];
+            tab.push_back(e);
+            ids.push_back(reg_ids[k]);
+          }
+        const int gm = (int)ids.size();
+        tab.insert(tab.end(), ids.begin(), ids.end());
+        std::string key(reinterpret_cast<const char*>(tab.data()), tab.size() * sizeof(long long));
+        auto it = c->gtabs.find(key);
+        long long* dtab;
+        if (it != c->gtabs.end()) {
+          dtab = it->second;
+        } else {
+          CUDA_TRY(cudaMalloc(&dtab, tab.size() * sizeof(long long)));
+          CUDA_TRY(cudaMemcpy(dtab, tab.data(), tab.size() * sizeof(long long), cudaMemcpyHostToDevice));
+          c->gtabs[key] = dtab;
+        }
+        unsigned long long sig = 1469598103934665603ull;
+        for (long long v : tab) sig = (sig ^ (unsigned long long)v) * 1099511628211ull;
+        L.gtab = dtab;
+        L.gmem = gm;
+        L.gsig = sig;
+        L.srcmode = SRC_GATHER;
       } else {
-        CUDA_TRY(cudaMalloc(&dtab, tab.size() * sizeof(long long)));
-        CUDA_TRY(cudaMemcpy(dtab, tab.data(), tab.size() * sizeof(long long), cudaMemcpyHostToDevice));
-        c->gtabs[key] = dtab;
+        // members of all groups are consecutive in the staged layout
+        if ((st = pack(gr[g].i, gr[h - 1].j))) return st;
+        L.srcmode = SRC_PRESTAGED;
       }
-      unsigned long long sig = 1469598103934665603ull;
-      for (long long v : tab) sig = (sig ^ (unsigned long long)v) * 1099511628211ull;
-      L.gtab = dtab;
-      L.gmem = gm;
-      L.gsig = sig;
-      L.srcmode = SRC_GATHER;
-      L.n = L.bn[0];
-      L.agree_gate = (pending && !inline_agree) ? ticket : 0;   // device-side gate: no host wait
-      tag_launch(L);
-      if ((st = launch_collective(c, L, stream))) return st;
-      if ((st = drain(g, h))) return st;
-      g = h;
-      continue;
-    }
-    if (h - g > 1) {
-      std::vector<const void*> srcs;
-      std::vector<void*> dsts;
-      std::vector<int64_t> bytes;
-      Launch L = gr[g].L;
-      L.nbuf = (int)(h - g);
-      int64_t boff = 0;
-      for (size_t t = g; t < h; ++t) {
-        for (int k = gr[t].i; k < gr[t].j; ++k) {
-          srcs.push_back(sends[k]);
-          dsts.push_back(reinterpret_cast<void*>((uintptr_t)((boff + 0) * sz)));
-          bytes.push_back(counts[k] * sz);
-          boff += counts[k];
-        }
-        L.bn[t - g] = gr[t].ng;
-        L.bboff[t - g] = boff - gr[t].ng;
-        L.bout[t - g] = gr[t].L.out[0];
-      }
-      // staged pack offsets are byte offsets; members of all groups are consecutive
-      {
-        int64_t o = 0;
-        for (size_t q = 0; q < dsts.size(); ++q) { dsts[q] = reinterpret_cast<void*>((uintptr_t)o); o += bytes[q]; }
-      }
-      if ((st = launch_batched_copy(c, (int)srcs.size(), srcs.data(), dsts.data(), bytes.data(), true, stream)))
-        return st;
-      L.srcmode = SRC_PRESTAGED;
-      L.n = L.bn[0];
-      L.agree_gate = (pending && !inline_agree) ? ticket : 0;   // the pack only touched local staging
       tag_launch(L);
       if ((st = launch_collective(c, L, stream))) return st;
       if ((st = drain(g, h))) return st;
@@ -1623,33 +1837,16 @@ int cm_fused_allreduce_agreed(cm_comm_t* c, int n, const void* const* sends,
       continue;
     }
     Grp& G = gr[g];
-    std::vector<const void*> srcs;
-    std::vector<void*> dsts;
-    std::vector<int64_t> bytes;
-    int64_t off = 0;
-    for (int k = G.i; k < G.j; ++k) {
-      srcs.push_back(sends[k]);
-      bytes.push_back(counts[k] * sz);
-      dsts.push_back(reinterpret_cast<void*>((uintptr_t)off));
-      off += counts[k] * sz;
-    }
     Launch L = G.L;
     if (G.any_host) {  // inputs arrive in indev on the h2d stream, then copy-in
       CUDA_TRY(cudaStreamWaitEvent(stream, in_ready[g], 0));
       L.srcmode = SRC_COPYIN;
-      L.in[0] = c->indev + G.off * sz;
+      for (int lr = 0; lr < nloc; ++lr) L.in[lr] = indev_at(lr, G);
     } else {         // pack straight into the IPC staging area (no extra copy)
-      if ((st = launch_batched_copy(c, G.j - G.i, srcs.data(), dsts.data(), bytes.data(), true, stream)))
-        return st;
+      if ((st = pack(G.i, G.j))) return st;
       L.srcmode = SRC_PRESTAGED;
     }
-    if (L.ll != 0 || c->rhd_logp) {          // LL / log-p kernels have no gate: wait on the host
-      if ((st = resolve_agree())) return st;
-      if (!*agreed) return CM_OK;
-    } else {
-      L.agree_gate = (pending && !inline_agree) ? ticket : 0;
-      tag_launch(L);
-    }
+    tag_launch(L);
     if ((st = launch_collective(c, L, stream))) return st;
     if ((st = drain(g, g + 1))) return st;
     ++g;
@@ -1657,11 +1854,62 @@ int cm_fused_allreduce_agreed(cm_comm_t* c, int n, const void* const* sends,
   if ((st = hp.join())) return st;
   // the agreement result arrives while the gated collectives run; on a
   // mismatch they were no-ops on every rank and the caller negotiates
-  if ((st = resolve_agree())) return st;
-  if (!*agreed) return CM_OK;
-  for (int q = 0; q < ngroups; ++q) count_stats(c, stats[q]);
+  if (want_agree) {
+    if (inline_mode) {
+      if ((st = inline_agree_wait(c, ticket, stream, agreed))) return st;
+    } else {
+      std::vector<int64_t> mx((size_t)nloc * 2 * n_agree);
+      if ((st = agree_wait(c, ticket, 2 * n_agree, mx.data(), stream))) return st;
+      for (int lr = 0; lr < nloc; ++lr) {
+        bool same = true;
+        for (int i = 0; i < n_agree; ++i)
+          same = same && mx[(size_t)lr * 2 * n_agree + i] == agree_values[lr * n_agree + i] &&
+                 mx[(size_t)lr * 2 * n_agree + n_agree + i] == -agree_values[lr * n_agree + i];
+        agreed[lr] = same ? 1 : 0;
+      }
+    }
+    for (int lr = 0; lr < nloc; ++lr)
+      if (!agreed[lr]) return CM_OK;
+  }
+  for (int lr = 0; lr < nloc; ++lr)
+    for (int q = 0; q < ngroups; ++q) count_stats(c, stats[(size_t)lr * n + q]);
   *n_calls = ngroups;
   return CM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int cm_fused_allreduce(cm_comm_t* c, int n, const void* const* sends, const int64_t* counts,
+                       int dtype, void* recv_fused, int algo, int64_t threshold,
+                       int64_t switch_bytes, int average, void* stream_, cm_stats_t* stats,
+                       int* n_calls) {
+  return cm_fused_allreduce_agreed(c, n, sends, counts, dtype, recv_fused, algo, threshold,
+                                   switch_bytes, average, nullptr, 0, nullptr, nullptr, stream_,
+                                   stats, n_calls);
+}
+
+int cm_fused_allreduce_agreed(cm_comm_t* c, int n, const void* const* sends,
+                              const int64_t* counts, int dtype, void* recv_fused, int algo,
+                              int64_t threshold, int64_t switch_bytes, int average,
+                              const int64_t* agree_values, int n_agree, int* agreed,
+                              const int64_t* reg_ids, void* stream, cm_stats_t* stats,
+                              int* n_calls) {
+  if (c->virt) return fail(CM_ERR_UNSUPPORTED, "use cm_fused_allreduce_agreed_v on a virtual group");
+  void* rv[1] = {recv_fused};
+  return fused_impl(c, n, sends, counts, dtype, rv, algo, threshold, switch_bytes, average, agree_values,
+                    n_agree, agreed, reg_ids, static_cast<cudaStream_t>(stream), stats, n_calls);
+}
+
+int cm_fused_allreduce_agreed_v(cm_comm_t* c, int n, const void* const* sends, const int64_t* counts,
+                                int dtype, void* const* recvs_fused, int algo, int64_t threshold,
+                                int64_t switch_bytes, int average, const int64_t* agree_values, int n_agree,
+                                int* agreed, const int64_t* reg_ids, void* stream, cm_stats_t* stats,
+                                int* n_calls) {
+  if (!c->virt) return fail(CM_ERR_UNSUPPORTED, "cm_fused_allreduce_agreed_v needs a virtual group");
+  return fused_impl(c, n, sends, counts, dtype, recvs_fused, algo, threshold, switch_bytes, average,
+                    agree_values, n_agree, agreed, reg_ids, static_cast<cudaStream_t>(stream), stats, n_calls);
 }
 
 // Parameter-server step (paramserver.py:171-271) on the NVLink heap: workers

@@ -67,10 +67,26 @@ constexpr size_t REG_SIZE = (size_t)MAXREG * MAXP * 8;
 // RFLAG[src][cta] = {(epoch << 8) | phase, call header}, pushed by src
 constexpr size_t RHDF_OFF = REG_OFF + REG_SIZE;
 constexpr size_t RHDF_SIZE = (size_t)MAXP * MAXBLK * 16;
+// Automatic registration of user allocations (the pointer cache's IPC side,
+// no host collective): rank r publishes allocation slot s in its own heap at
+// MAILBOX[s] = {IPC handle, allocation bytes}; every peer q maps it when its
+// kernels report r's new slot count, stores the mapping at AUTOTAB[s][r] in
+// its own heap and acknowledges by writing ACK[q] in r's heap.
+constexpr int MAXAUTO = 2048;
+constexpr size_t MAILBOX_BYTES = 128;
+constexpr size_t AUTOTAB_OFF = RHDF_OFF + RHDF_SIZE;
+constexpr size_t AUTOTAB_SIZE = (size_t)MAXAUTO * MAXP * 8;
+constexpr size_t MAILBOX_OFF = AUTOTAB_OFF + AUTOTAB_SIZE;
+constexpr size_t MAILBOX_SIZE = (size_t)MAXAUTO * MAILBOX_BYTES;
+constexpr size_t ACK_OFF = MAILBOX_OFF + MAILBOX_SIZE;
+constexpr size_t ACK_SIZE = (size_t)MAXP * 8;
 constexpr size_t HEAP_ALIGN = 2ull << 20;
-constexpr size_t LL_OFF = ((RHDF_OFF + RHDF_SIZE + HEAP_ALIGN - 1) / HEAP_ALIGN) * HEAP_ALIGN;
+constexpr size_t LL_OFF = ((ACK_OFF + ACK_SIZE + HEAP_ALIGN - 1) / HEAP_ALIGN) * HEAP_ALIGN;
 // record source encoding for registered inputs: bit 62 | id << 40 | byte delta
+// (collective registration id), bit 62 | bit 61 | slot << 40 | delta (the
+// sender's automatically registered allocation slot)
 constexpr unsigned long long REG_FLAG = 1ull << 62;
+constexpr unsigned long long AUTO_FLAG = 1ull << 61;
 constexpr size_t CTRL_REGION = LL_OFF;                  // zeroed at creation
 
 struct Ctrl {
@@ -89,7 +105,8 @@ struct Rec {
   long long redoff;  // element i of the sender's segment at heap + redoff + (i-seg_off)*sz
   long long akey;    // inline agreement (aggregate's ready-set hash and count)
   long long acnt;
-  long long pad[2];
+  long long regseq;  // allocation slots the sender has published in its mailbox
+  long long pad;
 };
 
 enum SrcMode { SRC_COPYIN = 0, SRC_PRESTAGED = 1, SRC_ZEROCOPY = 2, SRC_INLINE = 3, SRC_REGISTERED = 4,
@@ -126,13 +143,14 @@ struct CollParams {
   unsigned long long* trace; // optional: per-CTA phase timestamps (globaltimer ns)
   int trace_ctas;
   // several fused buffers in ONE launch (aggregate): buffer k holds bn[k]
-  // elements at staging element offset bboff[k] and is written to bout[k];
+  // elements at staging element offset bboff[k] and is written to
+  // out[lr] + bout_off[k] elements;
   // each keeps its own reduce-scatter layout (so ring chunking, and therefore
   // the fold order, is exactly that of one allreduce per buffer)
   int nbuf;
   long long bn[MAXBUF];
   long long bboff[MAXBUF];
-  char* bout[MAXBUF];
+  long long bout_off[MAXBUF];
   long long bseg_off[MAXBUF][MAXP];
   long long bseg_len[MAXBUF][MAXP];
   // SRC_GATHER (aggregate on registered gradients): the fused buffers are the
@@ -142,22 +160,34 @@ struct CollParams {
   const long long* gtab;
   int gmem;
   long long inl[8];          // SRC_INLINE: the input travels in the parameters (cm_agree)
-  unsigned long long* done_flag;  // optional: written with done_value when the call completes
+  unsigned long long* done_flag;  // optional: done_flag[lr] = done_value when the call completes
   unsigned long long done_value;
   int bulk_rs;               // >0: reduce through the bulk-copy engine with this many smem stages
-  int bulk_local;            // the reduce's own-rank source is loaded directly, not staged
   int bulk_stage;            // bytes per shared-memory stage of the bulk reduce
   // >0: run only if the agreement check with this ticket (queued before on the
-  // same stream) succeeded; otherwise every rank skips the call identically
+  // same stream: the LL agreement kernel, or the inline-agreement launch)
+  // succeeded; otherwise every CTA returns at once — no records, no barrier,
+  // no epoch advance — so ranks whose plans (and launch counts) differ stay
+  // in step
   unsigned long long agree_gate;
   // inline agreement: every rank publishes {akey, acnt} in its records; if any
-  // peer's differ, every rank skips the call identically and CTA 0 reports
-  // it through agree_out = {ok, ticket} (host-mapped)
+  // peer's differ, every rank skips the call identically (the start barrier
+  // and the epoch advance still happen: the grid is the same on every rank),
+  // CTA 0 reports it through agree_out[2*lr] = {ticket, ok} (host-mapped) and
+  // the last CTA leaves {agree_tag, agree_ok} in Ctrl for the gated launches
   int agree_inline;
-  long long akey, acnt;
+  long long akey[MAXP], acnt[MAXP];
   unsigned long long* agree_out;
   unsigned long long agree_ticket;
   int dyn_ag;                // allgather as a queue of (slice, peer) tasks shared by the CTAs
+  // automatic registration (real communicators): my published slot count,
+  // the slot counts of each peer I have mapped, and host-mapped words where
+  // CTA 0 reports peers' newer slot counts (notice[q]) and the smallest
+  // count every peer has acknowledged (acked)
+  long long reg_seq;
+  long long mapped_seq[MAXP];
+  unsigned long long* notice;
+  unsigned long long* acked;
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -210,9 +240,20 @@ template <> __device__ __forceinline__ double op2<CM_MAX, double>(double a, doub
 template <> __device__ __forceinline__ int32_t op2<CM_MAX, int32_t>(int32_t a, int32_t b) { return a > b ? a : b; }
 template <> __device__ __forceinline__ int64_t op2<CM_MAX, int64_t>(int64_t a, int64_t b) { return a > b ? a : b; }
 
-// IEEE division by p (aggregation.py:167-172: float32(float64(s)/p) == s/(float)p)
+// IEEE division by p (aggregation.py:167-172: float32(float64(s)/p) == s/(float)p).
+// float: RN32(RN64(s * RN64(1/p))) == RN32(s/p) for every float s and p <= 16:
+// the double product is within 2^-52 relative of s/p, while s/p (a rational
+// with denominator p) stays at least 2^-10 ulp away from any float rounding
+// midpoint unless it lies exactly on one — so both round alike, subnormals
+// included. Unlike __fdiv_rn this has no slow-path subroutine call, which
+// forced the hot loops to spill their operand registers around the call site.
+static __constant__ double c_rcp[MAXP + 1] = {
+    0.0,      1.0,      1.0 / 2,  1.0 / 3,  1.0 / 4,  1.0 / 5,  1.0 / 6,  1.0 / 7, 1.0 / 8,
+    1.0 / 9,  1.0 / 10, 1.0 / 11, 1.0 / 12, 1.0 / 13, 1.0 / 14, 1.0 / 15, 1.0 / 16};
 template <typename A> __device__ __forceinline__ A div_p(A a, int p);
-template <> __device__ __forceinline__ float div_p<float>(float a, int p) { return __fdiv_rn(a, (float)p); }
+template <> __device__ __forceinline__ float div_p<float>(float a, int p) {
+  return __double2float_rn(__dmul_rn((double)a, c_rcp[p]));
+}
 template <> __device__ __forceinline__ double div_p<double>(double a, int p) { return __ddiv_rn(a, (double)p); }
 template <> __device__ __forceinline__ int32_t div_p<int32_t>(int32_t a, int) { return a; }
 template <> __device__ __forceinline__ int64_t div_p<int64_t>(int64_t a, int) { return a; }
@@ -251,6 +292,39 @@ __device__ __forceinline__ unsigned long long* mid_slot(char* heap, int blk, int
   return reinterpret_cast<unsigned long long*>(heap + MID_OFF + ((size_t)blk * MAXP + src) * 8);
 }
 
+// a peer's published source offset -> its address in this process
+__device__ __forceinline__ const char* resolve_src(char* const* heap, char* myheap, int src, long long so) {
+  if (!((unsigned long long)so & REG_FLAG)) return heap[src] + so;
+  const long long delta = so & ((1ll << 40) - 1);
+  if ((unsigned long long)so & AUTO_FLAG) {       // the sender's auto-registered allocation
+    const long long slot = (so >> 40) & 0x1FFFFF;
+    return *reinterpret_cast<char* const*>(myheap + AUTOTAB_OFF + ((size_t)slot * MAXP + src) * 8) + delta;
+  }
+  const long long id = (so >> 40) & 0x1FFFFF;     // collective registration id
+  return *reinterpret_cast<char* const*>(myheap + REG_OFF + ((size_t)id * MAXP + src) * 8) + delta;
+}
+
+// CTA 0 only, after the start barrier: report peers' newer allocation slots
+// and the acknowledged slot count to the host (automatic registration)
+__device__ __forceinline__ void autoreg_report(const CollParams& P, char* myheap, int rank, int tid,
+                                               long long peer_seq) {
+  if (!P.notice) return;
+  if (tid < P.p && tid != rank && peer_seq > P.mapped_seq[tid])
+    reinterpret_cast<volatile unsigned long long*>(P.notice)[tid] = (unsigned long long)peer_seq;
+  if (tid == 0) {
+    unsigned long long lo = ~0ull;
+    const volatile unsigned long long* ack = reinterpret_cast<const volatile unsigned long long*>(myheap + ACK_OFF);
+    for (int q = 0; q < P.p; ++q)
+      if (q != rank) lo = ack[q] < lo ? ack[q] : lo;
+    *reinterpret_cast<volatile unsigned long long*>(P.acked) = lo;
+  }
+}
+
+// a gated launch whose agreement failed is a no-op (uniform for the grid)
+__device__ __forceinline__ bool gated_out(const CollParams& P, const Ctrl* ctrl) {
+  return P.agree_gate && !(ctrl->agree_tag == P.agree_gate && ctrl->agree_ok);
+}
+
 // bounded spin: returns false on timeout
 __device__ __forceinline__ bool wait_geq(const unsigned long long* f, unsigned long long e,
                                          unsigned long long timeout) {
@@ -266,11 +340,22 @@ __device__ __forceinline__ bool wait_geq(const unsigned long long* f, unsigned l
 // Slice b of segment [off, off+len) split over nb CTAs; interior boundaries
 // are multiples of SLICE_ALIGN (absolute element index) so they are vector
 // aligned and independent of the vector width.
+// floor(a * k / d) for 0 <= a < 2^50, 0 <= k <= d <= 2^20, exactly: a double
+// estimate (relative error < 2^-51, so off by at most one) corrected in
+// integers — no 128-bit or 64-bit division subroutine in the kernels
+__device__ __forceinline__ long long muldiv_floor(long long a, int k, int d) {
+  const long long num = a * k;
+  long long q = (long long)(__dmul_rn((double)num, __drcp_rn((double)d)));
+  if (q * d > num) --q;
+  else if ((q + 1) * d <= num) ++q;
+  return q;
+}
+
 __device__ __forceinline__ long long slice_bound(long long off, long long len, int k, int nb) {
   if (k <= 0) return off;
   if (k >= nb) return off + len;
-  long long x = off + (long long)(((__int128)len * k) / nb);
-  x = (x / SLICE_ALIGN) * SLICE_ALIGN;
+  long long x = off + muldiv_floor(len, k, nb);
+  x = x & ~(long long)(SLICE_ALIGN - 1);
   if (x < off) x = off;
   if (x > off + len) x = off + len;
   return x;
@@ -283,6 +368,11 @@ __device__ __forceinline__ void load_vec(const char* base, long long i, typename
   const S* p = reinterpret_cast<const S*>(base) + i;
   if constexpr (W * sizeof(S) == 16) {
     uint4 raw = *reinterpret_cast<const uint4*>(p);
+    const S* s = reinterpret_cast<const S*>(&raw);
+#pragma unroll
+    for (int w = 0; w < W; ++w) v[w] = to_acc<D>(s[w]);
+  } else if constexpr (W * sizeof(S) == 8) {
+    uint2 raw = *reinterpret_cast<const uint2*>(p);
     const S* s = reinterpret_cast<const S*>(&raw);
 #pragma unroll
     for (int w = 0; w < W; ++w) v[w] = to_acc<D>(s[w]);
@@ -302,10 +392,30 @@ __device__ __forceinline__ void store_vec(char* base, long long i, const typenam
 #pragma unroll
     for (int w = 0; w < W; ++w) s[w] = from_acc<D>(v[w]);
     *reinterpret_cast<uint4*>(p) = raw;
+  } else if constexpr (W * sizeof(S) == 8) {
+    uint2 raw;
+    S* s = reinterpret_cast<S*>(&raw);
+#pragma unroll
+    for (int w = 0; w < W; ++w) s[w] = from_acc<D>(v[w]);
+    *reinterpret_cast<uint2*>(p) = raw;
   } else {
 #pragma unroll
     for (int w = 0; w < W; ++w) p[w] = from_acc<D>(v[w]);
   }
+}
+
+// Elements folded per thread per step: a 16-byte vector, narrowed so that the
+// MP operands take at most REGS registers (bf16 accumulates in fp32, so a
+// 16-byte bf16 vector would need 64 at MP = 8). The bulk-engine consumers read
+// their operands from shared memory and use a 16-register budget; the SM-load
+// path keeps 32 so that enough NVLink loads are in flight.
+template <class D, int MP, int REGS = 32>
+__host__ __device__ constexpr int fold_width() {
+  constexpr int w16 = 16 / (int)sizeof(typename D::S);
+  constexpr int cap = REGS / (MP * (int)(sizeof(typename D::A) / 4));
+  int w = w16;
+  while (w > 1 && w > cap) w /= 2;
+  return w;
 }
 
 // ---- fold of p loaded operands in the reference order -------------------------
@@ -354,29 +464,61 @@ __device__ __forceinline__ void fold(A (&u)[MP][W], int p, int m, int excess) {
   }
 }
 
-// reduce U groups of W elements starting at element indices i0 + g*stride
-template <class D, int OP, int MP, int W, bool TREE>
-__device__ __forceinline__ void reduce_one(const char* const* seq, int p, int m, int excess,
-                                           long long i, int average, char* out,
-                                           long long out_shift, char* red, long long red_shift) {
+// One element, few registers: the sources are loaded one at a time. Left
+// fold for ring/flat; for the rhd tree, leaves L_v (v < m) are combined by a
+// binary counter (after leaf v, merge while v has trailing ones), which is the
+// balanced tree with the lower subtree first — the association of tree_fold.
+template <class D, int OP, int MP, bool TREE>
+__device__ __forceinline__ void reduce_elem(const char* const* seq, int p, int m, int excess, long long i,
+                                            int average, char* out, long long out_shift, char* red,
+                                            long long red_shift) {
   using A = typename D::A;
-  A u[MP][W];
+  using S = typename D::S;
+  auto ld = [&](int k) { return to_acc<D>(reinterpret_cast<const S*>(seq[k])[i]); };
+  A acc;
+  if constexpr (!TREE) {
+    acc = ld(0);
 #pragma unroll
-  for (int k = 0; k < MP; ++k)
-    if (k < p) load_vec<D, W>(seq[k], i, u[k]);
-  fold<OP, MP, W, TREE>(u, p, m, excess);
-  if (average) {
+    for (int k = 1; k < MP; ++k)
+      if (k < p) acc = op2<OP>(acc, ld(k));
+  } else {
+    A st[5];
 #pragma unroll
-    for (int w = 0; w < W; ++w) u[0][w] = div_p<A>(u[0][w], p);
+    for (int v = 0; v < MP; ++v) {
+      if (v < m) {
+        A x = ld(v);
+        if (v < excess) x = op2<OP>(x, ld(m + v));
+        int top = __popc(v) - 1;                       // entries on the stack before leaf v (compile time)
+#pragma unroll
+        for (int t = v; t & 1; t >>= 1) x = op2<OP>(st[top--], x);
+        st[top + 1] = x;
+      }
+    }
+    acc = st[0];
   }
-  store_vec<D, W>(out, i - out_shift, u[0]);
-  if (red) store_vec<D, W>(red, i - red_shift, u[0]);
+  if (average) acc = div_p<A>(acc, p);
+  reinterpret_cast<S*>(out)[i - out_shift] = from_acc<D>(acc);
+  if (red) reinterpret_cast<S*>(red)[i - red_shift] = from_acc<D>(acc);
+}
+
+// Scalar head [lo, a) and tail [z, hi) of a range whose body is vectorised
+template <class D, int OP, int MP, bool TREE>
+__device__ __forceinline__ void reduce_scalar(const char* const* seq, int p, int m, int excess, long long lo,
+                                              long long a, long long z, long long hi, int average, char* out,
+                                              long long out_shift, char* red, long long red_shift, int tid,
+                                              int nthr) {
+#pragma unroll 1
+  for (long long i = lo + tid; i < a; i += nthr)
+    reduce_elem<D, OP, MP, TREE>(seq, p, m, excess, i, average, out, out_shift, red, red_shift);
+#pragma unroll 1
+  for (long long i = z + tid; i < hi; i += nthr)
+    reduce_elem<D, OP, MP, TREE>(seq, p, m, excess, i, average, out, out_shift, red, red_shift);
 }
 
 // Process [lo, hi) of one segment: scalar head/tail, W-wide body with 2-way
 // unrolling for memory-level parallelism over NVLink.
 template <class D, int OP, int MP, bool TREE>
-__device__ void reduce_range(const char* const* seq, int p, int m, int excess, long long lo,
+__device__ __noinline__ void reduce_range(const char* const* seq, int p, int m, int excess, long long lo,
                              long long hi, bool vec, int average, char* out, long long out_shift,
                              char* red, long long red_shift, int tid, int nthr) {
   using S = typename D::S;
@@ -388,48 +530,51 @@ __device__ void reduce_range(const char* const* seq, int p, int m, int excess, l
     if (body_hi < body_lo) body_hi = body_lo = hi;
   }
   // scalar head and tail
-  for (long long i = lo + tid; i < body_lo; i += nthr)
-    reduce_one<D, OP, MP, 1, TREE>(seq, p, m, excess, i, average, out, out_shift, red, red_shift);
-  for (long long i = body_hi + tid; i < hi; i += nthr)
-    reduce_one<D, OP, MP, 1, TREE>(seq, p, m, excess, i, average, out, out_shift, red, red_shift);
-  // vector body: vectors j in [body_lo/W, body_hi/W)
-  const long long v0 = body_lo / W, v1 = body_hi / W;
+  reduce_scalar<D, OP, MP, TREE>(seq, p, m, excess, lo, body_lo, body_hi, hi, average, out, out_shift, red,
+                                 red_shift, tid, nthr);
+  // vector body: VW-element vectors j in [body_lo/VW, body_hi/VW)
+  constexpr int VW = fold_width<D, MP>();
+  const long long v0 = body_lo / VW, v1 = body_hi / VW;
   using A = typename D::A;
   // vector groups in flight per thread: ~32 operand registers whatever MP is (the
   // bulk-engine path carries the large-message traffic; this one stays spill-free)
-  constexpr int OPR = MP * W * (int)(sizeof(A) / 4);
+  constexpr int OPR = MP * VW * (int)(sizeof(A) / 4);
   constexpr int U = OPR >= 32 ? 1 : 32 / OPR;
   // Groups are predicated rather than peeled: the last partial round still
   // keeps every remaining load in flight at once (a peeled one-group tail
   // would pay one NVLink round trip per group).
+#pragma unroll 1
   for (long long j = v0 + tid; j < v1; j += U * (long long)nthr) {
-    A u[U][MP][W];
+    A u[U][MP][VW];
 #pragma unroll
     for (int g = 0; g < U; ++g)
       if (j + g * (long long)nthr < v1) {
 #pragma unroll
         for (int k = 0; k < MP; ++k)
-          if (k < p) load_vec<D, W>(seq[k], (j + g * (long long)nthr) * W, u[g][k]);
+          if (k < p) load_vec<D, VW>(seq[k], (j + g * (long long)nthr) * VW, u[g][k]);
       }
 #pragma unroll
     for (int g = 0; g < U; ++g) {
       if (j + g * (long long)nthr >= v1) break;
-      fold<OP, MP, W, TREE>(u[g], p, m, excess);
+      fold<OP, MP, VW, TREE>(u[g], p, m, excess);
       if (average) {
 #pragma unroll
-        for (int w = 0; w < W; ++w) u[g][0][w] = div_p<A>(u[g][0][w], p);
+        for (int w = 0; w < VW; ++w) u[g][0][w] = div_p<A>(u[g][0][w], p);
       }
-      const long long i = (j + g * (long long)nthr) * W;
-      store_vec<D, W>(out, i - out_shift, u[g][0]);
-      if (red) store_vec<D, W>(red, i - red_shift, u[g][0]);
+      const long long i = (j + g * (long long)nthr) * VW;
+      store_vec<D, VW>(out, i - out_shift, u[g][0]);
+      if (red) store_vec<D, VW>(red, i - red_shift, u[g][0]);
     }
   }
 }
 
 // Several element ranges copied CONCURRENTLY: range r moves elements
-// [lo, hi) with dst[i - dshift] = src[i - sshift]. Every thread issues the
-// loads of all ranges before any store, so the allgather pulls from all
-// peers at once (balanced NVLink traffic, one round trip per iteration).
+// [lo, hi) with dst[i - dshift] = src[i - sshift]. The 16-byte body of every
+// range is cut into 4 KiB chunks dealt round-robin over the ranges (chunk k
+// belongs to range k % nr), and the warps of the CTA stride over that chunk
+// sequence: at any time the CTA reads from every range (every peer of an
+// allgather) at once, and each warp keeps CP_U 16-byte loads per lane in
+// flight with a handful of registers (no per-range state in registers).
 struct CopyRange {
   const char* src;
   char* dst;
@@ -441,6 +586,9 @@ struct VecRange {
   uint4* dst;
   long long nv;
 };
+
+constexpr int CP_U = 8;                       // 16-byte loads in flight per lane
+constexpr int CP_CHUNK = 32 * CP_U;           // vectors per warp chunk (4 KiB)
 
 // R[0..nr) in shared memory; V is shared scratch of the same size.
 template <class D, int MP>
@@ -469,42 +617,27 @@ __device__ void multi_copy(const CopyRange* R, int nr, VecRange* V) {
     }
   }
   __syncthreads();
+  if (nr < 1) return;
   long long nvmax = 0;
   for (int r = 0; r < nr; ++r) nvmax = V[r].nv > nvmax ? V[r].nv : nvmax;
-  // NS 16-byte loads in flight per thread whatever the number of ranges:
-  // slot s copies range s % nr at vector offset (s / nr) * bd
-  constexpr int NS = MP > 8 ? MP : 8;
-  if (nr < 1) return;
-  // ranges are processed in blocks of at most NS (multi-buffer launches have
-  // up to MAXBUF * (p - 1) ranges)
-  for (int r0 = 0; r0 < nr; r0 += NS) {
-    const int nrb = nr - r0 < NS ? nr - r0 : NS;
-    const VecRange* VB = V + r0;
-    long long nvb = 0;
-    for (int r = 0; r < nrb; ++r) nvb = VB[r].nv > nvb ? VB[r].nv : nvb;
-    const int G = NS / nrb > 1 ? NS / nrb : 1;
-    const int act = nrb * G < NS ? nrb * G : NS;
-    int sr[NS], sg[NS];
+  const int nchunks = (int)((nvmax + CP_CHUNK - 1) / CP_CHUNK) * nr;   // < 2^31: slices are small
+#pragma unroll 1
+  for (int k = warp; k < nchunks; k += nwarps) {
+    const int r = k % nr;
+    const long long c0 = (long long)(k / nr) * CP_CHUNK;
+    const long long nv = V[r].nv;
+    if (c0 >= nv) continue;
+    const uint4* src = V[r].src + c0;
+    uint4* dst = V[r].dst + c0;
+    const int m = (int)(nv - c0 < CP_CHUNK ? nv - c0 : CP_CHUNK);
+    uint4 v[CP_U];
 #pragma unroll
-    for (int k = 0; k < NS; ++k) {
-      sr[k] = k % nrb;
-      sg[k] = k / nrb;
-    }
-    for (long long j0 = tid; j0 < nvb; j0 += (long long)bd * G) {
-      uint4 v[NS];
+    for (int u = 0; u < CP_U; ++u)
+      if (lane + 32 * u < m) v[u] = src[lane + 32 * u];
 #pragma unroll
-      for (int k = 0; k < NS; ++k) {
-        const long long j = j0 + (long long)sg[k] * bd;
-        if (k < act && j < VB[sr[k]].nv) v[k] = VB[sr[k]].src[j];
-      }
-#pragma unroll
-      for (int k = 0; k < NS; ++k) {
-        const long long j = j0 + (long long)sg[k] * bd;
-        if (k < act && j < VB[sr[k]].nv) VB[sr[k]].dst[j] = v[k];
-      }
-    }
+    for (int u = 0; u < CP_U; ++u)
+      if (lane + 32 * u < m) dst[lane + 32 * u] = v[u];
   }
-  (void)nvmax;
 }
 
 __device__ __forceinline__ bool al16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
@@ -537,6 +670,11 @@ __host__ __device__ constexpr size_t rs_smem_bytes(int stages, int stage_bytes =
   return (size_t)stages * stage_bytes + (2 * (size_t)stages + 2) * 8;
 }
 
+// The stage ring lives at the start of the launch's dynamic shared memory; its
+// view is rebuilt from (stages, stage_bytes) — kernel parameters — wherever it
+// is used, so no pointers to it stay live in registers across the kernel.
+extern __shared__ __align__(128) unsigned char cm_dyn_smem[];
+
 struct BulkRS {
   unsigned char* smem;        // stages x stage_bytes
   unsigned long long* full;   // [stages], 1 arrival + tx bytes
@@ -546,14 +684,19 @@ struct BulkRS {
   int stage_bytes;
 };
 
-__device__ __forceinline__ BulkRS bulk_rs_setup(unsigned char* dyn, int stages, int stage_bytes, int tid) {
+__device__ __forceinline__ BulkRS bulk_view(int stages, int stage_bytes) {
   BulkRS B;
   B.stages = stages;
   B.stage_bytes = stage_bytes;
-  B.smem = dyn;
-  B.full = reinterpret_cast<unsigned long long*>(dyn + (size_t)stages * stage_bytes);
+  B.smem = cm_dyn_smem;
+  B.full = reinterpret_cast<unsigned long long*>(cm_dyn_smem + (size_t)stages * stage_bytes);
   B.empty = B.full + stages;
   B.seqno = B.empty + stages;
+  return B;
+}
+
+__device__ __forceinline__ void bulk_rs_setup(int stages, int stage_bytes, int tid) {
+  const BulkRS B = bulk_view(stages, stage_bytes);
   if (tid == 0) {
     for (int s = 0; s < stages; ++s) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&B.full[s])));
@@ -562,90 +705,86 @@ __device__ __forceinline__ BulkRS bulk_rs_setup(unsigned char* dyn, int stages, 
     *B.seqno = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  return B;
 }
 
 // Same contract as reduce_range (sources 16-byte aligned at vector boundaries).
 template <class D, int OP, int MP, bool TREE>
-__device__ void reduce_range_bulk(const BulkRS& B, const char* const* seq, int p, int m, int excess,
+__device__ void reduce_range_bulk(int stages, int stage_bytes, const char* const* seq, int p, int m, int excess,
                                   long long lo, long long hi, int average, char* out, long long out_shift,
-                                  char* red, long long red_shift, int tid, int local_k = -1) {
-  // local_k >= 0: source local_k is this rank's own (HBM) buffer; the
-  // consumers load it directly, so every stage byte carries NVLink traffic
+                                  char* red, long long red_shift, int tid) {
+  const BulkRS B = bulk_view(stages, stage_bytes);
   using S = typename D::S;
   using A = typename D::A;
   constexpr int W = 16 / sizeof(S);
   constexpr int SZ = sizeof(S);
   long long body_lo = ((lo + W - 1) / W) * W, body_hi = (hi / W) * W;
   if (body_hi < body_lo) body_lo = body_hi = hi;
-  for (long long i = lo + tid; i < body_lo; i += THREADS)
-    reduce_one<D, OP, MP, 1, TREE>(seq, p, m, excess, i, average, out, out_shift, red, red_shift);
-  for (long long i = body_hi + tid; i < hi; i += THREADS)
-    reduce_one<D, OP, MP, 1, TREE>(seq, p, m, excess, i, average, out, out_shift, red, red_shift);
+  if (body_lo > lo || body_hi < hi)
+    reduce_scalar<D, OP, MP, TREE>(seq, p, m, excess, lo, body_lo, body_hi, hi, average, out, out_shift, red,
+                                   red_shift, tid, THREADS);
   const long long nbytes = (body_hi - body_lo) * SZ;
   if (nbytes <= 0) return;
-  const int nstaged = local_k >= 0 ? p - 1 : p;
-  const int ch = (B.stage_bytes / nstaged) & ~15;       // bytes per staged source per stage
-  const long long C = (nbytes + ch - 1) / ch;
-  const unsigned long long base = *B.seqno;
+  const int ch = (B.stage_bytes / p) & ~15;             // bytes per source per stage
+  const int C = (int)((nbytes + ch - 1) / ch);
+  // stage uses so far in this launch (< 2^32): stage index and mbarrier phase
+  // advance incrementally (no 64-bit division in the loops)
+  const unsigned base = (unsigned)*B.seqno;
   if (tid == RS_CONSUMERS) {                            // producer: warp 15, lane 0
     asm volatile("fence.proxy.async;" ::: "memory");
-    for (long long c = 0; c < C; ++c) {
-      const unsigned long long g = base + (unsigned long long)c;
-      const int s = (int)(g % B.stages);
-      if (g >= (unsigned long long)B.stages) mbar_wait(&B.empty[s], (unsigned)(((g / B.stages) - 1) & 1));
-      const long long off = body_lo * SZ + c * ch;
-      const int len = (int)((nbytes - c * ch) < ch ? (nbytes - c * ch) : ch);
+    int s = (int)(base % (unsigned)B.stages);
+    unsigned ph = (base / (unsigned)B.stages) & 1u;
+    bool wrapped = base >= (unsigned)B.stages;
+    for (int c = 0; c < C; ++c) {
+      if (wrapped) mbar_wait(&B.empty[s], ph ^ 1u);
+      const long long off = body_lo * SZ + (long long)c * ch;
+      const int len = (int)((nbytes - (long long)c * ch) < ch ? (nbytes - (long long)c * ch) : ch);
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&B.full[s])),
-                   "r"(len * nstaged)
+                   "r"(len * p)
                    : "memory");
       for (int k = 0; k < p; ++k) {
-        if (k == local_k) continue;
-        const int slot = (local_k >= 0 && k > local_k) ? k - 1 : k;
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                smem_u32(B.smem + (size_t)s * B.stage_bytes + (size_t)slot * ch)),
+                smem_u32(B.smem + (size_t)s * B.stage_bytes + (size_t)k * ch)),
             "l"(seq[k] + off), "r"(len), "r"(smem_u32(&B.full[s]))
             : "memory");
       }
+      if (++s == B.stages) { s = 0; ph ^= 1u; wrapped = true; }
     }
   } else if (tid < RS_CONSUMERS) {
-    for (long long c = 0; c < C; ++c) {
-      const unsigned long long g = base + (unsigned long long)c;
-      const int s = (int)(g % B.stages);
-      mbar_wait(&B.full[s], (unsigned)((g / B.stages) & 1));
-      const int len = (int)((nbytes - c * ch) < ch ? (nbytes - c * ch) : ch);
-      const int nv = len / 16;
+    int s = (int)(base % (unsigned)B.stages);
+    unsigned ph = (base / (unsigned)B.stages) & 1u;
+    for (int c = 0; c < C; ++c) {
+      mbar_wait(&B.full[s], ph);
+      const int len = (int)((nbytes - (long long)c * ch) < ch ? (nbytes - (long long)c * ch) : ch);
+      constexpr int VW = fold_width<D, MP, 16>();
+      const int nv = len / (VW * SZ);
       const char* st = reinterpret_cast<const char*>(B.smem + (size_t)s * B.stage_bytes);
-      const long long e0 = body_lo + c * (ch / SZ);
+      const long long e0 = body_lo + (long long)c * (ch / SZ);
+#pragma unroll 1
       for (int v = tid; v < nv; v += RS_CONSUMERS) {
-        A u[MP][W];
+        A u[MP][VW];
 #pragma unroll
         for (int k = 0; k < MP; ++k) {
           if (k >= p) continue;
-          if (k == local_k) {
-            load_vec<D, W>(seq[k], e0 + (long long)v * W, u[k]);
-          } else {
-            const int slot = (local_k >= 0 && k > local_k) ? k - 1 : k;
-            load_vec<D, W>(st + (size_t)slot * ch, (long long)v * W, u[k]);
-          }
+          load_vec<D, VW>(st + (size_t)k * ch, (long long)v * VW, u[k]);
         }
-        fold<OP, MP, W, TREE>(u, p, m, excess);
+        fold<OP, MP, VW, TREE>(u, p, m, excess);
         if (average) {
 #pragma unroll
-          for (int w = 0; w < W; ++w) u[0][w] = div_p<A>(u[0][w], p);
+          for (int w = 0; w < VW; ++w) u[0][w] = div_p<A>(u[0][w], p);
         }
-        const long long i = e0 + (long long)v * W;
-        store_vec<D, W>(out, i - out_shift, u[0]);
-        if (red) store_vec<D, W>(red, i - red_shift, u[0]);
+        const long long i = e0 + (long long)v * VW;
+        store_vec<D, VW>(out, i - out_shift, u[0]);
+        if (red) store_vec<D, VW>(red, i - red_shift, u[0]);
       }
       __syncwarp();
       if ((tid & 31) == 0)
         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&B.empty[s])) : "memory");
+      if (++s == B.stages) { s = 0; ph ^= 1u; }
     }
   }
   __syncthreads();
-  if (tid == 0) *B.seqno = base + (unsigned long long)C;
+  if (tid == 0) *B.seqno = base + (unsigned)C;
   __syncthreads();
 }
 __device__ __forceinline__ bool al16s(const char* base, long long shift_elems, int sz) {

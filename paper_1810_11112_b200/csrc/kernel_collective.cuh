@@ -156,7 +156,7 @@ __device__ void dynamic_allgather(const CollParams& P, int rank, int nb, unsigne
         for (int k = 0; k < P.nbuf; ++k) {
           const long long so = P.bseg_off[k][q], sl = P.bseg_len[k][q];
           const long long lo = slice_bound(so, sl, s, nb), hi = slice_bound(so, sl, s + 1, nb);
-          if (hi > lo) s_cr[r++] = CopyRange{s_src[q] + P.bboff[k] * SZ, P.bout[k], 0, 0, lo, hi};
+          if (hi > lo) s_cr[r++] = CopyRange{s_src[q] + P.bboff[k] * SZ, out + P.bout_off[k] * SZ, 0, 0, lo, hi};
         }
       } else {
         const long long so = P.seg_off[q], sl = P.seg_len[q];
@@ -172,8 +172,11 @@ __device__ void dynamic_allgather(const CollParams& P, int rank, int nb, unsigne
   }
 }
 
-template <class D, int OP, int MP, bool TREE, bool STREAM>
-__global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_constant__ CollParams P) {
+// MULTI: the multi-buffer / gathered-member aggregate launch (nbuf >= 1 or
+// SRC_GATHER); otherwise every single-buffer mode. Separate instantiations keep
+// each kernel's register footprint to its own mode.
+template <class D, int OP, int MP, bool TREE, bool STREAM, bool MULTI>
+__global__ void __launch_bounds__(THREADS, 1) collective_kernel(const __grid_constant__ CollParams P) {
   using S = typename D::S;
   constexpr int SZ = sizeof(S);
   const int lr = P.virt ? blockIdx.y : 0;       // index into in/out
@@ -188,18 +191,15 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
   __shared__ const char* s_seq[MAXP];   // fold sequence
   __shared__ int s_rord[MAXP];          // fold sequence as source ranks
   __shared__ int s_err;
-  __shared__ int s_skip;                // agreement gate failed: the call is a no-op
+  __shared__ int s_skip;                // 2: inline agreement failed, the call moves no data
 
-  extern __shared__ __align__(128) unsigned char coll_dyn[];
+  if (gated_out(P, ctrl)) return;       // agreement failed earlier in this call
   CM_TRACE(P, lr, b, 0);
-  BulkRS BR{};
-  if (!STREAM && P.bulk_rs) BR = bulk_rs_setup(coll_dyn, P.bulk_rs, P.bulk_stage, tid);
+  if (!STREAM && P.bulk_rs) bulk_rs_setup(P.bulk_rs, P.bulk_stage, tid);
   if (tid == 0) {
     s_epoch = ctrl->epoch + 1;
     s_err = 0;
-    // the agreement kernel ran before this one on the stream; its outcome is
-    // identical on every rank, so every rank skips (or runs) consistently
-    s_skip = P.agree_gate && !(ctrl->agree_tag == P.agree_gate && ctrl->agree_ok) ? 1 : 0;
+    s_skip = 0;
   }
   __syncthreads();
   const unsigned long long e = s_epoch;
@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
   __shared__ CopyRange s_cr[MAXBUF * MAXP + 1];
   __shared__ VecRange s_vr[MAXBUF * MAXP + 1];
   __shared__ int s_ncr;
-  if (P.srcmode == SRC_COPYIN && !s_skip) {
+  if (!MULTI && P.srcmode == SRC_COPYIN && !s_skip) {
     char* stage = myheap + stage_off;
     if (ag_only) {
       if (tid == 0) {
@@ -263,9 +263,10 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
     st_relaxed_sys_s64(&r->srcoff, my_srcoff);
     st_relaxed_sys_s64(&r->redoff, my_redoff);
     if (P.agree_inline) {
-      st_relaxed_sys_s64(&r->akey, P.akey);
-      st_relaxed_sys_s64(&r->acnt, P.acnt);
+      st_relaxed_sys_s64(&r->akey, P.akey[lr]);
+      st_relaxed_sys_s64(&r->acnt, P.acnt[lr]);
     }
+    st_relaxed_sys_s64(&r->regseq, P.reg_seq);
     st_release_sys(&r->epoch, e);
   }
   if (tid < p && !s_skip) {
@@ -273,18 +274,14 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
     if (!wait_geq(&r->epoch, e, P.timeout_cycles)) {
       atomicExch(&s_err, ERR_TRANSPORT);
     } else {
-      if (P.agree_inline && (ld_relaxed_sys_s64(&r->akey) != P.akey || ld_relaxed_sys_s64(&r->acnt) != P.acnt))
+      if (P.agree_inline &&
+          (ld_relaxed_sys_s64(&r->akey) != P.akey[lr] || ld_relaxed_sys_s64(&r->acnt) != P.acnt[lr]))
         atomicExch(&s_skip, 2);            // ready sets differ: nobody moves data
       if (ld_relaxed_sys(&r->hdr) != P.hdr) atomicExch(&s_err, ERR_SHAPE);
-      const long long so = ld_relaxed_sys_s64(&r->srcoff);
-      if ((unsigned long long)so & REG_FLAG) {   // peer's registered buffer, mapped here
-        const long long id = (so >> 40) & 0x3FFFFF, delta = so & ((1ll << 40) - 1);
-        const char* base = *reinterpret_cast<char* const*>(myheap + REG_OFF + ((size_t)id * MAXP + tid) * 8);
-        s_src[tid] = base + delta;
-      } else {
-        s_src[tid] = P.heap[tid] + so;
-      }
-      s_red[tid] = P.heap[tid] + ld_relaxed_sys_s64(&r->redoff);
+      // peer's staging / symmetric pool, or its registered buffer mapped here
+      s_src[tid] = resolve_src(P.heap, myheap, tid, ld_relaxed_sys_s64(&r->srcoff));
+      s_red[tid] = const_cast<char*>(resolve_src(P.heap, myheap, tid, ld_relaxed_sys_s64(&r->redoff)));
+      if (b == 0) autoreg_report(P, myheap, rank, tid, ld_relaxed_sys_s64(&r->regseq));
     }
   }
   __syncthreads();                       // s_src / s_red / s_err complete
@@ -296,9 +293,10 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
     __syncthreads();
     if (tid == 0 && !agreed) s_err = 0;
     if (tid == 0 && b == 0 && P.agree_out) {
-      reinterpret_cast<volatile unsigned long long*>(P.agree_out)[1] = agreed ? 1ull : 0ull;
+      volatile unsigned long long* ao = P.agree_out + 2 * lr;
+      ao[1] = agreed ? 1ull : 0ull;
       __threadfence_system();
-      reinterpret_cast<volatile unsigned long long*>(P.agree_out)[0] = P.agree_ticket;
+      ao[0] = P.agree_ticket;
     }
     __syncthreads();
   }
@@ -317,13 +315,6 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
     }
     for (int k = 0; k < p; ++k) s_seq[k] = s_src[s_rord[k]];
   }
-  __shared__ int s_localk;
-  if (tid == 0) {
-    s_localk = -1;
-    if (P.bulk_local && (P.phases & PH_RS))
-      for (int k = 0; k < p; ++k)
-        if (s_rord[k] == rank) s_localk = k;
-  }
   __syncthreads();
   CM_TRACE(P, lr, b, 2);
   if (s_err || s_skip) goto finish;
@@ -338,72 +329,79 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
     goto finish;
   }
 
-  if (P.nbuf > 1 || P.srcmode == SRC_GATHER) {
+  if constexpr (MULTI) {
     // ---- several fused buffers, one launch: RS of every buffer, ONE
     // RS->AG barrier, AG of every buffer. Input prestaged in staging, or
     // (SRC_GATHER) read in place from every rank's registered member tensors.
+    // The CTA walks its slice of every buffer as a sequence of pieces (a
+    // piece never crosses a member of a gathered buffer); thread 0 prepares
+    // each piece's source table in shared memory, so ONE reduce call site
+    // serves both input modes and no per-piece state lives in registers.
     __shared__ const char* s_seqk[MAXP];
-    __shared__ long long s_piece[2];
+    __shared__ char* s_bo;
+    __shared__ char* s_rd;
+    __shared__ long long s_i, s_pe, s_hi;
+    __shared__ int s_k, s_vec;
     int m = 1;
     while ((m << 1) <= p) m <<= 1;
     const int excess = p - m;
     char* mystage = myheap + stage_off;
-    const bool gather = P.srcmode == SRC_GATHER;
-    for (int k = 0; k < P.nbuf; ++k) {
-      const long long so = P.bseg_off[k][rank], sl = P.bseg_len[k][rank];
-      char* bo = P.bout[k];
-      char* red = mystage + P.bboff[k] * SZ;           // element 0 of buffer k (AG source)
-      const long long lo = slice_bound(so, sl, b, nb), hi = slice_bound(so, sl, b + 1, nb);
-      if (!gather) {
-        if (tid < p) s_seqk[tid] = s_seq[tid] + P.bboff[k] * SZ;
-        __syncthreads();
-        bool vec = al16(bo) && al16(red);
-        for (int q = 0; q < p; ++q) vec = vec && al16(s_seqk[q]);
-        if (P.bulk_rs && vec)
-          reduce_range_bulk<D, OP, MP, TREE>(BR, s_seqk, p, m, excess, lo, hi, P.average, bo, 0, red, 0, tid,
-                                             s_localk);
-        else
-          reduce_range<D, OP, MP, TREE>(s_seqk, p, m, excess, lo, hi, vec, P.average, bo, 0, red, 0,
-                                        tid, blockDim.x);
-        __syncthreads();
-        continue;
-      }
-      // gather: walk the members overlapping [lo, hi) of buffer k
-      const long long* gstart = P.gtab;
-      const long long* gid = P.gtab + P.gmem + 1;
-      long long i = lo;
-      while (i < hi) {
-        if (tid == 0) {                              // member holding global index bboff + i
-          const long long g = P.bboff[k] + i;
-          int a = 0, z = P.gmem;                     // gstart[a] <= g < gstart[z]
-          while (z - a > 1) {
-            const int mid = (a + z) >> 1;
-            if (gstart[mid] <= g) a = mid; else z = mid;
+    // piece iterator, advanced by thread 0 only (the loop state lives in
+    // shared memory, not in every thread's registers)
+    if (tid == 0) {
+      s_k = -1;
+      s_i = s_hi = 0;
+    }
+#pragma unroll 1
+    while (true) {
+      if (tid == 0) {
+        while (s_i >= s_hi && ++s_k < P.nbuf) {        // next buffer with a non-empty slice
+          const long long so = P.bseg_off[s_k][rank], sl = P.bseg_len[s_k][rank];
+          s_i = slice_bound(so, sl, b, nb);
+          s_hi = slice_bound(so, sl, b + 1, nb);
+        }
+        if (s_k < P.nbuf) {
+          const int k = s_k;
+          const long long i = s_i, hi = s_hi;
+          char* bo = out + P.bout_off[k] * SZ;
+          char* red = mystage + P.bboff[k] * SZ;       // element 0 of buffer k (AG source)
+          long long pe = hi;
+          if (P.srcmode == SRC_GATHER) {               // member holding global index bboff + i
+            const long long* gstart = P.gtab;
+            const long long* gid = P.gtab + P.gmem + 1;
+            const long long g = P.bboff[k] + i;
+            int a = 0, z = P.gmem;                     // gstart[a] <= g < gstart[z]
+            while (z - a > 1) {
+              const int mid = (a + z) >> 1;
+              if (gstart[mid] <= g) a = mid; else z = mid;
+            }
+            const long long mend = gstart[a + 1] - P.bboff[k];
+            pe = mend < hi ? mend : hi;
+            for (int q = 0; q < p; ++q) {
+              const char* base = *reinterpret_cast<char* const*>(
+                  myheap + REG_OFF + ((size_t)gid[a] * MAXP + s_rord[q]) * 8);
+              s_seqk[q] = base - (gstart[a] - P.bboff[k]) * SZ;   // element i of buffer k
+            }
+          } else {
+            for (int q = 0; q < p; ++q) s_seqk[q] = s_seq[q] + P.bboff[k] * SZ;
           }
-          s_piece[0] = a;
-          const long long mend = gstart[a + 1] - P.bboff[k];
-          s_piece[1] = mend < hi ? mend : hi;
+          bool vec = al16(bo) && al16(red);
+          for (int q = 0; q < p; ++q) vec = vec && al16(s_seqk[q]);
+          s_bo = bo;
+          s_rd = red;
+          s_pe = pe;
+          s_vec = vec ? 1 : 0;
         }
-        __syncthreads();
-        const int mi = (int)s_piece[0];
-        const long long pe = s_piece[1];
-        if (tid < p) {
-          const char* base = *reinterpret_cast<char* const*>(
-              myheap + REG_OFF + ((size_t)gid[mi] * MAXP + s_rord[tid]) * 8);
-          s_seqk[tid] = base - (gstart[mi] - P.bboff[k]) * SZ;   // element i of buffer k
-        }
-        __syncthreads();
-        bool vec = al16(bo) && al16(red);
-        for (int q = 0; q < p; ++q) vec = vec && al16(s_seqk[q]);
-        if (P.bulk_rs && vec)
-          reduce_range_bulk<D, OP, MP, TREE>(BR, s_seqk, p, m, excess, i, pe, P.average, bo, 0, red, 0, tid,
-                                             s_localk);
-        else
-          reduce_range<D, OP, MP, TREE>(s_seqk, p, m, excess, i, pe, vec, P.average, bo, 0, red, 0,
-                                        tid, blockDim.x);
-        __syncthreads();
-        i = pe;
       }
+      __syncthreads();
+      if (s_k >= P.nbuf) break;
+      if (P.bulk_rs && s_vec)
+        reduce_range_bulk<D, OP, MP, TREE>(P.bulk_rs, P.bulk_stage, s_seqk, p, m, excess, s_i, s_pe, P.average, s_bo, 0, s_rd, 0, tid);
+      else
+        reduce_range<D, OP, MP, TREE>(s_seqk, p, m, excess, s_i, s_pe, s_vec != 0, P.average, s_bo, 0, s_rd, 0,
+                                      tid, blockDim.x);
+      __syncthreads();
+      if (tid == 0) s_i = s_pe;
     }
     CM_TRACE(P, lr, b, 3);
     if (tid < p) st_release_sys(mid_slot(P.heap[tid], b, rank), e);
@@ -423,7 +421,7 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
           const long long so = P.bseg_off[k][q], sl = P.bseg_len[k][q];
           const long long lo = slice_bound(so, sl, b, nb), hi = slice_bound(so, sl, b + 1, nb);
           if (hi <= lo) continue;
-          s_cr[r++] = CopyRange{s_src[q] + P.bboff[k] * SZ, P.bout[k], 0, 0, lo, hi};
+          s_cr[r++] = CopyRange{s_src[q] + P.bboff[k] * SZ, out + P.bout_off[k] * SZ, 0, 0, lo, hi};
         }
       s_ncr = r;
     }
@@ -432,6 +430,7 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
     goto finish;
   }
 
+  if constexpr (!MULTI) {
   // 3. reduce my segment (RS) — or the whole vector (one-shot)
   if (P.phases & PH_RS) {
     const long long so = P.oneshot ? 0 : mso;
@@ -452,8 +451,8 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
     }
     const long long lo = slice_bound(so, sl, b, nb), hi = slice_bound(so, sl, b + 1, nb);
     if (P.bulk_rs && vec)
-      reduce_range_bulk<D, OP, MP, TREE>(BR, s_seq, p, m, excess, lo, hi, P.average, out, out_shift, red,
-                                         red_shift, tid, s_localk);
+      reduce_range_bulk<D, OP, MP, TREE>(P.bulk_rs, P.bulk_stage, s_seq, p, m, excess, lo, hi, P.average, out, out_shift, red,
+                                         red_shift, tid);
     else
       reduce_range<D, OP, MP, TREE>(s_seq, p, m, excess, lo, hi, vec, P.average, out, out_shift,
                                     red, red_shift, tid, blockDim.x);
@@ -480,7 +479,8 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
     if (tid == 0) {
       int k = 0;
       for (int q = 0; q < p; ++q) {
-        if (q == rank && !(ag_only && P.srcmode == SRC_ZEROCOPY)) continue;
+        // (allgather with my segment read in place: copy my own part too)
+        if (q == rank && !(ag_only && (P.srcmode == SRC_ZEROCOPY || P.srcmode == SRC_REGISTERED))) continue;
         const long long so = P.seg_off[q], sl = P.seg_len[q];
         const long long lo = slice_bound(so, sl, b, nb), hi = slice_bound(so, sl, b + 1, nb);
         if (hi <= lo) continue;
@@ -490,6 +490,8 @@ __global__ void __launch_bounds__(THREADS) collective_kernel(const __grid_consta
     }
     __syncthreads();
     multi_copy<D, MP>(s_cr, s_ncr, s_vr);
+  }
+
   }
 
 finish:
@@ -502,6 +504,10 @@ finish:
     if (old == (unsigned)nb - 1) {
       ctrl->done = 0;
       ctrl->ag_next = 0;
+      if (P.agree_inline) {               // outcome for the gated launches queued behind
+        ctrl->agree_ok = s_skip == 2 ? 0 : 1;
+        ctrl->agree_tag = P.agree_ticket;
+      }
       ctrl->epoch = e;
       __threadfence();
     }

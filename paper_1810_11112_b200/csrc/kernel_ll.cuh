@@ -48,7 +48,7 @@ __device__ __forceinline__ bool ll_wait(const char* slot, unsigned f, unsigned l
 }
 
 template <class D, int OP, int MP, bool TREE>
-__global__ void __launch_bounds__(THREADS) ll_kernel(const __grid_constant__ CollParams P) {
+__global__ void __launch_bounds__(THREADS, 1) ll_kernel(const __grid_constant__ CollParams P) {
   using S = typename D::S;
   using A = typename D::A;
   constexpr int E = 8 / sizeof(S);                    // elements per unit
@@ -57,6 +57,7 @@ __global__ void __launch_bounds__(THREADS) ll_kernel(const __grid_constant__ Col
   const int b = blockIdx.x, nb = gridDim.x, p = P.p, tid = threadIdx.x;
   char* myheap = P.heap[rank];
   Ctrl* ctrl = reinterpret_cast<Ctrl*>(myheap + CTRL_OFF);
+  if (gated_out(P, ctrl)) return;
   __shared__ unsigned long long s_epoch;
   __shared__ int s_err;
   __shared__ int s_seq[MAXP];
@@ -151,7 +152,8 @@ __global__ void __launch_bounds__(THREADS) ll_kernel(const __grid_constant__ Col
     for (int t = 0; t < E; ++t) res.s[t] = from_acc<D>(P.average ? div_p<A>(v[0][t], p) : v[0][t]);
     // agreement check (cm_agree): the MAX of every rank's values equals mine
     // for all values on every rank iff all ranks hold the same values
-    if (P.done_flag && u < 8 && (long long)(((unsigned long long)res.u.y << 32) | res.u.x) != P.inl[u])
+    if (P.done_flag && u < 8 &&
+        (long long)(((unsigned long long)res.u.y << 32) | res.u.x) != reinterpret_cast<const long long*>(in)[u])
       s_disagree = 1;
     const long long boff = u * 8;
     if (boff + 8 <= nbytes && ((((uintptr_t)out) & 7u) == 0)) {
@@ -175,7 +177,7 @@ ll_finish:
         ctrl->agree_ok = s_disagree ? 0 : 1;   // read by gated collectives queued behind
         ctrl->agree_tag = P.done_value;
         __threadfence_system();
-        *reinterpret_cast<volatile unsigned long long*>(P.done_flag) = P.done_value;
+        reinterpret_cast<volatile unsigned long long*>(P.done_flag)[lr] = P.done_value;
       }
     }
   }
@@ -215,7 +217,7 @@ __device__ __forceinline__ void unpack_elems(char* base, long long i, int cnt, u
 }
 
 template <class D, int OP, int MP, bool TREE>
-__global__ void __launch_bounds__(THREADS) ll2_kernel(const __grid_constant__ CollParams P) {
+__global__ void __launch_bounds__(THREADS, 1) ll2_kernel(const __grid_constant__ CollParams P) {
   using S = typename D::S;
   using A = typename D::A;
   constexpr int E = 8 / sizeof(S);
@@ -224,6 +226,7 @@ __global__ void __launch_bounds__(THREADS) ll2_kernel(const __grid_constant__ Co
   const int b = blockIdx.x, nb = gridDim.x, p = P.p, tid = threadIdx.x, bd = blockDim.x;
   char* myheap = P.heap[rank];
   Ctrl* ctrl = reinterpret_cast<Ctrl*>(myheap + CTRL_OFF);
+  if (gated_out(P, ctrl)) return;
   __shared__ unsigned long long s_epoch;
   __shared__ int s_err;
   __shared__ int s_seq[MAXP];

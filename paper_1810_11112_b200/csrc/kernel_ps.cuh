@@ -66,7 +66,7 @@ __device__ __forceinline__ void ps_pieces(const long long* table, int p, int q, 
 
 
 template <class D>
-__global__ void __launch_bounds__(THREADS) ps_kernel(const __grid_constant__ PsParams P) {
+__global__ void __launch_bounds__(THREADS, 1) ps_kernel(const __grid_constant__ PsParams P) {
   using S = typename D::S;
   constexpr int SZ = sizeof(S);
   constexpr int PS_U = SZ == 8 ? 4 : 8;   // elements in flight per thread (f64: keeps 2 CTAs/SM)

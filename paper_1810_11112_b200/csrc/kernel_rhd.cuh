@@ -90,12 +90,13 @@ __device__ void pair_pass(const char* a, const char* b, char* dst_raw, char* dst
 }
 
 template <class D, int OP>
-__global__ void __launch_bounds__(THREADS) rhd_kernel(const __grid_constant__ CollParams P) {
+__global__ void __launch_bounds__(THREADS, 1) rhd_kernel(const __grid_constant__ CollParams P) {
   const int lr = P.virt ? blockIdx.y : 0;
   const int rank = P.virt ? (int)blockIdx.y : P.rank;
   const int b = blockIdx.x, nb = gridDim.x, p = P.p, tid = threadIdx.x;
   char* myheap = P.heap[rank];
   Ctrl* ctrl = reinterpret_cast<Ctrl*>(myheap + CTRL_OFF);
+  if (gated_out(P, ctrl)) return;
   __shared__ unsigned long long s_epoch;
   __shared__ int s_err;
   CM_TRACE(P, lr, b, 0);

@@ -22,7 +22,7 @@ namespace dev {
 
 // ---- local_reduce (core.py:94-110) -------------------------------------------------
 template <class D, int OP>
-__global__ void __launch_bounds__(THREADS) local_reduce_kernel(const char* a, const char* b, char* out,
+__global__ void __launch_bounds__(THREADS, 1) local_reduce_kernel(const char* a, const char* b, char* out,
                                                               long long n, int vec) {
   using S = typename D::S;
   using A = typename D::A;
@@ -47,14 +47,20 @@ __global__ void __launch_bounds__(THREADS) local_reduce_kernel(const char* a, co
 }
 
 // kernel table of one element type: kind 0 collective, 1 pipelined two-shot,
-// 2 LL one-shot, 3 LL two-shot, 4 log-p recursive halving/doubling (defined in csrc/inst_<type>.cu)
+// 2 LL one-shot, 3 LL two-shot, 4 log-p recursive halving/doubling, 5 multi-buffer collective (defined in csrc/inst_<type>.cu)
 #define CM_KERNEL_TABLE(D)                                                          \
   template <int OP, int MP>                                                         \
   static void* cm_table_coll_##D(int kind, bool tree) {                             \
-    if (kind == 1) return tree ? (void*)collective_kernel<D, OP, MP, true, true>    \
-                               : (void*)collective_kernel<D, OP, MP, false, true>;  \
-    return tree ? (void*)collective_kernel<D, OP, MP, true, false>                  \
-                : (void*)collective_kernel<D, OP, MP, false, false>;                \
+    if (kind == 1) return tree ? (void*)collective_kernel<D, OP, MP, true, true, false>    \
+                               : (void*)collective_kernel<D, OP, MP, false, true, false>;  \
+    if (kind == 5) {                     /* aggregate only: SUM */                 \
+      if constexpr (OP == CM_SUM)                                                   \
+        return tree ? (void*)collective_kernel<D, OP, MP, true, false, true>        \
+                    : (void*)collective_kernel<D, OP, MP, false, false, true>;      \
+      return nullptr;                                                               \
+    }                                                                               \
+    return tree ? (void*)collective_kernel<D, OP, MP, true, false, false>                  \
+                : (void*)collective_kernel<D, OP, MP, false, false, false>;                \
   }                                                                                 \
   template <int OP, int MP>                                                         \
   static void* cm_table_ll_##D(int kind, bool tree) {                               \
@@ -64,7 +70,7 @@ __global__ void __launch_bounds__(THREADS) local_reduce_kernel(const char* a, co
   template <int OP>                                                                 \
   static void* cm_table_op_##D(int kind, int p, bool tree) {                        \
     if (kind == 4) return (void*)rhd_kernel<D, OP>;                                 \
-    if (kind >= 2) return p <= 8 ? cm_table_ll_##D<OP, 8>(kind, tree) : cm_table_ll_##D<OP, 16>(kind, tree); \
+    if (kind == 2 || kind == 3) return p <= 8 ? cm_table_ll_##D<OP, 8>(kind, tree) : cm_table_ll_##D<OP, 16>(kind, tree); \
     if (p <= 2) return cm_table_coll_##D<OP, 2>(kind, tree);                        \
     if (p <= 4) return cm_table_coll_##D<OP, 4>(kind, tree);                        \
     if (p <= 8) return cm_table_coll_##D<OP, 8>(kind, tree);                        \
@@ -75,8 +81,13 @@ __global__ void __launch_bounds__(THREADS) local_reduce_kernel(const char* a, co
 }  // namespace cm
 
 using cm_kfn_t = void (*)(cm::dev::CollParams);
-cm_kfn_t cm_kernels_f32(int kind, int op, int p, bool tree);
-cm_kfn_t cm_kernels_f64(int kind, int op, int p, bool tree);
-cm_kfn_t cm_kernels_bf16(int kind, int op, int p, bool tree);
-cm_kfn_t cm_kernels_i32(int kind, int op, int p, bool tree);
-cm_kfn_t cm_kernels_i64(int kind, int op, int p, bool tree);
+// one entry per (type, op) translation unit of csrc/inst.cu
+#define CM_INST_DECL(T)                              \
+  cm_kfn_t cm_kernels_##T##_sum(int kind, int p, bool tree); \
+  cm_kfn_t cm_kernels_##T##_max(int kind, int p, bool tree);
+CM_INST_DECL(f32)
+CM_INST_DECL(f64)
+CM_INST_DECL(bf16)
+CM_INST_DECL(i32)
+CM_INST_DECL(i64)
+#undef CM_INST_DECL

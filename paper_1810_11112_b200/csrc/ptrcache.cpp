@@ -10,6 +10,7 @@
 //    registered allocations through an ordered range map (torch hands out
 //    sub-allocations, so exact-address lookups are not enough on a GPU).
 // Every operation takes the registry mutex (registry.py:52-56 serialises).
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <chrono>
@@ -45,24 +46,51 @@ static std::string hexaddr(uint64_t a) {
   return b;
 }
 
-// Real driver query: memory type of `addr` (unregistered host memory is HOST).
-int Registry::driver_query_real(uint64_t addr, int* kind, bool count) {
-  cudaPointerAttributes attr;
+// Real driver query: ONE cuPointerGetAttributes call for memory type, device
+// ordinal, allocation range and buffer id (unregistered host memory is HOST).
+typedef CUresult (*PtrAttrsFn)(unsigned, CUpointer_attribute*, void**, CUdeviceptr);
+
+static PtrAttrsFn ptr_attrs_fn() {
+  static PtrAttrsFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuPointerGetAttributes", &f, cudaEnableDefault, &q) != cudaSuccess) {
+      cudaGetLastError();
+      f = nullptr;
+    }
+    return reinterpret_cast<PtrAttrsFn>(f);
+  }();
+  return fn;
+}
+
+int Registry::driver_query_real(uint64_t addr, Info* info, bool count) {
+  PtrAttrsFn fn = ptr_attrs_fn();
+  if (!fn) return fail(CM_ERR_UNSUPPORTED, "cuPointerGetAttributes unavailable");
+  unsigned mtype = 0;
+  int dev = -1;
+  CUdeviceptr start = 0;
+  size_t size = 0;
+  unsigned long long bid = 0;
+  unsigned managed = 0;
+  CUpointer_attribute at[6] = {CU_POINTER_ATTRIBUTE_MEMORY_TYPE, CU_POINTER_ATTRIBUTE_DEVICE_ORDINAL,
+                               CU_POINTER_ATTRIBUTE_RANGE_START_ADDR, CU_POINTER_ATTRIBUTE_RANGE_SIZE,
+                               CU_POINTER_ATTRIBUTE_BUFFER_ID, CU_POINTER_ATTRIBUTE_IS_MANAGED};
+  void* val[6] = {&mtype, &dev, &start, &size, &bid, &managed};
   const auto t0 = std::chrono::steady_clock::now();
-  cudaError_t e = cudaPointerGetAttributes(&attr, reinterpret_cast<const void*>(addr));
+  CUresult r = fn(6, at, val, (CUdeviceptr)addr);
   const auto t1 = std::chrono::steady_clock::now();
   if (count) {
     st.driver_queries += 1;
     query_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count();
   }
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    return fail(CM_ERR_UNKNOWN_BUFFER, "driver query failed for " + hexaddr(addr) + ": " +
-                                           cudaGetErrorString(e));
-  }
-  *kind = (attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged)
-              ? CM_KIND_DEVICE
-              : CM_KIND_HOST;
+  if (r != CUDA_SUCCESS)
+    return fail(CM_ERR_UNKNOWN_BUFFER, "driver query failed for " + hexaddr(addr) + " (CUresult " +
+                                           std::to_string((int)r) + ")");
+  info->kind = (mtype == CU_MEMORYTYPE_DEVICE || managed) ? CM_KIND_DEVICE : CM_KIND_HOST;
+  info->device = mtype ? dev : -1;
+  info->start = (uint64_t)start;
+  info->size = (int64_t)size;
+  info->buffer_id = bid;
   return CM_OK;
 }
 
@@ -83,23 +111,35 @@ const Registry::Range* Registry::find_range(uint64_t addr) const {
   return nullptr;
 }
 
-int Registry::classify(uint64_t addr, int* kind) {
+int Registry::classify(uint64_t addr, int* kind, Info* info) {
   std::lock_guard<std::mutex> g(mu);
-  if (policy == CM_NO_CACHE)
-    return simulated ? driver_query_sim(addr, kind) : driver_query_real(addr, kind, true);
+  Info tmp;
+  Info* out = info ? info : &tmp;
+  if (policy == CM_NO_CACHE) {
+    int s;
+    if (simulated) {
+      s = driver_query_sim(addr, &out->kind);
+    } else {
+      s = driver_query_real(addr, out, true);
+    }
+    if (!s) *kind = out->kind;
+    return s;
+  }
   if (policy == CM_LAZY_CACHE) {                             // registry.py:110-117
     auto it = cache.find(addr);
     if (it != cache.end()) {
       st.cache_hits += 1;
-      *kind = it->second;
+      *out = it->second;
+      *kind = it->second.kind;
       return CM_OK;
     }
-    int k;
-    int s = simulated ? driver_query_sim(addr, &k) : driver_query_real(addr, &k, true);
+    Info in;
+    int s = simulated ? driver_query_sim(addr, &in.kind) : driver_query_real(addr, &in, true);
     if (s) return s;
-    cache[addr] = k;
+    cache[addr] = in;
     st.inserts += 1;
-    *kind = k;
+    *out = in;
+    *kind = in.kind;
     return CM_OK;
   }
   // intercept: the cache is authoritative, zero driver traffic (registry.py:118-123)
@@ -108,13 +148,21 @@ int Registry::classify(uint64_t addr, int* kind) {
     if (it == cache.end())
       return fail(CM_ERR_UNKNOWN_BUFFER, "classify of never-allocated address " + hexaddr(addr));
     st.cache_hits += 1;
-    *kind = it->second;
+    *out = it->second;
+    *kind = it->second.kind;
     return CM_OK;
   }
-  const Range* r = find_range(addr);
-  if (!r) return fail(CM_ERR_UNKNOWN_BUFFER, "classify of never-registered address " + hexaddr(addr));
+  auto it = ranges.upper_bound(addr);
+  if (it == ranges.begin())
+    return fail(CM_ERR_UNKNOWN_BUFFER, "classify of never-registered address " + hexaddr(addr));
+  --it;
+  if (addr >= it->first + (uint64_t)it->second.size)
+    return fail(CM_ERR_UNKNOWN_BUFFER, "classify of never-registered address " + hexaddr(addr));
   st.cache_hits += 1;
-  *kind = r->kind;
+  out->kind = it->second.kind;
+  out->start = it->first;
+  out->size = it->second.size;
+  *kind = it->second.kind;
   return CM_OK;
 }
 
@@ -144,7 +192,7 @@ int Registry::alloc(int kind, int64_t size, uint64_t* out) {
   }
   live[a] = Live{size, kind};
   if (policy == CM_INTERCEPT_CACHE) {
-    if (simulated) { cache[a] = kind; st.inserts += 1; }
+    if (simulated) { Info in; in.kind = kind; cache[a] = in; st.inserts += 1; }
     else insert_range(a, size, kind);
   }
   *out = a;
@@ -179,7 +227,7 @@ int Registry::register_range(uint64_t addr, int64_t size, int kind) {
   std::lock_guard<std::mutex> g(mu);
   if (simulated) {
     live[addr] = Live{size, kind};
-    if (policy == CM_INTERCEPT_CACHE) { cache[addr] = kind; st.inserts += 1; }
+    if (policy == CM_INTERCEPT_CACHE) { Info in; in.kind = kind; cache[addr] = in; st.inserts += 1; }
     return CM_OK;
   }
   if (policy == CM_INTERCEPT_CACHE) insert_range(addr, size, kind);
@@ -207,7 +255,10 @@ int Registry::ground_truth(uint64_t addr, int* kind) {
     *kind = it->second.kind;
     return CM_OK;
   }
-  return driver_query_real(addr, kind, false);
+  Info in;
+  int s = driver_query_real(addr, &in, false);
+  if (!s) *kind = in.kind;
+  return s;
 }
 
 std::string Registry::stats_json() {
@@ -263,6 +314,18 @@ int cm_registry_unregister(cm_registry_t* reg, uint64_t address) {
 }
 int cm_registry_classify(cm_registry_t* reg, uint64_t address, int* kind) {
   return REG(reg)->classify(address, kind);
+}
+int cm_registry_info(cm_registry_t* reg, uint64_t address, cm_buffer_info_t* out) {
+  Registry::Info in;
+  int kind = 0;
+  int s = REG(reg)->classify(address, &kind, &in);
+  if (s) return s;
+  out->kind = in.kind;
+  out->device = in.device;
+  out->range_start = in.start;
+  out->range_size = in.size;
+  out->buffer_id = in.buffer_id;
+  return CM_OK;
 }
 int cm_registry_ground_truth(cm_registry_t* reg, uint64_t address, int* kind) {
   return REG(reg)->ground_truth(address, kind);

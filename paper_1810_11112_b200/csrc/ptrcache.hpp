@@ -25,6 +25,15 @@ struct Registry {
     int64_t size;
     int kind;
   };
+  // what a cache entry records about an address (real backend: one
+  // cuPointerGetAttributes call; sim backend: the kind only)
+  struct Info {
+    int kind = CM_KIND_HOST;
+    int device = -1;
+    uint64_t start = 0;       // allocation range holding the address
+    int64_t size = 0;
+    uint64_t buffer_id = 0;   // unique per allocation, never reused
+  };
 
   int policy = CM_NO_CACHE;
   int64_t delay_ns = 1000;
@@ -39,7 +48,7 @@ struct Registry {
   std::map<uint64_t, Live> external;
   // simulated caches are exact-address (registry.py:68); real intercept cache
   // is a range map; real lazy cache is exact-address like the reference
-  std::unordered_map<uint64_t, int> cache;
+  std::unordered_map<uint64_t, Info> cache;
   std::map<uint64_t, Range> ranges;
   std::priority_queue<uint64_t, std::vector<uint64_t>, std::greater<uint64_t>> freed;
   uint64_t next_address = 0x1000;                            // registry.py:20
@@ -49,12 +58,12 @@ struct Registry {
   int free_(uint64_t addr);
   int register_range(uint64_t addr, int64_t size, int kind);
   int unregister_range(uint64_t addr);
-  int classify(uint64_t addr, int* kind);
+  int classify(uint64_t addr, int* kind, Info* info = nullptr);
   int ground_truth(uint64_t addr, int* kind);
   std::string stats_json();
 
  private:
-  int driver_query_real(uint64_t addr, int* kind, bool count);
+  int driver_query_real(uint64_t addr, Info* info, bool count);
   int driver_query_sim(uint64_t addr, int* kind);
   int insert_range(uint64_t addr, int64_t size, int kind);
   const Range* find_range(uint64_t addr) const;

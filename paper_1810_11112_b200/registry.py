@@ -6,8 +6,10 @@ every collective call.
 ``backend="sim"`` (default) reproduces the reference model exactly (fake
 addresses, lowest-freed-address reuse, counted simulated driver queries);
 ``backend="cuda"`` allocates real device / pinned-host memory and the driver
-query is ``cudaPointerGetAttributes`` (its measured wall time is reported by
-``query_delay_seconds``).
+query is one ``cuPointerGetAttributes`` call (memory type, device ordinal,
+allocation range, buffer id; its measured wall time is reported by
+``query_delay_seconds``); the intercept cache answers interior pointers of
+registered ranges (torch sub-allocations).
 """
 
 from __future__ import annotations
@@ -98,6 +100,17 @@ class BufferRegistry:
         k = C.c_int()
         L.check(L.lib.cm_registry_classify(self._h, addr, C.byref(k)))
         return BufferKind(L.KIND_NAME[k.value])
+
+    def info(self, handle: BufferHandle | int) -> dict:
+        """Classify through the policy and return what the cache entry holds:
+        kind, device ordinal, allocation range and buffer id (real backend;
+        the sim backend and the intercept cache know the kind / range only)."""
+        addr = handle.address if isinstance(handle, BufferHandle) else int(handle)
+        bi = L.BufferInfo()
+        L.check(L.lib.cm_registry_info(self._h, addr, C.byref(bi)))
+        return {"kind": BufferKind(L.KIND_NAME[bi.kind]), "device": int(bi.device),
+                "range_start": int(bi.range_start), "range_size": int(bi.range_size),
+                "buffer_id": int(bi.buffer_id)}
 
     def ground_truth(self, handle: BufferHandle | int) -> BufferKind:
         addr = handle.address if isinstance(handle, BufferHandle) else int(handle)

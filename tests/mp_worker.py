@@ -32,7 +32,7 @@ def sha(b):
 def main():
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
-    local = int(os.environ.get("LOCAL_RANK", rank))
+    local = int(os.environ.get("LOCAL_RANK", rank)) % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dist.init_process_group("gloo")
     comm = P.Communicator(staging_bytes=256 << 20, pool_bytes=512 << 20, timeout_s=20.0)
@@ -355,6 +355,105 @@ def main():
     expect(res.names == sorted(nm for nm, _ in schema), "aggregate partial readiness intersection")
     res2 = P.aggregate(gs, group, comm)          # second call takes the same fallback
     expect([t.to_bytes() for t in res2.tensors] == [t.to_bytes() for t in res.tensors], "fallback repeatable")
+
+    # 4g. differing PLANS under a pending agreement: rank 0 holds an extra
+    # 5M-element tensor (more fused groups and launches than its peers), the
+    # last rank an extra small tensor that sorts first (its first group is a
+    # small LL-sized one). The call structure must not depend on the plan:
+    # the check fails identically everywhere, no rank moves data, the
+    # intersection is aggregated, and the collectives that follow line up.
+    base = I.synth_gradients(11, 0, [480_000] * 20 + [3, 1_000_000, 64], rank)
+    extra = []
+    if rank == 0:
+        extra = [("layer9999_big", np.full(5_000_000, 1.0, np.float32))]
+    if rank == world - 1:
+        extra = [("aaa_small_first", np.full(100, 2.0, np.float32))]
+    want_i, _, _ = OA.aggregate([I.synth_gradients(11, 0, [480_000] * 20 + [3, 1_000_000, 64], r)
+                                 for r in range(world)], "float32", "auto", 8 << 20)
+    for inline in (2, 1):
+        comm.set_param("inline_agree", inline)
+        for thr in (8 << 20, 64 << 20):
+            want_t, _, _ = OA.aggregate([I.synth_gradients(11, 0, [480_000] * 20 + [3, 1_000_000, 64], r)
+                                         for r in range(world)], "float32", "auto", thr)
+            gs = P.GradientSet(tuple(P.Tensor(nm, "float32", torch.from_numpy(a).cuda()) for nm, a in base + extra))
+            prev = P.aggregate(P.GradientSet(tuple(P.Tensor(nm, "float32", torch.from_numpy(a).cuda())
+                                                   for nm, a in base)), group, comm, cfg=P.FusionConfig(thr))
+            res = P.aggregate(gs, group, comm, cfg=P.FusionConfig(thr), out=prev)   # out= of another plan
+            expect(res.names == sorted(nm for nm, _ in base), f"differing plans: names inline={inline} thr={thr}")
+            expect(all(t.to_bytes() == want_t[t.name].tobytes() for t in res.tensors),
+                   f"differing plans: values inline={inline} thr={thr}")
+            for k in range(4):
+                gk = P.GradientSet(tuple(P.Tensor(nm, "float32", torch.from_numpy(a).cuda()) for nm, a in base))
+                rk = P.aggregate(gk, group, comm, cfg=P.FusionConfig(8 << 20))
+                expect(all(t.to_bytes() == want_i[t.name].tobytes() for t in rk.tensors),
+                       f"after differing plans: aggregate {k} inline={inline} thr={thr}")
+                x = torch.full((70_001 + k,), float(rank + k), device="cuda")
+                out, _ = P.allreduce(P.Tensor("x", "float32", x), P.ReduceOp.SUM, group, comm)
+                expect(bool(torch.all(out.payload == float(sum(r + k for r in range(world))))),
+                       f"after differing plans: allreduce {k} inline={inline} thr={thr}")
+    comm.set_param("inline_agree", 2)
+
+    # 4i. the communicator's pointer cache (registry.py:104-131): every call
+    # classifies send and recv; no_cache queries the driver each time,
+    # lazy_cache once per address, intercept_cache never (unregistered
+    # buffers are rejected with UnknownBufferError)
+    xs_small = torch.full((1000,), float(rank + 1), device="cuda")
+    ys_small = torch.empty_like(xs_small)
+    want_small = float(sum(r + 1 for r in range(world)))
+    for pol in ("no_cache", "lazy_cache", "intercept_cache"):
+        comm.set_policy(pol)
+        if pol == "intercept_cache":
+            try:
+                P.allreduce(P.Tensor("x", "float32", xs_small), P.ReduceOp.SUM, group, comm, out=ys_small)
+                expect(False, "intercept_cache must reject an unregistered buffer")
+            except P.UnknownBufferError:
+                pass
+            comm.register(xs_small)
+            comm.register(ys_small)
+        q0 = comm.registry_stats()["driver_queries"]
+        for _ in range(10):
+            P.allreduce(P.Tensor("x", "float32", xs_small), P.ReduceOp.SUM, group, comm, out=ys_small)
+            expect(bool(torch.all(ys_small == want_small)), f"policy {pol} result")
+        dq = comm.registry_stats()["driver_queries"] - q0
+        expect(dq == {"no_cache": 20, "lazy_cache": 2, "intercept_cache": 0}[pol], f"policy {pol}: {dq} queries")
+    comm.set_policy("lazy_cache")
+
+    # 4h. automatic registration (pointer cache -> IPC mapping, no host
+    # collective): plain torch tensors are copied in on first sight, then read
+    # in place once every peer has mapped their allocation; a freed and
+    # re-allocated range gets a new mailbox slot. Results stay bit-exact.
+    comm.set_param("auto_register", 2)
+    z0 = comm.get_param("auto_zero_copy_calls")
+    n_big = 3_000_017
+    for rep in range(3):
+        bufs = [torch.empty(n_big + 1000 * t, device="cuda") for t in range(3)]
+        for it in range(4):
+            for t, x in enumerate(bufs):
+                rng = np.random.default_rng([rep, it, t, rank])
+                xs_all = [np.random.default_rng([rep, it, t, r]).standard_normal(x.numel()).astype(np.float32)
+                          for r in range(world)]
+                x.copy_(torch.from_numpy(xs_all[rank]))
+                algo = ("ring_rsa", "rhd_rsa", "auto")[(it + t) % 3]
+                out, _ = P.allreduce(P.Tensor("x", "float32", x), P.ReduceOp.SUM, group, comm, algo=algo)
+                expect(out.to_bytes() == OC.allreduce(xs_all, "sum", algo, "float32").tobytes(),
+                       f"auto-registered allreduce rep={rep} it={it} t={t}")
+                del rng
+        seg, _ = P.reduce_scatter(P.Tensor("x", "float32", bufs[0]), P.ReduceOp.SUM, group, comm)
+        xs_all = [np.random.default_rng([rep, 3, 0, r]).standard_normal(bufs[0].numel()).astype(np.float32)
+                  for r in range(world)]
+        expect(seg.to_bytes() == OC.reduce_scatter(xs_all, "sum", "ring", "float32")[rank].tobytes(),
+               f"auto-registered reduce_scatter rep={rep}")
+        segx = seg.payload.clone()
+        full, _ = P.allgather(P.Tensor("s", "float32", segx), bufs[0].numel(), group, comm)
+        expect(full.to_bytes() == OC.allgather(OC.reduce_scatter(xs_all, "sum", "ring", "float32"),
+                                               bufs[0].numel(), "ring", "float32").tobytes(),
+               f"auto-registered allgather rep={rep}")
+        del bufs, segx
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()            # the ranges go back to the driver; new ones may reuse them
+    expect(comm.get_param("auto_published") >= 3, "allocations published in the mailbox")
+    expect(comm.get_param("auto_mapped") >= 3, "peers' allocations mapped")
+    expect(comm.get_param("auto_zero_copy_calls") > z0, "plain tensors read in place")
 
     # 5. negotiation: partial intersection falls back to the control plane
     ready = ["a", "b", "c"] if rank == 0 else ["b", "c", "d"]

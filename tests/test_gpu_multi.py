@@ -20,15 +20,26 @@ def _free_port():
     return port
 
 
-def _run(n):
+def _run(n, extra_env=None):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
            os.path.join(ROOT, "tests", "mp_worker.py")]
-    env = dict(os.environ, OMP_NUM_THREADS="1")
+    env = dict(os.environ, OMP_NUM_THREADS="1", **(extra_env or {}))
     proc = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
     out = proc.stdout + proc.stderr
     assert proc.returncode == 0, out[-6000:]
     assert out.count("checks passed") == n, out[-3000:]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [2, 3, 4, 8])
+def test_ranks_sharing_one_gpu(n):
+    """The real multi-process communicator (CUDA-IPC heaps, NVLink flag
+    protocol, cm_fused_allreduce_agreed, cm_agree, registration, the host
+    pipeline, the parameter server) with n processes on ONE GPU: IPC handles
+    open within a device too, and the contexts' kernels interleave, so every
+    cross-process path of the N-GPU tier runs on a single-GPU box."""
+    _run(n, {"CUDA_VISIBLE_DEVICES": os.environ.get("CUDA_VISIBLE_DEVICES", "0").split(",")[0]})
 
 
 @pytest.mark.gpu
@@ -50,8 +61,7 @@ def test_eight_gpus():
 
 
 @pytest.mark.gpu
-@pytest.mark.multigpu(2)
-def test_cli_microbench_and_train_two_gpus(tmp_path):
+def test_cli_microbench_and_train_two_ranks(tmp_path):
     """The reference-format harness (cli.py) under torchrun: CSV header and
     rows as collectium writes them, plus the B200 columns."""
     out = tmp_path / "micro.csv"

@@ -404,7 +404,7 @@ def test_dynamic_allgather_and_sm_reduce_variants(p):
     xs = [(rng.standard_normal(n) * 10.0 ** rng.integers(-3, 4, size=n)).astype(np.float32) for _ in range(p)]
     for algo in ("ring_rsa", "rhd_rsa"):
         want = OC.allreduce(xs, "sum", algo, "float32").tobytes()
-        for knobs in ({"dyn_ag": 2}, {"bulk_rs": 1}, {"bulk_rs": 3, "dyn_ag": 2}, {"bulk_local": 2},
+        for knobs in ({"dyn_ag": 2}, {"bulk_rs": 1}, {"bulk_rs": 3, "dyn_ag": 2},
                       {"bulk_stage_kb": 16}, {"bulk_stage_kb": 112}):
             for k, v in knobs.items():
                 g.set_param(k, v)
@@ -413,6 +413,5 @@ def test_dynamic_allgather_and_sm_reduce_variants(p):
                 assert all(t.to_bytes() == want for t, _ in res), knobs
             g.set_param("dyn_ag", 1)
             g.set_param("bulk_rs", 6)
-            g.set_param("bulk_local", 1)
             g.set_param("bulk_stage_kb", 64)
     g.close()
