@@ -106,6 +106,9 @@ struct cm_comm {
   int bulk_rs = 6;                            // reduce phase: bulk-engine stages in smem (0: SM loads)
   int dyn_ag = 0;                             // allgather as a shared (slice, peer) task queue (opt-in)
   int inline_agree = 1;                       // aggregate's agreement inside the collective's records
+  int overlap = 0;                            // multi-buffer two-shot: RS and AG CTAs run concurrently
+                                              // (opt-in: measured slower, the RS needs every SM)
+  int ovl_chunks = 4;                         // reduce chunks per progress report (overlap)
   int bulk_stage = 2 * RS_STAGE_BYTES;        // bytes per bulk-reduce stage (64 KiB: 3 stages fit)
   int64_t host_chunk = 8 << 20;               // host-gradient pipeline: bytes per H2D/D2H piece (p = 1)
   int64_t oneshot_bytes_per_cta = 8 * 1024;
@@ -411,8 +414,9 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
   if (ll == 1) nb = ((L.n * (int64_t)sz + 7) / 8 + c->ll_units_per_cta - 1) / c->ll_units_per_cta;
   if (ll == 2) nb = ((maxseg * (int64_t)sz + 7) / 8 + c->ll2_units_per_cta - 1) / c->ll2_units_per_cta;
   if (logp) nb = (L.n * (int64_t)sz + c->twoshot_bytes_per_cta - 1) / c->twoshot_bytes_per_cta;
-  if (L.force_pull) nb = MAXBLK;      // the full grid: independent of the (rank-local) plan
-  nb = std::max<int64_t>(1, std::min<int64_t>(nb, std::min(c->max_ctas, MAXBLK)));
+  const int full = std::max(2, std::min(c->max_ctas, MAXBLK) & ~1);
+  if (L.force_pull) nb = full;        // the full grid (even): independent of the (rank-local) plan
+  nb = std::max<int64_t>(1, std::min<int64_t>(nb, full));
   const bool tree = L.order == ORD_TREE;
   // pipelined two-shot when every CTA's slice spans >= 2 chunks
   const bool pipelined = ll == 0 && L.nbuf == 1 && L.srcmode != SRC_GATHER && !L.oneshot &&
@@ -439,6 +443,13 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
     while (stages > 1 && rs_smem_bytes(stages, c->bulk_stage) > (size_t)avail) --stages;
   P.bulk_rs = bulk ? stages : 0;
   P.bulk_stage = c->bulk_stage;
+  // overlapped two-shot: half the grid reduce-scatters, half allgathers
+  const bool ovl = multi && c->overlap && bulk && !c->dyn_ag;
+  if (ovl) {
+    int64_t nrs = std::max<int64_t>(1, std::min<int64_t>(nb, full / 2));
+    if (L.force_pull) nrs = full / 2;
+    nb = 2 * nrs;
+  }
   const size_t dsm = bulk ? rs_smem_bytes(stages, c->bulk_stage) : 0;
   void* args[] = {&P};
   int64_t alg = 0;   // busBW bytes of this launch (nccl-tests convention)
@@ -451,11 +462,17 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
     int per_sm = 0;
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k, THREADS, dsm));
     const int64_t cap = (int64_t)per_sm * c->sms / p;
-    if (cap < 1) return fail(CM_ERR_CONFIG, "virtual group too large for one GPU");
-    nb = std::min(nb, cap);
+    if (cap < (ovl ? 2 : 1)) return fail(CM_ERR_CONFIG, "virtual group too large for one GPU");
+    nb = std::min<int64_t>(nb, ovl ? (cap & ~(int64_t)1) : cap);
+    P.overlap = ovl ? 1 : 0;
+    P.nrs = (int)(nb / 2);
+    P.ovl_chunks = c->ovl_chunks;
     CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k, dim3((unsigned)nb, (unsigned)p),
                                          dim3(THREADS), args, dsm, stream));
   } else {
+    P.overlap = ovl ? 1 : 0;
+    P.nrs = (int)(nb / 2);
+    P.ovl_chunks = c->ovl_chunks;
     CUDA_TRY(cudaLaunchKernel((const void*)k, dim3((unsigned)nb), dim3(THREADS), args, dsm, stream));
   }
   c->launches += 1;
@@ -1161,6 +1178,8 @@ int cm_comm_set_param(cm_comm_t* c, const char* key, int64_t value) {
   else if (k == "dyn_ag") c->dyn_ag = value > 1 ? 1 : 0;
   else if (k == "inline_agree") c->inline_agree = value > 1 ? 1 : 0;
   else if (k == "auto_register") c->auto_reg = value > 1 ? 1 : 0;
+  else if (k == "overlap") c->overlap = value > 1 ? 1 : 0;
+  else if (k == "overlap_chunks") c->ovl_chunks = (int)std::min<int64_t>(value, 1 << 20);
   else if (k == "host_chunk_kb") c->host_chunk = std::max<int64_t>(64, value) * 1024;
   else if (k == "bulk_stage_kb") c->bulk_stage = (int)std::max<int64_t>(4, std::min<int64_t>(value, 112)) * 1024;
   else if (k == "oneshot_bytes_per_cta") c->oneshot_bytes_per_cta = value;
@@ -1185,6 +1204,8 @@ int cm_comm_get_param(cm_comm_t* c, const char* key, int64_t* value) {
   else if (k == "dyn_ag") *value = c->dyn_ag ? 2 : 1;
   else if (k == "inline_agree") *value = c->inline_agree ? 2 : 1;
   else if (k == "auto_register") *value = c->auto_reg ? 2 : 1;
+  else if (k == "overlap") *value = c->overlap ? 2 : 1;
+  else if (k == "overlap_chunks") *value = c->ovl_chunks;
   else if (k == "auto_published") *value = c->auto_published;
   else if (k == "auto_mapped") *value = c->auto_mapped;
   else if (k == "auto_zero_copy_calls") *value = c->auto_zc_calls;
@@ -1934,8 +1955,8 @@ int cm_ps_step_v(cm_comm_t* c, int n, const void* const* grads, void* const* par
     goff[t] = gtot;
     gtot += counts[t];
   }
-  if (2 * gtot * sz > (int64_t)c->staging_bytes)
-    return fail(CM_ERR_CONFIG, "parameter-server step needs 2 x " + std::to_string(gtot * sz) +
+  if (served_off(gtot, sz) + gtot * sz > (int64_t)c->staging_bytes)
+    return fail(CM_ERR_CONFIG, "parameter-server step needs " + std::to_string(served_off(gtot, sz) + gtot * sz) +
                                    " B of staging; the communicator has " + std::to_string(c->staging_bytes));
   // owner table: own_first[0..p], then {prefix, goff, len} per owned tensor
   std::vector<long long> tab(p + 1, 0);

@@ -80,8 +80,13 @@ constexpr size_t MAILBOX_OFF = AUTOTAB_OFF + AUTOTAB_SIZE;
 constexpr size_t MAILBOX_SIZE = (size_t)MAXAUTO * MAILBOX_BYTES;
 constexpr size_t ACK_OFF = MAILBOX_OFF + MAILBOX_SIZE;
 constexpr size_t ACK_SIZE = (size_t)MAXP * 8;
+// reduce-scatter progress of the overlapped two-shot: PROG[slice][src] =
+// (epoch << 32) | elements of slice `slice` (of every fused buffer, in order)
+// that rank `src` has reduced, pushed by src's reduce-scatter CTA
+constexpr size_t PROG_OFF = ACK_OFF + ACK_SIZE;
+constexpr size_t PROG_SIZE = (size_t)MAXBLK * MAXP * 8;
 constexpr size_t HEAP_ALIGN = 2ull << 20;
-constexpr size_t LL_OFF = ((ACK_OFF + ACK_SIZE + HEAP_ALIGN - 1) / HEAP_ALIGN) * HEAP_ALIGN;
+constexpr size_t LL_OFF = ((PROG_OFF + PROG_SIZE + HEAP_ALIGN - 1) / HEAP_ALIGN) * HEAP_ALIGN;
 // record source encoding for registered inputs: bit 62 | id << 40 | byte delta
 // (collective registration id), bit 62 | bit 61 | slot << 40 | delta (the
 // sender's automatically registered allocation slot)
@@ -180,6 +185,12 @@ struct CollParams {
   unsigned long long* agree_out;
   unsigned long long agree_ticket;
   int dyn_ag;                // allgather as a queue of (slice, peer) tasks shared by the CTAs
+  // overlapped two-shot (multi-buffer kernel): CTAs [0, nrs) reduce-scatter
+  // and publish per-chunk progress, CTAs [nrs, 2 nrs) allgather each peer's
+  // slice chunk by chunk as soon as it is reduced (no RS->AG barrier)
+  int overlap;
+  int nrs;
+  int ovl_chunks;            // reduce chunks per progress report / allgather block
   // automatic registration (real communicators): my published slot count,
   // the slot counts of each peer I have mapped, and host-mapped words where
   // CTA 0 reports peers' newer slot counts (notice[q]) and the smallest
@@ -707,11 +718,27 @@ __device__ __forceinline__ void bulk_rs_setup(int stages, int stage_bytes, int t
   }
 }
 
+// Progress publication of the overlapped two-shot: after each reduced chunk the
+// consumers synchronise and one thread pushes (tag | base + elements done in
+// this range) to every peer's PROG[blk][rank] with release semantics.
+struct Prog {
+  unsigned long long* dst[MAXP];   // peers' PROG slots for this CTA's slice (nullptr: self)
+  unsigned long long tag;          // epoch << 32
+  long long base;                  // slice-sequence position of the range start
+  int p;
+  int every;                       // report after every `every`-th chunk (and the last)
+};
+
+__device__ __forceinline__ void prog_publish(const Prog* pg, long long pos) {
+  for (int q = 0; q < pg->p; ++q)
+    if (pg->dst[q]) st_release_sys(pg->dst[q], pg->tag | (unsigned long long)pos);
+}
+
 // Same contract as reduce_range (sources 16-byte aligned at vector boundaries).
 template <class D, int OP, int MP, bool TREE>
 __device__ void reduce_range_bulk(int stages, int stage_bytes, const char* const* seq, int p, int m, int excess,
                                   long long lo, long long hi, int average, char* out, long long out_shift,
-                                  char* red, long long red_shift, int tid) {
+                                  char* red, long long red_shift, int tid, const Prog* prog = nullptr) {
   const BulkRS B = bulk_view(stages, stage_bytes);
   using S = typename D::S;
   using A = typename D::A;
@@ -724,6 +751,7 @@ __device__ void reduce_range_bulk(int stages, int stage_bytes, const char* const
                                    red_shift, tid, THREADS);
   const long long nbytes = (body_hi - body_lo) * SZ;
   if (nbytes <= 0) return;
+  if (prog) __syncthreads();      // the scalar head/tail precede every progress report
   const int ch = (B.stage_bytes / p) & ~15;             // bytes per source per stage
   const int C = (int)((nbytes + ch - 1) / ch);
   // stage uses so far in this launch (< 2^32): stage index and mbarrier phase
@@ -780,6 +808,14 @@ __device__ void reduce_range_bulk(int stages, int stage_bytes, const char* const
       __syncwarp();
       if ((tid & 31) == 0)
         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&B.empty[s])) : "memory");
+      if (prog && ((c + 1) % prog->every == 0 || c + 1 == C)) {   // chunks stored by every consumer: report
+        asm volatile("bar.sync 1, %0;" ::"r"(RS_CONSUMERS) : "memory");
+        if (tid == 0) {
+          // the scalar tail [body_hi, hi) was reduced before the first chunk
+          const long long done = c + 1 == C ? hi - lo : body_lo - lo + (long long)(c + 1) * (ch / SZ);
+          prog_publish(prog, prog->base + done);
+        }
+      }
       if (++s == B.stages) { s = 0; ph ^= 1u; }
     }
   }

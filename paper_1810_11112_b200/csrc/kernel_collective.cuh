@@ -330,35 +330,103 @@ __global__ void __launch_bounds__(THREADS, 1) collective_kernel(const __grid_con
   }
 
   if constexpr (MULTI) {
-    // ---- several fused buffers, one launch: RS of every buffer, ONE
-    // RS->AG barrier, AG of every buffer. Input prestaged in staging, or
-    // (SRC_GATHER) read in place from every rank's registered member tensors.
-    // The CTA walks its slice of every buffer as a sequence of pieces (a
-    // piece never crosses a member of a gathered buffer); thread 0 prepares
-    // each piece's source table in shared memory, so ONE reduce call site
-    // serves both input modes and no per-piece state lives in registers.
+    // ---- several fused buffers, one launch: RS of every buffer, then AG of
+    // every buffer. Input prestaged in staging, or (SRC_GATHER) read in place
+    // from every rank's registered member tensors. The CTA walks its slice of
+    // every buffer as a sequence of pieces (a piece never crosses a member of
+    // a gathered buffer); thread 0 prepares each piece's source table in
+    // shared memory, so ONE reduce call site serves both input modes and no
+    // per-piece state lives in registers.
+    //
+    // overlap: CTAs [0, nrs) reduce-scatter slice b and push their progress
+    // after every chunk; CTAs [nrs, 2 nrs) allgather slice b - nrs of every
+    // peer chunk by chunk as soon as that peer has reduced it. Otherwise every
+    // CTA reduces its slice, then one RS->AG barrier per CTA index, then AG.
     __shared__ const char* s_seqk[MAXP];
     __shared__ char* s_bo;
     __shared__ char* s_rd;
-    __shared__ long long s_i, s_pe, s_hi;
+    __shared__ long long s_i, s_pe, s_hi, s_pos;
     __shared__ int s_k, s_vec;
+    __shared__ Prog s_prog;
     int m = 1;
     while ((m << 1) <= p) m <<= 1;
     const int excess = p - m;
     char* mystage = myheap + stage_off;
+    const bool ovl = P.overlap != 0;
+    const int nrs = ovl ? P.nrs : nb;
+    if (ovl && b >= nrs) {
+      // ---- allgather role: slice j of every peer's segment, chunk by chunk
+      const int j = b - nrs;
+      // elements per allgather block: the reduce chunk times the report interval
+      const long long G = (long long)((P.bulk_stage / p) & ~15) / SZ * P.ovl_chunks;
+      __shared__ long long s_tot[MAXP];
+      if (tid < p) {
+        long long t = 0;
+        for (int k = 0; k < P.nbuf; ++k) {
+          const long long so = P.bseg_off[k][tid], sl = P.bseg_len[k][tid];
+          t += slice_bound(so, sl, j + 1, nrs) - slice_bound(so, sl, j, nrs);
+        }
+        s_tot[tid] = tid == rank ? 0 : t;
+      }
+      __syncthreads();
+      long long tmax = 0;
+      for (int q = 0; q < p; ++q) tmax = s_tot[q] > tmax ? s_tot[q] : tmax;
+      const unsigned long long tag = e << 32;
+#pragma unroll 1
+      for (long long pos = 0; pos < tmax; pos += G) {
+        if (tid < p && pos < s_tot[tid]) {
+          const long long need = pos + G < s_tot[tid] ? pos + G : s_tot[tid];
+          const unsigned long long* f =
+              reinterpret_cast<const unsigned long long*>(myheap + PROG_OFF + ((size_t)j * MAXP + tid) * 8);
+          if (!wait_geq(f, tag | (unsigned long long)need, P.timeout_cycles)) atomicExch(&s_err, ERR_TRANSPORT);
+        }
+        __syncthreads();
+        if (s_err) break;
+        if (tid == 0) {                               // [pos, pos + G) of each peer's slice sequence
+          int r = 0;
+          for (int q = 0; q < p; ++q) {
+            if (pos >= s_tot[q]) continue;
+            const long long end = pos + G < s_tot[q] ? pos + G : s_tot[q];
+            long long base = 0;
+            for (int k = 0; k < P.nbuf && base < end; ++k) {
+              const long long so = P.bseg_off[k][q], sl = P.bseg_len[k][q];
+              const long long lo = slice_bound(so, sl, j, nrs), hi = slice_bound(so, sl, j + 1, nrs);
+              const long long a = pos > base ? pos : base, z = end < base + hi - lo ? end : base + hi - lo;
+              if (z > a)
+                s_cr[r++] = CopyRange{P.heap[q] + stage_off + P.bboff[k] * SZ, out + P.bout_off[k] * SZ, 0, 0,
+                                      lo + (a - base), lo + (z - base)};
+              base += hi - lo;
+            }
+          }
+          s_ncr = r;
+        }
+        __syncthreads();
+        multi_copy<D, MP>(s_cr, s_ncr, s_vr);
+        __syncthreads();
+      }
+      goto finish;
+    }
     // piece iterator, advanced by thread 0 only (the loop state lives in
     // shared memory, not in every thread's registers)
     if (tid == 0) {
       s_k = -1;
       s_i = s_hi = 0;
+      s_pos = 0;
+      s_prog.tag = e << 32;
+      s_prog.p = p;
+      s_prog.every = P.ovl_chunks;
+      for (int q = 0; q < p; ++q)
+        s_prog.dst[q] = (ovl && q != rank)
+                            ? reinterpret_cast<unsigned long long*>(P.heap[q] + PROG_OFF + ((size_t)b * MAXP + rank) * 8)
+                            : nullptr;
     }
 #pragma unroll 1
     while (true) {
       if (tid == 0) {
         while (s_i >= s_hi && ++s_k < P.nbuf) {        // next buffer with a non-empty slice
           const long long so = P.bseg_off[s_k][rank], sl = P.bseg_len[s_k][rank];
-          s_i = slice_bound(so, sl, b, nb);
-          s_hi = slice_bound(so, sl, b + 1, nb);
+          s_i = slice_bound(so, sl, b, nrs);
+          s_hi = slice_bound(so, sl, b + 1, nrs);
         }
         if (s_k < P.nbuf) {
           const int k = s_k;
@@ -391,19 +459,30 @@ __global__ void __launch_bounds__(THREADS, 1) collective_kernel(const __grid_con
           s_rd = red;
           s_pe = pe;
           s_vec = vec ? 1 : 0;
+          s_prog.base = s_pos;
         }
       }
       __syncthreads();
       if (s_k >= P.nbuf) break;
-      if (P.bulk_rs && s_vec)
-        reduce_range_bulk<D, OP, MP, TREE>(P.bulk_rs, P.bulk_stage, s_seqk, p, m, excess, s_i, s_pe, P.average, s_bo, 0, s_rd, 0, tid);
-      else
+      if (P.bulk_rs && s_vec) {
+        reduce_range_bulk<D, OP, MP, TREE>(P.bulk_rs, P.bulk_stage, s_seqk, p, m, excess, s_i, s_pe, P.average,
+                                           s_bo, 0, s_rd, 0, tid, ovl ? &s_prog : nullptr);
+      } else {
         reduce_range<D, OP, MP, TREE>(s_seqk, p, m, excess, s_i, s_pe, s_vec != 0, P.average, s_bo, 0, s_rd, 0,
                                       tid, blockDim.x);
+        if (ovl) {
+          __syncthreads();
+          if (tid == 0) prog_publish(&s_prog, s_pos + (s_pe - s_i));
+        }
+      }
       __syncthreads();
-      if (tid == 0) s_i = s_pe;
+      if (tid == 0) {
+        s_pos += s_pe - s_i;
+        s_i = s_pe;
+      }
     }
     CM_TRACE(P, lr, b, 3);
+    if (ovl) goto finish;
     if (tid < p) st_release_sys(mid_slot(P.heap[tid], b, rank), e);
     if (P.dyn_ag) {
       dynamic_allgather<D, MP>(P, rank, nb, e, myheap, ctrl, s_src, s_red, out, true, s_cr, s_vr, &s_ncr, &s_err);

@@ -22,6 +22,12 @@
 
 namespace cm {
 namespace dev {
+// the served area follows the staged gradients, rounded up to 16 bytes so that
+// it shares the 16-byte alignment of the parameter buffers (element offsets
+// are equal): the pull phase's vector copies then apply to every piece
+__host__ __device__ constexpr long long served_off(long long gtot, long long sz) {
+  return (gtot * sz + 15) / 16 * 16;
+}
 
 struct PsParams {
   char* heap[MAXP];
@@ -109,7 +115,7 @@ __global__ void __launch_bounds__(THREADS, 1) ps_kernel(const __grid_constant__ 
                                     ps_entry(P.table, p, P.table[rank + 1] - 1)[2]
                               : 0;
     const long long lo = slice_bound(0, own, b, nb), hi = slice_bound(0, own, b + 1, nb);
-    S* served = reinterpret_cast<S*>(myheap + stage_off + P.gtot * SZ);
+    S* served = reinterpret_cast<S*>(myheap + stage_off + served_off(P.gtot, SZ));
     const double wcount = (double)P.nworkers;
     ps_pieces(P.table, p, rank, lo, hi, [&](long long g0, long long cnt) {
       // PS_U independent elements per thread (strided by THREADS so every
@@ -166,7 +172,7 @@ __global__ void __launch_bounds__(THREADS, 1) ps_kernel(const __grid_constant__ 
       if (s_err) break;
       const long long own = ps_entry(P.table, p, P.table[q + 1] - 1)[0] + ps_entry(P.table, p, P.table[q + 1] - 1)[2];
       const long long lo = slice_bound(0, own, b, nb), hi = slice_bound(0, own, b + 1, nb);
-      const S* src = reinterpret_cast<const S*>(P.heap[q] + stage_off + P.gtot * SZ);
+      const S* src = reinterpret_cast<const S*>(P.heap[q] + stage_off + served_off(P.gtot, SZ));
       ps_pieces(P.table, p, q, lo, hi, [&](long long g0, long long cnt) {
         // served area and parameters share the element offset, so they share
         // 16-byte alignment: scalar head, uint4 body, scalar tail

@@ -93,19 +93,23 @@ def test_model_golden_through_fused_path(case, registered):
 
 @pytest.mark.parametrize("p", [2, 3, 4, 8])
 @pytest.mark.parametrize("mode", ["prestaged", "registered"])
-def test_multi_buffer_launches_vs_oracle(p, mode):
+@pytest.mark.parametrize("overlap", [1, 2])
+def test_multi_buffer_launches_vs_oracle(p, mode, overlap):
     """8 MiB fusion threshold: the ResNet-like set splits into 13 fused groups,
-    batched MAXBUF=4 per multi-buffer launch (nbuf > 1)."""
+    batched MAXBUF=4 per multi-buffer launch (nbuf > 1); with the overlapped
+    two-shot (allgather CTAs follow the reduce-scatter CTAs' per-chunk
+    progress) and with the RS->AG barrier."""
     layers = I.MODELS["resnet50_like"][:24] + [77, 1_000_003, 5]
     per_rank = [I.synth_gradients(3, 1, layers, r) for r in range(p)]
     for algo in ("auto", "ring_rsa", "rhd_rsa"):
         want, groups, _ = OA.aggregate(per_rank, "float32", algo, 8 << 20)
         assert len(groups) > 4
         sets = sets_of(per_rank)
+        g = vg(p, overlap=overlap)
         if mode == "registered":
-            P.register_gradients_group(sets, vg(p))
+            P.register_gradients_group(sets, g)
         stats = []
-        outs = P.aggregate_group(sets, vg(p), algo=algo, cfg=P.FusionConfig(8 << 20), stats_out=stats)
+        outs = P.aggregate_group(sets, g, algo=algo, cfg=P.FusionConfig(8 << 20), stats_out=stats)
         check(outs, want, sorted(nm for nm, _ in per_rank[0]))
         for r in range(p):
             assert len(stats[r]) == len(groups)

@@ -61,19 +61,23 @@ def test_nvlink_ps_step_virtual_bit_exact(c):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("p", [2, 5, 8])
-def test_nvlink_ps_step_virtual_large_vs_oracle(p):
+@pytest.mark.parametrize("dtype", ["float32", "float64"])
+def test_nvlink_ps_step_virtual_large_vs_oracle(p, dtype):
+    """Large tensors reach the owner phase's unrolled loop (>= 4 x 512
+    elements per CTA piece, for float64 too) and, with a schema whose total is
+    not a multiple of 4 elements, a served area that starts 16-byte aligned."""
     import torch
     import paper_1810_11112_b200 as P
     rng = np.random.default_rng([p, 7])
     sizes = [300_001, 17, 1 << 20, 4096, 99_999, 2]
     names = [f"layer{i:03d}" for i in range(len(sizes))]
-    params = {nm: rng.standard_normal(n).astype(np.float32) for nm, n in zip(names, sizes)}
-    grads = [{nm: rng.standard_normal(n).astype(np.float32) for nm, n in zip(names, sizes)} for _ in range(p)]
+    params = {nm: rng.standard_normal(n).astype(dtype) for nm, n in zip(names, sizes)}
+    grads = [{nm: rng.standard_normal(n).astype(dtype) for nm, n in zip(names, sizes)} for _ in range(p)]
     want = OPS.ps_step(grads, params, list(range(p)), 0.1)
     vg = P.VirtualGroup(p, 0, staging_bytes=32 << 20, timeout_s=5.0)
     topo = P.PsTopology.create(range(p), range(p), names)
-    pt = [P.Tensor(nm, "float32", torch.from_numpy(params[nm]).cuda()) for nm in names]
-    gper = [[P.Tensor(nm, "float32", torch.from_numpy(grads[r][nm]).cuda()) for nm in names] for r in range(p)]
+    pt = [P.Tensor(nm, dtype, torch.from_numpy(params[nm]).cuda()) for nm in names]
+    gper = [[P.Tensor(nm, dtype, torch.from_numpy(grads[r][nm]).cuda()) for nm in names] for r in range(p)]
     res = P.run_ps_step_group(vg, topo, gper, [pt] * p, 0.1)
     for r in range(p):
         assert all(t.to_bytes() == want[t.name].tobytes() for t in res[r])

@@ -27,7 +27,7 @@ ap.add_argument("--param", action="append", default=[])
 ap.add_argument("--agg", action="store_true", help="trace the C5 aggregate step (registered gradients)")
 a = ap.parse_args()
 rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
-local = int(os.environ.get("LOCAL_RANK", rank))
+local = int(os.environ.get("LOCAL_RANK", rank)) % torch.cuda.device_count()
 torch.cuda.set_device(local)
 dist.init_process_group("gloo")
 comm = P.Communicator(staging_bytes=max(256 << 20 if a.agg else 64 << 20, a.bytes * 2), pool_bytes=max(64 << 20, a.bytes * 2),
@@ -64,8 +64,12 @@ for it in range(a.iters + 3):
         tr.zero_()
         agg_out[0] = P.aggregate(gs, P.GroupSpec(world), comm, out=agg_out[0])
     else:
-        L.check(L.lib.cm_allreduce(comm._h, x.data_ptr(), y.data_ptr(), n, 0, 0, L.ALGO[a.algo], 131072, 0,
-                                   torch.cuda.current_stream().cuda_stream, C.byref(st)))
+        # back-to-back pair as well: the second call is traced
+        for rep in range(2):
+            if rep:
+                tr.zero_()
+            L.check(L.lib.cm_allreduce(comm._h, x.data_ptr(), y.data_ptr(), n, 0, 0, L.ALGO[a.algo], 131072, 0,
+                                       torch.cuda.current_stream().cuda_stream, C.byref(st)))
     comm.synchronize()
     t = tr.view(ctas, 8).cpu()
     used = t[:, 0] > 0
