@@ -50,12 +50,20 @@ def stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, extra=(), ptxas_log: str | None = None) -> str:
+LIB_CHECKED = os.path.join(HERE, "libcm_checked.so")
+
+
+def build(verbose: bool = False, extra=(), ptxas_log: str | None = None, checked: bool = False) -> str:
     """Compile every translation unit in parallel (the per-dtype kernel
     tables dominate), then link libcm.so. ``ptxas_log``: also write the
-    `-Xptxas -v` register/spill report of every kernel to this file."""
+    `-Xptxas -v` register/spill report of every kernel to this file.
+    ``checked``: the device-side bounds-checked variant (-DCM_CHECKED) as
+    libcm_checked.so (load it with CM_LIB=...), for test runs only."""
     from concurrent.futures import ThreadPoolExecutor
-    objdir = os.path.join(HERE, "build")
+    objdir = os.path.join(HERE, "build_checked" if checked else "build")
+    lib = LIB_CHECKED if checked else LIB
+    if checked:
+        extra = (*extra, "-DCM_CHECKED")
     os.makedirs(objdir, exist_ok=True)
     inc = ["-I", os.path.join(ROOT, "include"), "-I", os.path.join(HERE, "csrc")]
     cflags = [f for f in FLAGS if f != "-shared"]
@@ -82,17 +90,19 @@ def build(verbose: bool = False, extra=(), ptxas_log: str | None = None) -> str:
         with open(ptxas_log, "w") as fh:
             for (_, name, _), (_, log) in zip(todo, res):
                 fh.write(f"==== {name}\n{log}")
-    cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", LIB + ".tmp"]
+    cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", lib + ".tmp"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(lib + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":
     args = sys.argv[1:]
     log = None
+    checked = "--checked" in args
+    args = [a for a in args if a != "--checked"]
     if args and args[0].startswith("--ptxas-log="):
         log = args.pop(0).split("=", 1)[1]
-    print(build(verbose=True, extra=args, ptxas_log=log))
+    print(build(verbose=True, extra=args, ptxas_log=log, checked=checked))

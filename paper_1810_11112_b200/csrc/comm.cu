@@ -236,6 +236,8 @@ int check_async_error(cm_comm* c) {
   if (code == ERR_SHAPE)
     return fail(CM_ERR_SHAPE,
                 "collective shape error: peers disagree on element count, dtype, op or algorithm");
+  if (code == ERR_CHECK)
+    return fail(CM_ERR_CUDA, "device-side bounds check failed (checked build; see the kernel's printf)");
   return fail(CM_ERR_TRANSPORT, "peer did not arrive within the timeout (rank failed or "
                                 "called a different collective)");
 }
@@ -356,6 +358,7 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
   P.timeout_cycles = c->timeout_cycles;
   P.staging_bytes = (long long)c->staging_bytes;
   P.herr = c->herr_dev;
+  P.heap_bytes = (long long)c->heap_bytes;
   P.p = p;
   P.rank = c->rank;
   P.virt = c->virt ? 1 : 0;

@@ -30,6 +30,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 
 #include "cm.h"
 
@@ -118,7 +119,31 @@ enum SrcMode { SRC_COPYIN = 0, SRC_PRESTAGED = 1, SRC_ZEROCOPY = 2, SRC_INLINE =
                SRC_GATHER = 5 };
 enum Order { ORD_SEQ = 0, ORD_RING = 1, ORD_TREE = 2 };
 enum Phase { PH_RS = 1, PH_AG = 2 };
-enum Err { ERR_SHAPE = 1, ERR_TRANSPORT = 4 };
+enum Err { ERR_SHAPE = 1, ERR_TRANSPORT = 4, ERR_CHECK = 8 };
+
+// Checked build (-DCM_CHECKED, python paper_1810_11112_b200/_build.py --checked
+// -> libcm_checked.so, loaded with CM_LIB=...): device-side bounds checks on
+// every computed range, staging offset, peer address and pipeline index —
+// the substitute for compute-sanitizer, which this pool does not run. A failed
+// check prints its location, raises CM_ERR_CHECK in the host-mapped error
+// word and traps the kernel (the host sees a launch failure).
+#ifdef CM_CHECKED
+static __device__ __noinline__ void cm_check_fail(const char* what, int line, unsigned* herr) {
+  printf("libcm checked build: '%s' failed at line %d (block %d,%d thread %d)\n", what, line, blockIdx.x,
+         blockIdx.y, threadIdx.x);
+  if (herr) *reinterpret_cast<volatile unsigned*>(herr) = ERR_CHECK;
+  __threadfence_system();
+  __trap();
+}
+#define CM_CHECK(cond, herr)                                  \
+  do {                                                        \
+    if (!(cond)) cm_check_fail(#cond, __LINE__, (herr));      \
+  } while (0)
+#else
+#define CM_CHECK(cond, herr) \
+  do {                       \
+  } while (0)
+#endif
 
 struct CollParams {
   char* heap[MAXP];          // every rank's heap, mapped in this process
@@ -132,6 +157,7 @@ struct CollParams {
   unsigned long long timeout_cycles;
   long long staging_bytes;   // per parity half
   unsigned int* herr;        // host-mapped error word
+  long long heap_bytes;      // size of every rank's heap (checked build)
   int p;
   int rank;                  // real mode
   int virt;                  // 1: blockIdx.y is the rank (single-GPU emulation)
@@ -304,15 +330,25 @@ __device__ __forceinline__ unsigned long long* mid_slot(char* heap, int blk, int
 }
 
 // a peer's published source offset -> its address in this process
-__device__ __forceinline__ const char* resolve_src(char* const* heap, char* myheap, int src, long long so) {
-  if (!((unsigned long long)so & REG_FLAG)) return heap[src] + so;
+__device__ __forceinline__ const char* resolve_src(char* const* heap, char* myheap, int src, long long so,
+                                                   long long heap_bytes = 0, unsigned* herr = nullptr) {
+  if (!((unsigned long long)so & REG_FLAG)) {
+    CM_CHECK(so >= 0 && so < heap_bytes, herr);
+    return heap[src] + so;
+  }
   const long long delta = so & ((1ll << 40) - 1);
   if ((unsigned long long)so & AUTO_FLAG) {       // the sender's auto-registered allocation
     const long long slot = (so >> 40) & 0x1FFFFF;
-    return *reinterpret_cast<char* const*>(myheap + AUTOTAB_OFF + ((size_t)slot * MAXP + src) * 8) + delta;
+    CM_CHECK(slot < MAXAUTO, herr);
+    const char* base = *reinterpret_cast<char* const*>(myheap + AUTOTAB_OFF + ((size_t)slot * MAXP + src) * 8);
+    CM_CHECK(base != nullptr, herr);
+    return base + delta;
   }
   const long long id = (so >> 40) & 0x1FFFFF;     // collective registration id
-  return *reinterpret_cast<char* const*>(myheap + REG_OFF + ((size_t)id * MAXP + src) * 8) + delta;
+  CM_CHECK(id < MAXREG, herr);
+  const char* base = *reinterpret_cast<char* const*>(myheap + REG_OFF + ((size_t)id * MAXP + src) * 8);
+  CM_CHECK(base != nullptr, herr);
+  return base + delta;
 }
 
 // CTA 0 only, after the start barrier: report peers' newer allocation slots
@@ -611,6 +647,7 @@ __device__ void multi_copy(const CopyRange* R, int nr, VecRange* V) {
   // scalar heads/tails (and misaligned ranges): one warp per range
   for (int r = warp; r < nr; r += nwarps) {
     const CopyRange c = R[r];
+    CM_CHECK(c.lo <= c.hi && c.src != nullptr && c.dst != nullptr, nullptr);
     const S* s = reinterpret_cast<const S*>(c.src) - c.sshift;
     S* d = reinterpret_cast<S*>(c.dst) - c.dshift;
     long long blo = c.hi, bhi = c.hi;
@@ -769,6 +806,8 @@ __device__ void reduce_range_bulk(int stages, int stage_bytes, const char* const
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&B.full[s])),
                    "r"(len * p)
                    : "memory");
+      CM_CHECK(s < B.stages && (size_t)p * ch <= (size_t)B.stage_bytes && len > 0 && len <= ch && (len & 15) == 0,
+               nullptr);
       for (int k = 0; k < p; ++k) {
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(

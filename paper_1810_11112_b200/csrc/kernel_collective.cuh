@@ -210,6 +210,8 @@ __global__ void __launch_bounds__(THREADS, 1) collective_kernel(const __grid_con
   const bool ag_only = !(P.phases & PH_RS);
   const bool two_shot = !P.oneshot;
 
+  CM_CHECK(stage_off + P.staging_bytes <= P.heap_bytes, P.herr);
+  CM_CHECK(MULTI || P.srcmode == SRC_ZEROCOPY || P.srcmode == SRC_REGISTERED || P.n * SZ <= P.staging_bytes, P.herr);
   // my own src/red offsets (published to peers)
   long long my_srcoff, my_redoff;
   const long long mso = P.seg_off[rank];
@@ -279,8 +281,9 @@ __global__ void __launch_bounds__(THREADS, 1) collective_kernel(const __grid_con
         atomicExch(&s_skip, 2);            // ready sets differ: nobody moves data
       if (ld_relaxed_sys(&r->hdr) != P.hdr) atomicExch(&s_err, ERR_SHAPE);
       // peer's staging / symmetric pool, or its registered buffer mapped here
-      s_src[tid] = resolve_src(P.heap, myheap, tid, ld_relaxed_sys_s64(&r->srcoff));
-      s_red[tid] = const_cast<char*>(resolve_src(P.heap, myheap, tid, ld_relaxed_sys_s64(&r->redoff)));
+      s_src[tid] = resolve_src(P.heap, myheap, tid, ld_relaxed_sys_s64(&r->srcoff), P.heap_bytes, P.herr);
+      s_red[tid] = const_cast<char*>(
+          resolve_src(P.heap, myheap, tid, ld_relaxed_sys_s64(&r->redoff), P.heap_bytes, P.herr));
       if (b == 0) autoreg_report(P, myheap, rank, tid, ld_relaxed_sys_s64(&r->regseq));
     }
   }
@@ -392,9 +395,11 @@ __global__ void __launch_bounds__(THREADS, 1) collective_kernel(const __grid_con
               const long long so = P.bseg_off[k][q], sl = P.bseg_len[k][q];
               const long long lo = slice_bound(so, sl, j, nrs), hi = slice_bound(so, sl, j + 1, nrs);
               const long long a = pos > base ? pos : base, z = end < base + hi - lo ? end : base + hi - lo;
-              if (z > a)
+              if (z > a) {
+                CM_CHECK(lo + (z - base) <= hi && (P.bboff[k] + hi) * SZ <= P.staging_bytes, P.herr);
                 s_cr[r++] = CopyRange{P.heap[q] + stage_off + P.bboff[k] * SZ, out + P.bout_off[k] * SZ, 0, 0,
                                       lo + (a - base), lo + (z - base)};
+              }
               base += hi - lo;
             }
           }
@@ -464,6 +469,9 @@ __global__ void __launch_bounds__(THREADS, 1) collective_kernel(const __grid_con
       }
       __syncthreads();
       if (s_k >= P.nbuf) break;
+      CM_CHECK(s_i <= s_pe && s_pe <= s_hi && s_hi <= P.bseg_off[s_k][rank] + P.bseg_len[s_k][rank] &&
+                   (P.bboff[s_k] + s_pe) * SZ <= P.staging_bytes && s_pe <= P.bn[s_k],
+               P.herr);
       if (P.bulk_rs && s_vec) {
         reduce_range_bulk<D, OP, MP, TREE>(P.bulk_rs, P.bulk_stage, s_seqk, p, m, excess, s_i, s_pe, P.average,
                                            s_bo, 0, s_rd, 0, tid, ovl ? &s_prog : nullptr);

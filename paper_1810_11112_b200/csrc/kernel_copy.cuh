@@ -90,6 +90,7 @@ static __global__ void __launch_bounds__(THREADS) batched_copy_kernel(const __gr
     const long long a = lo > P.start[k] ? lo : P.start[k];
     const long long z = hi < P.start[k + 1] ? hi : P.start[k + 1];
     const char* s = P.src[k] + (a - P.start[k]);
+    CM_CHECK(!P.staged || (long long)(uintptr_t)P.dst[k] + (P.start[k + 1] - P.start[k]) <= P.staging_bytes, nullptr);
     char* d = (P.staged ? base + (long long)(uintptr_t)P.dst[k] : P.dst[k]) + (a - P.start[k]);
     const long long nbytes = z - a;
     if ((((uintptr_t)s | (uintptr_t)d) & 15u) == 0) {

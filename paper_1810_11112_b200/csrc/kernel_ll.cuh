@@ -83,6 +83,7 @@ __global__ void __launch_bounds__(THREADS, 1) ll_kernel(const __grid_constant__ 
   const long long nbytes = P.n * (long long)sizeof(S);
   const long long nunits = (nbytes + 7) / 8;
   const long long u0 = nunits * b / nb, u1 = nunits * (b + 1) / nb;
+  CM_CHECK(nunits <= P.ll_units, P.herr);
   // prestaged input (fused pack) lives in staging[parity]
   CM_TRACE(P, lr, b, 0);
   const char* in = P.srcmode == SRC_PRESTAGED
@@ -261,6 +262,7 @@ __global__ void __launch_bounds__(THREADS, 1) ll2_kernel(const __grid_constant__
     const long long so = P.seg_off[q], sl = P.seg_len[q];
     const long long nu = (sl + E - 1) / E;
     const long long u0 = nu * b / nb, u1 = nu * (b + 1) / nb;
+    CM_CHECK(nu <= P.ll_units, P.herr);
     char* dst = P.heap[q];
     for (long long u = u0 + tid; u < u1; u += bd) {
       const long long el = u * E;
