@@ -704,7 +704,7 @@ def sweep(args, rank, world, local):
                 row[f"{algo}_graph_us"] = max_over_ranks(
                     _time_calls(ours(n, algo, True), iters, 3, graph=True) * 1e3, world)
         comm.synchronize()
-        if world > 1:
+        if world > 1 and not args.no_nccl:
             t = plain[:n]
             barrier(world)
             row["nccl_us"] = max_over_ranks(_time_calls(lambda: dist.all_reduce(t), iters, 5) * 1e3, world)

@@ -128,9 +128,10 @@ enum Err { ERR_SHAPE = 1, ERR_TRANSPORT = 4, ERR_CHECK = 8 };
 // check prints its location, raises CM_ERR_CHECK in the host-mapped error
 // word and traps the kernel (the host sees a launch failure).
 #ifdef CM_CHECKED
-static __device__ __noinline__ void cm_check_fail(const char* what, int line, unsigned* herr) {
-  printf("libcm checked build: '%s' failed at line %d (block %d,%d thread %d)\n", what, line, blockIdx.x,
-         blockIdx.y, threadIdx.x);
+static __device__ __noinline__ void cm_check_fail(const char* what, int line, unsigned* herr, long long v0 = 0,
+                                                  long long v1 = 0) {
+  printf("libcm checked build: '%s' failed at line %d (block %d,%d thread %d; values %lld %lld)\n", what, line,
+         blockIdx.x, blockIdx.y, threadIdx.x, v0, v1);
   if (herr) *reinterpret_cast<volatile unsigned*>(herr) = ERR_CHECK;
   __threadfence_system();
   __trap();
@@ -139,9 +140,16 @@ static __device__ __noinline__ void cm_check_fail(const char* what, int line, un
   do {                                                        \
     if (!(cond)) cm_check_fail(#cond, __LINE__, (herr));      \
   } while (0)
+#define CM_CHECKV(cond, herr, v0, v1)                                                   \
+  do {                                                                                  \
+    if (!(cond)) cm_check_fail(#cond, __LINE__, (herr), (long long)(v0), (long long)(v1)); \
+  } while (0)
 #else
 #define CM_CHECK(cond, herr) \
   do {                       \
+  } while (0)
+#define CM_CHECKV(cond, herr, v0, v1) \
+  do {                                \
   } while (0)
 #endif
 
@@ -647,7 +655,9 @@ __device__ void multi_copy(const CopyRange* R, int nr, VecRange* V) {
   // scalar heads/tails (and misaligned ranges): one warp per range
   for (int r = warp; r < nr; r += nwarps) {
     const CopyRange c = R[r];
-    CM_CHECK(c.lo <= c.hi && c.src != nullptr && c.dst != nullptr, nullptr);
+    CM_CHECKV(c.lo <= c.hi, nullptr, c.lo, c.hi);
+    CM_CHECKV(c.lo == c.hi || (c.src != nullptr && c.dst != nullptr), nullptr, (long long)(uintptr_t)c.src,
+              (long long)(uintptr_t)c.dst);
     const S* s = reinterpret_cast<const S*>(c.src) - c.sshift;
     S* d = reinterpret_cast<S*>(c.dst) - c.dshift;
     long long blo = c.hi, bhi = c.hi;
