@@ -347,7 +347,10 @@ int cm_local_reduce(const void* a, const void* b, void* out, int64_t count, int 
 int cm_batched_copy(int n, const void* const* srcs, void* const* dsts, const int64_t* nbytes,
                     void* stream);
 /* diagnostics: all-to-all NVLink bandwidth, mode 0 = every rank pulls `bytes`
- * from each peer, 1 = every rank pushes `bytes` to each peer; ms per round */
+ * from each peer, 1 = every rank pushes `bytes` to each peer; ms per round.
+ * Flag latency: mode 10 = ping-pong between ranks 0 and 1 (one thread),
+ * mode 11 = the start-barrier pattern on `ctas` CTAs; `bytes` = iterations
+ * per launch, ms_per_iter = time per launch (divide by the iterations) */
 int cm_bench_p2p(cm_comm_t* comm, int mode, int64_t bytes, int ctas, int iters, void* stream,
                  double* ms_per_iter);
 /* device-timed loop of cm_allreduce (CUDA events on `stream`), ms per call */

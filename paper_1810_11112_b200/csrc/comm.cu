@@ -2086,7 +2086,8 @@ int cm_batched_copy(int n, const void* const* srcs, void* const* dsts, const int
 int cm_bench_p2p(cm_comm_t* c, int mode, int64_t bytes, int ctas, int iters, void* stream_,
                  double* ms_per_iter) {
   if (c->virt || c->size < 2) return fail(CM_ERR_UNSUPPORTED, "needs a real group of >= 2 ranks");
-  const int64_t need = (int64_t)bytes * ((mode >= 6 && mode <= 9) ? 6 : c->size);
+  // modes 10/11 (flag latency): `bytes` is the number of iterations per launch
+  const int64_t need = (mode >= 10) ? 0 : (int64_t)bytes * ((mode >= 6 && mode <= 9) ? 6 : c->size);
   if (need > (int64_t)c->staging_bytes) return fail(CM_ERR_CONFIG, "bytes too large");
   cudaStream_t s = static_cast<cudaStream_t>(stream_);
   CollParams P;
@@ -2114,9 +2115,13 @@ int cm_bench_p2p(cm_comm_t* c, int mode, int64_t bytes, int ctas, int iters, voi
     }
     B.n = m;
   }
+  static unsigned long long flag_base = 1ull << 40;   // slot values only grow (same sequence on every rank)
   auto launch = [&]() {
     if (mode == 4) bulk_copy_kernel<<<ctas, BULK_THREADS, BULK_SMEM, s>>>(B);
-    else p2p_bw_kernel<<<ctas, THREADS, 0, s>>>(P, mode, bytes);
+    else if (mode >= 10 && mode <= 13) {
+      flag_latency_kernel<<<mode == 10 ? 1 : ctas, THREADS, 0, s>>>(P, mode, bytes, flag_base);
+      flag_base += (unsigned long long)bytes + 1;
+    } else p2p_bw_kernel<<<ctas, THREADS, 0, s>>>(P, mode, bytes);
   };
   launch();
   CUDA_TRY(cudaEventRecord(e0, s));

@@ -46,7 +46,7 @@ constexpr int MAXBUF = 4;        // fused buffers per multi-buffer launch
 // ---- heap layout (identical on every rank) ---------------------------------
 constexpr size_t CTRL_OFF = 0;
 constexpr size_t REC_OFF = 4096;
-constexpr size_t REC_BYTES = 64;
+constexpr size_t REC_BYTES = 128;             // REC_UNITS LL units (see rec_put)
 constexpr size_t REC_SIZE = 2ull * MAXBLK * MAXP * REC_BYTES;
 constexpr size_t MID_OFF = REC_OFF + REC_SIZE;
 constexpr size_t MID_SIZE = (size_t)MAXBLK * MAXP * 8;
@@ -104,15 +104,16 @@ struct Ctrl {
   unsigned long long ag_next;    // next allgather task of the current call (dynamic allgather)
 };
 
-struct Rec {
-  unsigned long long epoch;
-  unsigned long long hdr;
-  long long srcoff;  // element i of the sender's input at heap + srcoff + i*sz
-  long long redoff;  // element i of the sender's segment at heap + redoff + (i-seg_off)*sz
-  long long akey;    // inline agreement (aggregate's ready-set hash and count)
-  long long acnt;
-  long long regseq;  // allocation slots the sender has published in its mailbox
-  long long pad;
+// The start-barrier record a rank publishes to every peer (one per CTA and
+// epoch parity), as REC_UNITS LL units (rec_put / rec_get)
+enum RecField {
+  RF_HDR = 0,     // call signature
+  RF_SRCOFF = 1,  // element i of the sender's input at heap + srcoff + i*sz (or a REG_FLAG encoding)
+  RF_REDOFF = 2,  // element i of the sender's segment at heap + redoff + (i-seg_off)*sz
+  RF_AKEY = 3,    // inline agreement (aggregate's ready-set hash and count)
+  RF_ACNT = 4,
+  RF_REGSEQ = 5,  // allocation slots the sender has published in its mailbox
+  REC_UNITS = 6
 };
 
 enum SrcMode { SRC_COPYIN = 0, SRC_PRESTAGED = 1, SRC_ZEROCOPY = 2, SRC_INLINE = 3, SRC_REGISTERED = 4,
@@ -329,9 +330,86 @@ __device__ __forceinline__ long long ld_relaxed_sys_s64(const long long* p) {
   return v;
 }
 
-__device__ __forceinline__ Rec* rec_slot(char* heap, int par, int blk, int src) {
-  return reinterpret_cast<Rec*>(heap + REC_OFF +
-                                ((size_t)(par * MAXBLK + blk) * MAXP + src) * REC_BYTES);
+__device__ __forceinline__ char* rec_slot(char* heap, int par, int blk, int src) {
+  return heap + REC_OFF + ((size_t)(par * MAXBLK + blk) * MAXP + src) * REC_BYTES;
+}
+
+// ---- LL units: data and "ready" in one 16-byte store -----------------------------
+// {w0, flag, w1, flag}: a reader that sees both flags equal to the expected tag
+// sees the 8 payload bytes (NVLink delivers each 8-byte half whole), so no
+// release/acquire fence is needed — a sys-scope release costs ~3.5 us per
+// barrier on B200 (tools/flag_latency.py), a relaxed flag ~1.5 us.
+__device__ __forceinline__ void st_ll(void* p, unsigned w0, unsigned w1, unsigned f) {
+  asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(w0), "r"(f), "r"(w1),
+               "r"(f)
+               : "memory");
+}
+__device__ __forceinline__ uint4 ld_ll(const void* p) {
+  uint4 v;
+  asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p)
+               : "memory");
+  return v;
+}
+// poll one LL unit until both flags match; false on timeout
+__device__ __forceinline__ bool ll_wait(const char* slot, unsigned f, unsigned long long timeout,
+                                        uint4* out) {
+  uint4 v = ld_ll(slot);
+  if (v.y == f && v.w == f) { *out = v; return true; }
+  const long long t0 = clock64();
+  while (true) {
+    for (int i = 0; i < 32; ++i) {
+      v = ld_ll(slot);
+      if (v.y == f && v.w == f) { *out = v; return true; }
+    }
+    if ((unsigned long long)(clock64() - t0) > timeout) return false;
+  }
+}
+
+
+// the epoch's LL tag (never 0, so zeroed memory never matches)
+__device__ __forceinline__ unsigned ll_tag(unsigned long long e) {
+  return (unsigned)(e & 0x7fffffffu) | 0x80000000u;
+}
+
+__device__ __forceinline__ void rec_put(char* slot, unsigned tag, const long long (&v)[REC_UNITS], int nunits) {
+  for (int u = 0; u < nunits; ++u)
+    st_ll(slot + u * 16, (unsigned)(unsigned long long)v[u], (unsigned)((unsigned long long)v[u] >> 32), tag);
+}
+
+__device__ __forceinline__ bool rec_get(const char* slot, unsigned tag, long long (&v)[REC_UNITS], int nunits,
+                                        unsigned long long timeout) {
+  for (int u = 0; u < nunits; ++u) {
+    uint4 x;
+    if (!ll_wait(slot + u * 16, tag, timeout, &x)) return false;
+    v[u] = (long long)(((unsigned long long)x.z << 32) | x.x);
+  }
+  return true;
+}
+
+// Flags ordered by a gpu-scope fence instead of a sys-scope release/acquire:
+// the writer's data is performed at its own L2 — where peers' NVLink loads are
+// served — before the flag store leaves; the reader fences after seeing the
+// flag, and reads peer data with L1-bypassing loads (ld.cg / TMA).
+__device__ __forceinline__ void flag_put(unsigned long long* f, unsigned long long v) {
+  __threadfence();
+  st_relaxed_sys(f, v);
+}
+__device__ __forceinline__ bool flag_wait(const unsigned long long* f, unsigned long long e,
+                                          unsigned long long timeout) {
+  bool ok = true;
+  if (ld_relaxed_sys(f) < e) {
+    const long long t0 = clock64();
+    while (ld_relaxed_sys(f) < e) {
+      if ((unsigned long long)(clock64() - t0) > timeout) {
+        ok = false;
+        break;
+      }
+    }
+  }
+  __threadfence();
+  return ok;
 }
 __device__ __forceinline__ unsigned long long* mid_slot(char* heap, int blk, int src) {
   return reinterpret_cast<unsigned long long*>(heap + MID_OFF + ((size_t)blk * MAXP + src) * 8);
@@ -648,6 +726,19 @@ constexpr int CP_CHUNK = 32 * CP_U;           // vectors per warp chunk (4 KiB)
 // R[0..nr) in shared memory; V is shared scratch of the same size.
 template <class D, int MP>
 __device__ void multi_copy(const CopyRange* R, int nr, VecRange* V) {
+  auto ld_cg = [](const typename D::S* a) -> typename D::S {
+    using S = typename D::S;
+    if constexpr (sizeof(S) == 8) {
+      const unsigned long long v = __ldcg(reinterpret_cast<const unsigned long long*>(a));
+      return *reinterpret_cast<const S*>(&v);
+    } else if constexpr (sizeof(S) == 4) {
+      const unsigned v = __ldcg(reinterpret_cast<const unsigned*>(a));
+      return *reinterpret_cast<const S*>(&v);
+    } else {
+      const unsigned short v = __ldcg(reinterpret_cast<const unsigned short*>(a));
+      return *reinterpret_cast<const S*>(&v);
+    }
+  };
   using S = typename D::S;
   constexpr int W = 16 / sizeof(S);
   const int tid = threadIdx.x, bd = blockDim.x;
@@ -666,8 +757,8 @@ __device__ void multi_copy(const CopyRange* R, int nr, VecRange* V) {
       bhi = (c.hi / W) * W;
       if (bhi < blo) blo = bhi = c.hi;
     }
-    for (long long i = c.lo + lane; i < blo; i += 32) d[i] = s[i];
-    for (long long i = bhi + lane; i < c.hi; i += 32) d[i] = s[i];
+    for (long long i = c.lo + lane; i < blo; i += 32) d[i] = ld_cg(s + i);
+    for (long long i = bhi + lane; i < c.hi; i += 32) d[i] = ld_cg(s + i);
     if (lane == 0) {
       V[r].src = reinterpret_cast<const uint4*>(s + blo);
       V[r].dst = reinterpret_cast<uint4*>(d + blo);
@@ -691,7 +782,7 @@ __device__ void multi_copy(const CopyRange* R, int nr, VecRange* V) {
     uint4 v[CP_U];
 #pragma unroll
     for (int u = 0; u < CP_U; ++u)
-      if (lane + 32 * u < m) v[u] = src[lane + 32 * u];
+      if (lane + 32 * u < m) v[u] = __ldcg(src + lane + 32 * u);   // peer data: bypass L1
 #pragma unroll
     for (int u = 0; u < CP_U; ++u)
       if (lane + 32 * u < m) dst[lane + 32 * u] = v[u];
@@ -699,6 +790,10 @@ __device__ void multi_copy(const CopyRange* R, int nr, VecRange* V) {
 }
 
 __device__ __forceinline__ bool al16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+// one element through L2 only (peer data after a flag: no stale L1 line)
+__device__ __forceinline__ float ld_cg_elem(const float* a) { return __ldcg(a); }
+__device__ __forceinline__ double ld_cg_elem(const double* a) { return __ldcg(a); }
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return (unsigned)__cvta_generic_to_shared(p);
@@ -777,8 +872,9 @@ struct Prog {
 };
 
 __device__ __forceinline__ void prog_publish(const Prog* pg, long long pos) {
+  __threadfence();
   for (int q = 0; q < pg->p; ++q)
-    if (pg->dst[q]) st_release_sys(pg->dst[q], pg->tag | (unsigned long long)pos);
+    if (pg->dst[q]) st_relaxed_sys(pg->dst[q], pg->tag | (unsigned long long)pos);
 }
 
 // Same contract as reduce_range (sources 16-byte aligned at vector boundaries).

@@ -258,33 +258,28 @@ __global__ void __launch_bounds__(THREADS, 1) collective_kernel(const __grid_con
   __syncthreads();
   CM_TRACE(P, lr, b, 1);
 
-  // 2. publish my record to every peer, then collect theirs
+  // 2. publish my record to every peer (LL units, no release fence: only the
+  // copy-in above wrote data peers are about to read, and a gpu-scope fence
+  // puts it in my L2 first), then collect theirs
+  const unsigned tag = ll_tag(e);
   if (tid < p && !s_skip) {
-    Rec* r = rec_slot(P.heap[tid], par, b, rank);
-    st_relaxed_sys(&r->hdr, P.hdr);
-    st_relaxed_sys_s64(&r->srcoff, my_srcoff);
-    st_relaxed_sys_s64(&r->redoff, my_redoff);
-    if (P.agree_inline) {
-      st_relaxed_sys_s64(&r->akey, P.akey[lr]);
-      st_relaxed_sys_s64(&r->acnt, P.acnt[lr]);
-    }
-    st_relaxed_sys_s64(&r->regseq, P.reg_seq);
-    st_release_sys(&r->epoch, e);
+    if (P.srcmode == SRC_COPYIN) __threadfence();
+    const long long rv[REC_UNITS] = {(long long)P.hdr, my_srcoff, my_redoff, P.akey[lr], P.acnt[lr], P.reg_seq};
+    rec_put(rec_slot(P.heap[tid], par, b, rank), tag, rv, REC_UNITS);
   }
   if (tid < p && !s_skip) {
-    Rec* r = rec_slot(myheap, par, b, tid);
-    if (!wait_geq(&r->epoch, e, P.timeout_cycles)) {
+    long long rv[REC_UNITS];
+    if (!rec_get(rec_slot(myheap, par, b, tid), tag, rv, REC_UNITS, P.timeout_cycles)) {
       atomicExch(&s_err, ERR_TRANSPORT);
     } else {
-      if (P.agree_inline &&
-          (ld_relaxed_sys_s64(&r->akey) != P.akey[lr] || ld_relaxed_sys_s64(&r->acnt) != P.acnt[lr]))
+      __threadfence();                     // the peer's data is read after its record
+      if (P.agree_inline && (rv[RF_AKEY] != P.akey[lr] || rv[RF_ACNT] != P.acnt[lr]))
         atomicExch(&s_skip, 2);            // ready sets differ: nobody moves data
-      if (ld_relaxed_sys(&r->hdr) != P.hdr) atomicExch(&s_err, ERR_SHAPE);
+      if ((unsigned long long)rv[RF_HDR] != P.hdr) atomicExch(&s_err, ERR_SHAPE);
       // peer's staging / symmetric pool, or its registered buffer mapped here
-      s_src[tid] = resolve_src(P.heap, myheap, tid, ld_relaxed_sys_s64(&r->srcoff), P.heap_bytes, P.herr);
-      s_red[tid] = const_cast<char*>(
-          resolve_src(P.heap, myheap, tid, ld_relaxed_sys_s64(&r->redoff), P.heap_bytes, P.herr));
-      if (b == 0) autoreg_report(P, myheap, rank, tid, ld_relaxed_sys_s64(&r->regseq));
+      s_src[tid] = resolve_src(P.heap, myheap, tid, rv[RF_SRCOFF], P.heap_bytes, P.herr);
+      s_red[tid] = const_cast<char*>(resolve_src(P.heap, myheap, tid, rv[RF_REDOFF], P.heap_bytes, P.herr));
+      if (b == 0) autoreg_report(P, myheap, rank, tid, rv[RF_REGSEQ]);
     }
   }
   __syncthreads();                       // s_src / s_red / s_err complete
@@ -374,14 +369,14 @@ __global__ void __launch_bounds__(THREADS, 1) collective_kernel(const __grid_con
       __syncthreads();
       long long tmax = 0;
       for (int q = 0; q < p; ++q) tmax = s_tot[q] > tmax ? s_tot[q] : tmax;
-      const unsigned long long tag = e << 32;
+      const unsigned long long ptag = e << 32;
 #pragma unroll 1
       for (long long pos = 0; pos < tmax; pos += G) {
         if (tid < p && pos < s_tot[tid]) {
           const long long need = pos + G < s_tot[tid] ? pos + G : s_tot[tid];
           const unsigned long long* f =
               reinterpret_cast<const unsigned long long*>(myheap + PROG_OFF + ((size_t)j * MAXP + tid) * 8);
-          if (!wait_geq(f, tag | (unsigned long long)need, P.timeout_cycles)) atomicExch(&s_err, ERR_TRANSPORT);
+          if (!flag_wait(f, ptag | (unsigned long long)need, P.timeout_cycles)) atomicExch(&s_err, ERR_TRANSPORT);
         }
         __syncthreads();
         if (s_err) break;
@@ -491,12 +486,12 @@ __global__ void __launch_bounds__(THREADS, 1) collective_kernel(const __grid_con
     }
     CM_TRACE(P, lr, b, 3);
     if (ovl) goto finish;
-    if (tid < p) st_release_sys(mid_slot(P.heap[tid], b, rank), e);
+    if (tid < p) flag_put(mid_slot(P.heap[tid], b, rank), e);
     if (P.dyn_ag) {
       dynamic_allgather<D, MP>(P, rank, nb, e, myheap, ctrl, s_src, s_red, out, true, s_cr, s_vr, &s_ncr, &s_err);
       goto finish;
     }
-    if (tid < p && !wait_geq(mid_slot(myheap, b, tid), e, P.timeout_cycles)) atomicExch(&s_err, ERR_TRANSPORT);
+    if (tid < p && !flag_wait(mid_slot(myheap, b, tid), e, P.timeout_cycles)) atomicExch(&s_err, ERR_TRANSPORT);
     __syncthreads();
     CM_TRACE(P, lr, b, 4);
     if (s_err) goto finish;
@@ -550,13 +545,13 @@ __global__ void __launch_bounds__(THREADS, 1) collective_kernel(const __grid_con
   if (P.phases & PH_AG) {
     if (!ag_only) {
       __syncthreads();
-      if (tid < p) st_release_sys(mid_slot(P.heap[tid], b, rank), e);
+      if (tid < p) flag_put(mid_slot(P.heap[tid], b, rank), e);
       if (P.dyn_ag) {
         dynamic_allgather<D, MP>(P, rank, nb, e, myheap, ctrl, s_src, s_red, out, false, s_cr, s_vr, &s_ncr,
                                  &s_err);
         goto finish;
       }
-      if (tid < p && !wait_geq(mid_slot(myheap, b, tid), e, P.timeout_cycles))
+      if (tid < p && !flag_wait(mid_slot(myheap, b, tid), e, P.timeout_cycles))
         atomicExch(&s_err, ERR_TRANSPORT);
       __syncthreads();
       CM_TRACE(P, lr, b, 4);

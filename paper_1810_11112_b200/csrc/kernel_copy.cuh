@@ -58,6 +58,60 @@ static __global__ void __launch_bounds__(THREADS) p2p_bw_kernel(const __grid_con
   }
 }
 
+// ---- diagnostics: flag latency over NVLink ------------------------------------
+// mode 10 (1 CTA): ping-pong between ranks 0 and 1 — iteration i: rank 0
+//   stores i into rank 1's slot and waits for rank 1's answer; time per round trip
+// mode 11 (every CTA): the start-barrier pattern — CTA b stores the iteration
+//   into slot [b][rank] of every peer with st.release.sys, then waits for all
+//   peers' slot [b][q] with ld.acquire.sys; time per barrier
+// Slots live in the MID region (values only grow: base + i, base per call).
+static __global__ void __launch_bounds__(THREADS, 1) flag_latency_kernel(const __grid_constant__ CollParams P,
+                                                                         int mode, long long iters,
+                                                                         unsigned long long base) {
+  const int rank = P.rank, p = P.p, tid = threadIdx.x, b = blockIdx.x;
+  char* mine = P.heap[rank];
+  if (mode == 10) {
+    if (tid != 0 || rank > 1) return;
+    const int peer = 1 - rank;
+    for (long long i = 1; i <= iters; ++i) {
+      const unsigned long long v = base + (unsigned long long)i;
+      if (rank == 0) {
+        st_release_sys(mid_slot(P.heap[peer], 0, rank), v);
+        while (ld_acquire_sys(mid_slot(mine, 0, peer)) < v) {
+        }
+      } else {
+        while (ld_acquire_sys(mid_slot(mine, 0, peer)) < v) {
+        }
+        st_release_sys(mid_slot(P.heap[peer], 0, rank), v);
+      }
+    }
+    return;
+  }
+  for (long long i = 1; i <= iters; ++i) {
+    const unsigned long long v = base + (unsigned long long)i;
+    if (mode == 11) {
+      if (tid < p) st_release_sys(mid_slot(P.heap[tid], b, rank), v);
+      if (tid < p)
+        while (ld_acquire_sys(mid_slot(mine, b, tid)) < v) {
+        }
+    } else if (mode == 12) {   // relaxed stores and polls (no ordering; the raw path)
+      if (tid < p) st_relaxed_sys(mid_slot(P.heap[tid], b, rank), v);
+      if (tid < p)
+        while (ld_relaxed_sys(mid_slot(mine, b, tid)) < v) {
+        }
+    } else {                   // 13: gpu-scope fence, relaxed store, relaxed poll
+      if (tid < p) {
+        __threadfence();
+        st_relaxed_sys(mid_slot(P.heap[tid], b, rank), v);
+      }
+      if (tid < p)
+        while (ld_relaxed_sys(mid_slot(mine, b, tid)) < v) {
+        }
+    }
+    __syncthreads();
+  }
+}
+
 // ---- batched copy (fusion pack / unfuse / cm_batched_copy) ---------------------
 constexpr int MAXCOPY = 128;
 struct CopyParams {

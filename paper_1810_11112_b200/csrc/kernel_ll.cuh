@@ -13,38 +13,10 @@ namespace dev {
 // the p sources in the reference order. No fence, no separate flag round trip:
 // latency = launch + one NVLink store + local polls. Header units carry the
 // call signature so mismatched peers raise ShapeError.
-__device__ __forceinline__ void st_ll(void* p, unsigned w0, unsigned w1, unsigned f) {
-  asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(w0), "r"(f), "r"(w1),
-               "r"(f)
-               : "memory");
-}
-__device__ __forceinline__ uint4 ld_ll(const void* p) {
-  uint4 v;
-  asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-               : "l"(p)
-               : "memory");
-  return v;
-}
 #define LLSLOT(heap, par, phase, src, u) \
   ((heap) + LL_OFF + ((((size_t)(par) * 2 + (phase)) * P.p + (src)) * (size_t)P.ll_units + (size_t)(u)) * 16)
 __device__ __forceinline__ char* llh_slot(char* heap, int par, int blk, int src) {
   return heap + LLH_OFF + (((size_t)par * MAXBLK + blk) * MAXP + src) * 16;
-}
-
-// poll one LL unit until both flags match; false on timeout
-__device__ __forceinline__ bool ll_wait(const char* slot, unsigned f, unsigned long long timeout,
-                                        uint4* out) {
-  uint4 v = ld_ll(slot);
-  if (v.y == f && v.w == f) { *out = v; return true; }
-  const long long t0 = clock64();
-  while (true) {
-    for (int i = 0; i < 32; ++i) {
-      v = ld_ll(slot);
-      if (v.y == f && v.w == f) { *out = v; return true; }
-    }
-    if ((unsigned long long)(clock64() - t0) > timeout) return false;
-  }
 }
 
 template <class D, int OP, int MP, bool TREE>

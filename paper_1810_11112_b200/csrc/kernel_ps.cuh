@@ -26,7 +26,7 @@ namespace dev {
 // it shares the 16-byte alignment of the parameter buffers (element offsets
 // are equal): the pull phase's vector copies then apply to every piece
 __host__ __device__ constexpr long long served_off(long long gtot, long long sz) {
-  return (gtot * sz + 15) / 16 * 16;
+  return (gtot * sz + 127) / 128 * 128;    // own cache lines: no line shared with the staged gradients
 }
 
 struct PsParams {
@@ -95,15 +95,16 @@ __global__ void __launch_bounds__(THREADS, 1) ps_kernel(const __grid_constant__ 
 
   // 1. start barrier: every worker's gradients are staged (pack kernels ran
   // before this launch on each rank's stream)
+  const unsigned tag = ll_tag(e);
   if (tid < p) {
-    Rec* r = rec_slot(P.heap[tid], par, b, rank);
-    st_relaxed_sys(&r->hdr, P.hdr);
-    st_release_sys(&r->epoch, e);
+    const long long rv[REC_UNITS] = {(long long)P.hdr, 0, 0, 0, 0, 0};
+    rec_put(rec_slot(P.heap[tid], par, b, rank), tag, rv, 1);
   }
   if (tid < p) {
-    Rec* r = rec_slot(myheap, par, b, tid);
-    if (!wait_geq(&r->epoch, e, P.timeout_cycles)) atomicExch(&s_err, ERR_TRANSPORT);
-    else if (ld_relaxed_sys(&r->hdr) != P.hdr) atomicExch(&s_err, ERR_SHAPE);
+    long long rv[REC_UNITS];
+    if (!rec_get(rec_slot(myheap, par, b, tid), tag, rv, 1, P.timeout_cycles)) atomicExch(&s_err, ERR_TRANSPORT);
+    else if ((unsigned long long)rv[RF_HDR] != P.hdr) atomicExch(&s_err, ERR_SHAPE);
+    __threadfence();
   }
   __syncthreads();
   if (s_err) goto finish;
@@ -163,11 +164,11 @@ __global__ void __launch_bounds__(THREADS, 1) ps_kernel(const __grid_constant__ 
   }
   // 3. publish "slice b of my owned space is served", then pull the others'
   __syncthreads();
-  if (tid < p) st_release_sys(mid_slot(P.heap[tid], b, rank), e);
+  if (tid < p) flag_put(mid_slot(P.heap[tid], b, rank), e);
   if ((P.worker_mask >> rank) & 1u) {
     for (int q = 0; q < p; ++q) {
       if (q == rank || P.table[q + 1] == P.table[q]) continue;
-      if (tid == 0 && !wait_geq(mid_slot(myheap, b, q), e, P.timeout_cycles)) atomicExch(&s_err, ERR_TRANSPORT);
+      if (tid == 0 && !flag_wait(mid_slot(myheap, b, q), e, P.timeout_cycles)) atomicExch(&s_err, ERR_TRANSPORT);
       __syncthreads();
       if (s_err) break;
       const long long own = ps_entry(P.table, p, P.table[q + 1] - 1)[0] + ps_entry(P.table, p, P.table[q + 1] - 1)[2];
@@ -180,18 +181,20 @@ __global__ void __launch_bounds__(THREADS, 1) ps_kernel(const __grid_constant__ 
         const long long head = ((VE - ((reinterpret_cast<uintptr_t>(prm + g0) & 15) / SZ)) % VE);
         const bool vec = ((reinterpret_cast<uintptr_t>(src + g0) ^ reinterpret_cast<uintptr_t>(prm + g0)) & 15) == 0;
         const long long h = vec ? (head < cnt ? head : cnt) : cnt;
-        for (long long i = tid; i < h; i += THREADS) prm[g0 + i] = src[g0 + i];
+        // (peer data: L1-bypassing loads)
+        for (long long i = tid; i < h; i += THREADS) prm[g0 + i] = ld_cg_elem(src + g0 + i);
         if (vec) {
           const long long nv = (cnt - h) / VE;
           const uint4* vs = reinterpret_cast<const uint4*>(src + g0 + h);
           uint4* vd = reinterpret_cast<uint4*>(prm + g0 + h);
           long long i = tid;
           for (; i + 3 * THREADS < nv; i += 4 * THREADS) {
-            const uint4 a = vs[i], b2 = vs[i + THREADS], c = vs[i + 2 * THREADS], d = vs[i + 3 * THREADS];
+            const uint4 a = __ldcg(vs + i), b2 = __ldcg(vs + i + THREADS), c = __ldcg(vs + i + 2 * THREADS),
+                        d = __ldcg(vs + i + 3 * THREADS);
             vd[i] = a; vd[i + THREADS] = b2; vd[i + 2 * THREADS] = c; vd[i + 3 * THREADS] = d;
           }
-          for (; i < nv; i += THREADS) vd[i] = vs[i];
-          for (long long j = h + nv * VE + tid; j < cnt; j += THREADS) prm[g0 + j] = src[g0 + j];
+          for (; i < nv; i += THREADS) vd[i] = __ldcg(vs + i);
+          for (long long j = h + nv * VE + tid; j < cnt; j += THREADS) prm[g0 + j] = ld_cg_elem(src + g0 + j);
         }
       });
     }
