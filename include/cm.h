@@ -343,7 +343,8 @@ int cm_ps_step_v(cm_comm_t* comm, int n, const void* const* grads, void* const* 
 int cm_local_reduce(const void* a, const void* b, void* out, int64_t count, int dtype, int op,
                     void* stream);
 /* fuse/unfuse payload moves aggregation.py:110-111,133-135: one launch copies
- * n (src, dst, bytes) triples */
+ * n (src, dst, bytes) triples; members in pageable host memory (which the
+ * kernel cannot dereference) are moved by the copy engines instead */
 int cm_batched_copy(int n, const void* const* srcs, void* const* dsts, const int64_t* nbytes,
                     void* stream);
 /* diagnostics: all-to-all NVLink bandwidth, mode 0 = every rank pulls `bytes`

@@ -138,7 +138,10 @@ def _batched_copy(srcs, dsts, nbytes, device) -> None:
 
 def fuse(ready: list[Tensor], cfg: FusionConfig) -> list[FusedBuffer]:
     """aggregation.py:95-130; the concatenation is one batched-copy kernel
-    launch per buffer (device tensors) instead of np.concatenate."""
+    launch per buffer instead of np.concatenate. CUDA-aware semantics: the
+    fused buffer lives on the GPU (where its allreduce runs) even when the
+    members are host tensors — pinned members are read by the kernel, pageable
+    ones are moved by the copy engines; nothing is concatenated on the CPU."""
     buffers = []
     for grp in fuse_plan(ready, cfg):
         members, off = [], 0
@@ -146,15 +149,14 @@ def fuse(ready: list[Tensor], cfg: FusionConfig) -> list[FusedBuffer]:
         for t in ts:
             members.append((t.name, off, t.len))
             off += t.len
-        dev = ts[0].payload.device
+        dev = next((t.payload.device for t in ts if t.is_cuda), None)
+        if dev is None:
+            dev = torch.device("cuda", torch.cuda.current_device())
         payload = torch.empty(off, dtype=DTYPES[ts[0].dtype], device=dev)
-        if dev.type == "cuda":
-            esz = payload.element_size()
-            _batched_copy([t.payload.data_ptr() for t in ts],
-                          [payload.data_ptr() + o * esz for _, o, _ in members],
-                          [t.nbytes for t in ts], dev)
-        else:
-            torch.cat([t.payload for t in ts], out=payload)
+        esz = payload.element_size()
+        _batched_copy([t.payload.data_ptr() for t in ts],
+                      [payload.data_ptr() + o * esz for _, o, _ in members],
+                      [t.nbytes for t in ts], dev)
         buffers.append(FusedBuffer(ts[0].dtype, payload, members))
     return buffers
 

@@ -2080,7 +2080,32 @@ int cm_local_reduce(const void* a, const void* b, void* out, int64_t count, int 
 int cm_batched_copy(int n, const void* const* srcs, void* const* dsts, const int64_t* nbytes,
                     void* stream) {
   if (n < 0) return fail(CM_ERR_VALUE, "negative count");
-  return launch_batched_copy(nullptr, n, srcs, dsts, nbytes, false, static_cast<cudaStream_t>(stream));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // members the kernel cannot dereference (pageable host memory) go through
+  // the copy engines; the rest are one batched-copy launch
+  std::vector<const void*> ks;
+  std::vector<void*> kd;
+  std::vector<int64_t> kb;
+  for (int i = 0; i < n; ++i) {
+    bool direct = true;
+    for (const void* ptr : {srcs[i], static_cast<const void*>(dsts[i])}) {
+      cudaPointerAttributes a;
+      if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+        cudaGetLastError();
+        direct = false;
+      } else if (a.type == cudaMemoryTypeUnregistered) {
+        direct = false;
+      }
+    }
+    if (direct) {
+      ks.push_back(srcs[i]);
+      kd.push_back(dsts[i]);
+      kb.push_back(nbytes[i]);
+    } else if (nbytes[i] > 0) {
+      CUDA_TRY(cudaMemcpyAsync(dsts[i], srcs[i], nbytes[i], cudaMemcpyDefault, s));
+    }
+  }
+  return launch_batched_copy(nullptr, (int)ks.size(), ks.data(), kd.data(), kb.data(), false, s);
 }
 
 int cm_bench_p2p(cm_comm_t* c, int mode, int64_t bytes, int ctas, int iters, void* stream_,

@@ -138,13 +138,15 @@ def test_fuse_plan_matches_oracle_and_invariants(elem_counts, threshold):
     assert len(P.fuse_plan(ts, P.FusionConfig(threshold * 2))) <= len(plan)
 
 
-def test_fuse_and_unfuse_on_host_tensors():
-    ts = _tensors([16, 48, 32])
-    (buf,) = P.fuse(ts, P.FusionConfig(2 ** 20))
-    back = P.unfuse(buf)
-    assert [t.name for t in back] == [t.name for t in ts]
-    for a, b in zip(ts, back):
-        assert np.array_equal(a.numpy(), b.numpy())
+def test_fuse_of_host_tensors_has_no_cpu_fallback():
+    """fuse() puts the fused buffer on the GPU (CUDA-aware semantics; the
+    GPU test checks the values): without a device it fails loudly instead
+    of concatenating on the CPU."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present: covered by tests/test_gpu_fused_virtual.py")
+    with pytest.raises((RuntimeError, AssertionError)):
+        P.fuse(_tensors([16, 48, 32]), P.FusionConfig(2 ** 20))
 
 
 REG = of_kind("registry")

@@ -208,3 +208,23 @@ def test_negotiate_ready_group(p):
     assert P.negotiate_ready_group(same, g) == [["a", "b", "c"]] * p
     diff = [["a", "b", "c"] if r else ["b", "c", "d"] for r in range(p)]
     assert P.negotiate_ready_group(diff, g) == [["b", "c"]] * p
+
+
+def test_fuse_host_members_lands_on_the_device():
+    """fuse() of host tensors (pageable and pinned): the fused buffer is a
+    device tensor (the copy engines / the batched-copy kernel move the
+    members; nothing is concatenated on the CPU), unfuse() gives device views."""
+    rng = np.random.default_rng(3)
+    arrays = [rng.standard_normal(n).astype(np.float32) for n in (5, 70_001, 3, 4096)]
+    ts = []
+    for i, a in enumerate(arrays):
+        x = torch.from_numpy(a)
+        if i % 2:
+            x = x.pin_memory()
+        ts.append(P.Tensor(f"t{i}", "float32", x))
+    (buf,) = P.fuse(ts, P.FusionConfig(1 << 30))
+    assert buf.payload.is_cuda
+    torch.cuda.synchronize()
+    assert buf.payload.cpu().numpy().tobytes() == np.concatenate(arrays).tobytes()
+    for a, t in zip(arrays, P.unfuse(buf)):
+        assert t.is_cuda and t.to_bytes() == a.tobytes()
