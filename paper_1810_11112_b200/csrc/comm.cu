@@ -550,8 +550,13 @@ unsigned long long buffer_id_of(cm_comm* c, const void* ptr) {
 // NVLink, open the IPC handles (cached), write AUTOTAB[slot][q] in my heap and
 // acknowledge in the peer's heap. Synchronous on a private stream; runs only
 // when a peer published something new.
-int service_autoreg(cm_comm* c) {
+int service_autoreg(cm_comm* c, cudaStream_t stream) {
   if (!c->areg_host) return CM_OK;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(stream, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) {
+    cudaGetLastError();
+    return CM_OK;                    // mapped at the next eager call
+  }
   for (int q = 0; q < c->size; ++q) {
     if (q == c->rank) continue;
     const int64_t n = (int64_t) reinterpret_cast<volatile unsigned long long*>(c->areg_host)[q];
@@ -596,7 +601,7 @@ int service_autoreg(cm_comm* c) {
 // first sight), or -1 if it cannot be shared (not cudaMalloc memory, or the
 // mailbox is full). The allocation's buffer id is re-checked on every use so
 // a freed and re-allocated range at the same address gets a new slot.
-int64_t auto_slot(cm_comm* c, const void* ptr, int64_t bytes) {
+int64_t auto_slot(cm_comm* c, const void* ptr, int64_t bytes, bool may_publish) {
   static GetRangeFn get_range = driver_fn<GetRangeFn>("cuMemGetAddressRange");
   const uintptr_t a = reinterpret_cast<uintptr_t>(ptr);
   const unsigned long long bid = buffer_id_of(c, ptr);
@@ -607,6 +612,7 @@ int64_t auto_slot(cm_comm* c, const void* ptr, int64_t bytes) {
       return it->second.slot;
     if (a < it->first + it->second.size) c->autoregs.erase(it);     // stale: the range was re-allocated
   }
+  if (!may_publish) return -1;       // e.g. inside a CUDA-graph capture: no synchronous copies
   CUdeviceptr base = 0;
   size_t size = 0;
   if (!get_range || !bid || get_range(&base, &size, reinterpret_cast<CUdeviceptr>(ptr)) != CUDA_SUCCESS) return -1;
@@ -668,7 +674,9 @@ int place(cm_comm* c, const void* send, int64_t send_bytes, void* recv, int64_t 
       send_bytes > 0) {
     // automatic registration: peers read this allocation in place once every
     // peer has mapped its mailbox slot; until then it is copied in
-    const int64_t slot = auto_slot(c, send, send_bytes);
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(stream, &cap);
+    const int64_t slot = auto_slot(c, send, send_bytes, cap == cudaStreamCaptureStatusNone);
     const int64_t acked = (int64_t) reinterpret_cast<volatile unsigned long long*>(c->areg_host)[MAXP];
     if (slot >= 0 && slot < acked) {
       auto it = c->autoregs.upper_bound(reinterpret_cast<uintptr_t>(send));
@@ -757,7 +765,7 @@ int do_allreduce(cm_comm* c, const void* const* sends, void* const* recvs, int64
   plan_algo(c, concrete, nbytes, &L);
   Placement pl;
   if (!c->virt) {
-    if ((st = service_autoreg(c))) return st;
+    if ((st = service_autoreg(c, stream))) return st;
     const bool peers_read = !L.ll && !L.oneshot;    // the two-shot pull reads inputs in place
     if ((st = place(c, sends[0], nbytes, recvs[0], nbytes, stream, &pl, peers_read))) return st;
     L.srcmode = pl.srcmode;
@@ -806,7 +814,7 @@ int do_rs(cm_comm* c, const void* const* sends, void* const* recvs, int64_t coun
   L.out_rel = 1;
   Placement pl;
   if (!c->virt) {
-    if ((st = service_autoreg(c))) return st;
+    if ((st = service_autoreg(c, stream))) return st;
     if ((st = place(c, sends[0], count * sz, recvs[0], len[c->rank] * sz, stream, &pl, true))) return st;
     L.srcmode = pl.srcmode;
     L.in[0] = pl.in;
@@ -850,7 +858,7 @@ int do_ag(cm_comm* c, const void* const* sends, void* const* recvs, int64_t coun
   L.ag_in_rel = 1;
   Placement pl;
   if (!c->virt) {
-    if ((st = service_autoreg(c))) return st;
+    if ((st = service_autoreg(c, stream))) return st;
     if ((st = place(c, sends[0], len[c->rank] * sz, recvs[0], count * sz, stream, &pl, true))) return st;
     L.srcmode = pl.srcmode;
     L.in[0] = pl.in;
@@ -1664,6 +1672,7 @@ int fused_impl(cm_comm* c, int n, const void* const* sends, const int64_t* count
   }
   // host inputs or outputs: the copy-stream pipeline (device buffers sized for
   // every local rank's whole call) starts before the plan takes their addresses
+  if (!c->virt && (st = service_autoreg(c, stream))) return st;   // peers' new allocations, if any
   if ((any_host_in || out_host) &&
       (st = hp.start(any_host_in ? nloc * total_bytes : 0, out_host ? nloc * total_bytes : 0)))
     return st;

@@ -451,6 +451,32 @@ def main():
         del bufs, segx
         torch.cuda.synchronize()
         torch.cuda.empty_cache()            # the ranges go back to the driver; new ones may reuse them
+    # a CUDA graph captured on a never-seen plain tensor: no synchronous
+    # registration inside the capture (copy-in), replays stay exact
+    gx = torch.empty(2_000_003, device="cuda")
+    gy = torch.empty_like(gx)
+    cs = torch.cuda.Stream()
+    graph = torch.cuda.CUDAGraph()
+    from paper_1810_11112_b200 import _lib as LL
+    import ctypes as CT
+    gst = LL.Stats()
+    comm.blocking = False
+    with torch.cuda.stream(cs):
+        with torch.cuda.graph(graph, stream=cs):
+            LL.check(LL.lib.cm_allreduce(comm._h, gx.data_ptr(), gy.data_ptr(), gx.numel(), 0, 0,
+                                         LL.ALGO["ring_rsa"], 131072, 0, cs.cuda_stream, CT.byref(gst)))
+    for it in range(3):
+        xs_all = [np.random.default_rng([9, it, r]).standard_normal(gx.numel()).astype(np.float32)
+                  for r in range(world)]
+        gx.copy_(torch.from_numpy(xs_all[rank]))
+        torch.cuda.synchronize()
+        dist.barrier()
+        graph.replay()
+        torch.cuda.synchronize()
+        comm.poll()
+        expect(gy.cpu().numpy().tobytes() == OC.allreduce(xs_all, "sum", "ring_rsa", "float32").tobytes(),
+               f"graph-captured allreduce on a plain tensor, replay {it}")
+    comm.blocking = True
     expect(comm.get_param("auto_published") >= 3, "allocations published in the mailbox")
     expect(comm.get_param("auto_mapped") >= 3, "peers' allocations mapped")
     expect(comm.get_param("auto_zero_copy_calls") > z0, "plain tensors read in place")
