@@ -518,7 +518,7 @@ def headline(args, rank, world, local):
                     "launches": coll_n, "avg_launch_us": round(coll_ms / max(coll_n, 1) * 1e3, 2),
                     "other_launches": {"agreement_check_ll": small_n,
                                        "avg_us": round(small_ms / max(small_n, 1) * 1e3, 2),
-                                       "pack": pack_n},
+                                       "pack": pack_n, "pack_avg_us": round(pack_ms / max(pack_n, 1) * 1e3, 2)},
                     "measured": "second timed pass of K steps with CUDA events around every launch"}
     else:
         ach = pack_b / (pack_ms * 1e-3) / 1e9 if pack_ms > 0 else 0.0
