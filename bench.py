@@ -736,11 +736,13 @@ def sweep(args, rank, world, local):
 
 
 def tune(args, rank, world, local):
-    """Measure, per message size, rhd one-shot (LL), rhd two-shot and ring,
+    """Measure, per message size, rhd one-shot (LL), rhd two-shot, ring (LL
+    two-shot while the segments fit the LL slots) and ring on the pull kernel,
     all CUDA-graph timed, and store per group size: the largest size worth
-    reducing one-shot (oneshot_max_bytes = ll_max_bytes) and the switch point
-    from which ring_rsa beats rhd_rsa (collectives.py:239-247's threshold,
-    measured on this box) in paper_1810_11112_b200/tuning.json."""
+    reducing one-shot (oneshot_max_bytes = ll_max_bytes), the largest size
+    worth the LL two-shot (ll2_max_bytes) and the switch point from which
+    ring_rsa beats rhd_rsa (collectives.py:239-247's threshold, measured on
+    this box) in paper_1810_11112_b200/tuning.json."""
     import paper_1810_11112_b200 as P
     from paper_1810_11112_b200 import _lib as L
     device = torch.device("cuda", local)
@@ -755,10 +757,11 @@ def tune(args, rank, world, local):
     for nbytes in sizes:
         n = nbytes // 4
         t = {}
-        for name, algo, osm in (("rhd_oneshot", "rhd_rsa", big), ("rhd_twoshot", "rhd_rsa", 1),
-                                ("ring", "ring_rsa", big)):
+        for name, algo, osm, ll2 in (("rhd_oneshot", "rhd_rsa", big, big), ("rhd_twoshot", "rhd_rsa", 1, big),
+                                     ("ring", "ring_rsa", big, big), ("ring_pull", "ring_rsa", big, 1)):
             comm.set_param("oneshot_max_bytes", osm)
             comm.set_param("ll_max_bytes", osm)
+            comm.set_param("ll2_max_bytes", ll2)
             fn = lambda a=algo: L.check(L.lib.cm_allreduce(  # noqa: E731
                 comm._h, x.data_ptr(), y.data_ptr(), n, 0, 0, L.ALGO[a], 131072, 0,
                 torch.cuda.current_stream().cuda_stream, C.byref(st)))
@@ -773,6 +776,13 @@ def tune(args, rank, world, local):
             oneshot_max = nbytes
         else:
             break
+    ll2_max = 0
+    for nbytes in sizes:
+        if res[nbytes]["ring"] <= res[nbytes]["ring_pull"]:
+            ll2_max = nbytes
+        else:
+            break
+
     def rhd_best(b):
         return res[b]["rhd_oneshot"] if b <= oneshot_max else res[b]["rhd_twoshot"]
     switch = None
@@ -791,12 +801,14 @@ def tune(args, rank, world, local):
             data = {}
         data.setdefault("switch_bytes", {})[str(world)] = switch
         data.setdefault("oneshot_max_bytes", {})[str(world)] = max(oneshot_max, 1024)
+        data.setdefault("ll2_max_bytes", {})[str(world)] = max(ll2_max, 1024)
         data.setdefault("measured_us_cuda_graph", {})[str(world)] = {
             str(k): {a: round(v, 3) for a, v in t.items()} for k, t in res.items()}
         data["how"] = "bench.py --mode tune on a B200 box: CUDA-graph timed, max over ranks"
         with open(path, "w") as fh:
             json.dump(data, fh, indent=1)
-        emit({"mode": "tune", "p": world, "switch_bytes": switch, "oneshot_max_bytes": oneshot_max})
+        emit({"mode": "tune", "p": world, "switch_bytes": switch, "oneshot_max_bytes": oneshot_max,
+              "ll2_max_bytes": ll2_max})
     comm.close()
 
 

@@ -167,11 +167,14 @@ class Communicator(_Base):
         self.set_policy(policy)
         if timeout_s is not None:
             self.set_timeout(timeout_s)
-        from .tuning import oneshot_max_for
+        from .tuning import ll2_max_for, oneshot_max_for
         osm = oneshot_max_for(self.size)
         if osm:
             self.set_param("oneshot_max_bytes", osm)
             self.set_param("ll_max_bytes", osm)
+        l2m = ll2_max_for(self.size)
+        if l2m:
+            self.set_param("ll2_max_bytes", l2m)
         self._sym: dict[int, int] = {}
 
     # -- symmetric allocation (zero-copy collectives) -------------------------

@@ -19,9 +19,10 @@
 //   RS-only / AG-only : the public reduce_scatter / allgather.
 //
 // Synchronisation is flag based over NVLink: CTA b of rank r publishes a
-// record {epoch, header, src offset, reduced offset} into slot [parity][b][r]
-// of every peer's heap with st.release.sys, and waits on its own heap with
-// ld.acquire.sys. The epoch lives in device memory and is advanced by the last
+// record {header, src offset, reduced offset, ...} into slot [parity][b][r]
+// of every peer's heap as LL units tagged with the epoch (rec_put), and polls
+// its own heap (rec_get); later phase flags are a gpu-scope fence + relaxed
+// store (flag_put / flag_wait). The epoch lives in device memory and is advanced by the last
 // CTA of each launch, so launches can be captured into CUDA graphs. Staging is
 // double-buffered by epoch parity: a rank rewrites staging[e&1] only in call
 // e+2, after every peer has entered call e+1 (and therefore left call e).
@@ -862,7 +863,7 @@ __device__ __forceinline__ void bulk_rs_setup(int stages, int stage_bytes, int t
 
 // Progress publication of the overlapped two-shot: after each reduced chunk the
 // consumers synchronise and one thread pushes (tag | base + elements done in
-// this range) to every peer's PROG[blk][rank] with release semantics.
+// this range) to every peer's PROG[blk][rank] (gpu-scope fence + relaxed store).
 struct Prog {
   unsigned long long* dst[MAXP];   // peers' PROG slots for this CTA's slice (nullptr: self)
   unsigned long long tag;          // epoch << 32

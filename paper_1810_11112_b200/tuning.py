@@ -3,9 +3,10 @@ made by a size threshold measured on the box").
 
 ``tuning.json`` next to this file is written by ``bench.py --tune`` on a B200
 box: for every group size it stores the message size from which ring_rsa
-(two-shot reduce-scatter + allgather) beats rhd_rsa (one-shot tree) and the
-largest message worth reducing one-shot. Without an entry the reference
-default of 131072 B (collectives.py:23) applies.
+(two-shot reduce-scatter + allgather) beats rhd_rsa (one-shot tree), the
+largest message worth reducing one-shot and the largest worth the LL
+two-shot. Without an entry the reference default of 131072 B
+(collectives.py:23) applies.
 """
 
 from __future__ import annotations
@@ -33,4 +34,11 @@ def switch_bytes_for(p: int) -> int:
 
 def oneshot_max_for(p: int) -> int | None:
     v = table().get("oneshot_max_bytes", {}).get(str(p))
+    return None if v is None else int(v)
+
+
+def ll2_max_for(p: int) -> int | None:
+    """Largest message worth the LL two-shot kernel (above it: the pull
+    two-shot); None = the kernel's own limit (p x the LL slot payload)."""
+    v = table().get("ll2_max_bytes", {}).get(str(p))
     return None if v is None else int(v)
