@@ -108,7 +108,8 @@ struct cm_comm {
   int inline_agree = 1;                       // aggregate's agreement inside the collective's records
   int overlap = 0;                            // multi-buffer two-shot: RS and AG CTAs run concurrently
                                               // (opt-in: measured slower, the RS needs every SM)
-  int ovl_chunks = 4;                         // reduce chunks per progress report (overlap)
+  int ovl_chunks = 4;                         // reduce chunks per progress report (overlap, ws)
+  int ws = 0;                                 // multi-buffer two-shot: RS and AG warps in every CTA
   int bulk_stage = 2 * RS_STAGE_BYTES;        // bytes per bulk-reduce stage (64 KiB: 3 stages fit)
   int64_t host_chunk = 8 << 20;               // host-gradient pipeline: bytes per H2D/D2H piece (p = 1)
   int64_t oneshot_bytes_per_cta = 8 * 1024;
@@ -470,12 +471,14 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
     P.overlap = ovl ? 1 : 0;
     P.nrs = (int)(nb / 2);
     P.ovl_chunks = c->ovl_chunks;
+    P.ws = (multi && c->ws && bulk && !ovl && !c->dyn_ag) ? 1 : 0;
     CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k, dim3((unsigned)nb, (unsigned)p),
                                          dim3(THREADS), args, dsm, stream));
   } else {
     P.overlap = ovl ? 1 : 0;
     P.nrs = (int)(nb / 2);
     P.ovl_chunks = c->ovl_chunks;
+    P.ws = (multi && c->ws && bulk && !ovl && !c->dyn_ag) ? 1 : 0;
     CUDA_TRY(cudaLaunchKernel((const void*)k, dim3((unsigned)nb), dim3(THREADS), args, dsm, stream));
   }
   c->launches += 1;
@@ -1191,6 +1194,7 @@ int cm_comm_set_param(cm_comm_t* c, const char* key, int64_t value) {
   else if (k == "auto_register") c->auto_reg = value > 1 ? 1 : 0;
   else if (k == "overlap") c->overlap = value > 1 ? 1 : 0;
   else if (k == "overlap_chunks") c->ovl_chunks = (int)std::min<int64_t>(value, 1 << 20);
+  else if (k == "ws") c->ws = value > 1 ? 1 : 0;
   else if (k == "host_chunk_kb") c->host_chunk = std::max<int64_t>(64, value) * 1024;
   else if (k == "bulk_stage_kb") c->bulk_stage = (int)std::max<int64_t>(4, std::min<int64_t>(value, 112)) * 1024;
   else if (k == "oneshot_bytes_per_cta") c->oneshot_bytes_per_cta = value;
@@ -1217,6 +1221,7 @@ int cm_comm_get_param(cm_comm_t* c, const char* key, int64_t* value) {
   else if (k == "auto_register") *value = c->auto_reg ? 2 : 1;
   else if (k == "overlap") *value = c->overlap ? 2 : 1;
   else if (k == "overlap_chunks") *value = c->ovl_chunks;
+  else if (k == "ws") *value = c->ws ? 2 : 1;
   else if (k == "auto_published") *value = c->auto_published;
   else if (k == "auto_mapped") *value = c->auto_mapped;
   else if (k == "auto_zero_copy_calls") *value = c->auto_zc_calls;

@@ -227,6 +227,7 @@ struct CollParams {
   int overlap;
   int nrs;
   int ovl_chunks;            // reduce chunks per progress report / allgather block
+  int ws;                    // warp-specialised two-shot (multi-buffer kernel): RS and AG warps per CTA
   // automatic registration (real communicators): my published slot count,
   // the slot counts of each peer I have mapped, and host-mapped words where
   // CTA 0 reports peers' newer slot counts (notice[q]) and the smallest
@@ -726,7 +727,7 @@ constexpr int CP_CHUNK = 32 * CP_U;           // vectors per warp chunk (4 KiB)
 
 // R[0..nr) in shared memory; V is shared scratch of the same size.
 template <class D, int MP>
-__device__ void multi_copy(const CopyRange* R, int nr, VecRange* V) {
+__device__ void multi_copy(const CopyRange* R, int nr, VecRange* V, int t0 = 0, int nt = THREADS, int bar = 0) {
   auto ld_cg = [](const typename D::S* a) -> typename D::S {
     using S = typename D::S;
     if constexpr (sizeof(S) == 8) {
@@ -742,8 +743,8 @@ __device__ void multi_copy(const CopyRange* R, int nr, VecRange* V) {
   };
   using S = typename D::S;
   constexpr int W = 16 / sizeof(S);
-  const int tid = threadIdx.x, bd = blockDim.x;
-  const int warp = tid >> 5, lane = tid & 31, nwarps = bd >> 5;
+  const int tid = threadIdx.x - t0;
+  const int warp = tid >> 5, lane = tid & 31, nwarps = nt >> 5;
   // scalar heads/tails (and misaligned ranges): one warp per range
   for (int r = warp; r < nr; r += nwarps) {
     const CopyRange c = R[r];
@@ -766,7 +767,8 @@ __device__ void multi_copy(const CopyRange* R, int nr, VecRange* V) {
       V[r].nv = (bhi - blo) / W;
     }
   }
-  __syncthreads();
+  if (bar == 0) __syncthreads();
+  else asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(nt) : "memory");
   if (nr < 1) return;
   long long nvmax = 0;
   for (int r = 0; r < nr; ++r) nvmax = V[r].nv > nvmax ? V[r].nv : nvmax;
@@ -820,6 +822,24 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
 constexpr int RS_MAX_STAGES = 6;
 constexpr int RS_STAGE_BYTES = 32768;         // default stage size (knob bulk_stage_kb)
 constexpr int RS_CONSUMERS = THREADS - 32;
+
+// The threads that run a bulk-engine reduce: `ncons` consumers (tid < ncons),
+// the producer (tid == ncons, one lane of the next warp) and their group
+// barrier (`bar` 0 = the whole CTA). The warp-specialised two-shot runs the
+// reduce on warps 0..8 and the allgather on warps 9..15 of the same CTA.
+struct Team {
+  int ncons;
+  int grp;
+  int bar;
+};
+__host__ __device__ constexpr Team team_all() { return Team{RS_CONSUMERS, THREADS, 0}; }
+__host__ __device__ constexpr Team team_ws_rs() { return Team{256, 288, 3}; }
+constexpr int WS_AG_T0 = 288, WS_AG_N = THREADS - 288, WS_AG_BAR = 2;
+
+__device__ __forceinline__ void team_sync(const Team T) {
+  if (T.bar == 0) __syncthreads();
+  else asm volatile("bar.sync %0, %1;" ::"r"(T.bar), "r"(T.grp) : "memory");
+}
 __host__ __device__ constexpr size_t rs_smem_bytes(int stages, int stage_bytes = RS_STAGE_BYTES) {
   return (size_t)stages * stage_bytes + (2 * (size_t)stages + 2) * 8;
 }
@@ -849,12 +869,12 @@ __device__ __forceinline__ BulkRS bulk_view(int stages, int stage_bytes) {
   return B;
 }
 
-__device__ __forceinline__ void bulk_rs_setup(int stages, int stage_bytes, int tid) {
+__device__ __forceinline__ void bulk_rs_setup(int stages, int stage_bytes, int tid, int ncons = RS_CONSUMERS) {
   const BulkRS B = bulk_view(stages, stage_bytes);
   if (tid == 0) {
     for (int s = 0; s < stages; ++s) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&B.full[s])));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&B.empty[s])), "r"(RS_CONSUMERS / 32));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&B.empty[s])), "r"(ncons / 32));
     }
     *B.seqno = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -882,7 +902,8 @@ __device__ __forceinline__ void prog_publish(const Prog* pg, long long pos) {
 template <class D, int OP, int MP, bool TREE>
 __device__ void reduce_range_bulk(int stages, int stage_bytes, const char* const* seq, int p, int m, int excess,
                                   long long lo, long long hi, int average, char* out, long long out_shift,
-                                  char* red, long long red_shift, int tid, const Prog* prog = nullptr) {
+                                  char* red, long long red_shift, int tid, const Prog* prog = nullptr,
+                                  const Team T = team_all()) {
   const BulkRS B = bulk_view(stages, stage_bytes);
   using S = typename D::S;
   using A = typename D::A;
@@ -892,16 +913,16 @@ __device__ void reduce_range_bulk(int stages, int stage_bytes, const char* const
   if (body_hi < body_lo) body_lo = body_hi = hi;
   if (body_lo > lo || body_hi < hi)
     reduce_scalar<D, OP, MP, TREE>(seq, p, m, excess, lo, body_lo, body_hi, hi, average, out, out_shift, red,
-                                   red_shift, tid, THREADS);
+                                   red_shift, tid, T.grp);
   const long long nbytes = (body_hi - body_lo) * SZ;
   if (nbytes <= 0) return;
-  if (prog) __syncthreads();      // the scalar head/tail precede every progress report
+  if (prog) team_sync(T);         // the scalar head/tail precede every progress report
   const int ch = (B.stage_bytes / p) & ~15;             // bytes per source per stage
   const int C = (int)((nbytes + ch - 1) / ch);
   // stage uses so far in this launch (< 2^32): stage index and mbarrier phase
   // advance incrementally (no 64-bit division in the loops)
   const unsigned base = (unsigned)*B.seqno;
-  if (tid == RS_CONSUMERS) {                            // producer: warp 15, lane 0
+  if (tid == T.ncons) {                                 // producer: lane 0 of the warp after the consumers
     asm volatile("fence.proxy.async;" ::: "memory");
     int s = (int)(base % (unsigned)B.stages);
     unsigned ph = (base / (unsigned)B.stages) & 1u;
@@ -924,7 +945,7 @@ __device__ void reduce_range_bulk(int stages, int stage_bytes, const char* const
       }
       if (++s == B.stages) { s = 0; ph ^= 1u; wrapped = true; }
     }
-  } else if (tid < RS_CONSUMERS) {
+  } else if (tid < T.ncons) {
     int s = (int)(base % (unsigned)B.stages);
     unsigned ph = (base / (unsigned)B.stages) & 1u;
     for (int c = 0; c < C; ++c) {
@@ -935,7 +956,7 @@ __device__ void reduce_range_bulk(int stages, int stage_bytes, const char* const
       const char* st = reinterpret_cast<const char*>(B.smem + (size_t)s * B.stage_bytes);
       const long long e0 = body_lo + (long long)c * (ch / SZ);
 #pragma unroll 1
-      for (int v = tid; v < nv; v += RS_CONSUMERS) {
+      for (int v = tid; v < nv; v += T.ncons) {
         A u[MP][VW];
 #pragma unroll
         for (int k = 0; k < MP; ++k) {
@@ -955,7 +976,7 @@ __device__ void reduce_range_bulk(int stages, int stage_bytes, const char* const
       if ((tid & 31) == 0)
         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&B.empty[s])) : "memory");
       if (prog && ((c + 1) % prog->every == 0 || c + 1 == C)) {   // chunks stored by every consumer: report
-        asm volatile("bar.sync 1, %0;" ::"r"(RS_CONSUMERS) : "memory");
+        asm volatile("bar.sync 1, %0;" ::"r"(T.ncons) : "memory");
         if (tid == 0) {
           // the scalar tail [body_hi, hi) was reduced before the first chunk
           const long long done = c + 1 == C ? hi - lo : body_lo - lo + (long long)(c + 1) * (ch / SZ);
@@ -965,9 +986,9 @@ __device__ void reduce_range_bulk(int stages, int stage_bytes, const char* const
       if (++s == B.stages) { s = 0; ph ^= 1u; }
     }
   }
-  __syncthreads();
+  team_sync(T);
   if (tid == 0) *B.seqno = base + (unsigned)C;
-  __syncthreads();
+  team_sync(T);
 }
 __device__ __forceinline__ bool al16s(const char* base, long long shift_elems, int sz) {
   return (((uintptr_t)base - (uintptr_t)(shift_elems * sz)) & 15u) == 0;

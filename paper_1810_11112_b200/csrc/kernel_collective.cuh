@@ -195,7 +195,8 @@ __global__ void __launch_bounds__(THREADS, 1) collective_kernel(const __grid_con
 
   if (gated_out(P, ctrl)) return;       // agreement failed earlier in this call
   CM_TRACE(P, lr, b, 0);
-  if (!STREAM && P.bulk_rs) bulk_rs_setup(P.bulk_rs, P.bulk_stage, tid);
+  if (!STREAM && P.bulk_rs)
+    bulk_rs_setup(P.bulk_rs, P.bulk_stage, tid, (MULTI && P.ws) ? team_ws_rs().ncons : RS_CONSUMERS);
   if (tid == 0) {
     s_epoch = ctrl->epoch + 1;
     s_err = 0;
@@ -351,6 +352,11 @@ __global__ void __launch_bounds__(THREADS, 1) collective_kernel(const __grid_con
     const int excess = p - m;
     char* mystage = myheap + stage_off;
     const bool ovl = P.overlap != 0;
+    // warp-specialised two-shot: warps 0..8 reduce-scatter (8 consumer warps
+    // + the bulk-engine producer) and push per-chunk progress; warps 9..15 of
+    // the same CTA allgather each peer's chunks as soon as they are reduced
+    const bool ws = P.ws != 0 && !ovl;
+    const Team T = ws ? team_ws_rs() : team_all();
     const int nrs = ovl ? P.nrs : nb;
     if (ovl && b >= nrs) {
       // ---- allgather role: slice j of every peer's segment, chunk by chunk
@@ -406,6 +412,60 @@ __global__ void __launch_bounds__(THREADS, 1) collective_kernel(const __grid_con
       }
       goto finish;
     }
+    if (ws && tid >= T.grp) {
+      // ---- allgather team: slice b of every peer's segment, block by block
+      const int at = tid - WS_AG_T0;
+      const long long G = (long long)((P.bulk_stage / p) & ~15) / SZ * P.ovl_chunks;
+      __shared__ long long s_tot2[MAXP];
+      __shared__ CopyRange s_cr2[MAXBUF * MAXP + 1];
+      __shared__ VecRange s_vr2[MAXBUF * MAXP + 1];
+      __shared__ int s_ncr2;
+      if (at < p) {
+        long long t = 0;
+        for (int k = 0; k < P.nbuf; ++k) {
+          const long long so = P.bseg_off[k][at], sl = P.bseg_len[k][at];
+          t += slice_bound(so, sl, b + 1, nb) - slice_bound(so, sl, b, nb);
+        }
+        s_tot2[at] = at == rank ? 0 : t;
+      }
+      asm volatile("bar.sync %0, %1;" ::"r"(WS_AG_BAR), "r"(WS_AG_N) : "memory");
+      long long tmax = 0;
+      for (int q = 0; q < p; ++q) tmax = s_tot2[q] > tmax ? s_tot2[q] : tmax;
+      const unsigned long long ptag = e << 32;
+#pragma unroll 1
+      for (long long pos = 0; pos < tmax; pos += G) {
+        if (at < p && pos < s_tot2[at]) {
+          const long long need = pos + G < s_tot2[at] ? pos + G : s_tot2[at];
+          const unsigned long long* f =
+              reinterpret_cast<const unsigned long long*>(myheap + PROG_OFF + ((size_t)b * MAXP + at) * 8);
+          if (!flag_wait(f, ptag | (unsigned long long)need, P.timeout_cycles)) atomicExch(&s_err, ERR_TRANSPORT);
+        }
+        asm volatile("bar.sync %0, %1;" ::"r"(WS_AG_BAR), "r"(WS_AG_N) : "memory");
+        if (s_err) break;
+        if (at == 0) {
+          int r = 0;
+          for (int q = 0; q < p; ++q) {
+            if (pos >= s_tot2[q]) continue;
+            const long long end = pos + G < s_tot2[q] ? pos + G : s_tot2[q];
+            long long base = 0;
+            for (int k = 0; k < P.nbuf && base < end; ++k) {
+              const long long so = P.bseg_off[k][q], sl = P.bseg_len[k][q];
+              const long long lo = slice_bound(so, sl, b, nb), hi = slice_bound(so, sl, b + 1, nb);
+              const long long a = pos > base ? pos : base, z = end < base + hi - lo ? end : base + hi - lo;
+              if (z > a)
+                s_cr2[r++] = CopyRange{P.heap[q] + stage_off + P.bboff[k] * SZ, out + P.bout_off[k] * SZ, 0, 0,
+                                       lo + (a - base), lo + (z - base)};
+              base += hi - lo;
+            }
+          }
+          s_ncr2 = r;
+        }
+        asm volatile("bar.sync %0, %1;" ::"r"(WS_AG_BAR), "r"(WS_AG_N) : "memory");
+        multi_copy<D, MP>(s_cr2, s_ncr2, s_vr2, WS_AG_T0, WS_AG_N, WS_AG_BAR);
+        asm volatile("bar.sync %0, %1;" ::"r"(WS_AG_BAR), "r"(WS_AG_N) : "memory");
+      }
+      goto finish;
+    }
     // piece iterator, advanced by thread 0 only (the loop state lives in
     // shared memory, not in every thread's registers)
     if (tid == 0) {
@@ -416,7 +476,7 @@ __global__ void __launch_bounds__(THREADS, 1) collective_kernel(const __grid_con
       s_prog.p = p;
       s_prog.every = P.ovl_chunks;
       for (int q = 0; q < p; ++q)
-        s_prog.dst[q] = (ovl && q != rank)
+        s_prog.dst[q] = ((ovl || ws) && q != rank)
                             ? reinterpret_cast<unsigned long long*>(P.heap[q] + PROG_OFF + ((size_t)b * MAXP + rank) * 8)
                             : nullptr;
     }
@@ -462,30 +522,30 @@ __global__ void __launch_bounds__(THREADS, 1) collective_kernel(const __grid_con
           s_prog.base = s_pos;
         }
       }
-      __syncthreads();
+      team_sync(T);
       if (s_k >= P.nbuf) break;
       CM_CHECK(s_i <= s_pe && s_pe <= s_hi && s_hi <= P.bseg_off[s_k][rank] + P.bseg_len[s_k][rank] &&
                    (P.bboff[s_k] + s_pe) * SZ <= P.staging_bytes && s_pe <= P.bn[s_k],
                P.herr);
       if (P.bulk_rs && s_vec) {
         reduce_range_bulk<D, OP, MP, TREE>(P.bulk_rs, P.bulk_stage, s_seqk, p, m, excess, s_i, s_pe, P.average,
-                                           s_bo, 0, s_rd, 0, tid, ovl ? &s_prog : nullptr);
+                                           s_bo, 0, s_rd, 0, tid, (ovl || ws) ? &s_prog : nullptr, T);
       } else {
         reduce_range<D, OP, MP, TREE>(s_seqk, p, m, excess, s_i, s_pe, s_vec != 0, P.average, s_bo, 0, s_rd, 0,
-                                      tid, blockDim.x);
-        if (ovl) {
-          __syncthreads();
+                                      tid, T.grp);
+        if (ovl || ws) {
+          team_sync(T);
           if (tid == 0) prog_publish(&s_prog, s_pos + (s_pe - s_i));
         }
       }
-      __syncthreads();
+      team_sync(T);
       if (tid == 0) {
         s_pos += s_pe - s_i;
         s_i = s_pe;
       }
     }
     CM_TRACE(P, lr, b, 3);
-    if (ovl) goto finish;
+    if (ovl || ws) goto finish;
     if (tid < p) flag_put(mid_slot(P.heap[tid], b, rank), e);
     if (P.dyn_ag) {
       dynamic_allgather<D, MP>(P, rank, nb, e, myheap, ctrl, s_src, s_red, out, true, s_cr, s_vr, &s_ncr, &s_err);

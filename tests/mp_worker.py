@@ -208,6 +208,18 @@ def main():
             expect(all(t.to_bytes() == want[t.name].tobytes() for t in res.tensors),
                    f"multi-buffer aggregate {algo} mb={mb}")
     comm.set_param("multi_buffer", 2)
+    # the two overlapped two-shot variants of the multi-buffer launch
+    for knobs in ({"ws": 2}, {"overlap": 2}):
+        for k, v in knobs.items():
+            comm.set_param(k, v)
+        for algo in ("ring_rsa", "rhd_rsa"):
+            want, groups, _ = OA.aggregate(per_rank, "float32", algo, 8 << 20)
+            gs = P.GradientSet(tuple(P.Tensor(nm, "float32", torch.from_numpy(a).cuda())
+                                     for nm, a in per_rank[rank]))
+            res = P.aggregate(gs, group, comm, algo=algo, cfg=P.FusionConfig(8 << 20))
+            expect(all(t.to_bytes() == want[t.name].tobytes() for t in res.tensors), f"{knobs} aggregate {algo}")
+        comm.set_param("ws", 1)
+        comm.set_param("overlap", 1)
     # opt-in TMA bulk-copy pack (bulk_copy) into the staging heap
     comm.set_param("bulk_copy", 2)
     aligned = [I.synth_gradients(5, 0, [480_000] * 12 + [1_000_004, 76], r) for r in range(world)]

@@ -93,19 +93,19 @@ def test_model_golden_through_fused_path(case, registered):
 
 @pytest.mark.parametrize("p", [2, 3, 4, 8])
 @pytest.mark.parametrize("mode", ["prestaged", "registered"])
-@pytest.mark.parametrize("overlap", [1, 2])
-def test_multi_buffer_launches_vs_oracle(p, mode, overlap):
+@pytest.mark.parametrize("variant", ["barrier", "overlap", "ws"])
+def test_multi_buffer_launches_vs_oracle(p, mode, variant):
     """8 MiB fusion threshold: the ResNet-like set splits into 13 fused groups,
-    batched MAXBUF=4 per multi-buffer launch (nbuf > 1); with the overlapped
-    two-shot (allgather CTAs follow the reduce-scatter CTAs' per-chunk
-    progress) and with the RS->AG barrier."""
+    batched MAXBUF=4 per multi-buffer launch (nbuf > 1); with the RS->AG
+    barrier, the CTA-split overlap and the warp-specialised overlap (the
+    allgather follows the reduce-scatter's per-chunk progress)."""
     layers = I.MODELS["resnet50_like"][:24] + [77, 1_000_003, 5]
     per_rank = [I.synth_gradients(3, 1, layers, r) for r in range(p)]
     for algo in ("auto", "ring_rsa", "rhd_rsa"):
         want, groups, _ = OA.aggregate(per_rank, "float32", algo, 8 << 20)
         assert len(groups) > 4
         sets = sets_of(per_rank)
-        g = vg(p, overlap=overlap)
+        g = vg(p, **{"barrier": {}, "overlap": {"overlap": 2}, "ws": {"ws": 2}}[variant])
         if mode == "registered":
             P.register_gradients_group(sets, g)
         stats = []
