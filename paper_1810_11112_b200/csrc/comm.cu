@@ -110,6 +110,8 @@ struct cm_comm {
                                               // (opt-in: measured slower, the RS needs every SM)
   int ovl_chunks = 4;                         // reduce chunks per progress report (overlap, ws)
   int ws = 0;                                 // multi-buffer two-shot: RS and AG warps in every CTA
+  int pack_waves = 2;                         // batched copy: CTA waves (4 per SM per wave)
+  int pack_unroll = 4;                        // batched copy: 16-byte loads in flight per thread (4 or 8)
   int bulk_stage = 2 * RS_STAGE_BYTES;        // bytes per bulk-reduce stage (64 KiB: 3 stages fit)
   int64_t host_chunk = 8 << 20;               // host-gradient pipeline: bytes per H2D/D2H piece (p = 1)
   int64_t oneshot_bytes_per_cta = 8 * 1024;
@@ -917,13 +919,15 @@ int launch_batched_copy(cm_comm* c, int n, const void* const* srcs, void* const*
       if (c) c->launches += 1;
       continue;
     }
-    // >= 2 waves of 512-thread CTAs (4 resident per SM) for large packs
+    // `pack_waves` waves of 512-thread CTAs (4 resident per SM) for large packs
+    const int sms = c ? c->sms : 148;
+    const int waves = c ? c->pack_waves : 2;
     int64_t nb = (P.start[m] + (64 << 10) - 1) / (64 << 10);
-    nb = std::max<int64_t>(1, std::min<int64_t>(nb, 148 * 8));
+    nb = std::max<int64_t>(1, std::min<int64_t>(nb, (int64_t)sms * 4 * waves));
     void* args[] = {&P};
     ProfScope prof_scope(c, stream, 1, 2 * P.start[m]);
-    CUDA_TRY(cudaLaunchKernel((const void*)batched_copy_kernel, dim3((unsigned)nb), dim3(THREADS),
-                              args, 0, stream));
+    const void* kfn = (c && c->pack_unroll == 8) ? (const void*)batched_copy_kernel<8> : (const void*)batched_copy_kernel<4>;
+    CUDA_TRY(cudaLaunchKernel(kfn, dim3((unsigned)nb), dim3(THREADS), args, 0, stream));
     if (c) c->launches += 1;
   }
   return CM_OK;
@@ -1195,6 +1199,8 @@ int cm_comm_set_param(cm_comm_t* c, const char* key, int64_t value) {
   else if (k == "overlap") c->overlap = value > 1 ? 1 : 0;
   else if (k == "overlap_chunks") c->ovl_chunks = (int)std::min<int64_t>(value, 1 << 20);
   else if (k == "ws") c->ws = value > 1 ? 1 : 0;
+  else if (k == "pack_waves") c->pack_waves = (int)std::min<int64_t>(value, 64);
+  else if (k == "pack_unroll") c->pack_unroll = value >= 8 ? 8 : 4;
   else if (k == "host_chunk_kb") c->host_chunk = std::max<int64_t>(64, value) * 1024;
   else if (k == "bulk_stage_kb") c->bulk_stage = (int)std::max<int64_t>(4, std::min<int64_t>(value, 112)) * 1024;
   else if (k == "oneshot_bytes_per_cta") c->oneshot_bytes_per_cta = value;
@@ -1222,6 +1228,8 @@ int cm_comm_get_param(cm_comm_t* c, const char* key, int64_t* value) {
   else if (k == "overlap") *value = c->overlap ? 2 : 1;
   else if (k == "overlap_chunks") *value = c->ovl_chunks;
   else if (k == "ws") *value = c->ws ? 2 : 1;
+  else if (k == "pack_waves") *value = c->pack_waves;
+  else if (k == "pack_unroll") *value = c->pack_unroll;
   else if (k == "auto_published") *value = c->auto_published;
   else if (k == "auto_mapped") *value = c->auto_mapped;
   else if (k == "auto_zero_copy_calls") *value = c->auto_zc_calls;

@@ -125,7 +125,9 @@ struct CopyParams {
   long long staging_off;
 };
 
-static __global__ void __launch_bounds__(THREADS) batched_copy_kernel(const __grid_constant__ CopyParams P) {
+// U: 16-byte loads in flight per thread (all issued before the stores)
+template <int U>
+__global__ void __launch_bounds__(THREADS) batched_copy_kernel(const __grid_constant__ CopyParams P) {
   const long long total = P.start[P.n];
   const int b = blockIdx.x, nb = gridDim.x, tid = threadIdx.x;
   long long lo = (long long)(((__int128)total * b) / nb) & ~15ll;
@@ -152,9 +154,12 @@ static __global__ void __launch_bounds__(THREADS) batched_copy_kernel(const __gr
       const uint4* s4 = reinterpret_cast<const uint4*>(s);
       uint4* d4 = reinterpret_cast<uint4*>(d);
       long long j = tid;
-      for (; j + 3 * THREADS < nv; j += 4 * THREADS) {
-        uint4 r0 = s4[j], r1 = s4[j + THREADS], r2 = s4[j + 2 * THREADS], r3 = s4[j + 3 * THREADS];
-        d4[j] = r0; d4[j + THREADS] = r1; d4[j + 2 * THREADS] = r2; d4[j + 3 * THREADS] = r3;
+      for (; j + (U - 1) * THREADS < nv; j += U * THREADS) {
+        uint4 r[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) r[u] = s4[j + u * THREADS];
+#pragma unroll
+        for (int u = 0; u < U; ++u) d4[j + u * THREADS] = r[u];
       }
       for (; j < nv; j += THREADS) d4[j] = s4[j];
       for (long long t = (nv << 4) + tid; t < nbytes; t += THREADS) d[t] = s[t];
