@@ -5,7 +5,7 @@
  * (/root/reference/pkg/src/collectium/, paths below relative to it). The
  * reference is pure Python, so there is no reference FFI to bind; each entry
  * point below names the reference interface it replaces. The Python façade
- * (paper_1810_11112_b200/*.py) binds these with ctypes and keeps the
+ * (paper_1810_11112_b200/_lib.py) binds these with ctypes and keeps the
  * reference's signatures, argument meanings and exception classes.
  *
  * Conventions

@@ -27,9 +27,38 @@ INST = [(t, tl, o, ol) for t, tl in (("BF16", "bf16"), ("F32", "f32"), ("F64", "
         for o, ol in (("CM_SUM", "sum"), ("CM_MAX", "max"))]
 
 
+PYFAST_SRC = os.path.join(HERE, "csrc", "pyfast.cpp")
+
+
 def sources():
     return sorted(f for f in glob.glob(os.path.join(HERE, "csrc", "*.cu")) if not f.endswith("inst.cu")) + \
-        sorted(glob.glob(os.path.join(HERE, "csrc", "*.cpp")))
+        sorted(f for f in glob.glob(os.path.join(HERE, "csrc", "*.cpp")) if f != PYFAST_SRC)
+
+
+def pyfast_path() -> str:
+    import sysconfig
+    return os.path.join(HERE, "_cmfast" + sysconfig.get_config_var("EXT_SUFFIX"))
+
+
+def build_pyfast(verbose: bool = False) -> str:
+    """The CPython fast-call module (csrc/pyfast.cpp). It does not link
+    libcm.so: the ctypes binding hands it the entry points at import."""
+    import sysconfig
+    out = pyfast_path()
+    cmd = [os.environ.get("CXX", "g++"), "-O2", "-std=c++17", "-fPIC", "-shared", "-Wall",
+           "-I", sysconfig.get_paths()["include"], "-I", os.path.join(ROOT, "include"),
+           PYFAST_SRC, "-o", out + ".tmp"]
+    if verbose:
+        print(" ".join(cmd), file=sys.stderr)
+    subprocess.run(cmd, check=True)
+    os.replace(out + ".tmp", out)
+    return out
+
+
+def pyfast_stale() -> bool:
+    out = pyfast_path()
+    return not os.path.exists(out) or any(
+        os.path.getmtime(d) > os.path.getmtime(out) for d in (PYFAST_SRC, os.path.join(ROOT, "include", "cm.h")))
 
 
 def units():
@@ -106,3 +135,5 @@ if __name__ == "__main__":
     if args and args[0].startswith("--ptxas-log="):
         log = args.pop(0).split("=", 1)[1]
     print(build(verbose=True, extra=args, ptxas_log=log, checked=checked))
+    if not checked:
+        print(build_pyfast(verbose=True))

@@ -23,6 +23,24 @@ if not os.path.exists(LIB_PATH):
 
 lib = C.CDLL(LIB_PATH)
 
+
+def _bind_fast():
+    """The CPython fast-call module (csrc/pyfast.cpp) bound to THIS library
+    instance's entry points; None when it is not built (the ctypes calls are
+    then used — same library, only the per-call argument conversion differs)."""
+    try:
+        from . import _cmfast
+    except ImportError:
+        return None
+    addr = [C.cast(getattr(lib, n), C.c_void_p).value for n in (
+        "cm_allreduce", "cm_reduce_scatter", "cm_allgather", "cm_fused_allreduce_agreed", "cm_comm_poll",
+        "cm_comm_sync")]
+    _cmfast.bind(*addr)
+    return _cmfast
+
+
+fast = None if os.environ.get("CM_NO_FAST") else _bind_fast()
+
 # enums (cm.h)
 CM_OK = 0
 DTYPE = {"float32": 0, "float64": 1, "bfloat16": 2, "int32": 3, "int64": 4}

@@ -14,6 +14,7 @@ fused output buffer, as the reference returns slices of the mean
 
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import hashlib
 from dataclasses import dataclass, field
@@ -197,6 +198,9 @@ class _Plan:
                 ptrs=L.ptr_array([t.payload.data_ptr() for t in run]),
                 counts_c=L.i64_array(counts), n=len(run),
                 stats=(L.Stats * len(run))()))
+            r = self.runs[-1]       # plain addresses for the fast-call path
+            r["addr"] = (C.addressof(r["ptrs"]), C.addressof(r["counts_c"]),
+                         C.addressof(reg) if reg is not None else 0, C.addressof(r["stats"]))
             i = j
         self.ready = ready
 
@@ -263,6 +267,14 @@ def register_gradients(grads: GradientSet, transport: Communicator) -> None:
     grads.__dict__.pop("_plans", None)
 
 
+def _device_of(tp):
+    """torch's current device for the bucket allocations (a no-op context
+    when it already is the communicator's)."""
+    if torch.cuda.current_device() == tp.device.index:
+        return contextlib.nullcontext()
+    return torch.cuda.device(tp.device)
+
+
 def _aggregate_names(grads, names, tp, algo, cfg, sw, registry, handles, stats_out, out, agree):
     if not names:
         return GradientSet((), grads.iteration)
@@ -289,7 +301,8 @@ def _aggregate_names(grads, names, tp, algo, cfg, sw, registry, handles, stats_o
     result: list[Tensor] = []
     bufs = []
     stream = tp._stream()
-    with torch.cuda.device(tp.device):
+    fast = L.fast
+    with _device_of(tp):
         for ri, run in enumerate(plan.runs):
             dtype = run["dtype"]
             if reuse is not None:
@@ -301,17 +314,26 @@ def _aggregate_names(grads, names, tp, algo, cfg, sw, registry, handles, stats_o
                 fused = torch.empty(run["total"], dtype=DTYPES[dtype], pin_memory=True)
             else:
                 fused = torch.empty(run["total"], dtype=DTYPES[dtype], device=tp.device)
-            ncalls = C.c_int()
-            agreed = C.c_int(1)
-            L.check(L.lib.cm_fused_allreduce_agreed(
-                tp._h, run["n"], run["ptrs"], run["counts_c"], L.DTYPE[dtype], fused.data_ptr(),
-                L.ALGO[algo], int(cfg.threshold_bytes), sw, 1, agree, 2 if agree is not None else 0,
-                C.byref(agreed), run["reg"], stream, run["stats"], C.byref(ncalls)))
-            if not agreed.value:
+            if fast is not None:
+                pa, ca, ra, sa = run["addr"]
+                status, ok, ncalls = fast.fused(
+                    tp._hv, run["n"], pa, ca, L.DTYPE[dtype], fused.data_ptr(), L.ALGO[algo],
+                    int(cfg.threshold_bytes), sw, 1, C.addressof(agree) if agree is not None else 0,
+                    2 if agree is not None else 0, ra, stream, sa)
+                if status:
+                    L.check(status)
+            else:
+                nc, ag = C.c_int(), C.c_int(1)
+                L.check(L.lib.cm_fused_allreduce_agreed(
+                    tp._h, run["n"], run["ptrs"], run["counts_c"], L.DTYPE[dtype], fused.data_ptr(),
+                    L.ALGO[algo], int(cfg.threshold_bytes), sw, 1, agree, 2 if agree is not None else 0,
+                    C.byref(ag), run["reg"], stream, run["stats"], C.byref(nc)))
+                ok, ncalls = ag.value, nc.value
+            if not ok:
                 return None             # nothing was launched
             agree = None
             if stats_out is not None:
-                stats_out.extend(_stats(run["stats"][k]) for k in range(ncalls.value))
+                stats_out.extend(_stats(run["stats"][k]) for k in range(ncalls))
             bufs.append(fused)
             if refill:
                 continue

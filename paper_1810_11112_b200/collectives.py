@@ -78,28 +78,44 @@ def _finish(tp: Communicator, out: torch.Tensor) -> None:
         tp.poll()
 
 
+def _run(fast_fn, ctypes_fn, args) -> CollectiveStats:
+    """One entry-point call: through the CPython fast-call module when it is
+    built (integers in, (status, rounds, messages, bytes) out), else ctypes."""
+    if L.fast is not None:
+        status, r, m, b = fast_fn(*args)
+        if status:
+            L.check(status)
+        return CollectiveStats(r, m, b)
+    st = L.Stats()
+    L.check(ctypes_fn(*args, C.byref(st)))
+    return _stats(st)
+
+
 def allreduce(t: Tensor, op: ReduceOp, group: GroupSpec, transport: Communicator,
               algo: str = "auto", switch_bytes: int | None = DEFAULT_SWITCH_BYTES,
               out: torch.Tensor | None = None, average: bool = False
               ) -> tuple[Tensor, CollectiveStats]:
     """Allreduce ``t`` over the group; returns a NEW tensor (or ``out``) and
     the reference CollectiveStats of the resolved algorithm."""
-    _check_call(group, transport)
     tp = transport
-    sw = _switch(switch_bytes, tp.size)
-    if algo not in L.ALGO:
+    if group.size != tp.size:
+        _check_call(group, tp)
+    sw = switch_bytes if type(switch_bytes) is int else _switch(switch_bytes, tp.size)
+    a = L.ALGO.get(algo)
+    if a is None:
         raise ConfigError(f"unknown algorithm {algo!r}")
-    res = _out_like(t) if out is None else out
-    if res.numel() != t.len or res.dtype != t.payload.dtype:
-        raise ShapeError("output buffer does not match the input")
-    st = L.Stats()
-    dev = t.payload.device if t.is_cuda else tp.device
-    with torch.cuda.device(dev):
-        L.check(L.lib.cm_allreduce(tp._h, t.payload.data_ptr(), res.data_ptr(), t.len,
-                                   L.DTYPE[t.dtype], L.OP[op.value], L.ALGO[algo], sw,
-                                   1 if average else 0, tp._stream(), C.byref(st)))
+    x = t.payload
+    if out is None:
+        res = torch.empty_like(x)
+    else:
+        res = out
+        if res.numel() != x.shape[0] or res.dtype != x.dtype:
+            raise ShapeError("output buffer does not match the input")
+    st = _run(L.fast.allreduce if L.fast is not None else None, L.lib.cm_allreduce,
+              (tp._hv if L.fast is not None else tp._h, x.data_ptr(), res.data_ptr(), x.shape[0],
+               L.DTYPE[t.dtype], L.OP[op.value], a, sw, 1 if average else 0, tp._stream()))
     _finish(tp, res)
-    return Tensor(t.name, t.dtype, res), _stats(st)
+    return Tensor._wrap(t.name, t.dtype, res), st
 
 
 def allreduce_ring(t: Tensor, op: ReduceOp, group: GroupSpec,
@@ -131,14 +147,11 @@ def reduce_scatter(t: Tensor, op: ReduceOp, group: GroupSpec, transport: Communi
     from .core import layout as _layout
     off, ln = _layout(layout, t.len, tp.size)[tp.rank]
     res = torch.empty(ln, dtype=t.payload.dtype, device=t.payload.device)
-    st = L.Stats()
-    dev = t.payload.device if t.is_cuda else tp.device
-    with torch.cuda.device(dev):
-        L.check(L.lib.cm_reduce_scatter(tp._h, t.payload.data_ptr(), res.data_ptr(), t.len,
-                                        L.DTYPE[t.dtype], L.OP[op.value], L.LAYOUT[layout],
-                                        tp._stream(), C.byref(st)))
+    st = _run(L.fast.reduce_scatter if L.fast is not None else None, L.lib.cm_reduce_scatter,
+              (tp._hv if L.fast is not None else tp._h, t.payload.data_ptr(), res.data_ptr(), t.len,
+               L.DTYPE[t.dtype], L.OP[op.value], L.LAYOUT[layout], tp._stream()))
     _finish(tp, res)
-    return Tensor(t.name, t.dtype, res), _stats(st)
+    return Tensor._wrap(t.name, t.dtype, res), st
 
 
 def allgather(t: Tensor, n: int, group: GroupSpec, transport: Communicator,
@@ -153,13 +166,11 @@ def allgather(t: Tensor, n: int, group: GroupSpec, transport: Communicator,
     if t.len != ln:
         raise ShapeError(f"rank {tp.rank} owns {ln} elements of the {layout} layout, got {t.len}")
     res = torch.empty(n, dtype=t.payload.dtype, device=t.payload.device)
-    st = L.Stats()
-    dev = t.payload.device if t.is_cuda else tp.device
-    with torch.cuda.device(dev):
-        L.check(L.lib.cm_allgather(tp._h, t.payload.data_ptr(), res.data_ptr(), n,
-                                   L.DTYPE[t.dtype], L.LAYOUT[layout], tp._stream(), C.byref(st)))
+    st = _run(L.fast.allgather if L.fast is not None else None, L.lib.cm_allgather,
+              (tp._hv if L.fast is not None else tp._h, t.payload.data_ptr(), res.data_ptr(), n,
+               L.DTYPE[t.dtype], L.LAYOUT[layout], tp._stream()))
     _finish(tp, res)
-    return Tensor(t.name, t.dtype, res), _stats(st)
+    return Tensor._wrap(t.name, t.dtype, res), st
 
 
 # -- single-GPU group emulation -------------------------------------------------

@@ -26,11 +26,15 @@ DEFAULT_STAGING_BYTES = int(os.environ.get("CM_STAGING_BYTES", 1 << 30))
 DEFAULT_POOL_BYTES = int(os.environ.get("CM_POOL_BYTES", 1 << 30))
 
 
+_raw_stream = torch._C._cuda_getCurrentRawStream
+
+
 class _Base:
     _h: C.c_void_p | None = None
+    _hv: int | None = None            # the handle as a plain int (fast-call path)
 
     def _stream(self) -> int:
-        return torch.cuda.current_stream(self.device).cuda_stream
+        return _raw_stream(self.device.index)
 
     # -- tuning / policy ------------------------------------------------------
     def set_param(self, key: str, value: int) -> None:
@@ -74,10 +78,17 @@ class _Base:
     def synchronize(self) -> None:
         """Wait for this rank's stream; raise any device-side error
         (ShapeError for mismatched peers, TransportError on timeout)."""
-        L.check(L.lib.cm_comm_sync(self._h, self._stream()))
+        if L.fast is not None:
+            st = L.fast.sync(self._hv, self._stream())
+        else:
+            st = L.lib.cm_comm_sync(self._h, self._stream())
+        if st:
+            L.check(st)
 
     def poll(self) -> None:
-        L.check(L.lib.cm_comm_poll(self._h))
+        st = L.fast.poll(self._hv) if L.fast is not None else L.lib.cm_comm_poll(self._h)
+        if st:
+            L.check(st)
 
     def _counters(self):
         m, b, nv, c = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
@@ -110,6 +121,7 @@ class _Base:
         if self._h is not None:
             L.lib.cm_comm_destroy(self._h)
             self._h = None
+            self._hv = None
 
     def __del__(self):  # pragma: no cover - best effort
         try:
@@ -154,7 +166,7 @@ class Communicator(_Base):
         torch.cuda.set_device(self.device)
         L.check(L.lib.cm_comm_create(self.rank, self.size, self.device.index, int(staging_bytes),
                                      int(pool_bytes), C.byref(h)))
-        self._h = h
+        self._h, self._hv = h, h.value
         if self.size > 1:
             buf = (C.c_char * L.IPC_HANDLE_BYTES)()
             L.check(L.lib.cm_comm_ipc_handle(self._h, buf))
@@ -263,7 +275,7 @@ class VirtualGroup(_Base):
         h = C.c_void_p()
         torch.cuda.set_device(self.device)
         L.check(L.lib.cm_comm_create_virtual(self.size, dev, int(staging_bytes), C.byref(h)))
-        self._h = h
+        self._h, self._hv = h, h.value
         if timeout_s is not None:
             self.set_timeout(timeout_s)
 

@@ -145,6 +145,21 @@ int cuda_fail(cudaError_t e, const char* what) {
     if (_e != cudaSuccess) return cuda_fail(_e, #expr); \
   } while (0)
 
+// The communicator's device for the duration of one entry point (restored
+// after), so callers need not switch devices around every collective.
+struct DeviceScope {
+  int prev = -1;
+  explicit DeviceScope(int dev) {
+    int cur = -1;
+    if (cudaGetDevice(&cur) == cudaSuccess && cur != dev && cudaSetDevice(dev) == cudaSuccess) prev = cur;
+  }
+  ~DeviceScope() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  DeviceScope(const DeviceScope&) = delete;
+  DeviceScope& operator=(const DeviceScope&) = delete;
+};
+
 size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 // LL payload capacity per source: 2 MiB on real communicators (two-shot LL up
@@ -1550,6 +1565,7 @@ int cm_comm_profile_read(cm_comm_t* c, int kind, int64_t* launches, double* tota
 int cm_allreduce(cm_comm_t* c, const void* send, void* recv, int64_t count, int dtype, int op,
                  int algo, int64_t switch_bytes, int average, void* stream, cm_stats_t* stats) {
   if (c->virt) return fail(CM_ERR_UNSUPPORTED, "use cm_allreduce_v on a virtual group");
+  DeviceScope ds(c->device);
   return do_allreduce(c, &send, &recv, count, dtype, op, algo, switch_bytes, average, stream, stats);
 }
 
@@ -1557,30 +1573,35 @@ int cm_allreduce_v(cm_comm_t* c, const void* const* sends, void* const* recvs, i
                    int dtype, int op, int algo, int64_t switch_bytes, int average, void* stream,
                    cm_stats_t* stats) {
   if (!c->virt) return fail(CM_ERR_UNSUPPORTED, "cm_allreduce_v needs a virtual group");
+  DeviceScope ds(c->device);
   return do_allreduce(c, sends, recvs, count, dtype, op, algo, switch_bytes, average, stream, stats);
 }
 
 int cm_reduce_scatter(cm_comm_t* c, const void* send, void* recv, int64_t count, int dtype, int op,
                       int layout, void* stream, cm_stats_t* stats) {
   if (c->virt) return fail(CM_ERR_UNSUPPORTED, "use cm_reduce_scatter_v on a virtual group");
+  DeviceScope ds(c->device);
   return do_rs(c, &send, &recv, count, dtype, op, layout, stream, stats);
 }
 
 int cm_reduce_scatter_v(cm_comm_t* c, const void* const* sends, void* const* recvs, int64_t count,
                         int dtype, int op, int layout, void* stream, cm_stats_t* stats) {
   if (!c->virt) return fail(CM_ERR_UNSUPPORTED, "needs a virtual group");
+  DeviceScope ds(c->device);
   return do_rs(c, sends, recvs, count, dtype, op, layout, stream, stats);
 }
 
 int cm_allgather(cm_comm_t* c, const void* send, void* recv, int64_t count, int dtype, int layout,
                  void* stream, cm_stats_t* stats) {
   if (c->virt) return fail(CM_ERR_UNSUPPORTED, "use cm_allgather_v on a virtual group");
+  DeviceScope ds(c->device);
   return do_ag(c, &send, &recv, count, dtype, layout, stream, stats);
 }
 
 int cm_allgather_v(cm_comm_t* c, const void* const* sends, void* const* recvs, int64_t count,
                    int dtype, int layout, void* stream, cm_stats_t* stats) {
   if (!c->virt) return fail(CM_ERR_UNSUPPORTED, "needs a virtual group");
+  DeviceScope ds(c->device);
   return do_ag(c, sends, recvs, count, dtype, layout, stream, stats);
 }
 
@@ -1943,6 +1964,7 @@ int cm_fused_allreduce_agreed(cm_comm_t* c, int n, const void* const* sends,
                               const int64_t* reg_ids, void* stream, cm_stats_t* stats,
                               int* n_calls) {
   if (c->virt) return fail(CM_ERR_UNSUPPORTED, "use cm_fused_allreduce_agreed_v on a virtual group");
+  DeviceScope ds(c->device);
   void* rv[1] = {recv_fused};
   return fused_impl(c, n, sends, counts, dtype, rv, algo, threshold, switch_bytes, average, agree_values,
                     n_agree, agreed, reg_ids, static_cast<cudaStream_t>(stream), stats, n_calls);
@@ -1954,6 +1976,7 @@ int cm_fused_allreduce_agreed_v(cm_comm_t* c, int n, const void* const* sends, c
                                 int* agreed, const int64_t* reg_ids, void* stream, cm_stats_t* stats,
                                 int* n_calls) {
   if (!c->virt) return fail(CM_ERR_UNSUPPORTED, "cm_fused_allreduce_agreed_v needs a virtual group");
+  DeviceScope ds(c->device);
   return fused_impl(c, n, sends, counts, dtype, recvs_fused, algo, threshold, switch_bytes, average,
                     agree_values, n_agree, agreed, reg_ids, static_cast<cudaStream_t>(stream), stats, n_calls);
 }

@@ -32,6 +32,22 @@ def test_library_exports_every_header_symbol():
     assert b"sm_100a" in L.lib.cm_version()
 
 
+def test_fast_call_module_is_bound_to_the_loaded_library():
+    """csrc/pyfast.cpp: built next to libcm.so and bound to the entry points
+    of the same library instance; argument errors raise, not crash."""
+    if os.environ.get("CM_NO_FAST"):
+        pytest.skip("fast-call path disabled")
+    assert L.fast is not None, "the _cmfast module is not built (python paper_1810_11112_b200/_build.py)"
+    with pytest.raises(TypeError):
+        L.fast.allreduce(1, 2, 3)
+    with pytest.raises(TypeError):
+        L.fast.fused(*range(14))
+    with pytest.raises(TypeError):
+        L.fast.sync(0)
+    with pytest.raises(OverflowError):
+        L.fast.allreduce(-1, 0, 0, 0, 0, 0, 0, 0, 0, 0)
+
+
 def test_library_is_sm100a_build():
     import subprocess
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", L.LIB_PATH],
