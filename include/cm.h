@@ -347,10 +347,13 @@ int cm_local_reduce(const void* a, const void* b, void* out, int64_t count, int 
  * kernel cannot dereference) are moved by the copy engines instead */
 int cm_batched_copy(int n, const void* const* srcs, void* const* dsts, const int64_t* nbytes,
                     void* stream);
-/* diagnostics: all-to-all NVLink bandwidth, mode 0 = every rank pulls `bytes`
- * from each peer, 1 = every rank pushes `bytes` to each peer; ms per round.
+/* diagnostics: all-to-all NVLink bandwidth, every rank moving `bytes` to or
+ * from each peer per round (ms per round): 2 = SM pull (all peers
+ * concurrently), 3 = SM push, 4 = TMA bulk pull, 5 = pull + local add,
+ * 6..9 = two-rank store anatomy, 14 = copy-engine pull, 15 = copy-engine push
+ * (cudaMemcpyAsync over the IPC mappings, one stream per peer).
  * Flag latency: mode 10 = ping-pong between ranks 0 and 1 (one thread),
- * mode 11 = the start-barrier pattern on `ctas` CTAs; `bytes` = iterations
+ * 11..13 = the start-barrier pattern on `ctas` CTAs; `bytes` = iterations
  * per launch, ms_per_iter = time per launch (divide by the iterations) */
 int cm_bench_p2p(cm_comm_t* comm, int mode, int64_t bytes, int ctas, int iters, void* stream,
                  double* ms_per_iter);

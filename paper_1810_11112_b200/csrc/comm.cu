@@ -2185,9 +2185,40 @@ int cm_bench_p2p(cm_comm_t* c, int mode, int64_t bytes, int ctas, int iters, voi
     }
     B.n = m;
   }
+  // modes 14/15: copy engines (cudaMemcpyAsync over the IPC mappings), one
+  // stream per peer so the p-1 transfers run concurrently; 14 pulls, 15 pushes
+  std::vector<cudaStream_t> ce_s;
+  std::vector<cudaEvent_t> ce_e;
+  cudaEvent_t fork = nullptr;
+  if (mode == 14 || mode == 15) {
+    CUDA_TRY(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    for (int i = 1; i < c->size; ++i) {
+      cudaStream_t t;
+      cudaEvent_t e;
+      CUDA_TRY(cudaStreamCreateWithFlags(&t, cudaStreamNonBlocking));
+      CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      ce_s.push_back(t);
+      ce_e.push_back(e);
+    }
+  }
   static unsigned long long flag_base = 1ull << 40;   // slot values only grow (same sequence on every rank)
   auto launch = [&]() {
-    if (mode == 4) bulk_copy_kernel<<<ctas, BULK_THREADS, BULK_SMEM, s>>>(B);
+    if (mode == 14 || mode == 15) {
+      cudaEventRecord(fork, s);
+      for (int i = 1; i < c->size; ++i) {
+        const int q = (c->rank + i) % c->size;
+        cudaStream_t t = ce_s[i - 1];
+        cudaStreamWaitEvent(t, fork, 0);
+        if (mode == 14)
+          cudaMemcpyAsync(c->local + c->staging_off + (int64_t)q * bytes,
+                          c->heap[q] + c->staging_off + (int64_t)c->rank * bytes, bytes, cudaMemcpyDeviceToDevice, t);
+        else
+          cudaMemcpyAsync(c->heap[q] + c->staging_off + (int64_t)c->rank * bytes,
+                          c->local + c->staging_off + (int64_t)q * bytes, bytes, cudaMemcpyDeviceToDevice, t);
+        cudaEventRecord(ce_e[i - 1], t);
+        cudaStreamWaitEvent(s, ce_e[i - 1], 0);
+      }
+    } else if (mode == 4) bulk_copy_kernel<<<ctas, BULK_THREADS, BULK_SMEM, s>>>(B);
     else if (mode >= 10 && mode <= 13) {
       flag_latency_kernel<<<mode == 10 ? 1 : ctas, THREADS, 0, s>>>(P, mode, bytes, flag_base);
       flag_base += (unsigned long long)bytes + 1;
@@ -2202,6 +2233,9 @@ int cm_bench_p2p(cm_comm_t* c, int mode, int64_t bytes, int ctas, int iters, voi
   cudaEventElapsedTime(&ms, e0, e1);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
+  for (auto t : ce_s) cudaStreamDestroy(t);
+  for (auto e : ce_e) cudaEventDestroy(e);
+  if (fork) cudaEventDestroy(fork);
   *ms_per_iter = ms / iters;
   return CM_OK;
 }

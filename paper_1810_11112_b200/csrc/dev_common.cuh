@@ -380,13 +380,28 @@ __device__ __forceinline__ void rec_put(char* slot, unsigned tag, const long lon
     st_ll(slot + u * 16, (unsigned)(unsigned long long)v[u], (unsigned)((unsigned long long)v[u] >> 32), tag);
 }
 
+// All units are loaded back to back (independent loads, one L2 round trip per
+// poll instead of one per unit) and the record is taken once every unit
+// carries the tag.
 __device__ __forceinline__ bool rec_get(const char* slot, unsigned tag, long long (&v)[REC_UNITS], int nunits,
                                         unsigned long long timeout) {
-  for (int u = 0; u < nunits; ++u) {
-    uint4 x;
-    if (!ll_wait(slot + u * 16, tag, timeout, &x)) return false;
-    v[u] = (long long)(((unsigned long long)x.z << 32) | x.x);
+  uint4 x[REC_UNITS];
+  long long t0 = -1;
+  while (true) {
+#pragma unroll
+    for (int u = 0; u < REC_UNITS; ++u)
+      if (u < nunits) x[u] = ld_ll(slot + u * 16);
+    bool ok = true;
+#pragma unroll
+    for (int u = 0; u < REC_UNITS; ++u)
+      if (u < nunits) ok = ok && x[u].y == tag && x[u].w == tag;
+    if (ok) break;
+    if (t0 < 0) t0 = clock64();
+    else if ((unsigned long long)(clock64() - t0) > timeout) return false;
   }
+#pragma unroll
+  for (int u = 0; u < REC_UNITS; ++u)
+    if (u < nunits) v[u] = (long long)(((unsigned long long)x[u].z << 32) | x[u].x);
   return true;
 }
 

@@ -42,8 +42,8 @@ class UniqueId(C.Structure):
 
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--min", type=int, default=4)
-ap.add_argument("--max", type=int, default=1 << 30)
+ap.add_argument("--min-bytes", type=int, default=4)
+ap.add_argument("--max-bytes", type=int, default=1 << 30)
 ap.add_argument("--out", default=None)
 args = ap.parse_args()
 rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
@@ -61,8 +61,8 @@ dist.broadcast_object_list(obj, src=0)
 C.memmove(uid.internal, obj[0], 128)
 ncomm = C.c_void_p()
 assert nccl.ncclCommInitRank(C.byref(ncomm), world, uid, rank) == 0
-comm = P.Communicator(staging_bytes=max(64 << 20, args.max + (8 << 20)), pool_bytes=16 << 20, blocking=False)
-maxn = args.max // 4
+comm = P.Communicator(staging_bytes=max(64 << 20, args.max_bytes + (8 << 20)), pool_bytes=16 << 20, blocking=False)
+maxn = args.max_bytes // 4
 x = torch.randn(maxn, device="cuda")
 y = torch.empty_like(x)
 st = L.Stats()
@@ -104,8 +104,8 @@ def timed(fn, iters, graph):
     return e0.elapsed_time(e1) / iters * 1e3, host
 
 
-nbytes = args.min
-while nbytes <= args.max:
+nbytes = args.min_bytes
+while nbytes <= args.max_bytes:
     n = max(1, nbytes // 4)
     iters = 200 if nbytes <= (1 << 20) else (40 if nbytes <= (64 << 20) else 8)
     for _ in range(10):              # mapping of the automatically registered buffers settles first

@@ -14,14 +14,15 @@ import paper_1810_11112_b200 as P  # noqa: E402
 from paper_1810_11112_b200 import _lib as L  # noqa: E402
 
 rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
-torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
+torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)) % torch.cuda.device_count())
 dist.init_process_group("gloo")
 comm = P.Communicator(staging_bytes=int(os.environ.get("STAGING", 1 << 30)), pool_bytes=2 << 20, blocking=False)
 SIZES = [int(x) for x in os.environ.get("SIZES", str(64 << 20)).split(",")]
 for ctas in [int(x) for x in os.environ.get("CTAS", "148,296").split(",")]:
     names = {2: "pull-concurrent", 3: "push-concurrent", 4: "pull-TMA-bulk", 5: "pull+local-add (RS-like)",
              6: "p2-anatomy remote-only 1 store", 7: "p2-anatomy remote+local 1 store",
-             8: "p2-anatomy remote+local 2 stores", 9: "p2-anatomy remote-first then local, 2 stores"}
+             8: "p2-anatomy remote+local 2 stores", 9: "p2-anatomy remote-first then local, 2 stores",
+             14: "copy-engine pull", 15: "copy-engine push"}
     for mode in [int(x) for x in os.environ.get("MODES", "2,4,5,3").split(",")]:
         name = names[mode]
         for nb in SIZES:

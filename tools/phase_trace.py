@@ -84,6 +84,13 @@ for it in range(a.iters + 3):
     for k in range(6):
         col = t[:, k][t[:, k] > 0]
         skew[k] += float(col.max() - t[:, 0].min()) / 1e3 if len(col) else 0.0
+row = [v / a.iters for v in acc] + [tot / a.iters]
+rows = [None] * world
+dist.all_gather_object(rows, row)
+if rank == 0 and world > 1:
+    for r, rw in enumerate(rows):
+        print(f"  rank {r}: span {rw[5]:.2f} | " + " ".join(f"{ph} {v:.2f}" for ph, v in zip(phases, rw[:5])),
+              flush=True)
 if rank == 0:
     what = "C5 aggregate (registered, 2 fused groups)" if a.agg else f"bytes={a.bytes} algo={a.algo} zc={a.zc}"
     print(f"p={world} {what} ctas={int(used.sum())} "
