@@ -205,6 +205,11 @@ int cm_comm_registry(cm_comm_t* comm, cm_registry_t** reg);
  *                         peers map it when their kernels report the new slot
  *                         and acknowledge in this heap; from then on peers read
  *                         the buffer in place (no copy into staging). 1 = off.
+ *   "pdl"                 2 = (default) collective, low-latency, RHD and pack
+ *                         kernels are launched with programmatic stream
+ *                         serialization: the next launch is scheduled while the
+ *                         previous kernel drains and waits in griddepcontrol.wait
+ *                         (device gap between launches 2.5 -> 0.6 us); 1 = off.
  * get also reads the counters "auto_published", "auto_mapped",
  * "auto_zero_copy_calls" and "auto_buffer_checks" (allocation-id re-checks)
  * get also reads "staging_bytes", "pool_bytes" and "ll_payload_per_source" */

@@ -112,6 +112,7 @@ struct cm_comm {
   int ws = 0;                                 // multi-buffer two-shot: RS and AG warps in every CTA
   int pack_waves = 2;                         // batched copy: CTA waves (4 per SM per wave)
   int pack_unroll = 4;                        // batched copy: 16-byte loads in flight per thread (4 or 8)
+  bool pdl = true;                            // programmatic dependent launch of the collective kernels
   int bulk_stage = 2 * RS_STAGE_BYTES;        // bytes per bulk-reduce stage (64 KiB: 3 stages fit)
   int64_t host_chunk = 8 << 20;               // host-gradient pipeline: bytes per H2D/D2H piece (p = 1)
   int64_t oneshot_bytes_per_cta = 8 * 1024;
@@ -161,6 +162,23 @@ struct DeviceScope {
 };
 
 size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Launch with programmatic stream serialization (the kernel starts with
+// pdl_begin(): it waits for the preceding grid itself), or plainly.
+cudaError_t launch_k(bool pdl, const void* k, dim3 grid, dim3 block, void** args, size_t smem, cudaStream_t s) {
+  if (!pdl) return cudaLaunchKernel(k, grid, block, args, smem, s);
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelExC(&cfg, k, args);
+}
 
 // LL payload capacity per source: 2 MiB on real communicators (two-shot LL up
 // to p x 2 MiB), 256 KiB per virtual rank (single-GPU emulation)
@@ -496,7 +514,7 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
     P.nrs = (int)(nb / 2);
     P.ovl_chunks = c->ovl_chunks;
     P.ws = (multi && c->ws && bulk && !ovl && !c->dyn_ag) ? 1 : 0;
-    CUDA_TRY(cudaLaunchKernel((const void*)k, dim3((unsigned)nb), dim3(THREADS), args, dsm, stream));
+    CUDA_TRY(launch_k(c->pdl, (const void*)k, dim3((unsigned)nb), dim3(THREADS), args, dsm, stream));
   }
   c->launches += 1;
   // real bytes pulled over NVLink by this rank
@@ -929,8 +947,8 @@ int launch_batched_copy(cm_comm* c, int n, const void* const* srcs, void* const*
       nb = std::max<int64_t>(1, std::min<int64_t>(nb, 2 * (int64_t)sms));
       void* args[] = {&P};
       ProfScope prof_scope(c, stream, 1, 2 * P.start[m]);
-      CUDA_TRY(cudaLaunchKernel((const void*)bulk_copy_kernel, dim3((unsigned)nb), dim3(BULK_THREADS), args,
-                                BULK_SMEM, stream));
+      CUDA_TRY(launch_k(c ? c->pdl : true, (const void*)bulk_copy_kernel, dim3((unsigned)nb), dim3(BULK_THREADS),
+                        args, BULK_SMEM, stream));
       if (c) c->launches += 1;
       continue;
     }
@@ -942,7 +960,7 @@ int launch_batched_copy(cm_comm* c, int n, const void* const* srcs, void* const*
     void* args[] = {&P};
     ProfScope prof_scope(c, stream, 1, 2 * P.start[m]);
     const void* kfn = (c && c->pack_unroll == 8) ? (const void*)batched_copy_kernel<8> : (const void*)batched_copy_kernel<4>;
-    CUDA_TRY(cudaLaunchKernel(kfn, dim3((unsigned)nb), dim3(THREADS), args, 0, stream));
+    CUDA_TRY(launch_k(c ? c->pdl : true, kfn, dim3((unsigned)nb), dim3(THREADS), args, 0, stream));
     if (c) c->launches += 1;
   }
   return CM_OK;
@@ -1216,6 +1234,7 @@ int cm_comm_set_param(cm_comm_t* c, const char* key, int64_t value) {
   else if (k == "ws") c->ws = value > 1 ? 1 : 0;
   else if (k == "pack_waves") c->pack_waves = (int)std::min<int64_t>(value, 64);
   else if (k == "pack_unroll") c->pack_unroll = value >= 8 ? 8 : 4;
+  else if (k == "pdl") c->pdl = value > 1;
   else if (k == "host_chunk_kb") c->host_chunk = std::max<int64_t>(64, value) * 1024;
   else if (k == "bulk_stage_kb") c->bulk_stage = (int)std::max<int64_t>(4, std::min<int64_t>(value, 112)) * 1024;
   else if (k == "oneshot_bytes_per_cta") c->oneshot_bytes_per_cta = value;
@@ -1245,6 +1264,7 @@ int cm_comm_get_param(cm_comm_t* c, const char* key, int64_t* value) {
   else if (k == "ws") *value = c->ws ? 2 : 1;
   else if (k == "pack_waves") *value = c->pack_waves;
   else if (k == "pack_unroll") *value = c->pack_unroll;
+  else if (k == "pdl") *value = c->pdl ? 2 : 1;
   else if (k == "auto_published") *value = c->auto_published;
   else if (k == "auto_mapped") *value = c->auto_mapped;
   else if (k == "auto_zero_copy_calls") *value = c->auto_zc_calls;
@@ -2201,6 +2221,15 @@ int cm_bench_p2p(cm_comm_t* c, int mode, int64_t bytes, int ctas, int iters, voi
       ce_e.push_back(e);
     }
   }
+  if (mode == 17)
+    CUDA_TRY(cudaFuncSetAttribute((const void*)empty_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)bytes));
+  if (mode == 20 && bytes > 0)
+    CUDA_TRY(cudaFuncSetAttribute((const void*)spin_kernel_pdl, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)bytes));
+  int spin_i = 0;   // modes 18/19: launch index (stamps at staging[2 i], [2 i + 1])
+  if (mode >= 18 && mode <= 22 && (int64_t)(iters + 1) * 16 + 65536 > (int64_t)c->staging_bytes)
+    return fail(CM_ERR_CONFIG, "too many iterations");
   static unsigned long long flag_base = 1ull << 40;   // slot values only grow (same sequence on every rank)
   auto launch = [&]() {
     if (mode == 14 || mode == 15) {
@@ -2218,6 +2247,42 @@ int cm_bench_p2p(cm_comm_t* c, int mode, int64_t bytes, int ctas, int iters, voi
         cudaEventRecord(ce_e[i - 1], t);
         cudaStreamWaitEvent(s, ce_e[i - 1], 0);
       }
+    } else if (mode == 18 || mode == 19) {
+      auto* out = reinterpret_cast<unsigned long long*>(c->local + c->staging_off);
+      if (mode == 18) spin_kernel_big<<<ctas, THREADS, 0, s>>>(P, out, spin_i, 20000);
+      else spin_kernel_small<<<ctas, THREADS, 0, s>>>(out, spin_i, 20000);
+      ++spin_i;
+    } else if (mode == 20) {
+      auto* out = reinterpret_cast<unsigned long long*>(c->local + c->staging_off);
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)ctas);
+      cfg.blockDim = dim3(THREADS);
+      cfg.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      cfg.dynamicSmemBytes = (size_t)bytes;   // > 114 KiB: one CTA per SM, the next grid cannot co-reside
+      cudaLaunchKernelEx(&cfg, spin_kernel_pdl, P, out, spin_i, (long long)20000);
+      ++spin_i;
+    } else if (mode == 21 || mode == 22) {
+      auto* out = reinterpret_cast<unsigned long long*>(c->local + c->staging_off);
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)ctas);
+      cfg.blockDim = dim3(THREADS);
+      cfg.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      cudaLaunchKernelEx(&cfg, spin_kernel_remote, P, out, spin_i, (long long)20000, mode == 22 ? 1 : 0);
+      ++spin_i;
+    } else if (mode == 16) {
+      empty_kernel<<<ctas, THREADS, 0, s>>>(0);
+    } else if (mode == 17) {
+      empty_kernel<<<ctas, THREADS, (size_t)bytes, s>>>(0);
     } else if (mode == 4) bulk_copy_kernel<<<ctas, BULK_THREADS, BULK_SMEM, s>>>(B);
     else if (mode >= 10 && mode <= 13) {
       flag_latency_kernel<<<mode == 10 ? 1 : ctas, THREADS, 0, s>>>(P, mode, bytes, flag_base);
@@ -2233,6 +2298,14 @@ int cm_bench_p2p(cm_comm_t* c, int mode, int64_t bytes, int ctas, int iters, voi
   cudaEventElapsedTime(&ms, e0, e1);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
+  if (mode >= 18 && mode <= 22) {   // median device gap between consecutive launches
+    std::vector<unsigned long long> st((size_t)2 * spin_i);
+    CUDA_TRY(cudaMemcpy(st.data(), c->local + c->staging_off, st.size() * 8, cudaMemcpyDeviceToHost));
+    std::vector<double> gaps;
+    for (int i = 1; i < spin_i; ++i) gaps.push_back((double)(st[2 * i] - st[2 * i - 1]) * 1e-6);
+    std::sort(gaps.begin(), gaps.end());
+    ms = gaps.empty() ? 0.f : (float)(gaps[gaps.size() / 2] * iters);
+  }
   for (auto t : ce_s) cudaStreamDestroy(t);
   for (auto e : ce_e) cudaEventDestroy(e);
   if (fork) cudaEventDestroy(fork);

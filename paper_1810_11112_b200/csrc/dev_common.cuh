@@ -238,6 +238,17 @@ struct CollParams {
   unsigned long long* acked;
 };
 
+// Programmatic dependent launch: the kernels of the collective path are
+// launched with programmaticStreamSerialization, so the next launch is
+// scheduled while this one drains (hides the ~2.5 us launch gap between
+// back-to-back kernels). Every thread first waits for the preceding grid to
+// complete and flush (a no-op without the attribute), then lets the next
+// launch be scheduled.
+__device__ __forceinline__ void pdl_begin() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

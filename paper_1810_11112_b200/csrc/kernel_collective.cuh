@@ -177,6 +177,7 @@ __device__ void dynamic_allgather(const CollParams& P, int rank, int nb, unsigne
 // each kernel's register footprint to its own mode.
 template <class D, int OP, int MP, bool TREE, bool STREAM, bool MULTI>
 __global__ void __launch_bounds__(THREADS, 1) collective_kernel(const __grid_constant__ CollParams P) {
+  pdl_begin();
   using S = typename D::S;
   constexpr int SZ = sizeof(S);
   const int lr = P.virt ? blockIdx.y : 0;       // index into in/out
@@ -653,6 +654,7 @@ finish:
       ctrl->epoch = e;
       __threadfence();
     }
+    CM_TRACE(P, lr, b, 6);
   }
 }
 

@@ -6,6 +6,59 @@
 
 namespace cm {
 namespace dev {
+// ---- diagnostics: launch cost of an empty kernel with a small parameter block
+// (cm_bench_p2p modes 16/17; modes 2 with 0 bytes gives the CollParams block)
+static __global__ void __launch_bounds__(THREADS) empty_kernel(int x) {
+  extern __shared__ char dyn[];
+  if (x == 12345 && threadIdx.x == 0) dyn[0] = 1;
+}
+
+// launch-to-launch gap on the device (modes 18/19): every CTA spins `ns`, CTA 0
+// stamps its start and end into out[2 i], out[2 i + 1]
+template <class Param>
+__device__ __forceinline__ void spin_body(unsigned long long* out, int i, long long ns) {
+  const unsigned long long t0 = gtimer();
+  if (blockIdx.x == 0 && threadIdx.x == 0) out[2 * i] = t0;
+  while ((long long)(gtimer() - t0) < ns) {
+  }
+  __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x == 0) out[2 * i + 1] = gtimer();
+}
+static __global__ void __launch_bounds__(THREADS) spin_kernel_big(const __grid_constant__ CollParams P,
+                                                                  unsigned long long* out, int i, long long ns) {
+  if (P.p == 12345) out[0] = 0;
+  spin_body<CollParams>(out, i, ns);
+}
+static __global__ void __launch_bounds__(THREADS) spin_kernel_small(unsigned long long* out, int i, long long ns) {
+  spin_body<int>(out, i, ns);
+}
+// mode 20: the same under programmatic dependent launch (the next launch is
+// scheduled while this one runs and waits in griddepcontrol.wait)
+static __global__ void __launch_bounds__(THREADS, 1) spin_kernel_pdl(const __grid_constant__ CollParams P,
+                                                                     unsigned long long* out, int i, long long ns) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  extern __shared__ char spin_dyn[];
+  if (P.p == 12345) { out[0] = 0; spin_dyn[threadIdx.x] = 1; }
+  spin_body<CollParams>(out, i, ns);
+}
+
+// mode 21: PDL spin kernel whose CTA 0 first stores one word into the next
+// peer's heap (a remote NVLink write in flight long before the grid ends);
+// mode 22: the same with a remote load instead
+static __global__ void __launch_bounds__(THREADS, 1) spin_kernel_remote(const __grid_constant__ CollParams P,
+                                                                        unsigned long long* out, int i, long long ns,
+                                                                        int load) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  auto* peer = reinterpret_cast<unsigned long long*>(P.heap[(P.rank + 1) % P.p] + P.staging_off) + 4096 + P.rank;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (load) out[4095] = *reinterpret_cast<volatile unsigned long long*>(peer);
+    else *reinterpret_cast<volatile unsigned long long*>(peer) = (unsigned long long)i;
+  }
+  spin_body<CollParams>(out, i, ns);
+}
+
 // ---- diagnostics: raw NVLink read / write bandwidth between all ranks --------
 // mode 0: pull — every rank reads `bytes` from each peer's staging into its own
 // mode 1: push — every rank writes `bytes` into each peer's staging
@@ -128,6 +181,7 @@ struct CopyParams {
 // U: 16-byte loads in flight per thread (all issued before the stores)
 template <int U>
 __global__ void __launch_bounds__(THREADS) batched_copy_kernel(const __grid_constant__ CopyParams P) {
+  pdl_begin();
   const long long total = P.start[P.n];
   const int b = blockIdx.x, nb = gridDim.x, tid = threadIdx.x;
   long long lo = (long long)(((__int128)total * b) / nb) & ~15ll;
@@ -187,6 +241,7 @@ constexpr int BULK_THREADS = 32;
 constexpr size_t BULK_SMEM = (size_t)BULK_STAGES * BULK_CHUNK + BULK_STAGES * 8;
 
 static __global__ void __launch_bounds__(BULK_THREADS) bulk_copy_kernel(const __grid_constant__ CopyParams P) {
+  pdl_begin();
   extern __shared__ __align__(128) unsigned char bulk_smem[];
   if (threadIdx.x != 0) return;
   unsigned long long* bar = reinterpret_cast<unsigned long long*>(bulk_smem + (size_t)BULK_STAGES * BULK_CHUNK);

@@ -21,6 +21,7 @@ __device__ __forceinline__ char* llh_slot(char* heap, int par, int blk, int src)
 
 template <class D, int OP, int MP, bool TREE>
 __global__ void __launch_bounds__(THREADS, 1) ll_kernel(const __grid_constant__ CollParams P) {
+  pdl_begin();
   using S = typename D::S;
   using A = typename D::A;
   constexpr int E = 8 / sizeof(S);                    // elements per unit
@@ -191,6 +192,7 @@ __device__ __forceinline__ void unpack_elems(char* base, long long i, int cnt, u
 
 template <class D, int OP, int MP, bool TREE>
 __global__ void __launch_bounds__(THREADS, 1) ll2_kernel(const __grid_constant__ CollParams P) {
+  pdl_begin();
   using S = typename D::S;
   using A = typename D::A;
   constexpr int E = 8 / sizeof(S);

@@ -91,6 +91,7 @@ __device__ void pair_pass(const char* a, const char* b, char* dst_raw, char* dst
 
 template <class D, int OP>
 __global__ void __launch_bounds__(THREADS, 1) rhd_kernel(const __grid_constant__ CollParams P) {
+  pdl_begin();
   const int lr = P.virt ? blockIdx.y : 0;
   const int rank = P.virt ? (int)blockIdx.y : P.rank;
   const int b = blockIdx.x, nb = gridDim.x, p = P.p, tid = threadIdx.x;

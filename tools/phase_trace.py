@@ -41,6 +41,9 @@ x.normal_()
 y = torch.empty(n, device="cuda")
 ctas = 1024
 tr = torch.zeros(ctas * 8, dtype=torch.int64, device="cuda")
+tr0 = torch.zeros(ctas * 8, dtype=torch.int64, device="cuda")
+gap = 0.0
+fin_us = 0.0
 L.check(L.lib.cm_comm_set_trace(comm._h, tr.data_ptr(), ctas))
 st = L.Stats()
 phases = ["copyin", "start_barrier", "reduce", "mid_barrier", "allgather"]
@@ -64,13 +67,24 @@ for it in range(a.iters + 3):
         tr.zero_()
         agg_out[0] = P.aggregate(gs, P.GroupSpec(world), comm, out=agg_out[0])
     else:
-        # back-to-back pair as well: the second call is traced
+        # back-to-back pair as well: the second call is traced (the first into
+        # tr0, for the gap between the two kernels on this GPU)
+        tr0.zero_()
         for rep in range(2):
-            if rep:
-                tr.zero_()
+            L.check(L.lib.cm_comm_set_trace(comm._h, (tr if rep else tr0).data_ptr(), ctas))
             L.check(L.lib.cm_allreduce(comm._h, x.data_ptr(), y.data_ptr(), n, 0, 0, L.ALGO[a.algo], 131072, 0,
                                        torch.cuda.current_stream().cuda_stream, C.byref(st)))
     comm.synchronize()
+    if not a.agg and it >= 3:
+        t0v = tr0.view(ctas, 8).cpu()
+        t1v = tr.view(ctas, 8).cpu()
+        ends = t0v[:, 5][t0v[:, 5] > 0]
+        fin = t0v[:, 6][t0v[:, 6] > 0]
+        starts = t1v[:, 0][t1v[:, 0] > 0]
+        if len(ends) and len(starts):
+            gap += float(starts.min() - ends.max()) / 1e3
+        if len(fin) and len(ends):
+            fin_us += float(fin.max() - ends.max()) / 1e3
     t = tr.view(ctas, 8).cpu()
     used = t[:, 0] > 0
     t = t[used].double()
@@ -84,12 +98,12 @@ for it in range(a.iters + 3):
     for k in range(6):
         col = t[:, k][t[:, k] > 0]
         skew[k] += float(col.max() - t[:, 0].min()) / 1e3 if len(col) else 0.0
-row = [v / a.iters for v in acc] + [tot / a.iters]
+row = [v / a.iters for v in acc] + [tot / a.iters, gap / a.iters, fin_us / a.iters]
 rows = [None] * world
 dist.all_gather_object(rows, row)
 if rank == 0 and world > 1:
     for r, rw in enumerate(rows):
-        print(f"  rank {r}: span {rw[5]:.2f} | " + " ".join(f"{ph} {v:.2f}" for ph, v in zip(phases, rw[:5])),
+        print(f"  rank {r}: span {rw[5]:.2f} gap-before {rw[6]:.2f} (epoch hand-off {rw[7]:.2f}) | " + " ".join(f"{ph} {v:.2f}" for ph, v in zip(phases, rw[:5])),
               flush=True)
 if rank == 0:
     what = "C5 aggregate (registered, 2 fused groups)" if a.agg else f"bytes={a.bytes} algo={a.algo} zc={a.zc}"
