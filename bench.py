@@ -873,7 +873,7 @@ def overlap(args, rank, world, local):
 
     gs_view = P.GradientSet(tuple(P.Tensor(nm, "float32", g) for nm, g in zip(names, grads)))
     ov = P.OverlappedAggregator(gs_view, comm, algo=args.algo, cfg=cfg, max_ctas=args.ov_ctas or None,
-                                priority=args.ov_priority)
+                                priority=args.ov_priority, cluster_pairs=bool(args.ov_pairs))
 
     def step_seq():
         backward()
@@ -902,7 +902,24 @@ def overlap(args, rank, world, local):
     k = max(5, min(args.steps, 30))
     t_bwd, _ = timed(step_bwd, k)
     t_seq, r_seq = timed(step_seq, k)
-    t_ovl, r_ovl = timed(step_ovl, k)
+    if args.gemm_carveout:      # the overlapped backward leaves SMs to the collectives
+        torch._C._set_sm_carveout_experimental(args.gemm_carveout)
+    try:
+        t_ovl, r_ovl = timed(step_ovl, k)
+        t_bwd_cv = timed(step_bwd, k)[0] if args.gemm_carveout else t_bwd
+    finally:
+        if args.gemm_carveout:
+            torch._C._set_sm_carveout_experimental(None)
+    if os.environ.get("CM_OVERLAP_TRACE") and rank == 0:
+        # one overlapped step under torch.profiler (CUPTI kernel timeline), diagnostics only
+        from torch.profiler import ProfilerActivity, profile
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            step_ovl()
+            torch.cuda.synchronize()
+        prof.export_chrome_trace(os.environ["CM_OVERLAP_TRACE"])
+    elif os.environ.get("CM_OVERLAP_TRACE"):
+        step_ovl()
+        torch.cuda.synchronize()
     same = all(a.to_bytes() == b.to_bytes() for a, b in zip(r_seq.tensors, r_ovl.tensors))
     comm.synchronize()
     if rank == 0:
@@ -910,6 +927,8 @@ def overlap(args, rank, world, local):
               "backward_ms": round(t_bwd, 4), "sequential_ms": round(t_seq, 4), "overlapped_ms": round(t_ovl, 4),
               "hidden_frac": round((t_seq - t_ovl) / max(t_seq - t_bwd, 1e-9), 3),
               "groups": len(ov.groups), "ov_ctas": args.ov_ctas, "ov_priority": args.ov_priority,
+              "gemm_carveout": args.gemm_carveout, "backward_carveout_ms": round(t_bwd_cv, 4),
+              "ov_pairs": args.ov_pairs,
               "bit_identical": same})
     comm.close()
 
@@ -924,6 +943,10 @@ def main():
     ap.add_argument("--gemm", type=int, default=2048, help="overlap: per-layer bf16 GEMM size")
     ap.add_argument("--ov-ctas", type=int, default=64, help="overlap: CTA cap of overlapped collectives (0: none)")
     ap.add_argument("--ov-priority", type=int, default=-1, help="overlap: communication stream priority")
+    ap.add_argument("--ov-pairs", type=int, default=0, help="overlap: capped grids in 2-CTA clusters (1: on)")
+    ap.add_argument("--gemm-carveout", type=int, default=0,
+                    help="overlap: SMs the backward GEMMs leave free while the collectives overlap them "
+                         "(cuBLAS SM carve-out, overlapped step only; 0: none)")
     ap.add_argument("--ranks", type=int, default=4, help="refsweep: simulated ranks")
     ap.add_argument("--model", choices=tuple(MODELS), default="resnet50_like")
     ap.add_argument("--dtype", choices=("float32", "bfloat16"), default="float32")

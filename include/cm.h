@@ -210,6 +210,10 @@ int cm_comm_registry(cm_comm_t* comm, cm_registry_t** reg);
  *                         serialization: the next launch is scheduled while the
  *                         previous kernel drains and waits in griddepcontrol.wait
  *                         (device gap between launches 2.5 -> 0.6 us); 1 = off.
+ *   "cluster_pairs"       2 = collective grids of <= 64 CTAs launch in 2-CTA
+ *                         clusters (whole TPCs), so a capped collective next to
+ *                         2-CTA-cluster GEMMs does not break their SM pairs;
+ *                         1 = off (default; OverlappedAggregator(cluster_pairs=True) sets it)
  * get also reads the counters "auto_published", "auto_mapped",
  * "auto_zero_copy_calls" and "auto_buffer_checks" (allocation-id re-checks)
  * get also reads "staging_bytes", "pool_bytes" and "ll_payload_per_source" */

@@ -113,6 +113,7 @@ struct cm_comm {
   int pack_waves = 2;                         // batched copy: CTA waves (4 per SM per wave)
   int pack_unroll = 4;                        // batched copy: 16-byte loads in flight per thread (4 or 8)
   bool pdl = true;                            // programmatic dependent launch of the collective kernels
+  bool cluster2 = false;                      // capped collective grids in 2-CTA clusters (whole TPCs)
   int bulk_stage = 2 * RS_STAGE_BYTES;        // bytes per bulk-reduce stage (64 KiB: 3 stages fit)
   int64_t host_chunk = 8 << 20;               // host-gradient pipeline: bytes per H2D/D2H piece (p = 1)
   int64_t oneshot_bytes_per_cta = 8 * 1024;
@@ -165,18 +166,33 @@ size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 // Launch with programmatic stream serialization (the kernel starts with
 // pdl_begin(): it waits for the preceding grid itself), or plainly.
-cudaError_t launch_k(bool pdl, const void* k, dim3 grid, dim3 block, void** args, size_t smem, cudaStream_t s) {
-  if (!pdl) return cudaLaunchKernel(k, grid, block, args, smem, s);
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
+// cluster2: CTAs in clusters of two (both SMs of a TPC), so a capped grid
+// running next to 2-CTA-cluster GEMMs takes whole TPCs instead of breaking
+// one pair per CTA.
+cudaError_t launch_k(bool pdl, const void* k, dim3 grid, dim3 block, void** args, size_t smem, cudaStream_t s,
+                     bool cluster2 = false) {
+  if (!pdl && !cluster2) return cudaLaunchKernel(k, grid, block, args, smem, s);
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  if (pdl) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (cluster2) {
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = 2;
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = 1;
+    ++na;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = na;
   return cudaLaunchKernelExC(&cfg, k, args);
 }
 
@@ -514,7 +530,11 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
     P.nrs = (int)(nb / 2);
     P.ovl_chunks = c->ovl_chunks;
     P.ws = (multi && c->ws && bulk && !ovl && !c->dyn_ag) ? 1 : 0;
-    CUDA_TRY(launch_k(c->pdl, (const void*)k, dim3((unsigned)nb), dim3(THREADS), args, dsm, stream));
+    // pairs only for small (capped) grids: every cluster must be co-resident
+    // (CTA b of every rank waits for the others), which 2-SM clusters on
+    // partially floor-swept GPCs do not guarantee for a full-GPU grid
+    const bool pairs = c->cluster2 && nb % 2 == 0 && nb <= 64;
+    CUDA_TRY(launch_k(c->pdl, (const void*)k, dim3((unsigned)nb), dim3(THREADS), args, dsm, stream, pairs));
   }
   c->launches += 1;
   // real bytes pulled over NVLink by this rank
@@ -1235,6 +1255,7 @@ int cm_comm_set_param(cm_comm_t* c, const char* key, int64_t value) {
   else if (k == "pack_waves") c->pack_waves = (int)std::min<int64_t>(value, 64);
   else if (k == "pack_unroll") c->pack_unroll = value >= 8 ? 8 : 4;
   else if (k == "pdl") c->pdl = value > 1;
+  else if (k == "cluster_pairs") c->cluster2 = value > 1;
   else if (k == "host_chunk_kb") c->host_chunk = std::max<int64_t>(64, value) * 1024;
   else if (k == "bulk_stage_kb") c->bulk_stage = (int)std::max<int64_t>(4, std::min<int64_t>(value, 112)) * 1024;
   else if (k == "oneshot_bytes_per_cta") c->oneshot_bytes_per_cta = value;
@@ -1265,6 +1286,7 @@ int cm_comm_get_param(cm_comm_t* c, const char* key, int64_t* value) {
   else if (k == "pack_waves") *value = c->pack_waves;
   else if (k == "pack_unroll") *value = c->pack_unroll;
   else if (k == "pdl") *value = c->pdl ? 2 : 1;
+  else if (k == "cluster_pairs") *value = c->cluster2 ? 2 : 1;
   else if (k == "auto_published") *value = c->auto_published;
   else if (k == "auto_mapped") *value = c->auto_mapped;
   else if (k == "auto_zero_copy_calls") *value = c->auto_zc_calls;

@@ -44,8 +44,11 @@ class OverlappedAggregator:
     ``schema``: a GradientSet (used as a template) or ``[(name, numel,
     dtype), ...]``. ``launch_order``: "reverse" (default, last layers first)
     or "forward". ``max_ctas`` caps the CTAs of each overlapped collective
-    (None: the communicator's setting); ``priority`` is the communication
-    stream's priority (-1: high).
+    (None: the communicator's setting) — except the last group in launch
+    order, which runs once the backward pass is done and gets the full grid;
+    ``cluster_pairs``: capped grids launch in 2-CTA clusters so they occupy
+    whole TPCs (cuBLAS's 2-SM-cluster GEMMs keep their pairs);
+    ``priority`` is the communication stream's priority (-1: high).
 
     Stream rules (as for NCCL communicators): the means are views of
     persistent per-group buckets that the next step overwrites once its
@@ -56,7 +59,7 @@ class OverlappedAggregator:
 
     def __init__(self, schema, comm: Communicator, algo: str = "auto", cfg: FusionConfig | None = None,
                  switch_bytes: int | None = DEFAULT_SWITCH_BYTES, launch_order: str = "reverse",
-                 max_ctas: int | None = 64, priority: int = -1):
+                 max_ctas: int | None = 64, priority: int = -1, cluster_pairs: bool = False):
         if isinstance(schema, GradientSet):
             specs = [(t.name, t.len, t.dtype) for t in schema.tensors]
         else:
@@ -90,15 +93,27 @@ class OverlappedAggregator:
         # backward pass (the collective is NVLink-bound well below 148 CTAs)
         self.stream = torch.cuda.Stream(dev, priority=priority)
         self.max_ctas = max_ctas
+        self.cluster_pairs = cluster_pairs
         self.buckets = [torch.empty(sum(self.specs[i].len for i in m), dtype=DTYPES[self.specs[m[0]].dtype],
                                     device=dev) for m in self.groups]
         self.stats = [(L.Stats * 1)() for _ in self.groups]
+        # per group, allocated once: member pointer / count arrays, the
+        # producer-side event, and the plain addresses the fast-call path takes
+        # (ready() runs inside the backward loop, which is host-bound)
+        self._ptrs = [(C.c_void_p * len(m))() for m in self.groups]
+        self._counts = [L.i64_array([self.specs[i].len for i in m]) for m in self.groups]
+        self._ev = [torch.cuda.Event() for _ in self.groups]
+        self._gdtype = [L.DTYPE[self.specs[m[0]].dtype] for m in self.groups]
+        self._addr = [(C.addressof(p), C.addressof(c), C.addressof(st), b.data_ptr())
+                      for p, c, st, b in zip(self._ptrs, self._counts, self.stats, self.buckets)]
+        self._cap_set = None
         self.step_stats: list[CollectiveStats] = []
         self.iteration = 0
         self._reset()
 
     # -- per step ---------------------------------------------------------------
     def _reset(self):
+        self._cap_saved = getattr(self, "_cap_saved", None)
         self._tensors = {}
         self._missing = [len(m) for m in self.groups]
         self._events = [None] * len(self.groups)
@@ -121,7 +136,7 @@ class OverlappedAggregator:
         self._tensors[name] = t
         self._missing[g] -= 1
         if self._missing[g] == 0:
-            ev = torch.cuda.Event()
+            ev = self._ev[g]
             ev.record(torch.cuda.current_stream(t.device))
             self._events[g] = ev
             self._launch_due()
@@ -132,31 +147,44 @@ class OverlappedAggregator:
             self._next += 1
 
     def _launch(self, g: int):
-        members = [self.specs[i] for i in self.groups[g]]
-        ts = [self._tensors[s.name] for s in members]
-        n = len(ts)
-        ncalls = C.c_int()
-        agreed = C.c_int(1)
+        members = self.groups[g]
+        ptrs = self._ptrs[g]
+        for k, i in enumerate(members):
+            ptrs[k] = self._tensors[self.specs[i].name].data_ptr()
         self.stream.wait_event(self._events[g])
-        saved = None
-        if self.max_ctas:
-            saved = self.comm.get_param("max_ctas")
-            self.comm.set_param("max_ctas", self.max_ctas)
-        try:
-            self._call(g, members, ts, n, ncalls, agreed)
-        finally:
-            if saved is not None:
-                self.comm.set_param("max_ctas", saved)
-        if ncalls.value != 1:
+        # the last group in launch order runs after the backward pass is done:
+        # nothing to leave SMs for, so it gets the full grid (the cap is set
+        # once per step, not per group)
+        last = self._next == len(self.order) - 1
+        want = None if (last or not self.max_ctas) else self.max_ctas
+        if want != self._cap_set:
+            if want is not None and self._cap_saved is None:
+                self._cap_saved = (self.comm.get_param("max_ctas"), self.comm.get_param("cluster_pairs"))
+            self.comm.set_param("max_ctas", want if want is not None else self._cap_saved[0])
+            if self.cluster_pairs:   # capped grids take whole TPCs (see cm.h "cluster_pairs")
+                self.comm.set_param("cluster_pairs", 2 if want is not None else self._cap_saved[1])
+            self._cap_set = want
+        if self._call(g, len(members)) != 1:
             raise ShapeError("internal: an overlapped group split into several fused buffers")
 
-    def _call(self, g, members, ts, n, ncalls, agreed):
-        with torch.cuda.device(self.comm.device):
-            L.check(L.lib.cm_fused_allreduce_agreed(
-                self.comm._h, n, L.ptr_array([t.data_ptr() for t in ts]), L.i64_array([s.len for s in members]),
-                L.DTYPE[members[0].dtype], self.buckets[g].data_ptr(), L.ALGO[self.algo],
-                int(self.cfg.threshold_bytes), self.switch, 1, None, 0, C.byref(agreed), None,
-                self.stream.cuda_stream, self.stats[g], C.byref(ncalls)))
+    def _call(self, g, n) -> int:
+        """One fused collective for group g on the communication stream;
+        returns the number of fused buffers it ran as."""
+        pa, ca, sa, out = self._addr[g]
+        comm = self.comm
+        if L.fast is not None:
+            status, _, ncalls = L.fast.fused(comm._hv, n, pa, ca, self._gdtype[g], out, L.ALGO[self.algo],
+                                             int(self.cfg.threshold_bytes), self.switch, 1, 0, 0, 0,
+                                             self.stream.cuda_stream, sa)
+            if status:
+                L.check(status)
+            return ncalls
+        nc, ag = C.c_int(), C.c_int(1)
+        L.check(L.lib.cm_fused_allreduce_agreed(
+            comm._h, n, self._ptrs[g], self._counts[g], self._gdtype[g], out, L.ALGO[self.algo],
+            int(self.cfg.threshold_bytes), self.switch, 1, None, 0, C.byref(ag), None,
+            self.stream.cuda_stream, self.stats[g], C.byref(nc)))
+        return nc.value
 
     def finish(self) -> GradientSet:
         """Join the communication stream into the caller's stream and return
