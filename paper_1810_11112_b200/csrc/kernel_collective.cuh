@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(THREADS, 1) collective_kernel(const __grid_con
   if (!STREAM && P.bulk_rs)
     bulk_rs_setup(P.bulk_rs, P.bulk_stage, tid, (MULTI && P.ws) ? team_ws_rs().ncons : RS_CONSUMERS);
   if (tid == 0) {
-    s_epoch = ctrl->epoch + 1;
+    s_epoch = epoch_read(myheap, b) + 1;
     s_err = 0;
     s_skip = 0;
   }
@@ -642,20 +642,23 @@ finish:
   CM_TRACE(P, lr, b, 5);
   if (tid == 0) {
     if (s_err) *reinterpret_cast<volatile unsigned*>(P.herr) = (unsigned)s_err;
-    __threadfence();
-    const unsigned old = atomicAdd(&ctrl->done, 1u);
-    if (old == (unsigned)nb - 1) {
-      ctrl->done = 0;
-      ctrl->ag_next = 0;
-      if (P.agree_inline) {               // outcome for the gated launches queued behind
-        ctrl->agree_ok = s_skip == 2 ? 0 : 1;
-        ctrl->agree_tag = P.agree_ticket;
-      }
-      ctrl->epoch = e;
-      __threadfence();
+    // outcome for the gated launches queued behind (every CTA compared the
+    // same records, so CTA 0's verdict is the grid's)
+    if (P.agree_inline && b == 0) {
+      ctrl->agree_ok = s_skip == 2 ? 0 : 1;
+      ctrl->agree_tag = P.agree_ticket;
     }
-    CM_TRACE(P, lr, b, 6);
+    if (P.dyn_ag) {                       // the allgather task counter is reset by the last CTA
+      __threadfence();
+      const unsigned old = atomicAdd(&ctrl->done, 1u);
+      if (old == (unsigned)nb - 1) {
+        ctrl->done = 0;
+        ctrl->ag_next = 0;
+      }
+    }
   }
+  epoch_publish(myheap, b, nb, e);
+  CM_TRACE(P, lr, b, 6);
 }
 
 }  // namespace dev

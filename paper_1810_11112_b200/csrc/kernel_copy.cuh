@@ -189,8 +189,7 @@ __global__ void __launch_bounds__(THREADS) batched_copy_kernel(const __grid_cons
   if (b == 0) lo = 0;
   char* base = nullptr;
   if (P.staged) {
-    const Ctrl* ctrl = reinterpret_cast<const Ctrl*>(P.heap + CTRL_OFF);
-    const unsigned long long e = ctrl->epoch + 1;
+    const unsigned long long e = epoch_read(P.heap, 0) + 1;
     base = P.heap + P.staging_off + (long long)(e & 1) * P.staging_bytes;
   }
   // find the first member overlapping [lo, hi)
@@ -253,8 +252,7 @@ static __global__ void __launch_bounds__(BULK_THREADS) bulk_copy_kernel(const __
   if (hi <= lo) return;
   char* base = nullptr;
   if (P.staged) {
-    const Ctrl* ctrl = reinterpret_cast<const Ctrl*>(P.heap + CTRL_OFF);
-    base = P.heap + P.staging_off + (long long)((ctrl->epoch + 1) & 1) * P.staging_bytes;
+    base = P.heap + P.staging_off + (long long)((epoch_read(P.heap, 0) + 1) & 1) * P.staging_bytes;
   }
   for (int s = 0; s < BULK_STAGES; ++s)
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[s])));

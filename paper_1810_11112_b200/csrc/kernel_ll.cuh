@@ -36,7 +36,7 @@ __global__ void __launch_bounds__(THREADS, 1) ll_kernel(const __grid_constant__ 
   __shared__ int s_seq[MAXP];
   __shared__ int s_disagree;
   if (tid == 0) {
-    s_epoch = ctrl->epoch + 1;
+    s_epoch = epoch_read(myheap, b) + 1;
     s_err = 0;
     s_disagree = 0;
   }
@@ -141,13 +141,11 @@ ll_finish:
   CM_TRACE(P, lr, b, 5);
   if (tid == 0) {
     if (s_err) *reinterpret_cast<volatile unsigned*>(P.herr) = (unsigned)s_err;
-    __threadfence();
-    const unsigned old = atomicAdd(&ctrl->done, 1u);
-    if (old == (unsigned)nb - 1) {
-      ctrl->done = 0;
-      ctrl->epoch = e;
+    if (P.done_flag) {                   // host spins on this (cm_agree): after every CTA's output
       __threadfence();
-      if (P.done_flag) {                 // host spins on this (cm_agree)
+      const unsigned old = atomicAdd(&ctrl->done, 1u);
+      if (old == (unsigned)nb - 1) {
+        ctrl->done = 0;
         ctrl->agree_ok = s_disagree ? 0 : 1;   // read by gated collectives queued behind
         ctrl->agree_tag = P.done_value;
         __threadfence_system();
@@ -155,6 +153,7 @@ ll_finish:
       }
     }
   }
+  epoch_publish(myheap, b, nb, e);
 }
 
 // ---- LL two-shot (medium messages) ----------------------------------------------
@@ -207,7 +206,7 @@ __global__ void __launch_bounds__(THREADS, 1) ll2_kernel(const __grid_constant__
   __shared__ int s_seq[MAXP];
   CM_TRACE(P, lr, b, 0);
   if (tid == 0) {
-    s_epoch = ctrl->epoch + 1;
+    s_epoch = epoch_read(myheap, b) + 1;
     s_err = 0;
   }
   int m = 1;
@@ -313,16 +312,8 @@ __global__ void __launch_bounds__(THREADS, 1) ll2_kernel(const __grid_constant__
 ll2_finish:
   __syncthreads();
   CM_TRACE(P, lr, b, 5);
-  if (tid == 0) {
-    if (s_err) *reinterpret_cast<volatile unsigned*>(P.herr) = (unsigned)s_err;
-    __threadfence();
-    const unsigned old = atomicAdd(&ctrl->done, 1u);
-    if (old == (unsigned)nb - 1) {
-      ctrl->done = 0;
-      ctrl->epoch = e;
-      __threadfence();
-    }
-  }
+  if (tid == 0 && s_err) *reinterpret_cast<volatile unsigned*>(P.herr) = (unsigned)s_err;
+  epoch_publish(myheap, b, nb, e);
 }
 
 }  // namespace dev

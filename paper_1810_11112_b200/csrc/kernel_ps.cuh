@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(THREADS, 1) ps_kernel(const __grid_constant__ 
   __shared__ unsigned long long s_epoch;
   __shared__ int s_err;
   if (tid == 0) {
-    s_epoch = ctrl->epoch + 1;
+    s_epoch = epoch_read(myheap, b) + 1;
     s_err = 0;
   }
   __syncthreads();
@@ -202,16 +202,8 @@ __global__ void __launch_bounds__(THREADS, 1) ps_kernel(const __grid_constant__ 
 
 finish:
   __syncthreads();
-  if (tid == 0) {
-    if (s_err) *reinterpret_cast<volatile unsigned*>(P.herr) = (unsigned)s_err;
-    __threadfence();
-    const unsigned old = atomicAdd(&ctrl->done, 1u);
-    if (old == (unsigned)nb - 1) {
-      ctrl->done = 0;
-      ctrl->epoch = e;
-      __threadfence();
-    }
-  }
+  if (tid == 0 && s_err) *reinterpret_cast<volatile unsigned*>(P.herr) = (unsigned)s_err;
+  epoch_publish(myheap, b, nb, e);
 }
 
 }  // namespace dev

@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(THREADS, 1) rhd_kernel(const __grid_constant__
   __shared__ int s_err;
   CM_TRACE(P, lr, b, 0);
   if (tid == 0) {
-    s_epoch = ctrl->epoch + 1;
+    s_epoch = epoch_read(myheap, b) + 1;
     s_err = 0;
   }
   __syncthreads();
@@ -200,16 +200,8 @@ __global__ void __launch_bounds__(THREADS, 1) rhd_kernel(const __grid_constant__
 finish:
   __syncthreads();
   CM_TRACE(P, lr, b, 5);
-  if (tid == 0) {
-    if (s_err) *reinterpret_cast<volatile unsigned*>(P.herr) = (unsigned)s_err;
-    __threadfence();
-    const unsigned old = atomicAdd(&ctrl->done, 1u);
-    if (old == (unsigned)nb - 1) {
-      ctrl->done = 0;
-      ctrl->epoch = e;
-      __threadfence();
-    }
-  }
+  if (tid == 0 && s_err) *reinterpret_cast<volatile unsigned*>(P.herr) = (unsigned)s_err;
+  epoch_publish(myheap, b, nb, e);
 }
 
 }  // namespace dev
