@@ -316,6 +316,55 @@ def main():
                    f"overlapped aggregate {algo} step {step}")
             expect(len(ov.step_stats) == len(groups), "overlap stats")
 
+    # 4j. launch knobs: plain launches (pdl off) and 2-CTA-cluster capped grids
+    # give the same bits; grid sizes change from call to call (epoch slots)
+    for knobs in ({"pdl": 1}, {"cluster_pairs": 2, "max_ctas": 16}, {"pdl": 2, "max_ctas": 148}):
+        for k, v in knobs.items():
+            comm.set_param(k, v)
+        for n in (700, 300_001, 2_500_007):
+            xs = [np.random.default_rng([41, n, r]).standard_normal(n).astype(np.float32) for r in range(world)]
+            for algo in ("ring_rsa", "rhd_rsa"):
+                out, _ = P.allreduce(P.Tensor("x", "float32", torch.from_numpy(xs[rank]).cuda()),
+                                     P.ReduceOp.SUM, group, comm, algo=algo)
+                expect(out.to_bytes() == OC.allreduce(xs, "sum", algo, "float32").tobytes(),
+                       f"launch knobs {knobs} {algo} n={n}")
+    comm.set_param("cluster_pairs", 1)
+    want, groups, _ = OA.aggregate(per_rank, "float32", "auto", 8 << 20)
+    ov = P.OverlappedAggregator([(nm, a.size, "float32") for nm, a in per_rank[rank]], comm,
+                                cfg=P.FusionConfig(8 << 20), max_ctas=16, cluster_pairs=True)
+    for step in range(2):
+        for nm, a in per_rank[rank]:
+            ov.ready(nm, torch.from_numpy(a).cuda())
+        res = ov.finish()
+        expect(all(t.to_bytes() == want[t.name].tobytes() for t in res.tensors),
+               f"overlapped aggregate, 2-CTA clusters, step {step}")
+    expect(comm.get_param("cluster_pairs") == 1 and comm.get_param("max_ctas") == 148,
+           "overlapped aggregator restores the launch knobs")
+
+    # 4k. the façade's two call paths into the C ABI (the fast-call module and
+    # plain ctypes) give the same bits and stats
+    from paper_1810_11112_b200 import _lib as LF
+    expect(LF.fast is not None, "fast-call module loaded")
+    fast = LF.fast
+    n = 123_457
+    xs = [np.random.default_rng([43, r]).standard_normal(n).astype(np.float32) for r in range(world)]
+    res = {}
+    for path in ("fast", "ctypes"):
+        LF.fast = fast if path == "fast" else None
+        try:
+            x = P.Tensor("x", "float32", torch.from_numpy(xs[rank]).cuda())
+            ar, st = P.allreduce(x, P.ReduceOp.SUM, group, comm, algo="ring_rsa")
+            rs, st2 = P.reduce_scatter(x, P.ReduceOp.SUM, group, comm)
+            ag, st3 = P.allgather(P.Tensor("s", "float32", rs.payload.clone()), n, group, comm)
+            gs = P.GradientSet(tuple(P.Tensor(nm, "float32", torch.from_numpy(a).cuda()) for nm, a in per_rank[rank]))
+            agg = P.aggregate(gs, group, comm, cfg=P.FusionConfig(8 << 20))
+            res[path] = (ar.to_bytes(), st, rs.to_bytes(), st2, ag.to_bytes(), st3,
+                         [t.to_bytes() for t in agg.tensors])
+        finally:
+            LF.fast = fast
+    expect(res["fast"] == res["ctypes"], "fast-call and ctypes paths agree")
+    expect(res["fast"][0] == OC.allreduce(xs, "sum", "ring_rsa", "float32").tobytes(), "fast-call allreduce exact")
+
     # 4f. parameter-server pull step (paramserver.py:171-271): co-located and
     # split topologies, two steps each, bit-exact vs the oracle restatement
     from oracle import paramserver as OPSV
