@@ -1013,6 +1013,46 @@ std::vector<Run> coalesce(const void* const* srcs, const int64_t* bytes, int n, 
   return out;
 }
 
+// Piece boundaries over [0, total) for the single-rank host pipeline: pieces
+// of `piece` bytes, ramped piece/8, /4, /2 at both ends so the first D2H starts
+// after a small H2D and the last D2H after a small one (pipeline fill and
+// drain ~1/8 of a uniform piece); short totals get eight even pieces.
+std::vector<int64_t> graded_cuts(int64_t total, int64_t piece) {
+  std::vector<int64_t> cuts;
+  const int64_t ramp[3] = {piece / 8, piece / 4, piece / 2};
+  const int64_t head = ramp[0] + ramp[1] + ramp[2];
+  if (total <= 2 * head + piece) {
+    const int64_t q = std::max<int64_t>(64 << 10, (total + 7) / 8);
+    for (int64_t a = q; a < total; a += q) cuts.push_back(a);
+    cuts.push_back(total);
+    return cuts;
+  }
+  int64_t a = 0;
+  for (int64_t r : ramp) cuts.push_back(a += r);
+  const int64_t mid_end = total - head;
+  while (a + 2 * piece <= mid_end) cuts.push_back(a += piece);
+  if (a < mid_end) cuts.push_back(a = mid_end);
+  for (int i = 2; i >= 0; --i) cuts.push_back(a += ramp[i]);
+  return cuts;
+}
+
+// runs (sorted by offset, disjoint) split at the given offsets
+std::vector<Run> split_runs(const std::vector<Run>& runs, const std::vector<int64_t>& cuts) {
+  std::vector<Run> out;
+  for (const Run& r : runs) {
+    int64_t a = r.off;
+    const int64_t end = r.off + r.bytes;
+    auto it = std::upper_bound(cuts.begin(), cuts.end(), a);
+    while (a < end) {
+      const int64_t b = (it == cuts.end()) ? end : std::min(end, *it);
+      out.push_back(Run{r.src + (a - r.off), a, b - a});
+      a = b;
+      if (it != cuts.end() && *it <= a) ++it;
+    }
+  }
+  return out;
+}
+
 // Host-memory aggregate pipeline (CUDA-aware semantics for host gradients).
 // Stream roles: h2d copies inputs into `indev`, the caller's stream runs the
 // collectives, d2h copies results out of `outdev`. Every hand-off is an
@@ -1725,14 +1765,18 @@ int fused_impl(cm_comm* c, int n, const void* const* sends, const int64_t* count
       // (d2h stream) in host_chunk pieces so both PCIe directions stream at
       // once; members adjacent in memory are copied as one run (one DMA)
       if ((st = hp.start(out_host ? off : 0, 0))) return st;
-      std::vector<Run> runs = coalesce(srcs.data(), nbytes.data(), n, c->host_chunk);
+      const std::vector<int64_t> cuts = graded_cuts(off, c->host_chunk);
+      const std::vector<Run> runs = split_runs(coalesce(srcs.data(), nbytes.data(), n, INT64_MAX), cuts);
       int64_t chunk_lo = 0;
+      size_t ci = 0;
       for (size_t k = 0; k < runs.size(); ++k) {
         const Run& r = runs[k];
         CUDA_TRY(cudaMemcpyAsync((out_host ? c->indev : static_cast<char*>(recvs[0])) + r.off, r.src, r.bytes,
                                  cudaMemcpyDefault, c->h2d));
         const int64_t end = r.off + r.bytes;
-        if (out_host && (end - chunk_lo >= c->host_chunk || k + 1 == runs.size())) {
+        while (ci < cuts.size() && cuts[ci] < end) ++ci;
+        const bool at_cut = ci < cuts.size() && cuts[ci] == end;
+        if (out_host && (at_cut || k + 1 == runs.size())) {
           if ((st = hp.link(c->h2d, c->d2h))) return st;
           CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(recvs[0]) + chunk_lo, c->indev + chunk_lo, end - chunk_lo,
                                    cudaMemcpyDeviceToHost, c->d2h));

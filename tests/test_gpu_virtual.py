@@ -370,6 +370,21 @@ def test_single_rank_communicator_aggregate_host_and_device():
         assert res2 is res
         assert all(t.to_bytes() == (a * 3).tobytes() for t, (_, a) in zip(res.tensors, sorted(g)))
         assert all(t.is_cuda == (kind == "device") for t in res.tensors)
+    # graded pipeline pieces (ramped at both ends) for other piece sizes and a
+    # total below one piece (eight even pieces)
+    for chunk_kb, lay in ((64, layers), (1024, [77, 1000, 3]), (8192, [5, 300_000])):
+        comm.set_param("host_chunk_kb", chunk_kb)
+        gg = I.synth_gradients(1, 0, lay, 0)
+        fl = torch.empty(sum(a.size for _, a in gg), dtype=torch.float32).pin_memory()
+        ts, off = [], 0
+        for nm, a in gg:
+            v = fl[off:off + a.size]
+            v.copy_(torch.from_numpy(a))
+            ts.append(P.Tensor(nm, "float32", v))
+            off += a.size
+        res = P.aggregate(P.GradientSet(tuple(ts)), P.GroupSpec(1), comm)
+        assert all(t.to_bytes() == dict(gg)[t.name].tobytes() for t in res.tensors), chunk_kb
+    comm.set_param("host_chunk_kb", 8192)
     comm.close()
 
 

@@ -60,8 +60,30 @@ def both():
     cur.wait_stream(s2)
 
 
+def pipelined(piece):
+    """H2D piece k -> event -> D2H piece k of the same bytes (the single-rank
+    host pipeline's shape), pieces of `piece` bytes."""
+    def fn():
+        cur = torch.cuda.current_stream()
+        s1.wait_stream(cur)
+        s2.wait_stream(cur)
+        for a in range(0, S, piece):
+            b = min(S, a + piece)
+            with torch.cuda.stream(s1):
+                d1[a:b].copy_(hsrc[a:b], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(s1)
+            s2.wait_event(ev)
+            with torch.cuda.stream(s2):
+                hdst[a:b].copy_(d1[a:b], non_blocking=True)
+        cur.wait_stream(s1)
+        cur.wait_stream(s2)
+    return fn
+
+
 res = {}
-for name, fn in (("h2d", h2d), ("d2h", d2h), ("both", both)):
+for name, fn in (("h2d", h2d), ("d2h", d2h), ("both", both), ("pipe8M", pipelined(8 << 20)),
+                 ("pipe2M", pipelined(2 << 20)), ("pipe32M", pipelined(32 << 20))):
     ms = timed(fn)
     res[name] = (ms, S / (ms * 1e-3) / 1e9)
 line = f"rank {rank}/{world}: " + " ".join(f"{k} {ms:.3f} ms ({gb:.1f} GB/s)" for k, (ms, gb) in res.items())
