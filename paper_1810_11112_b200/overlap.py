@@ -164,6 +164,8 @@ class OverlappedAggregator:
             if self.cluster_pairs:   # capped grids take whole TPCs (see cm.h "cluster_pairs")
                 self.comm.set_param("cluster_pairs", 2 if want is not None else self._cap_saved[1])
             self._cap_set = want
+            if want is None:
+                self._cap_saved = None   # re-read next step (the caller may retune the communicator)
         if self._call(g, len(members)) != 1:
             raise ShapeError("internal: an overlapped group split into several fused buffers")
 
