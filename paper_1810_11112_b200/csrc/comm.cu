@@ -2294,7 +2294,7 @@ int cm_bench_p2p(cm_comm_t* c, int mode, int64_t bytes, int ctas, int iters, voi
     CUDA_TRY(cudaFuncSetAttribute((const void*)spin_kernel_pdl, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)bytes));
   int spin_i = 0;   // modes 18/19: launch index (stamps at staging[2 i], [2 i + 1])
-  if (mode >= 18 && mode <= 22 && (int64_t)(iters + 1) * 16 + 65536 > (int64_t)c->staging_bytes)
+  if (mode >= 18 && mode <= 24 && (int64_t)(iters + 1) * 16 + 65536 > (int64_t)c->staging_bytes)
     return fail(CM_ERR_CONFIG, "too many iterations");
   static unsigned long long flag_base = 1ull << 40;   // slot values only grow (same sequence on every rank)
   auto launch = [&]() {
@@ -2332,7 +2332,7 @@ int cm_bench_p2p(cm_comm_t* c, int mode, int64_t bytes, int ctas, int iters, voi
       cfg.dynamicSmemBytes = (size_t)bytes;   // > 114 KiB: one CTA per SM, the next grid cannot co-reside
       cudaLaunchKernelEx(&cfg, spin_kernel_pdl, P, out, spin_i, (long long)20000);
       ++spin_i;
-    } else if (mode == 21 || mode == 22) {
+    } else if (mode >= 21 && mode <= 24) {
       auto* out = reinterpret_cast<unsigned long long*>(c->local + c->staging_off);
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3((unsigned)ctas);
@@ -2343,7 +2343,7 @@ int cm_bench_p2p(cm_comm_t* c, int mode, int64_t bytes, int ctas, int iters, voi
       at[0].val.programmaticStreamSerializationAllowed = 1;
       cfg.attrs = at;
       cfg.numAttrs = 1;
-      cudaLaunchKernelEx(&cfg, spin_kernel_remote, P, out, spin_i, (long long)20000, mode == 22 ? 1 : 0);
+      cudaLaunchKernelEx(&cfg, spin_kernel_remote, P, out, spin_i, (long long)20000, mode - 21);
       ++spin_i;
     } else if (mode == 16) {
       empty_kernel<<<ctas, THREADS, 0, s>>>(0);
@@ -2364,7 +2364,7 @@ int cm_bench_p2p(cm_comm_t* c, int mode, int64_t bytes, int ctas, int iters, voi
   cudaEventElapsedTime(&ms, e0, e1);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
-  if (mode >= 18 && mode <= 22) {   // median device gap between consecutive launches
+  if (mode >= 18 && mode <= 24) {   // median device gap between consecutive launches
     std::vector<unsigned long long> st((size_t)2 * spin_i);
     CUDA_TRY(cudaMemcpy(st.data(), c->local + c->staging_off, st.size() * 8, cudaMemcpyDeviceToHost));
     std::vector<double> gaps;

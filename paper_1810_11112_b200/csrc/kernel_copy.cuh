@@ -52,9 +52,27 @@ static __global__ void __launch_bounds__(THREADS, 1) spin_kernel_remote(const __
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   auto* peer = reinterpret_cast<unsigned long long*>(P.heap[(P.rank + 1) % P.p] + P.staging_off) + 4096 + P.rank;
+  __shared__ __align__(128) unsigned char tma_buf[1024];
+  __shared__ __align__(8) unsigned long long tma_bar;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    if (load) out[4095] = *reinterpret_cast<volatile unsigned long long*>(peer);
-    else *reinterpret_cast<volatile unsigned long long*>(peer) = (unsigned long long)i;
+    if (load == 2) {     // mode 23: the remote load through the bulk-copy engine (TMA)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&tma_bar)));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&tma_bar)), "r"(1024)
+                   : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       smem_u32(tma_buf)),
+                   "l"(reinterpret_cast<const char*>(peer) - 8 * P.rank), "r"(1024), "r"(smem_u32(&tma_bar))
+                   : "memory");
+      mbar_wait(&tma_bar, 0);
+      out[4095] = tma_buf[5];
+    } else if (load == 3) {   // mode 24: L1-bypassing load (ld.global.cg), as the allgather copies
+      out[4095] = __ldcg(peer);
+    } else if (load) {
+      out[4095] = *reinterpret_cast<volatile unsigned long long*>(peer);
+    } else {
+      *reinterpret_cast<volatile unsigned long long*>(peer) = (unsigned long long)i;
+    }
   }
   spin_body<CollParams>(out, i, ns);
 }

@@ -39,7 +39,8 @@ for ctas in (1, 148):
     for mode, nbytes, what in ((18, 0, "spin, CollParams param block"), (19, 0, "spin, 20-byte params"),
                                (20, 0, "spin, CollParams, PDL launch"),
                                (20, 160 << 10, "spin, PDL, 160 KiB smem (1 CTA/SM)"),
-                               (21, 0, "spin, PDL, one remote store"), (22, 0, "spin, PDL, one remote load")):
+                               (21, 0, "spin, PDL, one remote store"), (22, 0, "spin, PDL, one remote load"),
+                               (24, 0, "spin, PDL, one remote ld.cg")):
         ms = C.c_double()
         L.check(L.lib.cm_bench_p2p(comm._h, mode, nbytes, ctas, 200, s, C.byref(ms)))
         if rank == 0:
