@@ -107,6 +107,13 @@ class OverlappedAggregator:
         self._addr = [(C.addressof(p), C.addressof(c), C.addressof(st), b.data_ptr())
                       for p, c, st, b in zip(self._ptrs, self._counts, self.stats, self.buckets)]
         self._cap_set = None
+        # the means are views of the persistent buckets: built once, handed out
+        # every step (finish() runs on the host critical path of the step)
+        views = {}
+        for g, m in enumerate(self.groups):
+            for sp, v in zip((self.specs[i] for i in m), self.buckets[g].split([self.specs[i].len for i in m])):
+                views[sp.name] = Tensor._wrap(sp.name, sp.dtype, v)
+        self._views = tuple(views[sp.name] for sp in self.specs)
         self.step_stats: list[CollectiveStats] = []
         self.iteration = 0
         self._reset()
@@ -196,17 +203,16 @@ class OverlappedAggregator:
             raise ShapeError(f"finish() before every gradient was ready: missing {missing[:8]}")
         torch.cuda.current_stream(self.comm.device).wait_stream(self.stream)
         if self.comm.blocking:
-            L.check(L.lib.cm_comm_sync(self.comm._h, self.stream.cuda_stream))
+            st = (L.fast.sync(self.comm._hv, self.stream.cuda_stream) if L.fast is not None
+                  else L.lib.cm_comm_sync(self.comm._h, self.stream.cuda_stream))
         else:
-            L.check(L.lib.cm_comm_poll(self.comm._h))
-        views = {}
-        for g, m in enumerate(self.groups):
-            for s, v in zip((self.specs[i] for i in m), self.buckets[g].split([self.specs[i].len for i in m])):
-                views[s.name] = Tensor._wrap(s.name, s.dtype, v)
+            st = L.fast.poll(self.comm._hv) if L.fast is not None else L.lib.cm_comm_poll(self.comm._h)
+        if st:
+            L.check(st)
         stats = [CollectiveStats(int(self.stats[g][0].rounds), int(self.stats[g][0].messages_per_rank),
                                  int(self.stats[g][0].bytes_sent_per_rank)) for g in self.order]
         gs = GradientSet.__new__(GradientSet)
-        object.__setattr__(gs, "tensors", tuple(views[s.name] for s in self.specs))
+        object.__setattr__(gs, "tensors", self._views)
         object.__setattr__(gs, "iteration", self.iteration)
         self.iteration += 1
         self._reset()
