@@ -392,7 +392,9 @@ def headline(args, rank, world, local):
         barrier(world)
         return max_over_ranks(statistics.mean(a.elapsed_time(b) for a, b in ev), world)
 
-    # unregistered gradients first (pack into the IPC staging heap every step)
+    # unregistered gradients first: plain tensors through the reference API
+    # (automatic member registration after the second agreed call, so the
+    # warm-up leaves them read in place; packed into staging before that)
     ms_unreg = None
     if world > 1 and not args.no_register:
         for _ in range(args.warmup):
@@ -562,6 +564,9 @@ def headline(args, rank, world, local):
                                      "region): peers read them in place, no pack")
                        if (world > 1 and not args.no_register) else "unregistered: packed every step"},
             "ms_per_step_unregistered": None if ms_unreg is None else round(ms_unreg, 4),
+            "unregistered_what": ("plain tensors through the reference API (no register_gradients): the "
+                                  "members are registered automatically after the second agreed aggregate "
+                                  "(warm-up), then read in place") if ms_unreg is not None else None,
             "ms_per_step_profiled_pass": round(ms_prof, 4),
             "latency_us": round(ms * 1e3, 2),
             "bus_gbps": round(2 * (world - 1) / world * S / (ms * 1e-3) / 1e9, 2) if world > 1 else None,

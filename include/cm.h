@@ -236,6 +236,10 @@ int cm_comm_export(cm_comm_t* comm, const void* ptr, int64_t bytes, void* handle
 int cm_comm_register(cm_comm_t* comm, const void* ptr, int64_t bytes, const void* all_handles,
                      const int64_t* all_offsets, int64_t* reg_id);
 int cm_comm_deregister(cm_comm_t* comm, const void* ptr);
+/* allocation ids (CU_POINTER_ATTRIBUTE_BUFFER_ID, 0 if unknown) of n device
+ * pointers: a re-allocated range gets a new id even at the same address
+ * (aggregate's automatic member registration checks its members with it) */
+int cm_buffer_ids(cm_comm_t* comm, int n, const void* const* ptrs, uint64_t* ids);
 /* virtual group (single-GPU emulation): register every virtual rank's buffer
  * (ptrs[size]) under one id; fused aggregates whose members all carry ids read
  * the members in place (the SRC_GATHER path of real communicators) */

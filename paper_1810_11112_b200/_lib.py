@@ -115,6 +115,7 @@ _SIGS = {
     "cm_comm_free": ([_vp, _vp], _i),
     "cm_comm_export": ([_vp, _vp, _i64, _vp, _P(_i64)], _i),
     "cm_comm_register": ([_vp, _vp, _i64, _vp, _P(_i64), _P(_i64)], _i),
+    "cm_buffer_ids": ([_vp, _i, _vp, _vp], _i),
     "cm_comm_deregister": ([_vp, _vp], _i),
     "cm_comm_register_v": ([_vp, _P(_vp), _i64, _P(_i64)], _i),
     "cm_comm_sync": ([_vp, _vp], _i),

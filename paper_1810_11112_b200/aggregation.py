@@ -173,7 +173,7 @@ class _Plan:
     same-dtype runs with their ctypes pointer/count arrays, and split sizes.
     GradientSet is immutable, so the plan is cached on it."""
 
-    def __init__(self, grads: GradientSet, names: list[str]):
+    def __init__(self, grads: GradientSet, names: list[str], regmap: dict | None = None):
         self.names = names
         ready = [grads.get(nm) for nm in names]
         self.runs = []
@@ -187,7 +187,6 @@ class _Plan:
                 if t.dtype not in ("float32", "float64", "bfloat16"):
                     raise ShapeError(f"aggregate averages floating-point gradients, got {t.dtype}")
             counts = [t.len for t in run]
-            regmap = grads.__dict__.get("_reg_ids")
             reg = None
             if regmap is not None and all(t.name in regmap for t in run):
                 reg = L.i64_array([regmap[t.name] for t in run])
@@ -237,17 +236,76 @@ def aggregate(grads: GradientSet, group: GroupSpec, transport: Communicator,
         object.__setattr__(grads, "_sorted_names", local)
         object.__setattr__(grads, "_name_key", _name_key(local))
     sw = _switch(switch_bytes, tp.size)
+    explicit = grads.__dict__.get("_reg_ids")
     if tp.size == 1:
-        return _aggregate_names(grads, local, tp, algo, cfg, sw, registry, handles, stats_out, out, None)
+        return _aggregate_names(grads, local, tp, algo, cfg, sw, registry, handles, stats_out, out, None, explicit)
     if not local:               # nothing to fuse: plain agree + gather
         names = negotiate_ready([], group, tp)
-        return _aggregate_names(grads, names, tp, algo, cfg, sw, registry, handles, stats_out, out, None)
-    agree = (C.c_int64 * 2)(grads.__dict__["_name_key"], len(local))
-    res = _aggregate_names(grads, local, tp, algo, cfg, sw, registry, handles, stats_out, out, agree)
-    if res is None:             # ready sets differ across ranks
+        return _aggregate_names(grads, names, tp, algo, cfg, sw, registry, handles, stats_out, out, None, explicit)
+    auto = None if explicit is not None else _auto_members(grads, local, tp)
+    flags = 0 if auto is None else auto[0]
+    agree = (C.c_int64 * 2)(grads.__dict__["_name_key"], len(local) | flags)
+    regmap = explicit if explicit is not None else (auto[1]["ids"] if flags & _AUTO_READY else None)
+    res = _aggregate_names(grads, local, tp, algo, cfg, sw, registry, handles, stats_out, out, agree, regmap)
+    if res is None:             # ready sets (or member-registration states) differ across ranks
         names = _negotiate_gather(local, group, tp)
-        res = _aggregate_names(grads, names, tp, algo, cfg, sw, registry, handles, stats_out, out, None)
+        if auto is not None and names == local:
+            auto[1]["disabled"] = True      # the member-registration states differed: stop offering
+        # no gathered members here: every rank packs (the modes must match)
+        res = _aggregate_names(grads, names, tp, algo, cfg, sw, registry, handles, stats_out, out, None,
+                               explicit)
+    elif auto is not None and flags & _AUTO_ON:
+        if flags & _AUTO_READY:
+            auto[1]["gathered_calls"] = auto[1].get("gathered_calls", 0) + 1
+        _auto_after_call(grads, local, tp, auto[1])
     return res
+
+
+# Automatic member registration (the pointer cache applied to aggregate's
+# fused members): after the second aggregate() of the same name set whose
+# ready-set agreement passed with every rank offering it, every rank
+# registers its member tensors collectively (as register_gradients does);
+# from then on a rank whose members are still the registered tensors (same
+# addresses, same allocation ids) offers the gathered path, and the first
+# fused launch's agreement checks that every rank does — otherwise all ranks
+# skip and repeat the step with packed members. Every decision that leads to
+# a collective depends only on agreed calls, so ranks cannot diverge.
+_AUTO_ON = 1 << 40          # this rank takes part (device gradients, knob on)
+_AUTO_READY = 1 << 41       # ... and its members are the registered tensors
+
+
+def _auto_members(grads: GradientSet, local: list[str], tp):
+    """(flags, state) for this call, or None when not applicable."""
+    st = tp.__dict__.setdefault("_auto_agg", {}).setdefault(
+        grads.__dict__["_name_key"], {"count": 0, "ids": None, "ptrs": None, "bids": None, "disabled": False})
+    if st["disabled"]:
+        return 0, st
+    ts = [grads.get(nm) for nm in local]
+    if not all(t.is_cuda for t in ts) or tp.__dict__.get("_knobs", {}).get("auto_register", 2) <= 1:
+        return 0, st
+    if st["ids"] is None:
+        return _AUTO_ON, st
+    ptrs = tuple(t.payload.data_ptr() for t in ts)
+    if ptrs != st["ptrs"] or _buffer_ids(tp, ptrs) != st["bids"]:
+        return _AUTO_ON, st
+    return _AUTO_ON | _AUTO_READY, st
+
+
+def _buffer_ids(tp, ptrs) -> tuple:
+    ids = (C.c_uint64 * max(1, len(ptrs)))()
+    L.check(L.lib.cm_buffer_ids(tp._h, len(ptrs), L.ptr_array(list(ptrs)), ids))
+    return tuple(ids[:len(ptrs)])
+
+
+def _auto_after_call(grads, local, tp, st):
+    """After an agreed call in which every rank offered registration."""
+    st["count"] += 1
+    if st["count"] == 2 and st["ids"] is None:
+        ts = [grads.get(nm) for nm in local]
+        ids = tp.register_buffers([t.payload for t in ts])     # collective, once per name set
+        st["ids"] = dict(zip(local, ids))
+        st["ptrs"] = tuple(t.payload.data_ptr() for t in ts)
+        st["bids"] = _buffer_ids(tp, st["ptrs"])
 
 
 def register_gradients(grads: GradientSet, transport: Communicator) -> None:
@@ -275,13 +333,14 @@ def _device_of(tp):
     return torch.cuda.device(tp.device)
 
 
-def _aggregate_names(grads, names, tp, algo, cfg, sw, registry, handles, stats_out, out, agree):
+def _aggregate_names(grads, names, tp, algo, cfg, sw, registry, handles, stats_out, out, agree, regmap=None):
     if not names:
         return GradientSet((), grads.iteration)
     cache = grads.__dict__.setdefault("_plans", {})
-    plan = cache.get(tuple(names))
+    pkey = (tuple(names), id(regmap) if regmap is not None else None)
+    plan = cache.get(pkey)
     if plan is None:
-        plan = cache[tuple(names)] = _Plan(grads, names)
+        plan = cache[pkey] = _Plan(grads, names, regmap)
     if registry is not None and handles is not None:
         for grp in fuse_plan(plan.ready, cfg):       # aggregation.py:159-161
             for i in grp:

@@ -39,6 +39,7 @@ class _Base:
     # -- tuning / policy ------------------------------------------------------
     def set_param(self, key: str, value: int) -> None:
         L.check(L.lib.cm_comm_set_param(self._h, key.encode(), int(value)))
+        self.__dict__.setdefault("_knobs", {})[key] = int(value)     # read back by the façade
 
     def get_param(self, key: str) -> int:
         v = C.c_int64()

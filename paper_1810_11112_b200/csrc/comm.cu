@@ -1460,6 +1460,12 @@ int cm_comm_deregister(cm_comm_t* c, const void* ptr) {
   return CM_OK;
 }
 
+int cm_buffer_ids(cm_comm_t* c, int n, const void* const* ptrs, uint64_t* ids) {
+  if (n < 0 || (n > 0 && (!ptrs || !ids))) return fail(CM_ERR_VALUE, "bad arguments");
+  for (int i = 0; i < n; ++i) ids[i] = buffer_id_of(c, ptrs[i]);
+  return CM_OK;
+}
+
 int cm_comm_sync(cm_comm_t* c, void* stream) {
   CUDA_TRY(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
   return check_async_error(c);

@@ -341,6 +341,32 @@ def main():
     expect(comm.get_param("cluster_pairs") == 1 and comm.get_param("max_ctas") == 148,
            "overlapped aggregator restores the launch knobs")
 
+    # 4l. automatic member registration: plain gradient tensors (no
+    # register_gradients) are registered collectively after the second agreed
+    # aggregate of a name set; later steps read them in place. A rank that
+    # swaps a tensor for a new allocation makes every rank repeat the step
+    # with packed members and stop offering the gathered path. Bit-exact
+    # throughout.
+    auto_layers = [300_001, 1_000_003, 7, 2_000_000, 65_536]
+    auto_rank = [[(f"auto{i:03d}", a) for i, (_, a) in enumerate(I.synth_gradients(11, 0, auto_layers, r))]
+                 for r in range(world)]
+    want, _, _ = OA.aggregate(auto_rank, "float32", "auto", 64 << 20)
+    auto_ts = [torch.from_numpy(a).cuda() for _, a in auto_rank[rank]]
+    key = None
+    for step in range(7):
+        if step == 5 and rank == 0:
+            auto_ts[1] = auto_ts[1].clone()            # a new allocation on rank 0 only
+        gs = P.GradientSet(tuple(P.Tensor(nm, "float32", t) for (nm, _), t in zip(auto_rank[rank], auto_ts)))
+        res = P.aggregate(gs, group, comm)
+        expect(all(t.to_bytes() == want[t.name].tobytes() for t in res.tensors), f"auto-registered aggregate step {step}")
+        key = gs.__dict__["_name_key"]
+        st = comm.__dict__["_auto_agg"][key]
+        if step == 1:
+            expect(st["ids"] is not None, "members registered after the second agreed call")
+        if step == 4:
+            expect(st.get("gathered_calls", 0) == 3, f"gathered path used: {st.get('gathered_calls')}")
+    expect(st["disabled"], "a rank's new allocation turns the gathered path off on every rank")
+
     # 4k. the façade's two call paths into the C ABI (the fast-call module and
     # plain ctypes) give the same bits and stats
     from paper_1810_11112_b200 import _lib as LF
