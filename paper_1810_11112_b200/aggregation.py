@@ -302,7 +302,10 @@ def _auto_after_call(grads, local, tp, st):
     st["count"] += 1
     if st["count"] == 2 and st["ids"] is None:
         ts = [grads.get(nm) for nm in local]
-        ids = tp.register_buffers([t.payload for t in ts])     # collective, once per name set
+        ids = tp.register_buffers([t.payload for t in ts], tolerant=True)   # collective, once per name set
+        if ids is None:                     # some rank's allocations cannot be shared: stay packed
+            st["disabled"] = True
+            return
         st["ids"] = dict(zip(local, ids))
         st["ptrs"] = tuple(t.payload.data_ptr() for t in ts)
         st["bids"] = _buffer_ids(tp, st["ptrs"])

@@ -210,27 +210,36 @@ class Communicator(_Base):
         del self._sym[p]
         L.check(L.lib.cm_comm_free(self._h, p))
 
-    def register_buffers(self, tensors) -> list[int]:
+    def register_buffers(self, tensors, tolerant: bool = False) -> list[int] | None:
         """Collective: register device tensors for zero-copy collectives (every
         rank passes its own tensors, same count and order). Each rank exports
         the CUDA-IPC handle of the allocation holding the tensor plus the
         offset; handles are all-gathered on the control plane and every peer
         allocation is opened once (cached). Afterwards, collectives whose send
         buffer lies inside a registered tensor are read by peers in place. The
-        tensors must stay alive until ``deregister_buffers``."""
+        tensors must stay alive until ``deregister_buffers``.
+
+        ``tolerant``: an allocation that cannot be exported (e.g. a virtual-
+        memory segment) does not raise; every rank learns it in the same
+        all-gather and the call returns None everywhere (nothing registered)."""
         import torch.distributed as dist
         mine = []
         for t in tensors:
             h = (C.c_char * L.IPC_HANDLE_BYTES)()
             off = C.c_int64()
-            L.check(L.lib.cm_comm_export(self._h, t.data_ptr(), t.numel() * t.element_size(), h,
-                                         C.byref(off)))
+            st = L.lib.cm_comm_export(self._h, t.data_ptr(), t.numel() * t.element_size(), h, C.byref(off))
+            if st and tolerant:
+                mine = None
+                break
+            L.check(st)
             mine.append((bytes(h), int(off.value)))
         gathered = [None] * self.size
         if self.size > 1:
             dist.all_gather_object(gathered, mine, group=self._group)
         else:
             gathered = [mine]
+        if any(g is None for g in gathered):
+            return None
         ids = []
         for i, t in enumerate(tensors):
             handles = b"".join(gathered[q][i][0] for q in range(self.size))
