@@ -219,7 +219,7 @@ struct CollParams {
   // peer's differ, every rank skips the call identically (the start barrier
   // and the epoch advance still happen: the grid is the same on every rank),
   // CTA 0 reports it through agree_out[2*lr] = {ticket, ok} (host-mapped) and
-  // the last CTA leaves {agree_tag, agree_ok} in Ctrl for the gated launches
+  // CTA 0 leaves {agree_tag, agree_ok} in Ctrl for the gated launches
   int agree_inline;
   long long akey[MAXP], acnt[MAXP];
   unsigned long long* agree_out;
