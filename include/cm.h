@@ -210,6 +210,9 @@ int cm_comm_registry(cm_comm_t* comm, cm_registry_t** reg);
  *                         serialization: the next launch is scheduled while the
  *                         previous kernel drains and waits in griddepcontrol.wait
  *                         (device gap between launches 2.5 -> 0.6 us); 1 = off.
+ *   "pack_max_ctas"       CTA cap of the fusion pack (batched copy); 1 = none
+ *                         (default). OverlappedAggregator(pack_ctas=...) sets it
+ *                         so a pack next to the backward pass keeps SMs free
  *   "cluster_pairs"       2 = collective grids of <= 64 CTAs launch in 2-CTA
  *                         clusters (whole TPCs), so a capped collective next to
  *                         2-CTA-cluster GEMMs does not break their SM pairs;

@@ -111,6 +111,7 @@ struct cm_comm {
   int ovl_chunks = 4;                         // reduce chunks per progress report (overlap, ws)
   int ws = 0;                                 // multi-buffer two-shot: RS and AG warps in every CTA
   int pack_waves = 2;                         // batched copy: CTA waves (4 per SM per wave)
+  int pack_max_ctas = 0;                      // batched copy: CTA cap (0: none; overlapped aggregation)
   int pack_unroll = 4;                        // batched copy: 16-byte loads in flight per thread (4 or 8)
   bool pdl = true;                            // programmatic dependent launch of the collective kernels
   bool cluster2 = false;                      // capped collective grids in 2-CTA clusters (whole TPCs)
@@ -977,6 +978,7 @@ int launch_batched_copy(cm_comm* c, int n, const void* const* srcs, void* const*
     const int waves = c ? c->pack_waves : 2;
     int64_t nb = (P.start[m] + (64 << 10) - 1) / (64 << 10);
     nb = std::max<int64_t>(1, std::min<int64_t>(nb, (int64_t)sms * 4 * waves));
+    if (c && c->pack_max_ctas > 0) nb = std::min<int64_t>(nb, c->pack_max_ctas);
     void* args[] = {&P};
     ProfScope prof_scope(c, stream, 1, 2 * P.start[m]);
     const void* kfn = (c && c->pack_unroll == 8) ? (const void*)batched_copy_kernel<8> : (const void*)batched_copy_kernel<4>;
@@ -1293,6 +1295,7 @@ int cm_comm_set_param(cm_comm_t* c, const char* key, int64_t value) {
   else if (k == "overlap_chunks") c->ovl_chunks = (int)std::min<int64_t>(value, 1 << 20);
   else if (k == "ws") c->ws = value > 1 ? 1 : 0;
   else if (k == "pack_waves") c->pack_waves = (int)std::min<int64_t>(value, 64);
+  else if (k == "pack_max_ctas") c->pack_max_ctas = value <= 1 ? 0 : (int)std::min<int64_t>(value, 4096);
   else if (k == "pack_unroll") c->pack_unroll = value >= 8 ? 8 : 4;
   else if (k == "pdl") c->pdl = value > 1;
   else if (k == "cluster_pairs") c->cluster2 = value > 1;
@@ -1324,6 +1327,7 @@ int cm_comm_get_param(cm_comm_t* c, const char* key, int64_t* value) {
   else if (k == "overlap_chunks") *value = c->ovl_chunks;
   else if (k == "ws") *value = c->ws ? 2 : 1;
   else if (k == "pack_waves") *value = c->pack_waves;
+  else if (k == "pack_max_ctas") *value = c->pack_max_ctas ? c->pack_max_ctas : 1;
   else if (k == "pack_unroll") *value = c->pack_unroll;
   else if (k == "pdl") *value = c->pdl ? 2 : 1;
   else if (k == "cluster_pairs") *value = c->cluster2 ? 2 : 1;

@@ -47,7 +47,8 @@ class OverlappedAggregator:
     (None: the communicator's setting) — except the last group in launch
     order, which runs once the backward pass is done and gets the full grid;
     ``cluster_pairs``: capped grids launch in 2-CTA clusters so they occupy
-    whole TPCs (cuBLAS's 2-SM-cluster GEMMs keep their pairs);
+    whole TPCs (cuBLAS's 2-SM-cluster GEMMs keep their pairs); ``pack_ctas``
+    caps the member pack that precedes each overlapped collective;
     ``priority`` is the communication stream's priority (-1: high).
 
     Stream rules (as for NCCL communicators): the means are views of
@@ -59,7 +60,8 @@ class OverlappedAggregator:
 
     def __init__(self, schema, comm: Communicator, algo: str = "auto", cfg: FusionConfig | None = None,
                  switch_bytes: int | None = DEFAULT_SWITCH_BYTES, launch_order: str = "reverse",
-                 max_ctas: int | None = 64, priority: int = -1, cluster_pairs: bool = False):
+                 max_ctas: int | None = 64, priority: int = -1, cluster_pairs: bool = False,
+                 pack_ctas: int | None = None):
         if isinstance(schema, GradientSet):
             specs = [(t.name, t.len, t.dtype) for t in schema.tensors]
         else:
@@ -94,6 +96,7 @@ class OverlappedAggregator:
         self.stream = torch.cuda.Stream(dev, priority=priority)
         self.max_ctas = max_ctas
         self.cluster_pairs = cluster_pairs
+        self.pack_ctas = pack_ctas
         self.buckets = [torch.empty(sum(self.specs[i].len for i in m), dtype=DTYPES[self.specs[m[0]].dtype],
                                     device=dev) for m in self.groups]
         self.stats = [(L.Stats * 1)() for _ in self.groups]
@@ -166,10 +169,13 @@ class OverlappedAggregator:
         want = None if (last or not self.max_ctas) else self.max_ctas
         if want != self._cap_set:
             if want is not None and self._cap_saved is None:
-                self._cap_saved = (self.comm.get_param("max_ctas"), self.comm.get_param("cluster_pairs"))
+                self._cap_saved = (self.comm.get_param("max_ctas"), self.comm.get_param("cluster_pairs"),
+                                   self.comm.get_param("pack_max_ctas"))
             self.comm.set_param("max_ctas", want if want is not None else self._cap_saved[0])
             if self.cluster_pairs:   # capped grids take whole TPCs (see cm.h "cluster_pairs")
                 self.comm.set_param("cluster_pairs", 2 if want is not None else self._cap_saved[1])
+            if self.pack_ctas:       # the member pack next to the backward pass, capped too
+                self.comm.set_param("pack_max_ctas", self.pack_ctas if want is not None else self._cap_saved[2])
             self._cap_set = want
             if want is None:
                 self._cap_saved = None   # re-read next step (the caller may retune the communicator)
