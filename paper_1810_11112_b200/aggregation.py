@@ -250,7 +250,7 @@ def aggregate(grads: GradientSet, group: GroupSpec, transport: Communicator,
     if res is None:             # ready sets (or member-registration states) differ across ranks
         names = _negotiate_gather(local, group, tp)
         if auto is not None and names == local:
-            auto[1]["disabled"] = True      # the member-registration states differed: stop offering
+            _auto_reset(tp, auto[1])        # the member-registration states differed: start over
         # no gathered members here: every rank packs (the modes must match)
         res = _aggregate_names(grads, names, tp, algo, cfg, sw, registry, handles, stats_out, out, None,
                                explicit)
@@ -268,10 +268,17 @@ def aggregate(grads: GradientSet, group: GroupSpec, transport: Communicator,
 # from then on a rank whose members are still the registered tensors (same
 # addresses, same allocation ids) offers the gathered path, and the first
 # fused launch's agreement checks that every rank does — otherwise all ranks
-# skip and repeat the step with packed members. Every decision that leads to
-# a collective depends only on agreed calls, so ranks cannot diverge.
+# skip and repeat the step with packed members, and every rank drops the
+# registration and counts agreed calls from zero again, so members that moved
+# for good (new allocations every few steps, a resized layer) are registered
+# anew; after _AUTO_MAX_RESETS such resets the name set stays packed. The
+# agreed-call count is part of the agreed value, so every decision that leads
+# to a collective (the registration) depends only on agreed state and ranks
+# cannot diverge.
 _AUTO_ON = 1 << 40          # this rank takes part (device gradients, knob on)
 _AUTO_READY = 1 << 41       # ... and its members are the registered tensors
+_AUTO_COUNT = 42            # bits 42-43: agreed calls so far (saturating at 3)
+_AUTO_MAX_RESETS = 4
 
 
 def _auto_members(grads: GradientSet, local: list[str], tp):
@@ -283,12 +290,26 @@ def _auto_members(grads: GradientSet, local: list[str], tp):
     ts = [grads.get(nm) for nm in local]
     if not all(t.is_cuda for t in ts) or tp.__dict__.get("_knobs", {}).get("auto_register", 2) <= 1:
         return 0, st
+    on = _AUTO_ON | (min(st["count"], 3) << _AUTO_COUNT)
     if st["ids"] is None:
-        return _AUTO_ON, st
+        return on, st
     ptrs = tuple(t.payload.data_ptr() for t in ts)
     if ptrs != st["ptrs"] or _buffer_ids(tp, ptrs) != st["bids"]:
-        return _AUTO_ON, st
-    return _AUTO_ON | _AUTO_READY, st
+        return on, st
+    return on | _AUTO_READY, st
+
+
+def _auto_reset(tp, st):
+    """After a call whose agreement failed on the registration state (every
+    rank runs this for the same call): drop this rank's registration of the
+    name set and count agreed calls from zero, or stop offering for good."""
+    if st["ptrs"] is not None:
+        for ptr in st["ptrs"]:          # local bookkeeping only; peers' mappings stay cached
+            L.lib.cm_comm_deregister(tp._h, C.c_void_p(ptr))
+    st.update(count=0, ids=None, ptrs=None, bids=None)
+    st["resets"] = st.get("resets", 0) + 1
+    if st["resets"] > _AUTO_MAX_RESETS:
+        st["disabled"] = True
 
 
 def _buffer_ids(tp, ptrs) -> tuple:

@@ -345,15 +345,15 @@ def main():
     # register_gradients) are registered collectively after the second agreed
     # aggregate of a name set; later steps read them in place. A rank that
     # swaps a tensor for a new allocation makes every rank repeat the step
-    # with packed members and stop offering the gathered path. Bit-exact
-    # throughout.
+    # with packed members, drop the registration and register the members
+    # anew after two more agreed calls. Bit-exact throughout.
     auto_layers = [300_001, 1_000_003, 7, 2_000_000, 65_536]
     auto_rank = [[(f"auto{i:03d}", a) for i, (_, a) in enumerate(I.synth_gradients(11, 0, auto_layers, r))]
                  for r in range(world)]
     want, _, _ = OA.aggregate(auto_rank, "float32", "auto", 64 << 20)
     auto_ts = [torch.from_numpy(a).cuda() for _, a in auto_rank[rank]]
     key = None
-    for step in range(7):
+    for step in range(10):
         if step == 5 and rank == 0:
             auto_ts[1] = auto_ts[1].clone()            # a new allocation on rank 0 only
         gs = P.GradientSet(tuple(P.Tensor(nm, "float32", t) for (nm, _), t in zip(auto_rank[rank], auto_ts)))
@@ -365,7 +365,13 @@ def main():
             expect(st["ids"] is not None, "members registered after the second agreed call")
         if step == 4:
             expect(st.get("gathered_calls", 0) == 3, f"gathered path used: {st.get('gathered_calls')}")
-    expect(st["disabled"], "a rank's new allocation turns the gathered path off on every rank")
+        if step == 5:
+            expect(st["ids"] is None and st.get("resets") == 1,
+                   "a rank's new allocation drops the registration on every rank")
+        if step == 7:
+            expect(st["ids"] is not None, "members registered again after two more agreed calls")
+    expect(not st["disabled"] and st.get("gathered_calls", 0) == 5,
+           f"gathered path used again after re-registration: {st.get('gathered_calls')}")
 
     # 4k. the façade's two call paths into the C ABI (the fast-call module and
     # plain ctypes) give the same bits and stats
