@@ -151,3 +151,18 @@ for name, fn in (("dma_members", dma_members), ("kernel_members", k_members), ("
     res[name] = ms
 print(f"rank {rank}/{world} member-wise 53 x 1.92 MB: " + " | ".join(f"{k} {v:.3f} ms" for k, v in res.items()),
       flush=True)
+
+# ---- host -> host through the SMs (one kernel reads pinned host memory over
+# PCIe and writes pinned host memory: both directions at once, no staging and
+# no H2D -> D2H dependency)
+hflat_in = torch.empty(M * E, dtype=torch.uint8).pin_memory()
+res = {}
+for name, fn in (("kernel_h2h_members", lambda: kcopy([h.data_ptr() for h in hm],
+                                                      [hout.data_ptr() + i * E for i in range(M)], [E] * M,
+                                                      torch.cuda.current_stream())),
+                 ("kernel_h2h_flat", lambda: kcopy([hflat_in.data_ptr()], [hout.data_ptr()], [M * E],
+                                                   torch.cuda.current_stream()))):
+    ms = timed(fn)
+    res[name] = ms
+print(f"rank {rank}/{world} host->host kernel, {M * E / 1e6:.2f} MB: " +
+      " | ".join(f"{k} {v:.3f} ms ({M * E / (v * 1e-3) / 1e9:.1f} GB/s each way)" for k, v in res.items()), flush=True)
