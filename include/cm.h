@@ -185,8 +185,14 @@ int cm_comm_registry(cm_comm_t* comm, cm_registry_t** reg);
  *   "dyn_ag"              2 = the allgather is a (slice, peer) task queue shared
  *                         by the CTAs, 1 = each CTA pulls its own slice index
  *                         after a per-index barrier (default; measured equal)
- *   "host_chunk_kb"       KiB per H2D/D2H piece of the single-rank host-gradient
- *                         pipeline (default 8192; 2048/4096/16384 measured slower)
+ *   "host_chunk_kb"       KiB per H2D/D2H piece of the host-gradient pipeline
+ *                         (default 8192; at p = 1 2048/4096/16384 measured slower)
+ *   "host_split"          2 = with host gradients at p > 1, a two-shot fused group
+ *                         moves H2D -> collective -> D2H in ~host_piece_kb pieces
+ *                         (the k-th 1/K of every rank's segment: same owners and
+ *                         fold order as one launch, bit-identical); 1 = one
+ *                         launch per group
+ *   "host_piece_kb"       KiB per piece of host_split (default 4096)
  *   "bulk_stage_kb"       KiB per bulk-reduce stage (default 64; the stage count
  *                         is clamped to the shared memory available)
  *   "inline_agree"        2 = aggregate's ready-set agreement travels in the fused

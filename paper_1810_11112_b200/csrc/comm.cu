@@ -113,10 +113,12 @@ struct cm_comm {
   int pack_waves = 2;                         // batched copy: CTA waves (4 per SM per wave)
   int pack_max_ctas = 0;                      // batched copy: CTA cap (0: none; overlapped aggregation)
   int pack_unroll = 4;                        // batched copy: 16-byte loads in flight per thread (4 or 8)
+  bool host_split = true;                     // host pipeline (p > 1): fused groups move in pieces
+  int64_t host_piece = 4 << 20;               // ... of about this many bytes
   bool pdl = true;                            // programmatic dependent launch of the collective kernels
   bool cluster2 = false;                      // capped collective grids in 2-CTA clusters (whole TPCs)
   int bulk_stage = 2 * RS_STAGE_BYTES;        // bytes per bulk-reduce stage (64 KiB: 3 stages fit)
-  int64_t host_chunk = 8 << 20;               // host-gradient pipeline: bytes per H2D/D2H piece (p = 1)
+  int64_t host_chunk = 8 << 20;               // host-gradient pipeline: bytes per H2D/D2H piece
   int64_t oneshot_bytes_per_cta = 8 * 1024;
   int64_t twoshot_bytes_per_cta = 4 * 1024;
   int max_ctas = 148;
@@ -326,6 +328,29 @@ unsigned long long make_hdr(int64_t n, int dtype, int op, int order, int phases,
   return h;
 }
 
+// Segment of every rank (ring chunk_partition or rhd layout of n elements),
+// optionally only the piece-th 1/npieces of each, cut on SLICE_ALIGN element
+// boundaries: the host pipeline moves a fused buffer through H2D -> collective
+// -> D2H in such pieces, and every element keeps the owner (and so the fold
+// order) it has in the whole-buffer allreduce, so pieces are bit-identical to
+// one launch over the buffer.
+void segments_of(int64_t n, int p, int layout, int piece, int npieces, int64_t* off, int64_t* len) {
+  if (layout == CM_LAYOUT_RHD) rhd_layout(n, p, off, len);
+  else chunk_partition(n, p, off, len);
+  if (npieces <= 1) return;
+  for (int q = 0; q < p; ++q) {
+    auto cut = [&](int i) -> int64_t {
+      if (i <= 0) return off[q];
+      if (i >= npieces) return off[q] + len[q];
+      const int64_t x = (off[q] + len[q] * i / npieces) / SLICE_ALIGN * SLICE_ALIGN;
+      return std::min(std::max(x, off[q]), off[q] + len[q]);
+    };
+    const int64_t a = cut(piece), z = cut(piece + 1);
+    off[q] = a;
+    len[q] = z - a;
+  }
+}
+
 struct Launch {
   int64_t n = 0;
   int dtype = 0, op = 0, order = ORD_SEQ, phases = PH_RS | PH_AG, oneshot = 0;
@@ -349,6 +374,7 @@ struct Launch {
   int force_pull = 0;               // pull collective kernel on the full grid (inline agreement:
                                     // the launch must have the same shape on every rank)
   int ll = 0;                       // one-shot through the LL slots
+  int piece = 0, npieces = 1;       // host pipeline: the piece-th 1/npieces of every segment
   const void* in[MAXP] = {};
   void* out[MAXP] = {};
   int64_t zc_srcoff[MAXP] = {};
@@ -369,10 +395,8 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
   int64_t off[MAXP], len[MAXP];
   if (L.oneshot) {
     for (int q = 0; q < p; ++q) { off[q] = 0; len[q] = L.n; }
-  } else if (L.layout == CM_LAYOUT_RHD) {
-    rhd_layout(L.n, p, off, len);
   } else {
-    chunk_partition(L.n, p, off, len);
+    segments_of(L.n, p, L.layout, L.piece, L.npieces, off, len);
   }
   int64_t maxseg = 0;
   for (int q = 0; q < p; ++q) {
@@ -448,7 +472,7 @@ int launch_collective(cm_comm* c, const Launch& L, cudaStream_t stream) {
   int64_t nb = (work + per - 1) / per;
   int ll = L.ll;
   // literal recursive halving/doubling (log2 p pairwise steps) for rhd_rsa allreduce
-  const bool logp = !L.force_pull && c->rhd_logp && L.order == ORD_TREE && L.nbuf == 1 && L.dtype != CM_BFLOAT16 &&
+  const bool logp = !L.force_pull && L.npieces == 1 && c->rhd_logp && L.order == ORD_TREE && L.nbuf == 1 && L.dtype != CM_BFLOAT16 &&
                     !L.out_rel && (L.oneshot || L.phases == (PH_RS | PH_AG)) &&
                     (L.srcmode == SRC_COPYIN || L.srcmode == SRC_ZEROCOPY || L.srcmode == SRC_REGISTERED);
   if (logp || L.force_pull) ll = 0;
@@ -1297,6 +1321,8 @@ int cm_comm_set_param(cm_comm_t* c, const char* key, int64_t value) {
   else if (k == "pack_waves") c->pack_waves = (int)std::min<int64_t>(value, 64);
   else if (k == "pack_max_ctas") c->pack_max_ctas = value <= 1 ? 0 : (int)std::min<int64_t>(value, 4096);
   else if (k == "pack_unroll") c->pack_unroll = value >= 8 ? 8 : 4;
+  else if (k == "host_split") c->host_split = value > 1;
+  else if (k == "host_piece_kb") c->host_piece = std::max<int64_t>(64, std::min<int64_t>(value, 1 << 20)) * 1024;
   else if (k == "pdl") c->pdl = value > 1;
   else if (k == "cluster_pairs") c->cluster2 = value > 1;
   else if (k == "host_chunk_kb") c->host_chunk = std::max<int64_t>(64, value) * 1024;
@@ -1329,6 +1355,8 @@ int cm_comm_get_param(cm_comm_t* c, const char* key, int64_t* value) {
   else if (k == "pack_waves") *value = c->pack_waves;
   else if (k == "pack_max_ctas") *value = c->pack_max_ctas ? c->pack_max_ctas : 1;
   else if (k == "pack_unroll") *value = c->pack_unroll;
+  else if (k == "host_split") *value = c->host_split ? 2 : 1;
+  else if (k == "host_piece_kb") *value = c->host_piece / 1024;
   else if (k == "pdl") *value = c->pdl ? 2 : 1;
   else if (k == "cluster_pairs") *value = c->cluster2 ? 2 : 1;
   else if (k == "auto_published") *value = c->auto_published;
@@ -1891,17 +1919,47 @@ int fused_impl(cm_comm* c, int n, const void* const* sends, const int64_t* count
   };
   // host-input groups: every group's H2D is queued up front on the h2d stream
   // (into indev at the local rank's and the group's offset); each collective
-  // waits only for its own group's event
-  std::vector<cudaEvent_t> in_ready(gr.size(), nullptr);
+  // waits only for its own input's event. A two-shot group moves in pieces of
+  // ~host_piece bytes (the piece-th 1/K of every rank's segment, segments_of):
+  // H2D of piece k+1 overlaps the collective of piece k and the D2H of piece
+  // k-1, so only one piece, not the whole group, fills and drains the pipeline
+  std::vector<std::vector<cudaEvent_t>> in_ready(gr.size());
   auto indev_at = [&](int lr, const Grp& G) { return c->indev + (int64_t)lr * total_bytes + G.off * sz; };
+  auto npieces = [&](const Grp& G) -> int {
+    if (!c->host_split || !G.any_host || G.L.ll != 0 || G.L.oneshot || G.L.phases != (PH_RS | PH_AG)) return 1;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(128, (G.ng * sz + c->host_piece / 2) / c->host_piece));
+  };
+  // element ranges [a, z) of piece k of group G (one per rank segment)
+  auto piece_ranges = [&](const Grp& G, int k, int K, int64_t* a, int64_t* z) {
+    int64_t off[MAXP], len[MAXP];
+    segments_of(G.ng, p, G.L.layout, k, K, off, len);
+    for (int q = 0; q < p; ++q) { a[q] = off[q]; z[q] = off[q] + len[q]; }
+  };
   for (size_t t = 0; t < gr.size(); ++t) {
     if (!gr[t].any_host) continue;
     std::vector<int64_t> gb(nbytes.begin() + gr[t].i, nbytes.begin() + gr[t].j);
+    const int K = npieces(gr[t]);
+    in_ready[t].assign(K, nullptr);
+    std::vector<std::vector<Run>> runs(nloc);
     for (int lr = 0; lr < nloc; ++lr)
-      for (const Run& r : coalesce(sends + (size_t)lr * n + gr[t].i, gb.data(), gr[t].j - gr[t].i, INT64_MAX))
-        CUDA_TRY(cudaMemcpyAsync(indev_at(lr, gr[t]) + r.off, r.src, r.bytes, cudaMemcpyDefault, c->h2d));
-    if ((st = hp.ev(&in_ready[t]))) return st;
-    CUDA_TRY(cudaEventRecord(in_ready[t], c->h2d));
+      runs[lr] = coalesce(sends + (size_t)lr * n + gr[t].i, gb.data(), gr[t].j - gr[t].i, INT64_MAX);
+    for (int k = 0; k < K; ++k) {
+      int64_t a[MAXP], z[MAXP];
+      if (K > 1) piece_ranges(gr[t], k, K, a, z);
+      const int nr = K > 1 ? p : 1;
+      for (int lr = 0; lr < nloc; ++lr)
+        for (int q = 0; q < nr; ++q) {
+          const int64_t lo = K > 1 ? a[q] * sz : 0, hi = K > 1 ? z[q] * sz : gr[t].ng * sz;
+          for (const Run& r : runs[lr]) {           // the runs' parts inside [lo, hi)
+            const int64_t x = std::max(lo, r.off), y = std::min(hi, r.off + r.bytes);
+            if (y > x)
+              CUDA_TRY(cudaMemcpyAsync(indev_at(lr, gr[t]) + x, r.src + (x - r.off), y - x, cudaMemcpyDefault,
+                                       c->h2d));
+          }
+        }
+      if ((st = hp.ev(&in_ready[t][k]))) return st;
+      CUDA_TRY(cudaEventRecord(in_ready[t][k], c->h2d));
+    }
   }
   // host outputs: after the launch of groups [a, b), copy their results out
   auto drain = [&](size_t a, size_t b) -> int {
@@ -2001,8 +2059,34 @@ int fused_impl(cm_comm* c, int n, const void* const* sends, const int64_t* count
     }
     Grp& G = gr[g];
     Launch L = G.L;
+    if (G.any_host && in_ready[g].size() > 1) {   // piece by piece (see the H2D loop above)
+      const int K = (int)in_ready[g].size();
+      for (int k = 0; k < K; ++k) {
+        Launch Lk = G.L;
+        CUDA_TRY(cudaStreamWaitEvent(stream, in_ready[g][k], 0));
+        Lk.srcmode = SRC_COPYIN;
+        Lk.piece = k;
+        Lk.npieces = K;
+        for (int lr = 0; lr < nloc; ++lr) Lk.in[lr] = indev_at(lr, G);
+        tag_launch(Lk);
+        if ((st = launch_collective(c, Lk, stream))) return st;
+        if (out_host) {
+          if ((st = hp.link(stream, c->d2h))) return st;
+          int64_t a[MAXP], z[MAXP];
+          piece_ranges(G, k, K, a, z);
+          for (int lr = 0; lr < nloc; ++lr)
+            for (int q = 0; q < p; ++q)
+              if (z[q] > a[q])
+                CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(recvs[lr]) + (G.off + a[q]) * sz,
+                                         outbase(lr) + (G.off + a[q]) * sz, (z[q] - a[q]) * sz,
+                                         cudaMemcpyDeviceToHost, c->d2h));
+        }
+      }
+      ++g;
+      continue;
+    }
     if (G.any_host) {  // inputs arrive in indev on the h2d stream, then copy-in
-      CUDA_TRY(cudaStreamWaitEvent(stream, in_ready[g], 0));
+      CUDA_TRY(cudaStreamWaitEvent(stream, in_ready[g][0], 0));
       L.srcmode = SRC_COPYIN;
       for (int lr = 0; lr < nloc; ++lr) L.in[lr] = indev_at(lr, G);
     } else {         // pack straight into the IPC staging area (no extra copy)

@@ -257,7 +257,9 @@ def main():
     # 4b. host gradients through the copy-stream pipeline (H2D / collectives /
     # D2H overlapped): pinned, pageable and mixed host/device members, many
     # fused groups, persistent pinned output buckets refilled by out=
-    for algo in ("ring_rsa", "auto"):
+    # (host_piece_kb=300: every fused group moves in ~300 KiB pieces)
+    for algo, chunk_kb in (("ring_rsa", 4096), ("auto", 4096), ("ring_rsa", 300), ("rhd_rsa", 300)):
+        comm.set_param("host_piece_kb", chunk_kb)
         want, groups, _ = OA.aggregate(per_rank, "float32", algo, 8 << 20)
         want2, _, _ = OA.aggregate([[(nm, a * 2) for nm, a in pr] for pr in per_rank], "float32", algo, 8 << 20)
         flat = torch.empty(sum(a.size for _, a in per_rank[rank]), dtype=torch.float32).pin_memory()
@@ -282,7 +284,8 @@ def main():
             expect(all(t.to_bytes() == want[t.name].tobytes() for t in res.tensors), f"host aggregate {algo} {kind}")
             res2 = P.aggregate(mk(2), group, comm, algo=algo, cfg=P.FusionConfig(8 << 20), out=res)
             expect(res2 is res and all(t.to_bytes() == want2[t.name].tobytes() for t in res2.tensors),
-                   f"host aggregate out= refill {algo} {kind}")
+                   f"host aggregate out= refill {algo} {kind} chunk {chunk_kb}")
+    comm.set_param("host_piece_kb", 4096)
 
     # 4e. a fused group larger than the staging area is a ConfigError on every rank
     small = P.Communicator(staging_bytes=16 << 20, pool_bytes=2 << 20, timeout_s=20.0)

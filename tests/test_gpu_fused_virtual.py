@@ -183,6 +183,24 @@ def test_host_gradients_through_copy_streams(p, where):
     assert all(not t.is_cuda for o in outs for t in o.tensors)
 
 
+@pytest.mark.parametrize("p", [2, 3, 4, 8])
+@pytest.mark.parametrize("algo", ["ring_rsa", "rhd_rsa", "auto"])
+@pytest.mark.parametrize("split", [1, 2])
+def test_host_gradients_in_pipeline_pieces(p, algo, split):
+    """Host gradients move H2D -> collective -> D2H in host_piece_kb pieces (the
+    piece-th 1/K of every rank's segment, so every element keeps its owner and
+    fold order): bit-identical to the whole-group launch and the reference;
+    host_split=1 is the one-launch-per-group pipeline."""
+    layers = [480_000] * 12 + [1_000_003, 77, 65_536]
+    per_rank = [I.synth_gradients(19, 0, layers, r) for r in range(p)]
+    want, _, _ = OA.aggregate(per_rank, "float32", algo, 8 << 20)
+    g = vg(p, host_piece_kb=300, host_split=split)
+    for where in ("pinned", "mixed"):
+        outs = P.aggregate_group(sets_of(per_rank, where=where), g, algo=algo, cfg=P.FusionConfig(8 << 20))
+        check(outs, want)
+        assert all(not t.is_cuda for o in outs for t in o.tensors)
+
+
 @pytest.mark.parametrize("p", [2, 4, 8])
 def test_bf16_and_fp64_fused(p):
     layers = [100_000, 7, 300_001, 64]
