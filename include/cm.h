@@ -101,6 +101,10 @@ int cm_chunk_partition(int64_t n, int p, int64_t* offsets, int64_t* lengths);
 /* ownership after reduce-scatter: ring = chunk_partition, rhd = halving segments
  * (collectives.py:198-216; folded odd ranks own (0,0)) */
 int cm_layout(int layout, int64_t n, int p, int64_t* offsets, int64_t* lengths);
+/* piece `piece` of `npieces` of every rank's segment (the host-gradient
+ * pipeline's unit, cm.h "host_split"): the piece-th 1/npieces of each segment,
+ * cut on 64-element boundaries; pieces of a segment are disjoint and cover it */
+int cm_layout_piece(int layout, int64_t n, int p, int piece, int npieces, int64_t* offsets, int64_t* lengths);
 /* resolve_algorithm collectives.py:239-247 (CM_ERR_CONFIG on bad algo/switch) */
 int cm_resolve_algorithm(int algo, int64_t nbytes, int64_t switch_bytes, int* concrete);
 /* CollectiveStats the reference reports for (algo, p, rank, n) — collectives.py:75-236 */

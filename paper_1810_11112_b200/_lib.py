@@ -81,6 +81,7 @@ _SIGS = {
     "cm_dtype_size": ([_i], C.c_size_t),
     "cm_chunk_partition": ([_i64, _i, _P(_i64), _P(_i64)], _i),
     "cm_layout": ([_i, _i64, _i, _P(_i64), _P(_i64)], _i),
+    "cm_layout_piece": ([_i, _i64, _i, _i, _i, _P(_i64), _P(_i64)], _i),
     "cm_resolve_algorithm": ([_i, _i64, _i64, _P(_i)], _i),
     "cm_algo_stats": ([_i, _i, _i, _i64, _i, _i64, _P(Stats)], _i),
     "cm_rs_stats": ([_i, _i, _i, _i64, _i, _P(Stats)], _i),

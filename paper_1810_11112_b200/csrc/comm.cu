@@ -328,28 +328,7 @@ unsigned long long make_hdr(int64_t n, int dtype, int op, int order, int phases,
   return h;
 }
 
-// Segment of every rank (ring chunk_partition or rhd layout of n elements),
-// optionally only the piece-th 1/npieces of each, cut on SLICE_ALIGN element
-// boundaries: the host pipeline moves a fused buffer through H2D -> collective
-// -> D2H in such pieces, and every element keeps the owner (and so the fold
-// order) it has in the whole-buffer allreduce, so pieces are bit-identical to
-// one launch over the buffer.
-void segments_of(int64_t n, int p, int layout, int piece, int npieces, int64_t* off, int64_t* len) {
-  if (layout == CM_LAYOUT_RHD) rhd_layout(n, p, off, len);
-  else chunk_partition(n, p, off, len);
-  if (npieces <= 1) return;
-  for (int q = 0; q < p; ++q) {
-    auto cut = [&](int i) -> int64_t {
-      if (i <= 0) return off[q];
-      if (i >= npieces) return off[q] + len[q];
-      const int64_t x = (off[q] + len[q] * i / npieces) / SLICE_ALIGN * SLICE_ALIGN;
-      return std::min(std::max(x, off[q]), off[q] + len[q]);
-    };
-    const int64_t a = cut(piece), z = cut(piece + 1);
-    off[q] = a;
-    len[q] = z - a;
-  }
-}
+static_assert(SLICE_ALIGN == 64, "segments_of (hostlogic.cpp) cuts pieces on 64-element slice boundaries");
 
 struct Launch {
   int64_t n = 0;

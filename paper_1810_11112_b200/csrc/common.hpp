@@ -37,6 +37,7 @@ inline const char* dtype_name(int dtype) {
 // Reference-schedule helpers (hostlogic.cpp)
 void chunk_partition(int64_t n, int p, int64_t* off, int64_t* len);
 void rhd_layout(int64_t n, int p, int64_t* off, int64_t* len);
+void segments_of(int64_t n, int p, int layout, int piece, int npieces, int64_t* off, int64_t* len);
 int rhd_vrank(int rank, int p);  // -1 for folded odd ranks
 
 }  // namespace cm

@@ -132,6 +132,33 @@ static cm_stats_t flat_stats(int p, int rank, int64_t n, int64_t isz) {   // :82
 
 }  // namespace cm
 
+namespace cm {
+constexpr int64_t kSliceAlign = 64;   // = dev::SLICE_ALIGN (kernel slice boundaries)
+// Segment of every rank (ring chunk_partition or rhd layout of n elements),
+// optionally only the piece-th 1/npieces of each, cut on kSliceAlign element
+// boundaries: the host pipeline moves a fused buffer through H2D -> collective
+// -> D2H in such pieces, and every element keeps the owner (and so the fold
+// order) it has in the whole-buffer allreduce, so pieces are bit-identical to
+// one launch over the buffer.
+void segments_of(int64_t n, int p, int layout, int piece, int npieces, int64_t* off, int64_t* len) {
+  if (layout == CM_LAYOUT_RHD) rhd_layout(n, p, off, len);
+  else chunk_partition(n, p, off, len);
+  if (npieces <= 1) return;
+  for (int q = 0; q < p; ++q) {
+    auto cut = [&](int i) -> int64_t {
+      if (i <= 0) return off[q];
+      if (i >= npieces) return off[q] + len[q];
+      const int64_t x = (off[q] + len[q] * i / npieces) / kSliceAlign * kSliceAlign;
+      return std::min(std::max(x, off[q]), off[q] + len[q]);
+    };
+    const int64_t a = cut(piece), z = cut(piece + 1);
+    off[q] = a;
+    len[q] = z - a;
+  }
+}
+
+}  // namespace cm
+
 using namespace cm;
 
 extern "C" {
@@ -144,6 +171,15 @@ int cm_chunk_partition(int64_t n, int p, int64_t* offsets, int64_t* lengths) {
   if (p < 1) return fail(CM_ERR_INVALID_GROUP, "cannot partition over p=" + std::to_string(p) + " processes");
   if (n < 0) return fail(CM_ERR_SHAPE, "negative element count " + std::to_string(n));
   chunk_partition(n, p, offsets, lengths);
+  return CM_OK;
+}
+
+int cm_layout_piece(int layout, int64_t n, int p, int piece, int npieces, int64_t* offsets, int64_t* lengths) {
+  if (p < 1) return fail(CM_ERR_INVALID_GROUP, "group size must be >= 1");
+  if (n < 0) return fail(CM_ERR_SHAPE, "negative element count");
+  if (layout != CM_LAYOUT_RING && layout != CM_LAYOUT_RHD) return fail(CM_ERR_CONFIG, "unknown layout");
+  if (npieces < 1 || piece < 0 || piece >= npieces) return fail(CM_ERR_VALUE, "piece out of range");
+  segments_of(n, p, layout, piece, npieces, offsets, lengths);
   return CM_OK;
 }
 

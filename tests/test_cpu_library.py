@@ -65,6 +65,29 @@ def test_chunk_partition_and_layouts_match_oracle(p):
         assert P.layout("rhd", n, p) == OC.layout("rhd", n, p)
 
 
+@settings(max_examples=300, deadline=None)
+@given(st.integers(0, 3_000_000), st.integers(1, 16), st.sampled_from([0, 1]), st.integers(1, 40))
+def test_layout_pieces_cover_every_segment(n, p, layout, K):
+    """cm_layout_piece (the host-gradient pipeline's unit, cm.h host_split):
+    for every rank, the K pieces of its segment are consecutive, disjoint,
+    cover the segment exactly and are cut on 64-element boundaries — so every
+    element is reduced by the owner (and in the fold order) it has in the
+    whole-buffer allreduce."""
+    import ctypes as C
+    whole = P.layout("ring" if layout == 0 else "rhd", n, p)
+    off, ln = (C.c_int64 * p)(), (C.c_int64 * p)()
+    for q, (o, l) in enumerate(whole):
+        pos = o
+        for k in range(K):
+            assert L.lib.cm_layout_piece(layout, n, p, k, K, off, ln) == 0
+            assert off[q] == pos and ln[q] >= 0
+            if 0 < k:
+                assert off[q] % 64 == 0 or off[q] in (o, o + l)
+            pos += ln[q]
+        assert pos == o + l
+    assert L.lib.cm_layout_piece(layout, n, p, K, K, off, ln) != 0
+
+
 @settings(max_examples=200, deadline=None)
 @given(st.integers(0, 1000), st.integers(1, 64))
 def test_chunk_partition_property(n, p):
