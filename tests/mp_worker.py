@@ -488,6 +488,30 @@ def main():
                 expect(bool(torch.all(out.payload == float(sum(r + k for r in range(world))))),
                        f"after differing plans: allreduce {k} inline={inline} thr={thr}")
     comm.set_param("inline_agree", 2)
+    # ... and with pinned host gradients, whose fused groups move through the
+    # host pipeline in pieces (rank 0's extra tensor changes its piece and
+    # launch count): every gated piece is skipped, the intersection is
+    # aggregated, later host and device calls line up
+    def host_set(items):
+        return P.GradientSet(tuple(P.Tensor(nm, "float32", torch.from_numpy(a).pin_memory()) for nm, a in items))
+    want_t, _, _ = OA.aggregate([I.synth_gradients(11, 0, [480_000] * 20 + [3, 1_000_000, 64], r)
+                                 for r in range(world)], "float32", "auto", 64 << 20)
+    for piece_kb in (4096, 700):
+        comm.set_param("host_piece_kb", piece_kb)
+        res = P.aggregate(host_set(base + extra), group, comm, cfg=P.FusionConfig(64 << 20))
+        expect(res.names == sorted(nm for nm, _ in base) and not res.tensors[0].is_cuda,
+               f"differing plans, host pieces {piece_kb}: names")
+        expect(all(t.to_bytes() == want_t[t.name].tobytes() for t in res.tensors),
+               f"differing plans, host pieces {piece_kb}: values")
+        for k in range(2):
+            rk = P.aggregate(host_set(base), group, comm, cfg=P.FusionConfig(64 << 20))
+            expect(all(t.to_bytes() == want_t[t.name].tobytes() for t in rk.tensors),
+                   f"after differing plans, host pieces {piece_kb}: aggregate {k}")
+            x = torch.full((70_001 + k,), float(rank + k), device="cuda")
+            out, _ = P.allreduce(P.Tensor("x", "float32", x), P.ReduceOp.SUM, group, comm)
+            expect(bool(torch.all(out.payload == float(sum(r + k for r in range(world))))),
+                   f"after differing plans, host pieces {piece_kb}: allreduce {k}")
+    comm.set_param("host_piece_kb", 4096)
 
     # 4i. the communicator's pointer cache (registry.py:104-131): every call
     # classifies send and recv; no_cache queries the driver each time,
