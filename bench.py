@@ -879,7 +879,7 @@ def overlap(args, rank, world, local):
     gs_view = P.GradientSet(tuple(P.Tensor(nm, "float32", g) for nm, g in zip(names, grads)))
     ov = P.OverlappedAggregator(gs_view, comm, algo=args.algo, cfg=cfg, max_ctas=args.ov_ctas or None,
                                 priority=args.ov_priority, cluster_pairs=bool(args.ov_pairs),
-                                pack_ctas=args.ov_pack_ctas or None)
+                                pack_ctas=args.ov_pack_ctas or None, register_members=bool(args.ov_register))
 
     def step_seq():
         backward()
@@ -934,7 +934,7 @@ def overlap(args, rank, world, local):
               "hidden_frac": round((t_seq - t_ovl) / max(t_seq - t_bwd, 1e-9), 3),
               "groups": len(ov.groups), "ov_ctas": args.ov_ctas, "ov_priority": args.ov_priority,
               "gemm_carveout": args.gemm_carveout, "backward_carveout_ms": round(t_bwd_cv, 4),
-              "ov_pairs": args.ov_pairs, "ov_pack_ctas": args.ov_pack_ctas,
+              "ov_pairs": args.ov_pairs, "ov_pack_ctas": args.ov_pack_ctas, "ov_register": args.ov_register,
               "bit_identical": same})
     comm.close()
 
@@ -951,6 +951,8 @@ def main():
     ap.add_argument("--ov-priority", type=int, default=-1, help="overlap: communication stream priority")
     ap.add_argument("--ov-pairs", type=int, default=0, help="overlap: capped grids in 2-CTA clusters (1: on)")
     ap.add_argument("--ov-pack-ctas", type=int, default=0, help="overlap: CTA cap of the member pack (0: none)")
+    ap.add_argument("--ov-register", type=int, default=0,
+                    help="overlap: register the persistent gradient buffers after the first step (1: on)")
     ap.add_argument("--gemm-carveout", type=int, default=0,
                     help="overlap: SMs the backward GEMMs leave free while the collectives overlap them "
                          "(cuBLAS SM carve-out, overlapped step only; 0: none)")

@@ -49,7 +49,14 @@ class OverlappedAggregator:
     ``cluster_pairs``: capped grids launch in 2-CTA clusters so they occupy
     whole TPCs (cuBLAS's 2-SM-cluster GEMMs keep their pairs); ``pack_ctas``
     caps the member pack that precedes each overlapped collective;
-    ``priority`` is the communication stream's priority (-1: high).
+    ``priority`` is the communication stream's priority (-1: high);
+    ``register_members``: at the end of the first step every rank registers
+    the gradient tensors it handed to ``ready()`` (collective, the pointer
+    cache's IPC side, as ``register_gradients``), and from then on peers read
+    them in place — no member pack next to the backward pass. The caller
+    hands over the same tensors every step (a framework's persistent
+    gradient buffers); a rank whose tensors moved packs instead, which the
+    fused launch's header check turns into a ShapeError on every rank.
 
     Stream rules (as for NCCL communicators): the means are views of
     persistent per-group buckets that the next step overwrites once its
@@ -61,7 +68,7 @@ class OverlappedAggregator:
     def __init__(self, schema, comm: Communicator, algo: str = "auto", cfg: FusionConfig | None = None,
                  switch_bytes: int | None = DEFAULT_SWITCH_BYTES, launch_order: str = "reverse",
                  max_ctas: int | None = 64, priority: int = -1, cluster_pairs: bool = False,
-                 pack_ctas: int | None = None):
+                 pack_ctas: int | None = None, register_members: bool = False):
         if isinstance(schema, GradientSet):
             specs = [(t.name, t.len, t.dtype) for t in schema.tensors]
         else:
@@ -97,6 +104,9 @@ class OverlappedAggregator:
         self.max_ctas = max_ctas
         self.cluster_pairs = cluster_pairs
         self.pack_ctas = pack_ctas
+        self.register_members = register_members
+        self._reg = [None] * len(self.groups)        # per group: member reg ids (C int64 array)
+        self._regptrs = [None] * len(self.groups)    # ... and the member addresses they belong to
         self.buckets = [torch.empty(sum(self.specs[i].len for i in m), dtype=DTYPES[self.specs[m[0]].dtype],
                                     device=dev) for m in self.groups]
         self.stats = [(L.Stats * 1)() for _ in self.groups]
@@ -187,9 +197,13 @@ class OverlappedAggregator:
         returns the number of fused buffers it ran as."""
         pa, ca, sa, out = self._addr[g]
         comm = self.comm
+        reg = self._reg[g]
+        if reg is not None and tuple(self._ptrs[g]) != self._regptrs[g]:
+            reg = None                              # moved: pack (peers see the header mismatch)
         if L.fast is not None:
             status, _, ncalls = L.fast.fused(comm._hv, n, pa, ca, self._gdtype[g], out, L.ALGO[self.algo],
-                                             int(self.cfg.threshold_bytes), self.switch, 1, 0, 0, 0,
+                                             int(self.cfg.threshold_bytes), self.switch, 1, 0, 0,
+                                             C.addressof(reg) if reg is not None else 0,
                                              self.stream.cuda_stream, sa)
             if status:
                 L.check(status)
@@ -197,9 +211,23 @@ class OverlappedAggregator:
         nc, ag = C.c_int(), C.c_int(1)
         L.check(L.lib.cm_fused_allreduce_agreed(
             comm._h, n, self._ptrs[g], self._counts[g], self._gdtype[g], out, L.ALGO[self.algo],
-            int(self.cfg.threshold_bytes), self.switch, 1, None, 0, C.byref(ag), None,
+            int(self.cfg.threshold_bytes), self.switch, 1, None, 0, C.byref(ag), reg,
             self.stream.cuda_stream, self.stats[g], C.byref(nc)))
         return nc.value
+
+    def _register_step_tensors(self):
+        """Collective (every rank, end of its first step): register this
+        step's gradient tensors in schema order; an allocation that cannot be
+        shared on any rank leaves every rank packing."""
+        ts = [self._tensors[s.name] for s in self.specs]
+        ids = self.comm.register_buffers(ts, tolerant=True)
+        if ids is None:
+            return
+        by_name = {s.name: i for s, i in zip(self.specs, ids)}
+        for g, members in enumerate(self.groups):
+            names = [self.specs[i].name for i in members]
+            self._reg[g] = L.i64_array([by_name[nm] for nm in names])
+            self._regptrs[g] = tuple(self._tensors[nm].data_ptr() for nm in names)
 
     def finish(self) -> GradientSet:
         """Join the communication stream into the caller's stream and return
@@ -217,6 +245,8 @@ class OverlappedAggregator:
             L.check(st)
         stats = [CollectiveStats(int(self.stats[g][0].rounds), int(self.stats[g][0].messages_per_rank),
                                  int(self.stats[g][0].bytes_sent_per_rank)) for g in self.order]
+        if self.register_members and self.iteration == 0 and self.comm.size > 1:
+            self._register_step_tensors()
         gs = GradientSet.__new__(GradientSet)
         object.__setattr__(gs, "tensors", self._views)
         object.__setattr__(gs, "iteration", self.iteration)

@@ -319,6 +319,30 @@ def main():
                    f"overlapped aggregate {algo} step {step}")
             expect(len(ov.step_stats) == len(groups), "overlap stats")
 
+    # 4m. overlapped aggregation with registered members: persistent gradient
+    # buffers handed over every step, registered collectively at the end of
+    # step 0 and read in place by peers afterwards (no member pack); the
+    # buffers are overwritten by the next step's "backward" right after
+    # finish(), so peers must be done reading them by then. Bit-exact.
+    want, groups, _ = OA.aggregate(per_rank, "float32", "auto", 8 << 20)
+    want2, _, _ = OA.aggregate([[(nm, a * 2) for nm, a in pr] for pr in per_rank], "float32", "auto", 8 << 20)
+    bufs = {nm: torch.empty(a.size, device="cuda") for nm, a in per_rank[rank]}
+    ov = P.OverlappedAggregator([(nm, a.size, "float32") for nm, a in per_rank[rank]], comm,
+                                cfg=P.FusionConfig(8 << 20), register_members=True)
+    rng = np.random.default_rng([78, rank])
+    for step in range(4):
+        scale = 1 + (step % 2)
+        for i in rng.permutation(len(per_rank[rank])):
+            nm, a = per_rank[rank][i]
+            bufs[nm].copy_(torch.from_numpy(a * scale))
+            ov.ready(nm, bufs[nm])
+        res = ov.finish()
+        w = want if scale == 1 else want2
+        expect(all(t.to_bytes() == w[t.name].tobytes() for t in res.tensors),
+               f"overlapped aggregate, registered members, step {step}")
+        if step == 0:
+            expect(all(r is not None for r in ov._reg), "members registered after the first step")
+
     # 4j. launch knobs: plain launches (pdl off) and 2-CTA-cluster capped grids
     # give the same bits; grid sizes change from call to call (epoch slots)
     for knobs in ({"pdl": 1}, {"cluster_pairs": 2, "max_ctas": 16}, {"pdl": 2, "max_ctas": 148}):
