@@ -948,7 +948,7 @@ def main():
     ap.add_argument("--mode", choices=("headline", "sweep", "tune", "refsweep", "overlap"), default="headline")
     ap.add_argument("--gemm", type=int, default=2048, help="overlap: per-layer bf16 GEMM size")
     ap.add_argument("--ov-ctas", type=int, default=64, help="overlap: CTA cap of overlapped collectives (0: none)")
-    ap.add_argument("--ov-priority", type=int, default=-1, help="overlap: communication stream priority")
+    ap.add_argument("--ov-priority", type=int, default=0, help="overlap: communication stream priority (-1: high)")
     ap.add_argument("--ov-pairs", type=int, default=0, help="overlap: capped grids in 2-CTA clusters (1: on)")
     ap.add_argument("--ov-pack-ctas", type=int, default=0, help="overlap: CTA cap of the member pack (0: none)")
     ap.add_argument("--ov-register", type=int, default=0,

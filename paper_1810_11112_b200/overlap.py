@@ -49,7 +49,8 @@ class OverlappedAggregator:
     ``cluster_pairs``: capped grids launch in 2-CTA clusters so they occupy
     whole TPCs (cuBLAS's 2-SM-cluster GEMMs keep their pairs); ``pack_ctas``
     caps the member pack that precedes each overlapped collective;
-    ``priority`` is the communication stream's priority (-1: high);
+    ``priority`` is the communication stream's priority (0: normal, measured
+    faster than -1 = high at N = 4, `profiles/r02_overlap_priority_n4.txt`);
     ``register_members``: at the end of the first step every rank registers
     the gradient tensors it handed to ``ready()`` (collective, the pointer
     cache's IPC side, as ``register_gradients``), and from then on peers read
@@ -67,7 +68,7 @@ class OverlappedAggregator:
 
     def __init__(self, schema, comm: Communicator, algo: str = "auto", cfg: FusionConfig | None = None,
                  switch_bytes: int | None = DEFAULT_SWITCH_BYTES, launch_order: str = "reverse",
-                 max_ctas: int | None = 64, priority: int = -1, cluster_pairs: bool = False,
+                 max_ctas: int | None = 64, priority: int = 0, cluster_pairs: bool = False,
                  pack_ctas: int | None = None, register_members: bool = False):
         if isinstance(schema, GradientSet):
             specs = [(t.name, t.len, t.dtype) for t in schema.tensors]
@@ -97,9 +98,10 @@ class OverlappedAggregator:
         else:
             raise ConfigError(f"launch_order must be 'reverse' or 'forward', got {launch_order!r}")
         dev = comm.device
-        # high-priority communication stream: its CTAs are scheduled first as
-        # the producer's kernels drain, and a CTA cap leaves SMs to the
-        # backward pass (the collective is NVLink-bound well below 148 CTAs)
+        # communication stream (normal priority by default: a high-priority
+        # stream's CTAs jump ahead of the backward GEMMs' and measured slower);
+        # a CTA cap leaves SMs to the backward pass (the collective is
+        # NVLink-bound well below 148 CTAs)
         self.stream = torch.cuda.Stream(dev, priority=priority)
         self.max_ctas = max_ctas
         self.cluster_pairs = cluster_pairs
