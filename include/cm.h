@@ -191,8 +191,10 @@ int cm_comm_registry(cm_comm_t* comm, cm_registry_t** reg);
  *                         after a per-index barrier (default; measured equal)
  *   "host_chunk_kb"       KiB per H2D/D2H piece of the host-gradient pipeline
  *                         (default 8192; at p = 1 2048/4096/16384 measured slower)
- *   "host_split"          2 = with host gradients at p > 1, a two-shot fused group
- *                         moves H2D -> collective -> D2H in ~host_piece_kb pieces
+ *   "host_split"          2 = with host gradients at p > 1 (aggregate's fused groups
+ *                         and allreduce() of a host send buffer), a two-shot
+ *                         collective moves H2D -> collective -> D2H in
+ *                         ~host_piece_kb pieces
  *                         (the k-th 1/K of every rank's segment: same owners and
  *                         fold order as one launch, bit-identical); 1 = one
  *                         launch per group

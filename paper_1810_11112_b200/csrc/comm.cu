@@ -581,6 +581,7 @@ struct Placement {
   void* out = nullptr;
   int64_t zc = 0;
   bool recv_host = false;
+  bool send_host = false;   // send staged into `scratch` (H2D deferred when defer_host_copy)
 };
 
 // ---- automatic registration (the pointer cache's IPC side) ----------------
@@ -703,7 +704,7 @@ int64_t auto_slot(cm_comm* c, const void* ptr, int64_t bytes, bool may_publish) 
 }
 
 int place(cm_comm* c, const void* send, int64_t send_bytes, void* recv, int64_t recv_bytes,
-          cudaStream_t stream, Placement* pl, bool peers_read_send = false) {
+          cudaStream_t stream, Placement* pl, bool peers_read_send = false, bool defer_host_copy = false) {
   int ks = CM_KIND_DEVICE, kr = CM_KIND_DEVICE;
   int st;
   if (send_bytes > 0 && (st = classify(c, send, &ks))) return st;
@@ -714,8 +715,9 @@ int place(cm_comm* c, const void* send, int64_t send_bytes, void* recv, int64_t 
   if ((ks == CM_KIND_HOST || kr == CM_KIND_HOST) && need > (int64_t)c->staging_bytes)
     return fail(CM_ERR_CONFIG, "host buffer larger than the device bounce buffer");
   if (ks == CM_KIND_HOST) {
-    CUDA_TRY(cudaMemcpyAsync(c->scratch, send, send_bytes, cudaMemcpyHostToDevice, stream));
+    if (!defer_host_copy) CUDA_TRY(cudaMemcpyAsync(c->scratch, send, send_bytes, cudaMemcpyHostToDevice, stream));
     pl->in = c->scratch;
+    pl->send_host = true;
   } else if (in_pool(c, send, send_bytes)) {
     pl->srcmode = SRC_ZEROCOPY;
     pl->zc = static_cast<const char*>(send) - c->local;
@@ -796,6 +798,9 @@ void plan_algo(cm_comm* c, int concrete, int64_t nbytes, Launch* L) {
   }
 }
 
+int host_allreduce_pieces(cm_comm* c, const Launch& L, const void* send, void* recv, bool recv_host, int K,
+                          cudaStream_t stream);
+
 int do_allreduce(cm_comm* c, const void* const* sends, void* const* recvs, int64_t count,
                  int dtype, int op, int algo, int64_t switch_bytes, int average, void* stream_,
                  cm_stats_t* stats) {
@@ -829,7 +834,19 @@ int do_allreduce(cm_comm* c, const void* const* sends, void* const* recvs, int64
   if (!c->virt) {
     if ((st = service_autoreg(c, stream))) return st;
     const bool peers_read = !L.ll && !L.oneshot;    // the two-shot pull reads inputs in place
-    if ((st = place(c, sends[0], nbytes, recvs[0], nbytes, stream, &pl, peers_read))) return st;
+    const bool pieceable = c->host_split && peers_read && L.phases == (PH_RS | PH_AG);
+    if ((st = place(c, sends[0], nbytes, recvs[0], nbytes, stream, &pl, peers_read, pieceable))) return st;
+    if (pl.send_host && pieceable) {
+      // host send buffer: H2D / collective / D2H in pieces (host_allreduce_pieces)
+      const int K = (int)std::max<int64_t>(1, std::min<int64_t>(128, (nbytes + c->host_piece / 2) / c->host_piece));
+      if (K > 1) {
+        L.srcmode = SRC_COPYIN;
+        L.in[0] = pl.in;
+        L.out[0] = pl.out;
+        return host_allreduce_pieces(c, L, sends[0], recvs[0], pl.recv_host, K, stream);
+      }
+      CUDA_TRY(cudaMemcpyAsync(c->scratch, sends[0], nbytes, cudaMemcpyHostToDevice, stream));
+    }
     L.srcmode = pl.srcmode;
     L.in[0] = pl.in;
     L.out[0] = pl.out;
@@ -1122,6 +1139,47 @@ struct HostPipe {
   }
   ~HostPipe() { join(); }
 };
+
+// allreduce() of a host send buffer at p > 1: the K pieces of segments_of move
+// H2D (h2d stream, queued up front) -> collective (caller's stream, after
+// the piece's event) -> D2H (d2h stream) so the two PCIe directions and the
+// collective overlap; every element keeps the owner and fold order of the
+// one-launch allreduce. L is the planned launch with `scratch` as in/out.
+int host_allreduce_pieces(cm_comm* c, const Launch& L, const void* send, void* recv, bool recv_host, int K,
+                          cudaStream_t stream) {
+  const int p = c->size;
+  const int64_t sz = (int64_t)dtype_size(L.dtype);
+  HostPipe hp(c, stream);
+  int st;
+  if ((st = hp.start(0, 0))) return st;
+  std::vector<cudaEvent_t> ready(K);
+  int64_t off[MAXP], len[MAXP];
+  for (int k = 0; k < K; ++k) {
+    segments_of(L.n, p, L.layout, k, K, off, len);
+    for (int q = 0; q < p; ++q)
+      if (len[q] > 0)
+        CUDA_TRY(cudaMemcpyAsync(c->scratch + off[q] * sz, static_cast<const char*>(send) + off[q] * sz,
+                                 len[q] * sz, cudaMemcpyHostToDevice, c->h2d));
+    if ((st = hp.ev(&ready[k]))) return st;
+    CUDA_TRY(cudaEventRecord(ready[k], c->h2d));
+  }
+  for (int k = 0; k < K; ++k) {
+    CUDA_TRY(cudaStreamWaitEvent(stream, ready[k], 0));
+    Launch Lk = L;
+    Lk.piece = k;
+    Lk.npieces = K;
+    if ((st = launch_collective(c, Lk, stream))) return st;
+    if (recv_host) {
+      if ((st = hp.link(stream, c->d2h))) return st;
+      segments_of(L.n, p, L.layout, k, K, off, len);
+      for (int q = 0; q < p; ++q)
+        if (len[q] > 0)
+          CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(recv) + off[q] * sz, static_cast<char*>(L.out[0]) + off[q] * sz,
+                                   len[q] * sz, cudaMemcpyDeviceToHost, c->d2h));
+    }
+  }
+  return hp.join();
+}
 
 }  // namespace
 

@@ -537,6 +537,25 @@ def main():
                    f"after differing plans, host pieces {piece_kb}: allreduce {k}")
     comm.set_param("host_piece_kb", 4096)
 
+    # 4n. allreduce() of host buffers: a pinned (or pageable) send moves H2D /
+    # collective / D2H in pieces (host_split), bit-exact vs the oracle for
+    # both layouts; host_split=1 is the one-launch path
+    n = 3_000_017
+    xs = [np.random.default_rng([47, r]).standard_normal(n).astype(np.float32) for r in range(world)]
+    for split, piece_kb in ((2, 4096), (2, 300), (1, 4096)):
+        comm.set_param("host_split", split)
+        comm.set_param("host_piece_kb", piece_kb)
+        for where in ("pinned", "pageable"):
+            x = torch.from_numpy(xs[rank].copy())
+            if where == "pinned":
+                x = x.pin_memory()
+            for algo in ("ring_rsa", "rhd_rsa"):
+                out, _ = P.allreduce(P.Tensor("x", "float32", x), P.ReduceOp.SUM, group, comm, algo=algo)
+                expect(not out.is_cuda and out.to_bytes() == OC.allreduce(xs, "sum", algo, "float32").tobytes(),
+                       f"host allreduce {where} {algo} split={split} piece={piece_kb}")
+    comm.set_param("host_split", 2)
+    comm.set_param("host_piece_kb", 4096)
+
     # 4i. the communicator's pointer cache (registry.py:104-131): every call
     # classifies send and recv; no_cache queries the driver each time,
     # lazy_cache once per address, intercept_cache never (unregistered
